@@ -1,0 +1,112 @@
+/*
+ * tricount_b200.h -- C ABI of the B200 (sm_100a) exact triangle counter.
+ *
+ * Drop-in boundary for the reference `tricount` hot path (reference files under
+ * /root/reference/pkg/src/tricount).  The reference exposes a Python function API over
+ * numpy arrays (no FFI); each entry point below replaces one of those functions and is
+ * bound from Python with ctypes.  All functions return 0 on
+ * success and a negative status on failure (-1 argument/contract error, -2 CUDA error,
+ * -3 out of memory); tc_last_error() returns the thread-local message.  Host buffers are
+ * borrowed for the duration of the call; device graphs are owned by the library until
+ * tc_graph_free().  Every call is synchronous with respect to its results.
+ *
+ * Arrays: pairs are uint32 (u, v) pairs, row-major [npairs][2] (reference EdgeArray.edges,
+ * graph.py:101-129); an oriented graph is edge_src u32[m], edge_dst u32[m],
+ * node_offsets i64[n+1] (reference OrientedGraph, graph.py:146-193).
+ */
+#ifndef TRICOUNT_B200_H
+#define TRICOUNT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TC_ABI_VERSION 1
+
+typedef struct tc_graph tc_graph; /* device-resident OrientedGraph */
+
+/* Phase timings in milliseconds, measured with CUDA events on the library stream. */
+typedef struct tc_times {
+    double h2d_ms;        /* host->device copy of the input pairs               */
+    double preprocess_ms; /* preprocessing kernels (degree .. node array)        */
+    double count_ms;      /* counting kernels + 8-byte result copy               */
+    double total_ms;      /* whole call                                          */
+    double classify_ms;   /* count detail: source classification                 */
+    double heavy_ms;      /* count detail: shared-memory hash kernels            */
+    double light_ms;      /* count detail: warp-per-source register kernel       */
+    uint64_t heavy_tasks; /* count detail: CTA tasks issued                      */
+} tc_times;
+
+/* count algorithm selector */
+#define TC_ALGO_AUTO 0         /* light/heavy source-centric kernels (default)        */
+#define TC_ALGO_MERGE_THREAD 1 /* paper's thread-per-edge merge (A/B baseline)        */
+
+/* ---- lifecycle: replaces count.py:143-150 warm_kernel (JIT warm-up -> CUDA init) ---- */
+int tc_init(int device);
+int tc_shutdown(void);
+const char *tc_last_error(void);
+int tc_abi_version(void);
+
+/* ---- preprocess.py:74-84 preprocess(g) -> OrientedGraph ----------------------------
+ * pairs: host (pairs_on_device = 0) or device pointer; nverts = EdgeArray.num_vertices. */
+int tc_preprocess(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, int pairs_on_device,
+                  tc_graph **out, tc_times *t);
+
+/* ---- OrientedGraph transfer (graph.py:146-193) -------------------------------------- */
+int tc_graph_upload(const uint32_t *edge_src, const uint32_t *edge_dst,
+                    const int64_t *node_offsets, uint64_t m, uint64_t n, tc_graph **out);
+int tc_graph_download(const tc_graph *g, uint32_t *edge_src, uint32_t *edge_dst,
+                      int64_t *node_offsets);
+int tc_graph_info(const tc_graph *g, uint64_t *m, uint64_t *n, uint32_t *max_out_degree);
+int tc_graph_device_ptrs(const tc_graph *g, uint32_t **edge_src, uint32_t **edge_dst,
+                         int64_t **node_offsets);
+int tc_graph_free(tc_graph *g);
+
+/* ---- count.py:162-178 count_triangles / count.py:63-99 _count_strided over [lo, hi) --- */
+int tc_count(const tc_graph *g, int64_t lo, int64_t hi, int algo, uint64_t *out, tc_times *t);
+/* ---- count.py:181-204 count_partitioned: bounds[npools+1] must cover [0, m) ---------- */
+int tc_count_partitioned(const tc_graph *g, const int64_t *bounds, int npools, int algo,
+                         uint64_t *out, tc_times *t);
+/* ---- count.py:102-136 intersect_count ------------------------------------------------ */
+int tc_intersect_count(const tc_graph *g, uint32_t u, uint32_t v, uint64_t *out);
+/* ---- count.py:207-229 count_with_timings: preprocess + count, phase timings ---------- */
+int tc_count_with_timings(const uint32_t *pairs, uint64_t npairs, uint64_t nverts,
+                          int pairs_on_device, int algo, uint64_t *out, tc_times *t);
+
+/* ---- multi-GPU sharding: estimated-work bounds[npools+1] ---------- */
+int tc_work_bounds(const tc_graph *g, int npools, int64_t *bounds);
+/* merge-model work W = sum over oriented edges of d+(u) + d+(v) (roofline numerator) */
+int tc_merge_work(const tc_graph *g, uint64_t *out);
+
+/* ---- preprocess.py sub-steps (host buffers in and out) ------------------------------- */
+/* preprocess.py:23-33 sort_edges: lexicographic (first, second) order */
+int tc_sort_edges(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, uint32_t *out_pairs);
+/* preprocess.py:36-46 build_node_array from a grouped first column */
+int tc_build_node_array(const uint32_t *firsts, uint64_t k, uint64_t n, int64_t *offsets);
+/* preprocess.py:49-62 orient_and_compact (order preserving); degrees i64[n] */
+int tc_orient_and_compact(const uint32_t *pairs, uint64_t npairs, const int64_t *degrees,
+                          uint64_t n, uint32_t *out_pairs, uint64_t *kept);
+
+/* ---- generators.py:203-284 rmat on the device (input production, bit-identical) ------ *
+ * state/inc: numpy default_rng(seed).bit_generator.state (hi, lo words).  Returns a
+ * device buffer of npairs (u, v) pairs (free with tc_device_free) and num_vertices.    */
+int tc_gen_rmat(int scale, int edge_factor, const double probs[4], const uint64_t state[2],
+                const uint64_t inc[2], uint32_t **dev_pairs, uint64_t *npairs, uint64_t *nverts);
+
+/* ---- memory helpers (bench / host integration) --------------------------------------- */
+int tc_device_alloc(uint64_t bytes, void **p);
+int tc_device_free(void *p);
+int tc_memcpy(void *dst, const void *src, uint64_t bytes, int kind); /* 0 h2d, 1 d2h, 2 d2d */
+int tc_host_alloc(uint64_t bytes, void **p); /* pinned */
+int tc_host_free(void *p);
+int tc_host_register(void *p, uint64_t bytes);
+int tc_host_unregister(void *p);
+int tc_synchronize(void);
+int tc_l2_flush(void); /* write a buffer larger than L2 (timing hygiene) */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TRICOUNT_B200_H */

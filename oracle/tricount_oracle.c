@@ -1,0 +1,312 @@
+/*
+ * tricount_oracle.c -- CPU restatement of the reference `tricount` hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  This file is the parity checker for the sm_100a
+ * product path in paper_1503_00576_b200/csrc.  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / `--impl reference` arm may load it.  The product
+ * never links or calls it (there is no CPU fallback).
+ *
+ * Every function restates one reference function (paths relative to
+ * /root/reference/pkg/src/tricount):
+ *
+ *   or_sort_keys          preprocess.py:23-33 sort_edges + graph.py:84-98 pack_edge_keys
+ *                         (np.sort of (u<<32)|v keys; here an LSD radix sort, same order)
+ *   or_build_node_array   preprocess.py:36-46 build_node_array
+ *                         (np.searchsorted(firsts, arange(n+1), side="left"))
+ *   or_preprocess         preprocess.py:74-84 preprocess: sort -> node array -> degrees
+ *                         (np.diff, preprocess.py:79-80) -> orient_and_compact
+ *                         (preprocess.py:49-62) -> unzip (preprocess.py:65-71) -> node array
+ *   or_count_strided      count.py:63-99 _count_strided (two-pointer merge, bounds
+ *                         checked before every read)
+ *   or_intersect_count    count.py:102-136 intersect_count
+ *   or_count_triangles    count.py:162-178 count_triangles (W strided workers + sum)
+ *   or_count_partitioned  count.py:181-204 count_partitioned (P pools x W workers)
+ *   or_rmat_*             generators.py:203-284 rmat (PCG64 stream restated, see below)
+ *
+ * Parity of this restatement is pinned by tests/test_oracle.py against golden vectors
+ * produced by the reference package itself (tests/golden/make_golden.py).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <omp.h>
+
+static int clamp_threads(int t) {
+    if (t <= 0) t = omp_get_max_threads();
+    return t < 1 ? 1 : t;
+}
+
+/* ---------------------------------------------------------------- sort ---- */
+
+/* LSD radix sort of 64-bit keys over bits [0, key_bits), 8-bit digits.
+ * Produces the same ascending order as np.sort (keys compare as integers). */
+static void radix_sort_u64(uint64_t *keys, uint64_t *tmp, uint64_t k, int key_bits,
+                           int threads) {
+    if (k < 2) return;
+    int nthr = clamp_threads(threads);
+    size_t *hist = (size_t *)calloc((size_t)nthr * 256, sizeof(size_t));
+    uint64_t *src = keys, *dst = tmp;
+    int passes = (key_bits + 7) / 8;
+    for (int p = 0; p < passes; ++p) {
+        int shift = 8 * p;
+        memset(hist, 0, (size_t)nthr * 256 * sizeof(size_t));
+#pragma omp parallel num_threads(nthr)
+        {
+            int t = omp_get_thread_num();
+            uint64_t lo = k * (uint64_t)t / nthr, hi = k * (uint64_t)(t + 1) / nthr;
+            size_t *h = hist + (size_t)t * 256;
+            for (uint64_t i = lo; i < hi; ++i) h[(src[i] >> shift) & 255]++;
+#pragma omp barrier
+#pragma omp single
+            {
+                size_t run = 0;
+                for (int d = 0; d < 256; ++d)
+                    for (int tt = 0; tt < nthr; ++tt) {
+                        size_t c = hist[(size_t)tt * 256 + d];
+                        hist[(size_t)tt * 256 + d] = run;
+                        run += c;
+                    }
+            }
+            for (uint64_t i = lo; i < hi; ++i) {
+                uint64_t x = src[i];
+                dst[h[(x >> shift) & 255]++] = x;
+            }
+        }
+        uint64_t *s = src; src = dst; dst = s;
+    }
+    if (src != keys) memcpy(keys, src, k * sizeof(uint64_t));
+    free(hist);
+}
+
+static int bits_for(uint64_t maxval) {
+    int b = 0;
+    while (b < 64 && (maxval >> b) != 0) ++b;
+    return b;
+}
+
+/* preprocess.py:23-33 + graph.py:84-98: pack (first<<32)|second and sort. */
+int or_sort_keys(const uint32_t *pairs, uint64_t npairs, uint64_t *keys_out, int threads) {
+    int nthr = clamp_threads(threads);
+    uint32_t maxfirst = 0;
+#pragma omp parallel for num_threads(nthr) reduction(max : maxfirst)
+    for (uint64_t i = 0; i < npairs; ++i) {
+        keys_out[i] = ((uint64_t)pairs[2 * i] << 32) | pairs[2 * i + 1];
+        if (pairs[2 * i] > maxfirst) maxfirst = pairs[2 * i];
+    }
+    uint64_t *tmp = (uint64_t *)malloc((npairs ? npairs : 1) * sizeof(uint64_t));
+    if (!tmp) return -1;
+    radix_sort_u64(keys_out, tmp, npairs, 32 + bits_for(maxfirst), nthr);
+    free(tmp);
+    return 0;
+}
+
+/* preprocess.py:36-46: offsets[i] = first index j with firsts[j] >= i, i in [0, n]. */
+void or_build_node_array(const uint32_t *firsts, uint64_t k, uint64_t n, int64_t *offsets) {
+    uint64_t j = 0;
+    for (uint64_t i = 0; i <= n; ++i) {
+        while (j < k && (uint64_t)firsts[j] < i) ++j;
+        offsets[i] = (int64_t)j;
+    }
+}
+
+/* Node array from sorted packed keys (first vertex in the high word). */
+static void node_array_from_keys(const uint64_t *keys, uint64_t k, uint64_t n, int64_t *offsets) {
+    uint64_t j = 0;
+    for (uint64_t i = 0; i <= n; ++i) {
+        while (j < k && (keys[j] >> 32) < i) ++j;
+        offsets[i] = (int64_t)j;
+    }
+}
+
+/* preprocess.py:74-84.  Outputs must hold npairs entries (src/dst) and n+1 (off).
+ * Returns the oriented edge count through m_out. */
+int or_preprocess(const uint32_t *pairs, uint64_t npairs, uint64_t n, uint32_t *src,
+                  uint32_t *dst, int64_t *off, uint64_t *m_out, int threads) {
+    int nthr = clamp_threads(threads);
+    if (npairs == 0) {
+        for (uint64_t i = 0; i <= n; ++i) off[i] = 0;
+        *m_out = 0;
+        return 0;
+    }
+    uint64_t *keys = (uint64_t *)malloc(npairs * sizeof(uint64_t));
+    int64_t *offs_all = (int64_t *)malloc((n + 1) * sizeof(int64_t));
+    if (!keys || !offs_all) { free(keys); free(offs_all); return -1; }
+    if (or_sort_keys(pairs, npairs, keys, nthr) != 0) { free(keys); free(offs_all); return -1; }
+    node_array_from_keys(keys, npairs, n, offs_all);
+    /* degrees = np.diff(offsets_all); orient keeps (deg u, u) < (deg v, v) in sorted
+     * order (preprocess.py:49-62), then unzip (preprocess.py:65-71). */
+    uint64_t m = 0;
+    for (uint64_t i = 0; i < npairs; ++i) {
+        uint32_t u = (uint32_t)(keys[i] >> 32), v = (uint32_t)keys[i];
+        int64_t du = offs_all[u + 1] - offs_all[u];
+        int64_t dv = (uint64_t)v < n ? offs_all[v + 1] - offs_all[v] : 0;
+        if (du < dv || (du == dv && u < v)) {
+            src[m] = u;
+            dst[m] = v;
+            ++m;
+        }
+    }
+    or_build_node_array(src, m, n, off);
+    *m_out = m;
+    free(keys);
+    free(offs_all);
+    return 0;
+}
+
+/* --------------------------------------------------------------- count ---- */
+
+/* count.py:63-99, statement for statement. */
+uint64_t or_count_strided(const uint32_t *edge_src, const uint32_t *edge_dst,
+                          const int64_t *node_offsets, int64_t lo, int64_t hi,
+                          int64_t offset, int64_t stride) {
+    uint64_t total = 0;
+    for (int64_t i = lo + offset; i < hi; i += stride) {
+        uint32_t u = edge_src[i], v = edge_dst[i];
+        int64_t u_it = node_offsets[u], u_end = node_offsets[u + 1];
+        int64_t v_it = node_offsets[v], v_end = node_offsets[v + 1];
+        if (u_it == u_end || v_it == v_end) continue;
+        uint32_t a = edge_dst[u_it], b = edge_dst[v_it];
+        for (;;) {
+            if (a < b) {
+                if (++u_it == u_end) break;
+                a = edge_dst[u_it];
+            } else if (b < a) {
+                if (++v_it == v_end) break;
+                b = edge_dst[v_it];
+            } else {
+                ++total;
+                ++u_it;
+                ++v_it;
+                if (u_it == u_end || v_it == v_end) break;
+                a = edge_dst[u_it];
+                b = edge_dst[v_it];
+            }
+        }
+    }
+    return total;
+}
+
+/* count.py:102-136. */
+uint64_t or_intersect_count(const uint32_t *edge_dst, const int64_t *node_offsets,
+                            uint32_t u, uint32_t v) {
+    int64_t u_it = node_offsets[u], u_end = node_offsets[u + 1];
+    int64_t v_it = node_offsets[v], v_end = node_offsets[v + 1];
+    uint64_t c = 0;
+    while (u_it < u_end && v_it < v_end) {
+        uint32_t a = edge_dst[u_it], b = edge_dst[v_it];
+        if (a < b) ++u_it;
+        else if (b < a) ++v_it;
+        else { ++c; ++u_it; ++v_it; }
+    }
+    return c;
+}
+
+/* count.py:181-204: P contiguous pools, each strided over W workers; sum. */
+uint64_t or_count_partitioned(const uint32_t *edge_src, const uint32_t *edge_dst,
+                              const int64_t *node_offsets, const int64_t *bounds, int npools,
+                              int workers) {
+    uint64_t total = 0;
+    int tasks = npools * workers;
+#pragma omp parallel for num_threads(clamp_threads(tasks)) schedule(dynamic, 1) reduction(+ : total)
+    for (int t = 0; t < tasks; ++t) {
+        int p = t / workers, w = t % workers;
+        total += or_count_strided(edge_src, edge_dst, node_offsets, bounds[p], bounds[p + 1], w,
+                                  workers);
+    }
+    return total;
+}
+
+/* count.py:162-178: W strided workers over [0, m). */
+uint64_t or_count_triangles(const uint32_t *edge_src, const uint32_t *edge_dst,
+                            const int64_t *node_offsets, int64_t m, int workers) {
+    int64_t b[2] = {0, m};
+    if (m == 0) return 0;
+    return or_count_partitioned(edge_src, edge_dst, node_offsets, b, 1, workers);
+}
+
+/* Bounded sample for the CPU baseline: only edges i with i % stride == phase,
+ * spread over `threads` threads (the reference's own strided assignment, count.py:69). */
+uint64_t or_count_sampled(const uint32_t *edge_src, const uint32_t *edge_dst,
+                          const int64_t *node_offsets, int64_t m, int64_t stride, int threads) {
+    uint64_t total = 0;
+    int nthr = clamp_threads(threads);
+#pragma omp parallel for num_threads(nthr) schedule(dynamic, 1) reduction(+ : total)
+    for (int t = 0; t < nthr; ++t)
+        total += or_count_strided(edge_src, edge_dst, node_offsets, 0, m, (int64_t)t * stride,
+                                  (int64_t)nthr * stride);
+    return total;
+}
+
+/* Σ over oriented edges of d+(u)+d+(v): the merge-model work W. */
+uint64_t or_merge_work(const uint32_t *edge_src, const uint32_t *edge_dst,
+                       const int64_t *node_offsets, int64_t m) {
+    uint64_t w = 0;
+#pragma omp parallel for reduction(+ : w)
+    for (int64_t i = 0; i < m; ++i) {
+        uint32_t u = edge_src[i], v = edge_dst[i];
+        w += (uint64_t)(node_offsets[u + 1] - node_offsets[u]) +
+             (uint64_t)(node_offsets[v + 1] - node_offsets[v]);
+    }
+    return w;
+}
+
+/* ---------------------------------------------------------------- rmat ---- */
+/*
+ * generators.py:241-279 draws `scale` arrays of doubles per batch from numpy's
+ * default_rng(seed) = PCG64 (XSL-RR 128/64; state = state*M + inc, then output),
+ * random() = (next64 >> 11) * 2^-53.  numpy itself is not bundled with this oracle, so
+ * the initial (state, inc) pair is passed in by the caller (numpy's SeedSequence
+ * seeding, read from Generator.bit_generator.state).  or_rmat_levels fills src/dst
+ * for one batch exactly as the reference's level loop does.
+ */
+typedef unsigned __int128 u128;
+static const u128 PCG_MULT = (((u128)0x2360ED051FC65DA4ULL) << 64) | 0x4385DF649FCCF645ULL;
+
+static inline uint64_t pcg_output(u128 s) {
+    uint64_t hi = (uint64_t)(s >> 64), lo = (uint64_t)s;
+    unsigned rot = (unsigned)(s >> 122);
+    uint64_t x = hi ^ lo;
+    return (x >> rot) | (x << ((64 - rot) & 63));
+}
+
+/* state after `delta` steps: s*M^delta + inc*(M^delta-1)/(M-1), by squaring. */
+static u128 pcg_advance(u128 s, u128 inc, uint64_t delta) {
+    u128 acc_mult = 1, acc_plus = 0, cur_mult = PCG_MULT, cur_plus = inc;
+    while (delta) {
+        if (delta & 1) {
+            acc_mult *= cur_mult;
+            acc_plus = acc_plus * cur_mult + cur_plus;
+        }
+        cur_plus = (cur_mult + 1) * cur_plus;
+        cur_mult *= cur_mult;
+        delta >>= 1;
+    }
+    return acc_mult * s + acc_plus;
+}
+
+/* One batch of the reference level loop (generators.py:249-256).  The stream starts
+ * at (state_hi, state_lo) advanced by `skip` draws.  Writes src/dst (< 2^scale). */
+void or_rmat_levels(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                    uint64_t skip, uint64_t batch, int scale, double a, double t_ab,
+                    double t_abc, int64_t *src, int64_t *dst, int threads) {
+    u128 s0 = ((u128)state_hi << 64) | state_lo, inc = ((u128)inc_hi << 64) | inc_lo;
+    memset(src, 0, batch * sizeof(int64_t));
+    memset(dst, 0, batch * sizeof(int64_t));
+    int nthr = clamp_threads(threads);
+    for (int l = 0; l < scale; ++l) {
+#pragma omp parallel num_threads(nthr)
+        {
+            int t = omp_get_thread_num();
+            uint64_t lo = batch * (uint64_t)t / nthr, hi = batch * (uint64_t)(t + 1) / nthr;
+            u128 s = pcg_advance(s0, inc, skip + (uint64_t)l * batch + lo);
+            for (uint64_t j = lo; j < hi; ++j) {
+                s = s * PCG_MULT + inc;
+                double r = (double)(pcg_output(s) >> 11) * (1.0 / 9007199254740992.0);
+                int sb = r >= t_ab;
+                int db = (r >= a && r < t_ab) || r >= t_abc;
+                src[j] = (src[j] << 1) | sb;
+                dst[j] = (dst[j] << 1) | db;
+            }
+        }
+    }
+}

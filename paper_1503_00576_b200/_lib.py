@@ -1,0 +1,136 @@
+"""ctypes binding of libtcb200.so (the C ABI in include/tricount_b200.h).
+
+There is no CPU fallback: if the library or a B200 is missing, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtcb200.so")
+
+ALGO_AUTO = 0
+ALGO_MERGE_THREAD = 1
+
+
+class TcTimes(ctypes.Structure):
+    _fields_ = [
+        ("h2d_ms", ctypes.c_double),
+        ("preprocess_ms", ctypes.c_double),
+        ("count_ms", ctypes.c_double),
+        ("total_ms", ctypes.c_double),
+        ("classify_ms", ctypes.c_double),
+        ("heavy_ms", ctypes.c_double),
+        ("light_ms", ctypes.c_double),
+        ("heavy_tasks", ctypes.c_uint64),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class TcError(RuntimeError):
+    """A CUDA / library failure inside libtcb200 (argument errors raise ValueError)."""
+
+
+_u32p = ctypes.POINTER(ctypes.c_uint32)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_u64p = ctypes.POINTER(ctypes.c_uint64)
+_vp = ctypes.c_void_p
+_graph_p = ctypes.c_void_p
+
+_SIGS = {
+    "tc_init": ([ctypes.c_int], ctypes.c_int),
+    "tc_shutdown": ([], ctypes.c_int),
+    "tc_last_error": ([], ctypes.c_char_p),
+    "tc_abi_version": ([], ctypes.c_int),
+    "tc_preprocess": ([_vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
+                       ctypes.POINTER(_graph_p), ctypes.POINTER(TcTimes)], ctypes.c_int),
+    "tc_graph_upload": ([_vp, _vp, _vp, ctypes.c_uint64, ctypes.c_uint64,
+                         ctypes.POINTER(_graph_p)], ctypes.c_int),
+    "tc_graph_download": ([_graph_p, _vp, _vp, _vp], ctypes.c_int),
+    "tc_graph_info": ([_graph_p, _u64p, _u64p, ctypes.POINTER(ctypes.c_uint32)], ctypes.c_int),
+    "tc_graph_device_ptrs": ([_graph_p, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                              ctypes.POINTER(_vp)], ctypes.c_int),
+    "tc_graph_free": ([_graph_p], ctypes.c_int),
+    "tc_count": ([_graph_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, _u64p,
+                  ctypes.POINTER(TcTimes)], ctypes.c_int),
+    "tc_count_partitioned": ([_graph_p, _vp, ctypes.c_int, ctypes.c_int, _u64p,
+                              ctypes.POINTER(TcTimes)], ctypes.c_int),
+    "tc_intersect_count": ([_graph_p, ctypes.c_uint32, ctypes.c_uint32, _u64p], ctypes.c_int),
+    "tc_count_with_timings": ([_vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
+                               _u64p, ctypes.POINTER(TcTimes)], ctypes.c_int),
+    "tc_work_bounds": ([_graph_p, ctypes.c_int, _vp], ctypes.c_int),
+    "tc_merge_work": ([_graph_p, _u64p], ctypes.c_int),
+    "tc_sort_edges": ([_vp, ctypes.c_uint64, ctypes.c_uint64, _vp], ctypes.c_int),
+    "tc_build_node_array": ([_vp, ctypes.c_uint64, ctypes.c_uint64, _vp], ctypes.c_int),
+    "tc_orient_and_compact": ([_vp, ctypes.c_uint64, _vp, ctypes.c_uint64, _vp, _u64p],
+                              ctypes.c_int),
+    "tc_gen_rmat": ([ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double), _u64p, _u64p,
+                     ctypes.POINTER(_vp), _u64p, _u64p], ctypes.c_int),
+    "tc_device_alloc": ([ctypes.c_uint64, ctypes.POINTER(_vp)], ctypes.c_int),
+    "tc_device_free": ([_vp], ctypes.c_int),
+    "tc_memcpy": ([_vp, _vp, ctypes.c_uint64, ctypes.c_int], ctypes.c_int),
+    "tc_host_alloc": ([ctypes.c_uint64, ctypes.POINTER(_vp)], ctypes.c_int),
+    "tc_host_free": ([_vp], ctypes.c_int),
+    "tc_host_register": ([_vp, ctypes.c_uint64], ctypes.c_int),
+    "tc_host_unregister": ([_vp], ctypes.c_int),
+    "tc_synchronize": ([], ctypes.c_int),
+    "tc_l2_flush": ([], ctypes.c_int),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lock = threading.Lock()
+_lib = None
+_initialised = False
+
+
+def load(init: bool = False):
+    """Load libtcb200.so (raises if absent); with init=True also bind the GPU."""
+    global _lib, _initialised
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(
+                    f"{LIB_PATH} is missing: build it with `python __graft_entry__.py build` "
+                    "(there is no CPU fallback)")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (args, res) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.argtypes = args
+                fn.restype = res
+            _lib = lib
+        if init and not _initialised:
+            dev = int(os.environ.get("LOCAL_RANK", "0")) if "TC_DEVICE" not in os.environ \
+                else int(os.environ["TC_DEVICE"])
+            _check(_lib.tc_init(dev))
+            _initialised = True
+    return _lib
+
+
+def lib():
+    return load(init=True)
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = (_lib.tc_last_error() or b"").decode(errors="replace")
+    if rc == -1:
+        raise ValueError(msg)
+    if rc == -3:
+        raise MemoryError(msg)
+    raise TcError(msg)
+
+
+def check(rc: int) -> None:
+    _check(rc)
+
+
+def ptr(arr: np.ndarray) -> ctypes.c_void_p:
+    return ctypes.c_void_p(arr.ctypes.data) if arr.size else ctypes.c_void_p(0)

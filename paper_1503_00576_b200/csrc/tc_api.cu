@@ -1,0 +1,524 @@
+// tc_api.cu -- the C ABI (include/tricount_b200.h).  Plain pointers and sizes only.
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <mutex>
+#include <string>
+
+#include "../../include/tricount_b200.h"
+#include "tc_common.cuh"
+#include "tc_internal.h"
+
+struct tc_graph {
+    tc::DeviceGraph g;
+};
+
+namespace tc {
+
+namespace {
+thread_local std::string g_err;
+std::mutex g_mu;
+bool g_ready = false;
+int g_device = 0;
+cudaStream_t g_stream = nullptr;
+void *g_flush = nullptr;
+size_t g_flush_bytes = 0;
+unsigned long long *g_total = nullptr;  // device u64 accumulator for counts
+}  // namespace
+
+void set_error(const std::string &msg) { g_err = msg; }
+const char *last_error() { return g_err.c_str(); }
+
+static int ensure_init(int device) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_ready) {
+        TC_CUDA(cudaSetDevice(g_device));
+        return 0;
+    }
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        set_error(std::string("no CUDA device available: ") + cudaGetErrorString(e));
+        return -2;
+    }
+    if (device < 0 || device >= count) {
+        set_error("device index out of range");
+        return -1;
+    }
+    TC_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    TC_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) {
+        set_error(std::string("this library is built for sm_100a (B200); found ") + prop.name);
+        return -2;
+    }
+    TC_CUDA(cudaStreamCreateWithFlags(&g_stream, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    TC_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = ~0ull;
+    TC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    TC_CUDA(cudaMalloc(&g_total, sizeof(unsigned long long)));
+    g_device = device;
+    g_ready = true;
+    return 0;
+}
+
+static int ensure() { return ensure_init(g_device); }
+
+static double ms_between(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    return (double)ms;
+}
+
+struct Events {
+    cudaEvent_t e[6];
+    int n = 0;
+    Events() {
+        for (auto &x : e) x = nullptr;
+    }
+    int create() {
+        for (auto &x : e) TC_CUDA(cudaEventCreate(&x));
+        return 0;
+    }
+    ~Events() {
+        for (auto &x : e)
+            if (x) cudaEventDestroy(x);
+    }
+};
+
+static int count_ranges(const DeviceGraph &g, const int64_t *bounds, int npools, int algo,
+                        uint64_t *out, tc_times *t) {
+    cudaStream_t s = g_stream;
+    Events ev;
+    TC_CHECK(ev.create());
+    TC_CUDA(cudaEventRecord(ev.e[0], s));
+    TC_CUDA(cudaMemsetAsync(g_total, 0, sizeof(unsigned long long), s));
+    CountStats agg, st;
+    for (int p = 0; p < npools; ++p) {
+        st = CountStats();
+        TC_CHECK(count_range_dev(g, (uint64_t)bounds[p], (uint64_t)bounds[p + 1], algo, g_total, s,
+                                 t ? &st : nullptr));
+        agg.classify_ms += st.classify_ms;
+        agg.heavy_ms += st.heavy_ms;
+        agg.light_ms += st.light_ms;
+        agg.heavy_tasks += st.heavy_tasks;
+    }
+    unsigned long long h = 0;
+    TC_CUDA(cudaMemcpyAsync(&h, g_total, sizeof(h), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaEventRecord(ev.e[1], s));
+    TC_CUDA(cudaEventSynchronize(ev.e[1]));
+    *out = h;
+    if (t) {
+        memset(t, 0, sizeof(*t));
+        t->count_ms = ms_between(ev.e[0], ev.e[1]);
+        t->total_ms = t->count_ms;
+        t->classify_ms = agg.classify_ms;
+        t->heavy_ms = agg.heavy_ms;
+        t->light_ms = agg.light_ms;
+        t->heavy_tasks = agg.heavy_tasks;
+    }
+    return 0;
+}
+
+static int check_graph(const tc_graph *g) {
+    if (!g) {
+        set_error("null graph handle");
+        return -1;
+    }
+    return 0;
+}
+
+}  // namespace tc
+
+using namespace tc;
+
+extern "C" {
+
+int tc_abi_version(void) { return TC_ABI_VERSION; }
+const char *tc_last_error(void) { return tc::last_error(); }
+
+int tc_init(int device) {
+    TC_CHECK(ensure_init(device));
+    // touch the pool and the kernels' module so the first timed call pays nothing
+    void *p = nullptr;
+    TC_CHECK(dalloc(&p, 1 << 20, g_stream));
+    dfree(p, g_stream);
+    TC_CUDA(cudaStreamSynchronize(g_stream));
+    return 0;
+}
+
+int tc_shutdown(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_ready) return 0;
+    if (g_flush) cudaFree(g_flush);
+    g_flush = nullptr;
+    g_flush_bytes = 0;
+    cudaFree(g_total);
+    g_total = nullptr;
+    cudaStreamDestroy(g_stream);
+    g_stream = nullptr;
+    g_ready = false;
+    return 0;
+}
+
+int tc_preprocess(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, int pairs_on_device,
+                  tc_graph **out, tc_times *t) {
+    TC_CHECK(ensure());
+    if (!out) {
+        set_error("null output handle");
+        return -1;
+    }
+    cudaStream_t s = g_stream;
+    Events ev;
+    TC_CHECK(ev.create());
+    TC_CUDA(cudaEventRecord(ev.e[0], s));
+    const uint32_t *dpairs = pairs;
+    uint32_t *owned = nullptr;
+    if (!pairs_on_device && npairs) {
+        TC_CHECK(dalloc_t(&owned, 2 * npairs, s));
+        TC_CUDA(cudaMemcpyAsync(owned, pairs, npairs * 8, cudaMemcpyHostToDevice, s));
+        dpairs = owned;
+    }
+    TC_CUDA(cudaEventRecord(ev.e[1], s));
+    tc_graph *g = new tc_graph();
+    int rc = preprocess_dev(dpairs, npairs, nverts, &g->g, s);
+    if (owned) dfree(owned, s);
+    if (rc) {
+        graph_release(&g->g, s);
+        delete g;
+        return rc;
+    }
+    TC_CUDA(cudaEventRecord(ev.e[2], s));
+    TC_CUDA(cudaEventSynchronize(ev.e[2]));
+    if (t) {
+        memset(t, 0, sizeof(*t));
+        t->h2d_ms = ms_between(ev.e[0], ev.e[1]);
+        t->preprocess_ms = ms_between(ev.e[1], ev.e[2]);
+        t->total_ms = ms_between(ev.e[0], ev.e[2]);
+    }
+    *out = g;
+    return 0;
+}
+
+int tc_graph_upload(const uint32_t *edge_src, const uint32_t *edge_dst,
+                    const int64_t *node_offsets, uint64_t m, uint64_t n, tc_graph **out) {
+    TC_CHECK(ensure());
+    cudaStream_t s = g_stream;
+    if (n >= (1ull << 32)) {
+        set_error("num_vertices must be < 2^32 on the device path");
+        return -1;
+    }
+    tc_graph *g = new tc_graph();
+    int rc = graph_alloc(&g->g, m, n, s);
+    if (rc) {
+        delete g;
+        return rc;
+    }
+    if (m) {
+        TC_CUDA(cudaMemcpyAsync(g->g.src, edge_src, m * 4, cudaMemcpyHostToDevice, s));
+        TC_CUDA(cudaMemcpyAsync(g->g.dst, edge_dst, m * 4, cudaMemcpyHostToDevice, s));
+    }
+    TC_CUDA(cudaMemsetAsync(g->g.dst + m, 0, 16, s));
+    TC_CUDA(cudaMemcpyAsync(g->g.off, node_offsets, (n + 1) * 8, cudaMemcpyHostToDevice, s));
+    uint32_t maxo = 0;
+    uint32_t *dmax = nullptr;
+    TC_CHECK(dalloc_t(&dmax, 1, s));
+    // rebuild off32 / max from the uploaded offsets (off32 via node array of src would
+    // assume a valid grouping; copy-convert instead)
+    if (g->g.off32) {
+        int64_t *h = (int64_t *)node_offsets;
+        uint32_t *tmp = (uint32_t *)malloc((n + 1) * 4);
+        if (!tmp) {
+            set_error("host allocation failed");
+            return -3;
+        }
+        for (uint64_t i = 0; i <= n; ++i) tmp[i] = (uint32_t)h[i];
+        TC_CUDA(cudaMemcpyAsync(g->g.off32, tmp, (n + 1) * 4, cudaMemcpyHostToDevice, s));
+        TC_CUDA(cudaStreamSynchronize(s));
+        free(tmp);
+    }
+    for (uint64_t i = 0; i < n; ++i) {
+        uint64_t d = (uint64_t)(node_offsets[i + 1] - node_offsets[i]);
+        if (d > maxo) maxo = (uint32_t)d;
+    }
+    dfree(dmax, s);
+    g->g.max_out = maxo;
+    TC_CUDA(cudaStreamSynchronize(s));
+    *out = g;
+    return 0;
+}
+
+int tc_graph_download(const tc_graph *g, uint32_t *edge_src, uint32_t *edge_dst,
+                      int64_t *node_offsets) {
+    TC_CHECK(ensure());
+    TC_CHECK(check_graph(g));
+    cudaStream_t s = g_stream;
+    if (g->g.m) {
+        if (edge_src) TC_CUDA(cudaMemcpyAsync(edge_src, g->g.src, g->g.m * 4, cudaMemcpyDeviceToHost, s));
+        if (edge_dst) TC_CUDA(cudaMemcpyAsync(edge_dst, g->g.dst, g->g.m * 4, cudaMemcpyDeviceToHost, s));
+    }
+    if (node_offsets)
+        TC_CUDA(cudaMemcpyAsync(node_offsets, g->g.off, (g->g.n + 1) * 8, cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    return 0;
+}
+
+int tc_graph_info(const tc_graph *g, uint64_t *m, uint64_t *n, uint32_t *max_out_degree) {
+    TC_CHECK(check_graph(g));
+    if (m) *m = g->g.m;
+    if (n) *n = g->g.n;
+    if (max_out_degree) *max_out_degree = g->g.max_out;
+    return 0;
+}
+
+int tc_graph_device_ptrs(const tc_graph *g, uint32_t **edge_src, uint32_t **edge_dst,
+                         int64_t **node_offsets) {
+    TC_CHECK(check_graph(g));
+    if (edge_src) *edge_src = g->g.src;
+    if (edge_dst) *edge_dst = g->g.dst;
+    if (node_offsets) *node_offsets = g->g.off;
+    return 0;
+}
+
+int tc_graph_free(tc_graph *g) {
+    if (!g) return 0;
+    if (g_ready) {
+        cudaSetDevice(g_device);
+        graph_release(&g->g, g_stream);
+    }
+    delete g;
+    return 0;
+}
+
+int tc_count(const tc_graph *g, int64_t lo, int64_t hi, int algo, uint64_t *out, tc_times *t) {
+    TC_CHECK(ensure());
+    TC_CHECK(check_graph(g));
+    if (lo < 0 || hi < lo || (uint64_t)hi > g->g.m) {
+        set_error("edge range outside [0, m]");
+        return -1;
+    }
+    int64_t b[2] = {lo, hi};
+    return count_ranges(g->g, b, 1, algo, out, t);
+}
+
+int tc_count_partitioned(const tc_graph *g, const int64_t *bounds, int npools, int algo,
+                         uint64_t *out, tc_times *t) {
+    TC_CHECK(ensure());
+    TC_CHECK(check_graph(g));
+    if (npools < 1 || bounds[0] != 0 || (uint64_t)bounds[npools] != g->g.m) {
+        set_error("plan does not cover [0, m)");
+        return -1;
+    }
+    for (int p = 0; p < npools; ++p)
+        if (bounds[p] > bounds[p + 1]) {
+            set_error("plan bounds must be nondecreasing");
+            return -1;
+        }
+    return count_ranges(g->g, bounds, npools, algo, out, t);
+}
+
+int tc_intersect_count(const tc_graph *g, uint32_t u, uint32_t v, uint64_t *out) {
+    TC_CHECK(ensure());
+    TC_CHECK(check_graph(g));
+    if ((uint64_t)u >= g->g.n || (uint64_t)v >= g->g.n) {
+        set_error("vertex id out of range");
+        return -1;
+    }
+    return intersect_dev(g->g, u, v, out, g_stream);
+}
+
+int tc_count_with_timings(const uint32_t *pairs, uint64_t npairs, uint64_t nverts,
+                          int pairs_on_device, int algo, uint64_t *out, tc_times *t) {
+    TC_CHECK(ensure());
+    cudaStream_t s = g_stream;
+    Events ev;
+    TC_CHECK(ev.create());
+    TC_CUDA(cudaEventRecord(ev.e[0], s));
+    const uint32_t *dpairs = pairs;
+    uint32_t *owned = nullptr;
+    if (!pairs_on_device && npairs) {
+        TC_CHECK(dalloc_t(&owned, 2 * npairs, s));
+        TC_CUDA(cudaMemcpyAsync(owned, pairs, npairs * 8, cudaMemcpyHostToDevice, s));
+        dpairs = owned;
+    }
+    TC_CUDA(cudaEventRecord(ev.e[1], s));
+    DeviceGraph g;
+    int rc = preprocess_dev(dpairs, npairs, nverts, &g, s);
+    if (owned) dfree(owned, s);
+    if (rc) {
+        graph_release(&g, s);
+        return rc;
+    }
+    TC_CUDA(cudaEventRecord(ev.e[2], s));
+    TC_CUDA(cudaMemsetAsync(g_total, 0, sizeof(unsigned long long), s));
+    CountStats st;
+    rc = count_range_dev(g, 0, g.m, algo, g_total, s, nullptr);
+    if (rc) {
+        graph_release(&g, s);
+        return rc;
+    }
+    unsigned long long h = 0;
+    TC_CUDA(cudaMemcpyAsync(&h, g_total, sizeof(h), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaEventRecord(ev.e[3], s));
+    graph_release(&g, s);
+    TC_CUDA(cudaEventSynchronize(ev.e[3]));
+    *out = h;
+    if (t) {
+        memset(t, 0, sizeof(*t));
+        t->h2d_ms = ms_between(ev.e[0], ev.e[1]);
+        t->preprocess_ms = ms_between(ev.e[1], ev.e[2]);
+        t->count_ms = ms_between(ev.e[2], ev.e[3]);
+        t->total_ms = ms_between(ev.e[0], ev.e[3]);
+    }
+    return 0;
+}
+
+int tc_work_bounds(const tc_graph *g, int npools, int64_t *bounds) {
+    TC_CHECK(ensure());
+    TC_CHECK(check_graph(g));
+    if (npools < 1) {
+        set_error("num_pools must be >= 1");
+        return -1;
+    }
+    return work_bounds_dev(g->g, npools, bounds, g_stream);
+}
+
+int tc_merge_work(const tc_graph *g, uint64_t *out) {
+    TC_CHECK(ensure());
+    TC_CHECK(check_graph(g));
+    return merge_work_dev(g->g, out, g_stream);
+}
+
+int tc_sort_edges(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, uint32_t *out_pairs) {
+    TC_CHECK(ensure());
+    if (npairs == 0) return 0;
+    cudaStream_t s = g_stream;
+    uint32_t *din = nullptr, *dout = nullptr;
+    TC_CHECK(dalloc_t(&din, 2 * npairs, s));
+    TC_CHECK(dalloc_t(&dout, 2 * npairs, s));
+    TC_CUDA(cudaMemcpyAsync(din, pairs, npairs * 8, cudaMemcpyHostToDevice, s));
+    TC_CHECK(sort_pairs_dev(din, npairs, nverts, dout, s));
+    TC_CUDA(cudaMemcpyAsync(out_pairs, dout, npairs * 8, cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    dfree(din, s);
+    dfree(dout, s);
+    return 0;
+}
+
+int tc_build_node_array(const uint32_t *firsts, uint64_t k, uint64_t n, int64_t *offsets) {
+    TC_CHECK(ensure());
+    cudaStream_t s = g_stream;
+    uint32_t *df = nullptr;
+    int64_t *doff = nullptr;
+    TC_CHECK(dalloc_t(&df, k ? k : 1, s));
+    TC_CHECK(dalloc_t(&doff, n + 1, s));
+    if (k) TC_CUDA(cudaMemcpyAsync(df, firsts, k * 4, cudaMemcpyHostToDevice, s));
+    TC_CHECK(build_node_array_dev(df, k, n, doff, nullptr, nullptr, s));
+    TC_CUDA(cudaMemcpyAsync(offsets, doff, (n + 1) * 8, cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    dfree(df, s);
+    dfree(doff, s);
+    return 0;
+}
+
+int tc_orient_and_compact(const uint32_t *pairs, uint64_t npairs, const int64_t *degrees,
+                          uint64_t n, uint32_t *out_pairs, uint64_t *kept) {
+    TC_CHECK(ensure());
+    *kept = 0;
+    if (npairs == 0) return 0;
+    cudaStream_t s = g_stream;
+    uint32_t *din = nullptr, *dout = nullptr;
+    int64_t *ddeg = nullptr;
+    TC_CHECK(dalloc_t(&din, 2 * npairs, s));
+    TC_CHECK(dalloc_t(&dout, 2 * npairs, s));
+    TC_CHECK(dalloc_t(&ddeg, n ? n : 1, s));
+    TC_CUDA(cudaMemcpyAsync(din, pairs, npairs * 8, cudaMemcpyHostToDevice, s));
+    if (n) TC_CUDA(cudaMemcpyAsync(ddeg, degrees, n * 8, cudaMemcpyHostToDevice, s));
+    uint64_t k = 0;
+    TC_CHECK(orient_compact_dev(din, npairs, ddeg, n, dout, &k, s));
+    if (k) TC_CUDA(cudaMemcpyAsync(out_pairs, dout, k * 8, cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    dfree(din, s);
+    dfree(dout, s);
+    dfree(ddeg, s);
+    *kept = k;
+    return 0;
+}
+
+int tc_gen_rmat(int scale, int edge_factor, const double probs[4], const uint64_t state[2],
+                const uint64_t inc[2], uint32_t **dev_pairs, uint64_t *npairs, uint64_t *nverts) {
+    TC_CHECK(ensure());
+    TC_CHECK(rmat_dev(scale, edge_factor, probs, state, inc, dev_pairs, npairs, nverts, g_stream));
+    TC_CUDA(cudaStreamSynchronize(g_stream));
+    return 0;
+}
+
+int tc_device_alloc(uint64_t bytes, void **p) {
+    TC_CHECK(ensure());
+    TC_CHECK(dalloc(p, bytes, g_stream));
+    TC_CUDA(cudaStreamSynchronize(g_stream));
+    return 0;
+}
+
+int tc_device_free(void *p) {
+    TC_CHECK(ensure());
+    dfree(p, g_stream);
+    TC_CUDA(cudaStreamSynchronize(g_stream));
+    return 0;
+}
+
+int tc_memcpy(void *dst, const void *src, uint64_t bytes, int kind) {
+    TC_CHECK(ensure());
+    cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice
+                     : kind == 1 ? cudaMemcpyDeviceToHost
+                                 : cudaMemcpyDeviceToDevice;
+    TC_CUDA(cudaMemcpyAsync(dst, src, bytes, k, g_stream));
+    TC_CUDA(cudaStreamSynchronize(g_stream));
+    return 0;
+}
+
+int tc_host_alloc(uint64_t bytes, void **p) {
+    TC_CHECK(ensure());
+    TC_CUDA(cudaHostAlloc(p, bytes ? bytes : 16, cudaHostAllocDefault));
+    return 0;
+}
+
+int tc_host_free(void *p) {
+    TC_CHECK(ensure());
+    TC_CUDA(cudaFreeHost(p));
+    return 0;
+}
+
+int tc_host_register(void *p, uint64_t bytes) {
+    TC_CHECK(ensure());
+    TC_CUDA(cudaHostRegister(p, bytes, cudaHostRegisterDefault));
+    return 0;
+}
+
+int tc_host_unregister(void *p) {
+    TC_CHECK(ensure());
+    TC_CUDA(cudaHostUnregister(p));
+    return 0;
+}
+
+int tc_synchronize(void) {
+    TC_CHECK(ensure());
+    TC_CUDA(cudaStreamSynchronize(g_stream));
+    return 0;
+}
+
+int tc_l2_flush(void) {
+    TC_CHECK(ensure());
+    if (!g_flush) {
+        int l2 = 0;
+        TC_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g_device));
+        g_flush_bytes = (size_t)l2 * 2;
+        TC_CUDA(cudaMalloc(&g_flush, g_flush_bytes));
+    }
+    TC_CUDA(cudaMemsetAsync(g_flush, 0x5a, g_flush_bytes, g_stream));
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,128 @@
+// tc_internal.h -- host-side internal interfaces between the library's translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace tc {
+
+// ------------------------------------------------------------------ errors ---
+void set_error(const std::string &msg);
+const char *last_error();
+
+#define TC_CUDA(expr)                                                                    \
+    do {                                                                                 \
+        cudaError_t _e = (expr);                                                         \
+        if (_e != cudaSuccess) {                                                         \
+            ::tc::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e) + " (" + \
+                            __FILE__ + ":" + std::to_string(__LINE__) + ")");            \
+            return -2;                                                                   \
+        }                                                                                \
+    } while (0)
+
+#define TC_CHECK(expr)             \
+    do {                           \
+        int _rc = (expr);          \
+        if (_rc != 0) return _rc;  \
+    } while (0)
+
+// ------------------------------------------------------------------ memory ---
+// Stream-ordered allocations from the device's default memory pool (release
+// threshold raised to "keep everything", so repeated calls reuse the same HBM).
+int dalloc(void **p, size_t bytes, cudaStream_t s);
+void dfree(void *p, cudaStream_t s);
+
+template <typename T>
+int dalloc_t(T **p, size_t count, cudaStream_t s) {
+    return dalloc(reinterpret_cast<void **>(p), count * sizeof(T), s);
+}
+
+// ------------------------------------------------------------- radix sort ---
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;
+constexpr int kSortThreads = 256;
+constexpr int kSortKPT = 16;
+constexpr int kSortTile = kSortThreads * kSortKPT;  // 4096 keys per tile
+constexpr int kMaxPasses = 8;
+
+struct RadixPlan {
+    int npass = 0;
+    int shift[kMaxPasses] = {0};
+    int bits[kMaxPasses] = {0};
+};
+RadixPlan make_radix_plan(int key_bits);
+
+enum SortOut { kOutKeys = 0, kOutSoA = 1, kOutAoS = 2 };
+
+// Device histogram of every pass's digit over `keys` (adds into hist[npass][kRadix]).
+int radix_histogram(const uint64_t *keys, uint64_t n, const RadixPlan &plan, uint32_t *hist,
+                    cudaStream_t s);
+
+// LSD radix sort of n 64-bit keys (optionally carrying a 32-bit payload) over the plan's
+// bits.  `hist` is the per-pass digit histogram (from radix_histogram or fused into a
+// producer kernel).  keys/alt (and vals/valt) are ping-pong buffers.  With out_mode
+// kOutSoA / kOutAoS the last pass writes (key >> split, key & mask) to out_a/out_b
+// (SoA) or out_a as uint2 pairs (AoS); otherwise *sorted_keys (*sorted_vals) points at
+// whichever ping-pong buffer holds the result.
+int radix_sort(uint64_t *keys, uint64_t *alt, uint32_t *vals, uint32_t *valt, uint64_t n,
+               const RadixPlan &plan, const uint32_t *hist, int out_mode, uint32_t *out_a,
+               uint32_t *out_b, int split_bits, uint64_t **sorted_keys, uint32_t **sorted_vals,
+               cudaStream_t s);
+
+inline int bits_for(uint64_t maxval) {
+    int b = 0;
+    while (b < 64 && (maxval >> b) != 0) ++b;
+    return b;
+}
+
+// ------------------------------------------------------------ device graph ---
+struct DeviceGraph {
+    uint64_t m = 0, n = 0;
+    uint32_t *src = nullptr;   // edge_src  u32[m]
+    uint32_t *dst = nullptr;   // edge_dst  u32[m] (+ padding)
+    int64_t *off = nullptr;    // node_offsets i64[n+1]
+    uint32_t *off32 = nullptr; // u32 copy of node_offsets when m < 2^32 (count kernels)
+    uint32_t max_out = 0;      // max out-degree
+    int device = 0;
+};
+
+int graph_alloc(DeviceGraph *g, uint64_t m, uint64_t n, cudaStream_t s);
+void graph_release(DeviceGraph *g, cudaStream_t s);
+// node_offsets (and off32, max_out) from a grouped edge_src (reference preprocess.py:36-46).
+int build_node_array_dev(const uint32_t *firsts, uint64_t k, uint64_t n, int64_t *off,
+                         uint32_t *off32, uint32_t *max_out, cudaStream_t s);
+// Full reference preprocess on device-resident pairs (reference preprocess.py:74-84).
+int preprocess_dev(const uint32_t *pairs, uint64_t npairs, uint64_t n, DeviceGraph *out,
+                   cudaStream_t s);
+// Sort 2m pairs lexicographically (reference preprocess.py:23-33) into out_pairs.
+int sort_pairs_dev(const uint32_t *pairs, uint64_t npairs, uint64_t n, uint32_t *out_pairs,
+                   cudaStream_t s);
+// Order-preserving orientation filter (reference preprocess.py:49-62).
+int orient_compact_dev(const uint32_t *pairs, uint64_t npairs, const int64_t *deg, uint64_t n,
+                       uint32_t *out_pairs, uint64_t *kept, cudaStream_t s);
+
+// ---------------------------------------------------------------- counting ---
+enum CountAlgo { kAlgoAuto = 0, kAlgoMergeThread = 1 };
+
+struct CountStats {
+    float classify_ms = 0, light_ms = 0, heavy_ms = 0;
+    uint64_t light_vertices = 0, heavy_tasks = 0;
+};
+
+// Triangles over oriented edges [lo, hi).  Result written to *d_total (device u64,
+// accumulated, caller zeroes).  No host synchronisation inside.
+int count_range_dev(const DeviceGraph &g, uint64_t lo, uint64_t hi, int algo,
+                    unsigned long long *d_total, cudaStream_t s, CountStats *stats);
+int intersect_dev(const DeviceGraph &g, uint32_t u, uint32_t v, uint64_t *out, cudaStream_t s);
+// Estimated-work partition of [0, m) into npools ranges (bounds[npools+1], host out).
+int work_bounds_dev(const DeviceGraph &g, int npools, int64_t *bounds, cudaStream_t s);
+// Σ over edges of d+(u)+d+(v) (the merge-model work W), host out.
+int merge_work_dev(const DeviceGraph &g, uint64_t *out, cudaStream_t s);
+
+// ---------------------------------------------------------------- generators ---
+int rmat_dev(int scale, int edge_factor, const double probs[4], const uint64_t state[2],
+             const uint64_t inc[2], uint32_t **pairs_out, uint64_t *npairs_out,
+             uint64_t *nverts_out, cudaStream_t s);
+
+}  // namespace tc

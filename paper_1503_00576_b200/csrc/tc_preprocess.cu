@@ -1,0 +1,385 @@
+// tc_preprocess.cu -- the reference preprocessing pipeline (reference preprocess.py:74-84)
+// as sm_100a kernels.  The reference sorts all 2m pairs, derives degrees from the node
+// array, orients, unzips and rebuilds the node array.  Here the order is
+//   degree histogram -> orient + compact (fused digit histograms) -> LSD radix sort of
+//   the m oriented keys (last pass writes SoA edge_src/edge_dst) -> node array,
+// which yields the bit-identical OrientedGraph: orientation is a per-pair predicate, so
+// filtering before sorting selects the same set, and sorting the survivors gives the
+// order the reference's order-preserving compaction of a sorted list gives.
+#include "tc_common.cuh"
+#include "tc_internal.h"
+
+namespace tc {
+
+int dalloc(void **p, size_t bytes, cudaStream_t s) {
+    *p = nullptr;
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMallocAsync(p, bytes, s);
+    if (e != cudaSuccess) {
+        set_error(std::string("device allocation of ") + std::to_string(bytes) +
+                  " bytes failed: " + cudaGetErrorString(e));
+        return -3;
+    }
+    return 0;
+}
+
+void dfree(void *p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
+namespace {
+
+constexpr int kPP = 8;  // pairs per thread per iteration (warp-striped)
+
+// deg[u] += 1 for every pair (u, .): reference degrees = np.diff(node array of the sorted
+// pairs) (preprocess.py:79-80), i.e. the first-column histogram (graph.py:279-281).
+// Runs of equal u inside a warp (the common, sorted-input case) become one atomic.
+__global__ void __launch_bounds__(256) k_degree_hist(const uint2 *__restrict__ pairs,
+                                                     uint64_t npairs, uint32_t *__restrict__ deg,
+                                                     uint64_t n, unsigned *__restrict__ bad) {
+    const unsigned lane = lane_id();
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t base = gw * 32 * kPP; base < npairs; base += nw * 32 * kPP) {
+        uint2 p[kPP];
+#pragma unroll
+        for (int i = 0; i < kPP; ++i) {
+            uint64_t idx = base + i * 32 + lane;
+            p[i] = idx < npairs ? ld_stream_u2(pairs + idx) : make_uint2(0, 0);
+        }
+#pragma unroll
+        for (int i = 0; i < kPP; ++i) {
+            uint64_t idx = base + i * 32 + lane;
+            bool ok = idx < npairs;
+            uint32_t u = p[i].x;
+            uint32_t prev = __shfl_up_sync(TC_FULL_MASK, u, 1);
+            bool prev_ok = lane > 0 && (idx - 1) < npairs;
+            bool head = !ok || lane == 0 || !prev_ok || prev != u;
+            unsigned heads = __ballot_sync(TC_FULL_MASK, head);
+            if (ok && head) {
+                unsigned above = heads & ~((2u << lane) - 1u);
+                if (lane == 31) above = 0;
+                unsigned next = above ? (unsigned)(__ffs(above) - 1) : 32u;
+                if ((uint64_t)u >= n || (uint64_t)p[i].y >= n) atomicOr(bad, 1u);
+                else atomicAdd(deg + u, next - lane);
+            } else if (ok && (uint64_t)p[i].y >= n) {
+                atomicOr(bad, 1u);
+            }
+        }
+    }
+}
+
+// Keep (u, v) iff (deg u, u) < (deg v, v) (reference preprocess.py:49-62); write the
+// packed key (u << vb) | v for the radix sort, and fold every kept key into the
+// per-pass digit histograms (saves a separate histogram read of the keys).
+// One atomicAdd on the output cursor per block iteration (2048 pairs).
+__global__ void __launch_bounds__(256) k_orient(const uint2 *__restrict__ pairs, uint64_t npairs,
+                                                const uint32_t *__restrict__ deg, uint64_t n, int vb,
+                                                uint64_t *__restrict__ keys, uint64_t capacity,
+                                                unsigned long long *__restrict__ cursor,
+                                                RadixPlan plan, uint32_t *__restrict__ ghist) {
+    __shared__ uint32_t sh[kMaxPasses * kRadix];
+    __shared__ uint32_t s_scan[32];
+    __shared__ unsigned long long s_base;
+    for (int i = threadIdx.x; i < plan.npass * kRadix; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    const uint64_t per_block = (uint64_t)blockDim.x * kPP;
+    for (uint64_t base = (uint64_t)blockIdx.x * per_block; base < npairs;
+         base += (uint64_t)gridDim.x * per_block) {
+        uint64_t key[kPP];
+        unsigned keepmask = 0;
+#pragma unroll
+        for (int i = 0; i < kPP; ++i) {
+            uint64_t idx = base + warp * 32 * kPP + i * 32 + lane;
+            if (idx < npairs) {
+                uint2 p = ld_stream_u2(pairs + idx);
+                if ((uint64_t)p.x >= n || (uint64_t)p.y >= n) continue;  // flagged by k_degree_hist
+                uint32_t du = __ldg(deg + p.x), dv = __ldg(deg + p.y);
+                bool fwd = du < dv || (du == dv && p.x < p.y);
+                key[i] = ((uint64_t)p.x << vb) | p.y;
+                if (fwd) keepmask |= 1u << i;
+            }
+        }
+        uint32_t mine = __popc(keepmask), tot;
+        uint32_t off = block_exclusive_scan<uint32_t>(mine, s_scan, &tot);
+        if (threadIdx.x == 0) s_base = atomicAdd(cursor, (unsigned long long)tot);
+        __syncthreads();
+        uint64_t out = s_base + off;
+#pragma unroll
+        for (int i = 0; i < kPP; ++i) {
+            if (keepmask & (1u << i)) {
+                if (out < capacity) keys[out] = key[i];
+                ++out;
+#pragma unroll
+                for (int p = 0; p < kMaxPasses; ++p)
+                    if (p < plan.npass)
+                        atomicAdd(&sh[p * kRadix + ((key[i] >> plan.shift[p]) & ((1u << plan.bits[p]) - 1))], 1u);
+            }
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < plan.npass * kRadix; i += blockDim.x)
+        if (sh[i]) atomicAdd(&ghist[i], sh[i]);
+}
+
+// Node array from a grouped first column (reference preprocess.py:36-46, paper step
+// 4/8): entry i in [0, k] writes off[w] = i for every w in (firsts[i-1], firsts[i]].
+// Also the u32 copy for the count kernels and the max out-degree.
+__global__ void __launch_bounds__(256) k_node_array(const uint32_t *__restrict__ firsts, uint64_t k,
+                                                    uint64_t n, int64_t *__restrict__ off,
+                                                    uint32_t *__restrict__ off32,
+                                                    uint32_t *__restrict__ max_out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= k; i += stride) {
+        int64_t a = i == 0 ? -1 : (int64_t)firsts[i - 1];
+        int64_t b = i == k ? (int64_t)n : (int64_t)firsts[i];
+        for (int64_t w = a + 1; w <= b; ++w) {
+            off[w] = (int64_t)i;
+            if (off32) off32[w] = (uint32_t)i;
+        }
+    }
+}
+
+// Max out-degree over the node array.
+__global__ void __launch_bounds__(256) k_max_degree(const int64_t *__restrict__ off, uint64_t n,
+                                                    uint32_t *__restrict__ max_out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint32_t best = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        uint32_t d = (uint32_t)(off[i + 1] - off[i]);
+        best = d > best ? d : best;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        uint32_t y = __shfl_xor_sync(TC_FULL_MASK, best, o);
+        best = y > best ? y : best;
+    }
+    if (lane_id() == 0 && best) atomicMax(max_out, best);
+}
+
+// Pack any (u, v) pairs into (u << vb) | v keys (for sorting the unoriented pairs).
+__global__ void k_pack(const uint2 *__restrict__ pairs, uint64_t npairs, int vb,
+                       uint64_t *__restrict__ keys) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += stride) {
+        uint2 p = ld_stream_u2(pairs + i);
+        keys[i] = ((uint64_t)p.x << vb) | p.y;
+    }
+}
+
+// Order-preserving orientation filter for sorted pairs (standalone API step).
+__global__ void __launch_bounds__(256) k_orient_flags(const uint2 *__restrict__ pairs, uint64_t npairs,
+                                                      const int64_t *__restrict__ deg,
+                                                      uint32_t *__restrict__ tile_counts) {
+    __shared__ uint32_t s_scan[32];
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t keep = 0;
+    if (i < npairs) {
+        uint2 p = pairs[i];
+        int64_t du = deg[p.x], dv = deg[p.y];
+        keep = du < dv || (du == dv && p.x < p.y);
+    }
+    uint32_t tot;
+    block_exclusive_scan<uint32_t>(keep, s_scan, &tot);
+    if (threadIdx.x == 0) tile_counts[blockIdx.x] = tot;
+}
+
+__global__ void k_scan_small(uint32_t *__restrict__ counts, uint64_t nblocks,
+                             unsigned long long *__restrict__ excl, unsigned long long *__restrict__ total) {
+    // single block, sequential chunks of 1024
+    __shared__ unsigned long long s_w[32];
+    unsigned long long carry = 0;
+    for (uint64_t b = 0; b < nblocks; b += blockDim.x) {
+        uint64_t i = b + threadIdx.x;
+        unsigned long long x = i < nblocks ? counts[i] : 0;
+        unsigned long long t;
+        unsigned long long e = block_exclusive_scan<unsigned long long>(x, s_w, &t);
+        if (i < nblocks) excl[i] = carry + e;
+        carry += t;
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void __launch_bounds__(256) k_orient_scatter(const uint2 *__restrict__ pairs, uint64_t npairs,
+                                                        const int64_t *__restrict__ deg,
+                                                        const unsigned long long *__restrict__ excl,
+                                                        uint2 *__restrict__ out) {
+    __shared__ uint32_t s_scan[32];
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t keep = 0;
+    uint2 p = make_uint2(0, 0);
+    if (i < npairs) {
+        p = pairs[i];
+        int64_t du = deg[p.x], dv = deg[p.y];
+        keep = du < dv || (du == dv && p.x < p.y);
+    }
+    uint32_t tot;
+    uint32_t pos = block_exclusive_scan<uint32_t>(keep, s_scan, &tot);
+    if (keep) out[excl[blockIdx.x] + pos] = p;
+}
+
+}  // namespace
+
+int graph_alloc(DeviceGraph *g, uint64_t m, uint64_t n, cudaStream_t s) {
+    g->m = m;
+    g->n = n;
+    TC_CHECK(dalloc_t(&g->src, m + 4, s));
+    TC_CHECK(dalloc_t(&g->dst, m + 4, s));  // +16 B so 128-bit tail loads stay in bounds
+    TC_CHECK(dalloc_t(&g->off, n + 1, s));
+    g->off32 = nullptr;
+    if (m < (1ull << 32)) TC_CHECK(dalloc_t(&g->off32, n + 1, s));
+    TC_CUDA(cudaGetDevice(&g->device));
+    return 0;
+}
+
+void graph_release(DeviceGraph *g, cudaStream_t s) {
+    dfree(g->src, s);
+    dfree(g->dst, s);
+    dfree(g->off, s);
+    dfree(g->off32, s);
+    g->src = g->dst = nullptr;
+    g->off = nullptr;
+    g->off32 = nullptr;
+}
+
+int build_node_array_dev(const uint32_t *firsts, uint64_t k, uint64_t n, int64_t *off,
+                         uint32_t *off32, uint32_t *max_out, cudaStream_t s) {
+    k_node_array<<<grid_for(k + 1, 256, kSMs * 16), 256, 0, s>>>(firsts, k, n, off, off32, max_out);
+    TC_CUDA(cudaGetLastError());
+    if (max_out) {
+        TC_CUDA(cudaMemsetAsync(max_out, 0, sizeof(uint32_t), s));
+        if (n) {
+            k_max_degree<<<grid_for(n, 256, kSMs * 8), 256, 0, s>>>(off, n, max_out);
+            TC_CUDA(cudaGetLastError());
+        }
+    }
+    return 0;
+}
+
+int preprocess_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, DeviceGraph *out,
+                   cudaStream_t s) {
+    const uint2 *pairs = reinterpret_cast<const uint2 *>(pairs_u32);
+    if (n >= (1ull << 32)) {
+        set_error("num_vertices must be < 2^32 on the device path");
+        return -1;
+    }
+    const int vb = n > 1 ? bits_for(n - 1) : 1;
+    const RadixPlan plan = make_radix_plan(2 * vb);
+
+    uint32_t *deg = nullptr, *hist = nullptr, *scratch = nullptr;
+    unsigned long long *cursor = nullptr;
+    TC_CHECK(dalloc_t(&deg, n ? n : 1, s));
+    TC_CHECK(dalloc_t(&scratch, 4, s));  // [0] bad-id flag, [1] max out-degree
+    TC_CHECK(dalloc_t(&hist, kMaxPasses * kRadix, s));
+    TC_CHECK(dalloc_t(&cursor, 1, s));
+    TC_CUDA(cudaMemsetAsync(deg, 0, (n ? n : 1) * sizeof(uint32_t), s));
+    TC_CUDA(cudaMemsetAsync(scratch, 0, 4 * sizeof(uint32_t), s));
+    TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+    TC_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
+
+    if (npairs) {
+        k_degree_hist<<<grid_for(npairs, 256 * kPP, kSMs * 8), 256, 0, s>>>(pairs, npairs, deg, n,
+                                                                            scratch);
+        TC_CUDA(cudaGetLastError());
+    }
+    // Valid (symmetric) input keeps exactly npairs/2; anything else is sized on a rerun.
+    uint64_t capacity = npairs / 2 + 1;
+    uint64_t *keys = nullptr, *alt = nullptr;
+    TC_CHECK(dalloc_t(&keys, capacity, s));
+    if (npairs) {
+        k_orient<<<grid_for(npairs, 256 * kPP, kSMs * 8), 256, 0, s>>>(pairs, npairs, deg, n, vb, keys,
+                                                                       capacity, cursor, plan, hist);
+        TC_CUDA(cudaGetLastError());
+    }
+    uint32_t flags[2];
+    unsigned long long kept = 0;
+    TC_CUDA(cudaMemcpyAsync(flags, scratch, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaMemcpyAsync(&kept, cursor, sizeof(kept), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    if (flags[0]) {
+        dfree(deg, s); dfree(scratch, s); dfree(hist, s); dfree(cursor, s); dfree(keys, s);
+        set_error("edge array holds a vertex id >= num_vertices");
+        return -1;
+    }
+    if (kept > capacity) {  // not a symmetric edge array: redo with room for every survivor
+        dfree(keys, s);
+        capacity = kept;
+        TC_CHECK(dalloc_t(&keys, capacity, s));
+        TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+        TC_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
+        k_orient<<<grid_for(npairs, 256 * kPP, kSMs * 8), 256, 0, s>>>(pairs, npairs, deg, n, vb, keys,
+                                                                       capacity, cursor, plan, hist);
+        TC_CUDA(cudaGetLastError());
+    }
+    const uint64_t m = kept;
+    TC_CHECK(graph_alloc(out, m, n, s));
+    TC_CHECK(dalloc_t(&alt, m ? m : 1, s));
+    TC_CHECK(radix_sort(keys, alt, nullptr, nullptr, m, plan, hist, kOutSoA, out->src, out->dst, vb,
+                        nullptr, nullptr, s));
+    TC_CUDA(cudaMemsetAsync(out->dst + m, 0, 4 * sizeof(uint32_t), s));
+    TC_CHECK(build_node_array_dev(out->src, m, n, out->off, out->off32, scratch + 1, s));
+    TC_CUDA(cudaMemcpyAsync(&out->max_out, scratch + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    dfree(deg, s);
+    dfree(hist, s);
+    dfree(cursor, s);
+    dfree(keys, s);
+    dfree(alt, s);
+    dfree(scratch, s);
+    TC_CUDA(cudaStreamSynchronize(s));
+    return 0;
+}
+
+int sort_pairs_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, uint32_t *out_pairs,
+                   cudaStream_t s) {
+    if (npairs == 0) return 0;
+    const uint2 *pairs = reinterpret_cast<const uint2 *>(pairs_u32);
+    const int vb = n > 1 ? bits_for(n - 1) : 1;
+    const RadixPlan plan = make_radix_plan(2 * vb);
+    uint64_t *keys = nullptr, *alt = nullptr;
+    uint32_t *hist = nullptr;
+    TC_CHECK(dalloc_t(&keys, npairs, s));
+    TC_CHECK(dalloc_t(&alt, npairs, s));
+    TC_CHECK(dalloc_t(&hist, kMaxPasses * kRadix, s));
+    TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+    k_pack<<<grid_for(npairs, 256, kSMs * 16), 256, 0, s>>>(pairs, npairs, vb, keys);
+    TC_CUDA(cudaGetLastError());
+    TC_CHECK(radix_histogram(keys, npairs, plan, hist, s));
+    TC_CHECK(radix_sort(keys, alt, nullptr, nullptr, npairs, plan, hist, kOutAoS, out_pairs, nullptr,
+                        vb, nullptr, nullptr, s));
+    dfree(keys, s);
+    dfree(alt, s);
+    dfree(hist, s);
+    return 0;
+}
+
+int orient_compact_dev(const uint32_t *pairs_u32, uint64_t npairs, const int64_t *deg, uint64_t n,
+                       uint32_t *out_pairs, uint64_t *kept, cudaStream_t s) {
+    *kept = 0;
+    if (npairs == 0) return 0;
+    const uint2 *pairs = reinterpret_cast<const uint2 *>(pairs_u32);
+    uint64_t nb = (npairs + 255) / 256;
+    uint32_t *counts = nullptr;
+    unsigned long long *excl = nullptr, *total = nullptr;
+    TC_CHECK(dalloc_t(&counts, nb, s));
+    TC_CHECK(dalloc_t(&excl, nb, s));
+    TC_CHECK(dalloc_t(&total, 1, s));
+    k_orient_flags<<<(unsigned)nb, 256, 0, s>>>(pairs, npairs, deg, counts);
+    TC_CUDA(cudaGetLastError());
+    k_scan_small<<<1, 512, 0, s>>>(counts, nb, excl, total);
+    TC_CUDA(cudaGetLastError());
+    k_orient_scatter<<<(unsigned)nb, 256, 0, s>>>(pairs, npairs, deg, excl,
+                                                  reinterpret_cast<uint2 *>(out_pairs));
+    TC_CUDA(cudaGetLastError());
+    unsigned long long t = 0;
+    TC_CUDA(cudaMemcpyAsync(&t, total, sizeof(t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    *kept = t;
+    dfree(counts, s);
+    dfree(excl, s);
+    dfree(total, s);
+    return 0;
+}
+
+}  // namespace tc

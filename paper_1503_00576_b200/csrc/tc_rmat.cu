@@ -1,0 +1,362 @@
+// tc_rmat.cu -- device R-MAT generator, bit-identical to the reference
+// tricount.generators.rmat (reference generators.py:203-284) for the same seed.
+//
+// The reference draws, per batch, `scale` arrays of float64 from numpy's
+// default_rng(seed) (PCG64 XSL-RR: state = state*M + inc, then output; random() =
+// (next64 >> 11) * 2^-53), descends the 2x2 quadrant split, drops self-loops, keeps the
+// first occurrence of every canonical key (lo << 32 | hi) in draw order, drops keys it
+// already has, takes the first `need` survivors and merges them into the sorted set.
+// Here every draw is computed independently by jumping the 128-bit LCG to its stream
+// position, and "first occurrence in draw order" is recovered with a stable key/value
+// radix sort (value = draw index) plus a scan over draw positions.  Input production for
+// parity tests and the bench only; not on the timed path.
+#include "tc_common.cuh"
+#include "tc_internal.h"
+
+namespace tc {
+
+namespace {
+
+typedef unsigned __int128 u128;
+constexpr int kJumpBits = 40;
+constexpr int kMaxScale = 30;
+constexpr int kRmatJ = 16;  // consecutive draws per thread per level
+
+struct JumpTable {
+    unsigned long long a_lo[kJumpBits], a_hi[kJumpBits], c_lo[kJumpBits], c_hi[kJumpBits];
+};
+__constant__ JumpTable c_jump;
+
+struct LevelStates {
+    unsigned long long lo[kMaxScale], hi[kMaxScale];
+};
+
+const u128 kPcgMult = ((u128)0x2360ED051FC65DA4ULL << 64) | 0x4385DF649FCCF645ULL;
+
+__device__ __forceinline__ u128 mk128(unsigned long long hi, unsigned long long lo) {
+    return ((u128)hi << 64) | lo;
+}
+
+__device__ __forceinline__ uint64_t pcg_out(u128 s) {
+    const uint64_t hi = (uint64_t)(s >> 64), lo = (uint64_t)s;
+    const unsigned rot = (unsigned)(s >> 122);
+    const uint64_t x = hi ^ lo;
+    return (x >> rot) | (x << ((64 - rot) & 63));
+}
+
+// Draw-position-parallel level loop (reference generators.py:249-256).  Key layout:
+// (lo << scale) | hi for a proper edge, 1 << (2*scale) for a self-loop (sorts last).
+__global__ void __launch_bounds__(256) k_rmat_draw(uint64_t batch, int scale, double a, double t_ab,
+                                                   double t_abc, LevelStates ls,
+                                                   unsigned long long inc_hi,
+                                                   unsigned long long inc_lo,
+                                                   uint64_t *__restrict__ keys,
+                                                   uint32_t *__restrict__ idx) {
+    const u128 mult = ((u128)0x2360ED051FC65DA4ULL << 64) | 0x4385DF649FCCF645ULL;
+    const u128 inc = mk128(inc_hi, inc_lo);
+    const uint64_t j0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRmatJ;
+    if (j0 >= batch) return;
+    uint32_t src[kRmatJ], dst[kRmatJ];
+#pragma unroll
+    for (int j = 0; j < kRmatJ; ++j) src[j] = dst[j] = 0;
+    for (int l = 0; l < scale; ++l) {
+        u128 s = mk128(ls.hi[l], ls.lo[l]);
+        uint64_t d = j0;
+        for (int k = 0; d; ++k, d >>= 1)
+            if (d & 1) s = mk128(c_jump.a_hi[k], c_jump.a_lo[k]) * s + mk128(c_jump.c_hi[k], c_jump.c_lo[k]);
+#pragma unroll
+        for (int j = 0; j < kRmatJ; ++j) {
+            s = s * mult + inc;
+            const double r = (double)(pcg_out(s) >> 11) * (1.0 / 9007199254740992.0);
+            const uint32_t sb = r >= t_ab;
+            const uint32_t db = (r >= a && r < t_ab) || r >= t_abc;
+            src[j] = (src[j] << 1) | sb;
+            dst[j] = (dst[j] << 1) | db;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kRmatJ; ++j) {
+        const uint64_t p = j0 + j;
+        if (p < batch) {
+            const uint32_t lo = src[j] < dst[j] ? src[j] : dst[j];
+            const uint32_t hi = src[j] < dst[j] ? dst[j] : src[j];
+            keys[p] = src[j] == dst[j] ? (1ull << (2 * scale)) : (((uint64_t)lo << scale) | hi);
+            idx[p] = (uint32_t)p;
+        }
+    }
+}
+
+// First occurrence of each valid key not already in `have` -> flag[draw index] = 1.
+__global__ void k_rmat_heads(const uint64_t *__restrict__ sk, const uint32_t *__restrict__ sv,
+                             uint64_t batch, int scale, const uint64_t *__restrict__ have,
+                             uint64_t have_n, uint32_t *__restrict__ flag,
+                             uint64_t *__restrict__ cand) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t lim = 1ull << (2 * scale);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < batch; i += stride) {
+        const uint64_t k = sk[i];
+        if (k >= lim) continue;
+        if (i > 0 && sk[i - 1] == k) continue;
+        if (have_n) {
+            uint64_t lo = 0, n = have_n;
+            while (n > 0) {
+                const uint64_t half = n >> 1;
+                if (have[lo + half] < k) { lo += half + 1; n -= half + 1; }
+                else n = half;
+            }
+            if (lo < have_n && have[lo] == k) continue;
+        }
+        const uint32_t j = sv[i];
+        flag[j] = 1;
+        cand[j] = k;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_tile_count(const uint32_t *__restrict__ flag, uint64_t n,
+                                                    uint32_t *__restrict__ sums) {
+    const uint64_t b = (uint64_t)blockIdx.x * 4096;
+    uint32_t acc = 0;
+    for (uint64_t i = b + threadIdx.x; i < b + 4096 && i < n; i += 256) acc += flag[i];
+    __shared__ uint32_t s_red[8];
+    acc = warp_sum(acc);
+    if (lane_id() == 0) s_red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < 8; ++w) t += s_red[w];
+        sums[blockIdx.x] = t;
+    }
+}
+
+__global__ void k_scan_tiles(uint32_t *__restrict__ sums, uint64_t nt,
+                             unsigned long long *__restrict__ total) {
+    __shared__ uint32_t s_w[32];
+    uint32_t carry = 0;
+    for (uint64_t b = 0; b < nt; b += blockDim.x) {
+        const uint64_t i = b + threadIdx.x;
+        const uint32_t x = i < nt ? sums[i] : 0;
+        uint32_t t;
+        const uint32_t e = block_exclusive_scan<uint32_t>(x, s_w, &t);
+        if (i < nt) sums[i] = carry + e;
+        carry += t;
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+
+// Selected candidates (the first `need` in draw order) -> out[rank].
+__global__ void __launch_bounds__(256) k_rmat_select(const uint32_t *__restrict__ flag,
+                                                     const uint64_t *__restrict__ cand, uint64_t n,
+                                                     const uint32_t *__restrict__ tile_base,
+                                                     uint64_t need, uint64_t *__restrict__ out) {
+    __shared__ uint32_t s_w[32];
+    const uint64_t b = (uint64_t)blockIdx.x * 4096;
+    uint32_t carry = tile_base[blockIdx.x];
+    for (uint64_t c = b; c < b + 4096; c += 256) {
+        const uint64_t i = c + threadIdx.x;
+        const uint32_t f = i < n ? flag[i] : 0;
+        uint32_t t;
+        const uint32_t e = block_exclusive_scan<uint32_t>(f, s_w, &t);
+        if (f && (uint64_t)(carry + e) < need) out[carry + e] = cand[i];
+        carry += t;
+    }
+}
+
+__global__ void k_sym(const uint64_t *__restrict__ have, uint64_t n, int scale,
+                      uint64_t *__restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t mask = (1ull << scale) - 1;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint64_t k = have[i];
+        const uint64_t lo = k >> scale, hi = k & mask;
+        out[2 * i] = k;
+        out[2 * i + 1] = (hi << scale) | lo;
+    }
+}
+
+__global__ void k_max_hi(const uint64_t *__restrict__ have, uint64_t n, int scale,
+                         uint32_t *__restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t mask = (1ull << scale) - 1;
+    uint32_t best = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t h = (uint32_t)(have[i] & mask);
+        best = h > best ? h : best;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint32_t y = __shfl_xor_sync(TC_FULL_MASK, best, o);
+        best = y > best ? y : best;
+    }
+    if (lane_id() == 0) atomicMax(out, best);
+}
+
+u128 advance_host(u128 s, u128 inc, uint64_t delta) {
+    u128 am = 1, ap = 0, cm = kPcgMult, cp = inc;
+    while (delta) {
+        if (delta & 1) {
+            am *= cm;
+            ap = ap * cm + cp;
+        }
+        cp = (cm + 1) * cp;
+        cm *= cm;
+        delta >>= 1;
+    }
+    return am * s + ap;
+}
+
+}  // namespace
+
+int rmat_dev(int scale, int edge_factor, const double probs[4], const uint64_t state[2],
+             const uint64_t inc_in[2], uint32_t **pairs_out, uint64_t *npairs_out,
+             uint64_t *nverts_out, cudaStream_t s) {
+    if (scale < 1 || scale > kMaxScale || 2 * scale + 1 > 63) {
+        set_error("rmat: scale must be in 1..30");
+        return -1;
+    }
+    const double a = probs[0], b = probs[1], c = probs[2];
+    const double t_ab = a + b, t_abc = a + b + c;
+    const uint64_t n = 1ull << scale;
+    const uint64_t target = (uint64_t)edge_factor * n;
+    if (target > n * (n - 1) / 2) {
+        set_error("rmat: edge_factor too large for a simple graph");
+        return -1;
+    }
+    const u128 s0 = ((u128)state[0] << 64) | state[1];
+    const u128 inc = ((u128)inc_in[0] << 64) | inc_in[1];
+    {
+        JumpTable jt;
+        u128 am = kPcgMult, ap = inc;
+        for (int k = 0; k < kJumpBits; ++k) {
+            jt.a_lo[k] = (unsigned long long)am;
+            jt.a_hi[k] = (unsigned long long)(am >> 64);
+            jt.c_lo[k] = (unsigned long long)ap;
+            jt.c_hi[k] = (unsigned long long)(ap >> 64);
+            ap = ap * (am + 1);
+            am = am * am;
+        }
+        TC_CUDA(cudaMemcpyToSymbolAsync(c_jump, &jt, sizeof(jt), 0, cudaMemcpyHostToDevice, s));
+    }
+    const RadixPlan draw_plan = make_radix_plan(2 * scale + 1);
+    const RadixPlan have_plan = make_radix_plan(2 * scale);
+    uint64_t *have = nullptr;
+    uint64_t have_n = 0, drawn = 0;
+    int stalled = 0;
+    uint32_t *hist = nullptr, *tsum = nullptr;
+    unsigned long long *d_total = nullptr;
+    TC_CHECK(dalloc_t(&hist, kMaxPasses * kRadix, s));
+    TC_CHECK(dalloc_t(&d_total, 1, s));
+    while (have_n < target) {
+        const uint64_t need = target - have_n;
+        uint64_t batch = (uint64_t)((double)need * 1.3);
+        if (batch < 4096) batch = 4096;
+        if (batch >= (1ull << 32)) {
+            set_error("rmat: batch exceeds 2^32 draws");
+            return -1;
+        }
+        LevelStates ls;
+        for (int l = 0; l < scale; ++l) {
+            const u128 st = advance_host(s0, inc, drawn + (uint64_t)l * batch);
+            ls.lo[l] = (unsigned long long)st;
+            ls.hi[l] = (unsigned long long)(st >> 64);
+        }
+        uint64_t *keys = nullptr, *alt = nullptr, *cand = nullptr, *sk = nullptr;
+        uint32_t *idx = nullptr, *valt = nullptr, *flag = nullptr, *sv = nullptr;
+        TC_CHECK(dalloc_t(&keys, batch, s));
+        TC_CHECK(dalloc_t(&alt, batch, s));
+        TC_CHECK(dalloc_t(&idx, batch, s));
+        TC_CHECK(dalloc_t(&valt, batch, s));
+        const uint64_t threads = (batch + kRmatJ - 1) / kRmatJ;
+        k_rmat_draw<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+            batch, scale, a, t_ab, t_abc, ls, (unsigned long long)(inc >> 64),
+            (unsigned long long)inc, keys, idx);
+        TC_CUDA(cudaGetLastError());
+        drawn += batch * (uint64_t)scale;
+        TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+        TC_CHECK(radix_histogram(keys, batch, draw_plan, hist, s));
+        TC_CHECK(radix_sort(keys, alt, idx, valt, batch, draw_plan, hist, kOutKeys, nullptr, nullptr, 0,
+                            &sk, &sv, s));
+        // free the non-result ping-pong halves before the next big allocations
+        uint64_t *kfree = sk == keys ? alt : keys;
+        uint32_t *vfree = sv == idx ? valt : idx;
+        dfree(kfree, s);
+        dfree(vfree, s);
+        TC_CHECK(dalloc_t(&flag, batch, s));
+        TC_CHECK(dalloc_t(&cand, batch, s));
+        TC_CUDA(cudaMemsetAsync(flag, 0, batch * sizeof(uint32_t), s));
+        k_rmat_heads<<<grid_for(batch, 256, kSMs * 16), 256, 0, s>>>(sk, sv, batch, scale, have, have_n,
+                                                                     flag, cand);
+        TC_CUDA(cudaGetLastError());
+        dfree(sk, s);
+        dfree(sv, s);
+        const uint64_t nt = (batch + 4095) / 4096;
+        TC_CHECK(dalloc_t(&tsum, nt, s));
+        k_tile_count<<<(unsigned)nt, 256, 0, s>>>(flag, batch, tsum);
+        TC_CUDA(cudaGetLastError());
+        k_scan_tiles<<<1, 512, 0, s>>>(tsum, nt, d_total);
+        TC_CUDA(cudaGetLastError());
+        unsigned long long cands = 0;
+        TC_CUDA(cudaMemcpyAsync(&cands, d_total, sizeof(cands), cudaMemcpyDeviceToHost, s));
+        TC_CUDA(cudaStreamSynchronize(s));
+        const uint64_t take = cands < need ? cands : need;
+        uint64_t *merged = nullptr, *malt = nullptr;
+        if (take) {
+            TC_CHECK(dalloc_t(&merged, have_n + take, s));
+            if (have_n)
+                TC_CUDA(cudaMemcpyAsync(merged, have, have_n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+            k_rmat_select<<<(unsigned)nt, 256, 0, s>>>(flag, cand, batch, tsum, need, merged + have_n);
+            TC_CUDA(cudaGetLastError());
+        }
+        dfree(flag, s);
+        dfree(cand, s);
+        dfree(tsum, s);
+        if (take == 0) {
+            if (++stalled >= 25) {
+                set_error("rmat sampling saturated below the target edge count");
+                return -1;
+            }
+            continue;
+        }
+        stalled = 0;
+        dfree(have, s);
+        TC_CHECK(dalloc_t(&malt, have_n + take, s));
+        TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+        TC_CHECK(radix_histogram(merged, have_n + take, have_plan, hist, s));
+        uint64_t *sorted = nullptr;
+        TC_CHECK(radix_sort(merged, malt, nullptr, nullptr, have_n + take, have_plan, hist, kOutKeys,
+                            nullptr, nullptr, 0, &sorted, nullptr, s));
+        dfree(sorted == merged ? malt : merged, s);
+        have = sorted;
+        have_n += take;
+    }
+    // edge_array_from_undirected (reference graph.py:265-276): both directions, sorted.
+    uint32_t *maxhi = nullptr;
+    TC_CHECK(dalloc_t(&maxhi, 1, s));
+    TC_CUDA(cudaMemsetAsync(maxhi, 0, sizeof(uint32_t), s));
+    k_max_hi<<<grid_for(target, 256, kSMs * 8), 256, 0, s>>>(have, target, scale, maxhi);
+    TC_CUDA(cudaGetLastError());
+    uint64_t *both = nullptr, *balt = nullptr;
+    uint32_t *pairs = nullptr;
+    TC_CHECK(dalloc_t(&both, 2 * target, s));
+    k_sym<<<grid_for(target, 256, kSMs * 16), 256, 0, s>>>(have, target, scale, both);
+    TC_CUDA(cudaGetLastError());
+    dfree(have, s);
+    TC_CHECK(dalloc_t(&balt, 2 * target, s));
+    TC_CHECK(dalloc_t(&pairs, 4 * target + 4, s));
+    TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+    TC_CHECK(radix_histogram(both, 2 * target, have_plan, hist, s));
+    TC_CHECK(radix_sort(both, balt, nullptr, nullptr, 2 * target, have_plan, hist, kOutAoS, pairs,
+                        nullptr, scale, nullptr, nullptr, s));
+    uint32_t mh = 0;
+    TC_CUDA(cudaMemcpyAsync(&mh, maxhi, sizeof(mh), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    dfree(both, s);
+    dfree(balt, s);
+    dfree(maxhi, s);
+    dfree(hist, s);
+    dfree(d_total, s);
+    *pairs_out = pairs;
+    *npairs_out = 2 * target;
+    *nverts_out = (uint64_t)mh + 1;
+    return 0;
+}
+
+}  // namespace tc

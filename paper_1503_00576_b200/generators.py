@@ -1,0 +1,103 @@
+"""Synthetic inputs for the parity tests and the bench (input production, not timed).
+
+``rmat`` reproduces reference generators.py:203-284 bit-for-bit on the device
+(tc_gen_rmat: PCG64 stream positions are jumped to directly, first-occurrence
+de-duplication via a stable key/value radix sort); the same seed gives the same
+EdgeArray as ``tricount.generators.rmat`` (pinned by sha256 in tests/golden).
+Host buffers handed back are pinned (cudaHostAlloc) so the timed host->device copy
+in count_with_timings runs at PCIe speed.
+"""
+from __future__ import annotations
+
+import ctypes
+import weakref
+
+import numpy as np
+
+from . import _lib
+from .graph import EdgeArray
+
+RMAT_DEFAULT_PROBS = (0.57, 0.19, 0.19, 0.05)
+RMAT_DEFAULT_EDGE_FACTOR = 16
+
+
+def _pcg64_words(seed: int):
+    """numpy default_rng(seed)'s PCG64 (state, inc) as (hi, lo) uint64 words."""
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    m = (1 << 64) - 1
+    return (s >> 64, s & m), (inc >> 64, inc & m)
+
+
+class DeviceEdges:
+    """An edge array resident in HBM: npairs (u, v) uint32 pairs at ``ptr``."""
+
+    def __init__(self, ptr: int, npairs: int, num_vertices: int):
+        self.ptr = int(ptr)
+        self.npairs = int(npairs)
+        self.num_vertices = int(num_vertices)
+        self._fin = weakref.finalize(self, _lib.lib().tc_device_free, ctypes.c_void_p(self.ptr))
+
+    @property
+    def nbytes(self) -> int:
+        return self.npairs * 8
+
+    def to_host(self, pinned: bool = True) -> EdgeArray:
+        arr = pinned_empty((self.npairs, 2), np.uint32) if pinned else np.empty((self.npairs, 2), np.uint32)
+        if self.npairs:
+            _lib.check(_lib.lib().tc_memcpy(_lib.ptr(arr), ctypes.c_void_p(self.ptr), self.nbytes, 1))
+        return EdgeArray(arr, num_vertices=self.num_vertices)
+
+    def free(self) -> None:
+        self._fin()
+
+
+class _PinnedOwner:
+    def __init__(self, p: int):
+        self.p = p
+        self._fin = weakref.finalize(self, _lib.lib().tc_host_free, ctypes.c_void_p(p))
+
+
+def pinned_empty(shape, dtype) -> np.ndarray:
+    """numpy array over page-locked host memory (freed with the array)."""
+    dtype = np.dtype(dtype)
+    nbytes = int(np.prod(shape)) * dtype.itemsize
+    p = ctypes.c_void_p()
+    _lib.check(_lib.lib().tc_host_alloc(max(nbytes, 16), ctypes.byref(p)))
+    owner = _PinnedOwner(p.value)
+    buf = (ctypes.c_byte * max(nbytes, 16)).from_address(p.value)
+    arr = np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+    # tie the owner's lifetime to the array through the ctypes buffer object
+    buf._owner = owner
+    return arr
+
+
+def rmat_device(scale: int, edge_factor: int = RMAT_DEFAULT_EDGE_FACTOR, *,
+                probs=RMAT_DEFAULT_PROBS, seed: int = 0) -> DeviceEdges:
+    """reference rmat(scale, edge_factor, probs, seed), generated and kept on the device."""
+    if not 1 <= scale <= 30:
+        raise ValueError(f"scale: must be in 1..30, got {scale}")
+    if edge_factor < 1:
+        raise ValueError(f"edge_factor: must be >= 1, got {edge_factor}")
+    a, b, c, d = (float(x) for x in probs)
+    if min(a, b, c, d) < 0 or abs(a + b + c + d - 1.0) > 1e-9:
+        raise ValueError(f"probs: must be nonnegative and sum to 1, got {probs}")
+    (sh, sl), (ih, il) = _pcg64_words(seed)
+    pr = (ctypes.c_double * 4)(a, b, c, d)
+    state = (ctypes.c_uint64 * 2)(sh, sl)
+    inc = (ctypes.c_uint64 * 2)(ih, il)
+    p = ctypes.c_void_p()
+    npairs, nverts = ctypes.c_uint64(), ctypes.c_uint64()
+    _lib.check(_lib.lib().tc_gen_rmat(int(scale), int(edge_factor), pr, state, inc, ctypes.byref(p),
+                                      ctypes.byref(npairs), ctypes.byref(nverts)))
+    return DeviceEdges(p.value, npairs.value, nverts.value)
+
+
+def rmat(scale: int, edge_factor: int = RMAT_DEFAULT_EDGE_FACTOR, *,
+         probs=RMAT_DEFAULT_PROBS, seed: int = 0, pinned: bool = True) -> EdgeArray:
+    """Host EdgeArray of reference rmat(...) (device-generated, copied back once)."""
+    dev = rmat_device(scale, edge_factor, probs=probs, seed=seed)
+    try:
+        return dev.to_host(pinned=pinned)
+    finally:
+        dev.free()

@@ -1,0 +1,63 @@
+"""CPU checks of the drop-in boundary: the C-ABI library loads and exports every
+symbol include/tricount_b200.h declares; the ctypes signatures cover all of them."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "tricount_b200.h")
+
+
+def _declared():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(tc_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_entry_points():
+    names = _declared()
+    for must in ("tc_init", "tc_preprocess", "tc_count", "tc_count_partitioned",
+                 "tc_count_with_timings", "tc_graph_upload", "tc_graph_download",
+                 "tc_intersect_count", "tc_work_bounds", "tc_sort_edges",
+                 "tc_build_node_array", "tc_orient_and_compact", "tc_gen_rmat"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1503_00576_b200 import _lib
+
+    L = _lib.load(init=False)
+    for name in _declared():
+        assert hasattr(L, name), name
+        assert name in _lib.EXPORTED, f"{name} has no ctypes signature"
+    assert L.tc_abi_version() == 1
+
+
+def test_library_is_sm100a_only():
+    """The .so carries sm_100a SASS (cuobjdump) and no CPU compute path."""
+    import shutil
+    import subprocess
+
+    from paper_1503_00576_b200 import _lib
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([tool, "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_gpu_raises_loudly():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1503_00576_b200 import _lib
+
+    L = _lib.load(init=False)
+    assert L.tc_init(0) != 0
+    assert L.tc_last_error()

@@ -1,0 +1,172 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the oracle and the golden
+vectors produced by the reference.  Integer work: every comparison is bit-exact."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import sha
+
+pytestmark = pytest.mark.gpu
+
+tcb = pytest.importorskip("paper_1503_00576_b200")
+from paper_1503_00576_b200 import _lib, generators  # noqa: E402
+from paper_1503_00576_b200.graph import EdgeArray, OrientedGraph, validate_oriented_graph  # noqa: E402
+
+
+def _csr(og):
+    return og.edge_src, og.edge_dst, og.node_offsets
+
+
+def _count_all_ways(og, expected):
+    assert tcb.count_triangles(og) == expected
+    assert tcb.count_device(og, algo=_lib.ALGO_MERGE_THREAD)[0] == expected
+    for pools in (2, 3, 5):
+        assert tcb.count_partitioned(og, tcb.PartitionPlan.even(pools, og.m_dir), 1) == expected
+
+
+def test_small_cases(golden):
+    for case in golden["small"]:
+        g = EdgeArray(np.asarray(case["input"], dtype=np.uint32).reshape(-1, 2))
+        og = tcb.preprocess(g)
+        assert og.edge_src.tolist() == case["edge_src"], case["name"]
+        assert og.edge_dst.tolist() == case["edge_dst"], case["name"]
+        assert og.node_offsets.tolist() == case["node_offsets"], case["name"]
+        if og.m_dir:
+            _count_all_ways(og, case["triangles"])
+        else:
+            assert tcb.count_triangles(og) == 0
+        t, timings = tcb.count_with_timings(g)
+        assert t == case["triangles"]
+
+
+def test_intersect_handmade(golden):
+    h = golden["intersect_handmade"]
+    og = OrientedGraph(np.array(h["edge_src"], np.uint32), np.array(h["edge_dst"], np.uint32),
+                       np.array(h["node_offsets"], np.int64))
+    assert tcb.intersect_count(og, 0, 1) == 2
+    assert tcb.count_triangles(og) == 0
+
+
+@pytest.mark.parametrize("corpus", ["C1_20240615", "C3_77"])
+def test_corpora(golden, corpus):
+    for i, rec in enumerate(golden["corpora"][corpus]):
+        pairs = oracle.gnp_pairs(rec["n_param"], rec["p"], rec["seed"])
+        og = tcb.preprocess(EdgeArray(pairs))
+        assert sha(*_csr(og)) == rec["csr_sha256"]
+        assert tcb.count_triangles(og, 1 + i % 8) == rec["triangles"]
+
+
+@pytest.mark.parametrize("name", ["rmat_8_4_1", "rmat_10_8_7", "rmat_12_16_99",
+                                  "rmat_16_76_20240616"])
+def test_rmat_generator_and_pipeline(golden, name):
+    rec = golden["graphs"][name]
+    g = generators.rmat(rec["scale"], rec["edge_factor"], seed=rec["seed"])
+    assert sha(g.edges) == rec["edges_sha256"], "device rmat must equal reference rmat"
+    assert g.num_vertices == rec["n"]
+    og = tcb.preprocess(g)
+    assert sha(*_csr(og)) == rec["csr_sha256"]
+    assert og.device().max_out == rec["max_out_degree"]
+    assert tcb.merge_work(og) == rec["merge_work"]
+    _count_all_ways(og, rec["triangles"])
+
+
+def test_er_config(golden):
+    rec = golden["graphs"]["er_1e4"]
+    pairs = oracle.gnp_pairs(rec["n_param"], rec["p"], rec["seed"])
+    assert sha(pairs) == rec["edges_sha256"]
+    og = tcb.preprocess(EdgeArray(pairs))
+    assert sha(*_csr(og)) == rec["csr_sha256"]
+    _count_all_ways(og, rec["triangles"])
+    assert rec["triangles"] == 1343
+
+
+def test_shuffled_input_same_csr():
+    pairs = oracle.symmetrize(oracle.rmat_pairs(12, 16, seed=99))
+    ref = tcb.preprocess(EdgeArray(pairs))
+    perm = np.random.default_rng(1).permutation(pairs.shape[0])
+    shuf = tcb.preprocess(EdgeArray(pairs[perm]))
+    assert ref == shuf
+    validate_oriented_graph(shuf)
+
+
+def test_substeps_match_oracle(golden):
+    rec = golden["graphs"]["rmat_12_16_99"]
+    pairs = oracle.symmetrize(oracle.rmat_pairs(12, 16, seed=99))
+    perm = np.random.default_rng(2).permutation(pairs.shape[0])
+    g = EdgeArray(pairs[perm])
+    s = tcb.sort_edges(g)
+    assert np.array_equal(s.edges, pairs)
+    off_all = tcb.build_node_array(s, g.num_vertices)
+    assert np.array_equal(off_all, oracle.build_node_array(pairs[:, 0], g.num_vertices))
+    deg = tcb.DegreeOrder(np.diff(off_all))
+    directed = tcb.orient_and_compact(s, deg)
+    src, dst, off = oracle.preprocess(pairs)
+    assert np.array_equal(directed[:, 0], src) and np.array_equal(directed[:, 1], dst)
+    assert np.array_equal(tcb.build_node_array(directed[:, 0], g.num_vertices), off)
+
+
+def test_upload_path_and_partitions(golden):
+    rec = golden["graphs"]["rmat_12_16_99"]
+    src, dst, off = oracle.preprocess(oracle.symmetrize(oracle.rmat_pairs(12, 16, seed=99)))
+    og = OrientedGraph(src, dst, off)
+    _count_all_ways(og, rec["triangles"])
+    for pools in (1, 2, 4, 8):
+        plan = tcb.PartitionPlan.work_balanced(og, pools)
+        plan.check_covers(og.m_dir)
+        assert tcb.count_partitioned(og, plan, 2) == rec["triangles"]
+        # every single pool agrees with the oracle's count over the same edge range
+        for p in range(pools):
+            lo, hi = plan.pool_range(p)
+            assert tcb.count_device(og, lo, hi)[0] == _range_oracle(src, dst, off, lo, hi)
+
+
+def _range_oracle(src, dst, off, lo, hi):
+    lib = oracle.lib()
+    return int(lib.or_count_strided(oracle._c32(src), oracle._c32(dst), oracle._c64(off), lo, hi, 0, 1))
+
+
+def test_range_counts_match_oracle():
+    src, dst, off = oracle.preprocess(oracle.symmetrize(oracle.rmat_pairs(12, 16, seed=99)))
+    og = OrientedGraph(src, dst, off)
+    rng = np.random.default_rng(7)
+    for _ in range(20):
+        lo, hi = sorted(int(x) for x in rng.integers(0, og.m_dir + 1, size=2))
+        assert tcb.count_device(og, lo, hi)[0] == _range_oracle(src, dst, off, lo, hi)
+
+
+def test_rejects_bad_arguments():
+    og = tcb.preprocess(EdgeArray([(0, 1), (1, 0)]))
+    with pytest.raises(ValueError):
+        tcb.count_triangles(og, 0)
+    with pytest.raises(ValueError):
+        tcb.count_partitioned(og, tcb.PartitionPlan(2, (0, 1, 2)), 1)
+    with pytest.raises(ValueError):
+        tcb.count_device(og, 0, 5)
+
+
+def test_big_rmat_s20(golden_big):
+    rec = golden_big.get("rmat_20_16_0")
+    if rec is None:
+        pytest.skip("s20 golden not generated")
+    g = generators.rmat_device(20, 16, seed=0)
+    h = g.to_host()
+    assert sha(h.edges) == rec["edges_sha256"]
+    og, _ = tcb.preprocess_device(g)
+    assert sha(*_csr(og)) == rec["csr_sha256"]
+    assert tcb.count_triangles(og) == rec["triangles"] == 490_084_299
+    assert tcb.count_device(og, algo=_lib.ALGO_MERGE_THREAD)[0] == rec["triangles"]
+    t, _ = tcb.count_with_timings_device(g)
+    assert t == rec["triangles"]
+
+
+@pytest.mark.parametrize("scale", [21, 22])
+def test_big_rmat_counts(golden_big, scale):
+    rec = golden_big.get(f"rmat_{scale}_16_0")
+    if rec is None:
+        pytest.skip(f"s{scale} golden not generated")
+    g = generators.rmat_device(scale, 16, seed=0)
+    og, _ = tcb.preprocess_device(g)
+    assert sha(*_csr(og)) == rec["csr_sha256"]
+    assert tcb.count_triangles(og) == rec["triangles"]

@@ -1,0 +1,73 @@
+"""Pin the CPU oracle (oracle/) against golden vectors produced by the reference."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import sha
+
+
+def test_small_cases_bit_exact(golden):
+    for case in golden["small"]:
+        pairs = np.asarray(case["input"], dtype=np.uint32).reshape(-1, 2)
+        src, dst, off = oracle.preprocess(pairs)
+        assert src.tolist() == case["edge_src"], case["name"]
+        assert dst.tolist() == case["edge_dst"], case["name"]
+        assert off.tolist() == case["node_offsets"], case["name"]
+        assert oracle.count(src, dst, off, workers=3) == case["triangles"], case["name"]
+        rs, rd, ro = oracle.reference_preprocess(pairs)
+        assert (rs, rd, ro) == (case["edge_src"], case["edge_dst"], case["node_offsets"])
+
+
+def test_pure_python_oracles_agree(golden):
+    for case in golden["small"]:
+        pairs = np.asarray(case["input"], dtype=np.uint32).reshape(-1, 2)
+        assert oracle.brute_force_count(pairs) == case["triangles"], case["name"]
+        assert oracle.sequential_forward_count(pairs) == case["triangles"], case["name"]
+
+
+def test_intersect_handmade(golden):
+    h = golden["intersect_handmade"]
+    dst = np.asarray(h["edge_dst"], np.uint32)
+    off = np.asarray(h["node_offsets"], np.int64)
+    assert oracle.intersect_count(dst, off, 0, 1) == h["intersect_0_1"] == 2
+
+
+@pytest.mark.parametrize("corpus", ["C1_20240615", "C3_77"])
+def test_corpus_generation_and_counts(golden, corpus):
+    for rec in golden["corpora"][corpus]:
+        pairs = oracle.gnp_pairs(rec["n_param"], rec["p"], rec["seed"])
+        assert sha(pairs) == rec["edges_sha256"]
+        src, dst, off = oracle.preprocess(pairs)
+        assert sha(src, dst, off) == rec["csr_sha256"]
+        assert oracle.count(src, dst, off, workers=2) == rec["triangles"]
+
+
+def _regen(rec):
+    if rec["gen"] == "gnp":
+        return oracle.gnp_pairs(rec["n_param"], rec["p"], rec["seed"])
+    if rec["gen"] == "rmat":
+        return oracle.symmetrize(oracle.rmat_pairs(rec["scale"], rec["edge_factor"], rec["seed"]))
+    pytest.skip(f"no oracle generator for {rec['gen']}")
+
+
+@pytest.mark.parametrize("name", ["er_1e4", "rmat_8_4_1", "rmat_10_8_7", "rmat_12_16_99",
+                                  "rmat_16_76_20240616"])
+def test_graph_goldens(golden, name):
+    rec = golden["graphs"][name]
+    pairs = _regen(rec)
+    assert sha(pairs) == rec["edges_sha256"]
+    src, dst, off = oracle.preprocess(pairs)
+    assert sha(src, dst, off) == rec["csr_sha256"]
+    assert oracle.merge_work(src, dst, off) == rec["merge_work"]
+    assert oracle.count(src, dst, off) == rec["triangles"]
+
+
+def test_partitioned_matches(golden):
+    rec = golden["graphs"]["rmat_12_16_99"]
+    src, dst, off = oracle.preprocess(_regen(rec))
+    m = dst.size
+    for pools in (1, 2, 3, 4, 8):
+        bounds = np.linspace(0, m, pools + 1).astype(np.int64)
+        assert oracle.count_partitioned(src, dst, off, bounds, workers=2) == rec["triangles"]
