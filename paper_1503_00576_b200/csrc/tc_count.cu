@@ -6,11 +6,11 @@
 // which is what this file computes, organised around the SOURCE vertex u so that
 // adj(u) is loaded once and reused by all of u's out-edges:
 //
-//  * light sources (1 <= d+(u) <= 32): one warp per u, adj(u) held one element per
-//    lane in registers.  All items of all edges (u, v) -- i.e. every element w of every
-//    adj(v) -- are flattened across the 32 lanes (load-balanced, each lane issues an
-//    independent coalesced load), and membership of w in adj(u) is a 5-step binary
-//    search over the lanes with shuffles.
+//  * light sources (1 <= d+(u) <= 32): one CTA per window of 512 consecutive edges.
+//    The source lists of the window are staged in shared memory; all items of all
+//    edges (u, v) -- every element w of every adj(v) -- are flattened across the CTA
+//    (load-balanced, each lane keeps 8 independent coalesced loads in flight) and w is
+//    tested against adj(u) by a <= 5-step binary search in shared memory.
 //  * heavy sources (d+(u) > 32): one CTA per (u, chunk of <= 1024 edges).  adj(u) is
 //    staged into a shared-memory open-addressing hash table (load <= 1/2), the items of
 //    a 512-edge window are split evenly across the 16 warps, and each w costs one
@@ -34,16 +34,21 @@ constexpr int kHeavyWarps = kHeavyThreads / 32;
 constexpr int kWin = 512;       // edges staged per window (== kHeavyThreads)
 constexpr int kChunk = 1024;    // edges per heavy task
 constexpr int kClasses = 4;
-constexpr uint32_t kClassMax[kClasses] = {1024, 8192, 16384, 0xffffffffu};
-constexpr int kClassLogT[kClasses] = {11, 14, 15, 0};  // 0 = sorted-array mode
+// Heavy classes by d+(u): hash-table capacity (entries) per class; 0 = sorted-array mode.
+// Tables are sized 8 d (load <= 1/8) up to the class capacity.
+constexpr uint32_t kClassMax[kClasses] = {512, 2048, 16384, 0xffffffffu};
+constexpr uint32_t kClassCap[kClasses] = {4096, 16384, 49152, 0};
 
 struct RangeDev {
-    uint64_t lo, hi;
+    uint64_t lo, hi, m;
     uint32_t u_lo, u_hi;
 };
 
-__device__ __forceinline__ uint32_t hash_slot(uint32_t w, int logT) {
-    return (w * 0x9E3779B1u) >> (32 - logT);
+constexpr int kUnroll = 8;  // independent item loads in flight per lane
+
+// Fibonacci hash, range-reduced to [0, T) with a multiply-high (any T, not only 2^k).
+__device__ __forceinline__ uint32_t hash_slot(uint32_t w, uint32_t T) {
+    return __umulhi(w * 0x9E3779B1u, T);
 }
 
 template <typename T>
@@ -60,76 +65,121 @@ __device__ __forceinline__ void block_add_total(T acc, unsigned long long *total
 }
 
 __global__ void k_range_init(const uint32_t *__restrict__ src, uint64_t lo, uint64_t hi,
-                             RangeDev *__restrict__ rg) {
+                             uint64_t m, RangeDev *__restrict__ rg) {
     rg->lo = lo;
     rg->hi = hi;
+    rg->m = m;
     rg->u_lo = hi > lo ? src[lo] : 0u;
     rg->u_hi = hi > lo ? src[hi - 1] + 1u : 0u;
 }
 
-// ------------------------------------------------------------------ light ---
+// ----------------------------------------------------------------- window ---
+// Edges whose source is light (d+(u) <= 32), in windows of kWin consecutive edges.
+// Every light source list that owns an edge of the window lies inside
+// dst[ws-31, we+31), so the window stages that slice in shared memory once; each item
+// w of each adj(v) is then tested against its source list by a <= 5-step binary
+// search in shared memory.  Items of the window are split evenly over the warps and
+// each lane keeps kUnroll independent loads in flight.
+constexpr int kStage = kWin + 2 * kLightMax;
+
 template <typename OffT>
-__global__ void __launch_bounds__(256) k_count_light(const uint32_t *__restrict__ dst,
-                                                     const OffT *__restrict__ off,
-                                                     const RangeDev *__restrict__ rg,
-                                                     unsigned long long *__restrict__ total) {
-    __shared__ OffT s_vs[8][32];
-    __shared__ uint32_t s_st[8][32];
-    const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
-    const uint64_t lo = rg->lo, hi = rg->hi;
-    const uint32_t u_lo = rg->u_lo, u_hi = rg->u_hi;
-    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-    const unsigned le = lanemask_le();
+__global__ void __launch_bounds__(kHeavyThreads)
+    k_count_window(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
+                   const OffT *__restrict__ off, const RangeDev *__restrict__ rg,
+                   unsigned *__restrict__ next, unsigned long long *__restrict__ total) {
+    __shared__ uint32_t s_stage[kStage];
+    __shared__ OffT s_eb[kWin];
+    __shared__ uint32_t s_st[kWin + 4];
+    __shared__ uint32_t s_ua[kWin];  // (list start in s_stage) | (d+(u) << 16)
+    __shared__ uint32_t s_scan[32];
+    __shared__ unsigned s_win;
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    const uint64_t lo = rg->lo, hi = rg->hi, m = rg->m;
+    const uint64_t nwin = (hi - lo + kWin - 1) / kWin;
     unsigned long long acc = 0;
-    for (uint32_t u = u_lo + gw; u < u_hi; u += nw) {
-        const OffT s = off[u], e = off[u + 1];
-        const uint32_t d = (uint32_t)(e - s);
-        if (d == 0 || d > (uint32_t)kLightMax) continue;
-        const uint64_t es = (uint64_t)s > lo ? (uint64_t)s : lo;
-        const uint64_t ee = (uint64_t)e < hi ? (uint64_t)e : hi;
-        if (es >= ee) continue;
-        const uint32_t a = lane < d ? __ldg(dst + s + lane) : kEmpty;
-        const uint64_t my_edge = (uint64_t)s + lane;
+    for (;;) {
+        if (threadIdx.x == 0) s_win = atomicAdd(next, 1u);
+        __syncthreads();
+        const uint64_t wi = s_win;
+        if (wi >= nwin) break;
+        const uint64_t ws = lo + wi * kWin;
+        const uint64_t we = ws + kWin < hi ? ws + kWin : hi;
+        const uint64_t sb = ws >= (uint64_t)(kLightMax - 1) ? ws - (kLightMax - 1) : 0;
+        const uint64_t se = we + (kLightMax - 1) < m ? we + (kLightMax - 1) : m;
+        for (uint32_t i = threadIdx.x; i < (uint32_t)(se - sb); i += kHeavyThreads)
+            s_stage[i] = __ldg(dst + sb + i);
+        uint32_t len = 0, ua = 0;
         OffT vs = 0;
-        uint32_t len = 0;
-        if (my_edge >= es && my_edge < ee) {
-            vs = __ldg(off + a);
-            len = (uint32_t)(__ldg(off + a + 1) - vs);
-        }
-        const uint32_t incl = warp_inclusive_scan<uint32_t>(len);
-        const uint32_t items = __shfl_sync(TC_FULL_MASK, incl, 31);
-        if (items == 0) continue;
-        const uint32_t st = incl - len;
-        const unsigned nonempty = __ballot_sync(TC_FULL_MASK, len > 0);
-        if (len > 0) {
-            const int r = __popc(nonempty & lanemask_lt());
-            s_vs[wib][r] = vs;
-            s_st[wib][r] = st;
-        }
-        __syncwarp();
-        int before = 0;  // nonempty edges whose items start before `base`
-        for (uint32_t base = 0; base < items; base += 32) {
-            const unsigned bit = (len > 0 && st >= base && st < base + 32) ? (1u << (st - base)) : 0u;
-            const unsigned starts = __reduce_or_sync(TC_FULL_MASK, bit);
-            const uint32_t item = base + lane;
-            uint32_t w = kEmpty;
-            const bool valid = item < items;
-            if (valid) {
-                const int k = before + __popc(starts & le) - 1;
-                w = __ldg(dst + s_vs[wib][k] + (item - s_st[wib][k]));
+        if (threadIdx.x < (uint32_t)(we - ws)) {
+            const uint64_t e = ws + threadIdx.x;
+            const uint32_t u = __ldg(src + e);
+            const OffT su = __ldg(off + u);
+            const uint32_t du = (uint32_t)(__ldg(off + u + 1) - su);
+            if (du <= (uint32_t)kLightMax) {
+                const uint32_t v = __ldg(dst + e);
+                vs = __ldg(off + v);
+                len = (uint32_t)(__ldg(off + v + 1) - vs);
+                ua = (uint32_t)((uint64_t)su - sb) | (du << 16);
             }
-            uint32_t p = 0;
+        }
+        uint32_t tot;
+        const uint32_t st = block_exclusive_scan<uint32_t>(len, s_scan, &tot);
+        if (threadIdx.x < kWin) {
+            s_eb[threadIdx.x] = vs - (OffT)st;
+            s_st[threadIdx.x] = st;
+            s_ua[threadIdx.x] = ua;
+        }
+        if (threadIdx.x == 0) s_st[kWin] = tot;
+        __syncthreads();
+        const uint32_t i0 = (uint32_t)((uint64_t)tot * warp / kHeavyWarps);
+        const uint32_t i1 = (uint32_t)((uint64_t)tot * (warp + 1) / kHeavyWarps);
+        if (i0 < i1) {
+            uint32_t k = 0;
+            {
+                const uint32_t item = i0 + lane;
+                uint32_t a = 0, b = kWin;  // largest k with s_st[k] <= item
+                while (b - a > 1) {
+                    const uint32_t mid = (a + b) >> 1;
+                    if (s_st[mid] <= item) a = mid; else b = mid;
+                }
+                k = a;
+            }
+            uint32_t nextb = s_st[k + 1];
+            OffT eb = s_eb[k];
+            uint32_t ua = s_ua[k];
+            uint32_t found = 0;
+            for (uint32_t base = i0; base < i1; base += 32 * kUnroll) {
+                uint32_t w[kUnroll], la[kUnroll];
 #pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const uint32_t x = __shfl_sync(TC_FULL_MASK, a, p + step - 1);
-                if (x < w) p += step;
+                for (int j = 0; j < kUnroll; ++j) {
+                    const uint32_t item = base + j * 32 + lane;
+                    w[j] = 0;
+                    la[j] = 0;  // empty list: never matches
+                    if (item < i1) {
+                        if (item >= nextb) {
+                            do { nextb = s_st[++k + 1]; } while (item >= nextb);
+                            eb = s_eb[k];
+                            ua = s_ua[k];
+                        }
+                        w[j] = __ldg(dst + (OffT)(eb + (OffT)item));
+                        la[j] = ua;
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < kUnroll; ++j) {
+                    uint32_t a = la[j] & 0xffffu, n = la[j] >> 16;
+                    const uint32_t end = a + n;
+                    while (n > 0) {
+                        const uint32_t half = n >> 1;
+                        if (s_stage[a + half] < w[j]) { a += half + 1; n -= half + 1; }
+                        else n = half;
+                    }
+                    found += (a < end && s_stage[a] == w[j]) ? 1u : 0u;
+                }
             }
-            const uint32_t x = __shfl_sync(TC_FULL_MASK, a, p);
-            acc += (valid && x == w && p < d) ? 1u : 0u;
-            before += __popc(starts);
+            acc += found;
         }
-        __syncwarp();
+        __syncthreads();
     }
     block_add_total(acc, total);
 }
@@ -158,15 +208,18 @@ __global__ void k_classify(const OffT *__restrict__ off, const RangeDev *__restr
 }
 
 // MODE 0: adj(u) in a shared-memory hash table; MODE 1: adj(u) as a sorted smem array.
+// Lane state caches the current edge: its item range end (nextb) and the dst index
+// base (eb = start of adj(v) - first item of v), so an item costs a compare, an add
+// and a load unless it crosses into the next edge.
 template <typename OffT, int MODE>
 __global__ void __launch_bounds__(kHeavyThreads)
     k_count_heavy(const uint32_t *__restrict__ dst, const OffT *__restrict__ off,
                   const RangeDev *__restrict__ rg, const uint2 *__restrict__ tasks,
-                  const unsigned *__restrict__ ntasks, unsigned *__restrict__ next, int log_tmax,
+                  const unsigned *__restrict__ ntasks, unsigned *__restrict__ next, uint32_t tcap,
                   unsigned long long *__restrict__ total) {
     extern __shared__ __align__(16) unsigned char smem[];
-    OffT *s_vs = reinterpret_cast<OffT *>(smem);
-    uint32_t *s_st = reinterpret_cast<uint32_t *>(s_vs + kWin);
+    OffT *s_eb = reinterpret_cast<OffT *>(smem);
+    uint32_t *s_st = reinterpret_cast<uint32_t *>(s_eb + kWin);
     uint32_t *table = s_st + kWin + 4;
     __shared__ uint32_t s_scan[32];
     __shared__ unsigned s_task;
@@ -188,22 +241,18 @@ __global__ void __launch_bounds__(kHeavyThreads)
         es += (uint64_t)task.y * kChunk;
         ee = ee < es + kChunk ? ee : es + kChunk;
 
-        int logT = 0;
-        uint32_t tmask = 0;
+        uint32_t T = 0;
         if (MODE == 0) {
-            logT = 32 - __clz(2 * d - 1);  // T = pow2 >= 2d
-            logT = logT < 6 ? 6 : (logT > log_tmax ? log_tmax : logT);
-            const uint32_t T = 1u << logT;
-            tmask = T - 1;
+            T = 8 * d < tcap ? 8 * d : tcap;
             for (uint32_t i = threadIdx.x; i < T; i += kHeavyThreads) table[i] = kEmpty;
             __syncthreads();
             for (uint32_t i = threadIdx.x; i < d; i += kHeavyThreads) {
                 const uint32_t w = __ldg(dst + s + i);
-                uint32_t h = hash_slot(w, logT);
+                uint32_t h = hash_slot(w, T);
                 for (;;) {
                     const uint32_t prev = atomicCAS(table + h, kEmpty, w);
                     if (prev == kEmpty || prev == w) break;
-                    h = (h + 1) & tmask;
+                    h = h + 1 == T ? 0 : h + 1;
                 }
             }
         } else {
@@ -223,7 +272,7 @@ __global__ void __launch_bounds__(kHeavyThreads)
             uint32_t tot;
             const uint32_t st = block_exclusive_scan<uint32_t>(len, s_scan, &tot);
             if (threadIdx.x < nwin) {
-                s_vs[threadIdx.x] = vs;
+                s_eb[threadIdx.x] = vs - (OffT)st;
                 s_st[threadIdx.x] = st;
             }
             if (threadIdx.x == 0) s_st[nwin] = tot;
@@ -231,9 +280,9 @@ __global__ void __launch_bounds__(kHeavyThreads)
             const uint32_t i0 = (uint32_t)((uint64_t)tot * warp / kHeavyWarps);
             const uint32_t i1 = (uint32_t)((uint64_t)tot * (warp + 1) / kHeavyWarps);
             if (i0 < i1) {
-                uint32_t item = i0 + lane;
                 uint32_t k = 0;
                 {
+                    const uint32_t item = i0 + lane;
                     uint32_t a = 0, b = nwin;  // largest k < nwin with s_st[k] <= item
                     while (b - a > 1) {
                         const uint32_t mid = (a + b) >> 1;
@@ -241,27 +290,44 @@ __global__ void __launch_bounds__(kHeavyThreads)
                     }
                     k = a;
                 }
+                uint32_t nextb = s_st[k + 1];
+                OffT eb = s_eb[k];
                 uint32_t found = 0;
-                for (uint32_t base = i0; base < i1; base += 32, item += 32) {
-                    if (item < i1) {
-                        while (s_st[k + 1] <= item) ++k;
-                        const uint32_t w = __ldg(dst + s_vs[k] + (item - s_st[k]));
-                        if (MODE == 0) {
-                            uint32_t h = hash_slot(w, logT);
-                            for (;;) {
-                                const uint32_t x = table[h];
-                                if (x == w) { ++found; break; }
-                                if (x == kEmpty) break;
-                                h = (h + 1) & tmask;
+                for (uint32_t base = i0; base < i1; base += 32 * kUnroll) {
+                    uint32_t w[kUnroll];
+#pragma unroll
+                    for (int j = 0; j < kUnroll; ++j) {
+                        const uint32_t it = base + j * 32 + lane;
+                        w[j] = kEmpty;
+                        if (it < i1) {
+                            if (it >= nextb) {
+                                do { nextb = s_st[++k + 1]; } while (it >= nextb);
+                                eb = s_eb[k];
                             }
+                            w[j] = __ldg(dst + (OffT)(eb + (OffT)it));
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < kUnroll; ++j) {
+                        if (MODE == 0) {
+                            uint32_t h = hash_slot(w[j], T);
+                            uint32_t x = table[h];
+                            if (x != w[j] && x != kEmpty) {
+                                do {
+                                    h = h + 1 == T ? 0 : h + 1;
+                                    x = table[h];
+                                } while (x != w[j] && x != kEmpty);
+                            }
+                            found += (x == w[j] && w[j] != kEmpty) ? 1u : 0u;
                         } else {
+                            if (w[j] == kEmpty) continue;
                             uint32_t a = 0, n = d;
                             while (n > 0) {
                                 const uint32_t half = n >> 1;
-                                if (table[a + half] < w) { a += half + 1; n -= half + 1; }
+                                if (table[a + half] < w[j]) { a += half + 1; n -= half + 1; }
                                 else n = half;
                             }
-                            found += (a < d && table[a] == w) ? 1u : 0u;
+                            found += (a < d && table[a] == w[j]) ? 1u : 0u;
                         }
                     }
                 }
@@ -350,7 +416,7 @@ __global__ void __launch_bounds__(256) k_tile_work(const uint32_t *__restrict__ 
 
 size_t heavy_smem(int cls, uint32_t max_out, bool off64) {
     size_t b = (size_t)kWin * (off64 ? 8 : 4) + (kWin + 4) * 4;
-    if (kClassLogT[cls] > 0) b += (size_t)4 << kClassLogT[cls];
+    if (kClassCap[cls] > 0) b += (size_t)4 * kClassCap[cls];
     else b += (size_t)4 * max_out;
     return b;
 }
@@ -360,11 +426,11 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
                unsigned long long *d_total, cudaStream_t s, CountStats *stats) {
     const bool off64 = sizeof(OffT) == 8;
     RangeDev *rg = nullptr;
-    unsigned *counters = nullptr;  // [0..3] ntasks per class, [4..7] queue heads
+    unsigned *counters = nullptr;  // [0..3] ntasks per class, [4..7] queue heads, [8] windows
     TC_CHECK(dalloc_t(&rg, 1, s));
-    TC_CHECK(dalloc_t(&counters, 2 * kClasses, s));
-    TC_CUDA(cudaMemsetAsync(counters, 0, 2 * kClasses * sizeof(unsigned), s));
-    k_range_init<<<1, 1, 0, s>>>(g.src, lo, hi, rg);
+    TC_CHECK(dalloc_t(&counters, 2 * kClasses + 1, s));
+    TC_CUDA(cudaMemsetAsync(counters, 0, (2 * kClasses + 1) * sizeof(unsigned), s));
+    k_range_init<<<1, 1, 0, s>>>(g.src, lo, hi, g.m, rg);
     TC_CUDA(cudaGetLastError());
 
     // Task capacity per class: every vertex in class c has > lower_c edges.
@@ -395,13 +461,13 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
             return -1;
         }
         int blocks_per_sm = 1;
-        if (kClassLogT[c] > 0) {
+        if (kClassCap[c] > 0) {
             auto kern = k_count_heavy<OffT, 0>;
             TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kHeavyThreads, sm));
             if (blocks_per_sm < 1) blocks_per_sm = 1;
             kern<<<kSMs * blocks_per_sm, kHeavyThreads, sm, s>>>(g.dst, off, rg, tasks[c], counters + c,
-                                                                counters + kClasses + c, kClassLogT[c],
+                                                                counters + kClasses + c, kClassCap[c],
                                                                 d_total);
         } else {
             auto kern = k_count_heavy<OffT, 1>;
@@ -414,7 +480,8 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
         TC_CUDA(cudaGetLastError());
     }
     TC_CUDA(cudaEventRecord(ev[2], s));
-    k_count_light<OffT><<<kSMs * 8, 256, 0, s>>>(g.dst, off, rg, d_total);
+    k_count_window<OffT><<<kSMs * 4, kHeavyThreads, 0, s>>>(g.src, g.dst, off, rg,
+                                                            counters + 2 * kClasses, d_total);
     TC_CUDA(cudaGetLastError());
     TC_CUDA(cudaEventRecord(ev[3], s));
     if (stats) {
