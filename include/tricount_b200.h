@@ -57,6 +57,11 @@ int tc_preprocess(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, int p
 /* ---- OrientedGraph transfer (graph.py:146-193) -------------------------------------- */
 int tc_graph_upload(const uint32_t *edge_src, const uint32_t *edge_dst,
                     const int64_t *node_offsets, uint64_t m, uint64_t n, tc_graph **out);
+/* Replication (multi-GPU): allocate an empty device graph, fill edge_dst and node_offsets
+ * through tc_graph_device_ptrs (e.g. an NCCL broadcast), then tc_graph_finalize rebuilds
+ * edge_src, the u32 offsets and the max out-degree on the device. */
+int tc_graph_create(uint64_t m, uint64_t n, tc_graph **out);
+int tc_graph_finalize(tc_graph *g);
 int tc_graph_download(const tc_graph *g, uint32_t *edge_src, uint32_t *edge_dst,
                       int64_t *node_offsets);
 int tc_graph_info(const tc_graph *g, uint64_t *m, uint64_t *n, uint32_t *max_out_degree);
@@ -105,6 +110,10 @@ int tc_host_register(void *p, uint64_t bytes);
 int tc_host_unregister(void *p);
 int tc_synchronize(void);
 int tc_l2_flush(void); /* write a buffer larger than L2 (timing hygiene) */
+/* CUDA events on the library stream (8 slots) and the number of kernels launched */
+int tc_timer_record(int slot);
+int tc_timer_elapsed(int slot_a, int slot_b, double *ms);
+int tc_launch_count(uint64_t *out);
 
 #ifdef __cplusplus
 }

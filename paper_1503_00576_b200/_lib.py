@@ -52,6 +52,8 @@ _SIGS = {
                        ctypes.POINTER(_graph_p), ctypes.POINTER(TcTimes)], ctypes.c_int),
     "tc_graph_upload": ([_vp, _vp, _vp, ctypes.c_uint64, ctypes.c_uint64,
                          ctypes.POINTER(_graph_p)], ctypes.c_int),
+    "tc_graph_create": ([ctypes.c_uint64, ctypes.c_uint64, ctypes.POINTER(_graph_p)], ctypes.c_int),
+    "tc_graph_finalize": ([_graph_p], ctypes.c_int),
     "tc_graph_download": ([_graph_p, _vp, _vp, _vp], ctypes.c_int),
     "tc_graph_info": ([_graph_p, _u64p, _u64p, ctypes.POINTER(ctypes.c_uint32)], ctypes.c_int),
     "tc_graph_device_ptrs": ([_graph_p, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
@@ -81,6 +83,9 @@ _SIGS = {
     "tc_host_unregister": ([_vp], ctypes.c_int),
     "tc_synchronize": ([], ctypes.c_int),
     "tc_l2_flush": ([], ctypes.c_int),
+    "tc_timer_record": ([ctypes.c_int], ctypes.c_int),
+    "tc_timer_elapsed": ([ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+    "tc_launch_count": ([_u64p], ctypes.c_int),
 }
 
 EXPORTED = tuple(_SIGS)

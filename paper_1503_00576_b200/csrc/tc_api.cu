@@ -3,6 +3,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
 #include <mutex>
 #include <string>
 
@@ -27,6 +28,10 @@ size_t g_flush_bytes = 0;
 unsigned long long *g_total = nullptr;  // device u64 accumulator for counts
 }  // namespace
 
+std::atomic<unsigned long long> g_launches{0};
+cudaEvent_t g_timer[8] = {nullptr};
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 void set_error(const std::string &msg) { g_err = msg; }
 const char *last_error() { return g_err.c_str(); }
 
@@ -248,6 +253,29 @@ int tc_graph_upload(const uint32_t *edge_src, const uint32_t *edge_dst,
     TC_CUDA(cudaStreamSynchronize(s));
     *out = g;
     return 0;
+}
+
+int tc_graph_create(uint64_t m, uint64_t n, tc_graph **out) {
+    TC_CHECK(ensure());
+    if (n >= (1ull << 32)) {
+        set_error("num_vertices must be < 2^32 on the device path");
+        return -1;
+    }
+    tc_graph *g = new tc_graph();
+    int rc = graph_alloc(&g->g, m, n, g_stream);
+    if (rc) {
+        delete g;
+        return rc;
+    }
+    TC_CUDA(cudaStreamSynchronize(g_stream));
+    *out = g;
+    return 0;
+}
+
+int tc_graph_finalize(tc_graph *g) {
+    TC_CHECK(ensure());
+    TC_CHECK(check_graph(g));
+    return finalize_graph_dev(&g->g, g_stream);
 }
 
 int tc_graph_download(const tc_graph *g, uint32_t *edge_src, uint32_t *edge_dst,
@@ -506,6 +534,35 @@ int tc_host_unregister(void *p) {
 int tc_synchronize(void) {
     TC_CHECK(ensure());
     TC_CUDA(cudaStreamSynchronize(g_stream));
+    return 0;
+}
+
+int tc_launch_count(uint64_t *out) {
+    *out = g_launches.load();
+    return 0;
+}
+
+int tc_timer_record(int slot) {
+    TC_CHECK(ensure());
+    if (slot < 0 || slot >= 8) {
+        set_error("timer slot must be in [0, 8)");
+        return -1;
+    }
+    if (!g_timer[slot]) TC_CUDA(cudaEventCreate(&g_timer[slot]));
+    TC_CUDA(cudaEventRecord(g_timer[slot], g_stream));
+    return 0;
+}
+
+int tc_timer_elapsed(int a, int b, double *ms) {
+    TC_CHECK(ensure());
+    if (a < 0 || a >= 8 || b < 0 || b >= 8 || !g_timer[a] || !g_timer[b]) {
+        set_error("timer slots not recorded");
+        return -1;
+    }
+    TC_CUDA(cudaEventSynchronize(g_timer[b]));
+    float f = 0;
+    TC_CUDA(cudaEventElapsedTime(&f, g_timer[a], g_timer[b]));
+    *ms = f;
     return 0;
 }
 

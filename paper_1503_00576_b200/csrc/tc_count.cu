@@ -431,7 +431,7 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
     TC_CHECK(dalloc_t(&counters, 2 * kClasses + 1, s));
     TC_CUDA(cudaMemsetAsync(counters, 0, (2 * kClasses + 1) * sizeof(unsigned), s));
     k_range_init<<<1, 1, 0, s>>>(g.src, lo, hi, g.m, rg);
-    TC_CUDA(cudaGetLastError());
+    TC_LAUNCHED();
 
     // Task capacity per class: every vertex in class c has > lower_c edges.
     const uint32_t lower[kClasses] = {(uint32_t)kLightMax, kClassMax[0], kClassMax[1], kClassMax[2]};
@@ -449,7 +449,7 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
     if (g.max_out > (uint32_t)kLightMax) {
         k_classify<OffT><<<grid_for(nverts, 256, kSMs * 8), 256, 0, s>>>(off, rg, tasks[0], tasks[1],
                                                                          tasks[2], tasks[3], counters);
-        TC_CUDA(cudaGetLastError());
+        TC_LAUNCHED();
     }
     TC_CUDA(cudaEventRecord(ev[1], s));
     // Heavy classes first (largest tasks first), then the light sweep.
@@ -477,12 +477,12 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
             kern<<<kSMs * blocks_per_sm, kHeavyThreads, sm, s>>>(g.dst, off, rg, tasks[c], counters + c,
                                                                 counters + kClasses + c, 0, d_total);
         }
-        TC_CUDA(cudaGetLastError());
+        TC_LAUNCHED();
     }
     TC_CUDA(cudaEventRecord(ev[2], s));
     k_count_window<OffT><<<kSMs * 4, kHeavyThreads, 0, s>>>(g.src, g.dst, off, rg,
                                                             counters + 2 * kClasses, d_total);
-    TC_CUDA(cudaGetLastError());
+    TC_LAUNCHED();
     TC_CUDA(cudaEventRecord(ev[3], s));
     if (stats) {
         TC_CUDA(cudaEventSynchronize(ev[3]));
@@ -514,7 +514,7 @@ int count_range_dev(const DeviceGraph &g, uint64_t lo, uint64_t hi, int algo,
         else
             k_count_merge_thread<int64_t><<<grid_for(span, 256, kSMs * 16), 256, 0, s>>>(
                 g.src, g.dst, g.off, lo, hi, d_total);
-        TC_CUDA(cudaGetLastError());
+        TC_LAUNCHED();
         return 0;
     }
     if (g.off32) return count_impl<uint32_t>(g, g.off32, lo, hi, d_total, s, stats);
@@ -525,7 +525,7 @@ int intersect_dev(const DeviceGraph &g, uint32_t u, uint32_t v, uint64_t *out, c
     unsigned long long *d = nullptr, h = 0;
     TC_CHECK(dalloc_t(&d, 1, s));
     k_intersect<<<1, 1, 0, s>>>(g.dst, g.off, u, v, d);
-    TC_CUDA(cudaGetLastError());
+    TC_LAUNCHED();
     TC_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));
     dfree(d, s);
@@ -544,7 +544,7 @@ int tile_sums(const DeviceGraph &g, uint64_t tile, uint32_t overhead, unsigned l
             k_tile_work<uint32_t><<<(unsigned)nt, 256, 0, s>>>(g.src, g.dst, g.off32, g.m, tile, overhead, sums);
         else
             k_tile_work<int64_t><<<(unsigned)nt, 256, 0, s>>>(g.src, g.dst, g.off, g.m, tile, overhead, sums);
-        TC_CUDA(cudaGetLastError());
+        TC_LAUNCHED();
     }
     *sums_out = sums;
     *ntiles_out = nt;

@@ -21,6 +21,15 @@ const char *last_error();
         }                                                                                \
     } while (0)
 
+// Every kernel launch site ends with TC_LAUNCHED(): counts the launch (tc_launch_count)
+// and surfaces launch errors.
+void note_launch();
+#define TC_LAUNCHED()                          \
+    do {                                       \
+        ::tc::note_launch();                   \
+        TC_CUDA(cudaGetLastError());           \
+    } while (0)
+
 #define TC_CHECK(expr)             \
     do {                           \
         int _rc = (expr);          \
@@ -92,6 +101,8 @@ void graph_release(DeviceGraph *g, cudaStream_t s);
 // node_offsets (and off32, max_out) from a grouped edge_src (reference preprocess.py:36-46).
 int build_node_array_dev(const uint32_t *firsts, uint64_t k, uint64_t n, int64_t *off,
                          uint32_t *off32, uint32_t *max_out, cudaStream_t s);
+// Rebuild edge_src, off32 and max_out from node_offsets (after a broadcast of dst + off).
+int finalize_graph_dev(DeviceGraph *g, cudaStream_t s);
 // Full reference preprocess on device-resident pairs (reference preprocess.py:74-84).
 int preprocess_dev(const uint32_t *pairs, uint64_t npairs, uint64_t n, DeviceGraph *out,
                    cudaStream_t s);

@@ -159,6 +159,24 @@ __global__ void __launch_bounds__(256) k_max_degree(const int64_t *__restrict__ 
     if (lane_id() == 0 && best) atomicMax(max_out, best);
 }
 
+// edge_src from node_offsets (rebuilding a replicated graph without shipping edge_src):
+// one warp per vertex writes its run of source ids.
+__global__ void __launch_bounds__(256) k_expand_src(const int64_t *__restrict__ off, uint64_t n,
+                                                    uint32_t *__restrict__ src,
+                                                    uint32_t *__restrict__ off32) {
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const unsigned lane = lane_id();
+    for (uint64_t u = gw; u < n; u += nw) {
+        const int64_t b = off[u], e = off[u + 1];
+        for (int64_t i = b + lane; i < e; i += 32) src[i] = (uint32_t)u;
+        if (lane == 0 && off32) {
+            off32[u] = (uint32_t)b;
+            if (u + 1 == n) off32[n] = (uint32_t)e;
+        }
+    }
+}
+
 // Pack any (u, v) pairs into (u << vb) | v keys (for sorting the unoriented pairs).
 __global__ void k_pack(const uint2 *__restrict__ pairs, uint64_t npairs, int vb,
                        uint64_t *__restrict__ keys) {
@@ -244,15 +262,36 @@ void graph_release(DeviceGraph *g, cudaStream_t s) {
     g->off32 = nullptr;
 }
 
+int finalize_graph_dev(DeviceGraph *g, cudaStream_t s) {
+    uint32_t *dmax = nullptr;
+    TC_CHECK(dalloc_t(&dmax, 1, s));
+    if (g->n) {
+        k_expand_src<<<grid_for(g->n * 32, 256, kSMs * 16), 256, 0, s>>>(g->off, g->n, g->src, g->off32);
+        TC_LAUNCHED();
+    } else if (g->off32) {
+        TC_CUDA(cudaMemsetAsync(g->off32, 0, sizeof(uint32_t), s));
+    }
+    TC_CUDA(cudaMemsetAsync(g->dst + g->m, 0, 4 * sizeof(uint32_t), s));
+    TC_CUDA(cudaMemsetAsync(dmax, 0, sizeof(uint32_t), s));
+    if (g->n) {
+        k_max_degree<<<grid_for(g->n, 256, kSMs * 8), 256, 0, s>>>(g->off, g->n, dmax);
+        TC_LAUNCHED();
+    }
+    TC_CUDA(cudaMemcpyAsync(&g->max_out, dmax, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    dfree(dmax, s);
+    return 0;
+}
+
 int build_node_array_dev(const uint32_t *firsts, uint64_t k, uint64_t n, int64_t *off,
                          uint32_t *off32, uint32_t *max_out, cudaStream_t s) {
     k_node_array<<<grid_for(k + 1, 256, kSMs * 16), 256, 0, s>>>(firsts, k, n, off, off32, max_out);
-    TC_CUDA(cudaGetLastError());
+    TC_LAUNCHED();
     if (max_out) {
         TC_CUDA(cudaMemsetAsync(max_out, 0, sizeof(uint32_t), s));
         if (n) {
             k_max_degree<<<grid_for(n, 256, kSMs * 8), 256, 0, s>>>(off, n, max_out);
-            TC_CUDA(cudaGetLastError());
+            TC_LAUNCHED();
         }
     }
     return 0;
@@ -282,7 +321,7 @@ int preprocess_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, Devic
     if (npairs) {
         k_degree_hist<<<grid_for(npairs, 256 * kPP, kSMs * 8), 256, 0, s>>>(pairs, npairs, deg, n,
                                                                             scratch);
-        TC_CUDA(cudaGetLastError());
+        TC_LAUNCHED();
     }
     // Valid (symmetric) input keeps exactly npairs/2; anything else is sized on a rerun.
     uint64_t capacity = npairs / 2 + 1;
@@ -291,7 +330,7 @@ int preprocess_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, Devic
     if (npairs) {
         k_orient<<<grid_for(npairs, 256 * kPP, kSMs * 8), 256, 0, s>>>(pairs, npairs, deg, n, vb, keys,
                                                                        capacity, cursor, plan, hist);
-        TC_CUDA(cudaGetLastError());
+        TC_LAUNCHED();
     }
     uint32_t flags[2];
     unsigned long long kept = 0;
@@ -311,7 +350,7 @@ int preprocess_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, Devic
         TC_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
         k_orient<<<grid_for(npairs, 256 * kPP, kSMs * 8), 256, 0, s>>>(pairs, npairs, deg, n, vb, keys,
                                                                        capacity, cursor, plan, hist);
-        TC_CUDA(cudaGetLastError());
+        TC_LAUNCHED();
     }
     const uint64_t m = kept;
     TC_CHECK(graph_alloc(out, m, n, s));
@@ -344,7 +383,7 @@ int sort_pairs_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, uint3
     TC_CHECK(dalloc_t(&hist, kMaxPasses * kRadix, s));
     TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
     k_pack<<<grid_for(npairs, 256, kSMs * 16), 256, 0, s>>>(pairs, npairs, vb, keys);
-    TC_CUDA(cudaGetLastError());
+    TC_LAUNCHED();
     TC_CHECK(radix_histogram(keys, npairs, plan, hist, s));
     TC_CHECK(radix_sort(keys, alt, nullptr, nullptr, npairs, plan, hist, kOutAoS, out_pairs, nullptr,
                         vb, nullptr, nullptr, s));
@@ -366,12 +405,12 @@ int orient_compact_dev(const uint32_t *pairs_u32, uint64_t npairs, const int64_t
     TC_CHECK(dalloc_t(&excl, nb, s));
     TC_CHECK(dalloc_t(&total, 1, s));
     k_orient_flags<<<(unsigned)nb, 256, 0, s>>>(pairs, npairs, deg, counts);
-    TC_CUDA(cudaGetLastError());
+    TC_LAUNCHED();
     k_scan_small<<<1, 512, 0, s>>>(counts, nb, excl, total);
-    TC_CUDA(cudaGetLastError());
+    TC_LAUNCHED();
     k_orient_scatter<<<(unsigned)nb, 256, 0, s>>>(pairs, npairs, deg, excl,
                                                   reinterpret_cast<uint2 *>(out_pairs));
-    TC_CUDA(cudaGetLastError());
+    TC_LAUNCHED();
     unsigned long long t = 0;
     TC_CUDA(cudaMemcpyAsync(&t, total, sizeof(t), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));

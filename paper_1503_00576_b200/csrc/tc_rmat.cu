@@ -268,7 +268,7 @@ int rmat_dev(int scale, int edge_factor, const double probs[4], const uint64_t s
         k_rmat_draw<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
             batch, scale, a, t_ab, t_abc, ls, (unsigned long long)(inc >> 64),
             (unsigned long long)inc, keys, idx);
-        TC_CUDA(cudaGetLastError());
+        TC_LAUNCHED();
         drawn += batch * (uint64_t)scale;
         TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
         TC_CHECK(radix_histogram(keys, batch, draw_plan, hist, s));
@@ -284,15 +284,15 @@ int rmat_dev(int scale, int edge_factor, const double probs[4], const uint64_t s
         TC_CUDA(cudaMemsetAsync(flag, 0, batch * sizeof(uint32_t), s));
         k_rmat_heads<<<grid_for(batch, 256, kSMs * 16), 256, 0, s>>>(sk, sv, batch, scale, have, have_n,
                                                                      flag, cand);
-        TC_CUDA(cudaGetLastError());
+        TC_LAUNCHED();
         dfree(sk, s);
         dfree(sv, s);
         const uint64_t nt = (batch + 4095) / 4096;
         TC_CHECK(dalloc_t(&tsum, nt, s));
         k_tile_count<<<(unsigned)nt, 256, 0, s>>>(flag, batch, tsum);
-        TC_CUDA(cudaGetLastError());
+        TC_LAUNCHED();
         k_scan_tiles<<<1, 512, 0, s>>>(tsum, nt, d_total);
-        TC_CUDA(cudaGetLastError());
+        TC_LAUNCHED();
         unsigned long long cands = 0;
         TC_CUDA(cudaMemcpyAsync(&cands, d_total, sizeof(cands), cudaMemcpyDeviceToHost, s));
         TC_CUDA(cudaStreamSynchronize(s));
@@ -303,7 +303,7 @@ int rmat_dev(int scale, int edge_factor, const double probs[4], const uint64_t s
             if (have_n)
                 TC_CUDA(cudaMemcpyAsync(merged, have, have_n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
             k_rmat_select<<<(unsigned)nt, 256, 0, s>>>(flag, cand, batch, tsum, need, merged + have_n);
-            TC_CUDA(cudaGetLastError());
+            TC_LAUNCHED();
         }
         dfree(flag, s);
         dfree(cand, s);
@@ -332,12 +332,12 @@ int rmat_dev(int scale, int edge_factor, const double probs[4], const uint64_t s
     TC_CHECK(dalloc_t(&maxhi, 1, s));
     TC_CUDA(cudaMemsetAsync(maxhi, 0, sizeof(uint32_t), s));
     k_max_hi<<<grid_for(target, 256, kSMs * 8), 256, 0, s>>>(have, target, scale, maxhi);
-    TC_CUDA(cudaGetLastError());
+    TC_LAUNCHED();
     uint64_t *both = nullptr, *balt = nullptr;
     uint32_t *pairs = nullptr;
     TC_CHECK(dalloc_t(&both, 2 * target, s));
     k_sym<<<grid_for(target, 256, kSMs * 16), 256, 0, s>>>(have, target, scale, both);
-    TC_CUDA(cudaGetLastError());
+    TC_LAUNCHED();
     dfree(have, s);
     TC_CHECK(dalloc_t(&balt, 2 * target, s));
     TC_CHECK(dalloc_t(&pairs, 4 * target + 4, s));

@@ -207,7 +207,7 @@ int launch_pass(const uint64_t *kin, uint64_t *kout, const uint32_t *vin, uint32
     uint64_t tiles = (n + kSortTile - 1) / kSortTile;
     kern<<<(unsigned)tiles, kSortThreads, sm, s>>>(kin, kout, vin, vout, a, b, split, n, pp, base,
                                                    status, counter);
-    TC_CUDA(cudaGetLastError());
+    TC_LAUNCHED();
     return 0;
 }
 
@@ -231,7 +231,7 @@ int radix_histogram(const uint64_t *keys, uint64_t n, const RadixPlan &plan, uin
     if (plan.npass == 0 || n == 0) return 0;
     unsigned grid = grid_for(n, 256 * 16, kSMs * 8);
     k_digit_hist<<<grid, 256, 0, s>>>(keys, n, plan, hist);
-    TC_CUDA(cudaGetLastError());
+    TC_LAUNCHED();
     return 0;
 }
 
@@ -246,7 +246,7 @@ int radix_sort(uint64_t *keys, uint64_t *alt, uint32_t *vals, uint32_t *valt, ui
         if (out_mode != kOutKeys) {
             k_split_copy<<<grid_for(n, 256, kSMs * 16), 256, 0, s>>>(keys, n, out_mode, out_a, out_b,
                                                                   split_bits);
-            TC_CUDA(cudaGetLastError());
+            TC_LAUNCHED();
         }
         return 0;
     }
@@ -258,7 +258,7 @@ int radix_sort(uint64_t *keys, uint64_t *alt, uint32_t *vals, uint32_t *valt, ui
     TC_CHECK(dalloc_t(&counters, kMaxPasses, s));
     TC_CUDA(cudaMemsetAsync(counters, 0, kMaxPasses * sizeof(unsigned), s));
     k_digit_base<<<1, kRadix, 0, s>>>(hist, plan.npass, base);
-    TC_CUDA(cudaGetLastError());
+    TC_LAUNCHED();
 
     const bool hv = vals != nullptr;
     uint64_t *kin = keys, *kout = alt;
