@@ -29,26 +29,175 @@ namespace {
 
 constexpr uint32_t kEmpty = 0xffffffffu;
 constexpr int kLightMax = 32;
-constexpr int kHeavyThreads = 512;
-constexpr int kHeavyWarps = kHeavyThreads / 32;
-constexpr int kWin = 512;       // edges staged per window (== kHeavyThreads)
+constexpr int kWinThreads = 256;  // window (light-source) CTA size == edges per window
 constexpr int kChunk = 1024;    // edges per heavy task
 constexpr int kClasses = 4;
-// Heavy classes by d+(u): hash-table capacity (entries) per class; 0 = sorted-array mode.
-// Tables are sized 8 d (load <= 1/8) up to the class capacity.
+// Heavy classes by d+(u): cuckoo tables of 4 d slots (load <= 1/4) up to the class
+// capacity (in slots; class 2 reaches load 1/3 at d = 16384); 0 = sorted-array mode.  Small CTAs for the
+// small classes so that many independent tasks overlap their setup phases on an SM.
 constexpr uint32_t kClassMax[kClasses] = {512, 2048, 16384, 0xffffffffu};
-constexpr uint32_t kClassCap[kClasses] = {4096, 16384, 49152, 0};
+constexpr uint32_t kClassCap[kClasses] = {2048, 8192, 49152, 0};
+constexpr int kClassThreads[kClasses] = {128, 256, 512, 512};
+constexpr uint32_t kWinSlots = 4 * kWinThreads + 256;  // window (source, w) cuckoo slots
 
 struct RangeDev {
     uint64_t lo, hi, m;
     uint32_t u_lo, u_hi;
 };
 
-constexpr int kUnroll = 8;  // independent item loads in flight per lane
+constexpr int kUnroll = 2;  // 16-byte chunks (4 items) in flight per lane per step
 
-// Fibonacci hash, range-reduced to [0, T) with a multiply-high (any T, not only 2^k).
-__device__ __forceinline__ uint32_t hash_slot(uint32_t w, uint32_t T) {
-    return __umulhi(w * 0x9E3779B1u, T);
+// ---------------------------------------------------------------- cuckoo ---
+// Both count kernels probe a shared-memory cuckoo table: every key lives in one of two
+// slots h1(key), h2(key), so a lookup is exactly two shared loads and two compares --
+// no probe loop, no divergence.  Tables are built cooperatively with atomicExch
+// (evict-and-reinsert, Alcantara et al. style); a build that exceeds the eviction bound
+// is retried with the next hash seed.  Load factor <= 1/4 makes retries rare.
+constexpr int kCuckooMaxKicks = 64;
+
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long lds64(uint32_t addr) {
+    unsigned long long v;
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ uint32_t seed_mult(uint32_t seed, int which) {
+    // odd multipliers derived from the seed (Fibonacci / murmur constants)
+    return (which ? 0x85EBCA77u : 0x9E3779B1u) + 0x632BE5A6u * seed * 2u;
+}
+
+struct Cuckoo32 {
+    uint32_t base;  // shared address of slot 0
+    uint32_t T;     // slots
+    uint32_t c1, c2;
+    __device__ __forceinline__ uint32_t h1(uint32_t k) const { return __umulhi(k * c1, T); }
+    __device__ __forceinline__ uint32_t h2(uint32_t k) const { return __umulhi(k * c2, T); }
+    __device__ __forceinline__ bool contains(uint32_t w) const {
+        const uint32_t x = lds32(base + 4 * h1(w));
+        const uint32_t y = lds32(base + 4 * h2(w));
+        return (x == w) | (y == w);
+    }
+};
+
+// Insert `key` into a 32-bit cuckoo table; returns false after too many evictions.
+__device__ __forceinline__ bool cuckoo_insert32(uint32_t *tab, const Cuckoo32 &c, uint32_t key) {
+    uint32_t h = c.h1(key);
+    for (int i = 0; i < kCuckooMaxKicks; ++i) {
+        const uint32_t old = atomicExch(tab + h, key);
+        if (old == kEmpty || old == key) return true;
+        key = old;
+        const uint32_t a = c.h1(key);
+        h = (h == a) ? c.h2(key) : a;
+    }
+    return false;  // a key is left out: the caller rebuilds with another seed
+}
+
+// (source id, w) pairs for the window kernel: 64-bit keys.
+struct Cuckoo64 {
+    uint32_t base, T, c1, c2;
+    __device__ __forceinline__ uint32_t mix(unsigned long long k, uint32_t c) const {
+        return ((uint32_t)k * c) ^ ((uint32_t)(k >> 32) * 0xC2B2AE35u);
+    }
+    __device__ __forceinline__ uint32_t h1(unsigned long long k) const { return __umulhi(mix(k, c1), T); }
+    __device__ __forceinline__ uint32_t h2(unsigned long long k) const { return __umulhi(mix(k, c2), T); }
+    __device__ __forceinline__ bool contains(unsigned long long key) const {
+        const unsigned long long x = lds64(base + 8 * h1(key));
+        const unsigned long long y = lds64(base + 8 * h2(key));
+        return (x == key) | (y == key);
+    }
+};
+
+__device__ __forceinline__ bool cuckoo_insert64(unsigned long long *tab, const Cuckoo64 &c,
+                                                unsigned long long key) {
+    uint32_t h = c.h1(key);
+    for (int i = 0; i < kCuckooMaxKicks; ++i) {
+        const unsigned long long old = atomicExch(tab + h, key);
+        if (old == ~0ull || old == key) return true;
+        key = old;
+        const uint32_t a = c.h1(key);
+        h = (h == a) ? c.h2(key) : a;
+    }
+    return false;
+}
+
+// Per-window edge table in shared memory: edge k's list adj(v) = dst[vs_k, ve_k) is read
+// as 16-byte chunks starting at the aligned a_k = vs_k & ~3; chunk j of the window
+// (cst_k <= j < cst_{k+1}) is at dst + cb_k + 4 j with cb_k = a_k - 4 cst_k.
+template <typename OffT>
+struct EdgeTable {
+    OffT *cb, *vs, *ve;
+    uint32_t *cst;  // window + 1
+    uint32_t *aux;  // per-edge probe argument (window: source id)
+};
+
+// Sweep chunks [c0, c1) of the window: every lane loads kUnroll 16-byte chunks, then
+// tests each valid item with probe(w, aux).  Returns the number of hits.
+template <typename OffT, bool HAS_AUX, typename Probe>
+__device__ __forceinline__ uint32_t sweep(const uint32_t *__restrict__ dst, const EdgeTable<OffT> &et,
+                                          uint32_t nwin, uint32_t c0, uint32_t c1, Probe probe) {
+    const unsigned lane = lane_id();
+    uint32_t k = 0;
+    {
+        const uint32_t c = c0 + lane;
+        uint32_t a = 0, b = nwin;  // largest k < nwin with cst[k] <= c
+        while (b - a > 1) {
+            const uint32_t mid = (a + b) >> 1;
+            if (et.cst[mid] <= c) a = mid; else b = mid;
+        }
+        k = a;
+    }
+    uint32_t nextb = et.cst[k + 1];
+    OffT cb = et.cb[k], lo = et.vs[k], hi = et.ve[k];
+    uint32_t aux = HAS_AUX ? et.aux[k] : 0u;
+    uint32_t found = 0;
+    for (uint32_t base = c0; base < c1; base += 32 * kUnroll) {
+        uint4 q[kUnroll];
+        OffT p[kUnroll], l[kUnroll], h[kUnroll];
+        uint32_t x[kUnroll];
+#pragma unroll
+        for (int j = 0; j < kUnroll; ++j) {
+            const uint32_t c = base + j * 32 + lane;
+            l[j] = 0;
+            h[j] = 0;
+            p[j] = 0;
+            x[j] = 0;
+            q[j] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+            if (c < c1) {
+                if (c >= nextb) {
+                    do { nextb = et.cst[++k + 1]; } while (c >= nextb);
+                    cb = et.cb[k];
+                    lo = et.vs[k];
+                    hi = et.ve[k];
+                    if (HAS_AUX) aux = et.aux[k];
+                }
+                p[j] = (OffT)(cb + (OffT)(4 * c));
+                q[j] = __ldg(reinterpret_cast<const uint4 *>(dst + p[j]));
+                l[j] = lo;
+                h[j] = hi;
+                x[j] = aux;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kUnroll; ++j) {
+            const uint32_t w4[4] = {q[j].x, q[j].y, q[j].z, q[j].w};
+            // item i is valid iff l <= p + i < h, i.e. (p + i - l) < (h - l) unsigned
+            const uint32_t rel = (uint32_t)(p[j] - l[j]), span = (uint32_t)(h[j] - l[j]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                found += ((rel + i < span) & probe(w4[i], x[j])) ? 1u : 0u;
+        }
+    }
+    return found;
 }
 
 template <typename T>
@@ -74,111 +223,91 @@ __global__ void k_range_init(const uint32_t *__restrict__ src, uint64_t lo, uint
 }
 
 // ----------------------------------------------------------------- window ---
-// Edges whose source is light (d+(u) <= 32), in windows of kWin consecutive edges.
-// Every light source list that owns an edge of the window lies inside
-// dst[ws-31, we+31), so the window stages that slice in shared memory once; each item
-// w of each adj(v) is then tested against its source list by a <= 5-step binary
-// search in shared memory.  Items of the window are split evenly over the warps and
-// each lane keeps kUnroll independent loads in flight.
-constexpr int kStage = kWin + 2 * kLightMax;
-
-template <typename OffT>
-__global__ void __launch_bounds__(kHeavyThreads)
+// Edges whose source is light (d+(u) <= 32), in windows of NT consecutive edges.
+// Every light source list that owns an edge of the window lies inside dst[ws-31, we+31);
+// those lists are inserted once per window into a shared-memory hash of (source, w)
+// pairs.  The items of the window -- every element w of every adj(v) -- are then read as
+// 16-byte chunks, split evenly over the warps, and tested with one 16-byte bucket load.
+template <typename OffT, int NT>
+__global__ void __launch_bounds__(NT)
     k_count_window(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
                    const OffT *__restrict__ off, const RangeDev *__restrict__ rg,
                    unsigned *__restrict__ next, unsigned long long *__restrict__ total) {
-    __shared__ uint32_t s_stage[kStage];
-    __shared__ OffT s_eb[kWin];
-    __shared__ uint32_t s_st[kWin + 4];
-    __shared__ uint32_t s_ua[kWin];  // (list start in s_stage) | (d+(u) << 16)
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned long long *s_tab = reinterpret_cast<unsigned long long *>(smem);  // kWinSlots
+    __shared__ OffT s_cb[NT], s_vs[NT], s_ve[NT];
+    __shared__ uint32_t s_cst[NT + 4];
+    __shared__ uint32_t s_aux[NT];
     __shared__ uint32_t s_scan[32];
-    __shared__ unsigned s_win;
-    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    __shared__ unsigned s_win, s_fail;
+    constexpr int NW = NT / 32;
+    const unsigned warp = threadIdx.x >> 5;
     const uint64_t lo = rg->lo, hi = rg->hi, m = rg->m;
-    const uint64_t nwin = (hi - lo + kWin - 1) / kWin;
+    const uint64_t nwin_total = (hi - lo + NT - 1) / NT;
+    const EdgeTable<OffT> et{s_cb, s_vs, s_ve, s_cst, s_aux};
     unsigned long long acc = 0;
     for (;;) {
         if (threadIdx.x == 0) s_win = atomicAdd(next, 1u);
         __syncthreads();
         const uint64_t wi = s_win;
-        if (wi >= nwin) break;
-        const uint64_t ws = lo + wi * kWin;
-        const uint64_t we = ws + kWin < hi ? ws + kWin : hi;
+        if (wi >= nwin_total) break;
+        const uint64_t ws = lo + wi * NT;
+        const uint64_t we = ws + NT < hi ? ws + NT : hi;
+        const uint32_t nwin = (uint32_t)(we - ws);
+        // the window's light source lists -> cuckoo table of (source, w) keys
         const uint64_t sb = ws >= (uint64_t)(kLightMax - 1) ? ws - (kLightMax - 1) : 0;
         const uint64_t se = we + (kLightMax - 1) < m ? we + (kLightMax - 1) : m;
-        for (uint32_t i = threadIdx.x; i < (uint32_t)(se - sb); i += kHeavyThreads)
-            s_stage[i] = __ldg(dst + sb + i);
-        uint32_t len = 0, ua = 0;
-        OffT vs = 0;
-        if (threadIdx.x < (uint32_t)(we - ws)) {
+        Cuckoo64 ck{smem_addr(s_tab), kWinSlots, 0, 0};
+        for (uint32_t seed = 0;; ++seed) {
+            if (seed == 32) __trap();  // cannot happen at load <= 1/4; never miscount
+            ck.c1 = seed_mult(seed, 0);
+            ck.c2 = seed_mult(seed, 1);
+            for (uint32_t i = threadIdx.x; i < kWinSlots; i += NT) s_tab[i] = ~0ull;
+            if (threadIdx.x == 0) s_fail = 0;
+            __syncthreads();
+            for (uint64_t P = sb + threadIdx.x; P < se; P += NT) {
+                const uint32_t su_u = __ldg(src + P);
+                const OffT su = __ldg(off + su_u), eu = __ldg(off + su_u + 1);
+                if (eu - su <= (OffT)kLightMax && (uint64_t)su < we && (uint64_t)eu > ws) {
+                    const unsigned long long key = ((unsigned long long)su_u << 32) | __ldg(dst + P);
+                    if (!cuckoo_insert64(s_tab, ck, key)) s_fail = 1;
+                }
+            }
+            __syncthreads();
+            const bool failed = s_fail != 0;
+            __syncthreads();
+            if (!failed) break;
+        }
+        uint32_t chunks = 0;
+        OffT vs = 0, ve = 0, a4 = 0;
+        uint32_t u = 0;
+        if (threadIdx.x < nwin) {
             const uint64_t e = ws + threadIdx.x;
-            const uint32_t u = __ldg(src + e);
+            u = __ldg(src + e);
             const OffT su = __ldg(off + u);
-            const uint32_t du = (uint32_t)(__ldg(off + u + 1) - su);
-            if (du <= (uint32_t)kLightMax) {
+            if (__ldg(off + u + 1) - su <= (OffT)kLightMax) {
                 const uint32_t v = __ldg(dst + e);
                 vs = __ldg(off + v);
-                len = (uint32_t)(__ldg(off + v + 1) - vs);
-                ua = (uint32_t)((uint64_t)su - sb) | (du << 16);
+                ve = __ldg(off + v + 1);
+                a4 = vs & ~(OffT)3;
+                chunks = ve > vs ? (uint32_t)((ve - a4 + 3) >> 2) : 0u;
             }
         }
         uint32_t tot;
-        const uint32_t st = block_exclusive_scan<uint32_t>(len, s_scan, &tot);
-        if (threadIdx.x < kWin) {
-            s_eb[threadIdx.x] = vs - (OffT)st;
-            s_st[threadIdx.x] = st;
-            s_ua[threadIdx.x] = ua;
-        }
-        if (threadIdx.x == 0) s_st[kWin] = tot;
+        const uint32_t cst = block_exclusive_scan<uint32_t>(chunks, s_scan, &tot);
+        s_cb[threadIdx.x] = a4 - (OffT)(4 * cst);
+        s_vs[threadIdx.x] = vs;
+        s_ve[threadIdx.x] = ve;
+        s_cst[threadIdx.x] = cst;
+        s_aux[threadIdx.x] = u;
+        if (threadIdx.x == 0) s_cst[NT] = tot;
         __syncthreads();
-        const uint32_t i0 = (uint32_t)((uint64_t)tot * warp / kHeavyWarps);
-        const uint32_t i1 = (uint32_t)((uint64_t)tot * (warp + 1) / kHeavyWarps);
-        if (i0 < i1) {
-            uint32_t k = 0;
-            {
-                const uint32_t item = i0 + lane;
-                uint32_t a = 0, b = kWin;  // largest k with s_st[k] <= item
-                while (b - a > 1) {
-                    const uint32_t mid = (a + b) >> 1;
-                    if (s_st[mid] <= item) a = mid; else b = mid;
-                }
-                k = a;
-            }
-            uint32_t nextb = s_st[k + 1];
-            OffT eb = s_eb[k];
-            uint32_t ua = s_ua[k];
-            uint32_t found = 0;
-            for (uint32_t base = i0; base < i1; base += 32 * kUnroll) {
-                uint32_t w[kUnroll], la[kUnroll];
-#pragma unroll
-                for (int j = 0; j < kUnroll; ++j) {
-                    const uint32_t item = base + j * 32 + lane;
-                    w[j] = 0;
-                    la[j] = 0;  // empty list: never matches
-                    if (item < i1) {
-                        if (item >= nextb) {
-                            do { nextb = s_st[++k + 1]; } while (item >= nextb);
-                            eb = s_eb[k];
-                            ua = s_ua[k];
-                        }
-                        w[j] = __ldg(dst + (OffT)(eb + (OffT)item));
-                        la[j] = ua;
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < kUnroll; ++j) {
-                    uint32_t a = la[j] & 0xffffu, n = la[j] >> 16;
-                    const uint32_t end = a + n;
-                    while (n > 0) {
-                        const uint32_t half = n >> 1;
-                        if (s_stage[a + half] < w[j]) { a += half + 1; n -= half + 1; }
-                        else n = half;
-                    }
-                    found += (a < end && s_stage[a] == w[j]) ? 1u : 0u;
-                }
-            }
-            acc += found;
-        }
+        const uint32_t c0 = (uint32_t)((uint64_t)tot * warp / NW);
+        const uint32_t c1 = (uint32_t)((uint64_t)tot * (warp + 1) / NW);
+        if (c0 < c1)
+            acc += sweep<OffT, true>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t sid) {
+                return ck.contains(((unsigned long long)sid << 32) | w);
+            });
         __syncthreads();
     }
     block_add_total(acc, total);
@@ -207,25 +336,25 @@ __global__ void k_classify(const OffT *__restrict__ off, const RangeDev *__restr
     }
 }
 
-// MODE 0: adj(u) in a shared-memory hash table; MODE 1: adj(u) as a sorted smem array.
-// Lane state caches the current edge: its item range end (nextb) and the dst index
-// base (eb = start of adj(v) - first item of v), so an item costs a compare, an add
-// and a load unless it crosses into the next edge.
-template <typename OffT, int MODE>
-__global__ void __launch_bounds__(kHeavyThreads)
+// MODE 0: adj(u) in a linear-probing hash table; MODE 1: adj(u) as a sorted smem array.
+// NT threads per CTA; windows of NT edges.
+template <typename OffT, int MODE, int NT>
+__global__ void __launch_bounds__(NT)
     k_count_heavy(const uint32_t *__restrict__ dst, const OffT *__restrict__ off,
                   const RangeDev *__restrict__ rg, const uint2 *__restrict__ tasks,
-                  const unsigned *__restrict__ ntasks, unsigned *__restrict__ next, uint32_t tcap,
+                  const unsigned *__restrict__ ntasks, unsigned *__restrict__ next, uint32_t cap,
                   unsigned long long *__restrict__ total) {
     extern __shared__ __align__(16) unsigned char smem[];
-    OffT *s_eb = reinterpret_cast<OffT *>(smem);
-    uint32_t *s_st = reinterpret_cast<uint32_t *>(s_eb + kWin);
-    uint32_t *table = s_st + kWin + 4;
+    uint32_t *table = reinterpret_cast<uint32_t *>(smem);  // cap slots (MODE 0) / d (MODE 1)
+    __shared__ OffT s_cb[NT], s_vs[NT], s_ve[NT];
+    __shared__ uint32_t s_cst[NT + 4];
     __shared__ uint32_t s_scan[32];
-    __shared__ unsigned s_task;
-    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    __shared__ unsigned s_task, s_fail;
+    constexpr int NW = NT / 32;
+    const unsigned warp = threadIdx.x >> 5;
     const uint64_t lo = rg->lo, hi = rg->hi;
     const unsigned nt = *ntasks;
+    const EdgeTable<OffT> et{s_cb, s_vs, s_ve, s_cst, nullptr};
     unsigned long long acc = 0;
     for (;;) {
         if (threadIdx.x == 0) s_task = atomicAdd(next, 1u);
@@ -241,97 +370,64 @@ __global__ void __launch_bounds__(kHeavyThreads)
         es += (uint64_t)task.y * kChunk;
         ee = ee < es + kChunk ? ee : es + kChunk;
 
-        uint32_t T = 0;
+        Cuckoo32 ck{smem_addr(table), 4 * d < cap ? 4 * d : cap, 0, 0};
         if (MODE == 0) {
-            T = 8 * d < tcap ? 8 * d : tcap;
-            for (uint32_t i = threadIdx.x; i < T; i += kHeavyThreads) table[i] = kEmpty;
-            __syncthreads();
-            for (uint32_t i = threadIdx.x; i < d; i += kHeavyThreads) {
-                const uint32_t w = __ldg(dst + s + i);
-                uint32_t h = hash_slot(w, T);
-                for (;;) {
-                    const uint32_t prev = atomicCAS(table + h, kEmpty, w);
-                    if (prev == kEmpty || prev == w) break;
-                    h = h + 1 == T ? 0 : h + 1;
-                }
+            for (uint32_t seed = 0;; ++seed) {
+                if (seed == 32) __trap();  // cannot happen at load <= 1/3; never miscount
+                ck.c1 = seed_mult(seed, 0);
+                ck.c2 = seed_mult(seed, 1);
+                for (uint32_t i = threadIdx.x; i < ck.T; i += NT) table[i] = kEmpty;
+                if (threadIdx.x == 0) s_fail = 0;
+                __syncthreads();
+                for (uint32_t i = threadIdx.x; i < d; i += NT)
+                    if (!cuckoo_insert32(table, ck, __ldg(dst + s + i))) s_fail = 1;
+                __syncthreads();
+                const bool failed = s_fail != 0;
+                __syncthreads();
+                if (!failed) break;
             }
         } else {
-            for (uint32_t i = threadIdx.x; i < d; i += kHeavyThreads) table[i] = __ldg(dst + s + i);
+            for (uint32_t i = threadIdx.x; i < d; i += NT) table[i] = __ldg(dst + s + i);
         }
-        __syncthreads();
 
-        for (uint64_t ws = es; ws < ee; ws += kWin) {
-            const uint32_t nwin = (uint32_t)(ee - ws < (uint64_t)kWin ? ee - ws : (uint64_t)kWin);
-            uint32_t len = 0;
-            OffT vs = 0;
+        for (uint64_t ws = es; ws < ee; ws += NT) {
+            const uint32_t nwin = (uint32_t)(ee - ws < (uint64_t)NT ? ee - ws : (uint64_t)NT);
+            uint32_t chunks = 0;
+            OffT vs = 0, ve = 0, a4 = 0;
             if (threadIdx.x < nwin) {
                 const uint32_t v = __ldg(dst + ws + threadIdx.x);
                 vs = __ldg(off + v);
-                len = (uint32_t)(__ldg(off + v + 1) - vs);
+                ve = __ldg(off + v + 1);
+                a4 = vs & ~(OffT)3;
+                chunks = ve > vs ? (uint32_t)((ve - a4 + 3) >> 2) : 0u;
             }
             uint32_t tot;
-            const uint32_t st = block_exclusive_scan<uint32_t>(len, s_scan, &tot);
+            const uint32_t cst = block_exclusive_scan<uint32_t>(chunks, s_scan, &tot);
             if (threadIdx.x < nwin) {
-                s_eb[threadIdx.x] = vs - (OffT)st;
-                s_st[threadIdx.x] = st;
+                s_cb[threadIdx.x] = a4 - (OffT)(4 * cst);
+                s_vs[threadIdx.x] = vs;
+                s_ve[threadIdx.x] = ve;
+                s_cst[threadIdx.x] = cst;
             }
-            if (threadIdx.x == 0) s_st[nwin] = tot;
+            if (threadIdx.x == 0) s_cst[nwin] = tot;
             __syncthreads();
-            const uint32_t i0 = (uint32_t)((uint64_t)tot * warp / kHeavyWarps);
-            const uint32_t i1 = (uint32_t)((uint64_t)tot * (warp + 1) / kHeavyWarps);
-            if (i0 < i1) {
-                uint32_t k = 0;
-                {
-                    const uint32_t item = i0 + lane;
-                    uint32_t a = 0, b = nwin;  // largest k < nwin with s_st[k] <= item
-                    while (b - a > 1) {
-                        const uint32_t mid = (a + b) >> 1;
-                        if (s_st[mid] <= item) a = mid; else b = mid;
-                    }
-                    k = a;
-                }
-                uint32_t nextb = s_st[k + 1];
-                OffT eb = s_eb[k];
-                uint32_t found = 0;
-                for (uint32_t base = i0; base < i1; base += 32 * kUnroll) {
-                    uint32_t w[kUnroll];
-#pragma unroll
-                    for (int j = 0; j < kUnroll; ++j) {
-                        const uint32_t it = base + j * 32 + lane;
-                        w[j] = kEmpty;
-                        if (it < i1) {
-                            if (it >= nextb) {
-                                do { nextb = s_st[++k + 1]; } while (it >= nextb);
-                                eb = s_eb[k];
-                            }
-                            w[j] = __ldg(dst + (OffT)(eb + (OffT)it));
+            const uint32_t c0 = (uint32_t)((uint64_t)tot * warp / NW);
+            const uint32_t c1 = (uint32_t)((uint64_t)tot * (warp + 1) / NW);
+            if (c0 < c1) {
+                if (MODE == 0) {
+                    acc += sweep<OffT, false>(dst, et, nwin, c0, c1,
+                                              [&](uint32_t w, uint32_t) { return ck.contains(w); });
+                } else {
+                    acc += sweep<OffT, false>(dst, et, nwin, c0, c1, [&](uint32_t w, uint32_t) {
+                        uint32_t a = 0, n = d;
+                        while (n > 0) {
+                            const uint32_t half = n >> 1;
+                            if (table[a + half] < w) { a += half + 1; n -= half + 1; }
+                            else n = half;
                         }
-                    }
-#pragma unroll
-                    for (int j = 0; j < kUnroll; ++j) {
-                        if (MODE == 0) {
-                            uint32_t h = hash_slot(w[j], T);
-                            uint32_t x = table[h];
-                            if (x != w[j] && x != kEmpty) {
-                                do {
-                                    h = h + 1 == T ? 0 : h + 1;
-                                    x = table[h];
-                                } while (x != w[j] && x != kEmpty);
-                            }
-                            found += (x == w[j] && w[j] != kEmpty) ? 1u : 0u;
-                        } else {
-                            if (w[j] == kEmpty) continue;
-                            uint32_t a = 0, n = d;
-                            while (n > 0) {
-                                const uint32_t half = n >> 1;
-                                if (table[a + half] < w[j]) { a += half + 1; n -= half + 1; }
-                                else n = half;
-                            }
-                            found += (a < d && table[a] == w[j]) ? 1u : 0u;
-                        }
-                    }
+                        return a < d && table[a] == w;
+                    });
                 }
-                acc += found;
             }
             __syncthreads();
         }
@@ -414,17 +510,31 @@ __global__ void __launch_bounds__(256) k_tile_work(const uint32_t *__restrict__ 
     }
 }
 
-size_t heavy_smem(int cls, uint32_t max_out, bool off64) {
-    size_t b = (size_t)kWin * (off64 ? 8 : 4) + (kWin + 4) * 4;
-    if (kClassCap[cls] > 0) b += (size_t)4 * kClassCap[cls];
-    else b += (size_t)4 * max_out;
-    return b;
+// Dynamic shared memory of a heavy class: the table for the largest d+(u) in the class.
+size_t heavy_smem(int cls, uint32_t max_out) {
+    if (kClassCap[cls] == 0) return (size_t)4 * max_out;
+    const uint32_t dmax = max_out < kClassMax[cls] ? max_out : kClassMax[cls];
+    const uint64_t slots = 4ull * dmax < kClassCap[cls] ? 4ull * dmax : kClassCap[cls];
+    return (size_t)4 * slots;
+}
+
+template <typename OffT, int MODE, int NT>
+int launch_heavy(const DeviceGraph &g, const OffT *off, const RangeDev *rg, const uint2 *tasks,
+                 const unsigned *ntasks, unsigned *next, uint32_t cap, size_t sm,
+                 unsigned long long *d_total, cudaStream_t s) {
+    auto kern = k_count_heavy<OffT, MODE, NT>;
+    TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int per_sm = 1;
+    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, sm));
+    if (per_sm < 1) per_sm = 1;
+    kern<<<kSMs * per_sm, NT, sm, s>>>(g.dst, off, rg, tasks, ntasks, next, cap, d_total);
+    TC_LAUNCHED();
+    return 0;
 }
 
 template <typename OffT>
 int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
                unsigned long long *d_total, cudaStream_t s, CountStats *stats) {
-    const bool off64 = sizeof(OffT) == 8;
     RangeDev *rg = nullptr;
     unsigned *counters = nullptr;  // [0..3] ntasks per class, [4..7] queue heads, [8] windows
     TC_CHECK(dalloc_t(&rg, 1, s));
@@ -455,33 +565,30 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
     // Heavy classes first (largest tasks first), then the light sweep.
     for (int c = kClasses - 1; c >= 0; --c) {
         if (g.max_out <= lower[c]) continue;
-        const size_t sm = heavy_smem(c, g.max_out, off64);
-        if (sm > 227 * 1024) {
+        const size_t sm = heavy_smem(c, g.max_out);
+        if (sm > 200 * 1024) {
             set_error("max out-degree too large for the shared-memory staging path");
             return -1;
         }
-        int blocks_per_sm = 1;
-        if (kClassCap[c] > 0) {
-            auto kern = k_count_heavy<OffT, 0>;
-            TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kHeavyThreads, sm));
-            if (blocks_per_sm < 1) blocks_per_sm = 1;
-            kern<<<kSMs * blocks_per_sm, kHeavyThreads, sm, s>>>(g.dst, off, rg, tasks[c], counters + c,
-                                                                counters + kClasses + c, kClassCap[c],
-                                                                d_total);
-        } else {
-            auto kern = k_count_heavy<OffT, 1>;
-            TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kHeavyThreads, sm));
-            if (blocks_per_sm < 1) blocks_per_sm = 1;
-            kern<<<kSMs * blocks_per_sm, kHeavyThreads, sm, s>>>(g.dst, off, rg, tasks[c], counters + c,
-                                                                counters + kClasses + c, 0, d_total);
-        }
-        TC_LAUNCHED();
+        const unsigned *nt_c = counters + c;
+        unsigned *next_c = counters + kClasses + c;
+        int rc = 0;
+        if (c == 0) rc = launch_heavy<OffT, 0, 128>(g, off, rg, tasks[c], nt_c, next_c, kClassCap[c], sm, d_total, s);
+        else if (c == 1) rc = launch_heavy<OffT, 0, 256>(g, off, rg, tasks[c], nt_c, next_c, kClassCap[c], sm, d_total, s);
+        else if (c == 2) rc = launch_heavy<OffT, 0, 512>(g, off, rg, tasks[c], nt_c, next_c, kClassCap[c], sm, d_total, s);
+        else rc = launch_heavy<OffT, 1, 512>(g, off, rg, tasks[c], nt_c, next_c, 0, sm, d_total, s);
+        if (rc) return rc;
     }
     TC_CUDA(cudaEventRecord(ev[2], s));
-    k_count_window<OffT><<<kSMs * 4, kHeavyThreads, 0, s>>>(g.src, g.dst, off, rg,
-                                                            counters + 2 * kClasses, d_total);
+    {
+        auto kern = k_count_window<OffT, kWinThreads>;
+        const int sm = kWinSlots * 8;
+        TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        int per_sm = 1;
+        TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWinThreads, sm));
+        kern<<<kSMs * (per_sm > 0 ? per_sm : 1), kWinThreads, sm, s>>>(g.src, g.dst, off, rg,
+                                                                     counters + 2 * kClasses, d_total);
+    }
     TC_LAUNCHED();
     TC_CUDA(cudaEventRecord(ev[3], s));
     if (stats) {
