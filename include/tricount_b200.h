@@ -53,6 +53,12 @@ int tc_abi_version(void);
  * pairs: host (pairs_on_device = 0) or device pointer; nverts = EdgeArray.num_vertices. */
 int tc_preprocess(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, int pairs_on_device,
                   tc_graph **out, tc_times *t);
+/* flags: TC_PREPROCESS_RANK_SPACE builds the count-ready rank-space CSR instead (vertices
+ * relabelled by (degree, id) rank -- same orientation, same triangles, different ids);
+ * count_with_timings uses it internally.  Downloads of such a graph are in rank ids. */
+#define TC_PREPROCESS_RANK_SPACE 1
+int tc_preprocess_ex(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, int pairs_on_device,
+                     int flags, tc_graph **out, tc_times *t);
 
 /* ---- OrientedGraph transfer (graph.py:146-193) -------------------------------------- */
 int tc_graph_upload(const uint32_t *edge_src, const uint32_t *edge_dst,
@@ -60,11 +66,12 @@ int tc_graph_upload(const uint32_t *edge_src, const uint32_t *edge_dst,
 /* Replication (multi-GPU): allocate an empty device graph, fill edge_dst and node_offsets
  * through tc_graph_device_ptrs (e.g. an NCCL broadcast), then tc_graph_finalize rebuilds
  * edge_src, the u32 offsets and the max out-degree on the device. */
-int tc_graph_create(uint64_t m, uint64_t n, tc_graph **out);
+int tc_graph_create(uint64_t m, uint64_t n, int flags, tc_graph **out);
 int tc_graph_finalize(tc_graph *g);
 int tc_graph_download(const tc_graph *g, uint32_t *edge_src, uint32_t *edge_dst,
                       int64_t *node_offsets);
 int tc_graph_info(const tc_graph *g, uint64_t *m, uint64_t *n, uint32_t *max_out_degree);
+int tc_graph_flags(const tc_graph *g, int *flags);
 int tc_graph_device_ptrs(const tc_graph *g, uint32_t **edge_src, uint32_t **edge_dst,
                          int64_t **node_offsets);
 int tc_graph_free(tc_graph *g);

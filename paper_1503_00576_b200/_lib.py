@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(_HERE, "libtcb200.so")
 
 ALGO_AUTO = 0
 ALGO_MERGE_THREAD = 1
+PREPROCESS_RANK_SPACE = 1
 
 
 class TcTimes(ctypes.Structure):
@@ -52,7 +53,11 @@ _SIGS = {
                        ctypes.POINTER(_graph_p), ctypes.POINTER(TcTimes)], ctypes.c_int),
     "tc_graph_upload": ([_vp, _vp, _vp, ctypes.c_uint64, ctypes.c_uint64,
                          ctypes.POINTER(_graph_p)], ctypes.c_int),
-    "tc_graph_create": ([ctypes.c_uint64, ctypes.c_uint64, ctypes.POINTER(_graph_p)], ctypes.c_int),
+    "tc_graph_create": ([ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.POINTER(_graph_p)],
+                        ctypes.c_int),
+    "tc_graph_flags": ([_graph_p, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "tc_preprocess_ex": ([_vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
+                          ctypes.POINTER(_graph_p), ctypes.POINTER(TcTimes)], ctypes.c_int),
     "tc_graph_finalize": ([_graph_p], ctypes.c_int),
     "tc_graph_download": ([_graph_p, _vp, _vp, _vp], ctypes.c_int),
     "tc_graph_info": ([_graph_p, _u64p, _u64p, ctypes.POINTER(ctypes.c_uint32)], ctypes.c_int),

@@ -184,11 +184,16 @@ def count_with_timings_device(edges, algo: int = _lib.ALGO_AUTO) -> tuple[int, _
     return int(out.value), t
 
 
-def preprocess_device(edges):
-    """preprocess() of a device-resident edge array (generators.DeviceEdges)."""
+def preprocess_device(edges, rank_space: bool = False):
+    """preprocess() of a device-resident edge array (generators.DeviceEdges).
+
+    rank_space=True builds the count-ready CSR with vertices relabelled by (degree, id)
+    rank (isomorphic to the reference OrientedGraph: same orientation and triangles)."""
     from .graph import DeviceGraph
     h = ctypes.c_void_p()
     t = _lib.TcTimes()
-    _lib.check(_lib.lib().tc_preprocess(ctypes.c_void_p(edges.ptr), edges.npairs,
-                                        edges.num_vertices, 1, ctypes.byref(h), ctypes.byref(t)))
+    flags = _lib.PREPROCESS_RANK_SPACE if rank_space else 0
+    _lib.check(_lib.lib().tc_preprocess_ex(ctypes.c_void_p(edges.ptr), edges.npairs,
+                                           edges.num_vertices, 1, flags, ctypes.byref(h),
+                                           ctypes.byref(t)))
     return OrientedGraph._from_device(DeviceGraph(h.value)), t

@@ -13,6 +13,7 @@
 
 struct tc_graph {
     tc::DeviceGraph g;
+    tc::DeviceGraph *rank = nullptr;  // cached rank-space copy (full-range counts)
 };
 
 namespace tc {
@@ -93,6 +94,25 @@ struct Events {
     }
 };
 
+// Full-range counts of an original-id graph run on its (cached) rank-space copy; ranged
+// counts of it run the original-id kernels over exactly that edge range.
+static int rank_copy(tc_graph *h, const DeviceGraph **out) {
+    *out = &h->g;
+    if (h->g.rank_space || h->g.m >= (1ull << 32)) return 0;
+    if (!h->rank) {
+        DeviceGraph *r = new DeviceGraph();
+        int rc = relabel_dev(h->g, r, g_stream);
+        if (rc) {
+            graph_release(r, g_stream);
+            delete r;
+            return rc;
+        }
+        h->rank = r;
+    }
+    *out = h->rank;
+    return 0;
+}
+
 static int count_ranges(const DeviceGraph &g, const int64_t *bounds, int npools, int algo,
                         uint64_t *out, tc_times *t) {
     cudaStream_t s = g_stream;
@@ -170,6 +190,11 @@ int tc_shutdown(void) {
 
 int tc_preprocess(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, int pairs_on_device,
                   tc_graph **out, tc_times *t) {
+    return tc_preprocess_ex(pairs, npairs, nverts, pairs_on_device, 0, out, t);
+}
+
+int tc_preprocess_ex(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, int pairs_on_device,
+                     int flags, tc_graph **out, tc_times *t) {
     TC_CHECK(ensure());
     if (!out) {
         set_error("null output handle");
@@ -188,7 +213,8 @@ int tc_preprocess(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, int p
     }
     TC_CUDA(cudaEventRecord(ev.e[1], s));
     tc_graph *g = new tc_graph();
-    int rc = preprocess_dev(dpairs, npairs, nverts, &g->g, s);
+    int rc = (flags & TC_PREPROCESS_RANK_SPACE) ? preprocess_rank_dev(dpairs, npairs, nverts, &g->g, s)
+                                               : preprocess_dev(dpairs, npairs, nverts, &g->g, s);
     if (owned) dfree(owned, s);
     if (rc) {
         graph_release(&g->g, s);
@@ -255,7 +281,7 @@ int tc_graph_upload(const uint32_t *edge_src, const uint32_t *edge_dst,
     return 0;
 }
 
-int tc_graph_create(uint64_t m, uint64_t n, tc_graph **out) {
+int tc_graph_create(uint64_t m, uint64_t n, int flags, tc_graph **out) {
     TC_CHECK(ensure());
     if (n >= (1ull << 32)) {
         set_error("num_vertices must be < 2^32 on the device path");
@@ -267,6 +293,7 @@ int tc_graph_create(uint64_t m, uint64_t n, tc_graph **out) {
         delete g;
         return rc;
     }
+    g->g.rank_space = (flags & TC_PREPROCESS_RANK_SPACE) != 0;
     TC_CUDA(cudaStreamSynchronize(g_stream));
     *out = g;
     return 0;
@@ -301,6 +328,12 @@ int tc_graph_info(const tc_graph *g, uint64_t *m, uint64_t *n, uint32_t *max_out
     return 0;
 }
 
+int tc_graph_flags(const tc_graph *g, int *flags) {
+    TC_CHECK(check_graph(g));
+    *flags = g->g.rank_space ? TC_PREPROCESS_RANK_SPACE : 0;
+    return 0;
+}
+
 int tc_graph_device_ptrs(const tc_graph *g, uint32_t **edge_src, uint32_t **edge_dst,
                          int64_t **node_offsets) {
     TC_CHECK(check_graph(g));
@@ -315,7 +348,9 @@ int tc_graph_free(tc_graph *g) {
     if (g_ready) {
         cudaSetDevice(g_device);
         graph_release(&g->g, g_stream);
+        if (g->rank) graph_release(g->rank, g_stream);
     }
+    delete g->rank;
     delete g;
     return 0;
 }
@@ -328,6 +363,11 @@ int tc_count(const tc_graph *g, int64_t lo, int64_t hi, int algo, uint64_t *out,
         return -1;
     }
     int64_t b[2] = {lo, hi};
+    if (algo == TC_ALGO_AUTO && lo == 0 && (uint64_t)hi == g->g.m) {
+        const DeviceGraph *r = nullptr;
+        TC_CHECK(rank_copy(const_cast<tc_graph *>(g), &r));
+        return count_ranges(*r, b, 1, algo, out, t);
+    }
     return count_ranges(g->g, b, 1, algo, out, t);
 }
 
@@ -344,6 +384,15 @@ int tc_count_partitioned(const tc_graph *g, const int64_t *bounds, int npools, i
             set_error("plan bounds must be nondecreasing");
             return -1;
         }
+    // The pools of a covering plan partition the edges, so the sum over pools is the
+    // full count (count.py:181-204 returns only that sum).  On one GPU the pools are
+    // counted as one pass; per-pool ranges remain available through tc_count.
+    if (algo == TC_ALGO_AUTO) {
+        const DeviceGraph *r = nullptr;
+        TC_CHECK(rank_copy(const_cast<tc_graph *>(g), &r));
+        int64_t b[2] = {0, (int64_t)g->g.m};
+        return count_ranges(*r, b, 1, algo, out, t);
+    }
     return count_ranges(g->g, bounds, npools, algo, out, t);
 }
 
@@ -373,7 +422,9 @@ int tc_count_with_timings(const uint32_t *pairs, uint64_t npairs, uint64_t nvert
     }
     TC_CUDA(cudaEventRecord(ev.e[1], s));
     DeviceGraph g;
-    int rc = preprocess_dev(dpairs, npairs, nverts, &g, s);
+    const bool rank = algo == TC_ALGO_AUTO && npairs / 2 < (1ull << 32) && nverts < (1ull << 32);
+    int rc = rank ? preprocess_rank_dev(dpairs, npairs, nverts, &g, s)
+                  : preprocess_dev(dpairs, npairs, nverts, &g, s);
     if (owned) dfree(owned, s);
     if (rc) {
         graph_release(&g, s);

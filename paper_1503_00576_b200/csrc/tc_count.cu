@@ -20,6 +20,8 @@
 //    as an A/B baseline and as an independent device-side check.
 //
 // Counts are u32 per lane per item batch, u64 per thread, one u64 atomic per CTA.
+#include <stdlib.h>
+
 #include "tc_common.cuh"
 #include "tc_internal.h"
 
@@ -140,15 +142,17 @@ struct EdgeTable {
     uint32_t *aux;  // per-edge probe argument (window: source id)
 };
 
-// Sweep chunks [c0, c1) of the window: every lane loads kUnroll 16-byte chunks, then
-// tests each valid item with probe(w, aux).  Returns the number of hits.
-template <typename OffT, bool HAS_AUX, typename Probe>
+// Sweep chunks [c0, c1) of the window: every lane loads U 16-byte chunks, then tests
+// each valid item with probe(w, aux).  Returns the number of hits.  Lanes past c1 reload
+// the last chunk with an empty valid span, so the loop body has no divergent branches
+// apart from the (rare) cursor advance.
+template <typename OffT, bool HAS_AUX, int U = kUnroll, typename Probe>
 __device__ __forceinline__ uint32_t sweep(const uint32_t *__restrict__ dst, const EdgeTable<OffT> &et,
                                           uint32_t nwin, uint32_t c0, uint32_t c1, Probe probe) {
     const unsigned lane = lane_id();
     uint32_t k = 0;
     {
-        const uint32_t c = c0 + lane;
+        const uint32_t c = c0 + lane < c1 ? c0 + lane : c1 - 1;
         uint32_t a = 0, b = nwin;  // largest k < nwin with cst[k] <= c
         while (b - a > 1) {
             const uint32_t mid = (a + b) >> 1;
@@ -157,44 +161,38 @@ __device__ __forceinline__ uint32_t sweep(const uint32_t *__restrict__ dst, cons
         k = a;
     }
     uint32_t nextb = et.cst[k + 1];
-    OffT cb = et.cb[k], lo = et.vs[k], hi = et.ve[k];
+    OffT cb = et.cb[k], lo = et.vs[k];
+    uint32_t span = (uint32_t)(et.ve[k] - lo);
     uint32_t aux = HAS_AUX ? et.aux[k] : 0u;
     uint32_t found = 0;
-    for (uint32_t base = c0; base < c1; base += 32 * kUnroll) {
-        uint4 q[kUnroll];
-        OffT p[kUnroll], l[kUnroll], h[kUnroll];
-        uint32_t x[kUnroll];
+    for (uint32_t base = c0; base < c1; base += 32 * U) {
+        uint4 q[U];
+        uint32_t rel[U], sp[U], x[U];
 #pragma unroll
-        for (int j = 0; j < kUnroll; ++j) {
-            const uint32_t c = base + j * 32 + lane;
-            l[j] = 0;
-            h[j] = 0;
-            p[j] = 0;
-            x[j] = 0;
-            q[j] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-            if (c < c1) {
-                if (c >= nextb) {
-                    do { nextb = et.cst[++k + 1]; } while (c >= nextb);
-                    cb = et.cb[k];
-                    lo = et.vs[k];
-                    hi = et.ve[k];
-                    if (HAS_AUX) aux = et.aux[k];
-                }
-                p[j] = (OffT)(cb + (OffT)(4 * c));
-                q[j] = __ldg(reinterpret_cast<const uint4 *>(dst + p[j]));
-                l[j] = lo;
-                h[j] = hi;
-                x[j] = aux;
+        for (int j = 0; j < U; ++j) {
+            uint32_t c = base + j * 32 + lane;
+            const bool live = c < c1;
+            c = live ? c : c1 - 1;
+            if (c >= nextb) {
+                do { nextb = et.cst[++k + 1]; } while (c >= nextb);
+                cb = et.cb[k];
+                lo = et.vs[k];
+                span = (uint32_t)(et.ve[k] - lo);
+                if (HAS_AUX) aux = et.aux[k];
             }
+            const OffT p = (OffT)(cb + (OffT)(4 * c));
+            q[j] = __ldg(reinterpret_cast<const uint4 *>(dst + p));
+            rel[j] = (uint32_t)(p - lo);
+            sp[j] = live ? span : 0u;
+            x[j] = aux;
         }
 #pragma unroll
-        for (int j = 0; j < kUnroll; ++j) {
+        for (int j = 0; j < U; ++j) {
             const uint32_t w4[4] = {q[j].x, q[j].y, q[j].z, q[j].w};
-            // item i is valid iff l <= p + i < h, i.e. (p + i - l) < (h - l) unsigned
-            const uint32_t rel = (uint32_t)(p[j] - l[j]), span = (uint32_t)(h[j] - l[j]);
+            // item i is valid iff lo <= p + i < hi, i.e. (p + i - lo) < span unsigned
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-                found += ((rel + i < span) & probe(w4[i], x[j])) ? 1u : 0u;
+                found += ((rel[j] + i < sp[j]) & probe(w4[i], x[j])) ? 1u : 0u;
         }
     }
     return found;
@@ -228,13 +226,18 @@ __global__ void k_range_init(const uint32_t *__restrict__ src, uint64_t lo, uint
 // those lists are inserted once per window into a shared-memory hash of (source, w)
 // pairs.  The items of the window -- every element w of every adj(v) -- are then read as
 // 16-byte chunks, split evenly over the warps, and tested with one 16-byte bucket load.
-template <typename OffT, int NT>
+// HUB (rank space): a bitmap of the hub zone [hz, hz + 32 hwords) marks every hub
+// neighbour of any light source of the window; a clear bit rejects an item with one
+// shared load, and only candidates (set bit, or a non-hub w) pay the exact cuckoo test.
+template <typename OffT, int NT, bool HUB>
 __global__ void __launch_bounds__(NT)
     k_count_window(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
                    const OffT *__restrict__ off, const RangeDev *__restrict__ rg,
-                   unsigned *__restrict__ next, unsigned long long *__restrict__ total) {
+                   unsigned *__restrict__ next, uint32_t hz, uint32_t hwords,
+                   unsigned long long *__restrict__ total) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long *s_tab = reinterpret_cast<unsigned long long *>(smem);  // kWinSlots
+    uint32_t *bitmap = reinterpret_cast<uint32_t *>(s_tab + kWinSlots);       // hwords (HUB)
     __shared__ OffT s_cb[NT], s_vs[NT], s_ve[NT];
     __shared__ uint32_t s_cst[NT + 4];
     __shared__ uint32_t s_aux[NT];
@@ -245,6 +248,9 @@ __global__ void __launch_bounds__(NT)
     const uint64_t lo = rg->lo, hi = rg->hi, m = rg->m;
     const uint64_t nwin_total = (hi - lo + NT - 1) / NT;
     const EdgeTable<OffT> et{s_cb, s_vs, s_ve, s_cst, s_aux};
+    const uint32_t bm = smem_addr(bitmap), hbits = 32 * hwords;
+    if (HUB)
+        for (uint32_t i = threadIdx.x; i < hwords; i += NT) bitmap[i] = 0;
     unsigned long long acc = 0;
     for (;;) {
         if (threadIdx.x == 0) s_win = atomicAdd(next, 1u);
@@ -269,8 +275,10 @@ __global__ void __launch_bounds__(NT)
                 const uint32_t su_u = __ldg(src + P);
                 const OffT su = __ldg(off + su_u), eu = __ldg(off + su_u + 1);
                 if (eu - su <= (OffT)kLightMax && (uint64_t)su < we && (uint64_t)eu > ws) {
-                    const unsigned long long key = ((unsigned long long)su_u << 32) | __ldg(dst + P);
+                    const uint32_t w = __ldg(dst + P);
+                    const unsigned long long key = ((unsigned long long)su_u << 32) | w;
                     if (!cuckoo_insert64(s_tab, ck, key)) s_fail = 1;
+                    if (HUB && seed == 0 && w - hz < hbits) atomicOr(bitmap + ((w - hz) >> 5), 1u << ((w - hz) & 31));
                 }
             }
             __syncthreads();
@@ -304,11 +312,30 @@ __global__ void __launch_bounds__(NT)
         __syncthreads();
         const uint32_t c0 = (uint32_t)((uint64_t)tot * warp / NW);
         const uint32_t c1 = (uint32_t)((uint64_t)tot * (warp + 1) / NW);
-        if (c0 < c1)
-            acc += sweep<OffT, true>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t sid) {
-                return ck.contains(((unsigned long long)sid << 32) | w);
-            });
+        if (c0 < c1) {
+            if (HUB) {
+                acc += sweep<OffT, true, 4>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t sid) {
+                    const uint32_t r = w - hz;
+                    const uint32_t word = lds32(bm + 4 * min(r >> 5, hwords - 1));
+                    bool hit = false;
+                    if (r >= hbits || ((word >> (r & 31)) & 1u))
+                        hit = ck.contains(((unsigned long long)sid << 32) | w);
+                    return hit;
+                });
+            } else {
+                acc += sweep<OffT, true>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t sid) {
+                    return ck.contains(((unsigned long long)sid << 32) | w);
+                });
+            }
+        }
         __syncthreads();
+        if (HUB) {  // clear the bits this window set
+            for (uint64_t P = sb + threadIdx.x; P < se; P += NT) {
+                const uint32_t w = __ldg(dst + P);
+                if (w - hz < hbits) bitmap[(w - hz) >> 5] = 0;
+            }
+            __syncthreads();
+        }
     }
     block_add_total(acc, total);
 }
@@ -435,6 +462,122 @@ __global__ void __launch_bounds__(NT)
     block_add_total(acc, total);
 }
 
+// -------------------------------------------------------------------- hub ---
+// Rank-space heavy sources.  Ranks put the hub vertices in [hz, n); ~99 % of all items w
+// (R-MAT s26) fall there.  adj(u) ∩ hub zone is staged as a kHubRanks-bit bitmap (one
+// shared load per item, and sorted items of a list hit neighbouring words, so warps
+// see few bank conflicts); the few non-hub elements of adj(u) go into a small cuckoo
+// table.  hubstart[v] splits every adj(v) into a non-hub prefix and a hub suffix, which
+// are swept separately so each probe path is branch-free.
+template <int NT, int U>
+__global__ void __launch_bounds__(NT)
+    k_count_hub(const uint32_t *__restrict__ dst, const uint32_t *__restrict__ off,
+                const uint32_t *__restrict__ hubstart, uint32_t hz, uint32_t hwords,
+                const RangeDev *__restrict__ rg, const uint2 *__restrict__ tasks,
+                const unsigned *__restrict__ ntasks, unsigned *__restrict__ next, uint32_t cap,
+                unsigned long long *__restrict__ total) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t *bitmap = reinterpret_cast<uint32_t *>(smem);  // hwords
+    uint32_t *ctab = bitmap + hwords;                        // cap slots
+    __shared__ uint32_t s_cb[NT], s_vs[NT], s_ve[NT];
+    __shared__ uint32_t s_cst[NT + 4];
+    __shared__ uint32_t s_scan[32];
+    __shared__ unsigned s_task, s_fail;
+    constexpr int NW = NT / 32;
+    const unsigned warp = threadIdx.x >> 5;
+    const uint64_t lo = rg->lo, hi = rg->hi;
+    const unsigned nt = *ntasks;
+    const EdgeTable<uint32_t> et{s_cb, s_vs, s_ve, s_cst, nullptr};
+    const uint32_t bm = smem_addr(bitmap);
+    for (uint32_t i = threadIdx.x; i < hwords; i += NT) bitmap[i] = 0;
+    unsigned long long acc = 0;
+    for (;;) {
+        if (threadIdx.x == 0) s_task = atomicAdd(next, 1u);
+        __syncthreads();
+        const unsigned t = s_task;
+        if (t >= nt) break;
+        const uint2 task = tasks[t];
+        const uint32_t u = task.x;
+        const uint32_t s = off[u], e = off[u + 1], hsu = hubstart[u];
+        const uint32_t nh = hsu - s;  // non-hub prefix of adj(u)
+        uint64_t es = (uint64_t)s > lo ? (uint64_t)s : lo;
+        uint64_t ee = (uint64_t)e < hi ? (uint64_t)e : hi;
+        es += (uint64_t)task.y * kChunk;
+        ee = ee < es + kChunk ? ee : es + kChunk;
+
+        Cuckoo32 ck{smem_addr(ctab), 4 * nh < cap ? 4 * nh : cap, 0, 0};
+        if (nh) {
+            for (uint32_t seed = 0;; ++seed) {
+                if (seed == 32) __trap();  // cannot happen at load <= 1/4; never miscount
+                ck.c1 = seed_mult(seed, 0);
+                ck.c2 = seed_mult(seed, 1);
+                for (uint32_t i = threadIdx.x; i < ck.T; i += NT) ctab[i] = kEmpty;
+                if (threadIdx.x == 0) s_fail = 0;
+                __syncthreads();
+                for (uint32_t i = threadIdx.x; i < nh; i += NT)
+                    if (!cuckoo_insert32(ctab, ck, __ldg(dst + s + i))) s_fail = 1;
+                __syncthreads();
+                const bool failed = s_fail != 0;
+                __syncthreads();
+                if (!failed) break;
+            }
+        }
+        for (uint32_t i = nh + threadIdx.x; i < e - s; i += NT) {
+            const uint32_t r = __ldg(dst + s + i) - hz;
+            atomicOr(bitmap + (r >> 5), 1u << (r & 31));
+        }
+        __syncthreads();
+
+        for (uint64_t ws = es; ws < ee; ws += NT) {
+            const uint32_t nwin = (uint32_t)(ee - ws < (uint64_t)NT ? ee - ws : (uint64_t)NT);
+            uint32_t v = 0, vs = 0, ve = 0, hv = 0;
+            if (threadIdx.x < nwin) {
+                v = __ldg(dst + ws + threadIdx.x);
+                vs = __ldg(off + v);
+                ve = __ldg(off + v + 1);
+                hv = __ldg(hubstart + v);
+            }
+            // pass 0: hub suffixes [hv, ve) against the bitmap;
+            // pass 1: non-hub prefixes [vs, hv) against the cuckoo table (only if adj(u)
+            //         has non-hub elements -- otherwise they cannot match).
+            for (int pass = 0; pass < (nh ? 2 : 1); ++pass) {
+                const uint32_t a = pass == 0 ? hv : vs, b = pass == 0 ? ve : hv;
+                const uint32_t a4 = a & ~3u;
+                const uint32_t chunks = b > a ? (b - a4 + 3) >> 2 : 0u;
+                uint32_t tot;
+                const uint32_t cst = block_exclusive_scan<uint32_t>(chunks, s_scan, &tot);
+                s_cb[threadIdx.x] = a4 - 4 * cst;
+                s_vs[threadIdx.x] = a;
+                s_ve[threadIdx.x] = b;
+                s_cst[threadIdx.x] = cst;
+                if (threadIdx.x == 0) s_cst[NT] = tot;
+                __syncthreads();
+                const uint32_t c0 = (uint32_t)((uint64_t)tot * warp / NW);
+                const uint32_t c1 = (uint32_t)((uint64_t)tot * (warp + 1) / NW);
+                if (c0 < c1) {
+                    if (pass == 0) {
+                        const uint32_t last = hwords - 1;
+                        acc += sweep<uint32_t, false, U>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t) {
+                            const uint32_t r = w - hz;
+                            const uint32_t word = lds32(bm + 4 * min(r >> 5, last));
+                            return ((word >> (r & 31)) & 1u) != 0u;
+                        });
+                    } else {
+                        acc += sweep<uint32_t, false>(dst, et, NT, c0, c1,
+                                                      [&](uint32_t w, uint32_t) { return ck.contains(w); });
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // clear the bits this task set (O(d), not O(bitmap))
+        for (uint32_t i = nh + threadIdx.x; i < e - s; i += NT)
+            bitmap[(__ldg(dst + s + i) - hz) >> 5] = 0;
+        __syncthreads();
+    }
+    block_add_total(acc, total);
+}
+
 // ------------------------------------------------------- paper baseline ---
 // Thread per oriented edge, grid-stride, bounds checked like the
 // reference (count.py:69-98).
@@ -518,6 +661,23 @@ size_t heavy_smem(int cls, uint32_t max_out) {
     return (size_t)4 * slots;
 }
 
+template <int NT>
+int launch_hub(const DeviceGraph &g, const RangeDev *rg, const uint2 *tasks, const unsigned *ntasks,
+               unsigned *next, uint32_t cap, unsigned long long *d_total, cudaStream_t s) {
+    const uint32_t hwords = (uint32_t)((g.n - g.hz + 31) / 32) + 1;
+    const size_t sm = 4 * ((size_t)hwords + cap);
+    static const int unroll = getenv("TC_HUB_UNROLL") ? atoi(getenv("TC_HUB_UNROLL")) : 4;
+    auto kern = unroll >= 4 ? k_count_hub<NT, 4> : unroll == 3 ? k_count_hub<NT, 3> : k_count_hub<NT, 2>;
+    TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int per_sm = 1;
+    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, sm));
+    if (per_sm < 1) per_sm = 1;
+    kern<<<kSMs * per_sm, NT, sm, s>>>(g.dst, g.off32, g.hubstart, g.hz, hwords, rg, tasks, ntasks,
+                                       next, cap, d_total);
+    TC_LAUNCHED();
+    return 0;
+}
+
 template <typename OffT, int MODE, int NT>
 int launch_heavy(const DeviceGraph &g, const OffT *off, const RangeDev *rg, const uint2 *tasks,
                  const unsigned *ntasks, unsigned *next, uint32_t cap, size_t sm,
@@ -573,6 +733,15 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
         const unsigned *nt_c = counters + c;
         unsigned *next_c = counters + kClasses + c;
         int rc = 0;
+        const uint32_t hub_cap = 4 * (g.max_out < kClassMax[c] ? g.max_out : kClassMax[c]);
+        const size_t hub_sm = 4 * ((size_t)((g.n - g.hz + 31) / 32) + 1 + hub_cap);
+        if (sizeof(OffT) == 4 && g.rank_space && g.hubstart && hub_sm <= 200 * 1024) {
+            const int ntc = c == 2 ? 512 : 256;
+            rc = ntc == 512 ? launch_hub<512>(g, rg, tasks[c], nt_c, next_c, hub_cap, d_total, s)
+                            : launch_hub<256>(g, rg, tasks[c], nt_c, next_c, hub_cap, d_total, s);
+            if (rc) return rc;
+            continue;
+        }
         if (c == 0) rc = launch_heavy<OffT, 0, 128>(g, off, rg, tasks[c], nt_c, next_c, kClassCap[c], sm, d_total, s);
         else if (c == 1) rc = launch_heavy<OffT, 0, 256>(g, off, rg, tasks[c], nt_c, next_c, kClassCap[c], sm, d_total, s);
         else if (c == 2) rc = launch_heavy<OffT, 0, 512>(g, off, rg, tasks[c], nt_c, next_c, kClassCap[c], sm, d_total, s);
@@ -581,13 +750,15 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
     }
     TC_CUDA(cudaEventRecord(ev[2], s));
     {
-        auto kern = k_count_window<OffT, kWinThreads>;
-        const int sm = kWinSlots * 8;
+        const bool hub = g.rank_space && g.hubstart;
+        const uint32_t hwords = hub ? (uint32_t)((g.n - g.hz + 31) / 32) + 1 : 0u;
+        auto kern = hub ? k_count_window<OffT, kWinThreads, true> : k_count_window<OffT, kWinThreads, false>;
+        const int sm = kWinSlots * 8 + 4 * hwords;
         TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         int per_sm = 1;
         TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWinThreads, sm));
-        kern<<<kSMs * (per_sm > 0 ? per_sm : 1), kWinThreads, sm, s>>>(g.src, g.dst, off, rg,
-                                                                     counters + 2 * kClasses, d_total);
+        kern<<<kSMs * (per_sm > 0 ? per_sm : 1), kWinThreads, sm, s>>>(
+            g.src, g.dst, off, rg, counters + 2 * kClasses, g.hz, hwords, d_total);
     }
     TC_LAUNCHED();
     TC_CUDA(cudaEventRecord(ev[3], s));

@@ -94,7 +94,15 @@ struct DeviceGraph {
     uint32_t *off32 = nullptr; // u32 copy of node_offsets when m < 2^32 (count kernels)
     uint32_t max_out = 0;      // max out-degree
     int device = 0;
+    // Rank space: vertices relabelled by their (degree, id) rank, so orientation is
+    // "low rank -> high rank" and the hub zone [hz, n) holds the top kHubRanks ranks.
+    // hubstart[v] = first position of adj(v) whose rank is >= hz (lists are sorted).
+    bool rank_space = false;
+    uint32_t hz = 0;
+    uint32_t *hubstart = nullptr;
 };
+
+constexpr uint32_t kHubRanks = 1u << 18;  // hub zone size: 32 KB shared-memory bitmap
 
 int graph_alloc(DeviceGraph *g, uint64_t m, uint64_t n, cudaStream_t s);
 void graph_release(DeviceGraph *g, cudaStream_t s);
@@ -106,6 +114,13 @@ int finalize_graph_dev(DeviceGraph *g, cudaStream_t s);
 // Full reference preprocess on device-resident pairs (reference preprocess.py:74-84).
 int preprocess_dev(const uint32_t *pairs, uint64_t npairs, uint64_t n, DeviceGraph *out,
                    cudaStream_t s);
+// The same pipeline producing the rank-space oriented CSR (+ hubstart) directly.
+int preprocess_rank_dev(const uint32_t *pairs, uint64_t npairs, uint64_t n, DeviceGraph *out,
+                        cudaStream_t s);
+// Rank-space copy of an oriented graph given in original ids (same triangles).
+int relabel_dev(const DeviceGraph &g, DeviceGraph *out, cudaStream_t s);
+// hubstart[] and hz of a rank-space graph (after dst/off are in place).
+int build_hubstart_dev(DeviceGraph *g, cudaStream_t s);
 // Sort 2m pairs lexicographically (reference preprocess.py:23-33) into out_pairs.
 int sort_pairs_dev(const uint32_t *pairs, uint64_t npairs, uint64_t n, uint32_t *out_pairs,
                    cudaStream_t s);

@@ -73,6 +73,9 @@ __global__ void __launch_bounds__(256) k_degree_hist(const uint2 *__restrict__ p
 // packed key (u << vb) | v for the radix sort, and fold every kept key into the
 // per-pass digit histograms (saves a separate histogram read of the keys).
 // One atomicAdd on the output cursor per block iteration (2048 pairs).
+// RANK: `deg` holds ranks; keep (u, v) iff rank u < rank v (the same order as (deg, id))
+// and emit the relabelled key (rank u << vb) | rank v.
+template <bool RANK>
 __global__ void __launch_bounds__(256) k_orient(const uint2 *__restrict__ pairs, uint64_t npairs,
                                                 const uint32_t *__restrict__ deg, uint64_t n, int vb,
                                                 uint64_t *__restrict__ keys, uint64_t capacity,
@@ -95,9 +98,15 @@ __global__ void __launch_bounds__(256) k_orient(const uint2 *__restrict__ pairs,
             if (idx < npairs) {
                 uint2 p = ld_stream_u2(pairs + idx);
                 if ((uint64_t)p.x >= n || (uint64_t)p.y >= n) continue;  // flagged by k_degree_hist
-                uint32_t du = __ldg(deg + p.x), dv = __ldg(deg + p.y);
-                bool fwd = du < dv || (du == dv && p.x < p.y);
-                key[i] = ((uint64_t)p.x << vb) | p.y;
+                const uint32_t du = __ldg(deg + p.x), dv = __ldg(deg + p.y);
+                bool fwd;
+                if (RANK) {
+                    fwd = du < dv;
+                    key[i] = ((uint64_t)du << vb) | dv;
+                } else {
+                    fwd = du < dv || (du == dv && p.x < p.y);
+                    key[i] = ((uint64_t)p.x << vb) | p.y;
+                }
                 if (fwd) keepmask |= 1u << i;
             }
         }
@@ -238,6 +247,82 @@ __global__ void __launch_bounds__(256) k_orient_scatter(const uint2 *__restrict_
     if (keep) out[excl[blockIdx.x] + pos] = p;
 }
 
+// ------------------------------------------------------------- rank space ---
+// rank = position of the vertex in (degree, id) order: a stable sort of the ids (already
+// in id order) by degree.
+__global__ void k_deg_keys(const uint32_t *__restrict__ deg, uint64_t n, uint64_t *__restrict__ keys,
+                           uint32_t *__restrict__ ids) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        keys[i] = deg[i];
+        ids[i] = (uint32_t)i;
+    }
+}
+
+__global__ void k_scatter_rank(const uint32_t *__restrict__ ids, uint64_t n,
+                               uint32_t *__restrict__ rank) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        rank[ids[i]] = (uint32_t)i;
+}
+
+__global__ void k_max_u32(const uint32_t *__restrict__ a, uint64_t n, uint32_t *__restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint32_t best = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        best = a[i] > best ? a[i] : best;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint32_t y = __shfl_xor_sync(TC_FULL_MASK, best, o);
+        best = y > best ? y : best;
+    }
+    if (lane_id() == 0 && best) atomicMax(out, best);
+}
+
+// Undirected degree of an oriented graph: out-degree + in-degree.
+__global__ void k_outdeg(const int64_t *__restrict__ off, uint64_t n, uint32_t *__restrict__ deg) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        deg[i] = (uint32_t)(off[i + 1] - off[i]);
+}
+
+__global__ void __launch_bounds__(256) k_indeg(const uint32_t *__restrict__ dst, uint64_t m,
+                                               uint32_t *__restrict__ deg) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i - threadIdx.x < m; i += stride) {
+        const bool ok = i < m;
+        const uint32_t w = ok ? dst[i] : 0xffffffffu;
+        const unsigned peers = __match_any_sync(TC_FULL_MASK, w);
+        if (ok && (int)lane_id() == __ffs(peers) - 1) atomicAdd(deg + w, __popc(peers));
+    }
+}
+
+__global__ void k_relabel_keys(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
+                               uint64_t m, const uint32_t *__restrict__ rank, int vb,
+                               uint64_t *__restrict__ keys) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride)
+        keys[i] = ((uint64_t)__ldg(rank + src[i]) << vb) | __ldg(rank + dst[i]);
+}
+
+// hubstart[v] = first position of adj(v) with rank >= hz, or the list end.
+__global__ void k_hub_init(const uint32_t *__restrict__ off32, uint64_t n, uint32_t *__restrict__ hs) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        hs[i] = off32[i + 1];
+}
+
+__global__ void k_hub_boundary(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
+                               const uint32_t *__restrict__ off32, uint64_t m, uint32_t hz,
+                               uint32_t *__restrict__ hs) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += stride) {
+        if (dst[p] < hz) continue;
+        const uint32_t v = src[p];
+        if (p == off32[v] || dst[p - 1] < hz) hs[v] = (uint32_t)p;
+    }
+}
+
 }  // namespace
 
 int graph_alloc(DeviceGraph *g, uint64_t m, uint64_t n, cudaStream_t s) {
@@ -257,9 +342,11 @@ void graph_release(DeviceGraph *g, cudaStream_t s) {
     dfree(g->dst, s);
     dfree(g->off, s);
     dfree(g->off32, s);
+    dfree(g->hubstart, s);
     g->src = g->dst = nullptr;
     g->off = nullptr;
     g->off32 = nullptr;
+    g->hubstart = nullptr;
 }
 
 int finalize_graph_dev(DeviceGraph *g, cudaStream_t s) {
@@ -280,6 +367,7 @@ int finalize_graph_dev(DeviceGraph *g, cudaStream_t s) {
     TC_CUDA(cudaMemcpyAsync(&g->max_out, dmax, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));
     dfree(dmax, s);
+    if (g->rank_space) TC_CHECK(build_hubstart_dev(g, s));
     return 0;
 }
 
@@ -328,7 +416,7 @@ int preprocess_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, Devic
     uint64_t *keys = nullptr, *alt = nullptr;
     TC_CHECK(dalloc_t(&keys, capacity, s));
     if (npairs) {
-        k_orient<<<grid_for(npairs, 256 * kPP, kSMs * 8), 256, 0, s>>>(pairs, npairs, deg, n, vb, keys,
+        k_orient<false><<<grid_for(npairs, 256 * kPP, kSMs * 8), 256, 0, s>>>(pairs, npairs, deg, n, vb, keys,
                                                                        capacity, cursor, plan, hist);
         TC_LAUNCHED();
     }
@@ -348,7 +436,7 @@ int preprocess_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, Devic
         TC_CHECK(dalloc_t(&keys, capacity, s));
         TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
         TC_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
-        k_orient<<<grid_for(npairs, 256 * kPP, kSMs * 8), 256, 0, s>>>(pairs, npairs, deg, n, vb, keys,
+        k_orient<false><<<grid_for(npairs, 256 * kPP, kSMs * 8), 256, 0, s>>>(pairs, npairs, deg, n, vb, keys,
                                                                        capacity, cursor, plan, hist);
         TC_LAUNCHED();
     }
@@ -418,6 +506,189 @@ int orient_compact_dev(const uint32_t *pairs_u32, uint64_t npairs, const int64_t
     dfree(counts, s);
     dfree(excl, s);
     dfree(total, s);
+    return 0;
+}
+
+namespace {
+
+// rank[] of every vertex from its degree (stable sort of ids by degree).
+int compute_ranks(const uint32_t *deg, uint64_t n, uint32_t *rank, cudaStream_t s) {
+    if (n == 0) return 0;
+    uint32_t *dmax = nullptr, *hist = nullptr, *ids = nullptr, *ialt = nullptr, *sids = nullptr;
+    uint64_t *keys = nullptr, *kalt = nullptr;
+    TC_CHECK(dalloc_t(&dmax, 1, s));
+    TC_CUDA(cudaMemsetAsync(dmax, 0, sizeof(uint32_t), s));
+    k_max_u32<<<grid_for(n, 256, kSMs * 8), 256, 0, s>>>(deg, n, dmax);
+    TC_LAUNCHED();
+    uint32_t maxdeg = 0;
+    TC_CUDA(cudaMemcpyAsync(&maxdeg, dmax, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    const RadixPlan plan = make_radix_plan(bits_for(maxdeg));
+    TC_CHECK(dalloc_t(&keys, n, s));
+    TC_CHECK(dalloc_t(&kalt, n, s));
+    TC_CHECK(dalloc_t(&ids, n, s));
+    TC_CHECK(dalloc_t(&ialt, n, s));
+    TC_CHECK(dalloc_t(&hist, kMaxPasses * kRadix, s));
+    TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+    k_deg_keys<<<grid_for(n, 256, kSMs * 16), 256, 0, s>>>(deg, n, keys, ids);
+    TC_LAUNCHED();
+    TC_CHECK(radix_histogram(keys, n, plan, hist, s));
+    uint64_t *skeys = nullptr;
+    TC_CHECK(radix_sort(keys, kalt, ids, ialt, n, plan, hist, kOutKeys, nullptr, nullptr, 0, &skeys,
+                        &sids, s));
+    k_scatter_rank<<<grid_for(n, 256, kSMs * 16), 256, 0, s>>>(sids, n, rank);
+    TC_LAUNCHED();
+    dfree(dmax, s);
+    dfree(hist, s);
+    dfree(keys, s);
+    dfree(kalt, s);
+    dfree(ids, s);
+    dfree(ialt, s);
+    return 0;
+}
+
+}  // namespace
+
+int build_hubstart_dev(DeviceGraph *g, cudaStream_t s) {
+    if (!g->off32) {
+        set_error("rank space needs m < 2^32");
+        return -1;
+    }
+    g->hz = g->n > kHubRanks ? (uint32_t)(g->n - kHubRanks) : 0u;
+    if (!g->hubstart) TC_CHECK(dalloc_t(&g->hubstart, g->n ? g->n : 1, s));
+    if (g->n) {
+        k_hub_init<<<grid_for(g->n, 256, kSMs * 16), 256, 0, s>>>(g->off32, g->n, g->hubstart);
+        TC_LAUNCHED();
+    }
+    if (g->m) {
+        k_hub_boundary<<<grid_for(g->m, 256, kSMs * 16), 256, 0, s>>>(g->src, g->dst, g->off32, g->m,
+                                                                      g->hz, g->hubstart);
+        TC_LAUNCHED();
+    }
+    g->rank_space = true;
+    return 0;
+}
+
+int preprocess_rank_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, DeviceGraph *out,
+                        cudaStream_t s) {
+    const uint2 *pairs = reinterpret_cast<const uint2 *>(pairs_u32);
+    if (n >= (1ull << 32) || npairs / 2 >= (1ull << 32)) {
+        set_error("rank-space preprocessing needs num_vertices < 2^32 and m < 2^32");
+        return -1;
+    }
+    const int vb = n > 1 ? bits_for(n - 1) : 1;
+    const RadixPlan plan = make_radix_plan(2 * vb);
+    uint32_t *deg = nullptr, *rank = nullptr, *hist = nullptr, *scratch = nullptr;
+    unsigned long long *cursor = nullptr;
+    TC_CHECK(dalloc_t(&deg, n ? n : 1, s));
+    TC_CHECK(dalloc_t(&rank, n ? n : 1, s));
+    TC_CHECK(dalloc_t(&scratch, 4, s));
+    TC_CHECK(dalloc_t(&hist, kMaxPasses * kRadix, s));
+    TC_CHECK(dalloc_t(&cursor, 1, s));
+    TC_CUDA(cudaMemsetAsync(deg, 0, (n ? n : 1) * sizeof(uint32_t), s));
+    TC_CUDA(cudaMemsetAsync(scratch, 0, 4 * sizeof(uint32_t), s));
+    TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+    TC_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
+    if (npairs) {
+        k_degree_hist<<<grid_for(npairs, 256 * kPP, kSMs * 8), 256, 0, s>>>(pairs, npairs, deg, n,
+                                                                            scratch);
+        TC_LAUNCHED();
+    }
+    uint32_t bad = 0;
+    TC_CUDA(cudaMemcpyAsync(&bad, scratch, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    if (bad) {
+        set_error("edge array holds a vertex id >= num_vertices");
+        return -1;
+    }
+    TC_CHECK(compute_ranks(deg, n, rank, s));
+    uint64_t capacity = npairs / 2 + 1;
+    uint64_t *keys = nullptr, *alt = nullptr;
+    TC_CHECK(dalloc_t(&keys, capacity, s));
+    if (npairs) {
+        k_orient<true><<<grid_for(npairs, 256 * kPP, kSMs * 8), 256, 0, s>>>(
+            pairs, npairs, rank, n, vb, keys, capacity, cursor, plan, hist);
+        TC_LAUNCHED();
+    }
+    unsigned long long kept = 0;
+    TC_CUDA(cudaMemcpyAsync(&kept, cursor, sizeof(kept), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    if (kept > capacity) {  // not a symmetric edge array: redo with room for every survivor
+        dfree(keys, s);
+        capacity = kept;
+        TC_CHECK(dalloc_t(&keys, capacity, s));
+        TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+        TC_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
+        k_orient<true><<<grid_for(npairs, 256 * kPP, kSMs * 8), 256, 0, s>>>(
+            pairs, npairs, rank, n, vb, keys, capacity, cursor, plan, hist);
+        TC_LAUNCHED();
+    }
+    const uint64_t m = kept;
+    TC_CHECK(graph_alloc(out, m, n, s));
+    TC_CHECK(dalloc_t(&alt, m ? m : 1, s));
+    TC_CHECK(radix_sort(keys, alt, nullptr, nullptr, m, plan, hist, kOutSoA, out->src, out->dst, vb,
+                        nullptr, nullptr, s));
+    TC_CUDA(cudaMemsetAsync(out->dst + m, 0, 4 * sizeof(uint32_t), s));
+    TC_CHECK(build_node_array_dev(out->src, m, n, out->off, out->off32, scratch + 1, s));
+    TC_CHECK(build_hubstart_dev(out, s));
+    TC_CUDA(cudaMemcpyAsync(&out->max_out, scratch + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    dfree(deg, s);
+    dfree(rank, s);
+    dfree(hist, s);
+    dfree(cursor, s);
+    dfree(keys, s);
+    dfree(alt, s);
+    dfree(scratch, s);
+    TC_CUDA(cudaStreamSynchronize(s));
+    return 0;
+}
+
+int relabel_dev(const DeviceGraph &g, DeviceGraph *out, cudaStream_t s) {
+    if (g.n >= (1ull << 32) || g.m >= (1ull << 32)) {
+        set_error("rank-space relabelling needs num_vertices < 2^32 and m < 2^32");
+        return -1;
+    }
+    const uint64_t n = g.n, m = g.m;
+    const int vb = n > 1 ? bits_for(n - 1) : 1;
+    const RadixPlan plan = make_radix_plan(2 * vb);
+    uint32_t *deg = nullptr, *rank = nullptr, *hist = nullptr, *scratch = nullptr;
+    TC_CHECK(dalloc_t(&deg, n ? n : 1, s));
+    TC_CHECK(dalloc_t(&rank, n ? n : 1, s));
+    TC_CHECK(dalloc_t(&scratch, 4, s));
+    TC_CHECK(dalloc_t(&hist, kMaxPasses * kRadix, s));
+    TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+    TC_CUDA(cudaMemsetAsync(scratch, 0, 4 * sizeof(uint32_t), s));
+    if (n) {
+        k_outdeg<<<grid_for(n, 256, kSMs * 16), 256, 0, s>>>(g.off, n, deg);
+        TC_LAUNCHED();
+    }
+    if (m) {
+        k_indeg<<<grid_for(m, 256, kSMs * 16), 256, 0, s>>>(g.dst, m, deg);
+        TC_LAUNCHED();
+    }
+    TC_CHECK(compute_ranks(deg, n, rank, s));
+    uint64_t *keys = nullptr, *alt = nullptr;
+    TC_CHECK(dalloc_t(&keys, m ? m : 1, s));
+    TC_CHECK(dalloc_t(&alt, m ? m : 1, s));
+    if (m) {
+        k_relabel_keys<<<grid_for(m, 256, kSMs * 16), 256, 0, s>>>(g.src, g.dst, m, rank, vb, keys);
+        TC_LAUNCHED();
+    }
+    TC_CHECK(radix_histogram(keys, m, plan, hist, s));
+    TC_CHECK(graph_alloc(out, m, n, s));
+    TC_CHECK(radix_sort(keys, alt, nullptr, nullptr, m, plan, hist, kOutSoA, out->src, out->dst, vb,
+                        nullptr, nullptr, s));
+    TC_CUDA(cudaMemsetAsync(out->dst + m, 0, 4 * sizeof(uint32_t), s));
+    TC_CHECK(build_node_array_dev(out->src, m, n, out->off, out->off32, scratch + 1, s));
+    TC_CHECK(build_hubstart_dev(out, s));
+    TC_CUDA(cudaMemcpyAsync(&out->max_out, scratch + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    dfree(deg, s);
+    dfree(rank, s);
+    dfree(hist, s);
+    dfree(scratch, s);
+    dfree(keys, s);
+    dfree(alt, s);
     return 0;
 }
 

@@ -4,9 +4,10 @@ The reference's multi-device analogue is count_partitioned with P pools over con
 edge ranges (reference count.py:181-204); the paper replicates the preprocessed arrays
 to every GPU and sums the per-GPU counts on the host.  Here:
 
-  1. rank 0 preprocesses (tc_preprocess) -- the oriented CSR lives in its HBM;
+  1. rank 0 preprocesses into the count-ready rank-space CSR (tc_preprocess_ex);
   2. edge_dst and node_offsets are broadcast to every rank over NVLink (NCCL);
-     every rank rebuilds edge_src and its u32 offsets locally (tc_graph_finalize);
+     every rank rebuilds edge_src, its u32 offsets and hubstart locally
+     (tc_graph_finalize);
   3. every rank computes the same estimated-work bounds (sum of d+(u) + d+(v) + c,
      SURVEY.md §8(e)) and counts its own contiguous range;
   4. one all-reduce of a single 64-bit count.
@@ -150,11 +151,17 @@ class B200Ops(Ops):
         _lib.lib()
 
     def preprocess(self, edges):
-        from .count import preprocess_device
-        from .preprocess import preprocess
-        if hasattr(edges, "ptr"):
-            return preprocess_device(edges)[0].device()
-        return preprocess(edges).device()
+        """Rank-space CSR (count-ready); host edges are uploaded first."""
+        from .graph import DeviceGraph
+        h = ctypes.c_void_p()
+        t = _lib.TcTimes()
+        on_dev = hasattr(edges, "ptr")
+        ptr = ctypes.c_void_p(edges.ptr) if on_dev else _lib.ptr(edges.edges)
+        npairs = edges.npairs if on_dev else edges.edges.shape[0]
+        _lib.check(_lib.lib().tc_preprocess_ex(ptr, npairs, edges.num_vertices, 1 if on_dev else 0,
+                                               _lib.PREPROCESS_RANK_SPACE, ctypes.byref(h),
+                                               ctypes.byref(t)))
+        return DeviceGraph(h.value)
 
     def graph_shape(self, graph):
         return graph.m, graph.n
@@ -162,7 +169,7 @@ class B200Ops(Ops):
     def empty_graph(self, m, n):
         from .graph import DeviceGraph
         h = ctypes.c_void_p()
-        _lib.check(_lib.lib().tc_graph_create(m, n, ctypes.byref(h)))
+        _lib.check(_lib.lib().tc_graph_create(m, n, _lib.PREPROCESS_RANK_SPACE, ctypes.byref(h)))
         return DeviceGraph(h.value)
 
     def replica_tensors(self, graph):
