@@ -133,21 +133,78 @@ __global__ void __launch_bounds__(256) k_orient(const uint2 *__restrict__ pairs,
         if (sh[i]) atomicAdd(&ghist[i], sh[i]);
 }
 
-// Node array from a grouped first column (reference preprocess.py:36-46, paper step
-// 4/8): entry i in [0, k] writes off[w] = i for every w in (firsts[i-1], firsts[i]].
-// Also the u32 copy for the count kernels and the max out-degree.
-__global__ void __launch_bounds__(256) k_node_array(const uint32_t *__restrict__ firsts, uint64_t k,
-                                                    uint64_t n, int64_t *__restrict__ off,
-                                                    uint32_t *__restrict__ off32,
-                                                    uint32_t *__restrict__ max_out) {
+// Node array from a grouped first column (reference preprocess.py:36-46, paper steps 4
+// and 8): out-degree histogram of the column (runs of equal ids inside a warp become one
+// atomic), then an exclusive scan into node_offsets.  Gaps of empty vertices -- huge in
+// rank space, where every isolated vertex ranks first -- cost nothing extra.
+__global__ void __launch_bounds__(256) k_run_hist(const uint32_t *__restrict__ col, uint64_t k,
+                                                  uint32_t *__restrict__ cnt) {
+    const unsigned lane = lane_id();
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= k; i += stride) {
-        int64_t a = i == 0 ? -1 : (int64_t)firsts[i - 1];
-        int64_t b = i == k ? (int64_t)n : (int64_t)firsts[i];
-        for (int64_t w = a + 1; w <= b; ++w) {
-            off[w] = (int64_t)i;
-            if (off32) off32[w] = (uint32_t)i;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < k;
+         base += stride) {
+        const uint64_t i = base + lane;
+        const bool ok = i < k;
+        const uint32_t u = ok ? col[i] : 0xffffffffu;
+        const uint32_t prev = __shfl_up_sync(TC_FULL_MASK, u, 1);
+        const bool head = ok && (lane == 0 || prev != u);
+        const unsigned heads = __ballot_sync(TC_FULL_MASK, head || !ok);
+        if (head) {
+            unsigned above = lane == 31 ? 0u : heads & ~((2u << lane) - 1u);
+            const unsigned next = above ? (unsigned)(__ffs(above) - 1) : 32u;
+            atomicAdd(cnt + u, next - lane);
         }
+    }
+}
+
+constexpr int kScanTile = 4096;
+
+__global__ void __launch_bounds__(256) k_tile_sum(const uint32_t *__restrict__ cnt, uint64_t n,
+                                                  unsigned long long *__restrict__ sums) {
+    const uint64_t b = (uint64_t)blockIdx.x * kScanTile;
+    unsigned long long acc = 0;
+    for (uint64_t i = b + threadIdx.x; i < b + kScanTile && i < n; i += 256) acc += cnt[i];
+    __shared__ unsigned long long s_red[8];
+    acc = warp_sum(acc);
+    if (lane_id() == 0) s_red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < 8; ++w) t += s_red[w];
+        sums[blockIdx.x] = t;
+    }
+}
+
+__global__ void k_scan_sums(unsigned long long *__restrict__ sums, uint64_t nt) {
+    __shared__ unsigned long long s_w[32];
+    unsigned long long carry = 0;
+    for (uint64_t b = 0; b < nt; b += blockDim.x) {
+        const uint64_t i = b + threadIdx.x;
+        const unsigned long long x = i < nt ? sums[i] : 0;
+        unsigned long long t;
+        const unsigned long long e = block_exclusive_scan<unsigned long long>(x, s_w, &t);
+        if (i < nt) sums[i] = carry + e;
+        carry += t;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_scan_apply(const uint32_t *__restrict__ cnt, uint64_t n,
+                                                    const unsigned long long *__restrict__ base,
+                                                    int64_t *__restrict__ off,
+                                                    uint32_t *__restrict__ off32) {
+    __shared__ unsigned long long s_w[32];
+    const uint64_t b = (uint64_t)blockIdx.x * kScanTile;
+    unsigned long long carry = base[blockIdx.x];
+    for (uint64_t c = b; c < b + kScanTile && c < n; c += 256) {
+        const uint64_t i = c + threadIdx.x;
+        const unsigned long long x = i < n ? cnt[i] : 0;
+        unsigned long long t;
+        const unsigned long long e = block_exclusive_scan<unsigned long long>(x, s_w, &t);
+        if (i < n) {
+            off[i] = (int64_t)(carry + e);
+            if (off32) off32[i] = (uint32_t)(carry + e);
+        }
+        carry += t;
     }
 }
 
@@ -373,15 +430,41 @@ int finalize_graph_dev(DeviceGraph *g, cudaStream_t s) {
 
 int build_node_array_dev(const uint32_t *firsts, uint64_t k, uint64_t n, int64_t *off,
                          uint32_t *off32, uint32_t *max_out, cudaStream_t s) {
-    k_node_array<<<grid_for(k + 1, 256, kSMs * 16), 256, 0, s>>>(firsts, k, n, off, off32, max_out);
-    TC_LAUNCHED();
+    uint32_t *cnt = nullptr;
+    unsigned long long *sums = nullptr;
+    const uint64_t nt = (n + kScanTile - 1) / kScanTile;
+    TC_CHECK(dalloc_t(&cnt, n ? n : 1, s));
+    TC_CHECK(dalloc_t(&sums, nt ? nt : 1, s));
+    if (n) TC_CUDA(cudaMemsetAsync(cnt, 0, n * sizeof(uint32_t), s));
+    if (k) {
+        k_run_hist<<<grid_for(k, 256, kSMs * 16), 256, 0, s>>>(firsts, k, cnt);
+        TC_LAUNCHED();
+    }
+    if (n) {
+        k_tile_sum<<<(unsigned)nt, 256, 0, s>>>(cnt, n, sums);
+        TC_LAUNCHED();
+        k_scan_sums<<<1, 512, 0, s>>>(sums, nt);
+        TC_LAUNCHED();
+        k_scan_apply<<<(unsigned)nt, 256, 0, s>>>(cnt, n, sums, off, off32);
+        TC_LAUNCHED();
+    }
+    // off[n] = k (every pair lies in some vertex's run for a valid grouped column)
+    const int64_t kk = (int64_t)k;
+    TC_CUDA(cudaMemcpyAsync(off + n, &kk, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    if (off32) {
+        const uint32_t k32 = (uint32_t)k;
+        TC_CUDA(cudaMemcpyAsync(off32 + n, &k32, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    }
     if (max_out) {
         TC_CUDA(cudaMemsetAsync(max_out, 0, sizeof(uint32_t), s));
         if (n) {
-            k_max_degree<<<grid_for(n, 256, kSMs * 8), 256, 0, s>>>(off, n, max_out);
+            k_max_u32<<<grid_for(n, 256, kSMs * 8), 256, 0, s>>>(cnt, n, max_out);
             TC_LAUNCHED();
         }
     }
+    TC_CUDA(cudaStreamSynchronize(s));  // host-side k/k32 sources of the async copies
+    dfree(cnt, s);
+    dfree(sums, s);
     return 0;
 }
 
