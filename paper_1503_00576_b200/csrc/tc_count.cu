@@ -69,6 +69,13 @@ __device__ __forceinline__ unsigned long long lds64(uint32_t addr) {
     return v;
 }
 
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -198,6 +205,52 @@ __device__ __forceinline__ uint32_t sweep(const uint32_t *__restrict__ dst, cons
     return found;
 }
 
+// Dense edges of a heavy source: |adj(u) ∩ adj(v)| = popcount(B_u & B_v) over the hub
+// words v can reach.  Chunk c of edge k reads 4 words of B_v at global word cb_k + 4c and
+// 4 words of the shared-memory B_u at word vs_k + 4c (both 16-byte aligned).
+template <int U>
+__device__ __forceinline__ uint32_t sweep_and(const uint32_t *__restrict__ bits,
+                                              const EdgeTable<uint32_t> &et, uint32_t nwin,
+                                              uint32_t c0, uint32_t c1, uint32_t bm) {
+    const unsigned lane = lane_id();
+    uint32_t k = 0;
+    {
+        const uint32_t c = c0 + lane < c1 ? c0 + lane : c1 - 1;
+        uint32_t a = 0, b = nwin;
+        while (b - a > 1) {
+            const uint32_t mid = (a + b) >> 1;
+            if (et.cst[mid] <= c) a = mid; else b = mid;
+        }
+        k = a;
+    }
+    uint32_t nextb = et.cst[k + 1], gb = et.cb[k], sb = et.vs[k];
+    uint32_t found = 0;
+    for (uint32_t base = c0; base < c1; base += 32 * U) {
+        uint4 q[U];
+        uint32_t sw[U], live[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            uint32_t c = base + j * 32 + lane;
+            live[j] = c < c1 ? 0xffffffffu : 0u;
+            c = c < c1 ? c : c1 - 1;
+            if (c >= nextb) {
+                do { nextb = et.cst[++k + 1]; } while (c >= nextb);
+                gb = et.cb[k];
+                sb = et.vs[k];
+            }
+            q[j] = __ldg(reinterpret_cast<const uint4 *>(bits + gb + 4 * c));
+            sw[j] = sb + 4 * c;
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const uint4 b = lds128(bm + 4 * sw[j]);
+            found += __popc(q[j].x & b.x & live[j]) + __popc(q[j].y & b.y & live[j]) +
+                     __popc(q[j].z & b.z & live[j]) + __popc(q[j].w & b.w & live[j]);
+        }
+    }
+    return found;
+}
+
 template <typename T>
 __device__ __forceinline__ void block_add_total(T acc, unsigned long long *total) {
     __shared__ unsigned long long s_red[32];
@@ -229,12 +282,17 @@ __global__ void k_range_init(const uint32_t *__restrict__ src, uint64_t lo, uint
 // HUB (rank space): a bitmap of the hub zone [hz, hz + 32 hwords) marks every hub
 // neighbour of any light source of the window; a clear bit rejects an item with one
 // shared load, and only candidates (set bit, or a non-hub w) pay the exact cuckoo test.
+// HUB also enables the dense-hub shortcut: for an edge (u, v) with v among the top ranks,
+// only the elements of adj(u) after v can close a triangle (ranks increase along a list),
+// so those <= 31 candidates are tested against v's global bitmap instead of streaming
+// all of adj(v).
 template <typename OffT, int NT, bool HUB>
 __global__ void __launch_bounds__(NT)
     k_count_window(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
                    const OffT *__restrict__ off, const RangeDev *__restrict__ rg,
-                   unsigned *__restrict__ next, uint32_t hz, uint32_t hwords,
-                   unsigned long long *__restrict__ total) {
+                   unsigned *__restrict__ next, uint32_t hz, uint32_t hwords, uint32_t vt,
+                   const uint32_t *__restrict__ dense_off, const uint32_t *__restrict__ dense_bits,
+                   uint32_t dense_words, unsigned long long *__restrict__ total) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long *s_tab = reinterpret_cast<unsigned long long *>(smem);  // kWinSlots
     uint32_t *bitmap = reinterpret_cast<uint32_t *>(s_tab + kWinSlots);       // hwords (HUB)
@@ -286,49 +344,69 @@ __global__ void __launch_bounds__(NT)
             __syncthreads();
             if (!failed) break;
         }
-        uint32_t chunks = 0;
-        OffT vs = 0, ve = 0, a4 = 0;
-        uint32_t u = 0;
+        OffT vs = 0, ve = 0, ua = 0, ub = 0;
+        uint32_t u = 0, bias = 0;
+        bool dense = false;
         if (threadIdx.x < nwin) {
             const uint64_t e = ws + threadIdx.x;
             u = __ldg(src + e);
-            const OffT su = __ldg(off + u);
-            if (__ldg(off + u + 1) - su <= (OffT)kLightMax) {
+            const OffT su = __ldg(off + u), eu = __ldg(off + u + 1);
+            if (eu - su <= (OffT)kLightMax) {
                 const uint32_t v = __ldg(dst + e);
-                vs = __ldg(off + v);
-                ve = __ldg(off + v + 1);
-                a4 = vs & ~(OffT)3;
-                chunks = ve > vs ? (uint32_t)((ve - a4 + 3) >> 2) : 0u;
+                dense = HUB && v >= vt;
+                if (dense) {
+                    ua = (OffT)e + 1;  // adj(u) after v
+                    ub = eu;
+                    bias = __ldg(dense_off + (v - vt)) - (((v + 1 - hz) >> 5) & ~3u);
+                } else {
+                    vs = __ldg(off + v);
+                    ve = __ldg(off + v + 1);
+                }
             }
         }
-        uint32_t tot;
-        const uint32_t cst = block_exclusive_scan<uint32_t>(chunks, s_scan, &tot);
-        s_cb[threadIdx.x] = a4 - (OffT)(4 * cst);
-        s_vs[threadIdx.x] = vs;
-        s_ve[threadIdx.x] = ve;
-        s_cst[threadIdx.x] = cst;
-        s_aux[threadIdx.x] = u;
-        if (threadIdx.x == 0) s_cst[NT] = tot;
-        __syncthreads();
-        const uint32_t c0 = (uint32_t)((uint64_t)tot * warp / NW);
-        const uint32_t c1 = (uint32_t)((uint64_t)tot * (warp + 1) / NW);
-        if (c0 < c1) {
-            if (HUB) {
-                acc += sweep<OffT, true, 4>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t sid) {
-                    const uint32_t r = w - hz;
-                    const uint32_t word = lds32(bm + 4 * min(r >> 5, hwords - 1));
-                    bool hit = false;
-                    if (r >= hbits || ((word >> (r & 31)) & 1u))
-                        hit = ck.contains(((unsigned long long)sid << 32) | w);
-                    return hit;
-                });
-            } else {
-                acc += sweep<OffT, true>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t sid) {
-                    return ck.contains(((unsigned long long)sid << 32) | w);
-                });
+        // pass 0: v-side items of sparse edges against the window's (source, w) table;
+        // pass 1: u-side candidates of dense edges against v's global bitmap.
+        for (int pass = 0; pass < (HUB ? 2 : 1); ++pass) {
+            const OffT a = pass == 0 ? vs : ua, bnd = pass == 0 ? ve : ub;
+            const OffT a4 = a & ~(OffT)3;
+            const uint32_t chunks = bnd > a ? (uint32_t)((bnd - a4 + 3) >> 2) : 0u;
+            uint32_t tot;
+            const uint32_t cst = block_exclusive_scan<uint32_t>(chunks, s_scan, &tot);
+            if (tot == 0) continue;  // block-uniform
+            s_cb[threadIdx.x] = a4 - (OffT)(4 * cst);
+            s_vs[threadIdx.x] = a;
+            s_ve[threadIdx.x] = bnd;
+            s_cst[threadIdx.x] = cst;
+            s_aux[threadIdx.x] = pass == 0 ? u : bias;
+            if (threadIdx.x == 0) s_cst[NT] = tot;
+            __syncthreads();
+            const uint32_t c0 = (uint32_t)((uint64_t)tot * warp / NW);
+            const uint32_t c1 = (uint32_t)((uint64_t)tot * (warp + 1) / NW);
+            if (c0 < c1) {
+                if (pass == 1) {
+                    // masked-out chunk items are probed too: clamp them into the array
+                    acc += sweep<OffT, true, 4>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t bw) {
+                        const uint32_t r = w - hz;
+                        const uint32_t i = min(bw + (r >> 5), dense_words - 1);
+                        return ((__ldg(dense_bits + i) >> (r & 31)) & 1u) != 0u;
+                    });
+                } else if (HUB) {
+                    acc += sweep<OffT, true, 4>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t sid) {
+                        const uint32_t r = w - hz;
+                        const uint32_t word = lds32(bm + 4 * min(r >> 5, hwords - 1));
+                        bool hit = false;
+                        if (r >= hbits || ((word >> (r & 31)) & 1u))
+                            hit = ck.contains(((unsigned long long)sid << 32) | w);
+                        return hit;
+                    });
+                } else {
+                    acc += sweep<OffT, true>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t sid) {
+                        return ck.contains(((unsigned long long)sid << 32) | w);
+                    });
+                }
             }
+            __syncthreads();
         }
-        __syncthreads();
         if (HUB) {  // clear the bits this window set
             for (uint64_t P = sb + threadIdx.x; P < se; P += NT) {
                 const uint32_t w = __ldg(dst + P);
@@ -473,6 +551,8 @@ template <int NT, int U>
 __global__ void __launch_bounds__(NT)
     k_count_hub(const uint32_t *__restrict__ dst, const uint32_t *__restrict__ off,
                 const uint32_t *__restrict__ hubstart, uint32_t hz, uint32_t hwords,
+                uint32_t vt, const uint32_t *__restrict__ dense_off,
+                const uint32_t *__restrict__ dense_bits,
                 const RangeDev *__restrict__ rg, const uint2 *__restrict__ tasks,
                 const unsigned *__restrict__ ntasks, unsigned *__restrict__ next, uint32_t cap,
                 unsigned long long *__restrict__ total) {
@@ -530,32 +610,53 @@ __global__ void __launch_bounds__(NT)
 
         for (uint64_t ws = es; ws < ee; ws += NT) {
             const uint32_t nwin = (uint32_t)(ee - ws < (uint64_t)NT ? ee - ws : (uint64_t)NT);
-            uint32_t v = 0, vs = 0, ve = 0, hv = 0;
+            uint32_t v = 0, vs = 0, ve = 0, hv = 0, dgo = 0, dws = 0;
+            bool dense = false;
             if (threadIdx.x < nwin) {
                 v = __ldg(dst + ws + threadIdx.x);
-                vs = __ldg(off + v);
-                ve = __ldg(off + v + 1);
-                hv = __ldg(hubstart + v);
+                dense = v >= vt;
+                if (dense) {  // v's adjacency is available as a bitmap: AND with B_u
+                    dgo = __ldg(dense_off + (v - vt));
+                    dws = ((v + 1 - hz) >> 5) & ~3u;
+                } else {
+                    vs = __ldg(off + v);
+                    ve = __ldg(off + v + 1);
+                    hv = __ldg(hubstart + v);
+                }
             }
-            // pass 0: hub suffixes [hv, ve) against the bitmap;
+            // pass 0: hub suffixes [hv, ve) of sparse edges against the bitmap;
             // pass 1: non-hub prefixes [vs, hv) against the cuckoo table (only if adj(u)
-            //         has non-hub elements -- otherwise they cannot match).
-            for (int pass = 0; pass < (nh ? 2 : 1); ++pass) {
-                const uint32_t a = pass == 0 ? hv : vs, b = pass == 0 ? ve : hv;
-                const uint32_t a4 = a & ~3u;
-                const uint32_t chunks = b > a ? (b - a4 + 3) >> 2 : 0u;
+            //         has non-hub elements -- otherwise they cannot match);
+            // pass 2: dense edges, popcount(B_u & B_v) over v's hub words.
+            for (int pass = 0; pass < 3; ++pass) {
+                if (pass == 1 && !nh) continue;
+                uint32_t chunks, cb, vsb;
+                if (pass < 2) {
+                    const uint32_t a = pass == 0 ? hv : vs, b = pass == 0 ? ve : hv;
+                    const uint32_t a4 = a & ~3u;
+                    chunks = b > a ? (b - a4 + 3) >> 2 : 0u;
+                    cb = a4;
+                    vsb = a;
+                    s_ve[threadIdx.x] = b;
+                } else {
+                    chunks = dense ? (hwords - dws) >> 2 : 0u;
+                    cb = dgo;
+                    vsb = dws;
+                }
                 uint32_t tot;
                 const uint32_t cst = block_exclusive_scan<uint32_t>(chunks, s_scan, &tot);
-                s_cb[threadIdx.x] = a4 - 4 * cst;
-                s_vs[threadIdx.x] = a;
-                s_ve[threadIdx.x] = b;
+                if (tot == 0) continue;  // block-uniform
+                s_cb[threadIdx.x] = cb - 4 * cst;
+                s_vs[threadIdx.x] = pass < 2 ? vsb : vsb - 4 * cst;
                 s_cst[threadIdx.x] = cst;
                 if (threadIdx.x == 0) s_cst[NT] = tot;
                 __syncthreads();
                 const uint32_t c0 = (uint32_t)((uint64_t)tot * warp / NW);
                 const uint32_t c1 = (uint32_t)((uint64_t)tot * (warp + 1) / NW);
                 if (c0 < c1) {
-                    if (pass == 0) {
+                    if (pass == 2) {
+                        acc += sweep_and<U>(dense_bits, et, NT, c0, c1, bm);
+                    } else if (pass == 0) {
                         const uint32_t last = hwords - 1;
                         acc += sweep<uint32_t, false, U>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t) {
                             const uint32_t r = w - hz;
@@ -664,7 +765,7 @@ size_t heavy_smem(int cls, uint32_t max_out) {
 template <int NT>
 int launch_hub(const DeviceGraph &g, const RangeDev *rg, const uint2 *tasks, const unsigned *ntasks,
                unsigned *next, uint32_t cap, unsigned long long *d_total, cudaStream_t s) {
-    const uint32_t hwords = (uint32_t)((g.n - g.hz + 31) / 32) + 1;
+    const uint32_t hwords = g.hwp;
     const size_t sm = 4 * ((size_t)hwords + cap);
     static const int unroll = getenv("TC_HUB_UNROLL") ? atoi(getenv("TC_HUB_UNROLL")) : 4;
     auto kern = unroll >= 4 ? k_count_hub<NT, 4> : unroll == 3 ? k_count_hub<NT, 3> : k_count_hub<NT, 2>;
@@ -672,8 +773,8 @@ int launch_hub(const DeviceGraph &g, const RangeDev *rg, const uint2 *tasks, con
     int per_sm = 1;
     TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, sm));
     if (per_sm < 1) per_sm = 1;
-    kern<<<kSMs * per_sm, NT, sm, s>>>(g.dst, g.off32, g.hubstart, g.hz, hwords, rg, tasks, ntasks,
-                                       next, cap, d_total);
+    kern<<<kSMs * per_sm, NT, sm, s>>>(g.dst, g.off32, g.hubstart, g.hz, hwords, g.vt, g.dense_off,
+                                       g.dense_bits, rg, tasks, ntasks, next, cap, d_total);
     TC_LAUNCHED();
     return 0;
 }
@@ -734,7 +835,7 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
         unsigned *next_c = counters + kClasses + c;
         int rc = 0;
         const uint32_t hub_cap = 4 * (g.max_out < kClassMax[c] ? g.max_out : kClassMax[c]);
-        const size_t hub_sm = 4 * ((size_t)((g.n - g.hz + 31) / 32) + 1 + hub_cap);
+        const size_t hub_sm = 4 * ((size_t)g.hwp + hub_cap);
         if (sizeof(OffT) == 4 && g.rank_space && g.hubstart && hub_sm <= 200 * 1024) {
             const int ntc = c == 2 ? 512 : 256;
             rc = ntc == 512 ? launch_hub<512>(g, rg, tasks[c], nt_c, next_c, hub_cap, d_total, s)
@@ -758,7 +859,8 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
         int per_sm = 1;
         TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWinThreads, sm));
         kern<<<kSMs * (per_sm > 0 ? per_sm : 1), kWinThreads, sm, s>>>(
-            g.src, g.dst, off, rg, counters + 2 * kClasses, g.hz, hwords, d_total);
+            g.src, g.dst, off, rg, counters + 2 * kClasses, g.hz, hwords, hub ? g.vt : 0u,
+            g.dense_off, g.dense_bits, g.dense_words, d_total);
     }
     TC_LAUNCHED();
     TC_CUDA(cudaEventRecord(ev[3], s));

@@ -100,9 +100,17 @@ struct DeviceGraph {
     bool rank_space = false;
     uint32_t hz = 0;
     uint32_t *hubstart = nullptr;
+    // Dense hubs: every vertex v of rank >= vt (the top kDenseRanks) also has adj(v) as a
+    // bitmap over hub-zone words [ws4(v), hwp) at dense_bits + dense_off[v - vt], where
+    // ws4(v) = ((v + 1 - hz) / 32) rounded down to a multiple of 4 and hwp = hub-zone
+    // words rounded up to a multiple of 4.
+    uint32_t vt = 0, hwp = 0, dense_words = 0;
+    uint32_t *dense_off = nullptr;   // [n - vt + 1] word offsets (multiples of 4)
+    uint32_t *dense_bits = nullptr;
 };
 
-constexpr uint32_t kHubRanks = 1u << 18;  // hub zone size: 32 KB shared-memory bitmap
+constexpr uint32_t kHubRanks = 1u << 18;    // hub zone size: 32 KB shared-memory bitmap
+constexpr uint32_t kDenseRanks = 1u << 15;  // dense-hub bitmaps: 64 MB at R-MAT s26
 
 int graph_alloc(DeviceGraph *g, uint64_t m, uint64_t n, cudaStream_t s);
 void graph_release(DeviceGraph *g, cudaStream_t s);

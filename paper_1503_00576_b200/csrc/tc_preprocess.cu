@@ -380,6 +380,44 @@ __global__ void k_hub_boundary(const uint32_t *__restrict__ src, const uint32_t 
     }
 }
 
+// Dense-hub bitmaps (see DeviceGraph): word offsets of every dense vertex, then one bit
+// per adjacency entry of a dense vertex.
+__global__ void k_dense_len(uint32_t T, uint32_t vt, uint32_t hz, uint32_t hwp,
+                            uint32_t *__restrict__ len) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < T; i += gridDim.x * blockDim.x) {
+        const uint32_t v = vt + i;
+        const uint32_t ws4 = ((v + 1 - hz) >> 5) & ~3u;
+        len[i] = hwp > ws4 ? hwp - ws4 : 0u;
+    }
+}
+
+__global__ void k_excl_scan_u32(uint32_t *__restrict__ a, uint32_t n1) {
+    // in place exclusive scan of a[0..n1) (n1 <= a few 10^5), one block
+    __shared__ uint32_t s_w[32];
+    uint32_t carry = 0;
+    for (uint32_t b = 0; b < n1; b += blockDim.x) {
+        const uint32_t i = b + threadIdx.x;
+        const uint32_t x = i < n1 ? a[i] : 0u;
+        uint32_t t;
+        const uint32_t e = block_exclusive_scan<uint32_t>(x, s_w, &t);
+        if (i < n1) a[i] = carry + e;
+        carry += t;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_dense_fill(const uint32_t *__restrict__ src,
+                                                    const uint32_t *__restrict__ dst, uint64_t p0,
+                                                    uint64_t m, uint32_t vt, uint32_t hz,
+                                                    const uint32_t *__restrict__ dense_off,
+                                                    uint32_t *__restrict__ bits) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t p = p0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += stride) {
+        const uint32_t v = src[p], r = dst[p] - hz;
+        const uint32_t ws4 = ((v + 1 - hz) >> 5) & ~3u;
+        atomicOr(bits + dense_off[v - vt] + (r >> 5) - ws4, 1u << (r & 31));
+    }
+}
+
 }  // namespace
 
 int graph_alloc(DeviceGraph *g, uint64_t m, uint64_t n, cudaStream_t s) {
@@ -400,6 +438,9 @@ void graph_release(DeviceGraph *g, cudaStream_t s) {
     dfree(g->off, s);
     dfree(g->off32, s);
     dfree(g->hubstart, s);
+    dfree(g->dense_off, s);
+    dfree(g->dense_bits, s);
+    g->dense_off = g->dense_bits = nullptr;
     g->src = g->dst = nullptr;
     g->off = nullptr;
     g->off32 = nullptr;
@@ -649,6 +690,35 @@ int build_hubstart_dev(DeviceGraph *g, cudaStream_t s) {
         TC_LAUNCHED();
     }
     g->rank_space = true;
+    // dense-hub bitmaps of the top kDenseRanks vertices
+    const uint32_t hub_n = (uint32_t)(g->n - g->hz);
+    g->hwp = ((hub_n + 31) / 32 + 3) & ~3u;
+    const uint32_t T = hub_n < kDenseRanks ? hub_n : kDenseRanks;
+    g->vt = (uint32_t)g->n - T;
+    dfree(g->dense_off, s);
+    dfree(g->dense_bits, s);
+    g->dense_off = g->dense_bits = nullptr;
+    TC_CHECK(dalloc_t(&g->dense_off, (size_t)T + 1, s));
+    uint32_t words = 0;
+    if (T) {
+        k_dense_len<<<grid_for(T, 256, kSMs * 4), 256, 0, s>>>(T, g->vt, g->hz, g->hwp, g->dense_off);
+        TC_LAUNCHED();
+        TC_CUDA(cudaMemsetAsync(g->dense_off + T, 0, sizeof(uint32_t), s));
+        k_excl_scan_u32<<<1, 1024 - 32, 0, s>>>(g->dense_off, T + 1);
+        TC_LAUNCHED();
+        TC_CUDA(cudaMemcpyAsync(&words, g->dense_off + T, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        uint32_t p0 = 0;
+        TC_CUDA(cudaMemcpyAsync(&p0, g->off32 + g->vt, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        TC_CUDA(cudaStreamSynchronize(s));
+        TC_CHECK(dalloc_t(&g->dense_bits, (size_t)words + 4, s));
+        g->dense_words = words + 4;
+        TC_CUDA(cudaMemsetAsync(g->dense_bits, 0, ((size_t)words + 4) * sizeof(uint32_t), s));
+        if (g->m > p0) {
+            k_dense_fill<<<grid_for(g->m - p0, 256, kSMs * 16), 256, 0, s>>>(
+                g->src, g->dst, p0, g->m, g->vt, g->hz, g->dense_off, g->dense_bits);
+            TC_LAUNCHED();
+        }
+    }
     return 0;
 }
 
