@@ -121,6 +121,9 @@ int tc_l2_flush(void); /* write a buffer larger than L2 (timing hygiene) */
 int tc_timer_record(int slot);
 int tc_timer_elapsed(int slot_a, int slot_b, double *ms);
 int tc_launch_count(uint64_t *out);
+/* keep >= bytes reserved in the library's device memory pool (called automatically by
+ * tc_preprocess* / tc_count_with_timings with an estimate of their scratch) */
+int tc_reserve(uint64_t bytes);
 
 #ifdef __cplusplus
 }

@@ -91,6 +91,7 @@ _SIGS = {
     "tc_timer_record": ([ctypes.c_int], ctypes.c_int),
     "tc_timer_elapsed": ([ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "tc_launch_count": ([_u64p], ctypes.c_int),
+    "tc_reserve": ([ctypes.c_uint64], ctypes.c_int),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -24,6 +24,7 @@ std::mutex g_mu;
 bool g_ready = false;
 int g_device = 0;
 cudaStream_t g_stream = nullptr;
+cudaMemPool_t g_scratch = nullptr;
 void *g_flush = nullptr;
 size_t g_flush_bytes = 0;
 unsigned long long *g_total = nullptr;  // device u64 accumulator for counts
@@ -33,6 +34,7 @@ std::atomic<unsigned long long> g_launches{0};
 cudaEvent_t g_timer[8] = {nullptr};
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+cudaMemPool_t scratch_pool() { return g_scratch; }
 void set_error(const std::string &msg) { g_err = msg; }
 const char *last_error() { return g_err.c_str(); }
 
@@ -64,6 +66,12 @@ static int ensure_init(int device) {
     TC_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t keep = ~0ull;
     TC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    TC_CUDA(cudaMemPoolCreate(&g_scratch, &props));
+    TC_CUDA(cudaMemPoolSetAttribute(g_scratch, cudaMemPoolAttrReleaseThreshold, &keep));
     TC_CUDA(cudaMalloc(&g_total, sizeof(unsigned long long)));
     g_device = device;
     g_ready = true;
@@ -71,6 +79,33 @@ static int ensure_init(int device) {
 }
 
 static int ensure() { return ensure_init(g_device); }
+
+// Keep at least `bytes` of device memory reserved in the stream-ordered pool: one large
+// allocation is made and freed, so later calls sub-allocate from mapped memory instead of
+// mapping new chunks (which showed up as 100+ ms gaps under fragmentation).
+static int reserve_pool(uint64_t bytes) {
+    cudaMemPool_t pool = g_scratch;
+    uint64_t reserved = 0, used = 0;
+    TC_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+    TC_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+    if (reserved - used >= bytes) return 0;
+    size_t free_b = 0, total_b = 0;
+    TC_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    uint64_t want = bytes - (reserved - used);
+    if (want > (uint64_t)free_b * 9 / 10) want = (uint64_t)free_b * 9 / 10;
+    if (want < (64ull << 20)) return 0;
+    void *p = nullptr;
+    if (cudaMallocFromPoolAsync(&p, want, pool, g_stream) != cudaSuccess) {
+        cudaGetLastError();  // best effort: not fatal
+        return 0;
+    }
+    TC_CUDA(cudaFreeAsync(p, g_stream));
+    TC_CUDA(cudaStreamSynchronize(g_stream));
+    return 0;
+}
+
+// Peak scratch of preprocess + count, ~14 B per input pair at R-MAT s26.
+static uint64_t scratch_estimate(uint64_t npairs) { return 16ull * npairs + (256ull << 20); }
 
 static double ms_between(cudaEvent_t a, cudaEvent_t b) {
     float ms = 0;
@@ -101,6 +136,7 @@ static int rank_copy(tc_graph *h, const DeviceGraph **out) {
     if (h->g.rank_space || h->g.m >= (1ull << 32)) return 0;
     if (!h->rank) {
         DeviceGraph *r = new DeviceGraph();
+        r->persistent = true;
         int rc = relabel_dev(h->g, r, g_stream);
         if (rc) {
             graph_release(r, g_stream);
@@ -182,6 +218,8 @@ int tc_shutdown(void) {
     g_flush_bytes = 0;
     cudaFree(g_total);
     g_total = nullptr;
+    if (g_scratch) cudaMemPoolDestroy(g_scratch);
+    g_scratch = nullptr;
     cudaStreamDestroy(g_stream);
     g_stream = nullptr;
     g_ready = false;
@@ -196,6 +234,7 @@ int tc_preprocess(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, int p
 int tc_preprocess_ex(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, int pairs_on_device,
                      int flags, tc_graph **out, tc_times *t) {
     TC_CHECK(ensure());
+    TC_CHECK(reserve_pool(scratch_estimate(npairs) + (pairs_on_device ? 0 : 8 * npairs)));
     if (!out) {
         set_error("null output handle");
         return -1;
@@ -213,6 +252,7 @@ int tc_preprocess_ex(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, in
     }
     TC_CUDA(cudaEventRecord(ev.e[1], s));
     tc_graph *g = new tc_graph();
+    g->g.persistent = true;
     int rc = (flags & TC_PREPROCESS_RANK_SPACE) ? preprocess_rank_dev(dpairs, npairs, nverts, &g->g, s)
                                                : preprocess_dev(dpairs, npairs, nverts, &g->g, s);
     if (owned) dfree(owned, s);
@@ -242,6 +282,7 @@ int tc_graph_upload(const uint32_t *edge_src, const uint32_t *edge_dst,
         return -1;
     }
     tc_graph *g = new tc_graph();
+    g->g.persistent = true;
     int rc = graph_alloc(&g->g, m, n, s);
     if (rc) {
         delete g;
@@ -288,6 +329,7 @@ int tc_graph_create(uint64_t m, uint64_t n, int flags, tc_graph **out) {
         return -1;
     }
     tc_graph *g = new tc_graph();
+    g->g.persistent = true;
     int rc = graph_alloc(&g->g, m, n, g_stream);
     if (rc) {
         delete g;
@@ -409,6 +451,7 @@ int tc_intersect_count(const tc_graph *g, uint32_t u, uint32_t v, uint64_t *out)
 int tc_count_with_timings(const uint32_t *pairs, uint64_t npairs, uint64_t nverts,
                           int pairs_on_device, int algo, uint64_t *out, tc_times *t) {
     TC_CHECK(ensure());
+    TC_CHECK(reserve_pool(scratch_estimate(npairs) + (pairs_on_device ? 0 : 8 * npairs)));
     cudaStream_t s = g_stream;
     Events ev;
     TC_CHECK(ev.create());
@@ -586,6 +629,11 @@ int tc_synchronize(void) {
     TC_CHECK(ensure());
     TC_CUDA(cudaStreamSynchronize(g_stream));
     return 0;
+}
+
+int tc_reserve(uint64_t bytes) {
+    TC_CHECK(ensure());
+    return reserve_pool(bytes);
 }
 
 int tc_launch_count(uint64_t *out) {

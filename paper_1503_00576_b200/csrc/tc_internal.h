@@ -37,14 +37,17 @@ void note_launch();
     } while (0)
 
 // ------------------------------------------------------------------ memory ---
-// Stream-ordered allocations from the device's default memory pool (release
-// threshold raised to "keep everything", so repeated calls reuse the same HBM).
-int dalloc(void **p, size_t bytes, cudaStream_t s);
+// Stream-ordered allocations.  Per-call scratch comes from a dedicated pool (release
+// threshold "keep everything"), so the same-sized temporaries of repeated calls are
+// reused without remapping; graphs handed to the caller (persistent) come from the
+// device's default pool, so they never fragment the scratch pool.
+int dalloc(void **p, size_t bytes, cudaStream_t s, bool persistent = false);
 void dfree(void *p, cudaStream_t s);
+cudaMemPool_t scratch_pool();
 
 template <typename T>
-int dalloc_t(T **p, size_t count, cudaStream_t s) {
-    return dalloc(reinterpret_cast<void **>(p), count * sizeof(T), s);
+int dalloc_t(T **p, size_t count, cudaStream_t s, bool persistent = false) {
+    return dalloc(reinterpret_cast<void **>(p), count * sizeof(T), s, persistent);
 }
 
 // ------------------------------------------------------------- radix sort ---
@@ -107,10 +110,11 @@ struct DeviceGraph {
     uint32_t vt = 0, hwp = 0, dense_words = 0;
     uint32_t *dense_off = nullptr;   // [n - vt + 1] word offsets (multiples of 4)
     uint32_t *dense_bits = nullptr;
+    bool persistent = false;  // arrays from the default pool (outlive the call)
 };
 
 constexpr uint32_t kHubRanks = 1u << 18;    // hub zone size: 32 KB shared-memory bitmap
-constexpr uint32_t kDenseRanks = 1u << 15;  // dense-hub bitmaps: 64 MB at R-MAT s26
+constexpr uint32_t kDenseRanks = 1u << 17;  // dense-hub bitmaps: 1 GB at R-MAT s26
 
 int graph_alloc(DeviceGraph *g, uint64_t m, uint64_t n, cudaStream_t s);
 void graph_release(DeviceGraph *g, cudaStream_t s);

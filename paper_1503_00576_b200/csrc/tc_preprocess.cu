@@ -6,15 +6,18 @@
 // which yields the bit-identical OrientedGraph: orientation is a per-pair predicate, so
 // filtering before sorting selects the same set, and sorting the survivors gives the
 // order the reference's order-preserving compaction of a sorted list gives.
+#include <stdlib.h>
+
 #include "tc_common.cuh"
 #include "tc_internal.h"
 
 namespace tc {
 
-int dalloc(void **p, size_t bytes, cudaStream_t s) {
+int dalloc(void **p, size_t bytes, cudaStream_t s, bool persistent) {
     *p = nullptr;
     if (bytes == 0) bytes = 16;
-    cudaError_t e = cudaMallocAsync(p, bytes, s);
+    cudaMemPool_t pool = persistent ? nullptr : scratch_pool();
+    cudaError_t e = pool ? cudaMallocFromPoolAsync(p, bytes, pool, s) : cudaMallocAsync(p, bytes, s);
     if (e != cudaSuccess) {
         set_error(std::string("device allocation of ") + std::to_string(bytes) +
                   " bytes failed: " + cudaGetErrorString(e));
@@ -423,11 +426,12 @@ __global__ void __launch_bounds__(256) k_dense_fill(const uint32_t *__restrict__
 int graph_alloc(DeviceGraph *g, uint64_t m, uint64_t n, cudaStream_t s) {
     g->m = m;
     g->n = n;
-    TC_CHECK(dalloc_t(&g->src, m + 4, s));
-    TC_CHECK(dalloc_t(&g->dst, m + 4, s));  // +16 B so 128-bit tail loads stay in bounds
-    TC_CHECK(dalloc_t(&g->off, n + 1, s));
+    const bool ps = g->persistent;
+    TC_CHECK(dalloc_t(&g->src, m + 4, s, ps));
+    TC_CHECK(dalloc_t(&g->dst, m + 4, s, ps));  // +16 B so 128-bit tail loads stay in bounds
+    TC_CHECK(dalloc_t(&g->off, n + 1, s, ps));
     g->off32 = nullptr;
-    if (m < (1ull << 32)) TC_CHECK(dalloc_t(&g->off32, n + 1, s));
+    if (m < (1ull << 32)) TC_CHECK(dalloc_t(&g->off32, n + 1, s, ps));
     TC_CUDA(cudaGetDevice(&g->device));
     return 0;
 }
@@ -679,7 +683,7 @@ int build_hubstart_dev(DeviceGraph *g, cudaStream_t s) {
         return -1;
     }
     g->hz = g->n > kHubRanks ? (uint32_t)(g->n - kHubRanks) : 0u;
-    if (!g->hubstart) TC_CHECK(dalloc_t(&g->hubstart, g->n ? g->n : 1, s));
+    if (!g->hubstart) TC_CHECK(dalloc_t(&g->hubstart, g->n ? g->n : 1, s, g->persistent));
     if (g->n) {
         k_hub_init<<<grid_for(g->n, 256, kSMs * 16), 256, 0, s>>>(g->off32, g->n, g->hubstart);
         TC_LAUNCHED();
@@ -693,12 +697,14 @@ int build_hubstart_dev(DeviceGraph *g, cudaStream_t s) {
     // dense-hub bitmaps of the top kDenseRanks vertices
     const uint32_t hub_n = (uint32_t)(g->n - g->hz);
     g->hwp = ((hub_n + 31) / 32 + 3) & ~3u;
-    const uint32_t T = hub_n < kDenseRanks ? hub_n : kDenseRanks;
+    static const uint32_t dense_ranks =
+        getenv("TC_DENSE_RANKS") ? (uint32_t)atoi(getenv("TC_DENSE_RANKS")) : kDenseRanks;
+    const uint32_t T = hub_n < dense_ranks ? hub_n : dense_ranks;
     g->vt = (uint32_t)g->n - T;
     dfree(g->dense_off, s);
     dfree(g->dense_bits, s);
     g->dense_off = g->dense_bits = nullptr;
-    TC_CHECK(dalloc_t(&g->dense_off, (size_t)T + 1, s));
+    TC_CHECK(dalloc_t(&g->dense_off, (size_t)T + 1, s, g->persistent));
     uint32_t words = 0;
     if (T) {
         k_dense_len<<<grid_for(T, 256, kSMs * 4), 256, 0, s>>>(T, g->vt, g->hz, g->hwp, g->dense_off);
@@ -710,7 +716,7 @@ int build_hubstart_dev(DeviceGraph *g, cudaStream_t s) {
         uint32_t p0 = 0;
         TC_CUDA(cudaMemcpyAsync(&p0, g->off32 + g->vt, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
         TC_CUDA(cudaStreamSynchronize(s));
-        TC_CHECK(dalloc_t(&g->dense_bits, (size_t)words + 4, s));
+        TC_CHECK(dalloc_t(&g->dense_bits, (size_t)words + 4, s, g->persistent));
         g->dense_words = words + 4;
         TC_CUDA(cudaMemsetAsync(g->dense_bits, 0, ((size_t)words + 4) * sizeof(uint32_t), s));
         if (g->m > p0) {
