@@ -234,7 +234,7 @@ int tc_preprocess(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, int p
 int tc_preprocess_ex(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, int pairs_on_device,
                      int flags, tc_graph **out, tc_times *t) {
     TC_CHECK(ensure());
-    TC_CHECK(reserve_pool(scratch_estimate(npairs) + (pairs_on_device ? 0 : 8 * npairs)));
+    TC_CHECK(reserve_pool(scratch_estimate(npairs)));
     if (!out) {
         set_error("null output handle");
         return -1;
@@ -244,9 +244,9 @@ int tc_preprocess_ex(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, in
     TC_CHECK(ev.create());
     TC_CUDA(cudaEventRecord(ev.e[0], s));
     const uint32_t *dpairs = pairs;
-    uint32_t *owned = nullptr;
+    uint32_t *owned = nullptr;  // staging copy: default pool, freed at the end of the call
     if (!pairs_on_device && npairs) {
-        TC_CHECK(dalloc_t(&owned, 2 * npairs, s));
+        TC_CHECK(dalloc_t(&owned, 2 * npairs, s, true));
         TC_CUDA(cudaMemcpyAsync(owned, pairs, npairs * 8, cudaMemcpyHostToDevice, s));
         dpairs = owned;
     }
@@ -451,15 +451,15 @@ int tc_intersect_count(const tc_graph *g, uint32_t u, uint32_t v, uint64_t *out)
 int tc_count_with_timings(const uint32_t *pairs, uint64_t npairs, uint64_t nverts,
                           int pairs_on_device, int algo, uint64_t *out, tc_times *t) {
     TC_CHECK(ensure());
-    TC_CHECK(reserve_pool(scratch_estimate(npairs) + (pairs_on_device ? 0 : 8 * npairs)));
+    TC_CHECK(reserve_pool(scratch_estimate(npairs)));
     cudaStream_t s = g_stream;
     Events ev;
     TC_CHECK(ev.create());
     TC_CUDA(cudaEventRecord(ev.e[0], s));
     const uint32_t *dpairs = pairs;
-    uint32_t *owned = nullptr;
+    uint32_t *owned = nullptr;  // staging copy: default pool, freed at the end of the call
     if (!pairs_on_device && npairs) {
-        TC_CHECK(dalloc_t(&owned, 2 * npairs, s));
+        TC_CHECK(dalloc_t(&owned, 2 * npairs, s, true));
         TC_CUDA(cudaMemcpyAsync(owned, pairs, npairs * 8, cudaMemcpyHostToDevice, s));
         dpairs = owned;
     }
@@ -468,8 +468,8 @@ int tc_count_with_timings(const uint32_t *pairs, uint64_t npairs, uint64_t nvert
     const bool rank = algo == TC_ALGO_AUTO && npairs / 2 < (1ull << 32) && nverts < (1ull << 32);
     int rc = rank ? preprocess_rank_dev(dpairs, npairs, nverts, &g, s)
                   : preprocess_dev(dpairs, npairs, nverts, &g, s);
-    if (owned) dfree(owned, s);
     if (rc) {
+        if (owned) dfree(owned, s);
         graph_release(&g, s);
         return rc;
     }
@@ -478,6 +478,7 @@ int tc_count_with_timings(const uint32_t *pairs, uint64_t npairs, uint64_t nvert
     CountStats st;
     rc = count_range_dev(g, 0, g.m, algo, g_total, s, nullptr);
     if (rc) {
+        if (owned) dfree(owned, s);
         graph_release(&g, s);
         return rc;
     }
@@ -485,6 +486,7 @@ int tc_count_with_timings(const uint32_t *pairs, uint64_t npairs, uint64_t nvert
     TC_CUDA(cudaMemcpyAsync(&h, g_total, sizeof(h), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaEventRecord(ev.e[3], s));
     graph_release(&g, s);
+    if (owned) dfree(owned, s);
     TC_CUDA(cudaEventSynchronize(ev.e[3]));
     *out = h;
     if (t) {
@@ -579,7 +581,7 @@ int tc_gen_rmat(int scale, int edge_factor, const double probs[4], const uint64_
 
 int tc_device_alloc(uint64_t bytes, void **p) {
     TC_CHECK(ensure());
-    TC_CHECK(dalloc(p, bytes, g_stream));
+    TC_CHECK(dalloc(p, bytes, g_stream, true));
     TC_CUDA(cudaStreamSynchronize(g_stream));
     return 0;
 }

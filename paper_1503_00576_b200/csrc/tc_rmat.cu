@@ -340,7 +340,7 @@ int rmat_dev(int scale, int edge_factor, const double probs[4], const uint64_t s
     TC_LAUNCHED();
     dfree(have, s);
     TC_CHECK(dalloc_t(&balt, 2 * target, s));
-    TC_CHECK(dalloc_t(&pairs, 4 * target + 4, s));
+    TC_CHECK(dalloc_t(&pairs, 4 * target + 4, s, true));  // handed to the caller
     TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
     TC_CHECK(radix_histogram(both, 2 * target, have_plan, hist, s));
     TC_CHECK(radix_sort(both, balt, nullptr, nullptr, 2 * target, have_plan, hist, kOutAoS, pairs,
