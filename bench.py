@@ -265,8 +265,11 @@ def main():
     alg_bytes = 4 * W + 40 * m
     peak, peak_src = measured_peak()
     achieved = alg_bytes / (count_ms / 1e3) / 1e9
+    traffic = traffic_from_profiles(workload)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic_from_profiles(workload),
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "traffic_gbs": round(traffic / (count_ms / 1e3) / 1e9, 1) if traffic else None,
+                "traffic_frac": round(traffic / (count_ms / 1e3) / 1e9 / peak, 4) if traffic else None,
                 "kernel": "count phase (k_count_heavy + k_count_window + k_classify)",
                 "algorithmic_bytes_per_launch": alg_bytes, "launch_ms": round(count_ms, 3),
                 "peak_source": peak_src}
