@@ -107,6 +107,11 @@ int tc_orient_and_compact(const uint32_t *pairs, uint64_t npairs, const int64_t 
 int tc_gen_rmat(int scale, int edge_factor, const double probs[4], const uint64_t state[2],
                 const uint64_t inc[2], uint32_t **dev_pairs, uint64_t *npairs, uint64_t *nverts);
 
+/* ---- generators.py:287-322 barabasi_albert (bit-identical; host sampling loop, device
+ * symmetrisation).  Device pairs (free with tc_device_free) and num_vertices.          */
+int tc_gen_ba(uint64_t n, uint32_t m_attach, const uint64_t state[2], const uint64_t inc[2],
+              uint32_t **dev_pairs, uint64_t *npairs, uint64_t *nverts);
+
 /* ---- memory helpers (bench / host integration) --------------------------------------- */
 int tc_device_alloc(uint64_t bytes, void **p);
 int tc_device_free(void *p);

@@ -22,6 +22,7 @@
  *   or_count_triangles    count.py:162-178 count_triangles (W strided workers + sum)
  *   or_count_partitioned  count.py:181-204 count_partitioned (P pools x W workers)
  *   or_rmat_*             generators.py:203-284 rmat (PCG64 stream restated, see below)
+ *   or_ba_pairs           generators.py:287-322 barabasi_albert (numpy integers() restated)
  *
  * Parity of this restatement is pinned by tests/test_oracle.py against golden vectors
  * produced by the reference package itself (tests/golden/make_golden.py).
@@ -309,4 +310,80 @@ void or_rmat_levels(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint6
             }
         }
     }
+}
+
+/* ------------------------------------------------------------------ BA ---- */
+/*
+ * generators.py:287-322 barabasi_albert(n, m_attach, seed): preferential attachment from
+ * K_{m_attach}.  Draws use numpy Generator.integers(0, len(repeated), size=k), i.e.
+ * Lemire's bounded method on PCG64's buffered 32-bit outputs (low half of a 64-bit draw
+ * first, the high half on the next call).  Writes the canonical (t, new) pairs in the
+ * reference's append order; returns the pair count or -1 on allocation failure.
+ */
+typedef struct {
+    u128 s, inc;
+    int has;
+    uint32_t buf;
+} or_pcg;
+
+static uint32_t or_next32(or_pcg *g) {
+    if (g->has) { g->has = 0; return g->buf; }
+    g->s = g->s * PCG_MULT + g->inc;
+    uint64_t v = pcg_output(g->s);
+    g->has = 1;
+    g->buf = (uint32_t)(v >> 32);
+    return (uint32_t)v;
+}
+
+static uint32_t or_bounded(or_pcg *g, uint32_t high) {  /* integers(0, high), high >= 1 */
+    uint32_t rng = high - 1;
+    if (rng == 0) return 0;
+    uint32_t excl = rng + 1;
+    uint64_t m = (uint64_t)or_next32(g) * excl;
+    uint32_t left = (uint32_t)m;
+    if (left < excl) {
+        uint32_t thr = (0xFFFFFFFFu - rng) % excl;
+        while (left < thr) {
+            m = (uint64_t)or_next32(g) * excl;
+            left = (uint32_t)m;
+        }
+    }
+    return (uint32_t)(m >> 32);
+}
+
+int64_t or_ba_pairs(uint64_t n, uint32_t m_attach, uint64_t state_hi, uint64_t state_lo,
+                    uint64_t inc_hi, uint64_t inc_lo, uint32_t *pairs_out) {
+    or_pcg g = {((u128)state_hi << 64) | state_lo, ((u128)inc_hi << 64) | inc_lo, 0, 0};
+    uint64_t np = 0;
+    uint64_t cap_rep = 2 * ((uint64_t)m_attach * m_attach + (n - m_attach) * (uint64_t)m_attach) + 2;
+    uint32_t *rep = (uint32_t *)malloc(cap_rep * sizeof(uint32_t));
+    if (!rep) return -1;
+    uint64_t nrep = 0;
+    for (uint32_t i = 0; i < m_attach; ++i)
+        for (uint32_t j = i + 1; j < m_attach; ++j) {
+            pairs_out[2 * np] = i; pairs_out[2 * np + 1] = j; ++np;
+            rep[nrep++] = i; rep[nrep++] = j;
+        }
+    uint32_t tg[64];
+    for (uint64_t v = m_attach; v < n; ++v) {
+        uint32_t nt = 0;
+        if (nrep == 0) tg[nt++] = or_bounded(&g, (uint32_t)v);
+        while (nt < m_attach) {
+            uint32_t k = m_attach - nt, draws[64];
+            for (uint32_t d = 0; d < k; ++d) draws[d] = or_bounded(&g, (uint32_t)nrep);
+            for (uint32_t d = 0; d < k; ++d) {
+                uint32_t t = rep[draws[d]], seen = 0;
+                for (uint32_t q = 0; q < nt; ++q) seen |= tg[q] == t;
+                if (!seen) tg[nt++] = t;
+            }
+        }
+        for (uint32_t a = 1; a < nt; ++a)  /* sorted(targets) */
+            for (uint32_t b = a; b > 0 && tg[b - 1] > tg[b]; --b) { uint32_t x = tg[b]; tg[b] = tg[b - 1]; tg[b - 1] = x; }
+        for (uint32_t q = 0; q < nt; ++q) {
+            pairs_out[2 * np] = tg[q]; pairs_out[2 * np + 1] = (uint32_t)v; ++np;
+            rep[nrep++] = tg[q]; rep[nrep++] = (uint32_t)v;
+        }
+    }
+    free(rep);
+    return (int64_t)np;
 }

@@ -79,6 +79,8 @@ _SIGS = {
                               ctypes.c_int),
     "tc_gen_rmat": ([ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double), _u64p, _u64p,
                      ctypes.POINTER(_vp), _u64p, _u64p], ctypes.c_int),
+    "tc_gen_ba": ([ctypes.c_uint64, ctypes.c_uint32, _u64p, _u64p, ctypes.POINTER(_vp), _u64p, _u64p],
+                  ctypes.c_int),
     "tc_device_alloc": ([ctypes.c_uint64, ctypes.POINTER(_vp)], ctypes.c_int),
     "tc_device_free": ([_vp], ctypes.c_int),
     "tc_memcpy": ([_vp, _vp, ctypes.c_uint64, ctypes.c_int], ctypes.c_int),

@@ -579,6 +579,13 @@ int tc_gen_rmat(int scale, int edge_factor, const double probs[4], const uint64_
     return 0;
 }
 
+int tc_gen_ba(uint64_t n, uint32_t m_attach, const uint64_t state[2], const uint64_t inc[2],
+              uint32_t **dev_pairs, uint64_t *npairs, uint64_t *nverts) {
+    TC_CHECK(ensure());
+    TC_CHECK(ba_dev(n, m_attach, state, inc, dev_pairs, npairs, nverts, g_stream));
+    return 0;
+}
+
 int tc_device_alloc(uint64_t bytes, void **p) {
     TC_CHECK(ensure());
     TC_CHECK(dalloc(p, bytes, g_stream, true));

@@ -162,5 +162,7 @@ int merge_work_dev(const DeviceGraph &g, uint64_t *out, cudaStream_t s);
 int rmat_dev(int scale, int edge_factor, const double probs[4], const uint64_t state[2],
              const uint64_t inc[2], uint32_t **pairs_out, uint64_t *npairs_out,
              uint64_t *nverts_out, cudaStream_t s);
+int ba_dev(uint64_t n, uint32_t m_attach, const uint64_t state[2], const uint64_t inc[2],
+           uint32_t **pairs_out, uint64_t *npairs_out, uint64_t *nverts_out, cudaStream_t s);
 
 }  // namespace tc

@@ -10,6 +10,9 @@
 // position, and "first occurrence in draw order" is recovered with a stable key/value
 // radix sort (value = draw index) plus a scan over draw positions.  Input production for
 // parity tests and the bench only; not on the timed path.
+#include <algorithm>
+#include <vector>
+
 #include "tc_common.cuh"
 #include "tc_internal.h"
 
@@ -356,6 +359,136 @@ int rmat_dev(int scale, int edge_factor, const double probs[4], const uint64_t s
     *pairs_out = pairs;
     *npairs_out = 2 * target;
     *nverts_out = (uint64_t)mh + 1;
+    return 0;
+}
+
+// --------------------------------------------------------------------- BA ---
+// Reference generators.py:287-322 barabasi_albert: inherently sequential (each new
+// vertex samples targets from the degree-weighted list built so far), so the sampling
+// loop runs on the host -- numpy's Generator.integers restated: Lemire's bounded method
+// on PCG64's buffered 32-bit outputs -- and only the symmetrisation + sort runs on the
+// device.  Input production only.
+namespace {
+
+struct HostPcg {
+    u128 s, inc;
+    bool has = false;
+    uint32_t buf = 0;
+    uint32_t next32() {
+        if (has) {
+            has = false;
+            return buf;
+        }
+        s = s * kPcgMult + inc;
+        const uint64_t hi = (uint64_t)(s >> 64), lo = (uint64_t)s;
+        const unsigned rot = (unsigned)(s >> 122);
+        const uint64_t x = hi ^ lo;
+        const uint64_t v = (x >> rot) | (x << ((64 - rot) & 63));
+        has = true;
+        buf = (uint32_t)(v >> 32);
+        return (uint32_t)v;
+    }
+    uint32_t bounded(uint32_t high) {  // integers(0, high)
+        const uint32_t rng = high - 1;
+        if (rng == 0) return 0;
+        const uint32_t excl = rng + 1;
+        uint64_t m = (uint64_t)next32() * excl;
+        uint32_t left = (uint32_t)m;
+        if (left < excl) {
+            const uint32_t thr = (0xFFFFFFFFu - rng) % excl;
+            while (left < thr) {
+                m = (uint64_t)next32() * excl;
+                left = (uint32_t)m;
+            }
+        }
+        return (uint32_t)(m >> 32);
+    }
+};
+
+__global__ void k_sym_pairs(const uint2 *__restrict__ pairs, uint64_t np, int vb,
+                            uint64_t *__restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += stride) {
+        const uint2 p = pairs[i];
+        out[2 * i] = ((uint64_t)p.x << vb) | p.y;
+        out[2 * i + 1] = ((uint64_t)p.y << vb) | p.x;
+    }
+}
+
+}  // namespace
+
+int ba_dev(uint64_t n, uint32_t m_attach, const uint64_t state[2], const uint64_t inc[2],
+           uint32_t **pairs_out, uint64_t *npairs_out, uint64_t *nverts_out, cudaStream_t s) {
+    if (n < 2 || m_attach < 1 || m_attach >= n || m_attach > 1024 || n >= (1ull << 32)) {
+        set_error("barabasi_albert: need 2 <= n < 2^32 and 1 <= m_attach < min(n, 1024)");
+        return -1;
+    }
+    HostPcg g;
+    g.s = ((u128)state[0] << 64) | state[1];
+    g.inc = ((u128)inc[0] << 64) | inc[1];
+    const uint64_t count = (uint64_t)m_attach * (m_attach - 1) / 2 + (n - m_attach) * (uint64_t)m_attach;
+    uint32_t *hp = nullptr;
+    TC_CUDA(cudaHostAlloc(&hp, 8 * (count ? count : 1), cudaHostAllocDefault));
+    std::vector<uint32_t> rep;
+    rep.reserve(2 * count + 2);
+    uint64_t np = 0;
+    for (uint32_t i = 0; i < m_attach; ++i)
+        for (uint32_t j = i + 1; j < m_attach; ++j) {
+            hp[2 * np] = i;
+            hp[2 * np + 1] = j;
+            ++np;
+            rep.push_back(i);
+            rep.push_back(j);
+        }
+    std::vector<uint32_t> tg, draws;
+    for (uint64_t v = m_attach; v < n; ++v) {
+        tg.clear();
+        if (rep.empty()) tg.push_back(g.bounded((uint32_t)v));
+        while (tg.size() < m_attach) {
+            const uint32_t k = m_attach - (uint32_t)tg.size();
+            draws.resize(k);
+            for (uint32_t d = 0; d < k; ++d) draws[d] = g.bounded((uint32_t)rep.size());
+            for (uint32_t d = 0; d < k; ++d) {
+                const uint32_t t = rep[draws[d]];
+                if (std::find(tg.begin(), tg.end(), t) == tg.end()) tg.push_back(t);
+            }
+        }
+        std::sort(tg.begin(), tg.end());
+        for (uint32_t t : tg) {
+            hp[2 * np] = t;
+            hp[2 * np + 1] = (uint32_t)v;
+            ++np;
+            rep.push_back(t);
+            rep.push_back((uint32_t)v);
+        }
+    }
+    // edge_array_from_undirected (reference graph.py:265-276): both directions, sorted
+    const int vb = bits_for(n - 1);
+    const RadixPlan plan = make_radix_plan(2 * vb);
+    uint32_t *dcanon = nullptr, *pairs = nullptr, *hist = nullptr;
+    uint64_t *keys = nullptr, *alt = nullptr;
+    TC_CHECK(dalloc_t(&dcanon, 2 * np, s));
+    TC_CHECK(dalloc_t(&keys, 2 * np, s));
+    TC_CHECK(dalloc_t(&alt, 2 * np, s));
+    TC_CHECK(dalloc_t(&hist, kMaxPasses * kRadix, s));
+    TC_CHECK(dalloc_t(&pairs, 4 * np + 4, s, true));  // handed to the caller
+    TC_CUDA(cudaMemcpyAsync(dcanon, hp, 8 * np, cudaMemcpyHostToDevice, s));
+    TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+    k_sym_pairs<<<grid_for(np, 256, kSMs * 16), 256, 0, s>>>(reinterpret_cast<const uint2 *>(dcanon),
+                                                              np, vb, keys);
+    TC_LAUNCHED();
+    TC_CHECK(radix_histogram(keys, 2 * np, plan, hist, s));
+    TC_CHECK(radix_sort(keys, alt, nullptr, nullptr, 2 * np, plan, hist, kOutAoS, pairs, nullptr, vb,
+                        nullptr, nullptr, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    cudaFreeHost(hp);
+    dfree(dcanon, s);
+    dfree(keys, s);
+    dfree(alt, s);
+    dfree(hist, s);
+    *pairs_out = pairs;
+    *npairs_out = 2 * np;
+    *nverts_out = n;  // every vertex >= 1 edge (BA attaches every new vertex)
     return 0;
 }
 

@@ -101,3 +101,29 @@ def rmat(scale: int, edge_factor: int = RMAT_DEFAULT_EDGE_FACTOR, *,
         return dev.to_host(pinned=pinned)
     finally:
         dev.free()
+
+
+def barabasi_albert_device(n: int, m_attach: int, seed: int = 0) -> DeviceEdges:
+    """reference barabasi_albert(n, m_attach, seed) (generators.py:287-322), bit-identical;
+    the sampling loop is sequential by construction and runs on the host."""
+    if n < 2:
+        raise ValueError(f"n: must be >= 2, got {n}")
+    if not 1 <= m_attach < n:
+        raise ValueError(f"m_attach: must satisfy 1 <= m_attach < n, got {m_attach}")
+    (sh, sl), (ih, il) = _pcg64_words(seed)
+    state = (ctypes.c_uint64 * 2)(sh, sl)
+    inc = (ctypes.c_uint64 * 2)(ih, il)
+    p = ctypes.c_void_p()
+    npairs, nverts = ctypes.c_uint64(), ctypes.c_uint64()
+    _lib.check(_lib.lib().tc_gen_ba(int(n), int(m_attach), state, inc, ctypes.byref(p),
+                                    ctypes.byref(npairs), ctypes.byref(nverts)))
+    return DeviceEdges(p.value, npairs.value, nverts.value)
+
+
+def barabasi_albert(n: int, m_attach: int, seed: int = 0, pinned: bool = True) -> EdgeArray:
+    """Host EdgeArray of reference barabasi_albert(n, m_attach, seed)."""
+    dev = barabasi_albert_device(n, m_attach, seed)
+    try:
+        return dev.to_host(pinned=pinned)
+    finally:
+        dev.free()

@@ -170,3 +170,30 @@ def test_big_rmat_counts(golden_big, scale):
     og, _ = tcb.preprocess_device(g)
     assert sha(*_csr(og)) == rec["csr_sha256"]
     assert tcb.count_triangles(og) == rec["triangles"]
+
+
+@pytest.mark.parametrize("name", ["ba_1000_3_5", "ba_100000_9_0"])
+def test_ba_generator_and_pipeline(golden, name):
+    rec = golden["graphs"][name]
+    g = generators.barabasi_albert(rec["n_param"], rec["m_attach"], seed=rec["seed"])
+    assert sha(g.edges) == rec["edges_sha256"], "device-symmetrised BA must equal reference BA"
+    og = tcb.preprocess(g)
+    assert sha(*_csr(og)) == rec["csr_sha256"]
+    _count_all_ways(og, rec["triangles"])
+    assert tcb.count_with_timings(g)[0] == rec["triangles"]
+
+
+@pytest.mark.parametrize("n", [1_000_000, 10_000_000])
+def test_big_ba(golden_big, n):
+    """BA config 3 (n = 10^7, m = 9): bit-identical input, CSR and count."""
+    rec = golden_big.get(f"ba_{n}_9_0")
+    if rec is None:
+        pytest.skip("BA golden not generated")
+    d = generators.barabasi_albert_device(n, 9, seed=0)
+    h = d.to_host()
+    assert sha(h.edges) == rec["edges_sha256"]
+    og, _ = tcb.preprocess_device(d)
+    assert sha(*_csr(og)) == rec["csr_sha256"]
+    assert tcb.count_triangles(og) == rec["triangles"]
+    assert tcb.count_with_timings_device(d)[0] == rec["triangles"]
+    assert tcb.count_device(og, algo=_lib.ALGO_MERGE_THREAD)[0] == rec["triangles"]
