@@ -110,17 +110,31 @@ void or_build_node_array(const uint32_t *firsts, uint64_t k, uint64_t n, int64_t
     }
 }
 
-/* Node array from sorted packed keys (first vertex in the high word). */
-static void node_array_from_keys(const uint64_t *keys, uint64_t k, uint64_t n, int64_t *offsets) {
-    uint64_t j = 0;
-    for (uint64_t i = 0; i <= n; ++i) {
-        while (j < k && (keys[j] >> 32) < i) ++j;
-        offsets[i] = (int64_t)j;
+/* Node array from sorted packed keys (first vertex in the high word): offs[i] = number of
+ * keys whose first vertex is < i, built in parallel from run boundaries. */
+static void node_array_from_keys(const uint64_t *keys, uint64_t k, uint64_t n, int64_t *offsets,
+                                 int nthr) {
+    if (k == 0) {
+        for (uint64_t i = 0; i <= n; ++i) offsets[i] = 0;
+        return;
+    }
+    /* vertices before the first key and after the last one */
+#pragma omp parallel for num_threads(nthr)
+    for (uint64_t i = 0; i <= (keys[0] >> 32); ++i) offsets[i] = 0;
+#pragma omp parallel for num_threads(nthr)
+    for (uint64_t i = (keys[k - 1] >> 32) + 1; i <= n; ++i) offsets[i] = (int64_t)k;
+    /* a run boundary at j (first of j-1 < i <= first of j) sets offsets[i] = j */
+#pragma omp parallel for num_threads(nthr) schedule(static)
+    for (uint64_t j = 1; j < k; ++j) {
+        uint64_t a = keys[j - 1] >> 32, b = keys[j] >> 32;
+        for (uint64_t i = a + 1; i <= b; ++i) offsets[i] = (int64_t)j;
     }
 }
 
 /* preprocess.py:74-84.  Outputs must hold npairs entries (src/dst) and n+1 (off).
- * Returns the oriented edge count through m_out. */
+ * Returns the oriented edge count through m_out.  The reference runs this phase
+ * single-threaded in numpy; the port uses all threads (order-preserving compaction by
+ * per-thread counts + prefix, so the output is identical). */
 int or_preprocess(const uint32_t *pairs, uint64_t npairs, uint64_t n, uint32_t *src,
                   uint32_t *dst, int64_t *off, uint64_t *m_out, int threads) {
     int nthr = clamp_threads(threads);
@@ -131,26 +145,47 @@ int or_preprocess(const uint32_t *pairs, uint64_t npairs, uint64_t n, uint32_t *
     }
     uint64_t *keys = (uint64_t *)malloc(npairs * sizeof(uint64_t));
     int64_t *offs_all = (int64_t *)malloc((n + 1) * sizeof(int64_t));
-    if (!keys || !offs_all) { free(keys); free(offs_all); return -1; }
-    if (or_sort_keys(pairs, npairs, keys, nthr) != 0) { free(keys); free(offs_all); return -1; }
-    node_array_from_keys(keys, npairs, n, offs_all);
+    uint64_t *cnt = (uint64_t *)calloc((size_t)nthr + 1, sizeof(uint64_t));
+    if (!keys || !offs_all || !cnt) { free(keys); free(offs_all); free(cnt); return -1; }
+    if (or_sort_keys(pairs, npairs, keys, nthr) != 0) { free(keys); free(offs_all); free(cnt); return -1; }
+    node_array_from_keys(keys, npairs, n, offs_all, nthr);
     /* degrees = np.diff(offsets_all); orient keeps (deg u, u) < (deg v, v) in sorted
      * order (preprocess.py:49-62), then unzip (preprocess.py:65-71). */
-    uint64_t m = 0;
-    for (uint64_t i = 0; i < npairs; ++i) {
-        uint32_t u = (uint32_t)(keys[i] >> 32), v = (uint32_t)keys[i];
-        int64_t du = offs_all[u + 1] - offs_all[u];
-        int64_t dv = (uint64_t)v < n ? offs_all[v + 1] - offs_all[v] : 0;
-        if (du < dv || (du == dv && u < v)) {
-            src[m] = u;
-            dst[m] = v;
-            ++m;
+#pragma omp parallel num_threads(nthr)
+    {
+        int t = omp_get_thread_num();
+        uint64_t lo = npairs * (uint64_t)t / nthr, hi = npairs * (uint64_t)(t + 1) / nthr, c = 0;
+        for (uint64_t i = lo; i < hi; ++i) {
+            uint32_t u = (uint32_t)(keys[i] >> 32), v = (uint32_t)keys[i];
+            int64_t du = offs_all[u + 1] - offs_all[u];
+            int64_t dv = (uint64_t)v < n ? offs_all[v + 1] - offs_all[v] : 0;
+            c += (du < dv || (du == dv && u < v));
+        }
+        cnt[t + 1] = c;
+#pragma omp barrier
+#pragma omp single
+        for (int q = 0; q < nthr; ++q) cnt[q + 1] += cnt[q];
+        uint64_t o = cnt[t];
+        for (uint64_t i = lo; i < hi; ++i) {
+            uint32_t u = (uint32_t)(keys[i] >> 32), v = (uint32_t)keys[i];
+            int64_t du = offs_all[u + 1] - offs_all[u];
+            int64_t dv = (uint64_t)v < n ? offs_all[v + 1] - offs_all[v] : 0;
+            if (du < dv || (du == dv && u < v)) {
+                src[o] = u;
+                dst[o] = v;
+                ++o;
+            }
         }
     }
-    or_build_node_array(src, m, n, off);
+    uint64_t m = cnt[nthr];
+    /* node array over the compacted sources (packed as keys for the shared helper) */
+#pragma omp parallel for num_threads(nthr)
+    for (uint64_t i = 0; i < m; ++i) keys[i] = (uint64_t)src[i] << 32;
+    node_array_from_keys(keys, m, n, off, nthr);
     *m_out = m;
     free(keys);
     free(offs_all);
+    free(cnt);
     return 0;
 }
 

@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(NT)
     k_count_hub(const uint32_t *__restrict__ dst, const uint32_t *__restrict__ off,
                 const uint32_t *__restrict__ hubstart, uint32_t hz, uint32_t hwords,
                 uint32_t vt, const uint32_t *__restrict__ dense_off,
-                const uint32_t *__restrict__ dense_bits,
+                const uint32_t *__restrict__ dense_bits, uint32_t dense_factor,
                 const RangeDev *__restrict__ rg, const uint2 *__restrict__ tasks,
                 const unsigned *__restrict__ ntasks, unsigned *__restrict__ next, uint32_t cap,
                 unsigned long long *__restrict__ total) {
@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(NT)
                 // than probing its items (~3.5 vs ~12 instructions per unit)
                 if (v >= vt) {
                     dws = ((v + 1 - hz) >> 5) & ~3u;
-                    dense = (hwords - dws) < 3 * (ve - vs);
+                    dense = (hwords - dws) < dense_factor * (ve - vs);
                     if (dense) dgo = __ldg(dense_off + (v - vt));
                 }
                 if (dense) vs = ve = 0;
@@ -776,8 +776,10 @@ int launch_hub(const DeviceGraph &g, const RangeDev *rg, const uint2 *tasks, con
     int per_sm = 1;
     TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, sm));
     if (per_sm < 1) per_sm = 1;
+    static const uint32_t dense_factor =
+        getenv("TC_DENSE_FACTOR") ? (uint32_t)atoi(getenv("TC_DENSE_FACTOR")) : 3u;
     kern<<<kSMs * per_sm, NT, sm, s>>>(g.dst, g.off32, g.hubstart, g.hz, hwords, g.vt, g.dense_off,
-                                       g.dense_bits, rg, tasks, ntasks, next, cap, d_total);
+                                       g.dense_bits, dense_factor, rg, tasks, ntasks, next, cap, d_total);
     TC_LAUNCHED();
     return 0;
 }

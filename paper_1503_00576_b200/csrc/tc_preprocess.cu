@@ -93,25 +93,35 @@ __global__ void __launch_bounds__(256) k_orient(const uint2 *__restrict__ pairs,
     const uint64_t per_block = (uint64_t)blockDim.x * kPP;
     for (uint64_t base = (uint64_t)blockIdx.x * per_block; base < npairs;
          base += (uint64_t)gridDim.x * per_block) {
+        // all pair loads first, then all degree/rank gathers: 2 kPP independent
+        // gathers in flight per thread (the kernel is gather-latency bound)
+        uint2 pr[kPP];
+#pragma unroll
+        for (int i = 0; i < kPP; ++i) {
+            const uint64_t idx = base + warp * 32 * kPP + i * 32 + lane;
+            pr[i] = idx < npairs ? ld_stream_u2(pairs + idx) : make_uint2(0xffffffffu, 0xffffffffu);
+        }
+        uint32_t du[kPP], dv[kPP];
+#pragma unroll
+        for (int i = 0; i < kPP; ++i) {
+            const bool ok = (uint64_t)pr[i].x < n && (uint64_t)pr[i].y < n;  // else flagged upstream
+            du[i] = __ldg(deg + (ok ? pr[i].x : 0u));
+            dv[i] = __ldg(deg + (ok ? pr[i].y : 0u));
+            if (!ok) { du[i] = 0xffffffffu; dv[i] = 0u; }  // never kept (du > dv)
+        }
         uint64_t key[kPP];
         unsigned keepmask = 0;
 #pragma unroll
         for (int i = 0; i < kPP; ++i) {
-            uint64_t idx = base + warp * 32 * kPP + i * 32 + lane;
-            if (idx < npairs) {
-                uint2 p = ld_stream_u2(pairs + idx);
-                if ((uint64_t)p.x >= n || (uint64_t)p.y >= n) continue;  // flagged by k_degree_hist
-                const uint32_t du = __ldg(deg + p.x), dv = __ldg(deg + p.y);
-                bool fwd;
-                if (RANK) {
-                    fwd = du < dv;
-                    key[i] = ((uint64_t)du << vb) | dv;
-                } else {
-                    fwd = du < dv || (du == dv && p.x < p.y);
-                    key[i] = ((uint64_t)p.x << vb) | p.y;
-                }
-                if (fwd) keepmask |= 1u << i;
+            bool fwd;
+            if (RANK) {
+                fwd = du[i] < dv[i];
+                key[i] = ((uint64_t)du[i] << vb) | dv[i];
+            } else {
+                fwd = du[i] < dv[i] || (du[i] == dv[i] && pr[i].x < pr[i].y);
+                key[i] = ((uint64_t)pr[i].x << vb) | pr[i].y;
             }
+            if (fwd) keepmask |= 1u << i;
         }
         uint32_t mine = __popc(keepmask), tot;
         uint32_t off = block_exclusive_scan<uint32_t>(mine, s_scan, &tot);

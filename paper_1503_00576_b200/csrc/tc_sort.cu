@@ -59,7 +59,7 @@ __global__ void k_digit_base(const uint32_t *__restrict__ ghist, int npass,
 }
 
 template <int MODE, bool HAS_VAL>
-__global__ void __launch_bounds__(kSortThreads)
+__global__ void __launch_bounds__(kSortThreads, 4)
     k_radix_pass(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
                  const uint32_t *__restrict__ vin, uint32_t *__restrict__ vout,
                  uint32_t *__restrict__ out_a, uint32_t *__restrict__ out_b, int split_bits,
