@@ -197,3 +197,29 @@ def test_big_ba(golden_big, n):
     assert tcb.count_triangles(og) == rec["triangles"]
     assert tcb.count_with_timings_device(d)[0] == rec["triangles"]
     assert tcb.count_device(og, algo=_lib.ALGO_MERGE_THREAD)[0] == rec["triangles"]
+
+
+def _complete_pairs(k: int) -> np.ndarray:
+    """K_k, both directions, lexicographically sorted (reference complete_graph)."""
+    iu = np.triu_indices(k, k=1)
+    a = np.stack([iu[0], iu[1]], axis=1).astype(np.uint32)
+    both = np.concatenate([a, a[:, ::-1]])
+    return both[np.lexsort((both[:, 1], both[:, 0]))]
+
+
+@pytest.mark.parametrize("k", [34, 600, 3000, 17000])
+def test_complete_graphs_every_size_class(k):
+    """Closed form C(k, 3) through every count path: the hub classes (d+ up to 16384),
+    the sorted-array class (d+ > 16384: K_17000), the window path (K_34 light part),
+    the fused rank-space path and the reference-id ranged kernels."""
+    import math
+    g = EdgeArray(_complete_pairs(k))
+    want = math.comb(k, 3)
+    assert tcb.count_with_timings(g)[0] == want
+    og = tcb.preprocess(g)
+    assert og.device().max_out == k - 1
+    assert tcb.count_triangles(og) == want
+    half = og.m_dir // 2
+    assert tcb.count_device(og, 0, half)[0] + tcb.count_device(og, half, og.m_dir)[0] == want
+    if k <= 3000:
+        assert tcb.count_device(og, algo=_lib.ALGO_MERGE_THREAD)[0] == want
