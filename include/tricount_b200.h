@@ -112,6 +112,27 @@ int tc_gen_rmat(int scale, int edge_factor, const double probs[4], const uint64_
 int tc_gen_ba(uint64_t n, uint32_t m_attach, const uint64_t state[2], const uint64_t inc[2],
               uint32_t **dev_pairs, uint64_t *npairs, uint64_t *nverts);
 
+/* ---- ingest ----------------------------------------------------- */
+/* io.py:127-152 read_binary: TRI1 file -> pinned host pairs (free with tc_host_free).
+ * Status -4 I/O error, -5 truncated (TruncatedFileError), -6 bad magic (BadMagicError). */
+int tc_read_tri1(const char *path, uint32_t **host_pairs, uint64_t *npairs);
+/* io.py:51-99 read_edge_list's parser (multi-threaded): text "u v" lines -> pinned host
+ * pairs in file order (free with tc_host_free).  Status -7 = parse error: *err_line is the
+ * 1-based line, *err_kind 1 wrong field count, 2 not an integer pair, 3 id out of u32
+ * range (ParseError).  Mode handling (strict/symmetrize/normalize) is the caller's. */
+int tc_parse_edge_list(const char *path, uint32_t **host_pairs, uint64_t *npairs,
+                       uint64_t *err_line, int *err_kind);
+/* graph.py:196-242 validate_edge_array on the device.  *code: 0 valid, 1 self-loop,
+ * 2 duplicate, 3 missing reverse, 4 vertex id >= nverts; *index: the offending input index
+ * the reference reports (first self-loop / earliest second occurrence / first pair
+ * without reverse / first out-of-range pair). */
+int tc_validate_edge_array(const uint32_t *pairs, uint64_t npairs, uint64_t nverts,
+                           int pairs_on_device, int *code, uint64_t *index);
+/* metrics.py:17-24 wedge_count: sum_v C(deg v, 2) (exact u64; approx = same in double,
+ * for the reference's 64-bit overflow check). */
+int tc_wedge_count(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, int pairs_on_device,
+                   uint64_t *out, double *approx);
+
 /* ---- memory helpers (bench / host integration) --------------------------------------- */
 int tc_device_alloc(uint64_t bytes, void **p);
 int tc_device_free(void *p);

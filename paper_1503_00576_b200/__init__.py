@@ -21,13 +21,19 @@ from .count import (
     warm_kernel,
 )
 from .graph import (
+    AsymmetricEdgeError,
     DegreeOrder,
+    DuplicateEdgeError,
     EdgeArray,
+    GraphValidationError,
     OrientedGraph,
+    SelfLoopError,
     degrees_of,
     max_out_degree_bound,
+    validate_edge_array,
     validate_oriented_graph,
 )
+from .metrics import CountOverflowError, InconsistentCountsError, transitivity, wedge_count
 from .preprocess import build_node_array, orient_and_compact, preprocess, sort_edges, unzip
 
 __version__ = "0.1.0"
@@ -38,5 +44,7 @@ __all__ = [
     "count_with_timings", "count_with_timings_device", "default_workers", "degrees_of",
     "intersect_count", "max_out_degree_bound", "merge_work", "orient_and_compact",
     "preprocess", "preprocess_device", "sort_edges", "unzip", "validate_oriented_graph",
-    "warm_kernel",
+    "warm_kernel", "AsymmetricEdgeError", "DuplicateEdgeError", "GraphValidationError",
+    "SelfLoopError", "validate_edge_array", "CountOverflowError", "InconsistentCountsError",
+    "transitivity", "wedge_count",
 ]

@@ -81,6 +81,13 @@ _SIGS = {
                      ctypes.POINTER(_vp), _u64p, _u64p], ctypes.c_int),
     "tc_gen_ba": ([ctypes.c_uint64, ctypes.c_uint32, _u64p, _u64p, ctypes.POINTER(_vp), _u64p, _u64p],
                   ctypes.c_int),
+    "tc_read_tri1": ([ctypes.c_char_p, ctypes.POINTER(_vp), _u64p], ctypes.c_int),
+    "tc_parse_edge_list": ([ctypes.c_char_p, ctypes.POINTER(_vp), _u64p, _u64p,
+                            ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "tc_validate_edge_array": ([_vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
+                                ctypes.POINTER(ctypes.c_int), _u64p], ctypes.c_int),
+    "tc_wedge_count": ([_vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, _u64p,
+                        ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "tc_device_alloc": ([ctypes.c_uint64, ctypes.POINTER(_vp)], ctypes.c_int),
     "tc_device_free": ([_vp], ctypes.c_int),
     "tc_memcpy": ([_vp, _vp, ctypes.c_uint64, ctypes.c_int], ctypes.c_int),
@@ -138,6 +145,8 @@ def _check(rc: int) -> None:
         raise ValueError(msg)
     if rc == -3:
         raise MemoryError(msg)
+    if rc == -4:
+        raise OSError(msg)
     raise TcError(msg)
 
 

@@ -586,6 +586,51 @@ int tc_gen_ba(uint64_t n, uint32_t m_attach, const uint64_t state[2], const uint
     return 0;
 }
 
+int tc_read_tri1(const char *path, uint32_t **host_pairs, uint64_t *npairs) {
+    TC_CHECK(ensure());
+    return read_tri1(path, host_pairs, npairs);
+}
+
+int tc_parse_edge_list(const char *path, uint32_t **host_pairs, uint64_t *npairs,
+                       uint64_t *err_line, int *err_kind) {
+    TC_CHECK(ensure());
+    return parse_edge_list(path, host_pairs, npairs, err_line, err_kind);
+}
+
+static int with_device_pairs(const uint32_t *pairs, uint64_t npairs, int on_device,
+                             const uint32_t **dp, uint32_t **owned) {
+    *dp = pairs;
+    *owned = nullptr;
+    if (!on_device && npairs) {
+        TC_CHECK(dalloc_t(owned, 2 * npairs, g_stream, true));
+        TC_CUDA(cudaMemcpyAsync(*owned, pairs, npairs * 8, cudaMemcpyHostToDevice, g_stream));
+        *dp = *owned;
+    }
+    return 0;
+}
+
+int tc_validate_edge_array(const uint32_t *pairs, uint64_t npairs, uint64_t nverts,
+                           int pairs_on_device, int *code, uint64_t *index) {
+    TC_CHECK(ensure());
+    const uint32_t *dp;
+    uint32_t *owned;
+    TC_CHECK(with_device_pairs(pairs, npairs, pairs_on_device, &dp, &owned));
+    const int rc = validate_pairs_dev(dp, npairs, nverts, code, index, g_stream);
+    if (owned) dfree(owned, g_stream);
+    return rc;
+}
+
+int tc_wedge_count(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, int pairs_on_device,
+                   uint64_t *out, double *approx) {
+    TC_CHECK(ensure());
+    const uint32_t *dp;
+    uint32_t *owned;
+    TC_CHECK(with_device_pairs(pairs, npairs, pairs_on_device, &dp, &owned));
+    const int rc = wedges_dev(dp, npairs, nverts, out, approx, g_stream);
+    if (owned) dfree(owned, g_stream);
+    return rc;
+}
+
 int tc_device_alloc(uint64_t bytes, void **p) {
     TC_CHECK(ensure());
     TC_CHECK(dalloc(p, bytes, g_stream, true));

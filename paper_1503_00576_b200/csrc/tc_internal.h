@@ -162,6 +162,14 @@ int merge_work_dev(const DeviceGraph &g, uint64_t *out, cudaStream_t s);
 int rmat_dev(int scale, int edge_factor, const double probs[4], const uint64_t state[2],
              const uint64_t inc[2], uint32_t **pairs_out, uint64_t *npairs_out,
              uint64_t *nverts_out, cudaStream_t s);
+// ingest (tc_ingest.cu)
+int validate_pairs_dev(const uint32_t *pairs, uint64_t np, uint64_t n, int *code, uint64_t *index,
+                       cudaStream_t s);
+int wedges_dev(const uint32_t *pairs, uint64_t np, uint64_t n, uint64_t *out, double *outd,
+               cudaStream_t s);
+int read_tri1(const char *path, uint32_t **pinned, uint64_t *npairs);
+int parse_edge_list(const char *path, uint32_t **pinned, uint64_t *npairs, uint64_t *err_line,
+                    int *err_kind);
 int ba_dev(uint64_t n, uint32_t m_attach, const uint64_t state[2], const uint64_t inc[2],
            uint32_t **pairs_out, uint64_t *npairs_out, uint64_t *nverts_out, cudaStream_t s);
 

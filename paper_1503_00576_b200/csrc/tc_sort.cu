@@ -124,14 +124,25 @@ __global__ void __launch_bounds__(kSortThreads, 4)
         st_volatile_u64(my, kFlagP | total);
     } else {
         st_volatile_u64(my, kFlagA | total);
+        // Look back in batches of kLook predecessors (independent loads, one round trip),
+        // consuming them newest-first until an inclusive prefix; a tile that has not
+        // published yet is re-polled alone.
+        constexpr int kLook = 8;
         int64_t j = (int64_t)tile - 1;
-        for (;;) {
-            uint64_t s = ld_volatile_u64(status + (uint64_t)j * kRadix + d);
-            uint64_t flag = s & ~kValMask;
-            if (flag == 0) continue;
-            excl += s & kValMask;
-            if (flag == kFlagP) break;
-            --j;
+        bool done = false;
+        while (!done) {
+            uint64_t st[kLook];
+#pragma unroll
+            for (int q = 0; q < kLook; ++q)
+                st[q] = j - q >= 0 ? ld_volatile_u64(status + (uint64_t)(j - q) * kRadix + d) : kFlagP;
+            int q = 0;
+            for (; q < kLook; ++q) {
+                const uint64_t flag = st[q] & ~kValMask;
+                if (flag == 0) break;  // not published yet: re-poll from here
+                excl += st[q] & kValMask;
+                if (flag == kFlagP) { done = true; break; }
+            }
+            j -= q;
         }
         st_volatile_u64(my, kFlagP | (excl + total));
     }

@@ -64,8 +64,15 @@ def pinned_empty(shape, dtype) -> np.ndarray:
     nbytes = int(np.prod(shape)) * dtype.itemsize
     p = ctypes.c_void_p()
     _lib.check(_lib.lib().tc_host_alloc(max(nbytes, 16), ctypes.byref(p)))
-    owner = _PinnedOwner(p.value)
-    buf = (ctypes.c_byte * max(nbytes, 16)).from_address(p.value)
+    return pinned_adopt(p.value, shape, dtype)
+
+
+def pinned_adopt(p: int, shape, dtype) -> np.ndarray:
+    """Wrap a library-allocated pinned buffer (tc_host_free'd with the array)."""
+    dtype = np.dtype(dtype)
+    nbytes = int(np.prod(shape)) * dtype.itemsize
+    owner = _PinnedOwner(p)
+    buf = (ctypes.c_byte * max(nbytes, 16)).from_address(p)
     arr = np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
     # tie the owner's lifetime to the array through the ctypes buffer object
     buf._owner = owner

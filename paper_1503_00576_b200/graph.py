@@ -87,6 +87,65 @@ class DegreeOrder:
         return (int(self.degrees[u]), u) < (int(self.degrees[v]), v)
 
 
+class GraphValidationError(ValueError):
+    """Base class for edge-array validation failures (reference graph.py:42-43)."""
+
+
+class SelfLoopError(GraphValidationError):
+    def __init__(self, vertex: int):
+        self.vertex = vertex
+        super().__init__(f"self-loop at vertex {vertex}")
+
+
+class AsymmetricEdgeError(GraphValidationError):
+    def __init__(self, u: int, v: int):
+        self.u, self.v = u, v
+        super().__init__(f"edge ({u}, {v}) has no reverse ({v}, {u})")
+
+
+class DuplicateEdgeError(GraphValidationError):
+    def __init__(self, u: int, v: int):
+        self.u, self.v = u, v
+        super().__init__(f"duplicate edge ({u}, {v})")
+
+
+def validate_edge_array(edges) -> EdgeArray:
+    """Check pairs against the edge-array contract on the device (graph.py:196-242).
+
+    Same checks, order and reported pair as the reference: the first self-loop in input
+    order, then the earliest second occurrence of a duplicate directed pair, then the
+    first pair whose reverse is missing.  Accepts raw pairs, an EdgeArray or a
+    device-resident ``DeviceEdges`` (validated in place, nothing copied).
+    """
+    if hasattr(edges, "ptr"):
+        ptr, npairs, n, on_dev, host = ctypes.c_void_p(edges.ptr), edges.npairs, edges.num_vertices, 1, None
+    else:
+        g = edges if isinstance(edges, EdgeArray) else EdgeArray(edges)
+        host = g.edges
+        ptr, npairs, n, on_dev = _lib.ptr(host), host.shape[0], g.num_vertices, 0
+    if npairs == 0:
+        return edges if hasattr(edges, "ptr") else EdgeArray(host)
+    code, index = ctypes.c_int(), ctypes.c_uint64()
+    _lib.check(_lib.lib().tc_validate_edge_array(ptr, npairs, n, on_dev, ctypes.byref(code),
+                                                 ctypes.byref(index)))
+    if code.value:
+        i = int(index.value)
+        if host is not None:
+            u, v = (int(x) for x in host[i])
+        else:
+            pair = np.empty(2, dtype=np.uint32)
+            _lib.check(_lib.lib().tc_memcpy(_lib.ptr(pair), ctypes.c_void_p(edges.ptr + 8 * i), 8, 1))
+            u, v = int(pair[0]), int(pair[1])
+        if code.value == 1:
+            raise SelfLoopError(u)
+        if code.value == 2:
+            raise DuplicateEdgeError(u, v)
+        if code.value == 3:
+            raise AsymmetricEdgeError(u, v)
+        raise ValueError(f"pair {i} ({u}, {v}) has a vertex id >= num_vertices={n}")
+    return edges if hasattr(edges, "ptr") else EdgeArray(host, num_vertices=n)
+
+
 def degrees_of(g: EdgeArray) -> DegreeOrder:
     """First-column histogram = undirected degree for symmetric input (graph.py:279-281)."""
     return DegreeOrder(np.bincount(g.edges[:, 0], minlength=g.num_vertices))
