@@ -112,6 +112,14 @@ int tc_gen_rmat(int scale, int edge_factor, const double probs[4], const uint64_
 int tc_gen_ba(uint64_t n, uint32_t m_attach, const uint64_t state[2], const uint64_t inc[2],
               uint32_t **dev_pairs, uint64_t *npairs, uint64_t *nverts);
 
+/* ---- random geometric graph, BASELINE config 5 (the reference has no generator, SURVEY.md
+ * §8(c)): points = numpy default_rng(seed).random((n, 2)) (x = draw 2i, y = draw 2i+1);
+ * edge {i, j} iff (xi-xj)^2 + (yi-yj)^2 < radius^2 in IEEE double (no FMA contraction).
+ * Sorted pairs, both directions (as edge_array_from_undirected); num_vertices = 1 + the
+ * largest id with an edge.                                                              */
+int tc_gen_rgg(uint64_t n, double radius, const uint64_t state[2], const uint64_t inc[2],
+               uint32_t **dev_pairs, uint64_t *npairs, uint64_t *nverts);
+
 /* ---- ingest ----------------------------------------------------- */
 /* io.py:127-152 read_binary: TRI1 file -> pinned host pairs (free with tc_host_free).
  * Status -4 I/O error, -5 truncated (TruncatedFileError), -6 bad magic (BadMagicError). */

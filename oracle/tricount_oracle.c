@@ -23,6 +23,11 @@
  *   or_count_partitioned  count.py:181-204 count_partitioned (P pools x W workers)
  *   or_rmat_*             generators.py:203-284 rmat (PCG64 stream restated, see below)
  *   or_ba_pairs           generators.py:287-322 barabasi_albert (numpy integers() restated)
+ *   or_rgg_*              random geometric graph (BASELINE config 5).  The reference has
+ *                         NO generator for it; the definition is ours
+ *                         (points = numpy random((n, 2)), edge iff squared distance <
+ *                         r^2) and parity is pinned by counting its output with the
+ *                         reference counter (tests/golden/make_golden.py --rgg).
  *
  * Parity of this restatement is pinned by tests/test_oracle.py against golden vectors
  * produced by the reference package itself (tests/golden/make_golden.py).
@@ -421,4 +426,128 @@ int64_t or_ba_pairs(uint64_t n, uint32_t m_attach, uint64_t state_hi, uint64_t s
     }
     free(rep);
     return (int64_t)np;
+}
+
+/* ----------------------------------------------------------------- RGG ---- */
+/* Points: numpy default_rng(seed).random((n, 2)) -> x_i = draw 2i, y_i = draw 2i+1. */
+void or_rgg_points(uint64_t n, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                   uint64_t inc_lo, double *xs, double *ys, int threads) {
+    u128 s0 = ((u128)state_hi << 64) | state_lo, inc = ((u128)inc_hi << 64) | inc_lo;
+    int nthr = clamp_threads(threads);
+#pragma omp parallel num_threads(nthr)
+    {
+        int t = omp_get_thread_num();
+        uint64_t lo = n * (uint64_t)t / nthr, hi = n * (uint64_t)(t + 1) / nthr;
+        u128 s = pcg_advance(s0, inc, 2 * lo);
+        for (uint64_t i = lo; i < hi; ++i) {
+            s = s * PCG_MULT + inc;
+            xs[i] = (double)(pcg_output(s) >> 11) * (1.0 / 9007199254740992.0);
+            s = s * PCG_MULT + inc;
+            ys[i] = (double)(pcg_output(s) >> 11) * (1.0 / 9007199254740992.0);
+        }
+    }
+}
+
+typedef struct {
+    uint32_t grid;
+    uint32_t *start; /* [grid*grid + 1] */
+    uint32_t *ids;   /* point ids bucketed by cell, ascending within a cell */
+} or_cells;
+
+static uint32_t rgg_cell(double v, uint32_t grid) {
+    uint32_t c = (uint32_t)(v * grid);
+    return c < grid ? c : grid - 1;
+}
+
+static int rgg_cells(const double *xs, const double *ys, uint64_t n, double r, or_cells *c) {
+    double fg = (double)(int64_t)(1.0 / r) - 2.0;  /* cell side > r (a different grid from the GPU's) */
+    c->grid = fg < 1 ? 1u : (fg > 65535 ? 65535u : (uint32_t)fg);
+    uint64_t cells = (uint64_t)c->grid * c->grid;
+    c->start = (uint32_t *)calloc(cells + 1, sizeof(uint32_t));
+    c->ids = (uint32_t *)malloc((n ? n : 1) * sizeof(uint32_t));
+    if (!c->start || !c->ids) return -1;
+    for (uint64_t i = 0; i < n; ++i)
+        c->start[(uint64_t)rgg_cell(ys[i], c->grid) * c->grid + rgg_cell(xs[i], c->grid) + 1]++;
+    for (uint64_t k = 0; k < cells; ++k) c->start[k + 1] += c->start[k];
+    uint32_t *fill = (uint32_t *)malloc(cells * sizeof(uint32_t));
+    if (!fill) return -1;
+    memcpy(fill, c->start, cells * sizeof(uint32_t));
+    for (uint64_t i = 0; i < n; ++i)
+        c->ids[fill[(uint64_t)rgg_cell(ys[i], c->grid) * c->grid + rgg_cell(xs[i], c->grid)]++] = (uint32_t)i;
+    free(fill);
+    return 0;
+}
+
+static int cmp_u32(const void *a, const void *b) {
+    uint32_t x = *(const uint32_t *)a, y = *(const uint32_t *)b;
+    return (x > y) - (x < y);
+}
+
+/* Neighbours of i (ascending) into out (may be NULL: count only). */
+static uint32_t rgg_neighbours(const double *xs, const double *ys, const or_cells *c, double r2,
+                               uint64_t i, uint32_t *out) {
+    uint32_t g = c->grid, cx = rgg_cell(xs[i], g), cy = rgg_cell(ys[i], g), k = 0;
+    uint32_t x0 = cx ? cx - 1 : 0, x1 = cx + 1 < g ? cx + 1 : g - 1;
+    uint32_t y0 = cy ? cy - 1 : 0, y1 = cy + 1 < g ? cy + 1 : g - 1;
+    for (uint32_t yy = y0; yy <= y1; ++yy)
+        for (uint32_t q = c->start[(uint64_t)yy * g + x0]; q < c->start[(uint64_t)yy * g + x1 + 1]; ++q) {
+            uint32_t j = c->ids[q];
+            if (j == i) continue;
+            volatile double dx = xs[i] - xs[j], dy = ys[i] - ys[j];
+            volatile double dx2 = dx * dx, dy2 = dy * dy;
+            if (dx2 + dy2 < r2) {
+                if (out) out[k] = j;
+                ++k;
+            }
+        }
+    if (out) qsort(out, k, sizeof(uint32_t), cmp_u32);
+    return k;
+}
+
+/* Pair count of the graph (both directions); deg[i] filled when non-NULL. */
+int64_t or_rgg_count(const double *xs, const double *ys, uint64_t n, double r, uint32_t *deg,
+                     int threads) {
+    or_cells c;
+    if (rgg_cells(xs, ys, n, r, &c)) return -1;
+    double r2 = r * r;
+    int64_t total = 0;
+#pragma omp parallel for num_threads(clamp_threads(threads)) schedule(dynamic, 4096) reduction(+ : total)
+    for (uint64_t i = 0; i < n; ++i) {
+        uint32_t k = rgg_neighbours(xs, ys, &c, r2, i, NULL);
+        if (deg) deg[i] = k;
+        total += k;
+    }
+    free(c.start);
+    free(c.ids);
+    return total;
+}
+
+/* All pairs (i, j), i ascending then j ascending; offsets[i] = first pair of i (n+1). */
+int or_rgg_fill(const double *xs, const double *ys, uint64_t n, double r,
+                const int64_t *offsets, uint32_t *pairs_out, int threads) {
+    or_cells c;
+    if (rgg_cells(xs, ys, n, r, &c)) return -1;
+    double r2 = r * r;
+    int bad = 0;
+#pragma omp parallel num_threads(clamp_threads(threads))
+    {
+        uint32_t cap = 1024, *buf = (uint32_t *)malloc(cap * sizeof(uint32_t));
+#pragma omp for schedule(dynamic, 4096)
+        for (uint64_t i = 0; i < n; ++i) {
+            uint64_t k = (uint64_t)(offsets[i + 1] - offsets[i]);
+            if (k > cap) {
+                cap = (uint32_t)k;
+                buf = (uint32_t *)realloc(buf, cap * sizeof(uint32_t));
+            }
+            if (rgg_neighbours(xs, ys, &c, r2, i, buf) != k) bad = 1;
+            for (uint64_t q = 0; q < k; ++q) {
+                pairs_out[2 * (offsets[i] + q)] = (uint32_t)i;
+                pairs_out[2 * (offsets[i] + q) + 1] = buf[q];
+            }
+        }
+        free(buf);
+    }
+    free(c.start);
+    free(c.ids);
+    return bad ? -1 : 0;
 }

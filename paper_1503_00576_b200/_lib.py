@@ -81,6 +81,8 @@ _SIGS = {
                      ctypes.POINTER(_vp), _u64p, _u64p], ctypes.c_int),
     "tc_gen_ba": ([ctypes.c_uint64, ctypes.c_uint32, _u64p, _u64p, ctypes.POINTER(_vp), _u64p, _u64p],
                   ctypes.c_int),
+    "tc_gen_rgg": ([ctypes.c_uint64, ctypes.c_double, _u64p, _u64p, ctypes.POINTER(_vp), _u64p, _u64p],
+                   ctypes.c_int),
     "tc_read_tri1": ([ctypes.c_char_p, ctypes.POINTER(_vp), _u64p], ctypes.c_int),
     "tc_parse_edge_list": ([ctypes.c_char_p, ctypes.POINTER(_vp), _u64p, _u64p,
                             ctypes.POINTER(ctypes.c_int)], ctypes.c_int),

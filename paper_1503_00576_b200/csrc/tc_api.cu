@@ -586,6 +586,13 @@ int tc_gen_ba(uint64_t n, uint32_t m_attach, const uint64_t state[2], const uint
     return 0;
 }
 
+int tc_gen_rgg(uint64_t n, double radius, const uint64_t state[2], const uint64_t inc[2],
+               uint32_t **dev_pairs, uint64_t *npairs, uint64_t *nverts) {
+    TC_CHECK(ensure());
+    TC_CHECK(rgg_dev(n, radius, state, inc, dev_pairs, npairs, nverts, g_stream));
+    return 0;
+}
+
 int tc_read_tri1(const char *path, uint32_t **host_pairs, uint64_t *npairs) {
     TC_CHECK(ensure());
     return read_tri1(path, host_pairs, npairs);

@@ -121,6 +121,8 @@ void graph_release(DeviceGraph *g, cudaStream_t s);
 // node_offsets (and off32, max_out) from a grouped edge_src (reference preprocess.py:36-46).
 int build_node_array_dev(const uint32_t *firsts, uint64_t k, uint64_t n, int64_t *off,
                          uint32_t *off32, uint32_t *max_out, cudaStream_t s);
+// off[i] = sum of cnt[0..i) for i < n (exclusive scan, u32 -> i64).
+int exclusive_scan_dev(const uint32_t *cnt, uint64_t n, int64_t *off, cudaStream_t s);
 // Rebuild edge_src, off32 and max_out from node_offsets (after a broadcast of dst + off).
 int finalize_graph_dev(DeviceGraph *g, cudaStream_t s);
 // Full reference preprocess on device-resident pairs (reference preprocess.py:74-84).
@@ -162,6 +164,10 @@ int merge_work_dev(const DeviceGraph &g, uint64_t *out, cudaStream_t s);
 int rmat_dev(int scale, int edge_factor, const double probs[4], const uint64_t state[2],
              const uint64_t inc[2], uint32_t **pairs_out, uint64_t *npairs_out,
              uint64_t *nverts_out, cudaStream_t s);
+// 2-D random geometric graph: n points from PCG64 random((n, 2)); edge iff squared
+// distance < radius^2 (IEEE double, no contraction).  Sorted pairs, both directions.
+int rgg_dev(uint64_t n, double radius, const uint64_t state[2], const uint64_t inc[2],
+            uint32_t **pairs_out, uint64_t *npairs_out, uint64_t *nverts_out, cudaStream_t s);
 // ingest (tc_ingest.cu)
 int validate_pairs_dev(const uint32_t *pairs, uint64_t np, uint64_t n, int *code, uint64_t *index,
                        cudaStream_t s);

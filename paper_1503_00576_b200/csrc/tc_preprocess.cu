@@ -483,6 +483,21 @@ int finalize_graph_dev(DeviceGraph *g, cudaStream_t s) {
     return 0;
 }
 
+int exclusive_scan_dev(const uint32_t *cnt, uint64_t n, int64_t *off, cudaStream_t s) {
+    if (n == 0) return 0;
+    const uint64_t nt = (n + kScanTile - 1) / kScanTile;
+    unsigned long long *sums = nullptr;
+    TC_CHECK(dalloc_t(&sums, nt, s));
+    k_tile_sum<<<(unsigned)nt, 256, 0, s>>>(cnt, n, sums);
+    TC_LAUNCHED();
+    k_scan_sums<<<1, 512, 0, s>>>(sums, nt);
+    TC_LAUNCHED();
+    k_scan_apply<<<(unsigned)nt, 256, 0, s>>>(cnt, n, sums, off, nullptr);
+    TC_LAUNCHED();
+    dfree(sums, s);
+    return 0;
+}
+
 int build_node_array_dev(const uint32_t *firsts, uint64_t k, uint64_t n, int64_t *off,
                          uint32_t *off32, uint32_t *max_out, cudaStream_t s) {
     uint32_t *cnt = nullptr;

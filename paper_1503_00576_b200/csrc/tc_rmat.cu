@@ -206,6 +206,23 @@ u128 advance_host(u128 s, u128 inc, uint64_t delta) {
     return am * s + ap;
 }
 
+// c_jump[k] = the affine map advancing the LCG by 2^k steps (s -> a*s + c).
+int upload_jump(u128 inc, cudaStream_t s) {
+    static JumpTable jt;  // host source of an async copy: keep it alive
+    TC_CUDA(cudaStreamSynchronize(s));
+    u128 am = kPcgMult, ap = inc;
+    for (int k = 0; k < kJumpBits; ++k) {
+        jt.a_lo[k] = (unsigned long long)am;
+        jt.a_hi[k] = (unsigned long long)(am >> 64);
+        jt.c_lo[k] = (unsigned long long)ap;
+        jt.c_hi[k] = (unsigned long long)(ap >> 64);
+        ap = ap * (am + 1);
+        am = am * am;
+    }
+    TC_CUDA(cudaMemcpyToSymbolAsync(c_jump, &jt, sizeof(jt), 0, cudaMemcpyHostToDevice, s));
+    return 0;
+}
+
 }  // namespace
 
 int rmat_dev(int scale, int edge_factor, const double probs[4], const uint64_t state[2],
@@ -225,19 +242,7 @@ int rmat_dev(int scale, int edge_factor, const double probs[4], const uint64_t s
     }
     const u128 s0 = ((u128)state[0] << 64) | state[1];
     const u128 inc = ((u128)inc_in[0] << 64) | inc_in[1];
-    {
-        JumpTable jt;
-        u128 am = kPcgMult, ap = inc;
-        for (int k = 0; k < kJumpBits; ++k) {
-            jt.a_lo[k] = (unsigned long long)am;
-            jt.a_hi[k] = (unsigned long long)(am >> 64);
-            jt.c_lo[k] = (unsigned long long)ap;
-            jt.c_hi[k] = (unsigned long long)(ap >> 64);
-            ap = ap * (am + 1);
-            am = am * am;
-        }
-        TC_CUDA(cudaMemcpyToSymbolAsync(c_jump, &jt, sizeof(jt), 0, cudaMemcpyHostToDevice, s));
-    }
+    TC_CHECK(upload_jump(inc, s));
     const RadixPlan draw_plan = make_radix_plan(2 * scale + 1);
     const RadixPlan have_plan = make_radix_plan(2 * scale);
     uint64_t *have = nullptr;
@@ -489,6 +494,239 @@ int ba_dev(uint64_t n, uint32_t m_attach, const uint64_t state[2], const uint64_
     *pairs_out = pairs;
     *npairs_out = 2 * np;
     *nverts_out = n;  // every vertex >= 1 edge (BA attaches every new vertex)
+    return 0;
+}
+
+// ---- random geometric graph (BASELINE config 5; no reference generator exists) --------
+// Points: numpy default_rng(seed).random((n, 2)) -- draw 2i is x_i, draw 2i+1 is y_i.
+// Edge {i, j}, i != j, iff dx*dx + dy*dy < r*r in IEEE double without contraction (the
+// oracle, oracle/tricount_oracle.c or_rgg_pairs, evaluates the same expression).  Cells
+// of side 1/G >= r (G = floor(1/r) - 1) so every neighbour lies in the 3x3 block; points
+// are bucketed by a stable radix sort of cell ids, counted and emitted warp-per-point
+// (ballot compaction), and the emitted (i, j) keys radix-sorted into the reference's
+// lexicographic both-directions layout.
+namespace {
+
+constexpr int kRggJ = 8;  // points per thread in the draw kernel
+
+__global__ void __launch_bounds__(256) k_rgg_points(uint64_t n, unsigned long long s_hi,
+                                                    unsigned long long s_lo,
+                                                    unsigned long long inc_hi,
+                                                    unsigned long long inc_lo, uint32_t grid,
+                                                    double *__restrict__ xs, double *__restrict__ ys,
+                                                    uint64_t *__restrict__ cell,
+                                                    uint32_t *__restrict__ idx) {
+    const u128 mult = ((u128)0x2360ED051FC65DA4ULL << 64) | 0x4385DF649FCCF645ULL;
+    const u128 inc = mk128(inc_hi, inc_lo);
+    const uint64_t p0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * kRggJ;
+    if (p0 >= n) return;
+    u128 s = mk128(s_hi, s_lo);
+    uint64_t d = 2 * p0;
+    for (int k = 0; d; ++k, d >>= 1)
+        if (d & 1) s = mk128(c_jump.a_hi[k], c_jump.a_lo[k]) * s + mk128(c_jump.c_hi[k], c_jump.c_lo[k]);
+    for (int j = 0; j < kRggJ && p0 + j < n; ++j) {
+        s = s * mult + inc;
+        const double x = (double)(pcg_out(s) >> 11) * (1.0 / 9007199254740992.0);
+        s = s * mult + inc;
+        const double y = (double)(pcg_out(s) >> 11) * (1.0 / 9007199254740992.0);
+        const uint64_t p = p0 + j;
+        xs[p] = x;
+        ys[p] = y;
+        uint32_t cx = (uint32_t)(x * grid), cy = (uint32_t)(y * grid);
+        cx = cx < grid ? cx : grid - 1;
+        cy = cy < grid ? cy : grid - 1;
+        cell[p] = (uint64_t)cy * grid + cx;
+        idx[p] = (uint32_t)p;
+    }
+}
+
+__global__ void k_rgg_gather(const uint32_t *__restrict__ sidx, uint64_t n, const double *__restrict__ xs,
+                             const double *__restrict__ ys, double2 *__restrict__ sxy) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
+        const uint32_t i = sidx[p];
+        sxy[p] = make_double2(xs[i], ys[i]);
+    }
+}
+
+// cstart[c] = first sorted position with cell >= c, c in [0, cells]
+__global__ void k_rgg_cell_start(const uint64_t *__restrict__ scell, uint64_t n, uint64_t cells,
+                                 uint32_t *__restrict__ cstart) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c <= cells; c += stride) {
+        uint64_t a = 0, len = n;
+        while (len > 0) {
+            const uint64_t h = len >> 1;
+            if (scell[a + h] < c) { a += h + 1; len -= h + 1; }
+            else len = h;
+        }
+        cstart[c] = (uint32_t)a;
+    }
+}
+
+__device__ __forceinline__ bool rgg_close(double2 a, double2 b, double r2) {
+    const double dx = __dsub_rn(a.x, b.x), dy = __dsub_rn(a.y, b.y);
+    return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)) < r2;
+}
+
+// EMIT = false: deg[i] = neighbours of i.  EMIT = true: keys at off[i] (unsorted).
+template <bool EMIT>
+__global__ void __launch_bounds__(256) k_rgg_scan(const double2 *__restrict__ sxy,
+                                                  const uint32_t *__restrict__ sidx, uint64_t n,
+                                                  const uint32_t *__restrict__ cstart, uint32_t grid,
+                                                  double r2, int vb, uint32_t *__restrict__ deg,
+                                                  const int64_t *__restrict__ off,
+                                                  uint64_t *__restrict__ keys) {
+    const unsigned lane = lane_id();
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t p = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); p < n; p += warps) {
+        const double2 me = sxy[p];
+        const uint32_t i = sidx[p];
+        uint32_t cx = (uint32_t)(me.x * grid), cy = (uint32_t)(me.y * grid);
+        cx = cx < grid ? cx : grid - 1;
+        cy = cy < grid ? cy : grid - 1;
+        const uint32_t x0 = cx ? cx - 1 : 0, x1 = cx + 1 < grid ? cx + 1 : grid - 1;
+        const uint32_t y0 = cy ? cy - 1 : 0, y1 = cy + 1 < grid ? cy + 1 : grid - 1;
+        uint64_t base = EMIT ? (uint64_t)off[i] : 0;
+        uint32_t cnt = 0;
+        for (uint32_t yy = y0; yy <= y1; ++yy) {
+            const uint32_t lo = cstart[(uint64_t)yy * grid + x0];
+            const uint32_t hi = cstart[(uint64_t)yy * grid + x1 + 1];
+            for (uint32_t q0 = lo; q0 < hi; q0 += 32) {
+                const uint32_t q = q0 + lane;
+                bool ok = false;
+                uint32_t j = 0;
+                if (q < hi && q != p) {
+                    ok = rgg_close(me, sxy[q], r2);
+                    j = sidx[q];
+                }
+                const unsigned mask = __ballot_sync(TC_FULL_MASK, ok);
+                if (EMIT) {
+                    if (ok) keys[base + __popc(mask & ((1u << lane) - 1))] = ((uint64_t)i << vb) | j;
+                    base += __popc(mask);
+                } else {
+                    cnt += __popc(mask);
+                }
+            }
+        }
+        if (!EMIT && lane == 0) deg[i] = cnt;
+    }
+}
+
+__global__ void k_last_nonzero(const uint32_t *__restrict__ deg, uint64_t n,
+                               unsigned long long *__restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    unsigned long long best = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        if (deg[i]) best = i + 1;
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(TC_FULL_MASK, best, o);
+        best = y > best ? y : best;
+    }
+    if (lane_id() == 0 && best) atomicMax(out, best);
+}
+
+}  // namespace
+
+int rgg_dev(uint64_t n, double radius, const uint64_t state[2], const uint64_t inc_in[2],
+            uint32_t **pairs_out, uint64_t *npairs_out, uint64_t *nverts_out, cudaStream_t s) {
+    *pairs_out = nullptr;
+    *npairs_out = *nverts_out = 0;
+    if (n < 1 || n >= (1ull << 32) || !(radius > 0) || !(radius < 2)) {
+        set_error("random_geometric: need 1 <= n < 2^32 and 0 < radius < 2");
+        return -1;
+    }
+    const double r2 = radius * radius;
+    const double fg = floor(1.0 / radius) - 1.0;
+    const uint32_t grid = fg < 1 ? 1u : (fg > 65535 ? 65535u : (uint32_t)fg);
+    const uint64_t cells = (uint64_t)grid * grid;
+    const u128 s0 = ((u128)state[0] << 64) | state[1];
+    const u128 inc = ((u128)inc_in[0] << 64) | inc_in[1];
+    TC_CHECK(upload_jump(inc, s));
+    double *xs = nullptr, *ys = nullptr;
+    double2 *sxy = nullptr;
+    uint64_t *cell = nullptr, *calt = nullptr, *scell = nullptr;
+    uint32_t *idx = nullptr, *ialt = nullptr, *sidx = nullptr, *hist = nullptr, *cstart = nullptr;
+    uint32_t *deg = nullptr;
+    int64_t *off = nullptr;
+    TC_CHECK(dalloc_t(&xs, n, s));
+    TC_CHECK(dalloc_t(&ys, n, s));
+    TC_CHECK(dalloc_t(&cell, n, s));
+    TC_CHECK(dalloc_t(&calt, n, s));
+    TC_CHECK(dalloc_t(&idx, n, s));
+    TC_CHECK(dalloc_t(&ialt, n, s));
+    TC_CHECK(dalloc_t(&hist, kMaxPasses * kRadix, s));
+    TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+    {
+        const uint64_t threads = (n + kRggJ - 1) / kRggJ;
+        k_rgg_points<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+            n, (unsigned long long)(s0 >> 64), (unsigned long long)s0, (unsigned long long)(inc >> 64),
+            (unsigned long long)inc, grid, xs, ys, cell, idx);
+        TC_LAUNCHED();
+    }
+    const RadixPlan cplan = make_radix_plan(bits_for(cells - 1 ? cells - 1 : 1));
+    TC_CHECK(radix_histogram(cell, n, cplan, hist, s));
+    TC_CHECK(radix_sort(cell, calt, idx, ialt, n, cplan, hist, kOutKeys, nullptr, nullptr, 0, &scell,
+                        &sidx, s));
+    TC_CHECK(dalloc_t(&sxy, n, s));
+    TC_CHECK(dalloc_t(&cstart, cells + 1, s));
+    k_rgg_gather<<<grid_for(n, 256, kSMs * 16), 256, 0, s>>>(sidx, n, xs, ys, sxy);
+    TC_LAUNCHED();
+    k_rgg_cell_start<<<grid_for(cells + 1, 256, kSMs * 16), 256, 0, s>>>(scell, n, cells, cstart);
+    TC_LAUNCHED();
+    dfree(xs, s);
+    dfree(ys, s);
+    TC_CHECK(dalloc_t(&deg, n, s));
+    TC_CHECK(dalloc_t(&off, n, s));
+    const int vb = bits_for(n > 1 ? n - 1 : 1);
+    const unsigned wgrid = grid_for(n * 32, 256, kSMs * 16);
+    k_rgg_scan<false><<<wgrid, 256, 0, s>>>(sxy, sidx, n, cstart, grid, r2, vb, deg, nullptr, nullptr);
+    TC_LAUNCHED();
+    TC_CHECK(exclusive_scan_dev(deg, n, off, s));
+    int64_t last_off = 0;
+    uint32_t last_deg = 0;
+    unsigned long long *d_nv = nullptr;
+    TC_CHECK(dalloc_t(&d_nv, 1, s));
+    TC_CUDA(cudaMemsetAsync(d_nv, 0, sizeof(unsigned long long), s));
+    k_last_nonzero<<<grid_for(n, 256, kSMs * 8), 256, 0, s>>>(deg, n, d_nv);
+    TC_LAUNCHED();
+    unsigned long long nv = 0;
+    TC_CUDA(cudaMemcpyAsync(&last_off, off + n - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaMemcpyAsync(&last_deg, deg + n - 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaMemcpyAsync(&nv, d_nv, sizeof(nv), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    const uint64_t np = (uint64_t)last_off + last_deg;
+    uint32_t *pairs = nullptr;
+    if (np) {
+        uint64_t *keys = nullptr, *alt = nullptr;
+        TC_CHECK(dalloc_t(&keys, np, s));
+        TC_CHECK(dalloc_t(&alt, np, s));
+        k_rgg_scan<true><<<wgrid, 256, 0, s>>>(sxy, sidx, n, cstart, grid, r2, vb, nullptr, off, keys);
+        TC_LAUNCHED();
+        const RadixPlan plan = make_radix_plan(2 * vb);
+        TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+        TC_CHECK(radix_histogram(keys, np, plan, hist, s));
+        TC_CHECK(dalloc_t(&pairs, 2 * np + 4, s, true));  // handed to the caller
+        TC_CHECK(radix_sort(keys, alt, nullptr, nullptr, np, plan, hist, kOutAoS, pairs, nullptr, vb,
+                            nullptr, nullptr, s));
+        TC_CUDA(cudaStreamSynchronize(s));
+        dfree(keys, s);
+        dfree(alt, s);
+    }
+    dfree(cell, s);
+    dfree(calt, s);
+    dfree(idx, s);
+    dfree(ialt, s);
+    dfree(hist, s);
+    dfree(sxy, s);
+    dfree(cstart, s);
+    dfree(deg, s);
+    dfree(off, s);
+    dfree(d_nv, s);
+    TC_CUDA(cudaStreamSynchronize(s));
+    *pairs_out = pairs;
+    *npairs_out = np;
+    *nverts_out = nv;
     return 0;
 }
 

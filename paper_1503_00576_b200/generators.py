@@ -10,6 +10,7 @@ in count_with_timings runs at PCIe speed.
 from __future__ import annotations
 
 import ctypes
+import math
 import weakref
 
 import numpy as np
@@ -125,6 +126,46 @@ def barabasi_albert_device(n: int, m_attach: int, seed: int = 0) -> DeviceEdges:
     _lib.check(_lib.lib().tc_gen_ba(int(n), int(m_attach), state, inc, ctypes.byref(p),
                                     ctypes.byref(npairs), ctypes.byref(nverts)))
     return DeviceEdges(p.value, npairs.value, nverts.value)
+
+
+def rgg_radius(n: int, avg_degree: float = 32.0) -> float:
+    """Radius giving expected degree ``avg_degree`` away from the border: sqrt(k / (pi n))."""
+    return math.sqrt(avg_degree / (math.pi * n))
+
+
+def random_geometric_device(n: int, avg_degree: float = 32.0, seed: int = 0,
+                            radius: float | None = None) -> DeviceEdges:
+    """2-D random geometric graph (BASELINE config 5; SURVEY.md §8(d) recipe).
+
+    Points are numpy ``default_rng(seed).random((n, 2))`` (row i = point i); vertices i, j
+    are adjacent iff (xi-xj)**2 + (yi-yj)**2 < radius**2 in float64, radius defaulting to
+    sqrt(avg_degree / (pi n)).  No torus wrap.  Pairs in both directions, sorted (the
+    reference generators' layout).  The reference has no RGG generator; parity is the
+    oracle restatement (oracle.rgg_pairs) and the reference counter on its output.
+    """
+    if n < 1 or n >= 2**32:
+        raise ValueError(f"n: must be in [1, 2^32), got {n}")
+    r = rgg_radius(n, avg_degree) if radius is None else float(radius)
+    if not 0 < r < 2:
+        raise ValueError(f"radius: must be in (0, 2), got {r}")
+    (sh, sl), (ih, il) = _pcg64_words(seed)
+    state = (ctypes.c_uint64 * 2)(sh, sl)
+    inc = (ctypes.c_uint64 * 2)(ih, il)
+    p = ctypes.c_void_p()
+    npairs, nverts = ctypes.c_uint64(), ctypes.c_uint64()
+    _lib.check(_lib.lib().tc_gen_rgg(int(n), r, state, inc, ctypes.byref(p), ctypes.byref(npairs),
+                                     ctypes.byref(nverts)))
+    return DeviceEdges(p.value or 0, npairs.value, nverts.value)
+
+
+def random_geometric(n: int, avg_degree: float = 32.0, seed: int = 0, radius: float | None = None,
+                     pinned: bool = True) -> EdgeArray:
+    """Host EdgeArray of :func:`random_geometric_device`."""
+    dev = random_geometric_device(n, avg_degree, seed, radius)
+    try:
+        return dev.to_host(pinned=pinned)
+    finally:
+        dev.free()
 
 
 def barabasi_albert(n: int, m_attach: int, seed: int = 0, pinned: bool = True) -> EdgeArray:

@@ -223,3 +223,39 @@ def test_complete_graphs_every_size_class(k):
     assert tcb.count_device(og, 0, half)[0] + tcb.count_device(og, half, og.m_dir)[0] == want
     if k <= 3000:
         assert tcb.count_device(og, algo=_lib.ALGO_MERGE_THREAD)[0] == want
+
+
+def _golden_rgg():
+    import json
+    import os
+    from conftest import GOLDEN_DIR
+    with open(os.path.join(GOLDEN_DIR, "golden_rgg.json")) as fh:
+        return json.load(fh)["rgg"]
+
+
+@pytest.mark.parametrize("case", _golden_rgg(), ids=lambda c: f"n{c['n']}_k{int(c['avg_degree'])}")
+def test_rgg_generator_and_count(case):
+    """RGG (config 5): device generator == oracle definition (sha), count == reference."""
+    d = generators.random_geometric_device(case["n"], case["avg_degree"], seed=case["seed"])
+    assert d.npairs == case["pairs"] and d.num_vertices == case["num_vertices"]
+    assert sha(d.to_host().edges) == case["edges_sha256"]
+    assert tcb.count_with_timings_device(d)[0] == case["triangles"]
+    og, _ = tcb.preprocess_device(d)
+    assert tcb.count_triangles(og) == case["triangles"]
+    assert tcb.count_device(og, algo=_lib.ALGO_MERGE_THREAD)[0] == case["triangles"]
+
+
+def test_rgg_config5_full_size():
+    """n = 2*10^7, avg degree 32: generator == oracle restatement bit for bit; every count
+    path agrees (the reference counter is too slow for this size; the smaller goldens pin
+    the counter)."""
+    n = 20_000_000
+    d = generators.random_geometric_device(n, 32.0, seed=0)
+    host = d.to_host()
+    ref = oracle.rgg_pairs(n, 32.0, seed=0)
+    assert np.array_equal(host.edges, ref)
+    t, _ = tcb.count_with_timings_device(d)
+    og, _ = tcb.preprocess_device(d)
+    assert tcb.count_triangles(og) == t
+    assert tcb.count_partitioned(og, tcb.PartitionPlan.work_balanced(og, 3), 1) == t
+    assert 1.9e9 < t < 2.1e9  # SURVEY.md §8(a) extrapolation: ~2.0e9

@@ -80,3 +80,21 @@ def test_ba_big_generator(golden_big):
     rec = golden_big["ba_1000000_9_0"]
     pairs = oracle.ba_pairs(rec["n_param"], rec["m_attach"], rec["seed"])
     assert sha(pairs) == rec["edges_sha256"]
+
+
+def test_rgg_oracle_matches_definition():
+    """oracle.rgg_points == numpy default_rng(seed).random((n, 2)); pairs pinned by the
+    golden (built with a direct numpy evaluation of the definition)."""
+    import json
+    import os
+    from conftest import GOLDEN_DIR
+    xs, ys = oracle.rgg_points(5000, seed=3)
+    pts = np.random.default_rng(3).random((5000, 2))
+    assert np.array_equal(xs, pts[:, 0]) and np.array_equal(ys, pts[:, 1])
+    with open(os.path.join(GOLDEN_DIR, "golden_rgg.json")) as fh:
+        cases = json.load(fh)["rgg"]
+    for c in cases[:2]:
+        pairs = oracle.rgg_pairs(c["n"], c["avg_degree"], seed=c["seed"])
+        assert sha(pairs) == c["edges_sha256"]
+        og = oracle.preprocess(pairs)
+        assert oracle.count(*og) == c["triangles"]
