@@ -112,6 +112,30 @@ int tc_gen_rmat(int scale, int edge_factor, const double probs[4], const uint64_
 int tc_gen_ba(uint64_t n, uint32_t m_attach, const uint64_t state[2], const uint64_t inc[2],
               uint32_t **dev_pairs, uint64_t *npairs, uint64_t *nverts);
 
+/* ---- distributed preprocessing -----------------
+ * One process per GPU, each holding a shard of the edge array.  The caller moves data
+ * between the steps with its collectives (torch.distributed / NCCL):
+ *   1. tc_dist_degrees: deg_dev[n] = first-column histogram of the shard  -> all-reduce SUM
+ *   2. tc_dist_orient: ranks from the global degrees, the shard's kept pairs as sorted
+ *      rank-space keys (*keys_dev, free with tc_device_free) + outdeg_dev[n] by source rank
+ *                                                                        -> all-reduce SUM
+ *   3. tc_graph_create(m, n, TC_PREPROCESS_RANK_SPACE) + tc_dist_layout: node_offsets
+ *      from the global out-degrees; cuts[parts+1] = source-rank boundaries balanced by
+ *      edges, edge_cuts[parts+1] = their edge positions
+ *   4. tc_dist_split: counts[parts] of the shard's keys per destination range -> all-to-all
+ *   5. tc_dist_place: sort the received keys (in place) into edge_dst[edge_pos ...]
+ *                                                     -> all-gather the edge_dst slices
+ *   6. tc_graph_finalize.                                                                  */
+int tc_dist_degrees(const uint32_t *pairs, uint64_t npairs, int pairs_on_device, uint64_t nverts,
+                    uint32_t *deg_dev);
+int tc_dist_orient(const uint32_t *pairs, uint64_t npairs, int pairs_on_device, uint64_t nverts,
+                   const uint32_t *deg_dev, uint64_t **keys_dev, uint64_t *nkeys, uint32_t *outdeg_dev);
+int tc_dist_layout(tc_graph *g, const uint32_t *outdeg_dev, int parts, int64_t *cuts,
+                   int64_t *edge_cuts);
+int tc_dist_split(const uint64_t *keys_dev, uint64_t nkeys, uint64_t nverts, const int64_t *cuts,
+                  int parts, int64_t *counts);
+int tc_dist_place(tc_graph *g, uint64_t *keys_dev, uint64_t nkeys, uint64_t edge_pos);
+
 /* ---- random geometric graph, BASELINE config 5 (the reference has no generator, SURVEY.md
  * §8(c)): points = numpy default_rng(seed).random((n, 2)) (x = draw 2i, y = draw 2i+1);
  * edge {i, j} iff (xi-xj)^2 + (yi-yj)^2 < radius^2 in IEEE double (no FMA contraction).

@@ -81,6 +81,12 @@ _SIGS = {
                      ctypes.POINTER(_vp), _u64p, _u64p], ctypes.c_int),
     "tc_gen_ba": ([ctypes.c_uint64, ctypes.c_uint32, _u64p, _u64p, ctypes.POINTER(_vp), _u64p, _u64p],
                   ctypes.c_int),
+    "tc_dist_degrees": ([_vp, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint64, _vp], ctypes.c_int),
+    "tc_dist_orient": ([_vp, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint64, _vp, ctypes.POINTER(_vp),
+                        _u64p, _vp], ctypes.c_int),
+    "tc_dist_layout": ([_graph_p, _vp, ctypes.c_int, _vp, _vp], ctypes.c_int),
+    "tc_dist_split": ([_vp, ctypes.c_uint64, ctypes.c_uint64, _vp, ctypes.c_int, _vp], ctypes.c_int),
+    "tc_dist_place": ([_graph_p, _vp, ctypes.c_uint64, ctypes.c_uint64], ctypes.c_int),
     "tc_gen_rgg": ([ctypes.c_uint64, ctypes.c_double, _u64p, _u64p, ctypes.POINTER(_vp), _u64p, _u64p],
                    ctypes.c_int),
     "tc_read_tri1": ([ctypes.c_char_p, ctypes.POINTER(_vp), _u64p], ctypes.c_int),

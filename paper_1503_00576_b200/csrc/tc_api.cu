@@ -586,6 +586,60 @@ int tc_gen_ba(uint64_t n, uint32_t m_attach, const uint64_t state[2], const uint
     return 0;
 }
 
+static int with_device_pairs(const uint32_t *pairs, uint64_t npairs, int on_device,
+                             const uint32_t **dp, uint32_t **owned) {
+    *dp = pairs;
+    *owned = nullptr;
+    if (!on_device && npairs) {
+        TC_CHECK(dalloc_t(owned, 2 * npairs, g_stream, true));
+        TC_CUDA(cudaMemcpyAsync(*owned, pairs, npairs * 8, cudaMemcpyHostToDevice, g_stream));
+        *dp = *owned;
+    }
+    return 0;
+}
+
+// ---- distributed preprocessing steps ---------------------------------
+int tc_dist_degrees(const uint32_t *pairs, uint64_t npairs, int pairs_on_device, uint64_t nverts,
+                    uint32_t *deg_dev) {
+    TC_CHECK(ensure());
+    const uint32_t *dp;
+    uint32_t *owned;
+    TC_CHECK(with_device_pairs(pairs, npairs, pairs_on_device, &dp, &owned));
+    const int rc = dist_degrees_dev(dp, npairs, nverts, deg_dev, g_stream);
+    if (owned) dfree(owned, g_stream);
+    return rc;
+}
+
+int tc_dist_orient(const uint32_t *pairs, uint64_t npairs, int pairs_on_device, uint64_t nverts,
+                   const uint32_t *deg_dev, uint64_t **keys_dev, uint64_t *nkeys, uint32_t *outdeg_dev) {
+    TC_CHECK(ensure());
+    const uint32_t *dp;
+    uint32_t *owned;
+    TC_CHECK(with_device_pairs(pairs, npairs, pairs_on_device, &dp, &owned));
+    const int rc = dist_orient_dev(dp, npairs, nverts, deg_dev, keys_dev, nkeys, outdeg_dev, g_stream);
+    if (owned) dfree(owned, g_stream);
+    return rc;
+}
+
+int tc_dist_layout(tc_graph *g, const uint32_t *outdeg_dev, int parts, int64_t *cuts,
+                   int64_t *edge_cuts) {
+    TC_CHECK(ensure());
+    TC_CHECK(check_graph(g));
+    return dist_layout_dev(&g->g, outdeg_dev, parts, cuts, edge_cuts, g_stream);
+}
+
+int tc_dist_split(const uint64_t *keys_dev, uint64_t nkeys, uint64_t nverts, const int64_t *cuts,
+                  int parts, int64_t *counts) {
+    TC_CHECK(ensure());
+    return dist_split_dev(keys_dev, nkeys, nverts, cuts, parts, counts, g_stream);
+}
+
+int tc_dist_place(tc_graph *g, uint64_t *keys_dev, uint64_t nkeys, uint64_t edge_pos) {
+    TC_CHECK(ensure());
+    TC_CHECK(check_graph(g));
+    return dist_place_dev(&g->g, keys_dev, nkeys, edge_pos, g_stream);
+}
+
 int tc_gen_rgg(uint64_t n, double radius, const uint64_t state[2], const uint64_t inc[2],
                uint32_t **dev_pairs, uint64_t *npairs, uint64_t *nverts) {
     TC_CHECK(ensure());
@@ -604,17 +658,6 @@ int tc_parse_edge_list(const char *path, uint32_t **host_pairs, uint64_t *npairs
     return parse_edge_list(path, host_pairs, npairs, err_line, err_kind);
 }
 
-static int with_device_pairs(const uint32_t *pairs, uint64_t npairs, int on_device,
-                             const uint32_t **dp, uint32_t **owned) {
-    *dp = pairs;
-    *owned = nullptr;
-    if (!on_device && npairs) {
-        TC_CHECK(dalloc_t(owned, 2 * npairs, g_stream, true));
-        TC_CUDA(cudaMemcpyAsync(*owned, pairs, npairs * 8, cudaMemcpyHostToDevice, g_stream));
-        *dp = *owned;
-    }
-    return 0;
-}
 
 int tc_validate_edge_array(const uint32_t *pairs, uint64_t npairs, uint64_t nverts,
                            int pairs_on_device, int *code, uint64_t *index) {

@@ -131,6 +131,15 @@ int preprocess_dev(const uint32_t *pairs, uint64_t npairs, uint64_t n, DeviceGra
 // The same pipeline producing the rank-space oriented CSR (+ hubstart) directly.
 int preprocess_rank_dev(const uint32_t *pairs, uint64_t npairs, uint64_t n, DeviceGraph *out,
                         cudaStream_t s);
+// Distributed preprocessing steps (tc_preprocess.cu).
+int dist_degrees_dev(const uint32_t *pairs, uint64_t npairs, uint64_t n, uint32_t *deg, cudaStream_t s);
+int dist_orient_dev(const uint32_t *pairs, uint64_t npairs, uint64_t n, const uint32_t *deg,
+                    uint64_t **keys_out, uint64_t *nkeys, uint32_t *outdeg, cudaStream_t s);
+int dist_layout_dev(DeviceGraph *g, const uint32_t *outdeg, int parts, int64_t *cuts,
+                    int64_t *ecuts, cudaStream_t s);
+int dist_split_dev(const uint64_t *keys, uint64_t nkeys, uint64_t n, const int64_t *cuts, int parts,
+                   int64_t *counts, cudaStream_t s);
+int dist_place_dev(DeviceGraph *g, uint64_t *keys, uint64_t nkeys, uint64_t pos, cudaStream_t s);
 // Rank-space copy of an oriented graph given in original ids (same triangles).
 int relabel_dev(const DeviceGraph &g, DeviceGraph *out, cudaStream_t s);
 // hubstart[] and hz of a rank-space graph (after dst/off are in place).

@@ -876,4 +876,206 @@ int relabel_dev(const DeviceGraph &g, DeviceGraph *out, cudaStream_t s) {
     return 0;
 }
 
+// ---- distributed preprocessing -----------------------------------
+// Each rank holds a shard of the pairs.  Global degrees = sum of the shards' first-column
+// histograms (all-reduce); ranks follow identically on every rank; each rank orients and
+// relabels its shard, sorts it, and ships every key to the rank owning its source range
+// (all-to-all); the owner sorts what it received into its slice of edge_dst; slices are
+// then all-gathered and every rank finalises the same count-ready CSR.
+namespace {
+
+__global__ void __launch_bounds__(256) k_key_src_hist(const uint64_t *__restrict__ keys, uint64_t k,
+                                                      int vb, uint32_t *__restrict__ cnt) {
+    const unsigned lane = lane_id();
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < k;
+         base += stride) {
+        const uint64_t i = base + lane;
+        const bool ok = i < k;
+        const uint32_t u = ok ? (uint32_t)(keys[i] >> vb) : 0xffffffffu;
+        const unsigned peers = __match_any_sync(TC_FULL_MASK, u);
+        if (ok && (int)lane == __ffs(peers) - 1) atomicAdd(cnt + u, __popc(peers));
+    }
+}
+
+// cuts[r] = first rank u with off[u] >= r * m / parts (r = 0..parts; cuts[parts] = n)
+__global__ void k_edge_cuts(const int64_t *__restrict__ off, uint64_t n, int parts,
+                            int64_t *__restrict__ cuts, int64_t *__restrict__ ecuts) {
+    const int r = threadIdx.x;
+    if (r > parts) return;
+    const int64_t m = off[n];
+    if (r == parts) {
+        cuts[r] = (int64_t)n;
+        ecuts[r] = m;
+        return;
+    }
+    const int64_t want = (int64_t)((__int128)m * r / parts);
+    uint64_t a = 0, len = n;  // first u in [0, n) with off[u] >= want
+    while (len > 0) {
+        const uint64_t h = len >> 1;
+        if (off[a + h] < want) { a += h + 1; len -= h + 1; }
+        else len = h;
+    }
+    cuts[r] = (int64_t)a;
+    ecuts[r] = off[a];
+}
+
+// counts[r] = #keys with source rank in [cuts[r], cuts[r+1]) (keys sorted)
+__global__ void k_key_split(const uint64_t *__restrict__ keys, uint64_t k, int vb,
+                            const int64_t *__restrict__ cuts, int parts, int64_t *__restrict__ counts) {
+    __shared__ uint64_t pos[65];
+    const int r = threadIdx.x;
+    if (r <= parts) {
+        const uint64_t want = (uint64_t)cuts[r] << vb;
+        uint64_t a = 0, len = k;
+        while (len > 0) {
+            const uint64_t h = len >> 1;
+            if (keys[a + h] < want) { a += h + 1; len -= h + 1; }
+            else len = h;
+        }
+        pos[r] = r == parts ? k : a;
+    }
+    __syncthreads();
+    if (r < parts) counts[r] = (int64_t)(pos[r + 1] - pos[r]);
+}
+
+}  // namespace
+
+int dist_degrees_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, uint32_t *deg,
+                     cudaStream_t s) {
+    const uint2 *pairs = reinterpret_cast<const uint2 *>(pairs_u32);
+    uint32_t *bad_d = nullptr;
+    TC_CHECK(dalloc_t(&bad_d, 1, s));
+    TC_CUDA(cudaMemsetAsync(bad_d, 0, sizeof(uint32_t), s));
+    TC_CUDA(cudaMemsetAsync(deg, 0, (n ? n : 1) * sizeof(uint32_t), s));
+    if (npairs) {
+        k_degree_hist<<<grid_for(npairs, 256 * kPP, kSMs * 8), 256, 0, s>>>(pairs, npairs, deg, n, bad_d);
+        TC_LAUNCHED();
+    }
+    uint32_t bad = 0;
+    TC_CUDA(cudaMemcpyAsync(&bad, bad_d, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    dfree(bad_d, s);
+    if (bad) {
+        set_error("edge array holds a vertex id >= num_vertices");
+        return -1;
+    }
+    return 0;
+}
+
+int dist_orient_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, const uint32_t *deg,
+                    uint64_t **keys_out, uint64_t *nkeys, uint32_t *outdeg, cudaStream_t s) {
+    const uint2 *pairs = reinterpret_cast<const uint2 *>(pairs_u32);
+    *keys_out = nullptr;
+    *nkeys = 0;
+    if (n >= (1ull << 32)) {
+        set_error("num_vertices must be < 2^32 on the device path");
+        return -1;
+    }
+    const int vb = n > 1 ? bits_for(n - 1) : 1;
+    const RadixPlan plan = make_radix_plan(2 * vb);
+    uint32_t *rank = nullptr, *hist = nullptr;
+    unsigned long long *cursor = nullptr;
+    TC_CHECK(dalloc_t(&rank, n ? n : 1, s));
+    TC_CHECK(dalloc_t(&hist, kMaxPasses * kRadix, s));
+    TC_CHECK(dalloc_t(&cursor, 1, s));
+    TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+    TC_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
+    TC_CUDA(cudaMemsetAsync(outdeg, 0, (n ? n : 1) * sizeof(uint32_t), s));
+    TC_CHECK(compute_ranks(deg, n, rank, s));
+    // a shard of a symmetric array keeps about half its pairs, but not exactly: size for all
+    uint64_t capacity = npairs ? npairs : 1;
+    uint64_t *keys = nullptr, *alt = nullptr;
+    TC_CHECK(dalloc_t(&keys, capacity, s, true));
+    if (npairs) {
+        k_orient<true><<<grid_for(npairs, 256 * kPP, kSMs * 8), 256, 0, s>>>(
+            pairs, npairs, rank, n, vb, keys, capacity, cursor, plan, hist);
+        TC_LAUNCHED();
+    }
+    unsigned long long kept = 0;
+    TC_CUDA(cudaMemcpyAsync(&kept, cursor, sizeof(kept), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    TC_CHECK(dalloc_t(&alt, kept ? kept : 1, s, true));
+    uint64_t *sorted = keys;
+    TC_CHECK(radix_sort(keys, alt, nullptr, nullptr, kept, plan, hist, kOutKeys, nullptr, nullptr, 0,
+                        &sorted, nullptr, s));
+    if (kept) {
+        k_key_src_hist<<<grid_for(kept, 256, kSMs * 16), 256, 0, s>>>(sorted, kept, vb, outdeg);
+        TC_LAUNCHED();
+    }
+    TC_CUDA(cudaStreamSynchronize(s));
+    dfree(sorted == keys ? alt : keys, s);
+    dfree(rank, s);
+    dfree(hist, s);
+    dfree(cursor, s);
+    *keys_out = sorted;
+    *nkeys = kept;
+    return 0;
+}
+
+int dist_layout_dev(DeviceGraph *g, const uint32_t *outdeg, int parts, int64_t *cuts,
+                    int64_t *ecuts, cudaStream_t s) {
+    if (parts < 1 || parts > 64) {
+        set_error("parts must be in 1..64");
+        return -1;
+    }
+    TC_CHECK(exclusive_scan_dev(outdeg, g->n, g->off, s));
+    const int64_t mm = (int64_t)g->m;
+    TC_CUDA(cudaMemcpyAsync(g->off + g->n, &mm, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    int64_t *d = nullptr;
+    TC_CHECK(dalloc_t(&d, 2 * (parts + 1), s));
+    k_edge_cuts<<<1, 96, 0, s>>>(g->off, g->n, parts, d, d + parts + 1);
+    TC_LAUNCHED();
+    TC_CUDA(cudaMemcpyAsync(cuts, d, (parts + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaMemcpyAsync(ecuts, d + parts + 1, (parts + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    dfree(d, s);
+    if (ecuts[parts] != mm) {
+        set_error("out-degrees do not sum to the graph's edge count");
+        return -1;
+    }
+    return 0;
+}
+
+int dist_split_dev(const uint64_t *keys, uint64_t nkeys, uint64_t n, const int64_t *cuts, int parts,
+                   int64_t *counts, cudaStream_t s) {
+    if (parts < 1 || parts > 64) {
+        set_error("parts must be in 1..64");
+        return -1;
+    }
+    const int vb = n > 1 ? bits_for(n - 1) : 1;
+    int64_t *d = nullptr;
+    TC_CHECK(dalloc_t(&d, 2 * (parts + 1), s));
+    TC_CUDA(cudaMemcpyAsync(d, cuts, (parts + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    k_key_split<<<1, 96, 0, s>>>(keys, nkeys, vb, d, parts, d + parts + 1);
+    TC_LAUNCHED();
+    TC_CUDA(cudaMemcpyAsync(counts, d + parts + 1, parts * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    dfree(d, s);
+    return 0;
+}
+
+int dist_place_dev(DeviceGraph *g, uint64_t *keys, uint64_t nkeys, uint64_t pos, cudaStream_t s) {
+    if (pos + nkeys > g->m) {
+        set_error("placed slice exceeds the graph's edge count");
+        return -1;
+    }
+    if (nkeys == 0) return 0;
+    const int vb = g->n > 1 ? bits_for(g->n - 1) : 1;
+    const RadixPlan plan = make_radix_plan(2 * vb);
+    uint64_t *alt = nullptr;
+    uint32_t *hist = nullptr;
+    TC_CHECK(dalloc_t(&alt, nkeys, s));
+    TC_CHECK(dalloc_t(&hist, kMaxPasses * kRadix, s));
+    TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+    TC_CHECK(radix_histogram(keys, nkeys, plan, hist, s));
+    // src lands in the graph's own edge_src (rebuilt by finalize anyway)
+    TC_CHECK(radix_sort(keys, alt, nullptr, nullptr, nkeys, plan, hist, kOutSoA, g->src + pos,
+                        g->dst + pos, vb, nullptr, nullptr, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    dfree(alt, s);
+    dfree(hist, s);
+    return 0;
+}
+
 }  // namespace tc

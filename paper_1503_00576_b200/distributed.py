@@ -12,6 +12,19 @@ to every GPU and sums the per-GPU counts on the host.  Here:
      SURVEY.md §8(e)) and counts its own contiguous range;
   4. one all-reduce of a single 64-bit count.
 
+``count_distributed_sharded`` is the v2 path:
+no serial preprocessing.  Every rank holds a shard of the edge array (its slice of the
+pairs, device-resident or copied from host memory by that rank alone):
+
+  1. shard degree histograms -> all-reduce -> global degrees (every rank);
+  2. each rank ranks the vertices by (degree, id) itself (same result everywhere),
+     orients + relabels its shard and sorts it locally; out-degrees -> all-reduce;
+  3. node_offsets from the global out-degrees; source-rank ranges balanced by edges;
+  4. all-to-all: every key goes to the rank owning its source range;
+  5. each rank sorts what it received into its slice of edge_dst; the slices are
+     all-gathered (one broadcast per owner); every rank finalises the same CSR;
+  6. work-balanced shards + one 64-bit all-reduce, as in v1.
+
 The orchestration is written against a small ``Ops`` interface so the same code runs
 under gloo on CPU in the tests (with the CPU oracle behind ``Ops``) and under NCCL on
 B200s (``B200Ops``, backed by libtcb200).
@@ -25,7 +38,8 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["Ops", "B200Ops", "count_distributed", "ShardReport"]
+__all__ = ["Ops", "B200Ops", "count_distributed", "count_distributed_sharded", "ShardReport",
+           "shard_bounds"]
 
 
 class Ops:
@@ -58,6 +72,41 @@ class Ops:
     def count_tensor(self, value: int):
         import torch
         return torch.tensor([value], dtype=torch.int64)
+
+    # ---- v2 (sharded preprocessing); tensors returned/accepted are "comm" tensors,
+    # i.e. ready for the process group's backend
+    def shard_degrees(self, shard, n: int):  # -> int32[n]
+        raise NotImplementedError
+
+    def shard_orient(self, shard, n: int, deg):  # -> (keys, nkeys, outdeg int32[n])
+        raise NotImplementedError
+
+    def create_graph(self, m: int, n: int):
+        raise NotImplementedError
+
+    def layout(self, graph, outdeg, parts: int):  # -> (cuts[parts+1], edge_cuts[parts+1])
+        raise NotImplementedError
+
+    def split(self, keys, nkeys: int, n: int, cuts, parts: int):  # -> counts[parts]
+        raise NotImplementedError
+
+    def send_tensor(self, keys, nkeys: int):  # int64[nkeys]
+        raise NotImplementedError
+
+    def recv_tensor(self, k: int):  # int64[k]
+        raise NotImplementedError
+
+    def place(self, graph, recv, k: int, pos: int) -> None:
+        raise NotImplementedError
+
+    def dst_slice(self, graph, lo: int, hi: int):  # int32[hi-lo] for an in-place broadcast
+        raise NotImplementedError
+
+    def dst_slice_done(self, graph, lo: int, hi: int, t) -> None:
+        pass
+
+    def free_keys(self, keys) -> None:
+        pass
 
 
 @dataclass
@@ -116,18 +165,89 @@ def count_distributed(ops: Ops, edges=None, group=None, graph=None) -> ShardRepo
     return ShardReport(total, local, tuple(int(b) for b in bounds), m, n)
 
 
+def shard_bounds(npairs: int, world: int) -> list[int]:
+    """Contiguous pair ranges [b[r], b[r+1]) of an edge array split over ``world`` ranks."""
+    return [npairs * r // world for r in range(world + 1)]
+
+
+def count_distributed_sharded(ops: Ops, shard, num_vertices: int, group=None) -> ShardReport:
+    """Triangles of the edge array whose shards the ranks of ``group`` hold (v2: sharded
+    preprocessing, no serial step).  ``shard`` is this rank's slice of the pairs (any
+    split works: the result does not depend on it); ``num_vertices`` is the global
+    vertex count, identical on every rank.  Returns the global count on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    n = int(num_vertices)
+    gr = [dist.get_global_rank(group, r) if group is not None else r for r in range(world)]
+    # 1. global degrees
+    deg = ops.shard_degrees(shard, n)
+    dist.all_reduce(deg, op=dist.ReduceOp.SUM, group=group)
+    _backend_sync(ops)
+    # 2. local orientation in rank space; global out-degrees and m
+    keys, nkeys, outdeg = ops.shard_orient(shard, n, deg)
+    del deg
+    dist.all_reduce(outdeg, op=dist.ReduceOp.SUM, group=group)
+    mt = _to_backend(torch.tensor([nkeys], dtype=torch.int64), ops)
+    dist.all_reduce(mt, op=dist.ReduceOp.SUM, group=group)
+    _backend_sync(ops)
+    m = int(mt.cpu().item())
+    # 3. offsets + source ranges
+    g = ops.create_graph(m, n)
+    cuts, ecuts = ops.layout(g, outdeg, world)
+    del outdeg
+    # 4. all-to-all of the keys by source range
+    send_counts = [int(c) for c in ops.split(keys, nkeys, n, cuts, world)]
+    sc = _to_backend(torch.tensor(send_counts, dtype=torch.int64), ops)
+    rc = _to_backend(torch.empty(world, dtype=torch.int64), ops)
+    dist.all_to_all_single(rc, sc, group=group)
+    _backend_sync(ops)
+    recv_counts = [int(c) for c in rc.cpu().tolist()]
+    k = sum(recv_counts)
+    if k != int(ecuts[rank + 1] - ecuts[rank]):
+        raise RuntimeError("all-to-all delivered a different edge count than the layout")
+    recv = ops.recv_tensor(k)
+    send = ops.send_tensor(keys, nkeys)
+    dist.all_to_all_single(recv, send, output_split_sizes=recv_counts,
+                           input_split_sizes=send_counts, group=group)
+    _backend_sync(ops)
+    del send
+    ops.free_keys(keys)
+    # 5. sort the received keys into this rank's slice of edge_dst; all-gather the slices
+    ops.place(g, recv, k, int(ecuts[rank]))
+    del recv
+    for r in range(world):
+        lo, hi = int(ecuts[r]), int(ecuts[r + 1])
+        if hi > lo:
+            t = ops.dst_slice(g, lo, hi)
+            dist.broadcast(t, src=gr[r], group=group)
+            _backend_sync(ops)
+            ops.dst_slice_done(g, lo, hi, t)
+    ops.finalize(g)
+    # 6. count the work-balanced shard; one all-reduce
+    bounds = ops.work_bounds(g, world)
+    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+    local = ops.count_range(g, lo, hi) if hi > lo else 0
+    t = _to_backend(ops.count_tensor(local), ops)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    total = int(t.cpu().item())
+    return ShardReport(total, local, tuple(int(b) for b in bounds), m, n)
+
+
 def _global_src(group) -> int:
     import torch.distributed as dist
     return dist.get_global_rank(group, 0) if group is not None else 0
 
 
 def _to_backend(t, ops):
-    dev = getattr(ops, "torch_device", None)
+    dev = getattr(ops, "comm_device", None)
     return t.to(dev) if dev is not None else t
 
 
 def _backend_sync(ops) -> None:
-    dev = getattr(ops, "torch_device", None)
+    dev = getattr(ops, "comm_device", None)
     if dev is not None and dev.type == "cuda":
         import torch
         torch.cuda.synchronize(dev)
@@ -136,17 +256,35 @@ def _backend_sync(ops) -> None:
 class _CudaArray:
     """Minimal __cuda_array_interface__ so torch can alias library-owned HBM."""
 
-    def __init__(self, ptr: int, nbytes: int):
-        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+    def __init__(self, ptr: int, count: int, typestr: str = "|u1"):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr,
                                          "data": (ptr, False), "version": 3, "strides": None}
 
 
-class B200Ops(Ops):
-    """Ops over libtcb200 on this process's GPU (cuda:LOCAL_RANK)."""
+class _Keys:
+    """Library-allocated device buffer of sorted rank-space keys (tc_device_free'd)."""
 
-    def __init__(self, device_index: int):
+    def __init__(self, ptr: int):
+        import weakref
+        self.ptr = int(ptr)
+        self._fin = weakref.finalize(self, _lib.lib().tc_device_free, ctypes.c_void_p(self.ptr))
+
+    def free(self):
+        self._fin()
+
+
+class B200Ops(Ops):
+    """Ops over libtcb200 on this process's GPU (cuda:LOCAL_RANK).
+
+    ``comm="cuda"`` (NCCL) hands device tensors to the collectives, aliasing library
+    memory where it can; ``comm="cpu"`` stages every collective through host memory so
+    several processes can share one GPU under gloo (the single-GPU test of the v2 path).
+    """
+
+    def __init__(self, device_index: int, comm: str = "cuda"):
         import torch
         self.torch_device = torch.device("cuda", device_index)
+        self.comm_device = self.torch_device if comm == "cuda" else None
         torch.cuda.set_device(self.torch_device)
         _lib.lib()
 
@@ -204,3 +342,91 @@ class B200Ops(Ops):
 
     def sync(self):
         _lib.check(_lib.lib().tc_synchronize())
+
+    # ---- v2 -----------------------------------------------------------------------
+    def _out(self, t):
+        return t if self.comm_device is not None else t.cpu()
+
+    def _in(self, t):
+        import torch
+        if t.is_cuda:
+            torch.cuda.synchronize(self.torch_device)
+            return t
+        return t.to(self.torch_device)
+
+    @staticmethod
+    def _shard_args(shard):
+        if hasattr(shard, "ptr"):
+            return ctypes.c_void_p(shard.ptr), int(shard.npairs), 1
+        arr = shard.edges if hasattr(shard, "edges") else shard
+        return _lib.ptr(arr), int(arr.shape[0]), 0
+
+    def shard_degrees(self, shard, n):
+        import torch
+        deg = torch.empty(max(n, 1), dtype=torch.int32, device=self.torch_device)[:n]
+        p, k, on_dev = self._shard_args(shard)
+        torch.cuda.synchronize(self.torch_device)
+        _lib.check(_lib.lib().tc_dist_degrees(p, k, on_dev, n, ctypes.c_void_p(deg.data_ptr())))
+        return self._out(deg)
+
+    def shard_orient(self, shard, n, deg):
+        import torch
+        deg = self._in(deg)
+        outdeg = torch.empty(max(n, 1), dtype=torch.int32, device=self.torch_device)[:n]
+        p, k, on_dev = self._shard_args(shard)
+        kp, nk = ctypes.c_void_p(), ctypes.c_uint64()
+        _lib.check(_lib.lib().tc_dist_orient(p, k, on_dev, n, ctypes.c_void_p(deg.data_ptr()),
+                                             ctypes.byref(kp), ctypes.byref(nk),
+                                             ctypes.c_void_p(outdeg.data_ptr())))
+        return _Keys(kp.value or 0), int(nk.value), self._out(outdeg)
+
+    def create_graph(self, m, n):
+        return self.empty_graph(m, n)
+
+    def layout(self, graph, outdeg, parts):
+        outdeg = self._in(outdeg)
+        cuts = np.zeros(parts + 1, dtype=np.int64)
+        ecuts = np.zeros(parts + 1, dtype=np.int64)
+        _lib.check(_lib.lib().tc_dist_layout(graph.handle, ctypes.c_void_p(outdeg.data_ptr()), parts,
+                                             _lib.ptr(cuts), _lib.ptr(ecuts)))
+        return cuts, ecuts
+
+    def split(self, keys, nkeys, n, cuts, parts):
+        counts = np.zeros(parts, dtype=np.int64)
+        c = np.ascontiguousarray(cuts, dtype=np.int64)
+        _lib.check(_lib.lib().tc_dist_split(ctypes.c_void_p(keys.ptr), nkeys, n, _lib.ptr(c), parts,
+                                            _lib.ptr(counts)))
+        return counts
+
+    def send_tensor(self, keys, nkeys):
+        import torch
+        if nkeys == 0:
+            return self._out(torch.empty(0, dtype=torch.int64, device=self.torch_device))
+        t = torch.as_tensor(_CudaArray(keys.ptr, nkeys, "<i8"), device=self.torch_device)
+        return self._out(t)
+
+    def recv_tensor(self, k):
+        import torch
+        return torch.empty(k, dtype=torch.int64, device=self.comm_device or "cpu")
+
+    def place(self, graph, recv, k, pos):
+        recv = self._in(recv)
+        _lib.check(_lib.lib().tc_dist_place(graph.handle, ctypes.c_void_p(recv.data_ptr() if k else 0),
+                                            k, pos))
+
+    def dst_slice(self, graph, lo, hi):
+        import torch
+        _, dst, _ = graph.device_pointers()
+        t = torch.as_tensor(_CudaArray(dst + 4 * lo, hi - lo, "<i4"), device=self.torch_device)
+        return self._out(t)
+
+    def dst_slice_done(self, graph, lo, hi, t):
+        if self.comm_device is None:  # staged through host: write the broadcast back
+            import torch
+            _, dst, _ = graph.device_pointers()
+            d = torch.as_tensor(_CudaArray(dst + 4 * lo, hi - lo, "<i4"), device=self.torch_device)
+            d.copy_(t)
+            torch.cuda.synchronize(self.torch_device)
+
+    def free_keys(self, keys):
+        keys.free()

@@ -53,6 +53,22 @@ class DeviceEdges:
         self._fin()
 
 
+class DeviceEdgesView:
+    """Pairs [lo, hi) of a DeviceEdges (a rank's shard); keeps the parent alive, owns nothing."""
+
+    def __init__(self, parent: DeviceEdges, lo: int, hi: int):
+        if not 0 <= lo <= hi <= parent.npairs:
+            raise ValueError(f"bad shard [{lo}, {hi}) of {parent.npairs} pairs")
+        self.parent = parent
+        self.ptr = parent.ptr + 8 * int(lo)
+        self.npairs = int(hi - lo)
+        self.num_vertices = parent.num_vertices
+
+    @property
+    def nbytes(self) -> int:
+        return self.npairs * 8
+
+
 class _PinnedOwner:
     def __init__(self, p: int):
         self.p = p

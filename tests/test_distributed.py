@@ -14,7 +14,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle
-from paper_1503_00576_b200.distributed import Ops, count_distributed
+from paper_1503_00576_b200.distributed import (Ops, count_distributed, count_distributed_sharded,
+                                               shard_bounds)
 
 
 class OracleOps(Ops):
@@ -51,6 +52,72 @@ class OracleOps(Ops):
         L = oracle.lib()
         return int(L.or_count_strided(oracle._c32(g["src"]), oracle._c32(g["dst"]),
                                       oracle._c64(g["off"]), lo, hi, 0, 1))
+
+    # ---- v2: numpy restatement of each device step (see include/tricount_b200.h) ----
+    @staticmethod
+    def _vb(n):
+        return max(int(n - 1).bit_length(), 1)
+
+    def shard_degrees(self, shard, n):
+        return torch.from_numpy(np.bincount(shard[:, 0], minlength=n).astype(np.int32))
+
+    def shard_orient(self, shard, n, deg):
+        deg = deg.numpy().astype(np.int64)
+        order = np.lexsort((np.arange(n), deg))
+        rank = np.empty(n, np.int64)
+        rank[order] = np.arange(n)
+        ru, rv = rank[shard[:, 0]], rank[shard[:, 1]]
+        keep = ru < rv
+        keys = np.sort((ru[keep] << self._vb(n)) | rv[keep]).astype(np.int64)
+        outdeg = np.bincount(ru[keep], minlength=n).astype(np.int32)
+        return keys, int(keys.size), torch.from_numpy(outdeg)
+
+    def create_graph(self, m, n):
+        return self.empty_graph(m, n)
+
+    def layout(self, g, outdeg, parts):
+        n = g["off"].size - 1
+        np.cumsum(outdeg.numpy().astype(np.int64), out=g["off"][1:])
+        m = int(g["off"][-1])
+        want = (m * np.arange(parts + 1)) // parts
+        cuts = np.searchsorted(g["off"][:n], want, side="left").astype(np.int64)
+        cuts[parts] = n
+        return cuts, g["off"][cuts].copy()
+
+    def split(self, keys, nkeys, n, cuts, parts):
+        pos = np.searchsorted(keys, np.asarray(cuts, np.int64) << self._vb(n))
+        pos[-1] = nkeys
+        return np.diff(pos)
+
+    def send_tensor(self, keys, nkeys):
+        return torch.from_numpy(keys)
+
+    def recv_tensor(self, k):
+        return torch.empty(k, dtype=torch.int64)
+
+    def place(self, g, recv, k, pos):
+        n = g["off"].size - 1
+        keys = np.sort(recv.numpy())
+        g["dst"][pos:pos + k] = (keys & ((1 << self._vb(n)) - 1)).astype(np.uint32)
+
+    def dst_slice(self, g, lo, hi):
+        return torch.from_numpy(g["dst"][lo:hi].view(np.int32))
+
+
+def _rank_space_csr(pairs):
+    """Single-process restatement of the rank-space CSR the sharded path must rebuild."""
+    n = int(pairs.max()) + 1
+    deg = np.bincount(pairs[:, 0], minlength=n)
+    order = np.lexsort((np.arange(n), deg))
+    rank = np.empty(n, np.int64)
+    rank[order] = np.arange(n)
+    ru, rv = rank[pairs[:, 0]], rank[pairs[:, 1]]
+    keep = ru < rv
+    o = np.lexsort((rv[keep], ru[keep]))
+    dst = rv[keep][o].astype(np.uint32)
+    off = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(ru[keep], minlength=n), out=off[1:])
+    return dst, off
 
 
 def _free_port() -> int:
@@ -89,3 +156,51 @@ def test_count_distributed_gloo(golden, world):
     bounds = res[0][3]
     assert bounds[0] == 0 and bounds[-1] == rec["m"] and list(bounds) == sorted(bounds)
     assert all(r[3] == bounds for r in res)
+
+
+def _worker_sharded(rank, world, port, pairs, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        b = shard_bounds(pairs.shape[0], world)
+        ops = OracleOps()
+        n = int(pairs.max()) + 1
+        holder = {}
+        orig = ops.finalize
+
+        def fin(g):
+            orig(g)
+            holder["g"] = g
+        ops.finalize = fin
+        rep = count_distributed_sharded(ops, pairs[b[rank]:b[rank + 1]], n)
+        g = holder["g"]
+        q.put((rank, rep.triangles, rep.local, rep.bounds, rep.m, None, g["dst"].copy(), g["off"].copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,shuffle", [(2, False), (3, True), (4, False)])
+def test_count_distributed_sharded_gloo(golden, world, shuffle):
+    """v2: sharded degrees -> ranks -> local orient/sort -> all-to-all by source range ->
+    placed slices -> all-gather; every rank ends with the same rank-space CSR as a
+    single-process build and the golden triangle count."""
+    rec = golden["graphs"]["rmat_12_16_99"]
+    pairs = oracle.symmetrize(oracle.rmat_pairs(12, 16, seed=99))
+    if shuffle:
+        pairs = pairs[np.random.default_rng(7).permutation(pairs.shape[0])]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_sharded, args=(r, world, port, pairs, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=180) for _ in range(world)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert {r[1] for r in res} == {rec["triangles"]}
+    assert sum(r[2] for r in res) == rec["triangles"]
+    dst, off = _rank_space_csr(pairs)
+    for r in res:
+        assert r[4] == rec["m"]
+        assert np.array_equal(r[6], dst) and np.array_equal(r[7], off)

@@ -1,0 +1,95 @@
+"""The v2 sharded path (count_distributed_sharded) through libtcb200 on ONE GPU: two or
+three processes share cuda:0 under gloo, staging every collective through host memory
+(B200Ops(comm="cpu")).  Device steps are the ones NCCL ranks run; only the transport
+differs.  Checks the golden count and that every rank rebuilt the same rank-space CSR as
+the single-GPU rank-space preprocess."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, scale, seed, on_device, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), TC_DEVICE="0")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1503_00576_b200 as tcb
+        from paper_1503_00576_b200 import generators
+        from paper_1503_00576_b200.distributed import (B200Ops, count_distributed_sharded,
+                                                       shard_bounds)
+        ops = B200Ops(0, comm="cpu")
+        dev = generators.rmat_device(scale, 16, seed=seed)
+        b = shard_bounds(dev.npairs, world)
+        if on_device:
+            shard = generators.DeviceEdgesView(dev, b[rank], b[rank + 1])
+        else:
+            shard = dev.to_host().edges[b[rank]:b[rank + 1]]
+        holder = {}
+        orig = ops.finalize
+
+        def fin(g):
+            orig(g)
+            holder["g"] = g
+        ops.finalize = fin
+        rep = count_distributed_sharded(ops, shard, dev.num_vertices)
+        g = holder["g"]
+        og = tcb.OrientedGraph._from_device(g)
+        ref, _ = tcb.preprocess_device(dev, rank_space=True)
+        same = (np.array_equal(og.edge_dst, ref.edge_dst) and np.array_equal(og.node_offsets, ref.node_offsets)
+                and np.array_equal(og.edge_src, ref.edge_src))
+        q.put((rank, rep.triangles, rep.local, rep.m, same))
+    except Exception as e:  # noqa: BLE001 - surfaced through the queue
+        q.put((rank, repr(e), None, None, False))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,on_device", [(2, True), (3, False)])
+def test_sharded_preprocess_one_gpu(golden, world, on_device):
+    rec = golden["graphs"]["rmat_12_16_99"]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, 12, 99, on_device, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=300) for _ in range(world)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs), res
+    assert {r[1] for r in res} == {rec["triangles"]}, res
+    assert sum(r[2] for r in res) == rec["triangles"]
+    assert all(r[3] == rec["m"] and r[4] for r in res), res
+
+
+def test_sharded_preprocess_one_gpu_big():
+    """R-MAT s20 over 2 sharing processes == the single-GPU golden count."""
+    import json
+    from conftest import GOLDEN_DIR
+    with open(os.path.join(GOLDEN_DIR, "golden_big.json")) as fh:
+        want = json.load(fh)["rmat_20_16_0"]["triangles"]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, 20, 0, True, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=600) for _ in range(2)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+    assert {r[1] for r in res} == {want}, res
+    assert all(r[4] for r in res)
