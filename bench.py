@@ -17,6 +17,7 @@ over NCCL, shards are work balanced, one 64-bit all-reduce; timing = max over ra
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -24,6 +25,8 @@ import subprocess
 import sys
 import tempfile
 import time
+
+import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -42,6 +45,10 @@ def parse():
     ap.add_argument("--edge-factor", type=int, default=16)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--dist", choices=["v1", "v2"], default="v2",
+                    help="multi-GPU path: v1 rank-0 preprocess + broadcast, v2 sharded preprocess")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="testing only: all ranks on cuda:0, gloo, collectives staged through host")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU work per baseline sample step")
@@ -164,6 +171,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.share_gpu:
+        local = 0
     os.environ.setdefault("TC_DEVICE", str(local))
     workload = f"rmat_s{args.scale}_ef{args.edge_factor}_seed{args.seed}"
 
@@ -174,13 +183,17 @@ def main():
 
     import paper_1503_00576_b200 as tcb
     from paper_1503_00576_b200 import _lib, generators
-    from paper_1503_00576_b200.distributed import B200Ops, count_distributed
+    from paper_1503_00576_b200.distributed import (B200Ops, count_distributed,
+                                                   count_distributed_sharded, shard_bounds)
 
     dist = None
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     L = _lib.lib()
 
     def timer(a):
@@ -207,7 +220,7 @@ def main():
     def max_over_ranks(x):
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if args.share_gpu else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -220,13 +233,18 @@ def main():
     W = tcb.merge_work(og)
     assert og.m_dir == m
     host_graph = None
-    ops = B200Ops(local) if world > 1 else None
+    ops = B200Ops(local, comm="cpu" if args.share_gpu else "cuda") if world > 1 else None
+    sb = shard_bounds(npairs, world)
+    shard = generators.DeviceEdgesView(dev_edges, sb[rank], sb[rank + 1])
 
     def step_device():
         if world == 1:
             tri, t = tcb.count_with_timings_device(dev_edges)
             return tri, t.preprocess_ms, t.count_ms
-        rep = count_distributed(ops, dev_edges if rank == 0 else None)
+        if args.dist == "v1":
+            rep = count_distributed(ops, dev_edges if rank == 0 else None)
+        else:
+            rep = count_distributed_sharded(ops, shard, dev_edges.num_vertices)
         return rep.triangles, None, None
 
     for _ in range(args.warmup):
@@ -296,6 +314,25 @@ def main():
                "ms_per_step": e2e_ms / e2e_steps,
                "preprocess_ms_incl_h2d": statistics.mean(p.preprocess_ms for p in phase),
                "count_ms": statistics.mean(p.count_ms for p in phase)}
+    elif world > 1 and e2e_steps > 0:
+        # every rank copies only its own shard of the pinned host edge array (sharded H2D)
+        host_shard = generators.pinned_empty((shard.npairs, 2), np.uint32)
+        if shard.npairs:
+            _lib.check(L.tc_memcpy(_lib.ptr(host_shard), ctypes.c_void_p(shard.ptr), shard.nbytes, 1))
+        count_distributed_sharded(ops, host_shard, dev_edges.num_vertices)  # warm
+        barrier()
+        timer(2)
+        for _ in range(e2e_steps):
+            rep = count_distributed_sharded(ops, host_shard, dev_edges.num_vertices)
+            if rep.triangles != tri_ref:
+                raise RuntimeError("e2e count differs")
+        timer(3)
+        barrier()
+        e2e_ms = max_over_ranks(elapsed(2, 3))
+        e2e = {"value": m * e2e_steps / (e2e_ms / 1e3), "unit": "edges/s",
+               "h2d_bytes_per_step": npairs * 8, "d2h_bytes_per_step": 8 * world,
+               "ms_per_step": e2e_ms / e2e_steps,
+               "path": "sharded H2D (each rank its 1/N of the pinned pairs) + v2 distributed preprocessing"}
 
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
@@ -315,7 +352,10 @@ def main():
                        "undirected_edges": m, "pairs": npairs, "triangles": tri_ref,
                        "merge_work_W": W, "inputs_vs_L2": "inputs 8*pairs bytes >> 126 MB L2; no flush",
                        "parallelism": f"{world} GPU(s)" + ("" if world == 1 else
-                                      ": rank-0 preprocess, NCCL CSR broadcast, work-balanced shards, 1 all-reduce")},
+                                      (": rank-0 preprocess, NCCL CSR broadcast, work-balanced shards, 1 all-reduce"
+                                       if args.dist == "v1" else
+                                       ": sharded degrees/orient/sort, NCCL all-to-all by source range, "
+                                       "slice all-gather, work-balanced shards, 1 all-reduce"))},
             "phases_ms": {"preprocess": statistics.mean(pre) if pre else None,
                           "count": statistics.mean(cnt) if cnt else None,
                           "count_heavy": heavy_ms, "count_window": window_ms,

@@ -75,6 +75,9 @@ class Ops:
 
     # ---- v2 (sharded preprocessing); tensors returned/accepted are "comm" tensors,
     # i.e. ready for the process group's backend
+    def stage(self, shard):  # host shard -> device copy (once per call); device shards as-is
+        return shard
+
     def shard_degrees(self, shard, n: int):  # -> int32[n]
         raise NotImplementedError
 
@@ -182,6 +185,7 @@ def count_distributed_sharded(ops: Ops, shard, num_vertices: int, group=None) ->
     world = dist.get_world_size(group)
     n = int(num_vertices)
     gr = [dist.get_global_rank(group, r) if group is not None else r for r in range(world)]
+    shard = ops.stage(shard)  # host shards: this rank's H2D copy, once
     # 1. global degrees
     deg = ops.shard_degrees(shard, n)
     dist.all_reduce(deg, op=dist.ReduceOp.SUM, group=group)
@@ -360,6 +364,19 @@ class B200Ops(Ops):
             return ctypes.c_void_p(shard.ptr), int(shard.npairs), 1
         arr = shard.edges if hasattr(shard, "edges") else shard
         return _lib.ptr(arr), int(arr.shape[0]), 0
+
+    def stage(self, shard):
+        if hasattr(shard, "ptr"):
+            return shard
+        from .generators import DeviceEdges
+        arr = shard.edges if hasattr(shard, "edges") else shard
+        arr = np.ascontiguousarray(arr, dtype=np.uint32)
+        p = ctypes.c_void_p()
+        _lib.check(_lib.lib().tc_device_alloc(max(arr.nbytes, 16), ctypes.byref(p)))
+        d = DeviceEdges(p.value, arr.shape[0], 0)
+        if arr.size:
+            _lib.check(_lib.lib().tc_memcpy(p, _lib.ptr(arr), arr.nbytes, 0))
+        return d
 
     def shard_degrees(self, shard, n):
         import torch
