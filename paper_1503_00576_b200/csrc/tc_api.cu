@@ -476,7 +476,8 @@ int tc_count_with_timings(const uint32_t *pairs, uint64_t npairs, uint64_t nvert
     TC_CUDA(cudaEventRecord(ev.e[2], s));
     TC_CUDA(cudaMemsetAsync(g_total, 0, sizeof(unsigned long long), s));
     CountStats st;
-    rc = count_range_dev(g, 0, g.m, algo, g_total, s, nullptr);
+    static const bool want_stats = getenv("TC_COUNT_STATS") && atoi(getenv("TC_COUNT_STATS"));
+    rc = count_range_dev(g, 0, g.m, algo, g_total, s, want_stats ? &st : nullptr);
     if (rc) {
         if (owned) dfree(owned, s);
         graph_release(&g, s);
@@ -495,6 +496,12 @@ int tc_count_with_timings(const uint32_t *pairs, uint64_t npairs, uint64_t nvert
         t->preprocess_ms = ms_between(ev.e[1], ev.e[2]);
         t->count_ms = ms_between(ev.e[2], ev.e[3]);
         t->total_ms = ms_between(ev.e[0], ev.e[3]);
+        if (want_stats) {
+            t->classify_ms = st.classify_ms;
+            t->heavy_ms = st.heavy_ms;
+            t->light_ms = st.light_ms;
+            t->heavy_tasks = st.heavy_tasks;
+        }
     }
     return 0;
 }

@@ -419,6 +419,243 @@ __global__ void __launch_bounds__(NT)
     block_add_total(acc, total);
 }
 
+// ------------------------------------------------------------ light, TPE ---
+// Thread per oriented edge (u, v) with a light source (d+(u) <= 32).  In rank space
+// (RANKED) ranks increase along a list and every element of adj(v) exceeds v, so only the
+// suffix A = adj(u) after v -- dst[e+1, eu), <= 31 elements -- can close a triangle;
+// otherwise A is all of adj(u).  B = adj(v).  The intersection |A ∩ B| is taken by one of
+//  * bitmap test (HUB, v a dense hub, |A| < |B|): each element of A is one bit of v's
+//    global bitmap (independent loads);
+//  * binary search (skewed lengths, |A| log|B| < |A| + |B|): each element of A is
+//    searched in B, the lower bound moving forward monotonically;
+//  * merge: VEC = 4-wide block merge over aligned 16-byte chunks of A and B (16 compares
+//    per step, the block with the smaller maximum advances, ~(|A|+|B|)/4 dependent
+//    steps); otherwise the scalar branch-free two-pointer merge.
+// VEC needs sentinels outside the id range: rank space, n <= 2^32 - 2, elements >= 1.
+__device__ __forceinline__ uint32_t eq4(uint32_t x, const uint4 &b) {
+    return (x == b.x) | (x == b.y) | (x == b.z) | (x == b.w);
+}
+
+template <typename OffT, bool RANKED, bool HUB, bool VEC>
+__global__ void __launch_bounds__(256)
+    k_count_light_tpe(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
+                      const OffT *__restrict__ off, const RangeDev *__restrict__ rg, uint32_t hz,
+                      uint32_t vt, const uint32_t *__restrict__ dense_off,
+                      const uint32_t *__restrict__ dense_bits, uint32_t dense_words,
+                      unsigned long long *__restrict__ total) {
+    const uint64_t lo = rg->lo, hi = rg->hi;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint32_t acc = 0;
+    for (uint64_t e = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < hi; e += stride) {
+        const uint32_t u = __ldg(src + e);
+        const OffT su = __ldg(off + u), eu = __ldg(off + u + 1);
+        OffT i = RANKED ? (OffT)e + 1 : su;
+        if (eu - su > (OffT)kLightMax || i >= eu) continue;
+        const uint32_t v = __ldg(dst + e);
+        OffT j = __ldg(off + v);
+        const OffT je = __ldg(off + v + 1);
+        if (j >= je) continue;
+        const uint32_t la = (uint32_t)(eu - i), lb = (uint32_t)(je - j);
+        if (HUB && v >= vt && la < lb) {
+            const uint32_t bias = __ldg(dense_off + (v - vt)) - (((v + 1 - hz) >> 5) & ~3u);
+            for (; i < eu; ++i) {
+                const uint32_t r = __ldg(dst + i) - hz;
+                const uint32_t wi = min(bias + (r >> 5), dense_words - 1);
+                acc += (__ldg(dense_bits + wi) >> (r & 31)) & 1u;
+            }
+            continue;
+        }
+        if (la * (32u - __clz(lb)) < la + lb) {
+            for (; i < eu && j < je; ++i) {
+                const uint32_t a = __ldg(dst + i);
+                OffT n = je - j;  // lower_bound(a) in [j, je)
+                while (n > 0) {
+                    const OffT h = n >> 1;
+                    if (__ldg(dst + j + h) < a) { j += h + 1; n -= h + 1; }
+                    else n = h;
+                }
+                if (j < je && __ldg(dst + j) == a) { ++acc; ++j; }
+            }
+            continue;
+        }
+        if (VEC) {
+            OffT pa = i & ~(OffT)3, pb = j & ~(OffT)3;
+            for (;;) {
+                const uint4 qa = __ldg(reinterpret_cast<const uint4 *>(dst + pa));
+                const uint4 qb = __ldg(reinterpret_cast<const uint4 *>(dst + pb));
+                // invalid A lanes -> 0, invalid B lanes -> ~0: neither is a valid element
+                const uint32_t a0 = pa + 0 >= i && pa + 0 < eu ? qa.x : 0u;
+                const uint32_t a1 = pa + 1 >= i && pa + 1 < eu ? qa.y : 0u;
+                const uint32_t a2 = pa + 2 >= i && pa + 2 < eu ? qa.z : 0u;
+                const uint32_t a3 = pa + 3 < eu ? qa.w : 0u;
+                uint4 bb;
+                bb.x = pb + 0 >= j && pb + 0 < je ? qb.x : ~0u;
+                bb.y = pb + 1 >= j && pb + 1 < je ? qb.y : ~0u;
+                bb.z = pb + 2 >= j && pb + 2 < je ? qb.z : ~0u;
+                bb.w = pb + 3 < je ? qb.w : ~0u;
+                acc += eq4(a0, bb) + eq4(a1, bb) + eq4(a2, bb) + eq4(a3, bb);
+                // block maxima; a block that ends its list counts as +inf
+                const uint32_t amax = pa + 4 <= eu ? qa.w : ~0u;
+                const uint32_t bmax = pb + 4 <= je ? qb.w : ~0u;
+                if (amax <= bmax) pa += 4;
+                if (bmax <= amax) pb += 4;
+                if (pa >= eu || pb >= je) break;
+            }
+            continue;
+        }
+        uint32_t a = __ldg(dst + i), b = __ldg(dst + j);
+        for (;;) {
+            acc += a == b;
+            const bool sa = a <= b, sb = b <= a;
+            i += sa;
+            j += sb;
+            if (i >= eu || j >= je) break;
+            if (sa) a = __ldg(dst + i);
+            if (sb) b = __ldg(dst + j);
+        }
+    }
+    block_add_total(acc, total);
+}
+
+// ----------------------------------------------------------- light, warp ---
+// Rank space, light sources.  One warp per window of 32 consecutive oriented edges, no
+// block-level synchronisation.  For lane e = (u, v) only the suffix A_e = dst[e+1, eu)
+// of adj(u) can close a triangle (ranks increase along a list, every element of adj(v)
+// exceeds v), and eu <= e + 32 for a light u, so every A_e of the window lies in
+// dst[ws+1, ws+64): the warp stages that slice in shared memory once.  Per edge:
+//  * dense-hub v with |A| < |B| (HUB): the lane tests its <= 31 suffix elements in v's
+//    global bitmap (independent loads);
+//  * strongly skewed |B| > kSkew |A|: the lane binary-searches each suffix element in
+//    adj(v) (moving lower bound);
+//  * otherwise the items of all B = adj(v) of the window are flattened over the 32 lanes
+//    as 16-byte chunks (warp scan of chunk counts) and every item w is looked up in its
+//    edge's A by a fixed 5-step binary search in shared memory.
+constexpr int kLwWarps = 8;  // warps per CTA
+
+template <typename OffT, bool HUB>
+__global__ void __launch_bounds__(32 * kLwWarps)
+    k_count_light_warp(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
+                       const OffT *__restrict__ off, const RangeDev *__restrict__ rg, uint32_t hz,
+                       uint32_t vt, const uint32_t *__restrict__ dense_off,
+                       const uint32_t *__restrict__ dense_bits, uint32_t dense_words,
+                       uint32_t skew, unsigned long long *__restrict__ total) {
+    __shared__ uint32_t s_list[kLwWarps][64];
+    __shared__ OffT s_cb[kLwWarps][32], s_vs[kLwWarps][32], s_ve[kLwWarps][32];
+    __shared__ uint32_t s_a[kLwWarps][32], s_cst[kLwWarps][33];
+    const unsigned lane = lane_id(), wp = threadIdx.x >> 5;
+    const uint64_t lo = rg->lo, hi = rg->hi, m = rg->m;
+    const uint64_t nwin = (hi - lo + 31) / 32;
+    const uint64_t wstride = (uint64_t)gridDim.x * kLwWarps;
+    uint32_t *list = s_list[wp];
+    const uint32_t lbase = smem_addr(list);
+    uint32_t acc = 0;
+    for (uint64_t wi = (uint64_t)blockIdx.x * kLwWarps + wp; wi < nwin; wi += wstride) {
+        const uint64_t ws = lo + wi * 32;
+        const uint64_t e = ws + lane;
+        // stage dst[ws+1, ws+65) (positions past m read as 0; never inside a suffix)
+        list[lane] = ws + 1 + lane < m ? __ldg(dst + ws + 1 + lane) : 0u;
+        list[32 + lane] = ws + 33 + lane < m ? __ldg(dst + ws + 33 + lane) : 0u;
+        __syncwarp();
+        uint32_t chunks = 0, a0 = 0, a1 = 0;
+        OffT vs = 0, ve = 0;
+        if (e < hi) {
+            const uint32_t u = __ldg(src + e);
+            const OffT su = __ldg(off + u), eu = __ldg(off + u + 1);
+            if (eu - su <= (OffT)kLightMax && (OffT)e + 1 < eu) {
+                const uint32_t v = __ldg(dst + e);
+                vs = __ldg(off + v);
+                ve = __ldg(off + v + 1);
+                const uint32_t la = (uint32_t)(eu - (OffT)e - 1), lb = (uint32_t)(ve - vs);
+                a0 = lane;  // A_e = list[a0, a1)
+                a1 = lane + la;
+                if (lb == 0) {
+                } else if (HUB && v >= vt && la < lb) {
+                    const uint32_t bias = __ldg(dense_off + (v - vt)) - (((v + 1 - hz) >> 5) & ~3u);
+                    for (uint32_t k = a0; k < a1; ++k) {
+                        const uint32_t r = list[k] - hz;
+                        const uint32_t wi2 = min(bias + (r >> 5), dense_words - 1);
+                        acc += (__ldg(dense_bits + wi2) >> (r & 31)) & 1u;
+                    }
+                } else if (lb > skew * la) {
+                    OffT j = vs;
+                    for (uint32_t k = a0; k < a1 && j < ve; ++k) {
+                        const uint32_t a = list[k];
+                        OffT n = ve - j;
+                        while (n > 0) {
+                            const OffT h = n >> 1;
+                            if (__ldg(dst + j + h) < a) { j += h + 1; n -= h + 1; }
+                            else n = h;
+                        }
+                        if (j < ve && __ldg(dst + j) == a) { ++acc; ++j; }
+                    }
+                } else {
+                    chunks = (uint32_t)((ve - (vs & ~(OffT)3) + 3) >> 2);
+                }
+            }
+        }
+        const uint32_t incl = warp_inclusive_scan(chunks);
+        const uint32_t tot = __shfl_sync(TC_FULL_MASK, incl, 31);
+        const uint32_t cst = incl - chunks;
+        s_cb[wp][lane] = (vs & ~(OffT)3) - (OffT)(4 * cst);
+        s_vs[wp][lane] = vs;
+        s_ve[wp][lane] = ve;
+        s_a[wp][lane] = a0 | (a1 << 8);
+        s_cst[wp][lane] = cst;
+        if (lane == 0) s_cst[wp][32] = tot;
+        __syncwarp();
+        if (tot) {
+            // owner k of chunk c: largest k with cst[k] <= c (edges without chunks have
+            // cst[k] == cst[k+1] and are skipped by the forward advance)
+            uint32_t c = lane < tot ? lane : tot - 1;
+            uint32_t k = 0;
+            {
+                uint32_t a = 0, b = 32;
+                while (b - a > 1) {
+                    const uint32_t mid = (a + b) >> 1;
+                    if (s_cst[wp][mid] <= c) a = mid; else b = mid;
+                }
+                k = a;
+            }
+            uint32_t nextb = s_cst[wp][k + 1];
+            OffT cb = s_cb[wp][k], lo_k = s_vs[wp][k];
+            uint32_t span = (uint32_t)(s_ve[wp][k] - lo_k), ab = s_a[wp][k];
+            for (uint32_t base = 0; base < tot; base += 32) {
+                c = base + lane;
+                const bool live = c < tot;
+                c = live ? c : tot - 1;
+                if (c >= nextb) {
+                    do { nextb = s_cst[wp][++k + 1]; } while (c >= nextb);
+                    cb = s_cb[wp][k];
+                    lo_k = s_vs[wp][k];
+                    span = (uint32_t)(s_ve[wp][k] - lo_k);
+                    ab = s_a[wp][k];
+                }
+                const OffT p = cb + (OffT)(4 * c);
+                const uint4 q = __ldg(reinterpret_cast<const uint4 *>(dst + p));
+                const uint32_t rel = (uint32_t)(p - lo_k), sp = live ? span : 0u;
+                const uint32_t ka = ab & 0xff, kb = ab >> 8;
+                const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const uint32_t w = w4[t];
+                    // lower bound of w in list[ka, kb) in 5 fixed steps
+                    uint32_t pos = ka;
+#pragma unroll
+                    for (uint32_t step = 16; step; step >>= 1) {
+                        const uint32_t qq = pos + step - 1;
+                        const uint32_t x = lds32(lbase + 4 * min(qq, 63u));
+                        pos = (qq < kb && x < w) ? pos + step : pos;
+                    }
+                    const uint32_t y = lds32(lbase + 4 * min(pos, 63u));
+                    acc += ((rel + t < sp) & (pos < kb) & (y == w)) ? 1u : 0u;
+                }
+            }
+        }
+        __syncwarp();
+    }
+    block_add_total(acc, total);
+}
+
 // ------------------------------------------------------------------ heavy ---
 template <typename OffT>
 __global__ void k_classify(const OffT *__restrict__ off, const RangeDev *__restrict__ rg,
@@ -896,7 +1133,24 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
         if (rc) return rc;
     }
     TC_CUDA(cudaEventRecord(ev[2], s));
-    {
+    // Light sources: 1 = thread per edge (default), 2 = warp windows, 0 = CTA windows.
+    static const int light_algo = getenv("TC_LIGHT") ? atoi(getenv("TC_LIGHT")) : 1;
+    if (light_algo == 2 && g.rank_space) {
+        const bool hub = g.hubstart && g.dense_bits;
+        static const uint32_t skew = getenv("TC_SKEW") ? (uint32_t)atoi(getenv("TC_SKEW")) : 32u;
+        auto kern = hub ? k_count_light_warp<OffT, true> : k_count_light_warp<OffT, false>;
+        kern<<<kSMs * 8, 32 * kLwWarps, 0, s>>>(g.src, g.dst, off, rg, g.hz, hub ? g.vt : 0xffffffffu,
+                                                g.dense_off, g.dense_bits, g.dense_words, skew, d_total);
+    } else if (light_algo == 1) {
+        const bool hub = g.rank_space && g.hubstart && g.dense_bits;
+        const bool vec = g.rank_space && g.n <= 0xfffffffeull && getenv("TC_LIGHT_VEC") &&
+                         atoi(getenv("TC_LIGHT_VEC"));
+        auto kern = hub ? (vec ? k_count_light_tpe<OffT, true, true, true> : k_count_light_tpe<OffT, true, true, false>)
+                    : g.rank_space ? (vec ? k_count_light_tpe<OffT, true, false, true> : k_count_light_tpe<OffT, true, false, false>)
+                                   : k_count_light_tpe<OffT, false, false, false>;
+        kern<<<kSMs * 8, 256, 0, s>>>(g.src, g.dst, off, rg, g.hz, hub ? g.vt : 0xffffffffu,
+                                      g.dense_off, g.dense_bits, g.dense_words, d_total);
+    } else {
         const bool hub = g.rank_space && g.hubstart;
         const uint32_t hwords = hub ? (uint32_t)((g.n - g.hz + 31) / 32) + 1 : 0u;
         auto kern = hub ? k_count_window<OffT, kWinThreads, true> : k_count_window<OffT, kWinThreads, false>;

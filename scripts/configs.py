@@ -15,9 +15,11 @@ def run(name, dev, reps=5):
     tri = {t[0] for t in ts}
     pre = statistics.median(t[1].preprocess_ms for t in ts)
     cnt = statistics.median(t[1].count_ms for t in ts)
+    hv = statistics.median(t[1].heavy_ms for t in ts)
+    lt = statistics.median(t[1].light_ms for t in ts)
     m = dev.npairs // 2
     print(json.dumps({"config": name, "m": m, "triangles": sorted(tri), "preprocess_ms": round(pre, 3),
-                      "count_ms": round(cnt, 3), "edges_per_s": m / ((pre + cnt) / 1e3)}), flush=True)
+                      "count_ms": round(cnt, 3), "heavy_ms": round(hv, 3), "light_ms": round(lt, 3), "edges_per_s": m / ((pre + cnt) / 1e3)}), flush=True)
 
 
 which = sys.argv[1:] or ["rmat20", "ba1e7", "rmat22"]
@@ -28,3 +30,5 @@ for w in which:
         run(w, generators.barabasi_albert_device(10_000_000, 9, seed=0))
     elif w == "ba1e6":
         run(w, generators.barabasi_albert_device(1_000_000, 9, seed=0))
+    elif w.startswith("rgg"):  # rgg2e7 -> n = 2*10^7, avg degree 32
+        run(w, generators.random_geometric_device(int(float(w[3:])), 32.0, seed=0))
