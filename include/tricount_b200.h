@@ -34,9 +34,10 @@ typedef struct tc_times {
     double count_ms;      /* counting kernels + 8-byte result copy               */
     double total_ms;      /* whole call                                          */
     double classify_ms;   /* count detail: source classification                 */
-    double heavy_ms;      /* count detail: shared-memory hash kernels            */
-    double light_ms;      /* count detail: warp-per-source register kernel       */
+    double heavy_ms;      /* count detail: u-major heavy-source kernels          */
+    double light_ms;      /* count detail: light-source kernel                   */
     uint64_t heavy_tasks; /* count detail: CTA tasks issued                      */
+    double vmajor_ms;     /* count detail: v-major hub-head kernel (in classify) */
 } tc_times;
 
 /* count algorithm selector */

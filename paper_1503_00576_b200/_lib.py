@@ -28,6 +28,7 @@ class TcTimes(ctypes.Structure):
         ("heavy_ms", ctypes.c_double),
         ("light_ms", ctypes.c_double),
         ("heavy_tasks", ctypes.c_uint64),
+        ("vmajor_ms", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

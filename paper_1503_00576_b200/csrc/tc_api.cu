@@ -164,6 +164,7 @@ static int count_ranges(const DeviceGraph &g, const int64_t *bounds, int npools,
         agg.classify_ms += st.classify_ms;
         agg.heavy_ms += st.heavy_ms;
         agg.light_ms += st.light_ms;
+        agg.vmajor_ms += st.vmajor_ms;
         agg.heavy_tasks += st.heavy_tasks;
     }
     unsigned long long h = 0;
@@ -178,6 +179,7 @@ static int count_ranges(const DeviceGraph &g, const int64_t *bounds, int npools,
         t->classify_ms = agg.classify_ms;
         t->heavy_ms = agg.heavy_ms;
         t->light_ms = agg.light_ms;
+        t->vmajor_ms = agg.vmajor_ms;
         t->heavy_tasks = agg.heavy_tasks;
     }
     return 0;
@@ -501,6 +503,7 @@ int tc_count_with_timings(const uint32_t *pairs, uint64_t npairs, uint64_t nvert
             t->heavy_ms = st.heavy_ms;
             t->light_ms = st.light_ms;
             t->heavy_tasks = st.heavy_tasks;
+            t->vmajor_ms = st.vmajor_ms;
         }
     }
     return 0;

@@ -419,6 +419,26 @@ __global__ void __launch_bounds__(NT)
     block_add_total(acc, total);
 }
 
+// ------------------------------------------------------- v-major choice ---
+// Edge e = (u, v) with v in the hub zone runs v-major (k_count_vmajor: re-reads the
+// suffix of adj(u) after v, 4 B per item) when that is cheaper than the u-major read of
+// v's data (dense bitmap words, or adj(v) as 16-byte chunks).  Every kernel evaluates the
+// same predicate, so each edge is counted exactly once.  Edges with an empty suffix or
+// an empty adj(v) close no triangle and are skipped by everyone.
+struct VSplit {
+    uint32_t hz, vt, hwp, factor;  // hz = 0xffffffff: v-major off
+};
+
+__device__ __forceinline__ bool vmajor_edge(const VSplit &vp, uint32_t e, uint32_t eu, uint32_t v,
+                                            uint32_t vs, uint32_t ve) {
+    if (v < vp.hz) return false;
+    if (e + 1 >= eu || vs >= ve) return true;  // no work either way
+    const uint32_t ws = ((v + 1 - vp.hz) >> 5) & ~3u;
+    const bool dense = v >= vp.vt && (vp.hwp - ws) < vp.factor * (ve - vs);
+    const uint32_t ucost = dense ? 4 * (vp.hwp - ws) : 16 * ((ve - (vs & ~3u) + 3) >> 2);
+    return 4 * (eu - e - 1) + 8 < ucost;
+}
+
 // ------------------------------------------------------------ light, TPE ---
 // Thread per oriented edge (u, v) with a light source (d+(u) <= 32).  In rank space
 // (RANKED) ranks increase along a list and every element of adj(v) exceeds v, so only the
@@ -442,7 +462,7 @@ __global__ void __launch_bounds__(256)
                       const OffT *__restrict__ off, const RangeDev *__restrict__ rg, uint32_t hz,
                       uint32_t vt, const uint32_t *__restrict__ dense_off,
                       const uint32_t *__restrict__ dense_bits, uint32_t dense_words,
-                      unsigned long long *__restrict__ total) {
+                      VSplit vp, unsigned long long *__restrict__ total) {
     const uint64_t lo = rg->lo, hi = rg->hi;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     uint32_t acc = 0;
@@ -455,6 +475,7 @@ __global__ void __launch_bounds__(256)
         OffT j = __ldg(off + v);
         const OffT je = __ldg(off + v + 1);
         if (j >= je) continue;
+        if (RANKED && vmajor_edge(vp, (uint32_t)e, (uint32_t)eu, v, (uint32_t)j, (uint32_t)je)) continue;
         const uint32_t la = (uint32_t)(eu - i), lb = (uint32_t)(je - j);
         if (HUB && v >= vt && la < lb) {
             const uint32_t bias = __ldg(dense_off + (v - vt)) - (((v + 1 - hz) >> 5) & ~3u);
@@ -659,8 +680,9 @@ __global__ void __launch_bounds__(32 * kLwWarps)
 // ------------------------------------------------------------------ heavy ---
 template <typename OffT>
 __global__ void k_classify(const OffT *__restrict__ off, const RangeDev *__restrict__ rg,
-                           uint2 *__restrict__ t0, uint2 *__restrict__ t1, uint2 *__restrict__ t2,
-                           uint2 *__restrict__ t3, unsigned *__restrict__ ntasks) {
+                           const uint32_t *__restrict__ hend, uint2 *__restrict__ t0,
+                           uint2 *__restrict__ t1, uint2 *__restrict__ t2, uint2 *__restrict__ t3,
+                           unsigned *__restrict__ ntasks) {
     const uint64_t lo = rg->lo, hi = rg->hi;
     const uint32_t u_lo = rg->u_lo, u_hi = rg->u_hi;
     const uint32_t stride = gridDim.x * blockDim.x;
@@ -669,7 +691,8 @@ __global__ void k_classify(const OffT *__restrict__ off, const RangeDev *__restr
         const uint32_t d = (uint32_t)(e - s);
         if (d <= (uint32_t)kLightMax) continue;
         const uint64_t es = (uint64_t)s > lo ? (uint64_t)s : lo;
-        const uint64_t ee = (uint64_t)e < hi ? (uint64_t)e : hi;
+        uint64_t ee = (uint64_t)e < hi ? (uint64_t)e : hi;
+        if (hend && (uint64_t)hend[u] < ee) ee = hend[u];  // v-major: hub heads excluded
         if (es >= ee) continue;
         const int cls = d <= kClassMax[0] ? 0 : d <= kClassMax[1] ? 1 : d <= kClassMax[2] ? 2 : 3;
         const uint32_t chunks = (uint32_t)((ee - es + kChunk - 1) / kChunk);
@@ -790,7 +813,7 @@ __global__ void __launch_bounds__(NT)
     k_count_hub(const uint32_t *__restrict__ dst, const uint32_t *__restrict__ off,
                 const uint32_t *__restrict__ hubstart, uint32_t hz, uint32_t hwords,
                 uint32_t vt, const uint32_t *__restrict__ dense_off,
-                const uint32_t *__restrict__ dense_bits, uint32_t dense_factor,
+                const uint32_t *__restrict__ dense_bits, uint32_t dense_factor, VSplit vp,
                 const RangeDev *__restrict__ rg, const uint2 *__restrict__ tasks,
                 const unsigned *__restrict__ ntasks, unsigned *__restrict__ next, uint32_t cap,
                 unsigned long long *__restrict__ total) {
@@ -854,15 +877,19 @@ __global__ void __launch_bounds__(NT)
                 v = __ldg(dst + ws + threadIdx.x);
                 vs = __ldg(off + v);
                 ve = __ldg(off + v + 1);
-                // v's adjacency is also a bitmap: AND with B_u when its words cost less
-                // than probing its items (~3.5 vs ~12 instructions per unit)
-                if (v >= vt) {
-                    dws = ((v + 1 - hz) >> 5) & ~3u;
-                    dense = (hwords - dws) < dense_factor * (ve - vs);
-                    if (dense) dgo = __ldg(dense_off + (v - vt));
+                if (vmajor_edge(vp, (uint32_t)(ws + threadIdx.x), e, v, vs, ve)) {
+                    vs = ve = 0;  // counted by k_count_vmajor
+                } else {
+                    // v's adjacency is also a bitmap: AND with B_u when its words cost less
+                    // than probing its items (~3.5 vs ~12 instructions per unit)
+                    if (v >= vt) {
+                        dws = ((v + 1 - hz) >> 5) & ~3u;
+                        dense = (hwords - dws) < dense_factor * (ve - vs);
+                        if (dense) dgo = __ldg(dense_off + (v - vt));
+                    }
+                    if (dense) vs = ve = 0;
+                    else hv = __ldg(hubstart + v);
                 }
-                if (dense) vs = ve = 0;
-                else hv = __ldg(hubstart + v);
             }
             // pass 0: hub suffixes [hv, ve) of sparse edges against the bitmap;
             // pass 1: non-hub prefixes [vs, hv) against the cuckoo table (only if adj(u)
@@ -915,6 +942,158 @@ __global__ void __launch_bounds__(NT)
         for (uint32_t i = nh + threadIdx.x; i < e - s; i += NT)
             bitmap[(__ldg(dst + s + i) - hz) >> 5] = 0;
         __syncthreads();
+    }
+    block_add_total(acc, total);
+}
+
+// ---------------------------------------------------------------- v-major ---
+// Rank space, edges e = (u, v) whose head v is in the hub zone [hz, n) (R-MAT s26: 77 % of
+// all edges, ~90 % of the u-major kernels' bytes).  adj(v) lies in (v, n), inside the hub
+// zone, and only the suffix of adj(u) after v -- dst[e+1, off[u+1]) -- can close a
+// triangle.  Grouping these edges by v lets a CTA stage adj(v) ONCE as a shared-memory
+// bitmap over hub words [ws(v), hwp) and stream the suffixes of all of v's in-edges
+// against it (one LDS bit test per item): the re-read data becomes the suffixes of adj(u)
+// (coalesced streams, 4 B per item) instead of adj(v) / v's bitmap per in-edge.
+//
+// Index: in-edges of each hub head, counting sort by v (only edges whose suffix and adj(v)
+// are both non-empty); tasks = (v, chunk of kVChunk in-edges) in v order.
+constexpr uint32_t kVChunk = 2048;
+
+__global__ void __launch_bounds__(256)
+    k_vin_count(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
+                const uint32_t *__restrict__ off, const RangeDev *__restrict__ rg, VSplit vp,
+                uint32_t *__restrict__ cnt) {
+    const uint64_t lo = rg->lo, hi = rg->hi;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t e = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < hi; e += stride) {
+        const uint32_t v = __ldg(dst + e);
+        if (v < vp.hz) continue;
+        const uint32_t eu = __ldg(off + __ldg(src + e) + 1), vs = __ldg(off + v), ve = __ldg(off + v + 1);
+        if (e + 1 >= eu || vs >= ve || !vmajor_edge(vp, (uint32_t)e, eu, v, vs, ve)) continue;
+        atomicAdd(cnt + (v - vp.hz), 1u);
+    }
+}
+
+// One block: start[i] = exclusive scan of cnt, tstart[i] = exclusive scan of task counts
+// ceil(cnt / kVChunk); start[nh], tstart[nh] = totals.  cnt is zeroed (fill cursors).
+__global__ void k_vin_scan(uint32_t *__restrict__ cnt, uint32_t nh, uint32_t *__restrict__ start,
+                           uint32_t *__restrict__ tstart) {
+    __shared__ uint32_t s_w[32], s_w2[32];
+    uint32_t carry = 0, tcarry = 0;
+    for (uint32_t b = 0; b < nh; b += blockDim.x) {
+        const uint32_t i = b + threadIdx.x;
+        const uint32_t x = i < nh ? cnt[i] : 0u;
+        const uint32_t tx = (x + kVChunk - 1) / kVChunk;
+        uint32_t t, tt;
+        const uint32_t e = block_exclusive_scan<uint32_t>(x, s_w, &t);
+        const uint32_t te = block_exclusive_scan<uint32_t>(tx, s_w2, &tt);
+        if (i < nh) {
+            start[i] = carry + e;
+            tstart[i] = tcarry + te;
+            cnt[i] = 0;
+        }
+        carry += t;
+        tcarry += tt;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        start[nh] = carry;
+        tstart[nh] = tcarry;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+    k_vin_fill(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
+               const uint32_t *__restrict__ off, const RangeDev *__restrict__ rg, VSplit vp,
+               const uint32_t *__restrict__ start, uint32_t *__restrict__ cursor,
+               uint32_t *__restrict__ in_e) {
+    const uint64_t lo = rg->lo, hi = rg->hi;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t e = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < hi; e += stride) {
+        const uint32_t v = __ldg(dst + e);
+        if (v < vp.hz) continue;
+        const uint32_t eu = __ldg(off + __ldg(src + e) + 1), vs = __ldg(off + v), ve = __ldg(off + v + 1);
+        if (e + 1 >= eu || vs >= ve || !vmajor_edge(vp, (uint32_t)e, eu, v, vs, ve)) continue;
+        const uint32_t h = v - vp.hz;
+        in_e[start[h] + atomicAdd(cursor + h, 1u)] = (uint32_t)e;
+    }
+}
+
+__global__ void k_vin_tasks(const uint32_t *__restrict__ start, const uint32_t *__restrict__ tstart,
+                            uint32_t nh, uint2 *__restrict__ tasks) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += stride) {
+        const uint32_t t0 = tstart[h], t1 = tstart[h + 1];
+        for (uint32_t t = t0; t < t1; ++t) tasks[t] = make_uint2(h, t - t0);
+    }
+}
+
+template <int NT, int U>
+__global__ void __launch_bounds__(NT)
+    k_count_vmajor(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
+                   const uint32_t *__restrict__ off, uint32_t hz, uint32_t hwp,
+                   const uint32_t *__restrict__ start, const uint32_t *__restrict__ in_e,
+                   const uint2 *__restrict__ tasks, const uint32_t *__restrict__ ntasks,
+                   unsigned *__restrict__ next, unsigned long long *__restrict__ total) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t *bitmap = reinterpret_cast<uint32_t *>(smem);  // hwp words
+    __shared__ uint32_t s_cb[NT], s_vs[NT], s_ve[NT];
+    __shared__ uint32_t s_cst[NT + 4];
+    __shared__ uint32_t s_scan[32];
+    __shared__ unsigned s_task;
+    constexpr int NW = NT / 32;
+    const unsigned warp = threadIdx.x >> 5;
+    const unsigned nt = *ntasks;
+    const EdgeTable<uint32_t> et{s_cb, s_vs, s_ve, s_cst, nullptr};
+    const uint32_t bm = smem_addr(bitmap);
+    unsigned long long acc = 0;
+    for (;;) {
+        if (threadIdx.x == 0) s_task = atomicAdd(next, 1u);
+        __syncthreads();
+        const unsigned t = s_task;
+        if (t >= nt) break;
+        const uint2 task = tasks[t];
+        const uint32_t h = task.x, v = hz + h;
+        const uint32_t vs = __ldg(off + v), ve = __ldg(off + v + 1);
+        const uint32_t ws = ((h + 1) >> 5) & ~3u;  // first hub word adj(v) can touch
+        for (uint32_t i = ws + 4 * threadIdx.x; i < hwp; i += 4 * NT)
+            *reinterpret_cast<uint4 *>(bitmap + i) = make_uint4(0, 0, 0, 0);
+        __syncthreads();
+        for (uint32_t i = vs + threadIdx.x; i < ve; i += NT) {
+            const uint32_t r = __ldg(dst + i) - hz;
+            atomicOr(bitmap + (r >> 5), 1u << (r & 31));
+        }
+        __syncthreads();
+        const uint32_t p0 = __ldg(start + h) + task.y * kVChunk;
+        const uint32_t p1 = min(p0 + kVChunk, __ldg(start + h + 1));
+        for (uint32_t ps = p0; ps < p1; ps += NT) {
+            const uint32_t nwin = min((uint32_t)NT, p1 - ps);
+            uint32_t chunks = 0, a = 0, b = 0;
+            if (threadIdx.x < nwin) {
+                const uint32_t e = __ldg(in_e + ps + threadIdx.x);
+                a = e + 1;
+                b = __ldg(off + __ldg(src + e) + 1);
+                chunks = (b - (a & ~3u) + 3) >> 2;  // a < b by construction
+            }
+            uint32_t tot;
+            const uint32_t cst = block_exclusive_scan<uint32_t>(chunks, s_scan, &tot);
+            s_cb[threadIdx.x] = (a & ~3u) - 4 * cst;
+            s_vs[threadIdx.x] = a;
+            s_ve[threadIdx.x] = b;
+            s_cst[threadIdx.x] = cst;
+            if (threadIdx.x == 0) s_cst[NT] = tot;
+            __syncthreads();
+            const uint32_t c0 = (uint32_t)((uint64_t)tot * warp / NW);
+            const uint32_t c1 = (uint32_t)((uint64_t)tot * (warp + 1) / NW);
+            if (c0 < c1) {
+                // suffix items are > v: their words are >= ws, inside the staged range
+                acc += sweep<uint32_t, false, U>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t) {
+                    const uint32_t r = w - hz;
+                    return ((lds32(bm + 4 * min(r >> 5, hwp - 1)) >> (r & 31)) & 1u) != 0u;
+                });
+            }
+            __syncthreads();
+        }
     }
     block_add_total(acc, total);
 }
@@ -1002,9 +1181,14 @@ size_t heavy_smem(int cls, uint32_t max_out) {
     return (size_t)4 * slots;
 }
 
+static uint32_t dense_factor_env() {
+    static const uint32_t f = getenv("TC_DENSE_FACTOR") ? (uint32_t)atoi(getenv("TC_DENSE_FACTOR")) : 3u;
+    return f;
+}
+
 template <int NT>
 int launch_hub(const DeviceGraph &g, const RangeDev *rg, const uint2 *tasks, const unsigned *ntasks,
-               unsigned *next, uint32_t cap, unsigned long long *d_total, cudaStream_t s) {
+               unsigned *next, uint32_t cap, bool vmajor, unsigned long long *d_total, cudaStream_t s) {
     const uint32_t hwords = g.hwp;
     const size_t sm = 4 * ((size_t)hwords + cap);
     static const int unroll = getenv("TC_HUB_UNROLL") ? atoi(getenv("TC_HUB_UNROLL")) : 4;
@@ -1015,8 +1199,10 @@ int launch_hub(const DeviceGraph &g, const RangeDev *rg, const uint2 *tasks, con
     if (per_sm < 1) per_sm = 1;
     static const uint32_t dense_factor =
         getenv("TC_DENSE_FACTOR") ? (uint32_t)atoi(getenv("TC_DENSE_FACTOR")) : 3u;
+    const VSplit vp{vmajor ? g.hz : 0xffffffffu, g.vt, g.hwp, dense_factor};
     kern<<<kSMs * per_sm, NT, sm, s>>>(g.dst, g.off32, g.hubstart, g.hz, hwords, g.vt, g.dense_off,
-                                       g.dense_bits, dense_factor, rg, tasks, ntasks, next, cap, d_total);
+                                       g.dense_bits, dense_factor, vp, rg, tasks, ntasks, next, cap,
+                                       d_total);
     TC_LAUNCHED();
     return 0;
 }
@@ -1073,6 +1259,63 @@ static void clear_l2_window(cudaStream_t s) {
     cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);  // give the carve-out back
 }
 
+// v-major phase: index the hub-head in-edges of [lo, hi) and count them (see k_count_vmajor).
+int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
+                 unsigned long long *d_total, cudaStream_t s, CountStats *stats) {
+    const uint32_t nh = (uint32_t)(g.n - g.hz);
+    uint32_t *cnt = nullptr, *start = nullptr, *tstart = nullptr, *in_e = nullptr;
+    unsigned *next = nullptr;
+    uint2 *tasks = nullptr;
+    TC_CHECK(dalloc_t(&cnt, nh, s));
+    TC_CHECK(dalloc_t(&start, (size_t)nh + 1, s));
+    TC_CHECK(dalloc_t(&tstart, (size_t)nh + 1, s));
+    TC_CHECK(dalloc_t(&in_e, span ? span : 1, s));
+    TC_CHECK(dalloc_t(&tasks, (size_t)nh + span / kVChunk + 1, s));
+    TC_CHECK(dalloc_t(&next, 1, s));
+    TC_CUDA(cudaMemsetAsync(cnt, 0, (size_t)nh * sizeof(uint32_t), s));
+    TC_CUDA(cudaMemsetAsync(next, 0, sizeof(unsigned), s));
+    const unsigned grid = grid_for(span, 256, kSMs * 16);
+    const VSplit vp{g.hz, g.vt, g.hwp, dense_factor_env()};
+    k_vin_count<<<grid, 256, 0, s>>>(g.src, g.dst, g.off32, rg, vp, cnt);
+    TC_LAUNCHED();
+    k_vin_scan<<<1, 1024 - 32, 0, s>>>(cnt, nh, start, tstart);  // block scan: <= 31 warps
+    TC_LAUNCHED();
+    k_vin_fill<<<grid, 256, 0, s>>>(g.src, g.dst, g.off32, rg, vp, start, cnt, in_e);
+    TC_LAUNCHED();
+    k_vin_tasks<<<grid_for(nh, 256, kSMs * 4), 256, 0, s>>>(start, tstart, nh, tasks);
+    TC_LAUNCHED();
+    constexpr int NT = 256;
+    auto kern = k_count_vmajor<NT, 4>;
+    const size_t sm = 4 * (size_t)g.hwp;
+    TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int per_sm = 1;
+    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, sm));
+    if (per_sm < 1) per_sm = 1;
+    cudaEvent_t e0, e1;
+    if (stats) {
+        TC_CUDA(cudaEventCreate(&e0));
+        TC_CUDA(cudaEventCreate(&e1));
+        TC_CUDA(cudaEventRecord(e0, s));
+    }
+    kern<<<kSMs * per_sm, NT, sm, s>>>(g.src, g.dst, g.off32, g.hz, g.hwp, start, in_e, tasks,
+                                       tstart + nh, next, d_total);
+    TC_LAUNCHED();
+    if (stats) {
+        TC_CUDA(cudaEventRecord(e1, s));
+        TC_CUDA(cudaEventSynchronize(e1));
+        cudaEventElapsedTime(&stats->vmajor_ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
+    dfree(cnt, s);
+    dfree(start, s);
+    dfree(tstart, s);
+    dfree(in_e, s);
+    dfree(tasks, s);
+    dfree(next, s);
+    return 0;
+}
+
 template <typename OffT>
 int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
                unsigned long long *d_total, cudaStream_t s, CountStats *stats) {
@@ -1100,11 +1343,23 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
     for (auto &e : ev) TC_CUDA(cudaEventCreate(&e));
     TC_CUDA(cudaEventRecord(ev[0], s));
     const uint32_t nverts = (uint32_t)(g.n < 0xffffffffull ? g.n : 0xffffffffull);
+    // v-major hub heads (rank space): every heavy class must run the hub kernel (which
+    // skips the hub-head edges), so it is all or nothing.
+    // TC_VMAJOR: -1 = auto (large skewed graphs: the in-edge index costs a few ms, the
+    // hub reuse it unlocks pays from ~10^8 edges with hub-sized out-degrees), 0 off, 1 on.
+    static const int vm_env = getenv("TC_VMAJOR") ? atoi(getenv("TC_VMAJOR")) : -1;
+    bool vmajor = vm_env != 0 && sizeof(OffT) == 4 && g.rank_space && g.hubstart && g.n > g.hz &&
+                  (vm_env == 1 || (g.m >= (1ull << 27) && g.max_out > 256));
+    for (int c = 0; c < kClasses && vmajor; ++c)
+        if (g.max_out > lower[c] &&
+            4 * ((size_t)g.hwp + 4 * (g.max_out < kClassMax[c] ? g.max_out : kClassMax[c])) > 200 * 1024)
+            vmajor = false;
     if (g.max_out > (uint32_t)kLightMax) {
-        k_classify<OffT><<<grid_for(nverts, 256, kSMs * 8), 256, 0, s>>>(off, rg, tasks[0], tasks[1],
-                                                                         tasks[2], tasks[3], counters);
+        k_classify<OffT><<<grid_for(nverts, 256, kSMs * 8), 256, 0, s>>>(
+            off, rg, nullptr, tasks[0], tasks[1], tasks[2], tasks[3], counters);
         TC_LAUNCHED();
     }
+    if (vmajor) TC_CHECK(count_vmajor(g, rg, span, d_total, s, stats));
     TC_CUDA(cudaEventRecord(ev[1], s));
     // Heavy classes first (largest tasks first), then the light sweep.
     for (int c = kClasses - 1; c >= 0; --c) {
@@ -1121,8 +1376,8 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
         const size_t hub_sm = 4 * ((size_t)g.hwp + hub_cap);
         if (sizeof(OffT) == 4 && g.rank_space && g.hubstart && hub_sm <= 200 * 1024) {
             const int ntc = c == 2 ? 512 : 256;
-            rc = ntc == 512 ? launch_hub<512>(g, rg, tasks[c], nt_c, next_c, hub_cap, d_total, s)
-                            : launch_hub<256>(g, rg, tasks[c], nt_c, next_c, hub_cap, d_total, s);
+            rc = ntc == 512 ? launch_hub<512>(g, rg, tasks[c], nt_c, next_c, hub_cap, vmajor, d_total, s)
+                            : launch_hub<256>(g, rg, tasks[c], nt_c, next_c, hub_cap, vmajor, d_total, s);
             if (rc) return rc;
             continue;
         }
@@ -1135,13 +1390,13 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
     TC_CUDA(cudaEventRecord(ev[2], s));
     // Light sources: 1 = thread per edge (default), 2 = warp windows, 0 = CTA windows.
     static const int light_algo = getenv("TC_LIGHT") ? atoi(getenv("TC_LIGHT")) : 1;
-    if (light_algo == 2 && g.rank_space) {
+    if (light_algo == 2 && g.rank_space && !vmajor) {
         const bool hub = g.hubstart && g.dense_bits;
         static const uint32_t skew = getenv("TC_SKEW") ? (uint32_t)atoi(getenv("TC_SKEW")) : 32u;
         auto kern = hub ? k_count_light_warp<OffT, true> : k_count_light_warp<OffT, false>;
         kern<<<kSMs * 8, 32 * kLwWarps, 0, s>>>(g.src, g.dst, off, rg, g.hz, hub ? g.vt : 0xffffffffu,
                                                 g.dense_off, g.dense_bits, g.dense_words, skew, d_total);
-    } else if (light_algo == 1) {
+    } else if (light_algo == 1 || vmajor) {
         const bool hub = g.rank_space && g.hubstart && g.dense_bits;
         const bool vec = g.rank_space && g.n <= 0xfffffffeull && getenv("TC_LIGHT_VEC") &&
                          atoi(getenv("TC_LIGHT_VEC"));
@@ -1149,7 +1404,9 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
                     : g.rank_space ? (vec ? k_count_light_tpe<OffT, true, false, true> : k_count_light_tpe<OffT, true, false, false>)
                                    : k_count_light_tpe<OffT, false, false, false>;
         kern<<<kSMs * 8, 256, 0, s>>>(g.src, g.dst, off, rg, g.hz, hub ? g.vt : 0xffffffffu,
-                                      g.dense_off, g.dense_bits, g.dense_words, d_total);
+                                      g.dense_off, g.dense_bits, g.dense_words,
+                                      VSplit{vmajor ? g.hz : 0xffffffffu, g.vt, g.hwp, dense_factor_env()},
+                                      d_total);
     } else {
         const bool hub = g.rank_space && g.hubstart;
         const uint32_t hwords = hub ? (uint32_t)((g.n - g.hz + 31) / 32) + 1 : 0u;

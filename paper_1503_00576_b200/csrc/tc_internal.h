@@ -155,7 +155,7 @@ int orient_compact_dev(const uint32_t *pairs, uint64_t npairs, const int64_t *de
 enum CountAlgo { kAlgoAuto = 0, kAlgoMergeThread = 1 };
 
 struct CountStats {
-    float classify_ms = 0, light_ms = 0, heavy_ms = 0;
+    float classify_ms = 0, light_ms = 0, heavy_ms = 0, vmajor_ms = 0;
     uint64_t light_vertices = 0, heavy_tasks = 0;
 };
 

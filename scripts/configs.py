@@ -17,9 +17,10 @@ def run(name, dev, reps=5):
     cnt = statistics.median(t[1].count_ms for t in ts)
     hv = statistics.median(t[1].heavy_ms for t in ts)
     lt = statistics.median(t[1].light_ms for t in ts)
+    vm = statistics.median(t[1].vmajor_ms for t in ts)
     m = dev.npairs // 2
     print(json.dumps({"config": name, "m": m, "triangles": sorted(tri), "preprocess_ms": round(pre, 3),
-                      "count_ms": round(cnt, 3), "heavy_ms": round(hv, 3), "light_ms": round(lt, 3), "edges_per_s": m / ((pre + cnt) / 1e3)}), flush=True)
+                      "count_ms": round(cnt, 3), "heavy_ms": round(hv, 3), "light_ms": round(lt, 3), "vmajor_ms": round(vm, 3), "edges_per_s": m / ((pre + cnt) / 1e3)}), flush=True)
 
 
 which = sys.argv[1:] or ["rmat20", "ba1e7", "rmat22"]
