@@ -11,7 +11,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtcb200.so")
+# TC_LIB_PATH: development override (A/B of compile-time variants)
+LIB_PATH = os.environ.get("TC_LIB_PATH") or os.path.join(_HERE, "libtcb200.so")
 
 ALGO_AUTO = 0
 ALGO_MERGE_THREAD = 1

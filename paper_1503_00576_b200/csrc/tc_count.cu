@@ -426,17 +426,27 @@ __global__ void __launch_bounds__(NT)
 // same predicate, so each edge is counted exactly once.  Edges with an empty suffix or
 // an empty adj(v) close no triangle and are skipped by everyone.
 struct VSplit {
-    uint32_t hz, vt, hwp, factor;  // hz = 0xffffffff: v-major off
+    uint32_t z0, hz, vt, hwp, factor, nhcap;  // v-major zone [z0, n); z0 = ~0: v-major off
+    uint32_t bias;                            // v-major iff bias/4 * vcost < ucost
+    const uint32_t *hubstart;
 };
 
 __device__ __forceinline__ bool vmajor_edge(const VSplit &vp, uint32_t e, uint32_t eu, uint32_t v,
                                             uint32_t vs, uint32_t ve) {
-    if (v < vp.hz) return false;
+    if (v < vp.z0) return false;
     if (e + 1 >= eu || vs >= ve) return true;  // no work either way
-    const uint32_t ws = ((v + 1 - vp.hz) >> 5) & ~3u;
-    const bool dense = v >= vp.vt && (vp.hwp - ws) < vp.factor * (ve - vs);
-    const uint32_t ucost = dense ? 4 * (vp.hwp - ws) : 16 * ((ve - (vs & ~3u) + 3) >> 2);
-    return 4 * (eu - e - 1) + 8 < ucost;
+    uint32_t ucost;
+    if (v >= vp.hz) {
+        const uint32_t ws = ((v + 1 - vp.hz) >> 5) & ~3u;
+        const bool dense = v >= vp.vt && (vp.hwp - ws) < vp.factor * (ve - vs);
+        ucost = dense ? 4 * (vp.hwp - ws) : 16 * ((ve - (vs & ~3u) + 3) >> 2);
+    } else {
+        // below the hub zone adj(v) = non-hub prefix (shared-memory cuckoo table in the
+        // v-major kernel, bounded) + hub suffix (bitmap)
+        if (__ldg(vp.hubstart + v) - vs > vp.nhcap) return false;
+        ucost = 16 * ((ve - (vs & ~3u) + 3) >> 2) + 16;
+    }
+    return (uint64_t)(4 * (eu - e - 1) + 8) * vp.bias < (uint64_t)ucost * 4;
 }
 
 // ------------------------------------------------------------ light, TPE ---
@@ -967,10 +977,10 @@ __global__ void __launch_bounds__(256)
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t e = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < hi; e += stride) {
         const uint32_t v = __ldg(dst + e);
-        if (v < vp.hz) continue;
+        if (v < vp.z0) continue;
         const uint32_t eu = __ldg(off + __ldg(src + e) + 1), vs = __ldg(off + v), ve = __ldg(off + v + 1);
         if (e + 1 >= eu || vs >= ve || !vmajor_edge(vp, (uint32_t)e, eu, v, vs, ve)) continue;
-        atomicAdd(cnt + (v - vp.hz), 1u);
+        atomicAdd(cnt + (v - vp.z0), 1u);
     }
 }
 
@@ -1006,16 +1016,16 @@ __global__ void __launch_bounds__(256)
     k_vin_fill(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
                const uint32_t *__restrict__ off, const RangeDev *__restrict__ rg, VSplit vp,
                const uint32_t *__restrict__ start, uint32_t *__restrict__ cursor,
-               uint32_t *__restrict__ in_e) {
+               uint2 *__restrict__ in_e) {
     const uint64_t lo = rg->lo, hi = rg->hi;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t e = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < hi; e += stride) {
         const uint32_t v = __ldg(dst + e);
-        if (v < vp.hz) continue;
+        if (v < vp.z0) continue;
         const uint32_t eu = __ldg(off + __ldg(src + e) + 1), vs = __ldg(off + v), ve = __ldg(off + v + 1);
         if (e + 1 >= eu || vs >= ve || !vmajor_edge(vp, (uint32_t)e, eu, v, vs, ve)) continue;
-        const uint32_t h = v - vp.hz;
-        in_e[start[h] + atomicAdd(cursor + h, 1u)] = (uint32_t)e;
+        const uint32_t h = v - vp.z0;
+        in_e[start[h] + atomicAdd(cursor + h, 1u)] = make_uint2((uint32_t)e, eu);
     }
 }
 
@@ -1031,16 +1041,18 @@ __global__ void k_vin_tasks(const uint32_t *__restrict__ start, const uint32_t *
 template <int NT, int U>
 __global__ void __launch_bounds__(NT)
     k_count_vmajor(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
-                   const uint32_t *__restrict__ off, uint32_t hz, uint32_t hwp,
-                   const uint32_t *__restrict__ start, const uint32_t *__restrict__ in_e,
+                   const uint32_t *__restrict__ off, const uint32_t *__restrict__ hubstart,
+                   uint32_t z0, uint32_t hz, uint32_t hwp, uint32_t cap,
+                   const uint32_t *__restrict__ start, const uint2 *__restrict__ in_e,
                    const uint2 *__restrict__ tasks, const uint32_t *__restrict__ ntasks,
                    unsigned *__restrict__ next, unsigned long long *__restrict__ total) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t *bitmap = reinterpret_cast<uint32_t *>(smem);  // hwp words
+    uint32_t *ctab = bitmap + hwp;                           // cap slots (v below hz)
     __shared__ uint32_t s_cb[NT], s_vs[NT], s_ve[NT];
     __shared__ uint32_t s_cst[NT + 4];
     __shared__ uint32_t s_scan[32];
-    __shared__ unsigned s_task;
+    __shared__ unsigned s_task, s_fail;
     constexpr int NW = NT / 32;
     const unsigned warp = threadIdx.x >> 5;
     const unsigned nt = *ntasks;
@@ -1053,13 +1065,34 @@ __global__ void __launch_bounds__(NT)
         const unsigned t = s_task;
         if (t >= nt) break;
         const uint2 task = tasks[t];
-        const uint32_t h = task.x, v = hz + h;
+        const uint32_t h = task.x, v = z0 + h;
         const uint32_t vs = __ldg(off + v), ve = __ldg(off + v + 1);
-        const uint32_t ws = ((h + 1) >> 5) & ~3u;  // first hub word adj(v) can touch
+        // hub part of adj(v) -> bitmap over hub words [ws, hwp); below the hub zone the
+        // non-hub prefix [vs, hs) goes into a cuckoo table
+        const uint32_t hs = v >= hz ? vs : __ldg(hubstart + v);
+        const uint32_t nh = hs - vs;
+        const uint32_t ws = v >= hz ? ((v + 1 - hz) >> 5) & ~3u : 0u;
         for (uint32_t i = ws + 4 * threadIdx.x; i < hwp; i += 4 * NT)
             *reinterpret_cast<uint4 *>(bitmap + i) = make_uint4(0, 0, 0, 0);
+        Cuckoo32 ck{smem_addr(ctab), 4 * nh < cap ? 4 * nh : cap, 0, 0};
+        if (nh) {
+            for (uint32_t seed = 0;; ++seed) {
+                if (seed == 32) __trap();  // cannot happen at load <= 1/4; never miscount
+                ck.c1 = seed_mult(seed, 0);
+                ck.c2 = seed_mult(seed, 1);
+                for (uint32_t i = threadIdx.x; i < ck.T; i += NT) ctab[i] = kEmpty;
+                if (threadIdx.x == 0) s_fail = 0;
+                __syncthreads();
+                for (uint32_t i = vs + threadIdx.x; i < hs; i += NT)
+                    if (!cuckoo_insert32(ctab, ck, __ldg(dst + i))) s_fail = 1;
+                __syncthreads();
+                const bool failed = s_fail != 0;
+                __syncthreads();
+                if (!failed) break;
+            }
+        }
         __syncthreads();
-        for (uint32_t i = vs + threadIdx.x; i < ve; i += NT) {
+        for (uint32_t i = hs + threadIdx.x; i < ve; i += NT) {
             const uint32_t r = __ldg(dst + i) - hz;
             atomicOr(bitmap + (r >> 5), 1u << (r & 31));
         }
@@ -1070,9 +1103,9 @@ __global__ void __launch_bounds__(NT)
             const uint32_t nwin = min((uint32_t)NT, p1 - ps);
             uint32_t chunks = 0, a = 0, b = 0;
             if (threadIdx.x < nwin) {
-                const uint32_t e = __ldg(in_e + ps + threadIdx.x);
-                a = e + 1;
-                b = __ldg(off + __ldg(src + e) + 1);
+                const uint2 ie = __ldg(in_e + ps + threadIdx.x);  // (edge, end of adj(u))
+                a = ie.x + 1;
+                b = ie.y;
                 chunks = (b - (a & ~3u) + 3) >> 2;  // a < b by construction
             }
             uint32_t tot;
@@ -1086,11 +1119,20 @@ __global__ void __launch_bounds__(NT)
             const uint32_t c0 = (uint32_t)((uint64_t)tot * warp / NW);
             const uint32_t c1 = (uint32_t)((uint64_t)tot * (warp + 1) / NW);
             if (c0 < c1) {
-                // suffix items are > v: their words are >= ws, inside the staged range
-                acc += sweep<uint32_t, false, U>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t) {
-                    const uint32_t r = w - hz;
-                    return ((lds32(bm + 4 * min(r >> 5, hwp - 1)) >> (r & 31)) & 1u) != 0u;
-                });
+                // suffix items are > v: hub items hit words >= ws (staged); non-hub items
+                // (only when v < hz) are looked up in the cuckoo table
+                if (nh) {
+                    acc += sweep<uint32_t, false, U>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t) {
+                        const uint32_t r = w - hz;
+                        const bool b = ((lds32(bm + 4 * min(r >> 5, hwp - 1)) >> (r & 31)) & 1u) != 0u;
+                        return w >= hz ? b : ck.contains(w);
+                    });
+                } else {
+                    acc += sweep<uint32_t, false, U>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t) {
+                        const uint32_t r = w - hz;
+                        return (w >= hz) & (((lds32(bm + 4 * min(r >> 5, hwp - 1)) >> (r & 31)) & 1u) != 0u);
+                    });
+                }
             }
             __syncthreads();
         }
@@ -1181,6 +1223,20 @@ size_t heavy_smem(int cls, uint32_t max_out) {
     return (size_t)4 * slots;
 }
 
+constexpr uint32_t kVNonHubCap = 1024;  // v-major: max non-hub prefix of adj(v) (cuckoo slots / 4)
+
+static uint32_t vzone_start(const DeviceGraph &g) {
+    static const int lg = getenv("TC_VZONE_LOG2") ? atoi(getenv("TC_VZONE_LOG2")) : 18;
+    const uint64_t Z = 1ull << (lg < 18 ? 18 : lg > 31 ? 31 : lg);
+    const uint64_t z0 = g.n > Z ? g.n - Z : 0;
+    return (uint32_t)(z0 < g.hz ? z0 : g.hz);
+}
+
+static uint32_t vm_bias_env() {
+    static const uint32_t b = getenv("TC_VM_BIAS") ? (uint32_t)atoi(getenv("TC_VM_BIAS")) : 4u;
+    return b;
+}
+
 static uint32_t dense_factor_env() {
     static const uint32_t f = getenv("TC_DENSE_FACTOR") ? (uint32_t)atoi(getenv("TC_DENSE_FACTOR")) : 3u;
     return f;
@@ -1188,7 +1244,8 @@ static uint32_t dense_factor_env() {
 
 template <int NT>
 int launch_hub(const DeviceGraph &g, const RangeDev *rg, const uint2 *tasks, const unsigned *ntasks,
-               unsigned *next, uint32_t cap, bool vmajor, unsigned long long *d_total, cudaStream_t s) {
+               unsigned *next, uint32_t cap, bool vmajor, int share, unsigned long long *d_total,
+               cudaStream_t s) {
     const uint32_t hwords = g.hwp;
     const size_t sm = 4 * ((size_t)hwords + cap);
     static const int unroll = getenv("TC_HUB_UNROLL") ? atoi(getenv("TC_HUB_UNROLL")) : 4;
@@ -1196,10 +1253,12 @@ int launch_hub(const DeviceGraph &g, const RangeDev *rg, const uint2 *tasks, con
     TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int per_sm = 1;
     TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, sm));
+    per_sm = (per_sm + share - 1) / share;
     if (per_sm < 1) per_sm = 1;
     static const uint32_t dense_factor =
         getenv("TC_DENSE_FACTOR") ? (uint32_t)atoi(getenv("TC_DENSE_FACTOR")) : 3u;
-    const VSplit vp{vmajor ? g.hz : 0xffffffffu, g.vt, g.hwp, dense_factor};
+    const VSplit vp{vmajor ? vzone_start(g) : 0xffffffffu, g.hz, g.vt, g.hwp, dense_factor, kVNonHubCap,
+                    vm_bias_env(), g.hubstart};
     kern<<<kSMs * per_sm, NT, sm, s>>>(g.dst, g.off32, g.hubstart, g.hz, hwords, g.vt, g.dense_off,
                                        g.dense_bits, dense_factor, vp, rg, tasks, ntasks, next, cap,
                                        d_total);
@@ -1259,61 +1318,90 @@ static void clear_l2_window(cudaStream_t s) {
     cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);  // give the carve-out back
 }
 
-// v-major phase: index the hub-head in-edges of [lo, hi) and count them (see k_count_vmajor).
-int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
-                 unsigned long long *d_total, cudaStream_t s, CountStats *stats) {
-    const uint32_t nh = (uint32_t)(g.n - g.hz);
-    uint32_t *cnt = nullptr, *start = nullptr, *tstart = nullptr, *in_e = nullptr;
+// v-major phase: index the hub-head in-edges of [lo, hi) (on stream s) and count them
+// (k_count_vmajor) on stream s2 -- concurrently with the u-major kernels when s2 != s, each
+// kernel then taking a share of every SM (the v-major kernel is DRAM-bound, the u-major
+// ones latency/issue-bound, so they overlap well).  vmajor_finish joins and frees.
+struct VmajorState {
+    uint32_t *cnt = nullptr, *start = nullptr, *tstart = nullptr;
+    uint2 *in_e = nullptr;  // (edge, off[u+1]) per indexed in-edge
     unsigned *next = nullptr;
     uint2 *tasks = nullptr;
-    TC_CHECK(dalloc_t(&cnt, nh, s));
-    TC_CHECK(dalloc_t(&start, (size_t)nh + 1, s));
-    TC_CHECK(dalloc_t(&tstart, (size_t)nh + 1, s));
-    TC_CHECK(dalloc_t(&in_e, span ? span : 1, s));
-    TC_CHECK(dalloc_t(&tasks, (size_t)nh + span / kVChunk + 1, s));
-    TC_CHECK(dalloc_t(&next, 1, s));
-    TC_CUDA(cudaMemsetAsync(cnt, 0, (size_t)nh * sizeof(uint32_t), s));
-    TC_CUDA(cudaMemsetAsync(next, 0, sizeof(unsigned), s));
+    cudaEvent_t e0 = nullptr, e1 = nullptr, done = nullptr;
+    cudaStream_t s2 = nullptr;
+};
+
+int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
+                 unsigned long long *d_total, cudaStream_t s, cudaStream_t s2, int share,
+                 VmajorState *st) {
+    const uint32_t z0 = vzone_start(g);
+    const uint32_t nh = (uint32_t)(g.n - z0);  // v-major zone size
+    TC_CHECK(dalloc_t(&st->cnt, nh, s));
+    TC_CHECK(dalloc_t(&st->start, (size_t)nh + 1, s));
+    TC_CHECK(dalloc_t(&st->tstart, (size_t)nh + 1, s));
+    TC_CHECK(dalloc_t(&st->in_e, span ? span : 1, s));
+    TC_CHECK(dalloc_t(&st->tasks, (size_t)nh + span / kVChunk + 1, s));
+    TC_CHECK(dalloc_t(&st->next, 1, s));
+    TC_CUDA(cudaMemsetAsync(st->cnt, 0, (size_t)nh * sizeof(uint32_t), s));
+    TC_CUDA(cudaMemsetAsync(st->next, 0, sizeof(unsigned), s));
     const unsigned grid = grid_for(span, 256, kSMs * 16);
-    const VSplit vp{g.hz, g.vt, g.hwp, dense_factor_env()};
-    k_vin_count<<<grid, 256, 0, s>>>(g.src, g.dst, g.off32, rg, vp, cnt);
+    const VSplit vp{z0, g.hz, g.vt, g.hwp, dense_factor_env(), kVNonHubCap, vm_bias_env(), g.hubstart};
+    k_vin_count<<<grid, 256, 0, s>>>(g.src, g.dst, g.off32, rg, vp, st->cnt);
     TC_LAUNCHED();
-    k_vin_scan<<<1, 1024 - 32, 0, s>>>(cnt, nh, start, tstart);  // block scan: <= 31 warps
+    k_vin_scan<<<1, 1024 - 32, 0, s>>>(st->cnt, nh, st->start, st->tstart);  // block scan: <= 31 warps
     TC_LAUNCHED();
-    k_vin_fill<<<grid, 256, 0, s>>>(g.src, g.dst, g.off32, rg, vp, start, cnt, in_e);
+    k_vin_fill<<<grid, 256, 0, s>>>(g.src, g.dst, g.off32, rg, vp, st->start, st->cnt, st->in_e);
     TC_LAUNCHED();
-    k_vin_tasks<<<grid_for(nh, 256, kSMs * 4), 256, 0, s>>>(start, tstart, nh, tasks);
+    k_vin_tasks<<<grid_for(nh, 256, kSMs * 4), 256, 0, s>>>(st->start, st->tstart, nh, st->tasks);
     TC_LAUNCHED();
     constexpr int NT = 256;
     auto kern = k_count_vmajor<NT, 4>;
-    const size_t sm = 4 * (size_t)g.hwp;
+    const uint32_t cap = z0 < g.hz ? 4 * kVNonHubCap : 0u;
+    const size_t sm = 4 * ((size_t)g.hwp + cap);
     TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int per_sm = 1;
     TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, sm));
+    per_sm = per_sm / share;
     if (per_sm < 1) per_sm = 1;
-    cudaEvent_t e0, e1;
-    if (stats) {
-        TC_CUDA(cudaEventCreate(&e0));
-        TC_CUDA(cudaEventCreate(&e1));
-        TC_CUDA(cudaEventRecord(e0, s));
-    }
-    kern<<<kSMs * per_sm, NT, sm, s>>>(g.src, g.dst, g.off32, g.hz, g.hwp, start, in_e, tasks,
-                                       tstart + nh, next, d_total);
+    st->s2 = s2;
+    TC_CUDA(cudaEventCreateWithFlags(&st->done, cudaEventDisableTiming));
+    TC_CUDA(cudaEventCreate(&st->e0));
+    TC_CUDA(cudaEventCreate(&st->e1));
+    TC_CUDA(cudaEventRecord(st->e0, s));
+    if (s2 != s) TC_CUDA(cudaStreamWaitEvent(s2, st->e0, 0));
+    kern<<<kSMs * per_sm, NT, sm, s2>>>(g.src, g.dst, g.off32, g.hubstart, z0, g.hz, g.hwp, cap,
+                                        st->start, st->in_e, st->tasks, st->tstart + nh, st->next,
+                                        d_total);
     TC_LAUNCHED();
-    if (stats) {
-        TC_CUDA(cudaEventRecord(e1, s));
-        TC_CUDA(cudaEventSynchronize(e1));
-        cudaEventElapsedTime(&stats->vmajor_ms, e0, e1);
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-    }
-    dfree(cnt, s);
-    dfree(start, s);
-    dfree(tstart, s);
-    dfree(in_e, s);
-    dfree(tasks, s);
-    dfree(next, s);
+    TC_CUDA(cudaEventRecord(st->e1, s2));
+    TC_CUDA(cudaEventRecord(st->done, s2));
     return 0;
+}
+
+int vmajor_finish(VmajorState *st, cudaStream_t s, CountStats *stats) {
+    if (!st->done) return 0;
+    if (st->s2 != s) TC_CUDA(cudaStreamWaitEvent(s, st->done, 0));
+    if (stats) {
+        TC_CUDA(cudaEventSynchronize(st->e1));
+        cudaEventElapsedTime(&stats->vmajor_ms, st->e0, st->e1);
+    }
+    cudaEventDestroy(st->e0);
+    cudaEventDestroy(st->e1);
+    cudaEventDestroy(st->done);
+    dfree(st->cnt, s);
+    dfree(st->start, s);
+    dfree(st->tstart, s);
+    dfree(st->in_e, s);
+    dfree(st->tasks, s);
+    dfree(st->next, s);
+    *st = VmajorState{};
+    return 0;
+}
+
+static cudaStream_t side_stream() {
+    static cudaStream_t s2 = nullptr;
+    if (!s2) cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
+    return s2;
 }
 
 template <typename OffT>
@@ -1359,7 +1447,11 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
             off, rg, nullptr, tasks[0], tasks[1], tasks[2], tasks[3], counters);
         TC_LAUNCHED();
     }
-    if (vmajor) TC_CHECK(count_vmajor(g, rg, span, d_total, s, stats));
+    static const int conc_env = getenv("TC_CONCURRENT") ? atoi(getenv("TC_CONCURRENT")) : 0;
+    const bool conc = vmajor && conc_env;
+    const int share = conc ? 2 : 1;  // SM share of each concurrent kernel
+    VmajorState vst;
+    if (vmajor) TC_CHECK(count_vmajor(g, rg, span, d_total, s, conc ? side_stream() : s, share, &vst));
     TC_CUDA(cudaEventRecord(ev[1], s));
     // Heavy classes first (largest tasks first), then the light sweep.
     for (int c = kClasses - 1; c >= 0; --c) {
@@ -1376,8 +1468,8 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
         const size_t hub_sm = 4 * ((size_t)g.hwp + hub_cap);
         if (sizeof(OffT) == 4 && g.rank_space && g.hubstart && hub_sm <= 200 * 1024) {
             const int ntc = c == 2 ? 512 : 256;
-            rc = ntc == 512 ? launch_hub<512>(g, rg, tasks[c], nt_c, next_c, hub_cap, vmajor, d_total, s)
-                            : launch_hub<256>(g, rg, tasks[c], nt_c, next_c, hub_cap, vmajor, d_total, s);
+            rc = ntc == 512 ? launch_hub<512>(g, rg, tasks[c], nt_c, next_c, hub_cap, vmajor, share, d_total, s)
+                            : launch_hub<256>(g, rg, tasks[c], nt_c, next_c, hub_cap, vmajor, share, d_total, s);
             if (rc) return rc;
             continue;
         }
@@ -1405,7 +1497,8 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
                                    : k_count_light_tpe<OffT, false, false, false>;
         kern<<<kSMs * 8, 256, 0, s>>>(g.src, g.dst, off, rg, g.hz, hub ? g.vt : 0xffffffffu,
                                       g.dense_off, g.dense_bits, g.dense_words,
-                                      VSplit{vmajor ? g.hz : 0xffffffffu, g.vt, g.hwp, dense_factor_env()},
+                                      VSplit{vmajor ? vzone_start(g) : 0xffffffffu, g.hz, g.vt, g.hwp,
+                                             dense_factor_env(), kVNonHubCap, vm_bias_env(), g.hubstart},
                                       d_total);
     } else {
         const bool hub = g.rank_space && g.hubstart;
@@ -1420,6 +1513,7 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
             g.dense_off, g.dense_bits, g.dense_words, d_total);
     }
     TC_LAUNCHED();
+    TC_CHECK(vmajor_finish(&vst, s, stats));
     TC_CUDA(cudaEventRecord(ev[3], s));
     if (stats) {
         TC_CUDA(cudaEventSynchronize(ev[3]));

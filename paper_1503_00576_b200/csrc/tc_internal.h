@@ -53,8 +53,14 @@ int dalloc_t(T **p, size_t count, cudaStream_t s, bool persistent = false) {
 // ------------------------------------------------------------- radix sort ---
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
-constexpr int kSortThreads = 256;
-constexpr int kSortKPT = 16;
+#ifndef TC_SORT_THREADS
+#define TC_SORT_THREADS 256
+#endif
+#ifndef TC_SORT_KPT
+#define TC_SORT_KPT 16
+#endif
+constexpr int kSortThreads = TC_SORT_THREADS;
+constexpr int kSortKPT = TC_SORT_KPT;
 constexpr int kSortTile = kSortThreads * kSortKPT;  // 4096 keys per tile
 constexpr int kMaxPasses = 8;
 

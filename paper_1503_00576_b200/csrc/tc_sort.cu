@@ -58,8 +58,11 @@ __global__ void k_digit_base(const uint32_t *__restrict__ ghist, int npass,
     }
 }
 
+#ifndef TC_SORT_MINB
+#define TC_SORT_MINB 4
+#endif
 template <int MODE, bool HAS_VAL>
-__global__ void __launch_bounds__(kSortThreads, 4)
+__global__ void __launch_bounds__(kSortThreads, TC_SORT_MINB)
     k_radix_pass(const uint64_t *__restrict__ kin, uint64_t *__restrict__ kout,
                  const uint32_t *__restrict__ vin, uint32_t *__restrict__ vout,
                  uint32_t *__restrict__ out_a, uint32_t *__restrict__ out_b, int split_bits,
@@ -96,7 +99,19 @@ __global__ void __launch_bounds__(kSortThreads, 4)
     for (int i = 0; i < kSortKPT; ++i) {
         uint64_t idx = tile_base + warp * (32 * kSortKPT) + i * 32 + lane;
         unsigned d = idx < n ? (unsigned)(k[i] >> pp.shift) & dmask : (unsigned)kRadix;
+#if TC_SORT_BALLOT
+        // warp multi-split: lanes with the same digit agree on every digit bit
+        unsigned peers = __ballot_sync(TC_FULL_MASK, idx < n);
+        if (idx >= n) peers = ~peers;
+#pragma unroll
+        for (int b = 0; b < kRadixBits; ++b) {
+            const unsigned bit = (d >> b) & 1u;
+            const unsigned bal = __ballot_sync(TC_FULL_MASK, bit);
+            peers &= b < pp.bits ? (bit ? bal : ~bal) : 0xffffffffu;
+        }
+#else
         unsigned peers = __match_any_sync(TC_FULL_MASK, d);
+#endif
         int leader = __ffs(peers) - 1;
         unsigned old = 0;
         if ((int)lane == leader && d < (unsigned)kRadix) {
@@ -138,7 +153,12 @@ __global__ void __launch_bounds__(kSortThreads, 4)
             int q = 0;
             for (; q < kLook; ++q) {
                 const uint64_t flag = st[q] & ~kValMask;
-                if (flag == 0) break;  // not published yet: re-poll from here
+                if (flag == 0) {  // not published yet: re-poll from here
+#if TC_SORT_SLEEP
+                    __nanosleep(TC_SORT_SLEEP);
+#endif
+                    break;
+                }
                 excl += st[q] & kValMask;
                 if (flag == kFlagP) { done = true; break; }
             }
