@@ -280,6 +280,7 @@ def main():
     count_ms = statistics.median(t.count_ms for t in count_runs)
     heavy_ms = statistics.median(t.heavy_ms for t in count_runs)
     window_ms = statistics.median(t.light_ms for t in count_runs)
+    vmajor_ms = statistics.median(t.vmajor_ms for t in count_runs)
     alg_bytes = 4 * W + 40 * m
     peak, peak_src = measured_peak()
     achieved = alg_bytes / (count_ms / 1e3) / 1e9
@@ -288,7 +289,8 @@ def main():
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "traffic_gbs": round(traffic / (count_ms / 1e3) / 1e9, 1) if traffic else None,
                 "traffic_frac": round(traffic / (count_ms / 1e3) / 1e9 / peak, 4) if traffic else None,
-                "kernel": "count phase (k_count_heavy + k_count_window + k_classify)",
+                "kernel": "count phase (k_classify + k_vin_* hub-head index + k_count_vmajor + "
+                          "k_count_hub + k_count_light_tpe)",
                 "algorithmic_bytes_per_launch": alg_bytes, "launch_ms": round(count_ms, 3),
                 "peak_source": peak_src}
 
@@ -358,7 +360,8 @@ def main():
                                        "slice all-gather, work-balanced shards, 1 all-reduce"))},
             "phases_ms": {"preprocess": statistics.mean(pre) if pre else None,
                           "count": statistics.mean(cnt) if cnt else None,
-                          "count_heavy": heavy_ms, "count_window": window_ms,
+                          "count_umajor_heavy": heavy_ms, "count_light": window_ms,
+                          "count_vmajor": vmajor_ms,
                           "generate_input_s": gen_s},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
             "gpu_launches": l1 - l0,
