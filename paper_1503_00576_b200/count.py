@@ -193,7 +193,10 @@ def preprocess_device(edges, rank_space: bool = False):
     h = ctypes.c_void_p()
     t = _lib.TcTimes()
     flags = _lib.PREPROCESS_RANK_SPACE if rank_space else 0
-    _lib.check(_lib.lib().tc_preprocess_ex(ctypes.c_void_p(edges.ptr), edges.npairs,
-                                           edges.num_vertices, 1, flags, ctypes.byref(h),
-                                           ctypes.byref(t)))
+    if isinstance(edges, EdgeArray):  # host pairs (copied in by the library)
+        ptr, npairs, on_dev = edges.edges.ctypes.data, edges.edges.shape[0], 0
+    else:
+        ptr, npairs, on_dev = edges.ptr, edges.npairs, 1
+    _lib.check(_lib.lib().tc_preprocess_ex(ctypes.c_void_p(ptr), npairs, edges.num_vertices, on_dev,
+                                           flags, ctypes.byref(h), ctypes.byref(t)))
     return OrientedGraph._from_device(DeviceGraph(h.value)), t

@@ -818,8 +818,13 @@ __global__ void __launch_bounds__(NT)
 // see few bank conflicts); the few non-hub elements of adj(u) go into a small cuckoo
 // table.  hubstart[v] splits every adj(v) into a non-hub prefix and a hub suffix, which
 // are swept separately so each probe path is branch-free.
+#ifdef TC_HUB_MINB
+#define TC_HUB_BOUNDS(nt) __launch_bounds__(nt, TC_HUB_MINB)
+#else
+#define TC_HUB_BOUNDS(nt) __launch_bounds__(nt)
+#endif
 template <int NT, int U>
-__global__ void __launch_bounds__(NT)
+__global__ void TC_HUB_BOUNDS(NT)
     k_count_hub(const uint32_t *__restrict__ dst, const uint32_t *__restrict__ off,
                 const uint32_t *__restrict__ hubstart, uint32_t hz, uint32_t hwords,
                 uint32_t vt, const uint32_t *__restrict__ dense_off,

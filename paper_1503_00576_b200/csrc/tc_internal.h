@@ -119,7 +119,10 @@ struct DeviceGraph {
     bool persistent = false;  // arrays from the default pool (outlive the call)
 };
 
-constexpr uint32_t kHubRanks = 1u << 18;    // hub zone size: 32 KB shared-memory bitmap
+#ifndef TC_HUB_LOG2
+#define TC_HUB_LOG2 18
+#endif
+constexpr uint32_t kHubRanks = 1u << TC_HUB_LOG2;  // hub zone size: 32 KB shared-memory bitmap
 constexpr uint32_t kDenseRanks = 1u << 17;  // dense-hub bitmaps: 1 GB at R-MAT s26
 
 int graph_alloc(DeviceGraph *g, uint64_t m, uint64_t n, cudaStream_t s);
@@ -127,6 +130,9 @@ void graph_release(DeviceGraph *g, cudaStream_t s);
 // node_offsets (and off32, max_out) from a grouped edge_src (reference preprocess.py:36-46).
 int build_node_array_dev(const uint32_t *firsts, uint64_t k, uint64_t n, int64_t *off,
                          uint32_t *off32, uint32_t *max_out, cudaStream_t s);
+// The scan half of it from per-vertex counts; `sums` holds ceil(n / kScanTile) u64.
+int node_array_from_counts(const uint32_t *cnt, uint64_t n, uint64_t k, int64_t *off, uint32_t *off32,
+                           uint32_t *max_out, unsigned long long *sums, cudaStream_t s);
 // off[i] = sum of cnt[0..i) for i < n (exclusive scan, u32 -> i64).
 int exclusive_scan_dev(const uint32_t *cnt, uint64_t n, int64_t *off, cudaStream_t s);
 // Rebuild edge_src, off32 and max_out from node_offsets (after a broadcast of dst + off).

@@ -83,7 +83,8 @@ __global__ void __launch_bounds__(256) k_orient(const uint2 *__restrict__ pairs,
                                                 const uint32_t *__restrict__ deg, uint64_t n, int vb,
                                                 uint64_t *__restrict__ keys, uint64_t capacity,
                                                 unsigned long long *__restrict__ cursor,
-                                                RadixPlan plan, uint32_t *__restrict__ ghist) {
+                                                RadixPlan plan, uint32_t *__restrict__ ghist,
+                                                uint32_t *__restrict__ outdeg = nullptr) {
     __shared__ uint32_t sh[kMaxPasses * kRadix];
     __shared__ uint32_t s_scan[32];
     __shared__ unsigned long long s_base;
@@ -122,6 +123,17 @@ __global__ void __launch_bounds__(256) k_orient(const uint2 *__restrict__ pairs,
                 key[i] = ((uint64_t)pr[i].x << vb) | pr[i].y;
             }
             if (fwd) keepmask |= 1u << i;
+        }
+        if (RANK && outdeg) {
+            // out-degree by source rank; consecutive lanes mostly share the source (inputs
+            // grouped by first id): one atomic per run of equal sources in the warp
+#pragma unroll
+            for (int i = 0; i < kPP; ++i) {
+                const bool k = (keepmask >> i) & 1u;
+                const unsigned src = k ? du[i] : 0xffffffffu;
+                const unsigned peers = __match_any_sync(TC_FULL_MASK, src);
+                if (k && lane == (unsigned)(__ffs(peers) - 1)) atomicAdd(outdeg + src, (unsigned)__popc(peers));
+            }
         }
         uint32_t mine = __popc(keepmask), tot;
         uint32_t off = block_exclusive_scan<uint32_t>(mine, s_scan, &tot);
@@ -510,6 +522,16 @@ int build_node_array_dev(const uint32_t *firsts, uint64_t k, uint64_t n, int64_t
         k_run_hist<<<grid_for(k, 256, kSMs * 16), 256, 0, s>>>(firsts, k, cnt);
         TC_LAUNCHED();
     }
+    TC_CHECK(node_array_from_counts(cnt, n, k, off, off32, max_out, sums, s));
+    dfree(cnt, s);
+    dfree(sums, s);
+    return 0;
+}
+
+// off / off32 = exclusive scan of per-vertex counts (k = total), max_out = max count.
+int node_array_from_counts(const uint32_t *cnt, uint64_t n, uint64_t k, int64_t *off, uint32_t *off32,
+                           uint32_t *max_out, unsigned long long *sums, cudaStream_t s) {
+    const uint64_t nt = (n + kScanTile - 1) / kScanTile;
     if (n) {
         k_tile_sum<<<(unsigned)nt, 256, 0, s>>>(cnt, n, sums);
         TC_LAUNCHED();
@@ -533,8 +555,6 @@ int build_node_array_dev(const uint32_t *firsts, uint64_t k, uint64_t n, int64_t
         }
     }
     TC_CUDA(cudaStreamSynchronize(s));  // host-side k/k32 sources of the async copies
-    dfree(cnt, s);
-    dfree(sums, s);
     return 0;
 }
 
@@ -753,6 +773,359 @@ int build_hubstart_dev(DeviceGraph *g, cudaStream_t s) {
     return 0;
 }
 
+// ------------------------------------------------------- bucket CSR build ---
+// Rank-space CSR without the global key sort: the out-degree histogram (fused into
+// k_orient) gives node_offsets directly; every oriented key is scattered into its source's
+// bucket (warp-aggregated cursor atomics -- sources repeat along the key stream), then
+// each adjacency list is sorted in place by a size-class segmented sort:
+//   d <= 16      thread per list, bitonic network in registers;
+//   17..64       warp per list, 2 elements per lane, shuffle bitonic;
+//   65..4096     CTA per list, shared-memory bitonic;
+//   > 4096       (few lists) composite (list, v) keys through the global LSD radix sort.
+// The result is byte-identical to the sorted-key build (adjacency lists hold distinct
+// ranks, so their sorted order is unique).
+namespace {
+
+__global__ void __launch_bounds__(256)
+    k_bucket_scatter(const uint64_t *__restrict__ keys, uint64_t m, int vb,
+                     const uint32_t *__restrict__ off32, uint32_t *__restrict__ cursor,
+                     uint32_t *__restrict__ dst) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t mask = (1ull << vb) - 1;
+    const unsigned lane = lane_id();
+    // uniform trip count per warp so the warp-aggregated atomics see full warps
+    const uint64_t wbase = ((uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u));
+    for (uint64_t b = wbase; b < m; b += stride) {
+        const uint64_t i = b + lane;
+        const bool ok = i < m;
+        const uint64_t key = ok ? __ldcs(keys + i) : 0ull;
+        const uint32_t u = ok ? (uint32_t)(key >> vb) : 0xffffffffu;
+        const unsigned peers = __match_any_sync(TC_FULL_MASK, u);
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (ok && (int)lane == leader) base = atomicAdd(cursor + u, (unsigned)__popc(peers));
+        base = __shfl_sync(TC_FULL_MASK, base, leader);
+        if (ok) dst[__ldg(off32 + u) + base + __popc(peers & lanemask_lt())] = (uint32_t)(key & mask);
+    }
+}
+
+// Lists by size class (append order is irrelevant: lists are disjoint).
+__global__ void k_seg_classify(const uint32_t *__restrict__ off32, uint64_t n,
+                               uint32_t *__restrict__ mid, uint32_t *__restrict__ big,
+                               uint32_t *__restrict__ warpl, uint32_t *__restrict__ w256,
+                               uint32_t *__restrict__ w1k, unsigned *__restrict__ counts) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += stride) {
+        const uint32_t d = off32[u + 1] - off32[u];
+        if (d <= 16) continue;
+        if (d <= 64) warpl[atomicAdd(counts + 0, 1u)] = (uint32_t)u;
+        else if (d <= 256) w256[atomicAdd(counts + 3, 1u)] = (uint32_t)u;
+        else if (d <= 1024) w1k[atomicAdd(counts + 4, 1u)] = (uint32_t)u;
+        else if (d <= 4096) mid[atomicAdd(counts + 1, 1u)] = (uint32_t)u;
+        else big[atomicAdd(counts + 2, 1u)] = (uint32_t)u;
+    }
+}
+
+__device__ __forceinline__ void cswap(uint32_t &a, uint32_t &b) {
+    const uint32_t lo = min(a, b), hi = max(a, b);
+    a = lo;
+    b = hi;
+}
+
+// d <= 16: thread per list, 16-wide bitonic network in registers (pad = ~0).
+__global__ void __launch_bounds__(256)
+    k_seg_sort16(const uint32_t *__restrict__ off32, uint64_t n, uint32_t *__restrict__ dst) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += stride) {
+        const uint32_t s = off32[u], d = off32[u + 1] - s;
+        if (d < 2 || d > 16) continue;
+        uint32_t x[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) x[i] = (uint32_t)i < d ? dst[s + i] : 0xffffffffu;
+#pragma unroll
+        for (int k = 2; k <= 16; k <<= 1)
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int l = i ^ j;
+                    if (l > i) {
+                        if ((i & k) == 0) cswap(x[i], x[l]);
+                        else cswap(x[l], x[i]);
+                    }
+                }
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            if ((uint32_t)i < d) dst[s + i] = x[i];
+    }
+}
+
+// 17..64: warp per list, element 2*lane+h in register h; bitonic over 64 with shuffles.
+__global__ void __launch_bounds__(256)
+    k_seg_sort64(const uint32_t *__restrict__ off32, const uint32_t *__restrict__ list,
+                 const unsigned *__restrict__ count, uint32_t *__restrict__ dst) {
+    const unsigned lane = lane_id();
+    const unsigned nl = *count;
+    const unsigned gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned nw = (gridDim.x * blockDim.x) >> 5;
+    for (unsigned w = gw; w < nl; w += nw) {
+        const uint32_t u = list[w];
+        const uint32_t s = off32[u], d = off32[u + 1] - s;
+        uint32_t x[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t i = 2 * lane + h;
+            x[h] = i < d ? dst[s + i] : 0xffffffffu;
+        }
+        for (int k = 2; k <= 64; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                if (j == 1) {  // partner inside the lane
+                    const uint32_t i = 2 * lane;
+                    if ((i & k) == 0) cswap(x[0], x[1]);
+                    else cswap(x[1], x[0]);
+                } else {  // partner lane = lane ^ (j / 2), same register
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t i = 2 * lane + h;
+                        const uint32_t y = __shfl_xor_sync(TC_FULL_MASK, x[h], j >> 1);
+                        const bool lower = (i & j) == 0;  // i < partner
+                        const bool asc = (i & k) == 0;
+                        x[h] = (lower == asc) ? min(x[h], y) : max(x[h], y);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t i = 2 * lane + h;
+            if (i < d) dst[s + i] = x[h];
+        }
+    }
+}
+
+// 65..32K lists: warp per list, K registers per lane, element i = 32 r + lane; partners at
+// distance j >= 32 are in the same lane (register r ^ j/32), closer ones in lane ^ j.
+template <int K>
+__global__ void __launch_bounds__(256)
+    k_seg_sort_warp(const uint32_t *__restrict__ off32, const uint32_t *__restrict__ list,
+                    const unsigned *__restrict__ count, uint32_t *__restrict__ dst) {
+    constexpr int N = 32 * K;
+    const unsigned lane = lane_id();
+    const unsigned nl = *count;
+    const unsigned gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned nw = (gridDim.x * blockDim.x) >> 5;
+    for (unsigned w = gw; w < nl; w += nw) {
+        const uint32_t u = list[w];
+        const uint32_t s = off32[u], d = off32[u + 1] - s;
+        uint32_t x[K];
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+            const uint32_t i = 32 * r + lane;
+            x[r] = i < d ? dst[s + i] : 0xffffffffu;
+        }
+#pragma unroll
+        for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                if (j >= 32) {
+#pragma unroll
+                    for (int r = 0; r < K; ++r) {
+                        const int q = r ^ (j >> 5);
+                        if (q > r) {
+                            // i & k for i = 32 r + lane, k >= 64: depends on r only
+                            if (((32 * r) & k) == 0) cswap(x[r], x[q]);
+                            else cswap(x[q], x[r]);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int r = 0; r < K; ++r) {
+                        const uint32_t i = 32 * r + lane;
+                        const uint32_t y = __shfl_xor_sync(TC_FULL_MASK, x[r], j);
+                        const bool lower = (i & j) == 0;
+                        const bool asc = (i & k) == 0;
+                        x[r] = (lower == asc) ? min(x[r], y) : max(x[r], y);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+            const uint32_t i = 32 * r + lane;
+            if (i < d) dst[s + i] = x[r];
+        }
+    }
+}
+
+// 257..4096: CTA per list, shared-memory bitonic over the next power of two.
+__global__ void __launch_bounds__(256)
+    k_seg_sort4k(const uint32_t *__restrict__ off32, const uint32_t *__restrict__ list,
+                 const unsigned *__restrict__ count, uint32_t *__restrict__ dst) {
+    __shared__ uint32_t sh[4096];
+    const unsigned nl = *count;
+    for (unsigned w = blockIdx.x; w < nl; w += gridDim.x) {
+        const uint32_t u = list[w];
+        const uint32_t s = off32[u], d = off32[u + 1] - s;
+        uint32_t N = 2048;
+        while (N < d) N <<= 1;
+        for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) sh[i] = i < d ? dst[s + i] : 0xffffffffu;
+        __syncthreads();
+        for (uint32_t k = 2; k <= N; k <<= 1) {
+            for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+                for (uint32_t t = threadIdx.x; t < N / 2; t += blockDim.x) {
+                    const uint32_t i = ((t & ~(j - 1)) << 1) | (t & (j - 1)), l = i + j;
+                    const uint32_t a = sh[i], b = sh[l];
+                    if ((a > b) == ((i & k) == 0)) {
+                        sh[i] = b;
+                        sh[l] = a;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) dst[s + i] = sh[i];
+        __syncthreads();
+    }
+}
+
+// > 4096: composite keys (big-list index << vb | v) in list order.
+__global__ void k_big_keys(const uint32_t *__restrict__ off32, const uint32_t *__restrict__ big,
+                           const uint32_t *__restrict__ cstart, uint32_t nbig, int vb,
+                           const uint32_t *__restrict__ dst, uint64_t *__restrict__ keys) {
+    for (uint32_t b = blockIdx.x; b < nbig; b += gridDim.x) {
+        const uint32_t u = big[b], s = off32[u], d = off32[u + 1] - s, c = cstart[b];
+        for (uint32_t i = threadIdx.x; i < d; i += blockDim.x)
+            keys[c + i] = ((uint64_t)b << vb) | dst[s + i];
+    }
+}
+
+__global__ void k_big_back(const uint32_t *__restrict__ off32, const uint32_t *__restrict__ big,
+                           const uint32_t *__restrict__ cstart, uint32_t nbig, int vb,
+                           const uint64_t *__restrict__ keys, uint32_t *__restrict__ dst) {
+    const uint64_t mask = (1ull << vb) - 1;
+    for (uint32_t b = blockIdx.x; b < nbig; b += gridDim.x) {
+        const uint32_t u = big[b], s = off32[u], d = off32[u + 1] - s, c = cstart[b];
+        for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) dst[s + i] = (uint32_t)(keys[c + i] & mask);
+    }
+}
+
+__global__ void k_big_sizes(const uint32_t *__restrict__ off32, const uint32_t *__restrict__ big,
+                            uint32_t nbig, uint32_t *__restrict__ sz) {
+    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nbig; b += gridDim.x * blockDim.x)
+        sz[b] = off32[big[b] + 1] - off32[big[b]];
+}
+
+// edge_src from node_offsets: thread per vertex (long lists are rare and short-lived).
+__global__ void __launch_bounds__(256)
+    k_fill_src(const uint32_t *__restrict__ off32, uint64_t n, uint32_t *__restrict__ src) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const unsigned lane = lane_id();
+    // thread per vertex for short lists; lists longer than 32 are written by the whole warp
+    for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); b < n; b += stride) {
+        const uint64_t u = b + lane;
+        uint32_t s = 0, e = 0;
+        if (u < n) {
+            s = off32[u];
+            e = off32[u + 1];
+        }
+        const bool longl = e - s > 32;
+        if (!longl)
+            for (uint32_t p = s; p < e; ++p) src[p] = (uint32_t)u;
+        unsigned lm = __ballot_sync(TC_FULL_MASK, longl);
+        while (lm) {
+            const int l = __ffs(lm) - 1;
+            lm &= lm - 1;
+            const uint32_t ls = __shfl_sync(TC_FULL_MASK, s, l), le = __shfl_sync(TC_FULL_MASK, e, l);
+            for (uint32_t p = ls + lane; p < le; p += 32) src[p] = (uint32_t)(b + l);
+        }
+    }
+}
+
+}  // namespace
+
+// keys: m oriented rank keys (u << vb | v), outdeg: per-source counts (consumed as cursors).
+static int bucket_csr_dev(const uint64_t *keys, uint64_t m, uint64_t n, int vb, uint32_t *outdeg,
+                          DeviceGraph *out, uint32_t *max_out_dev, cudaStream_t s) {
+    unsigned long long *sums = nullptr;
+    const uint64_t nt = (n + kScanTile - 1) / kScanTile;
+    TC_CHECK(dalloc_t(&sums, nt ? nt : 1, s));
+    TC_CHECK(node_array_from_counts(outdeg, n, m, out->off, out->off32, max_out_dev, sums, s));
+    dfree(sums, s);
+    if (n) TC_CUDA(cudaMemsetAsync(outdeg, 0, n * sizeof(uint32_t), s));
+    if (m) {
+        k_bucket_scatter<<<grid_for(m, 256, kSMs * 16), 256, 0, s>>>(keys, m, vb, out->off32, outdeg, out->dst);
+        TC_LAUNCHED();
+    }
+    if (!n) return 0;
+    uint32_t *warpl = nullptr, *w256 = nullptr, *w1k = nullptr, *mid = nullptr, *big = nullptr;
+    unsigned *counts = nullptr;
+    TC_CHECK(dalloc_t(&counts, 8, s));
+    TC_CHECK(dalloc_t(&warpl, n, s));
+    TC_CHECK(dalloc_t(&w256, n, s));
+    TC_CHECK(dalloc_t(&w1k, n, s));
+    TC_CHECK(dalloc_t(&mid, n, s));
+    TC_CHECK(dalloc_t(&big, n, s));
+    TC_CUDA(cudaMemsetAsync(counts, 0, 8 * sizeof(unsigned), s));
+    k_seg_classify<<<grid_for(n, 256, kSMs * 8), 256, 0, s>>>(out->off32, n, mid, big, warpl, w256,
+                                                              w1k, counts);
+    TC_LAUNCHED();
+    k_seg_sort16<<<grid_for(n, 256, kSMs * 16), 256, 0, s>>>(out->off32, n, out->dst);
+    TC_LAUNCHED();
+    k_seg_sort64<<<kSMs * 8, 256, 0, s>>>(out->off32, warpl, counts + 0, out->dst);
+    TC_LAUNCHED();
+    k_seg_sort_warp<8><<<kSMs * 8, 256, 0, s>>>(out->off32, w256, counts + 3, out->dst);
+    TC_LAUNCHED();
+    k_seg_sort_warp<32><<<kSMs * 8, 256, 0, s>>>(out->off32, w1k, counts + 4, out->dst);
+    TC_LAUNCHED();
+    k_seg_sort4k<<<kSMs * 8, 256, 0, s>>>(out->off32, mid, counts + 1, out->dst);
+    TC_LAUNCHED();
+    unsigned nbig = 0;
+    TC_CUDA(cudaMemcpyAsync(&nbig, counts + 2, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    if (nbig) {
+        uint32_t *cstart = nullptr;
+        TC_CHECK(dalloc_t(&cstart, (size_t)nbig + 1, s));
+        k_big_sizes<<<grid_for(nbig, 256, kSMs), 256, 0, s>>>(out->off32, big, nbig, cstart);
+        TC_LAUNCHED();
+        TC_CUDA(cudaMemsetAsync(cstart + nbig, 0, sizeof(uint32_t), s));
+        k_excl_scan_u32<<<1, 1024 - 32, 0, s>>>(cstart, nbig + 1);
+        TC_LAUNCHED();
+        uint32_t tot = 0;
+        TC_CUDA(cudaMemcpyAsync(&tot, cstart + nbig, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        TC_CUDA(cudaStreamSynchronize(s));
+        uint64_t *bk = nullptr, *balt = nullptr, *sorted = nullptr;
+        uint32_t *hist = nullptr;
+        TC_CHECK(dalloc_t(&bk, tot, s));
+        TC_CHECK(dalloc_t(&balt, tot, s));
+        TC_CHECK(dalloc_t(&hist, kMaxPasses * kRadix, s));
+        TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+        k_big_keys<<<nbig < kSMs * 8 ? nbig : kSMs * 8, 256, 0, s>>>(out->off32, big, cstart, nbig, vb,
+                                                                    out->dst, bk);
+        TC_LAUNCHED();
+        const int bb = nbig > 1 ? bits_for(nbig - 1) : 1;
+        const RadixPlan plan = make_radix_plan(bb + vb);
+        TC_CHECK(radix_histogram(bk, tot, plan, hist, s));
+        TC_CHECK(radix_sort(bk, balt, nullptr, nullptr, tot, plan, hist, kOutKeys, nullptr, nullptr, 0,
+                            &sorted, nullptr, s));
+        k_big_back<<<nbig < kSMs * 8 ? nbig : kSMs * 8, 256, 0, s>>>(out->off32, big, cstart, nbig, vb,
+                                                                    sorted, out->dst);
+        TC_LAUNCHED();
+        dfree(bk, s);
+        dfree(balt, s);
+        dfree(hist, s);
+        dfree(cstart, s);
+    }
+    k_fill_src<<<grid_for(n, 256, kSMs * 16), 256, 0, s>>>(out->off32, n, out->src);
+    TC_LAUNCHED();
+    dfree(counts, s);
+    dfree(warpl, s);
+    dfree(w256, s);
+    dfree(w1k, s);
+    dfree(mid, s);
+    dfree(big, s);
+    return 0;
+}
+
 int preprocess_rank_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, DeviceGraph *out,
                         cudaStream_t s) {
     const uint2 *pairs = reinterpret_cast<const uint2 *>(pairs_u32);
@@ -789,9 +1162,14 @@ int preprocess_rank_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, 
     uint64_t capacity = npairs / 2 + 1;
     uint64_t *keys = nullptr, *alt = nullptr;
     TC_CHECK(dalloc_t(&keys, capacity, s));
+    static const int bucket_env = getenv("TC_BUCKET") ? atoi(getenv("TC_BUCKET")) : 1;
+    const bool bucket = bucket_env != 0 && n > 0;
+    uint32_t *outdeg = bucket ? deg : nullptr;  // degrees are consumed by compute_ranks
+    const RadixPlan oplan = bucket ? RadixPlan{} : plan;
+    if (bucket) TC_CUDA(cudaMemsetAsync(outdeg, 0, n * sizeof(uint32_t), s));
     if (npairs) {
         k_orient<true><<<grid_for(npairs, 256 * kPP, kSMs * 8), 256, 0, s>>>(
-            pairs, npairs, rank, n, vb, keys, capacity, cursor, plan, hist);
+            pairs, npairs, rank, n, vb, keys, capacity, cursor, oplan, hist, outdeg);
         TC_LAUNCHED();
     }
     unsigned long long kept = 0;
@@ -803,17 +1181,23 @@ int preprocess_rank_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, 
         TC_CHECK(dalloc_t(&keys, capacity, s));
         TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
         TC_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
+        if (bucket) TC_CUDA(cudaMemsetAsync(outdeg, 0, n * sizeof(uint32_t), s));
         k_orient<true><<<grid_for(npairs, 256 * kPP, kSMs * 8), 256, 0, s>>>(
-            pairs, npairs, rank, n, vb, keys, capacity, cursor, plan, hist);
+            pairs, npairs, rank, n, vb, keys, capacity, cursor, oplan, hist, outdeg);
         TC_LAUNCHED();
     }
     const uint64_t m = kept;
     TC_CHECK(graph_alloc(out, m, n, s));
-    TC_CHECK(dalloc_t(&alt, m ? m : 1, s));
-    TC_CHECK(radix_sort(keys, alt, nullptr, nullptr, m, plan, hist, kOutSoA, out->src, out->dst, vb,
-                        nullptr, nullptr, s));
-    TC_CUDA(cudaMemsetAsync(out->dst + m, 0, 4 * sizeof(uint32_t), s));
-    TC_CHECK(build_node_array_dev(out->src, m, n, out->off, out->off32, scratch + 1, s));
+    if (bucket) {
+        TC_CHECK(bucket_csr_dev(keys, m, n, vb, outdeg, out, scratch + 1, s));
+        TC_CUDA(cudaMemsetAsync(out->dst + m, 0, 4 * sizeof(uint32_t), s));
+    } else {
+        TC_CHECK(dalloc_t(&alt, m ? m : 1, s));
+        TC_CHECK(radix_sort(keys, alt, nullptr, nullptr, m, plan, hist, kOutSoA, out->src, out->dst, vb,
+                            nullptr, nullptr, s));
+        TC_CUDA(cudaMemsetAsync(out->dst + m, 0, 4 * sizeof(uint32_t), s));
+        TC_CHECK(build_node_array_dev(out->src, m, n, out->off, out->off32, scratch + 1, s));
+    }
     TC_CHECK(build_hubstart_dev(out, s));
     TC_CUDA(cudaMemcpyAsync(&out->max_out, scratch + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     dfree(deg, s);

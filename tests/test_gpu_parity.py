@@ -259,3 +259,41 @@ def test_rgg_config5_full_size():
     assert tcb.count_triangles(og) == t
     assert tcb.count_partitioned(og, tcb.PartitionPlan.work_balanced(og, 3), 1) == t
     assert 1.9e9 < t < 2.1e9  # SURVEY.md §8(a) extrapolation: ~2.0e9
+
+
+def _rank_csr_numpy(pairs: np.ndarray, n: int):
+    """Rank-space CSR restated in numpy: vertices relabelled by (degree, id) rank (the
+    reference orientation order, preprocess.py:49-62), oriented low -> high rank, sorted."""
+    deg = np.bincount(pairs[:, 0], minlength=n)
+    order = np.lexsort((np.arange(n), deg))
+    rank = np.empty(n, np.int64)
+    rank[order] = np.arange(n)
+    ru, rv = rank[pairs[:, 0]], rank[pairs[:, 1]]
+    keep = ru < rv
+    ru, rv = ru[keep], rv[keep]
+    o = np.lexsort((rv, ru))
+    off = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(ru, minlength=n), out=off[1:])
+    return ru[o].astype(np.uint32), rv[o].astype(np.uint32), off
+
+
+@pytest.mark.parametrize("case", ["rmat14", "ba", "k600_shuffled", "k5000"])
+def test_rank_space_csr_matches_numpy(case):
+    """The count-ready rank-space CSR (bucket scatter + size-class segmented sort: register,
+    warp, CTA and global-radix classes) is byte-identical to a numpy restatement."""
+    if case == "rmat14":
+        pairs = oracle.symmetrize(oracle.rmat_pairs(14, 16, seed=3))
+    elif case == "ba":
+        pairs = generators.barabasi_albert(20000, 9, seed=1, pinned=False).edges
+    elif case == "k600_shuffled":
+        pairs = _complete_pairs(600)
+        pairs = pairs[np.random.default_rng(5).permutation(pairs.shape[0])]
+    else:
+        pairs = _complete_pairs(5000)  # lists of 4999: the global-radix class
+    pairs = np.ascontiguousarray(pairs, dtype=np.uint32)
+    n = int(pairs.max()) + 1
+    og, _ = tcb.preprocess_device(EdgeArray(pairs, num_vertices=n), rank_space=True)
+    src, dst, off = _rank_csr_numpy(pairs, n)
+    assert np.array_equal(og.edge_src, src)
+    assert np.array_equal(og.edge_dst, dst)
+    assert np.array_equal(og.node_offsets, off)
