@@ -961,6 +961,86 @@ __global__ void TC_HUB_BOUNDS(NT)
     block_add_total(acc, total);
 }
 
+// --------------------------------------------------------- mid, warp/task ---
+// Heavy sources of the smallest class (33 <= d+(u) <= 512), rank space: ONE WARP per task
+// instead of a CTA.  adj(u) goes into a per-warp shared-memory cuckoo table (load <= 1/4,
+// 8 KB), the task's u-major edges (v-major heads and empty intersections dropped) are taken
+// 32 at a time, and all items of their adj(v) are flattened over the warp's lanes as
+// 16-byte chunks and probed in the table.  No block barriers: 8 independent tasks per CTA
+// keep their dependent load chains (task -> offsets -> lists) in flight together, which
+// the CTA-per-task hub kernel (one 32 KB bitmap per task) cannot.
+constexpr int kMidWarps = 8;
+constexpr uint32_t kMidSlots = 4 * 512;
+
+__global__ void __launch_bounds__(32 * kMidWarps)
+    k_count_mid_warp(const uint32_t *__restrict__ dst, const uint32_t *__restrict__ off, VSplit vp,
+                     const RangeDev *__restrict__ rg, const uint2 *__restrict__ tasks,
+                     const unsigned *__restrict__ ntasks, unsigned *__restrict__ next,
+                     unsigned long long *__restrict__ total) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t s_cb[kMidWarps][32], s_vs[kMidWarps][32], s_ve[kMidWarps][32];
+    __shared__ uint32_t s_cst[kMidWarps][36];
+    const unsigned lane = lane_id(), wp = threadIdx.x >> 5;
+    uint32_t *tab = reinterpret_cast<uint32_t *>(smem) + wp * kMidSlots;
+    const EdgeTable<uint32_t> et{s_cb[wp], s_vs[wp], s_ve[wp], s_cst[wp], nullptr};
+    const uint64_t lo = rg->lo, hi = rg->hi;
+    const unsigned nt = *ntasks;
+    uint32_t acc = 0;
+    for (;;) {
+        unsigned t = 0;
+        if (lane == 0) t = atomicAdd(next, 1u);
+        t = __shfl_sync(TC_FULL_MASK, t, 0);
+        if (t >= nt) break;
+        const uint2 task = tasks[t];
+        const uint32_t u = task.x;
+        const uint32_t s = __ldg(off + u), e = __ldg(off + u + 1), d = e - s;
+        uint64_t es = (uint64_t)s > lo ? (uint64_t)s : lo;
+        uint64_t ee = (uint64_t)e < hi ? (uint64_t)e : hi;
+        es += (uint64_t)task.y * kChunk;
+        ee = ee < es + kChunk ? ee : es + kChunk;
+        Cuckoo32 ck{smem_addr(tab), 4 * d < kMidSlots ? 4 * d : kMidSlots, 0, 0};
+        for (uint32_t seed = 0;; ++seed) {
+            if (seed == 32) __trap();  // cannot happen at load <= 1/4; never miscount
+            ck.c1 = seed_mult(seed, 0);
+            ck.c2 = seed_mult(seed, 1);
+            for (uint32_t i = lane; i < ck.T; i += 32) tab[i] = kEmpty;
+            __syncwarp();
+            bool fail = false;
+            for (uint32_t i = lane; i < d; i += 32)
+                if (!cuckoo_insert32(tab, ck, __ldg(dst + s + i))) fail = true;
+            __syncwarp();
+            if (!__any_sync(TC_FULL_MASK, fail)) break;
+        }
+        for (uint64_t ws = es; ws < ee; ws += 32) {
+            uint32_t vs = 0, ve = 0, chunks = 0;
+            if (ws + lane < ee) {
+                const uint32_t p = (uint32_t)(ws + lane);
+                const uint32_t v = __ldg(dst + p);
+                vs = __ldg(off + v);
+                ve = __ldg(off + v + 1);
+                if (p + 1 < e && vs < ve && !vmajor_edge(vp, p, e, v, vs, ve))
+                    chunks = (ve - (vs & ~3u) + 3) >> 2;
+                else
+                    vs = ve = 0;
+            }
+            const uint32_t incl = warp_inclusive_scan(chunks);
+            const uint32_t tot = __shfl_sync(TC_FULL_MASK, incl, 31);
+            if (tot == 0) continue;  // warp-uniform
+            const uint32_t cst = incl - chunks;
+            s_cb[wp][lane] = (vs & ~3u) - 4 * cst;
+            s_vs[wp][lane] = vs;
+            s_ve[wp][lane] = ve;
+            s_cst[wp][lane] = cst;
+            if (lane == 0) s_cst[wp][32] = tot;
+            __syncwarp();
+            acc += sweep<uint32_t, false, 2>(dst, et, 32, 0, tot,
+                                            [&](uint32_t w, uint32_t) { return ck.contains(w); });
+            __syncwarp();
+        }
+    }
+    block_add_total(acc, total);
+}
+
 // ---------------------------------------------------------------- v-major ---
 // Rank space, edges e = (u, v) whose head v is in the hub zone [hz, n) (R-MAT s26: 77 % of
 // all edges, ~90 % of the u-major kernels' bytes).  adj(v) lies in (v, n), inside the hub
@@ -1471,6 +1551,23 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
         int rc = 0;
         const uint32_t hub_cap = 4 * (g.max_out < kClassMax[c] ? g.max_out : kClassMax[c]);
         const size_t hub_sm = 4 * ((size_t)g.hwp + hub_cap);
+        static const int midwarp = getenv("TC_MIDWARP") ? atoi(getenv("TC_MIDWARP")) : 1;
+        // with v-major on, the hub heads' dense edges are gone and the class-0 tasks are
+        // latency-bound: one warp per task (without it the CTA bitmap kernel wins)
+        if (c == 0 && midwarp && vmajor && sizeof(OffT) == 4 && g.rank_space && g.hubstart &&
+            kClassMax[0] * 4 <= kMidSlots) {
+            const size_t msm = (size_t)4 * kMidSlots * kMidWarps;
+            TC_CUDA(cudaFuncSetAttribute(k_count_mid_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm));
+            int per_sm = 1;
+            TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_count_mid_warp, 32 * kMidWarps, msm));
+            if (per_sm < 1) per_sm = 1;
+            const VSplit vp{vmajor ? vzone_start(g) : 0xffffffffu, g.hz, g.vt, g.hwp, dense_factor_env(),
+                            kVNonHubCap, vm_bias_env(), g.hubstart};
+            k_count_mid_warp<<<kSMs * per_sm, 32 * kMidWarps, msm, s>>>(g.dst, g.off32, vp, rg, tasks[c],
+                                                                      nt_c, next_c, d_total);
+            TC_LAUNCHED();
+            continue;
+        }
         if (sizeof(OffT) == 4 && g.rank_space && g.hubstart && hub_sm <= 200 * 1024) {
             const int ntc = c == 2 ? 512 : 256;
             rc = ntc == 512 ? launch_hub<512>(g, rg, tasks[c], nt_c, next_c, hub_cap, vmajor, share, d_total, s)
