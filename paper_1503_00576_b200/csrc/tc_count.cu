@@ -428,6 +428,7 @@ __global__ void __launch_bounds__(NT)
 struct VSplit {
     uint32_t z0, hz, vt, hwp, factor, nhcap;  // v-major zone [z0, n); z0 = ~0: v-major off
     uint32_t bias;                            // v-major iff bias/4 * vcost < ucost
+    uint32_t lowall;                          // below hz: 0 = short suffixes only, 1 = by bytes
     const uint32_t *hubstart;
 };
 
@@ -441,9 +442,9 @@ __device__ __forceinline__ bool vmajor_edge(const VSplit &vp, uint32_t e, uint32
         const bool dense = v >= vp.vt && (vp.hwp - ws) < vp.factor * (ve - vs);
         ucost = dense ? 4 * (vp.hwp - ws) : 16 * ((ve - (vs & ~3u) + 3) >> 2);
     } else {
-        // below the hub zone adj(v) = non-hub prefix (shared-memory cuckoo table in the
-        // v-major kernel, bounded) + hub suffix (bitmap)
-        if (__ldg(vp.hubstart + v) - vs > vp.nhcap) return false;
+        // below the hub zone: adj(v) goes into a per-warp cuckoo table (k_count_vlow_warp),
+        // so it must fit; by default only short suffixes (light sources) go there
+        if (ve - vs > vp.nhcap || (!vp.lowall && eu - e - 1 >= 32)) return false;
         ucost = 16 * ((ve - (vs & ~3u) + 3) >> 2) + 16;
     }
     return (uint64_t)(4 * (eu - e - 1) + 8) * vp.bias < (uint64_t)ucost * 4;
@@ -972,16 +973,17 @@ __global__ void TC_HUB_BOUNDS(NT)
 constexpr int kMidWarps = 8;
 constexpr uint32_t kMidSlots = 4 * 512;
 
-__global__ void __launch_bounds__(32 * kMidWarps)
+template <int WARPS, uint32_t SLOTS, uint32_t LOADINV>
+__global__ void __launch_bounds__(32 * WARPS)
     k_count_mid_warp(const uint32_t *__restrict__ dst, const uint32_t *__restrict__ off, VSplit vp,
                      const RangeDev *__restrict__ rg, const uint2 *__restrict__ tasks,
                      const unsigned *__restrict__ ntasks, unsigned *__restrict__ next,
                      unsigned long long *__restrict__ total) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ uint32_t s_cb[kMidWarps][32], s_vs[kMidWarps][32], s_ve[kMidWarps][32];
-    __shared__ uint32_t s_cst[kMidWarps][36];
+    __shared__ uint32_t s_cb[WARPS][32], s_vs[WARPS][32], s_ve[WARPS][32];
+    __shared__ uint32_t s_cst[WARPS][36];
     const unsigned lane = lane_id(), wp = threadIdx.x >> 5;
-    uint32_t *tab = reinterpret_cast<uint32_t *>(smem) + wp * kMidSlots;
+    uint32_t *tab = reinterpret_cast<uint32_t *>(smem) + wp * SLOTS;
     const EdgeTable<uint32_t> et{s_cb[wp], s_vs[wp], s_ve[wp], s_cst[wp], nullptr};
     const uint64_t lo = rg->lo, hi = rg->hi;
     const unsigned nt = *ntasks;
@@ -998,7 +1000,7 @@ __global__ void __launch_bounds__(32 * kMidWarps)
         uint64_t ee = (uint64_t)e < hi ? (uint64_t)e : hi;
         es += (uint64_t)task.y * kChunk;
         ee = ee < es + kChunk ? ee : es + kChunk;
-        Cuckoo32 ck{smem_addr(tab), 4 * d < kMidSlots ? 4 * d : kMidSlots, 0, 0};
+        Cuckoo32 ck{smem_addr(tab), LOADINV * d < SLOTS ? LOADINV * d : SLOTS, 0, 0};
         for (uint32_t seed = 0;; ++seed) {
             if (seed == 32) __trap();  // cannot happen at load <= 1/4; never miscount
             ck.c1 = seed_mult(seed, 0);
@@ -1129,8 +1131,9 @@ __global__ void __launch_bounds__(NT)
                    const uint32_t *__restrict__ off, const uint32_t *__restrict__ hubstart,
                    uint32_t z0, uint32_t hz, uint32_t hwp, uint32_t cap,
                    const uint32_t *__restrict__ start, const uint2 *__restrict__ in_e,
-                   const uint2 *__restrict__ tasks, const uint32_t *__restrict__ ntasks,
-                   unsigned *__restrict__ next, unsigned long long *__restrict__ total) {
+                   const uint2 *__restrict__ tasks, const uint32_t *__restrict__ tlo,
+                   const uint32_t *__restrict__ ntasks, unsigned *__restrict__ next,
+                   unsigned long long *__restrict__ total) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t *bitmap = reinterpret_cast<uint32_t *>(smem);  // hwp words
     uint32_t *ctab = bitmap + hwp;                           // cap slots (v below hz)
@@ -1140,12 +1143,12 @@ __global__ void __launch_bounds__(NT)
     __shared__ unsigned s_task, s_fail;
     constexpr int NW = NT / 32;
     const unsigned warp = threadIdx.x >> 5;
-    const unsigned nt = *ntasks;
+    const unsigned nt = *ntasks, t0 = *tlo;
     const EdgeTable<uint32_t> et{s_cb, s_vs, s_ve, s_cst, nullptr};
     const uint32_t bm = smem_addr(bitmap);
     unsigned long long acc = 0;
     for (;;) {
-        if (threadIdx.x == 0) s_task = atomicAdd(next, 1u);
+        if (threadIdx.x == 0) s_task = t0 + atomicAdd(next, 1u);
         __syncthreads();
         const unsigned t = s_task;
         if (t >= nt) break;
@@ -1308,10 +1311,15 @@ size_t heavy_smem(int cls, uint32_t max_out) {
     return (size_t)4 * slots;
 }
 
-constexpr uint32_t kVNonHubCap = 1024;  // v-major: max non-hub prefix of adj(v) (cuckoo slots / 4)
+constexpr uint32_t kVNonHubCap = 512;  // v-major below hz: max |adj(v)| (per-warp cuckoo slots / 4)
+
+static uint32_t vm_lowall_env() {
+    static const uint32_t b = getenv("TC_VLOW_ALL") ? (uint32_t)atoi(getenv("TC_VLOW_ALL")) : 1u;
+    return b;
+}
 
 static uint32_t vzone_start(const DeviceGraph &g) {
-    static const int lg = getenv("TC_VZONE_LOG2") ? atoi(getenv("TC_VZONE_LOG2")) : 18;
+    static const int lg = getenv("TC_VZONE_LOG2") ? atoi(getenv("TC_VZONE_LOG2")) : 20;
     const uint64_t Z = 1ull << (lg < 18 ? 18 : lg > 31 ? 31 : lg);
     const uint64_t z0 = g.n > Z ? g.n - Z : 0;
     return (uint32_t)(z0 < g.hz ? z0 : g.hz);
@@ -1343,7 +1351,7 @@ int launch_hub(const DeviceGraph &g, const RangeDev *rg, const uint2 *tasks, con
     static const uint32_t dense_factor =
         getenv("TC_DENSE_FACTOR") ? (uint32_t)atoi(getenv("TC_DENSE_FACTOR")) : 3u;
     const VSplit vp{vmajor ? vzone_start(g) : 0xffffffffu, g.hz, g.vt, g.hwp, dense_factor, kVNonHubCap,
-                    vm_bias_env(), g.hubstart};
+                    vm_bias_env(), vm_lowall_env(), g.hubstart};
     kern<<<kSMs * per_sm, NT, sm, s>>>(g.dst, g.off32, g.hubstart, g.hz, hwords, g.vt, g.dense_off,
                                        g.dense_bits, dense_factor, vp, rg, tasks, ntasks, next, cap,
                                        d_total);
@@ -1403,6 +1411,75 @@ static void clear_l2_window(cudaStream_t s) {
     cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);  // give the carve-out back
 }
 
+// v-major heads below the hub zone (|adj(v)| <= kVNonHubCap): ONE WARP per task (v, chunk
+// of in-edges), adj(v) in a per-warp cuckoo table, the suffixes of the in-edges flattened
+// over the lanes and probed.  These heads have small in-degrees, so many small independent
+// tasks are in flight per SM (no block barriers).
+constexpr int kVlWarps = 8;
+constexpr uint32_t kVlSlots = 4 * kVNonHubCap;
+
+__global__ void __launch_bounds__(32 * kVlWarps)
+    k_count_vlow_warp(const uint32_t *__restrict__ dst, const uint32_t *__restrict__ off, uint32_t z0,
+                      const uint32_t *__restrict__ start, const uint2 *__restrict__ in_e,
+                      const uint2 *__restrict__ tasks, const uint32_t *__restrict__ ntasks,
+                      unsigned *__restrict__ next, unsigned long long *__restrict__ total) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t s_cb[kVlWarps][32], s_vs[kVlWarps][32], s_ve[kVlWarps][32];
+    __shared__ uint32_t s_cst[kVlWarps][36];
+    const unsigned lane = lane_id(), wp = threadIdx.x >> 5;
+    uint32_t *tab = reinterpret_cast<uint32_t *>(smem) + wp * kVlSlots;
+    const EdgeTable<uint32_t> et{s_cb[wp], s_vs[wp], s_ve[wp], s_cst[wp], nullptr};
+    const unsigned nt = *ntasks;
+    uint32_t acc = 0;
+    for (;;) {
+        unsigned t = 0;
+        if (lane == 0) t = atomicAdd(next, 1u);
+        t = __shfl_sync(TC_FULL_MASK, t, 0);
+        if (t >= nt) break;
+        const uint2 task = tasks[t];
+        const uint32_t h = task.x, v = z0 + h;
+        const uint32_t vs = __ldg(off + v), ve = __ldg(off + v + 1), d = ve - vs;
+        Cuckoo32 ck{smem_addr(tab), 4 * d < kVlSlots ? 4 * d : kVlSlots, 0, 0};
+        for (uint32_t seed = 0;; ++seed) {
+            if (seed == 32) __trap();  // cannot happen at load <= 1/4; never miscount
+            ck.c1 = seed_mult(seed, 0);
+            ck.c2 = seed_mult(seed, 1);
+            for (uint32_t i = lane; i < ck.T; i += 32) tab[i] = kEmpty;
+            __syncwarp();
+            bool fail = false;
+            for (uint32_t i = lane; i < d; i += 32)
+                if (!cuckoo_insert32(tab, ck, __ldg(dst + vs + i))) fail = true;
+            __syncwarp();
+            if (!__any_sync(TC_FULL_MASK, fail)) break;
+        }
+        const uint32_t p0 = __ldg(start + h) + task.y * kVChunk;
+        const uint32_t p1 = min(p0 + kVChunk, __ldg(start + h + 1));
+        for (uint32_t ps = p0; ps < p1; ps += 32) {
+            uint32_t a = 0, b = 0, chunks = 0;
+            if (ps + lane < p1) {
+                const uint2 ie = __ldg(in_e + ps + lane);
+                a = ie.x + 1;
+                b = ie.y;
+                chunks = (b - (a & ~3u) + 3) >> 2;
+            }
+            const uint32_t incl = warp_inclusive_scan(chunks);
+            const uint32_t tot = __shfl_sync(TC_FULL_MASK, incl, 31);
+            const uint32_t cst = incl - chunks;
+            s_cb[wp][lane] = (a & ~3u) - 4 * cst;
+            s_vs[wp][lane] = a;
+            s_ve[wp][lane] = b;
+            s_cst[wp][lane] = cst;
+            if (lane == 0) s_cst[wp][32] = tot;
+            __syncwarp();
+            if (tot)
+                acc += sweep<uint32_t, false, 2>(dst, et, 32, 0, tot,
+                                                [&](uint32_t w, uint32_t) { return ck.contains(w); });
+            __syncwarp();
+        }
+    }
+    block_add_total(acc, total);
+}
+
 // v-major phase: index the hub-head in-edges of [lo, hi) (on stream s) and count them
 // (k_count_vmajor) on stream s2 -- concurrently with the u-major kernels when s2 != s, each
 // kernel then taking a share of every SM (the v-major kernel is DRAM-bound, the u-major
@@ -1426,11 +1503,11 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
     TC_CHECK(dalloc_t(&st->tstart, (size_t)nh + 1, s));
     TC_CHECK(dalloc_t(&st->in_e, span ? span : 1, s));
     TC_CHECK(dalloc_t(&st->tasks, (size_t)nh + span / kVChunk + 1, s));
-    TC_CHECK(dalloc_t(&st->next, 1, s));
+    TC_CHECK(dalloc_t(&st->next, 2, s));
     TC_CUDA(cudaMemsetAsync(st->cnt, 0, (size_t)nh * sizeof(uint32_t), s));
-    TC_CUDA(cudaMemsetAsync(st->next, 0, sizeof(unsigned), s));
+    TC_CUDA(cudaMemsetAsync(st->next, 0, 2 * sizeof(unsigned), s));
     const unsigned grid = grid_for(span, 256, kSMs * 16);
-    const VSplit vp{z0, g.hz, g.vt, g.hwp, dense_factor_env(), kVNonHubCap, vm_bias_env(), g.hubstart};
+    const VSplit vp{z0, g.hz, g.vt, g.hwp, dense_factor_env(), kVNonHubCap, vm_bias_env(), vm_lowall_env(), g.hubstart};
     k_vin_count<<<grid, 256, 0, s>>>(g.src, g.dst, g.off32, rg, vp, st->cnt);
     TC_LAUNCHED();
     k_vin_scan<<<1, 1024 - 32, 0, s>>>(st->cnt, nh, st->start, st->tstart);  // block scan: <= 31 warps
@@ -1441,7 +1518,7 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
     TC_LAUNCHED();
     constexpr int NT = 256;
     auto kern = k_count_vmajor<NT, 4>;
-    const uint32_t cap = z0 < g.hz ? 4 * kVNonHubCap : 0u;
+    const uint32_t cap = 0;  // heads below hz run in k_count_vlow_warp
     const size_t sm = 4 * ((size_t)g.hwp + cap);
     TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int per_sm = 1;
@@ -1454,9 +1531,21 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
     TC_CUDA(cudaEventCreate(&st->e1));
     TC_CUDA(cudaEventRecord(st->e0, s));
     if (s2 != s) TC_CUDA(cudaStreamWaitEvent(s2, st->e0, 0));
+    const uint32_t hb = (uint32_t)(g.hz - z0);  // first hub-zone head: tasks [tstart[hb], ...)
+    if (hb) {
+        const size_t wsm = (size_t)4 * kVlSlots * kVlWarps;
+        TC_CUDA(cudaFuncSetAttribute(k_count_vlow_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+        int wper = 1;
+        TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wper, k_count_vlow_warp, 32 * kVlWarps, wsm));
+        if (wper < 1) wper = 1;
+        k_count_vlow_warp<<<kSMs * wper, 32 * kVlWarps, wsm, s2>>>(g.dst, g.off32, z0, st->start, st->in_e,
+                                                                 st->tasks, st->tstart + hb, st->next + 1,
+                                                                 d_total);
+        TC_LAUNCHED();
+    }
     kern<<<kSMs * per_sm, NT, sm, s2>>>(g.src, g.dst, g.off32, g.hubstart, z0, g.hz, g.hwp, cap,
-                                        st->start, st->in_e, st->tasks, st->tstart + nh, st->next,
-                                        d_total);
+                                        st->start, st->in_e, st->tasks, st->tstart + hb, st->tstart + nh,
+                                        st->next, d_total);
     TC_LAUNCHED();
     TC_CUDA(cudaEventRecord(st->e1, s2));
     TC_CUDA(cudaEventRecord(st->done, s2));
@@ -1487,6 +1576,20 @@ static cudaStream_t side_stream() {
     static cudaStream_t s2 = nullptr;
     if (!s2) cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
     return s2;
+}
+
+template <int WARPS, uint32_t SLOTS, uint32_t LOADINV>
+int launch_mid(const DeviceGraph &g, const VSplit &vp, const RangeDev *rg, const uint2 *tasks,
+               const unsigned *ntasks, unsigned *next, unsigned long long *d_total, cudaStream_t s) {
+    auto kern = k_count_mid_warp<WARPS, SLOTS, LOADINV>;
+    const size_t msm = (size_t)4 * SLOTS * WARPS;
+    TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm));
+    int per_sm = 1;
+    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * WARPS, msm));
+    if (per_sm < 1) per_sm = 1;
+    kern<<<kSMs * per_sm, 32 * WARPS, msm, s>>>(g.dst, g.off32, vp, rg, tasks, ntasks, next, d_total);
+    TC_LAUNCHED();
+    return 0;
 }
 
 template <typename OffT>
@@ -1554,18 +1657,12 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
         static const int midwarp = getenv("TC_MIDWARP") ? atoi(getenv("TC_MIDWARP")) : 1;
         // with v-major on, the hub heads' dense edges are gone and the class-0 tasks are
         // latency-bound: one warp per task (without it the CTA bitmap kernel wins)
-        if (c == 0 && midwarp && vmajor && sizeof(OffT) == 4 && g.rank_space && g.hubstart &&
-            kClassMax[0] * 4 <= kMidSlots) {
-            const size_t msm = (size_t)4 * kMidSlots * kMidWarps;
-            TC_CUDA(cudaFuncSetAttribute(k_count_mid_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm));
-            int per_sm = 1;
-            TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_count_mid_warp, 32 * kMidWarps, msm));
-            if (per_sm < 1) per_sm = 1;
+        if (c <= (midwarp >= 2 ? 1 : 0) && midwarp && vmajor && sizeof(OffT) == 4 && g.rank_space &&
+            g.hubstart) {
             const VSplit vp{vmajor ? vzone_start(g) : 0xffffffffu, g.hz, g.vt, g.hwp, dense_factor_env(),
-                            kVNonHubCap, vm_bias_env(), g.hubstart};
-            k_count_mid_warp<<<kSMs * per_sm, 32 * kMidWarps, msm, s>>>(g.dst, g.off32, vp, rg, tasks[c],
-                                                                      nt_c, next_c, d_total);
-            TC_LAUNCHED();
+                            kVNonHubCap, vm_bias_env(), vm_lowall_env(), g.hubstart};
+            if (c == 0) TC_CHECK((launch_mid<kMidWarps, kMidSlots, 4>(g, vp, rg, tasks[c], nt_c, next_c, d_total, s)));
+            else TC_CHECK((launch_mid<4, 3 * 2048, 3>(g, vp, rg, tasks[c], nt_c, next_c, d_total, s)));
             continue;
         }
         if (sizeof(OffT) == 4 && g.rank_space && g.hubstart && hub_sm <= 200 * 1024) {
@@ -1600,7 +1697,7 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
         kern<<<kSMs * 8, 256, 0, s>>>(g.src, g.dst, off, rg, g.hz, hub ? g.vt : 0xffffffffu,
                                       g.dense_off, g.dense_bits, g.dense_words,
                                       VSplit{vmajor ? vzone_start(g) : 0xffffffffu, g.hz, g.vt, g.hwp,
-                                             dense_factor_env(), kVNonHubCap, vm_bias_env(), g.hubstart},
+                                             dense_factor_env(), kVNonHubCap, vm_bias_env(), vm_lowall_env(), g.hubstart},
                                       d_total);
     } else {
         const bool hub = g.rank_space && g.hubstart;

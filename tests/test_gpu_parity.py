@@ -297,3 +297,47 @@ def test_rank_space_csr_matches_numpy(case):
     assert np.array_equal(og.edge_src, src)
     assert np.array_equal(og.edge_dst, dst)
     assert np.array_equal(og.node_offsets, off)
+
+
+_VMAJOR_SCRIPT = r"""
+import json, sys
+sys.path.insert(0, ".")
+import paper_1503_00576_b200 as tcb
+from paper_1503_00576_b200 import generators
+out = {}
+for scale in (14, 18, 20):
+    g = generators.rmat_device(scale, 16, seed=0)
+    tri, _ = tcb.count_with_timings_device(g)
+    og, _ = tcb.preprocess_device(g, rank_space=True)
+    half = og.m_dir // 3
+    parts = [tcb.count_device(og, 0, half)[0], tcb.count_device(og, half, og.m_dir)[0]]
+    out[scale] = [tri, sum(parts), tcb.count_device(og)[0]]
+    g.free()
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("env", [
+    {"TC_VMAJOR": "1"},                                        # hub-zone heads v-major
+    {"TC_VMAJOR": "1", "TC_VZONE_LOG2": "19", "TC_VLOW_ALL": "1"},  # + heads below the hub zone
+    {"TC_VMAJOR": "1", "TC_VM_BIAS": "1"},                     # (almost) every hub-head edge v-major
+    {"TC_VMAJOR": "1", "TC_MIDWARP": "0", "TC_LIGHT": "2"},    # CTA mid class, warp light kernel
+    {"TC_VMAJOR": "0", "TC_LIGHT": "0"},                       # u-major only, CTA-window light kernel
+])
+def test_count_schedules_agree(env, golden, golden_big):
+    """Every count schedule (v-major on/off and its zone, the per-edge bias, the light and
+    mid-class kernels) gives the golden count, for full and ranged counts.  The library reads
+    these knobs once per process, hence the subprocess."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _VMAJOR_SCRIPT], cwd=root, capture_output=True, text=True,
+                       env={**os.environ, **env}, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = json.loads(r.stdout.strip().splitlines()[-1])
+    want = {14: None, 18: None, 20: 490084299}
+    for scale, counts in got.items():
+        ref = want[int(scale)] or oracle.count(*oracle.preprocess(oracle.symmetrize(oracle.rmat_pairs(int(scale), 16, seed=0))))
+        assert counts == [ref, ref, ref], (scale, counts, ref)
