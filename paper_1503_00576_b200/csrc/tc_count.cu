@@ -697,19 +697,39 @@ __global__ void k_classify(const OffT *__restrict__ off, const RangeDev *__restr
     const uint64_t lo = rg->lo, hi = rg->hi;
     const uint32_t u_lo = rg->u_lo, u_hi = rg->u_hi;
     const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t u = u_lo + blockIdx.x * blockDim.x + threadIdx.x; u < u_hi; u += stride) {
-        const OffT s = off[u], e = off[u + 1];
-        const uint32_t d = (uint32_t)(e - s);
-        if (d <= (uint32_t)kLightMax) continue;
-        const uint64_t es = (uint64_t)s > lo ? (uint64_t)s : lo;
-        uint64_t ee = (uint64_t)e < hi ? (uint64_t)e : hi;
-        if (hend && (uint64_t)hend[u] < ee) ee = hend[u];  // v-major: hub heads excluded
-        if (es >= ee) continue;
-        const int cls = d <= kClassMax[0] ? 0 : d <= kClassMax[1] ? 1 : d <= kClassMax[2] ? 2 : 3;
-        const uint32_t chunks = (uint32_t)((ee - es + kChunk - 1) / kChunk);
-        const unsigned slot = atomicAdd(ntasks + cls, chunks);
-        uint2 *t = cls == 0 ? t0 : cls == 1 ? t1 : cls == 2 ? t2 : t3;
-        for (uint32_t c = 0; c < chunks; ++c) t[slot + c] = make_uint2(u, c);
+    const unsigned lane = lane_id();
+    // warp-uniform trip count; one task-cursor atomic per (warp, class) instead of per source
+    for (uint32_t b = u_lo + blockIdx.x * blockDim.x + (threadIdx.x & ~31u); b < u_hi; b += stride) {
+        const uint32_t u = b + lane;
+        int cls = -1;
+        uint32_t chunks = 0;
+        if (u < u_hi) {
+            const OffT s = off[u], e = off[u + 1];
+            const uint32_t d = (uint32_t)(e - s);
+            const uint64_t es = (uint64_t)s > lo ? (uint64_t)s : lo;
+            uint64_t ee = (uint64_t)e < hi ? (uint64_t)e : hi;
+            if (hend && (uint64_t)hend[u] < ee) ee = hend[u];  // v-major: hub heads excluded
+            if (d > (uint32_t)kLightMax && es < ee) {
+                constexpr uint32_t m0 = kClassMax[0], m1 = kClassMax[1], m2 = kClassMax[2];
+                cls = d <= m0 ? 0 : d <= m1 ? 1 : d <= m2 ? 2 : 3;
+                chunks = (uint32_t)((ee - es + kChunk - 1) / kChunk);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < kClasses; ++c) {
+            const uint32_t x = cls == c ? chunks : 0u;
+            if (!__any_sync(TC_FULL_MASK, x != 0)) continue;
+            const uint32_t incl = warp_inclusive_scan(x);
+            const uint32_t tot = __shfl_sync(TC_FULL_MASK, incl, 31);
+            unsigned base = 0;
+            if (lane == 31) base = atomicAdd(ntasks + c, tot);
+            base = __shfl_sync(TC_FULL_MASK, base, 31);
+            if (x) {
+                uint2 *t = c == 0 ? t0 : c == 1 ? t1 : c == 2 ? t2 : t3;
+                const unsigned slot = base + incl - x;
+                for (uint32_t k = 0; k < x; ++k) t[slot + k] = make_uint2(u, k);
+            }
+        }
     }
 }
 
@@ -1056,63 +1076,118 @@ __global__ void __launch_bounds__(32 * WARPS)
 // are both non-empty); tasks = (v, chunk of kVChunk in-edges) in v order.
 constexpr uint32_t kVChunk = 2048;
 
-__global__ void __launch_bounds__(256)
-    k_vin_count(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
-                const uint32_t *__restrict__ off, const RangeDev *__restrict__ rg, VSplit vp,
-                uint32_t *__restrict__ cnt) {
-    const uint64_t lo = rg->lo, hi = rg->hi;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t e = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < hi; e += stride) {
-        const uint32_t v = __ldg(dst + e);
-        if (v < vp.z0) continue;
-        const uint32_t eu = __ldg(off + __ldg(src + e) + 1), vs = __ldg(off + v), ve = __ldg(off + v + 1);
-        if (e + 1 >= eu || vs >= ve || !vmajor_edge(vp, (uint32_t)e, eu, v, vs, ve)) continue;
-        atomicAdd(cnt + (v - vp.z0), 1u);
-    }
-}
+// Both index passes evaluate the v-major predicate of every edge; each thread keeps
+// kVinPP edges in flight (all loads of a stage issued before any is used): the passes are
+// bound by dependent global-load latency (src/dst -> offsets -> atomic), not bandwidth.
+constexpr int kVinPP = 8;
 
-// One block: start[i] = exclusive scan of cnt, tstart[i] = exclusive scan of task counts
-// ceil(cnt / kVChunk); start[nh], tstart[nh] = totals.  cnt is zeroed (fill cursors).
-__global__ void k_vin_scan(uint32_t *__restrict__ cnt, uint32_t nh, uint32_t *__restrict__ start,
-                           uint32_t *__restrict__ tstart) {
-    __shared__ uint32_t s_w[32], s_w2[32];
-    uint32_t carry = 0, tcarry = 0;
-    for (uint32_t b = 0; b < nh; b += blockDim.x) {
-        const uint32_t i = b + threadIdx.x;
-        const uint32_t x = i < nh ? cnt[i] : 0u;
-        const uint32_t tx = (x + kVChunk - 1) / kVChunk;
-        uint32_t t, tt;
-        const uint32_t e = block_exclusive_scan<uint32_t>(x, s_w, &t);
-        const uint32_t te = block_exclusive_scan<uint32_t>(tx, s_w2, &tt);
-        if (i < nh) {
-            start[i] = carry + e;
-            tstart[i] = tcarry + te;
-            cnt[i] = 0;
-        }
-        carry += t;
-        tcarry += tt;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        start[nh] = carry;
-        tstart[nh] = tcarry;
-    }
-}
-
+template <bool FILL>
 __global__ void __launch_bounds__(256)
-    k_vin_fill(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
+    k_vin_pass(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
                const uint32_t *__restrict__ off, const RangeDev *__restrict__ rg, VSplit vp,
-               const uint32_t *__restrict__ start, uint32_t *__restrict__ cursor,
+               const uint32_t *__restrict__ start, uint32_t *__restrict__ cnt,
                uint2 *__restrict__ in_e) {
     const uint64_t lo = rg->lo, hi = rg->hi;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t e = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < hi; e += stride) {
-        const uint32_t v = __ldg(dst + e);
-        if (v < vp.z0) continue;
-        const uint32_t eu = __ldg(off + __ldg(src + e) + 1), vs = __ldg(off + v), ve = __ldg(off + v + 1);
-        if (e + 1 >= eu || vs >= ve || !vmajor_edge(vp, (uint32_t)e, eu, v, vs, ve)) continue;
-        const uint32_t h = v - vp.z0;
-        in_e[start[h] + atomicAdd(cursor + h, 1u)] = make_uint2((uint32_t)e, eu);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * kVinPP;
+    for (uint64_t b = lo + ((uint64_t)blockIdx.x * blockDim.x) * kVinPP + threadIdx.x; b < hi; b += stride) {
+        uint32_t v[kVinPP], u[kVinPP];
+#pragma unroll
+        for (int i = 0; i < kVinPP; ++i) {
+            const uint64_t e = b + (uint64_t)i * blockDim.x;
+            v[i] = e < hi ? __ldg(dst + e) : 0u;
+            u[i] = e < hi ? __ldg(src + e) : 0u;
+        }
+        uint32_t eu[kVinPP], vs[kVinPP], ve[kVinPP];
+#pragma unroll
+        for (int i = 0; i < kVinPP; ++i) {
+            const uint64_t e = b + (uint64_t)i * blockDim.x;
+            const bool cand = e < hi && v[i] >= vp.z0;
+            eu[i] = cand ? __ldg(off + u[i] + 1) : 0u;
+            vs[i] = cand ? __ldg(off + v[i]) : 0u;
+            ve[i] = cand ? __ldg(off + v[i] + 1) : 0u;
+        }
+        // all atomics of the batch first (independent, in flight together), then the stores
+        uint32_t pos[kVinPP];
+#pragma unroll
+        for (int i = 0; i < kVinPP; ++i) {
+            const uint32_t e = (uint32_t)(b + (uint64_t)i * blockDim.x);
+            pos[i] = 0xffffffffu;
+            if (e + 1 >= eu[i] || vs[i] >= ve[i] || !vmajor_edge(vp, e, eu[i], v[i], vs[i], ve[i])) continue;
+            const uint32_t h = v[i] - vp.z0;
+            if (FILL) pos[i] = __ldg(start + h) + atomicAdd(cnt + h, 1u);
+            else atomicAdd(cnt + h, 1u);
+        }
+        if (FILL) {
+#pragma unroll
+            for (int i = 0; i < kVinPP; ++i)
+                if (pos[i] != 0xffffffffu)
+                    in_e[pos[i]] = make_uint2((uint32_t)(b + (uint64_t)i * blockDim.x), eu[i]);
+        }
+    }
+}
+
+// start[i] = exclusive scan of cnt, tstart[i] = exclusive scan of task counts
+// ceil(cnt / kVChunk); start[nh], tstart[nh] = totals; cnt is zeroed (fill cursors).
+// Three launches: per-tile sums, one-block scan of the tile sums, per-tile apply.
+constexpr uint32_t kVinTile = 4096;
+
+__global__ void __launch_bounds__(256) k_vin_tilesum(const uint32_t *__restrict__ cnt, uint32_t nh,
+                                                     uint2 *__restrict__ tsum) {
+    const uint32_t b = blockIdx.x * kVinTile;
+    uint32_t x = 0, y = 0;
+    for (uint32_t i = b + threadIdx.x; i < b + kVinTile && i < nh; i += 256) {
+        const uint32_t c = cnt[i];
+        x += c;
+        y += (c + kVChunk - 1) / kVChunk;
+    }
+    __shared__ uint32_t s_w[32];
+    uint32_t tx, ty;
+    block_exclusive_scan<uint32_t>(x, s_w, &tx);
+    block_exclusive_scan<uint32_t>(y, s_w, &ty);
+    if (threadIdx.x == 0) tsum[blockIdx.x] = make_uint2(tx, ty);
+}
+
+__global__ void k_vin_tilescan(uint2 *__restrict__ tsum, uint32_t ntile, uint32_t *__restrict__ start,
+                               uint32_t *__restrict__ tstart, uint32_t nh) {
+    __shared__ uint32_t s_w[32];
+    uint32_t cx = 0, cy = 0;
+    for (uint32_t b = 0; b < ntile; b += blockDim.x) {
+        const uint32_t i = b + threadIdx.x;
+        const uint2 v = i < ntile ? tsum[i] : make_uint2(0, 0);
+        uint32_t tx, ty;
+        const uint32_t ex = block_exclusive_scan<uint32_t>(v.x, s_w, &tx);
+        const uint32_t ey = block_exclusive_scan<uint32_t>(v.y, s_w, &ty);
+        if (i < ntile) tsum[i] = make_uint2(cx + ex, cy + ey);
+        cx += tx;
+        cy += ty;
+    }
+    if (threadIdx.x == 0) {
+        start[nh] = cx;
+        tstart[nh] = cy;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_vin_apply(uint32_t *__restrict__ cnt, uint32_t nh,
+                                                   const uint2 *__restrict__ tsum,
+                                                   uint32_t *__restrict__ start,
+                                                   uint32_t *__restrict__ tstart) {
+    __shared__ uint32_t s_w[32];
+    const uint32_t b = blockIdx.x * kVinTile;
+    uint2 carry = tsum[blockIdx.x];
+    for (uint32_t o = 0; o < kVinTile; o += 256) {
+        const uint32_t i = b + o + threadIdx.x;
+        const uint32_t c = i < nh ? cnt[i] : 0u;
+        const uint32_t tc = (c + kVChunk - 1) / kVChunk;
+        uint32_t tx, ty;
+        const uint32_t ex = block_exclusive_scan<uint32_t>(c, s_w, &tx);
+        const uint32_t ey = block_exclusive_scan<uint32_t>(tc, s_w, &ty);
+        if (i < nh) {
+            start[i] = carry.x + ex;
+            tstart[i] = carry.y + ey;
+            cnt[i] = 0;
+        }
+        carry.x += tx;
+        carry.y += ty;
     }
 }
 
@@ -1506,15 +1581,33 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
     TC_CHECK(dalloc_t(&st->next, 2, s));
     TC_CUDA(cudaMemsetAsync(st->cnt, 0, (size_t)nh * sizeof(uint32_t), s));
     TC_CUDA(cudaMemsetAsync(st->next, 0, 2 * sizeof(unsigned), s));
-    const unsigned grid = grid_for(span, 256, kSMs * 16);
+    // everything below runs on s2 (the index build too, so that with s2 != s it overlaps
+    // the u-major kernels on s)
+    st->s2 = s2;
+    TC_CUDA(cudaEventCreateWithFlags(&st->done, cudaEventDisableTiming));
+    TC_CUDA(cudaEventCreate(&st->e0));
+    TC_CUDA(cudaEventCreate(&st->e1));
+    TC_CUDA(cudaEventRecord(st->e0, s));
+    if (s2 != s) TC_CUDA(cudaStreamWaitEvent(s2, st->e0, 0));
+    const unsigned grid = grid_for(span, 256 * kVinPP, kSMs * 8);
     const VSplit vp{z0, g.hz, g.vt, g.hwp, dense_factor_env(), kVNonHubCap, vm_bias_env(), vm_lowall_env(), g.hubstart};
-    k_vin_count<<<grid, 256, 0, s>>>(g.src, g.dst, g.off32, rg, vp, st->cnt);
+    k_vin_pass<false><<<grid, 256, 0, s2>>>(g.src, g.dst, g.off32, rg, vp, nullptr, st->cnt, nullptr);
     TC_LAUNCHED();
-    k_vin_scan<<<1, 1024 - 32, 0, s>>>(st->cnt, nh, st->start, st->tstart);  // block scan: <= 31 warps
+    {
+        const uint32_t ntile = (nh + kVinTile - 1) / kVinTile;
+        uint2 *tsum = nullptr;
+        TC_CHECK(dalloc_t(&tsum, ntile, s2));
+        k_vin_tilesum<<<ntile, 256, 0, s2>>>(st->cnt, nh, tsum);
+        TC_LAUNCHED();
+        k_vin_tilescan<<<1, 1024 - 32, 0, s2>>>(tsum, ntile, st->start, st->tstart, nh);  // <= 31 warps
+        TC_LAUNCHED();
+        k_vin_apply<<<ntile, 256, 0, s2>>>(st->cnt, nh, tsum, st->start, st->tstart);
+        TC_LAUNCHED();
+        dfree(tsum, s2);
+    }
+    k_vin_pass<true><<<grid, 256, 0, s2>>>(g.src, g.dst, g.off32, rg, vp, st->start, st->cnt, st->in_e);
     TC_LAUNCHED();
-    k_vin_fill<<<grid, 256, 0, s>>>(g.src, g.dst, g.off32, rg, vp, st->start, st->cnt, st->in_e);
-    TC_LAUNCHED();
-    k_vin_tasks<<<grid_for(nh, 256, kSMs * 4), 256, 0, s>>>(st->start, st->tstart, nh, st->tasks);
+    k_vin_tasks<<<grid_for(nh, 256, kSMs * 4), 256, 0, s2>>>(st->start, st->tstart, nh, st->tasks);
     TC_LAUNCHED();
     constexpr int NT = 256;
     auto kern = k_count_vmajor<NT, 4>;
@@ -1525,12 +1618,6 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
     TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, sm));
     per_sm = per_sm / share;
     if (per_sm < 1) per_sm = 1;
-    st->s2 = s2;
-    TC_CUDA(cudaEventCreateWithFlags(&st->done, cudaEventDisableTiming));
-    TC_CUDA(cudaEventCreate(&st->e0));
-    TC_CUDA(cudaEventCreate(&st->e1));
-    TC_CUDA(cudaEventRecord(st->e0, s));
-    if (s2 != s) TC_CUDA(cudaStreamWaitEvent(s2, st->e0, 0));
     const uint32_t hb = (uint32_t)(g.hz - z0);  // first hub-zone head: tasks [tstart[hb], ...)
     if (hb) {
         const size_t wsm = (size_t)4 * kVlSlots * kVlWarps;
@@ -1637,7 +1724,8 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
     }
     static const int conc_env = getenv("TC_CONCURRENT") ? atoi(getenv("TC_CONCURRENT")) : 0;
     const bool conc = vmajor && conc_env;
-    const int share = conc ? 2 : 1;  // SM share of each concurrent kernel
+    static const int share_env = getenv("TC_SHARE") ? atoi(getenv("TC_SHARE")) : 1;
+    const int share = conc ? share_env : 1;  // SM share of each concurrent kernel
     VmajorState vst;
     if (vmajor) TC_CHECK(count_vmajor(g, rg, span, d_total, s, conc ? side_stream() : s, share, &vst));
     TC_CUDA(cudaEventRecord(ev[1], s));
