@@ -1457,19 +1457,25 @@ static size_t l2_window_bytes() {
 
 static bool apply_l2_window(const DeviceGraph &g, cudaStream_t s) {
     size_t want = l2_window_bytes();
-    if (!want || !g.dense_bits || !g.dense_words) return false;
+    // TC_L2_TARGET: 0 = tail of the dense-hub bitmaps, 1 = tail of edge_dst (the adjacency
+    // lists of the top-ranked sources, whose suffixes the v-major kernel re-reads most)
+    static const int target = getenv("TC_L2_TARGET") ? atoi(getenv("TC_L2_TARGET")) : 0;
+    const char *base = target == 1 ? reinterpret_cast<const char *>(g.dst)
+                                   : reinterpret_cast<const char *>(g.dense_bits);
+    const size_t tbytes = target == 1 ? (size_t)g.m * 4 : (size_t)g.dense_words * 4;
+    if (!want || !base || !tbytes) return false;
     int dev = 0, maxwin = 0, maxpersist = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);
     cudaDeviceGetAttribute(&maxpersist, cudaDevAttrMaxPersistingL2CacheSize, dev);
-    const size_t total = (size_t)g.dense_words * 4;
+    const size_t total = tbytes;
     if (want > total) want = total;
     if (want > (size_t)maxwin) want = (size_t)maxwin;
     if (want > (size_t)maxpersist) want = (size_t)maxpersist;
     if (!want) return false;
     if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) return false;
     cudaStreamAttrValue v = {};
-    v.accessPolicyWindow.base_ptr = reinterpret_cast<char *>(g.dense_bits) + (total - want);
+    v.accessPolicyWindow.base_ptr = const_cast<char *>(base) + ((total - want) & ~(size_t)127);
     v.accessPolicyWindow.num_bytes = want;
     v.accessPolicyWindow.hitRatio = 1.0f;
     v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
@@ -1699,9 +1705,6 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
         if (g.max_out > lower[c]) cap = span / (lower[c] + 1) + span / kChunk + 2;
         TC_CHECK(dalloc_t(&tasks[c], cap ? cap : 1, s));
     }
-    // The hottest data of the count is the tail of the dense-hub bitmaps (top ranks: short
-    // bitmaps read by almost every heavy source).  Keep a window of it L2-resident.
-    const bool l2win = apply_l2_window(g, s);
     cudaEvent_t ev[4];
     for (auto &e : ev) TC_CUDA(cudaEventCreate(&e));
     TC_CUDA(cudaEventRecord(ev[0], s));
@@ -1722,6 +1725,10 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
             off, rg, nullptr, tasks[0], tasks[1], tasks[2], tasks[3], counters);
         TC_LAUNCHED();
     }
+    // u-major only: the hottest data is the tail of the dense-hub bitmaps (top ranks: short
+    // bitmaps read by almost every heavy source); keep a window of it L2-resident (-2 % at
+    // s26).  With v-major heads those reads are gone and the window only costs L2 capacity.
+    const bool l2win = !vmajor && apply_l2_window(g, s);
     static const int conc_env = getenv("TC_CONCURRENT") ? atoi(getenv("TC_CONCURRENT")) : 0;
     const bool conc = vmajor && conc_env;
     static const int share_env = getenv("TC_SHARE") ? atoi(getenv("TC_SHARE")) : 1;
