@@ -1086,7 +1086,7 @@ __global__ void __launch_bounds__(256)
     k_vin_pass(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
                const uint32_t *__restrict__ off, const RangeDev *__restrict__ rg, VSplit vp,
                const uint32_t *__restrict__ start, uint32_t *__restrict__ cnt,
-               uint2 *__restrict__ in_e) {
+               uint2 *__restrict__ in_e, uint32_t *__restrict__ capflag) {
     const uint64_t lo = rg->lo, hi = rg->hi;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * kVinPP;
     for (uint64_t b = lo + ((uint64_t)blockIdx.x * blockDim.x) * kVinPP + threadIdx.x; b < hi; b += stride) {
@@ -1114,8 +1114,15 @@ __global__ void __launch_bounds__(256)
             pos[i] = 0xffffffffu;
             if (e + 1 >= eu[i] || vs[i] >= ve[i] || !vmajor_edge(vp, e, eu[i], v[i], vs[i], ve[i])) continue;
             const uint32_t h = v[i] - vp.z0;
-            if (FILL) pos[i] = __ldg(start + h) + atomicAdd(cnt + h, 1u);
-            else atomicAdd(cnt + h, 1u);
+            if (FILL) {
+                const uint32_t k = atomicAdd(cnt + h, 1u);
+                // capacity layout: a slot past v's capacity means the input was not
+                // symmetric (in-degree != degree - out-degree); flag it, never write past
+                if (capflag && k >= __ldg(start + h + 1) - __ldg(start + h)) *capflag = 1u;
+                else pos[i] = __ldg(start + h) + k;
+            } else {
+                atomicAdd(cnt + h, 1u);
+            }
         }
         if (FILL) {
 #pragma unroll
@@ -1131,63 +1138,79 @@ __global__ void __launch_bounds__(256)
 // Three launches: per-tile sums, one-block scan of the tile sums, per-tile apply.
 constexpr uint32_t kVinTile = 4096;
 
+// TASKS = false: value = cnt, output start, cnt zeroed (fill cursors);
+// TASKS = true:  value = ceil(cnt / kVChunk), output tstart, cnt kept (fill counts).
+template <bool TASKS>
+__device__ __forceinline__ uint32_t vin_val(uint32_t c) { return TASKS ? (c + kVChunk - 1) / kVChunk : c; }
+
+template <bool TASKS>
 __global__ void __launch_bounds__(256) k_vin_tilesum(const uint32_t *__restrict__ cnt, uint32_t nh,
-                                                     uint2 *__restrict__ tsum) {
+                                                     uint32_t *__restrict__ tsum) {
     const uint32_t b = blockIdx.x * kVinTile;
-    uint32_t x = 0, y = 0;
-    for (uint32_t i = b + threadIdx.x; i < b + kVinTile && i < nh; i += 256) {
-        const uint32_t c = cnt[i];
-        x += c;
-        y += (c + kVChunk - 1) / kVChunk;
-    }
+    uint32_t x = 0;
+    for (uint32_t i = b + threadIdx.x; i < b + kVinTile && i < nh; i += 256) x += vin_val<TASKS>(cnt[i]);
     __shared__ uint32_t s_w[32];
-    uint32_t tx, ty;
+    uint32_t tx;
     block_exclusive_scan<uint32_t>(x, s_w, &tx);
-    block_exclusive_scan<uint32_t>(y, s_w, &ty);
-    if (threadIdx.x == 0) tsum[blockIdx.x] = make_uint2(tx, ty);
+    if (threadIdx.x == 0) tsum[blockIdx.x] = tx;
 }
 
-__global__ void k_vin_tilescan(uint2 *__restrict__ tsum, uint32_t ntile, uint32_t *__restrict__ start,
-                               uint32_t *__restrict__ tstart, uint32_t nh) {
+__global__ void k_vin_tilescan(uint32_t *__restrict__ tsum, uint32_t ntile, uint32_t *__restrict__ out,
+                               uint32_t nh) {
     __shared__ uint32_t s_w[32];
-    uint32_t cx = 0, cy = 0;
+    uint32_t cx = 0;
     for (uint32_t b = 0; b < ntile; b += blockDim.x) {
         const uint32_t i = b + threadIdx.x;
-        const uint2 v = i < ntile ? tsum[i] : make_uint2(0, 0);
-        uint32_t tx, ty;
-        const uint32_t ex = block_exclusive_scan<uint32_t>(v.x, s_w, &tx);
-        const uint32_t ey = block_exclusive_scan<uint32_t>(v.y, s_w, &ty);
-        if (i < ntile) tsum[i] = make_uint2(cx + ex, cy + ey);
+        const uint32_t v = i < ntile ? tsum[i] : 0u;
+        uint32_t tx;
+        const uint32_t ex = block_exclusive_scan<uint32_t>(v, s_w, &tx);
+        if (i < ntile) tsum[i] = cx + ex;
         cx += tx;
-        cy += ty;
     }
-    if (threadIdx.x == 0) {
-        start[nh] = cx;
-        tstart[nh] = cy;
+    if (threadIdx.x == 0) out[nh] = cx;
+}
+
+template <bool TASKS>
+__global__ void __launch_bounds__(256) k_vin_apply(uint32_t *__restrict__ cnt, uint32_t nh,
+                                                   const uint32_t *__restrict__ tsum,
+                                                   uint32_t *__restrict__ out) {
+    __shared__ uint32_t s_w[32];
+    const uint32_t b = blockIdx.x * kVinTile;
+    uint32_t carry = tsum[blockIdx.x];
+    for (uint32_t o = 0; o < kVinTile; o += 256) {
+        const uint32_t i = b + o + threadIdx.x;
+        const uint32_t c = i < nh ? vin_val<TASKS>(cnt[i]) : 0u;
+        uint32_t tx;
+        const uint32_t ex = block_exclusive_scan<uint32_t>(c, s_w, &tx);
+        if (i < nh) {
+            out[i] = carry + ex;
+            if (!TASKS) cnt[i] = 0;
+        }
+        carry += tx;
     }
 }
 
-__global__ void __launch_bounds__(256) k_vin_apply(uint32_t *__restrict__ cnt, uint32_t nh,
-                                                   const uint2 *__restrict__ tsum,
-                                                   uint32_t *__restrict__ start,
-                                                   uint32_t *__restrict__ tstart) {
-    __shared__ uint32_t s_w[32];
-    const uint32_t b = blockIdx.x * kVinTile;
-    uint2 carry = tsum[blockIdx.x];
-    for (uint32_t o = 0; o < kVinTile; o += 256) {
-        const uint32_t i = b + o + threadIdx.x;
-        const uint32_t c = i < nh ? cnt[i] : 0u;
-        const uint32_t tc = (c + kVChunk - 1) / kVChunk;
-        uint32_t tx, ty;
-        const uint32_t ex = block_exclusive_scan<uint32_t>(c, s_w, &tx);
-        const uint32_t ey = block_exclusive_scan<uint32_t>(tc, s_w, &ty);
-        if (i < nh) {
-            start[i] = carry.x + ex;
-            tstart[i] = carry.y + ey;
-            cnt[i] = 0;
-        }
-        carry.x += tx;
-        carry.y += ty;
+// exclusive scan of vin_val<TASKS>(cnt) into out[0..nh] (three launches)
+template <bool TASKS>
+int vin_scan(uint32_t *cnt, uint32_t nh, uint32_t *out, cudaStream_t s) {
+    const uint32_t ntile = (nh + kVinTile - 1) / kVinTile;
+    uint32_t *tsum = nullptr;
+    TC_CHECK(dalloc_t(&tsum, ntile ? ntile : 1, s));
+    k_vin_tilesum<TASKS><<<ntile, 256, 0, s>>>(cnt, nh, tsum);
+    TC_LAUNCHED();
+    k_vin_tilescan<<<1, 1024 - 32, 0, s>>>(tsum, ntile, out, nh);  // block scan: <= 31 warps
+    TC_LAUNCHED();
+    k_vin_apply<TASKS><<<ntile, 256, 0, s>>>(cnt, nh, tsum, out);
+    TC_LAUNCHED();
+    dfree(tsum, s);
+    return 0;
+}
+
+__global__ void k_vin_capacity(const uint32_t *__restrict__ deg_by_rank, const uint32_t *__restrict__ off,
+                               uint32_t z0, uint32_t nz, uint32_t *__restrict__ cap) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nz; i += gridDim.x * blockDim.x) {
+        const uint32_t v = z0 + i;
+        cap[i] = deg_by_rank[v] - (off[v + 1] - off[v]);  // in-degree = degree - out-degree
     }
 }
 
@@ -1205,7 +1228,8 @@ __global__ void __launch_bounds__(NT)
     k_count_vmajor(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
                    const uint32_t *__restrict__ off, const uint32_t *__restrict__ hubstart,
                    uint32_t z0, uint32_t hz, uint32_t hwp, uint32_t cap,
-                   const uint32_t *__restrict__ start, const uint2 *__restrict__ in_e,
+                   const uint32_t *__restrict__ start, const uint32_t *__restrict__ fillc,
+                   const uint2 *__restrict__ in_e,
                    const uint2 *__restrict__ tasks, const uint32_t *__restrict__ tlo,
                    const uint32_t *__restrict__ ntasks, unsigned *__restrict__ next,
                    unsigned long long *__restrict__ total) {
@@ -1261,7 +1285,7 @@ __global__ void __launch_bounds__(NT)
         }
         __syncthreads();
         const uint32_t p0 = __ldg(start + h) + task.y * kVChunk;
-        const uint32_t p1 = min(p0 + kVChunk, __ldg(start + h + 1));
+        const uint32_t p1 = min(p0 + kVChunk, __ldg(start + h) + __ldg(fillc + h));
         for (uint32_t ps = p0; ps < p1; ps += NT) {
             const uint32_t nwin = min((uint32_t)NT, p1 - ps);
             uint32_t chunks = 0, a = 0, b = 0;
@@ -1393,12 +1417,7 @@ static uint32_t vm_lowall_env() {
     return b;
 }
 
-static uint32_t vzone_start(const DeviceGraph &g) {
-    static const int lg = getenv("TC_VZONE_LOG2") ? atoi(getenv("TC_VZONE_LOG2")) : 20;
-    const uint64_t Z = 1ull << (lg < 18 ? 18 : lg > 31 ? 31 : lg);
-    const uint64_t z0 = g.n > Z ? g.n - Z : 0;
-    return (uint32_t)(z0 < g.hz ? z0 : g.hz);
-}
+static uint32_t vzone_start(const DeviceGraph &g) { return vzone_start_of(g.n, g.hz); }
 
 static uint32_t vm_bias_env() {
     static const uint32_t b = getenv("TC_VM_BIAS") ? (uint32_t)atoi(getenv("TC_VM_BIAS")) : 4u;
@@ -1501,7 +1520,8 @@ constexpr uint32_t kVlSlots = 4 * kVNonHubCap;
 
 __global__ void __launch_bounds__(32 * kVlWarps)
     k_count_vlow_warp(const uint32_t *__restrict__ dst, const uint32_t *__restrict__ off, uint32_t z0,
-                      const uint32_t *__restrict__ start, const uint2 *__restrict__ in_e,
+                      const uint32_t *__restrict__ start, const uint32_t *__restrict__ fillc,
+                      const uint2 *__restrict__ in_e,
                       const uint2 *__restrict__ tasks, const uint32_t *__restrict__ ntasks,
                       unsigned *__restrict__ next, unsigned long long *__restrict__ total) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1534,7 +1554,7 @@ __global__ void __launch_bounds__(32 * kVlWarps)
             if (!__any_sync(TC_FULL_MASK, fail)) break;
         }
         const uint32_t p0 = __ldg(start + h) + task.y * kVChunk;
-        const uint32_t p1 = min(p0 + kVChunk, __ldg(start + h + 1));
+        const uint32_t p1 = min(p0 + kVChunk, __ldg(start + h) + __ldg(fillc + h));
         for (uint32_t ps = p0; ps < p1; ps += 32) {
             uint32_t a = 0, b = 0, chunks = 0;
             if (ps + lane < p1) {
@@ -1568,6 +1588,7 @@ __global__ void __launch_bounds__(32 * kVlWarps)
 struct VmajorState {
     uint32_t *cnt = nullptr, *start = nullptr, *tstart = nullptr;
     uint2 *in_e = nullptr;  // (edge, off[u+1]) per indexed in-edge
+    bool capl = false;      // capacity layout used (overflow flag in next[2])
     unsigned *next = nullptr;
     uint2 *tasks = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr, done = nullptr;
@@ -1582,11 +1603,15 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
     TC_CHECK(dalloc_t(&st->cnt, nh, s));
     TC_CHECK(dalloc_t(&st->start, (size_t)nh + 1, s));
     TC_CHECK(dalloc_t(&st->tstart, (size_t)nh + 1, s));
-    TC_CHECK(dalloc_t(&st->in_e, span ? span : 1, s));
+    // capacity layout from preprocessing (in-degree prefix over the zone) when present: the
+    // counting pass is skipped and in-edges land at vin_cap[v] + cursor
+    const bool capl = g.vin_cap && g.vin_z0 == z0;
+    TC_CHECK(dalloc_t(&st->in_e, capl ? (g.m ? g.m : 1) : (span ? span : 1), s));
     TC_CHECK(dalloc_t(&st->tasks, (size_t)nh + span / kVChunk + 1, s));
-    TC_CHECK(dalloc_t(&st->next, 2, s));
+    TC_CHECK(dalloc_t(&st->next, 3, s));  // [0], [1] task cursors, [2] capacity overflow flag
     TC_CUDA(cudaMemsetAsync(st->cnt, 0, (size_t)nh * sizeof(uint32_t), s));
-    TC_CUDA(cudaMemsetAsync(st->next, 0, 2 * sizeof(unsigned), s));
+    TC_CUDA(cudaMemsetAsync(st->next, 0, 3 * sizeof(unsigned), s));
+    st->capl = capl;
     // everything below runs on s2 (the index build too, so that with s2 != s it overlaps
     // the u-major kernels on s)
     st->s2 = s2;
@@ -1597,23 +1622,19 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
     if (s2 != s) TC_CUDA(cudaStreamWaitEvent(s2, st->e0, 0));
     const unsigned grid = grid_for(span, 256 * kVinPP, kSMs * 8);
     const VSplit vp{z0, g.hz, g.vt, g.hwp, dense_factor_env(), kVNonHubCap, vm_bias_env(), vm_lowall_env(), g.hubstart};
-    k_vin_pass<false><<<grid, 256, 0, s2>>>(g.src, g.dst, g.off32, rg, vp, nullptr, st->cnt, nullptr);
-    TC_LAUNCHED();
-    {
-        const uint32_t ntile = (nh + kVinTile - 1) / kVinTile;
-        uint2 *tsum = nullptr;
-        TC_CHECK(dalloc_t(&tsum, ntile, s2));
-        k_vin_tilesum<<<ntile, 256, 0, s2>>>(st->cnt, nh, tsum);
+    const uint32_t *startp = g.vin_cap;
+    if (!capl) {
+        k_vin_pass<false><<<grid, 256, 0, s2>>>(g.src, g.dst, g.off32, rg, vp, nullptr, st->cnt, nullptr,
+                                                nullptr);
         TC_LAUNCHED();
-        k_vin_tilescan<<<1, 1024 - 32, 0, s2>>>(tsum, ntile, st->start, st->tstart, nh);  // <= 31 warps
-        TC_LAUNCHED();
-        k_vin_apply<<<ntile, 256, 0, s2>>>(st->cnt, nh, tsum, st->start, st->tstart);
-        TC_LAUNCHED();
-        dfree(tsum, s2);
+        TC_CHECK(vin_scan<false>(st->cnt, nh, st->start, s2));  // exact layout, cursors zeroed
+        startp = st->start;
     }
-    k_vin_pass<true><<<grid, 256, 0, s2>>>(g.src, g.dst, g.off32, rg, vp, st->start, st->cnt, st->in_e);
+    k_vin_pass<true><<<grid, 256, 0, s2>>>(g.src, g.dst, g.off32, rg, vp, startp, st->cnt, st->in_e,
+                                           capl ? st->next + 2 : nullptr);
     TC_LAUNCHED();
-    k_vin_tasks<<<grid_for(nh, 256, kSMs * 4), 256, 0, s2>>>(st->start, st->tstart, nh, st->tasks);
+    TC_CHECK(vin_scan<true>(st->cnt, nh, st->tstart, s2));  // tasks from the fill counts
+    k_vin_tasks<<<grid_for(nh, 256, kSMs * 4), 256, 0, s2>>>(startp, st->tstart, nh, st->tasks);
     TC_LAUNCHED();
     constexpr int NT = 256;
     auto kern = k_count_vmajor<NT, 4>;
@@ -1631,13 +1652,13 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
         int wper = 1;
         TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wper, k_count_vlow_warp, 32 * kVlWarps, wsm));
         if (wper < 1) wper = 1;
-        k_count_vlow_warp<<<kSMs * wper, 32 * kVlWarps, wsm, s2>>>(g.dst, g.off32, z0, st->start, st->in_e,
+        k_count_vlow_warp<<<kSMs * wper, 32 * kVlWarps, wsm, s2>>>(g.dst, g.off32, z0, startp, st->cnt, st->in_e,
                                                                  st->tasks, st->tstart + hb, st->next + 1,
                                                                  d_total);
         TC_LAUNCHED();
     }
     kern<<<kSMs * per_sm, NT, sm, s2>>>(g.src, g.dst, g.off32, g.hubstart, z0, g.hz, g.hwp, cap,
-                                        st->start, st->in_e, st->tasks, st->tstart + hb, st->tstart + nh,
+                                        startp, st->cnt, st->in_e, st->tasks, st->tstart + hb, st->tstart + nh,
                                         st->next, d_total);
     TC_LAUNCHED();
     TC_CUDA(cudaEventRecord(st->e1, s2));
@@ -1645,9 +1666,16 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
     return 0;
 }
 
-int vmajor_finish(VmajorState *st, cudaStream_t s, CountStats *stats) {
+int vmajor_finish(VmajorState *st, cudaStream_t s, CountStats *stats, bool *overflow) {
+    *overflow = false;
     if (!st->done) return 0;
     if (st->s2 != s) TC_CUDA(cudaStreamWaitEvent(s, st->done, 0));
+    if (st->capl) {
+        unsigned f = 0;
+        TC_CUDA(cudaMemcpyAsync(&f, st->next + 2, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+        TC_CUDA(cudaStreamSynchronize(s));
+        *overflow = f != 0;
+    }
     if (stats) {
         TC_CUDA(cudaEventSynchronize(st->e1));
         cudaEventElapsedTime(&stats->vmajor_ms, st->e0, st->e1);
@@ -1671,6 +1699,10 @@ static cudaStream_t side_stream() {
     return s2;
 }
 
+__global__ void k_add_u64(unsigned long long *__restrict__ out, const unsigned long long *__restrict__ x) {
+    *out += *x;
+}
+
 template <int WARPS, uint32_t SLOTS, uint32_t LOADINV>
 int launch_mid(const DeviceGraph &g, const VSplit &vp, const RangeDev *rg, const uint2 *tasks,
                const unsigned *ntasks, unsigned *next, unsigned long long *d_total, cudaStream_t s) {
@@ -1687,7 +1719,14 @@ int launch_mid(const DeviceGraph &g, const VSplit &vp, const RangeDev *rg, const
 
 template <typename OffT>
 int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
-               unsigned long long *d_total, cudaStream_t s, CountStats *stats) {
+               unsigned long long *d_out, cudaStream_t s, CountStats *stats) {
+    // with a capacity layout the v-major index can detect a non-symmetric input only at the
+    // end: count into a private total and add it to *d_out unless a recount is needed
+    unsigned long long *d_total = d_out;
+    if (g.vin_cap) {
+        TC_CHECK(dalloc_t(&d_total, 1, s));
+        TC_CUDA(cudaMemsetAsync(d_total, 0, sizeof(unsigned long long), s));
+    }
     RangeDev *rg = nullptr;
     unsigned *counters = nullptr;  // [0..3] ntasks per class, [4..7] queue heads, [8] windows
     TC_CHECK(dalloc_t(&rg, 1, s));
@@ -1807,7 +1846,19 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
             g.dense_off, g.dense_bits, g.dense_words, d_total);
     }
     TC_LAUNCHED();
-    TC_CHECK(vmajor_finish(&vst, s, stats));
+    bool overflow = false;
+    TC_CHECK(vmajor_finish(&vst, s, stats, &overflow));
+    if (overflow) {
+        // not a symmetric edge array: redo the whole range without the capacity layout
+        DeviceGraph g2 = g;
+        g2.vin_cap = nullptr;
+        for (auto &e : ev) cudaEventDestroy(e);
+        for (int c = 0; c < kClasses; ++c) dfree(tasks[c], s);
+        dfree(rg, s);
+        dfree(counters, s);
+        dfree(d_total, s);
+        return count_impl<OffT>(g2, off, lo, hi, d_out, s, stats);
+    }
     TC_CUDA(cudaEventRecord(ev[3], s));
     if (stats) {
         TC_CUDA(cudaEventSynchronize(ev[3]));
@@ -1823,6 +1874,11 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
     for (int c = 0; c < kClasses; ++c) dfree(tasks[c], s);
     dfree(rg, s);
     dfree(counters, s);
+    if (d_total != d_out) {
+        k_add_u64<<<1, 1, 0, s>>>(d_out, d_total);
+        TC_LAUNCHED();
+        dfree(d_total, s);
+    }
     return 0;
 }
 
@@ -1911,6 +1967,23 @@ int work_bounds_dev(const DeviceGraph &g, int npools, int64_t *bounds, cudaStrea
     }
     bounds[npools] = (int64_t)g.m;
     free(h);
+    return 0;
+}
+
+int vin_capacity_dev(DeviceGraph *g, const uint32_t *deg_by_rank, cudaStream_t s) {
+    if (!g->off32 || g->n == 0) return 0;
+    const uint32_t z0 = vzone_start_of(g->n, g->hz);
+    const uint32_t nz = (uint32_t)(g->n - z0);
+    uint32_t *tmp = nullptr;
+    dfree(g->vin_cap, s);
+    g->vin_cap = nullptr;
+    TC_CHECK(dalloc_t(&g->vin_cap, (size_t)nz + 1, s, g->persistent));
+    TC_CHECK(dalloc_t(&tmp, nz, s));
+    k_vin_capacity<<<grid_for(nz, 256, kSMs * 4), 256, 0, s>>>(deg_by_rank, g->off32, z0, nz, tmp);
+    TC_LAUNCHED();
+    TC_CHECK(vin_scan<false>(tmp, nz, g->vin_cap, s));
+    dfree(tmp, s);
+    g->vin_z0 = z0;
     return 0;
 }
 

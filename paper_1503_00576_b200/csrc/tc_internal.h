@@ -1,6 +1,7 @@
 // tc_internal.h -- host-side internal interfaces between the library's translation units.
 #pragma once
 #include <cuda_runtime.h>
+#include <stdlib.h>
 #include <stdint.h>
 
 #include <string>
@@ -117,7 +118,22 @@ struct DeviceGraph {
     uint32_t *dense_off = nullptr;   // [n - vt + 1] word offsets (multiples of 4)
     uint32_t *dense_bits = nullptr;
     bool persistent = false;  // arrays from the default pool (outlive the call)
+    // v-major in-edge capacity layout (rank-space preprocessing only): vin_cap[i] = in-degree
+    // prefix over the v-major zone [vin_z0, n) (exclusive scan, n - vin_z0 + 1 entries)
+    uint32_t *vin_cap = nullptr;
+    uint32_t vin_z0 = 0;
 };
+
+// First vertex of the v-major zone: the top 2^TC_VZONE_LOG2 ranks (default 2^20), never
+// above the hub zone start hz.
+inline uint32_t vzone_start_of(uint64_t n, uint32_t hz) {
+    static const int lg = getenv("TC_VZONE_LOG2") ? atoi(getenv("TC_VZONE_LOG2")) : 20;
+    const uint64_t Z = 1ull << (lg < 18 ? 18 : lg > 31 ? 31 : lg);
+    const uint64_t z0 = n > Z ? n - Z : 0;
+    return (uint32_t)(z0 < hz ? z0 : hz);
+}
+// vin_cap for a rank-space graph from its degrees in rank order (tc_count.cu).
+int vin_capacity_dev(DeviceGraph *g, const uint32_t *deg_by_rank, cudaStream_t s);
 
 #ifndef TC_HUB_LOG2
 #define TC_HUB_LOG2 18

@@ -342,10 +342,13 @@ __global__ void k_deg_keys(const uint32_t *__restrict__ deg, uint64_t n, uint64_
 }
 
 __global__ void k_scatter_rank(const uint32_t *__restrict__ ids, uint64_t n,
-                               uint32_t *__restrict__ rank) {
+                               uint32_t *__restrict__ rank, const uint64_t *__restrict__ skeys,
+                               uint32_t *__restrict__ deg_by_rank) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         rank[ids[i]] = (uint32_t)i;
+        if (deg_by_rank) deg_by_rank[i] = (uint32_t)skeys[i];
+    }
 }
 
 __global__ void k_max_u32(const uint32_t *__restrict__ a, uint64_t n, uint32_t *__restrict__ out) {
@@ -466,6 +469,8 @@ void graph_release(DeviceGraph *g, cudaStream_t s) {
     dfree(g->hubstart, s);
     dfree(g->dense_off, s);
     dfree(g->dense_bits, s);
+    dfree(g->vin_cap, s);
+    g->vin_cap = nullptr;
     g->dense_off = g->dense_bits = nullptr;
     g->src = g->dst = nullptr;
     g->off = nullptr;
@@ -685,7 +690,8 @@ int orient_compact_dev(const uint32_t *pairs_u32, uint64_t npairs, const int64_t
 namespace {
 
 // rank[] of every vertex from its degree (stable sort of ids by degree).
-int compute_ranks(const uint32_t *deg, uint64_t n, uint32_t *rank, cudaStream_t s) {
+int compute_ranks(const uint32_t *deg, uint64_t n, uint32_t *rank, cudaStream_t s,
+                  uint32_t *deg_by_rank = nullptr) {
     if (n == 0) return 0;
     uint32_t *dmax = nullptr, *hist = nullptr, *ids = nullptr, *ialt = nullptr, *sids = nullptr;
     uint64_t *keys = nullptr, *kalt = nullptr;
@@ -709,7 +715,7 @@ int compute_ranks(const uint32_t *deg, uint64_t n, uint32_t *rank, cudaStream_t 
     uint64_t *skeys = nullptr;
     TC_CHECK(radix_sort(keys, kalt, ids, ialt, n, plan, hist, kOutKeys, nullptr, nullptr, 0, &skeys,
                         &sids, s));
-    k_scatter_rank<<<grid_for(n, 256, kSMs * 16), 256, 0, s>>>(sids, n, rank);
+    k_scatter_rank<<<grid_for(n, 256, kSMs * 16), 256, 0, s>>>(sids, n, rank, skeys, deg_by_rank);
     TC_LAUNCHED();
     dfree(dmax, s);
     dfree(hist, s);
@@ -748,6 +754,8 @@ int build_hubstart_dev(DeviceGraph *g, cudaStream_t s) {
     g->vt = (uint32_t)g->n - T;
     dfree(g->dense_off, s);
     dfree(g->dense_bits, s);
+    dfree(g->vin_cap, s);
+    g->vin_cap = nullptr;
     g->dense_off = g->dense_bits = nullptr;
     TC_CHECK(dalloc_t(&g->dense_off, (size_t)T + 1, s, g->persistent));
     uint32_t words = 0;
@@ -1158,12 +1166,14 @@ int preprocess_rank_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, 
         set_error("edge array holds a vertex id >= num_vertices");
         return -1;
     }
-    TC_CHECK(compute_ranks(deg, n, rank, s));
+    static const int bucket_env = getenv("TC_BUCKET") ? atoi(getenv("TC_BUCKET")) : 1;
+    const bool bucket = bucket_env != 0 && n > 0;
+    uint32_t *deg_by_rank = nullptr;  // degrees in rank order (v-major capacity layout)
+    if (bucket) TC_CHECK(dalloc_t(&deg_by_rank, n, s));
+    TC_CHECK(compute_ranks(deg, n, rank, s, deg_by_rank));
     uint64_t capacity = npairs / 2 + 1;
     uint64_t *keys = nullptr, *alt = nullptr;
     TC_CHECK(dalloc_t(&keys, capacity, s));
-    static const int bucket_env = getenv("TC_BUCKET") ? atoi(getenv("TC_BUCKET")) : 1;
-    const bool bucket = bucket_env != 0 && n > 0;
     uint32_t *outdeg = bucket ? deg : nullptr;  // degrees are consumed by compute_ranks
     const RadixPlan oplan = bucket ? RadixPlan{} : plan;
     if (bucket) TC_CUDA(cudaMemsetAsync(outdeg, 0, n * sizeof(uint32_t), s));
@@ -1199,6 +1209,10 @@ int preprocess_rank_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, 
         TC_CHECK(build_node_array_dev(out->src, m, n, out->off, out->off32, scratch + 1, s));
     }
     TC_CHECK(build_hubstart_dev(out, s));
+    if (deg_by_rank) {
+        TC_CHECK(vin_capacity_dev(out, deg_by_rank, s));
+        dfree(deg_by_rank, s);
+    }
     TC_CUDA(cudaMemcpyAsync(&out->max_out, scratch + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     dfree(deg, s);
     dfree(rank, s);

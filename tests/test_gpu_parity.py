@@ -313,6 +313,13 @@ for scale in (14, 18, 20):
     parts = [tcb.count_device(og, 0, half)[0], tcb.count_device(og, half, og.m_dir)[0]]
     out[scale] = [tri, sum(parts), tcb.count_device(og)[0]]
     g.free()
+# a non-symmetric array (10 % of the pairs dropped): the v-major capacity layout must notice
+import numpy as np
+import oracle
+from paper_1503_00576_b200.graph import EdgeArray
+p = oracle.symmetrize(oracle.rmat_pairs(16, 16, seed=4))
+p = np.ascontiguousarray(p[np.random.default_rng(2).random(p.shape[0]) < 0.9])
+out["asym"] = [tcb.count_with_timings(EdgeArray(p))[0], oracle.count(*oracle.preprocess(p))]
 print(json.dumps(out))
 """
 
@@ -338,6 +345,8 @@ def test_count_schedules_agree(env, golden, golden_big):
     assert r.returncode == 0, r.stderr[-2000:]
     got = json.loads(r.stdout.strip().splitlines()[-1])
     want = {14: None, 18: None, 20: 490084299}
+    asym = got.pop("asym")
+    assert asym[0] == asym[1], asym
     for scale, counts in got.items():
         ref = want[int(scale)] or oracle.count(*oracle.preprocess(oracle.symmetrize(oracle.rmat_pairs(int(scale), 16, seed=0))))
         assert counts == [ref, ref, ref], (scale, counts, ref)
