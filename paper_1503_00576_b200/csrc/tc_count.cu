@@ -1210,7 +1210,8 @@ __global__ void k_vin_capacity(const uint32_t *__restrict__ deg_by_rank, const u
                                uint32_t z0, uint32_t nz, uint32_t *__restrict__ cap) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nz; i += gridDim.x * blockDim.x) {
         const uint32_t v = z0 + i;
-        cap[i] = deg_by_rank[v] - (off[v + 1] - off[v]);  // in-degree = degree - out-degree
+        const uint32_t d = deg_by_rank[v], o = off[v + 1] - off[v];
+        cap[i] = d > o ? d - o : 0u;  // in-degree = degree - out-degree (symmetric input)
     }
 }
 
@@ -1285,7 +1286,8 @@ __global__ void __launch_bounds__(NT)
         }
         __syncthreads();
         const uint32_t p0 = __ldg(start + h) + task.y * kVChunk;
-        const uint32_t p1 = min(p0 + kVChunk, __ldg(start + h) + __ldg(fillc + h));
+        // fill count, clamped to the slot range (an overflowed capacity layout is recounted)
+        const uint32_t p1 = min(p0 + kVChunk, min(__ldg(start + h) + __ldg(fillc + h), __ldg(start + h + 1)));
         for (uint32_t ps = p0; ps < p1; ps += NT) {
             const uint32_t nwin = min((uint32_t)NT, p1 - ps);
             uint32_t chunks = 0, a = 0, b = 0;
@@ -1554,7 +1556,8 @@ __global__ void __launch_bounds__(32 * kVlWarps)
             if (!__any_sync(TC_FULL_MASK, fail)) break;
         }
         const uint32_t p0 = __ldg(start + h) + task.y * kVChunk;
-        const uint32_t p1 = min(p0 + kVChunk, __ldg(start + h) + __ldg(fillc + h));
+        // fill count, clamped to the slot range (an overflowed capacity layout is recounted)
+        const uint32_t p1 = min(p0 + kVChunk, min(__ldg(start + h) + __ldg(fillc + h), __ldg(start + h + 1)));
         for (uint32_t ps = p0; ps < p1; ps += 32) {
             uint32_t a = 0, b = 0, chunks = 0;
             if (ps + lane < p1) {
@@ -1606,7 +1609,8 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
     // capacity layout from preprocessing (in-degree prefix over the zone) when present: the
     // counting pass is skipped and in-edges land at vin_cap[v] + cursor
     const bool capl = g.vin_cap && g.vin_z0 == z0;
-    TC_CHECK(dalloc_t(&st->in_e, capl ? (g.m ? g.m : 1) : (span ? span : 1), s));
+    const uint64_t ie = capl ? (g.vin_total > span ? g.vin_total : span) : span;
+    TC_CHECK(dalloc_t(&st->in_e, ie ? ie : 1, s));
     TC_CHECK(dalloc_t(&st->tasks, (size_t)nh + span / kVChunk + 1, s));
     TC_CHECK(dalloc_t(&st->next, 3, s));  // [0], [1] task cursors, [2] capacity overflow flag
     TC_CUDA(cudaMemsetAsync(st->cnt, 0, (size_t)nh * sizeof(uint32_t), s));
@@ -1983,6 +1987,10 @@ int vin_capacity_dev(DeviceGraph *g, const uint32_t *deg_by_rank, cudaStream_t s
     TC_LAUNCHED();
     TC_CHECK(vin_scan<false>(tmp, nz, g->vin_cap, s));
     dfree(tmp, s);
+    uint32_t total = 0;
+    TC_CUDA(cudaMemcpyAsync(&total, g->vin_cap + nz, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    g->vin_total = total;
     g->vin_z0 = z0;
     return 0;
 }

@@ -110,6 +110,7 @@ struct DeviceGraph {
     bool rank_space = false;
     uint32_t hz = 0;
     uint32_t *hubstart = nullptr;
+    bool hubstart_ready = false;  // hubstart filled by the rank-space segmented sort
     // Dense hubs: every vertex v of rank >= vt (the top kDenseRanks) also has adj(v) as a
     // bitmap over hub-zone words [ws4(v), hwp) at dense_bits + dense_off[v - vt], where
     // ws4(v) = ((v + 1 - hz) / 32) rounded down to a multiple of 4 and hwp = hub-zone
@@ -122,6 +123,7 @@ struct DeviceGraph {
     // prefix over the v-major zone [vin_z0, n) (exclusive scan, n - vin_z0 + 1 entries)
     uint32_t *vin_cap = nullptr;
     uint32_t vin_z0 = 0;
+    uint64_t vin_total = 0;  // vin_cap[n - vin_z0]
 };
 
 // First vertex of the v-major zone: the top 2^TC_VZONE_LOG2 ranks (default 2^20), never

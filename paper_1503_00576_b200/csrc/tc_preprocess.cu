@@ -735,11 +735,11 @@ int build_hubstart_dev(DeviceGraph *g, cudaStream_t s) {
     }
     g->hz = g->n > kHubRanks ? (uint32_t)(g->n - kHubRanks) : 0u;
     if (!g->hubstart) TC_CHECK(dalloc_t(&g->hubstart, g->n ? g->n : 1, s, g->persistent));
-    if (g->n) {
+    if (g->n && !g->hubstart_ready) {
         k_hub_init<<<grid_for(g->n, 256, kSMs * 16), 256, 0, s>>>(g->off32, g->n, g->hubstart);
         TC_LAUNCHED();
     }
-    if (g->m) {
+    if (g->m && !g->hubstart_ready) {
         k_hub_boundary<<<grid_for(g->m, 256, kSMs * 16), 256, 0, s>>>(g->src, g->dst, g->off32, g->m,
                                                                       g->hz, g->hubstart);
         TC_LAUNCHED();
@@ -842,11 +842,16 @@ __device__ __forceinline__ void cswap(uint32_t &a, uint32_t &b) {
 
 // d <= 16: thread per list, 16-wide bitonic network in registers (pad = ~0).
 __global__ void __launch_bounds__(256)
-    k_seg_sort16(const uint32_t *__restrict__ off32, uint64_t n, uint32_t *__restrict__ dst) {
+    k_seg_sort16(const uint32_t *__restrict__ off32, uint64_t n, uint32_t *__restrict__ dst, uint32_t hz,
+                 uint32_t *__restrict__ hs) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += stride) {
         const uint32_t s = off32[u], d = off32[u + 1] - s;
-        if (d < 2 || d > 16) continue;
+        if (d > 16) continue;
+        if (d < 2) {
+            if (hs) hs[u] = s + (d == 1 && dst[s] < hz ? 1u : 0u);
+            continue;
+        }
         uint32_t x[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) x[i] = (uint32_t)i < d ? dst[s + i] : 0xffffffffu;
@@ -862,16 +867,21 @@ __global__ void __launch_bounds__(256)
                         else cswap(x[l], x[i]);
                     }
                 }
+        uint32_t below = 0;  // non-hub prefix length (elements < hz; pads are ~0)
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
+        for (int i = 0; i < 16; ++i) {
             if ((uint32_t)i < d) dst[s + i] = x[i];
+            below += x[i] < hz ? 1u : 0u;
+        }
+        if (hs) hs[u] = s + below;
     }
 }
 
 // 17..64: warp per list, element 2*lane+h in register h; bitonic over 64 with shuffles.
 __global__ void __launch_bounds__(256)
     k_seg_sort64(const uint32_t *__restrict__ off32, const uint32_t *__restrict__ list,
-                 const unsigned *__restrict__ count, uint32_t *__restrict__ dst) {
+                 const unsigned *__restrict__ count, uint32_t *__restrict__ dst, uint32_t hz,
+                 uint32_t *__restrict__ hs) {
     const unsigned lane = lane_id();
     const unsigned nl = *count;
     const unsigned gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -908,6 +918,11 @@ __global__ void __launch_bounds__(256)
             const uint32_t i = 2 * lane + h;
             if (i < d) dst[s + i] = x[h];
         }
+        if (hs) {
+            const uint32_t below = __popc(__ballot_sync(TC_FULL_MASK, x[0] < hz)) +
+                                   __popc(__ballot_sync(TC_FULL_MASK, x[1] < hz));
+            if (lane == 0) hs[u] = s + below;
+        }
     }
 }
 
@@ -916,7 +931,8 @@ __global__ void __launch_bounds__(256)
 template <int K>
 __global__ void __launch_bounds__(256)
     k_seg_sort_warp(const uint32_t *__restrict__ off32, const uint32_t *__restrict__ list,
-                    const unsigned *__restrict__ count, uint32_t *__restrict__ dst) {
+                    const unsigned *__restrict__ count, uint32_t *__restrict__ dst, uint32_t hz,
+                    uint32_t *__restrict__ hs) {
     constexpr int N = 32 * K;
     const unsigned lane = lane_id();
     const unsigned nl = *count;
@@ -957,18 +973,22 @@ __global__ void __launch_bounds__(256)
                 }
             }
         }
+        uint32_t below = 0;
 #pragma unroll
         for (int r = 0; r < K; ++r) {
             const uint32_t i = 32 * r + lane;
             if (i < d) dst[s + i] = x[r];
+            below += __popc(__ballot_sync(TC_FULL_MASK, x[r] < hz));
         }
+        if (hs && lane == 0) hs[u] = s + below;
     }
 }
 
 // 257..4096: CTA per list, shared-memory bitonic over the next power of two.
 __global__ void __launch_bounds__(256)
     k_seg_sort4k(const uint32_t *__restrict__ off32, const uint32_t *__restrict__ list,
-                 const unsigned *__restrict__ count, uint32_t *__restrict__ dst) {
+                 const unsigned *__restrict__ count, uint32_t *__restrict__ dst, uint32_t hz,
+                 uint32_t *__restrict__ hs) {
     __shared__ uint32_t sh[4096];
     const unsigned nl = *count;
     for (unsigned w = blockIdx.x; w < nl; w += gridDim.x) {
@@ -992,6 +1012,14 @@ __global__ void __launch_bounds__(256)
             }
         }
         for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) dst[s + i] = sh[i];
+        if (hs && threadIdx.x == 0) {  // lower bound of hz in the sorted list
+            uint32_t a = 0, n2 = d;
+            while (n2 > 0) {
+                const uint32_t h2 = n2 >> 1;
+                if (sh[a + h2] < hz) { a += h2 + 1; n2 -= h2 + 1; } else n2 = h2;
+            }
+            hs[u] = s + a;
+        }
         __syncthreads();
     }
 }
@@ -1014,6 +1042,20 @@ __global__ void k_big_back(const uint32_t *__restrict__ off32, const uint32_t *_
     for (uint32_t b = blockIdx.x; b < nbig; b += gridDim.x) {
         const uint32_t u = big[b], s = off32[u], d = off32[u + 1] - s, c = cstart[b];
         for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) dst[s + i] = (uint32_t)(keys[c + i] & mask);
+    }
+}
+
+__global__ void k_big_hubstart(const uint32_t *__restrict__ off32, const uint32_t *__restrict__ big,
+                               uint32_t nbig, const uint32_t *__restrict__ dst, uint32_t hz,
+                               uint32_t *__restrict__ hs) {
+    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nbig; b += gridDim.x * blockDim.x) {
+        const uint32_t u = big[b], s = off32[u];
+        uint32_t a = 0, n2 = off32[u + 1] - s;
+        while (n2 > 0) {
+            const uint32_t h2 = n2 >> 1;
+            if (dst[s + a + h2] < hz) { a += h2 + 1; n2 -= h2 + 1; } else n2 = h2;
+        }
+        hs[u] = s + a;
     }
 }
 
@@ -1077,15 +1119,19 @@ static int bucket_csr_dev(const uint64_t *keys, uint64_t m, uint64_t n, int vb, 
     k_seg_classify<<<grid_for(n, 256, kSMs * 8), 256, 0, s>>>(out->off32, n, mid, big, warpl, w256,
                                                               w1k, counts);
     TC_LAUNCHED();
-    k_seg_sort16<<<grid_for(n, 256, kSMs * 16), 256, 0, s>>>(out->off32, n, out->dst);
+    // hubstart (first element >= hz of every list) falls out of the sorts for free
+    const uint32_t hz = n > kHubRanks ? (uint32_t)(n - kHubRanks) : 0u;
+    if (!out->hubstart) TC_CHECK(dalloc_t(&out->hubstart, n, s, out->persistent));
+    uint32_t *hs = out->hubstart;
+    k_seg_sort16<<<grid_for(n, 256, kSMs * 16), 256, 0, s>>>(out->off32, n, out->dst, hz, hs);
     TC_LAUNCHED();
-    k_seg_sort64<<<kSMs * 8, 256, 0, s>>>(out->off32, warpl, counts + 0, out->dst);
+    k_seg_sort64<<<kSMs * 8, 256, 0, s>>>(out->off32, warpl, counts + 0, out->dst, hz, hs);
     TC_LAUNCHED();
-    k_seg_sort_warp<8><<<kSMs * 8, 256, 0, s>>>(out->off32, w256, counts + 3, out->dst);
+    k_seg_sort_warp<8><<<kSMs * 8, 256, 0, s>>>(out->off32, w256, counts + 3, out->dst, hz, hs);
     TC_LAUNCHED();
-    k_seg_sort_warp<32><<<kSMs * 8, 256, 0, s>>>(out->off32, w1k, counts + 4, out->dst);
+    k_seg_sort_warp<32><<<kSMs * 8, 256, 0, s>>>(out->off32, w1k, counts + 4, out->dst, hz, hs);
     TC_LAUNCHED();
-    k_seg_sort4k<<<kSMs * 8, 256, 0, s>>>(out->off32, mid, counts + 1, out->dst);
+    k_seg_sort4k<<<kSMs * 8, 256, 0, s>>>(out->off32, mid, counts + 1, out->dst, hz, hs);
     TC_LAUNCHED();
     unsigned nbig = 0;
     TC_CUDA(cudaMemcpyAsync(&nbig, counts + 2, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
@@ -1118,6 +1164,8 @@ static int bucket_csr_dev(const uint64_t *keys, uint64_t m, uint64_t n, int vb, 
         k_big_back<<<nbig < kSMs * 8 ? nbig : kSMs * 8, 256, 0, s>>>(out->off32, big, cstart, nbig, vb,
                                                                     sorted, out->dst);
         TC_LAUNCHED();
+        k_big_hubstart<<<grid_for(nbig, 256, kSMs), 256, 0, s>>>(out->off32, big, nbig, out->dst, hz, hs);
+        TC_LAUNCHED();
         dfree(bk, s);
         dfree(balt, s);
         dfree(hist, s);
@@ -1125,6 +1173,7 @@ static int bucket_csr_dev(const uint64_t *keys, uint64_t m, uint64_t n, int vb, 
     }
     k_fill_src<<<grid_for(n, 256, kSMs * 16), 256, 0, s>>>(out->off32, n, out->src);
     TC_LAUNCHED();
+    out->hubstart_ready = true;
     dfree(counts, s);
     dfree(warpl, s);
     dfree(w256, s);
