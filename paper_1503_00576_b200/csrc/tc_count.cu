@@ -205,6 +205,62 @@ __device__ __forceinline__ uint32_t sweep(const uint32_t *__restrict__ dst, cons
     return found;
 }
 
+// sweep() specialised to a shared-memory bitmap probe over the hub zone: item w hits iff
+// bit (w - hz) of `bitmap` is set.  Branch-free and lean: an invalid item (outside its
+// list in a boundary chunk) is replaced by hz before the probe (bit 0 of word 0 -- always
+// in range) and its hit is masked; valid items are >= hz by construction of the callers.
+template <int U>
+__device__ __forceinline__ uint32_t sweep_bits(const uint32_t *__restrict__ dst, const EdgeTable<uint32_t> &et,
+                                               uint32_t nwin, uint32_t c0, uint32_t c1,
+                                               const uint32_t *bitmap, uint32_t hz) {
+    const unsigned lane = lane_id();
+    uint32_t k = 0;
+    {
+        const uint32_t c = c0 + lane < c1 ? c0 + lane : c1 - 1;
+        uint32_t a = 0, b = nwin;
+        while (b - a > 1) {
+            const uint32_t mid = (a + b) >> 1;
+            if (et.cst[mid] <= c) a = mid; else b = mid;
+        }
+        k = a;
+    }
+    uint32_t nextb = et.cst[k + 1];
+    uint32_t cb = et.cb[k], lo = et.vs[k];
+    uint32_t span = et.ve[k] - lo;
+    uint32_t found = 0;
+    for (uint32_t base = c0; base < c1; base += 32 * U) {
+        uint4 q[U];
+        uint32_t rel[U], sp[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            uint32_t c = base + j * 32 + lane;
+            const bool live = c < c1;
+            c = live ? c : c1 - 1;
+            if (c >= nextb) {
+                do { nextb = et.cst[++k + 1]; } while (c >= nextb);
+                cb = et.cb[k];
+                lo = et.vs[k];
+                span = et.ve[k] - lo;
+            }
+            const uint32_t p = cb + 4 * c;
+            q[j] = __ldg(reinterpret_cast<const uint4 *>(dst + p));
+            rel[j] = p - lo;
+            sp[j] = live ? span : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const uint32_t w4[4] = {q[j].x, q[j].y, q[j].z, q[j].w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t ok = (rel[j] + i < sp[j]) ? 1u : 0u;
+                const uint32_t r = (ok ? w4[i] : hz) - hz;
+                found += (bitmap[r >> 5] >> (r & 31)) & ok;
+            }
+        }
+    }
+    return found;
+}
+
 // Dense edges of a heavy source: |adj(u) ∩ adj(v)| = popcount(B_u & B_v) over the hub
 // words v can reach.  Chunk c of edge k reads 4 words of B_v at global word cb_k + 4c and
 // 4 words of the shared-memory B_u at word vs_k + 4c (both 16-byte aligned).
@@ -960,12 +1016,8 @@ __global__ void TC_HUB_BOUNDS(NT)
                     if (pass == 2) {
                         acc += sweep_and<U>(dense_bits, et, NT, c0, c1, bm);
                     } else if (pass == 0) {
-                        const uint32_t last = hwords - 1;
-                        acc += sweep<uint32_t, false, U>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t) {
-                            const uint32_t r = w - hz;
-                            const uint32_t word = lds32(bm + 4 * min(r >> 5, last));
-                            return ((word >> (r & 31)) & 1u) != 0u;
-                        });
+                        // hub suffixes [hubstart[v], ve): every valid item is >= hz
+                        acc += sweep_bits<U>(dst, et, NT, c0, c1, bitmap, hz);
                     } else {
                         acc += sweep<uint32_t, false>(dst, et, NT, c0, c1,
                                                       [&](uint32_t w, uint32_t) { return ck.contains(w); });
@@ -1317,10 +1369,8 @@ __global__ void __launch_bounds__(NT)
                         return w >= hz ? b : ck.contains(w);
                     });
                 } else {
-                    acc += sweep<uint32_t, false, U>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t) {
-                        const uint32_t r = w - hz;
-                        return (w >= hz) & (((lds32(bm + 4 * min(r >> 5, hwp - 1)) >> (r & 31)) & 1u) != 0u);
-                    });
+                    // suffix items exceed v >= hz: every valid item is a hub item
+                    acc += sweep_bits<U>(dst, et, NT, c0, c1, bitmap, hz);
                 }
             }
             __syncthreads();
