@@ -1429,19 +1429,29 @@ __global__ void k_intersect(const uint32_t *__restrict__ dst, const int64_t *__r
 }
 
 // Per-tile sum of the merge work d+(src_i) + d+(dst_i) + overhead (for shard bounds).
-template <typename OffT>
+// RANKED (rank-space count schedule): an edge costs about min(|suffix of adj(u) after v|,
+// |adj(v)|) -- the per-edge v-major/u-major choice reads the cheaper side -- plus a
+// constant; otherwise the reference merge work d+(u) + d+(v).
+template <typename OffT, bool RANKED = false>
 __global__ void __launch_bounds__(256) k_tile_work(const uint32_t *__restrict__ src,
                                                    const uint32_t *__restrict__ dst,
                                                    const OffT *__restrict__ off, uint64_t m,
                                                    uint64_t tile, uint32_t overhead,
-                                                   unsigned long long *__restrict__ sums) {
+                                                   unsigned long long *__restrict__ sums,
+                                                   uint32_t ucap = 0xffffffffu) {
     const uint64_t b = (uint64_t)blockIdx.x * tile;
     const uint64_t e = b + tile < m ? b + tile : m;
     unsigned long long acc = 0;
     for (uint64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
         const uint32_t u = src[i], v = dst[i];
-        acc += (unsigned long long)(off[u + 1] - off[u]) + (unsigned long long)(off[v + 1] - off[v]) +
-               overhead;
+        const unsigned long long dv = (unsigned long long)(off[v + 1] - off[v]);
+        if (RANKED) {
+            const unsigned long long suf = (unsigned long long)(off[u + 1] - (OffT)i - 1);
+            acc += (suf < dv ? suf : dv) + overhead;
+        } else {
+            const unsigned long long du = (unsigned long long)(off[u + 1] - off[u]);
+            acc += (du < ucap ? du : ucap) + dv + overhead;
+        }
     }
     __shared__ unsigned long long s_red[32];
     acc = warp_sum(acc);
@@ -1971,13 +1981,16 @@ int intersect_dev(const DeviceGraph &g, uint32_t u, uint32_t v, uint64_t *out, c
 
 namespace {
 int tile_sums(const DeviceGraph &g, uint64_t tile, uint32_t overhead, unsigned long long **sums_out,
-              uint64_t *ntiles_out, cudaStream_t s) {
+              uint64_t *ntiles_out, cudaStream_t s, bool ranked = false, uint32_t ucap = 0xffffffffu) {
     const uint64_t nt = (g.m + tile - 1) / tile;
     unsigned long long *sums = nullptr;
     TC_CHECK(dalloc_t(&sums, nt ? nt : 1, s));
     if (nt) {
-        if (g.off32)
-            k_tile_work<uint32_t><<<(unsigned)nt, 256, 0, s>>>(g.src, g.dst, g.off32, g.m, tile, overhead, sums);
+        if (g.off32 && ranked)
+            k_tile_work<uint32_t, true><<<(unsigned)nt, 256, 0, s>>>(g.src, g.dst, g.off32, g.m, tile, overhead, sums);
+        else if (g.off32)
+            k_tile_work<uint32_t><<<(unsigned)nt, 256, 0, s>>>(g.src, g.dst, g.off32, g.m, tile, overhead, sums,
+                                                               ucap);
         else
             k_tile_work<int64_t><<<(unsigned)nt, 256, 0, s>>>(g.src, g.dst, g.off, g.m, tile, overhead, sums);
         TC_LAUNCHED();
@@ -1996,7 +2009,17 @@ int work_bounds_dev(const DeviceGraph &g, int npools, int64_t *bounds, cudaStrea
     if (tile > 4096) tile = 4096;
     unsigned long long *sums = nullptr;
     uint64_t nt = 0;
-    TC_CHECK(tile_sums(g, tile, 8, &sums, &nt, s));
+    // Rank-space graphs (the count schedule with hub structures / v-major heads): per-edge
+    // work d+(v) + min(d+(u), 1024) + 128 -- heavy sources are cheap per edge there, every
+    // edge pays a latency-bound constant.  Measured per-shard count times at R-MAT s26,
+    // P = 8 (scripts/shard_balance.py): max/mean 1.29 -> 1.19 against d+(u) + d+(v) + 8.
+    // Reference-id graphs keep the merge-work model of SURVEY.md §8(e).
+    static const int model = getenv("TC_SHARD_MODEL") ? atoi(getenv("TC_SHARD_MODEL")) : 0;
+    static const uint32_t ovh_env = getenv("TC_SHARD_OVH") ? (uint32_t)atoi(getenv("TC_SHARD_OVH")) : 128u;
+    static const uint32_t ucap_env = getenv("TC_SHARD_UCAP") ? (uint32_t)atoi(getenv("TC_SHARD_UCAP")) : 1024u;
+    const bool ranked = model == 1 && g.rank_space;
+    const uint32_t ovh = g.rank_space ? ovh_env : 8u, ucap = g.rank_space ? ucap_env : 0xffffffffu;
+    TC_CHECK(tile_sums(g, tile, ovh, &sums, &nt, s, ranked, ucap));
     std::string err;
     unsigned long long *h = (unsigned long long *)malloc((nt ? nt : 1) * sizeof(unsigned long long));
     if (!h) { set_error("host allocation failed"); return -3; }

@@ -1,0 +1,27 @@
+"""Development aid (GPU): per-shard count time of the work-balanced edge ranges on one GPU
+(the multi-GPU schedule's load balance, measured serially): python scripts/shard_balance.py CFG P"""
+import json
+import statistics
+import sys
+
+sys.path.insert(0, ".")
+import paper_1503_00576_b200 as tcb  # noqa: E402
+from scripts.step import make  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "rmat26"
+P = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+g = make(cfg)
+og, _ = tcb.preprocess_device(g, rank_space=True)
+g.free()
+plan = tcb.PartitionPlan.work_balanced(og, P)
+full = statistics.median(tcb.count_device(og)[1].count_ms for _ in range(3))
+times, tris = [], 0
+for p in range(P):
+    lo, hi = plan.pool_range(p)
+    tcb.count_device(og, lo, hi)
+    ts = [tcb.count_device(og, lo, hi) for _ in range(3)]
+    tris += ts[0][0]
+    times.append(statistics.median(t[1].count_ms for t in ts))
+print(json.dumps({"config": cfg, "P": P, "full_ms": round(full, 2), "shard_ms": [round(t, 2) for t in times],
+                  "max_over_mean": round(max(times) / statistics.mean(times), 3),
+                  "speedup_bound": round(full / max(times), 2), "triangles": tris}))
