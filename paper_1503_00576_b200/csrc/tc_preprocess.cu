@@ -452,8 +452,8 @@ int graph_alloc(DeviceGraph *g, uint64_t m, uint64_t n, cudaStream_t s) {
     g->m = m;
     g->n = n;
     const bool ps = g->persistent;
-    TC_CHECK(dalloc_t(&g->src, m + 4, s, ps));
-    TC_CHECK(dalloc_t(&g->dst, m + 4, s, ps));  // +16 B so 128-bit tail loads stay in bounds
+    TC_CHECK(dalloc_t(&g->src, m + 8, s, ps));
+    TC_CHECK(dalloc_t(&g->dst, m + 8, s, ps));  // +32 B so 32-byte chunk loads stay in bounds
     TC_CHECK(dalloc_t(&g->off, n + 1, s, ps));
     g->off32 = nullptr;
     if (m < (1ull << 32)) TC_CHECK(dalloc_t(&g->off32, n + 1, s, ps));
@@ -487,7 +487,7 @@ int finalize_graph_dev(DeviceGraph *g, cudaStream_t s) {
     } else if (g->off32) {
         TC_CUDA(cudaMemsetAsync(g->off32, 0, sizeof(uint32_t), s));
     }
-    TC_CUDA(cudaMemsetAsync(g->dst + g->m, 0, 4 * sizeof(uint32_t), s));
+    TC_CUDA(cudaMemsetAsync(g->dst + g->m, 0, 8 * sizeof(uint32_t), s));
     TC_CUDA(cudaMemsetAsync(dmax, 0, sizeof(uint32_t), s));
     if (g->n) {
         k_max_degree<<<grid_for(g->n, 256, kSMs * 8), 256, 0, s>>>(g->off, g->n, dmax);
@@ -623,7 +623,7 @@ int preprocess_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, Devic
     TC_CHECK(dalloc_t(&alt, m ? m : 1, s));
     TC_CHECK(radix_sort(keys, alt, nullptr, nullptr, m, plan, hist, kOutSoA, out->src, out->dst, vb,
                         nullptr, nullptr, s));
-    TC_CUDA(cudaMemsetAsync(out->dst + m, 0, 4 * sizeof(uint32_t), s));
+    TC_CUDA(cudaMemsetAsync(out->dst + m, 0, 8 * sizeof(uint32_t), s));
     TC_CHECK(build_node_array_dev(out->src, m, n, out->off, out->off32, scratch + 1, s));
     TC_CUDA(cudaMemcpyAsync(&out->max_out, scratch + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     dfree(deg, s);
@@ -1249,12 +1249,12 @@ int preprocess_rank_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, 
     TC_CHECK(graph_alloc(out, m, n, s));
     if (bucket) {
         TC_CHECK(bucket_csr_dev(keys, m, n, vb, outdeg, out, scratch + 1, s));
-        TC_CUDA(cudaMemsetAsync(out->dst + m, 0, 4 * sizeof(uint32_t), s));
+        TC_CUDA(cudaMemsetAsync(out->dst + m, 0, 8 * sizeof(uint32_t), s));
     } else {
         TC_CHECK(dalloc_t(&alt, m ? m : 1, s));
         TC_CHECK(radix_sort(keys, alt, nullptr, nullptr, m, plan, hist, kOutSoA, out->src, out->dst, vb,
                             nullptr, nullptr, s));
-        TC_CUDA(cudaMemsetAsync(out->dst + m, 0, 4 * sizeof(uint32_t), s));
+        TC_CUDA(cudaMemsetAsync(out->dst + m, 0, 8 * sizeof(uint32_t), s));
         TC_CHECK(build_node_array_dev(out->src, m, n, out->off, out->off32, scratch + 1, s));
     }
     TC_CHECK(build_hubstart_dev(out, s));
@@ -1309,7 +1309,7 @@ int relabel_dev(const DeviceGraph &g, DeviceGraph *out, cudaStream_t s) {
     TC_CHECK(graph_alloc(out, m, n, s));
     TC_CHECK(radix_sort(keys, alt, nullptr, nullptr, m, plan, hist, kOutSoA, out->src, out->dst, vb,
                         nullptr, nullptr, s));
-    TC_CUDA(cudaMemsetAsync(out->dst + m, 0, 4 * sizeof(uint32_t), s));
+    TC_CUDA(cudaMemsetAsync(out->dst + m, 0, 8 * sizeof(uint32_t), s));
     TC_CHECK(build_node_array_dev(out->src, m, n, out->off, out->off32, scratch + 1, s));
     TC_CHECK(build_hubstart_dev(out, s));
     TC_CUDA(cudaMemcpyAsync(&out->max_out, scratch + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
