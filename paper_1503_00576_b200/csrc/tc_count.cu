@@ -1043,7 +1043,7 @@ __global__ void TC_HUB_BOUNDS(NT)
 // keep their dependent load chains (task -> offsets -> lists) in flight together, which
 // the CTA-per-task hub kernel (one 32 KB bitmap per task) cannot.
 constexpr int kMidWarps = 8;
-constexpr uint32_t kMidSlots = 4 * 512;
+constexpr uint32_t kMidSlots = 3 * 512;
 
 template <int WARPS, uint32_t SLOTS, uint32_t LOADINV>
 __global__ void __launch_bounds__(32 * WARPS)
@@ -1578,7 +1578,7 @@ static void clear_l2_window(cudaStream_t s) {
 // over the lanes and probed.  These heads have small in-degrees, so many small independent
 // tasks are in flight per SM (no block barriers).
 constexpr int kVlWarps = 8;
-constexpr uint32_t kVlSlots = 4 * kVNonHubCap;
+constexpr uint32_t kVlSlots = 3 * kVNonHubCap;  // cuckoo load <= 1/3: 4 CTAs per SM
 
 __global__ void __launch_bounds__(32 * kVlWarps)
     k_count_vlow_warp(const uint32_t *__restrict__ dst, const uint32_t *__restrict__ off, uint32_t z0,
@@ -1602,7 +1602,7 @@ __global__ void __launch_bounds__(32 * kVlWarps)
         const uint2 task = tasks[t];
         const uint32_t h = task.x, v = z0 + h;
         const uint32_t vs = __ldg(off + v), ve = __ldg(off + v + 1), d = ve - vs;
-        Cuckoo32 ck{smem_addr(tab), 4 * d < kVlSlots ? 4 * d : kVlSlots, 0, 0};
+        Cuckoo32 ck{smem_addr(tab), 3 * d < kVlSlots ? 3 * d : kVlSlots, 0, 0};
         for (uint32_t seed = 0;; ++seed) {
             if (seed == 32) __trap();  // cannot happen at load <= 1/4; never miscount
             ck.c1 = seed_mult(seed, 0);
@@ -1859,7 +1859,8 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
             g.hubstart) {
             const VSplit vp{vmajor ? vzone_start(g) : 0xffffffffu, g.hz, g.vt, g.hwp, dense_factor_env(),
                             kVNonHubCap, vm_bias_env(), vm_lowall_env(), g.hubstart};
-            if (c == 0) TC_CHECK((launch_mid<kMidWarps, kMidSlots, 4>(g, vp, rg, tasks[c], nt_c, next_c, d_total, s)));
+            // cuckoo load <= 1/3: 6 KB per warp, 4 CTAs (32 warps) per SM (load 1/4: 3 CTAs, +12 %)
+            if (c == 0) TC_CHECK((launch_mid<kMidWarps, kMidSlots, 3>(g, vp, rg, tasks[c], nt_c, next_c, d_total, s)));
             else TC_CHECK((launch_mid<4, 3 * 2048, 3>(g, vp, rg, tasks[c], nt_c, next_c, d_total, s)));
             continue;
         }
