@@ -938,7 +938,7 @@ __global__ void TC_HUB_BOUNDS(NT)
         es += (uint64_t)task.y * kChunk;
         ee = ee < es + kChunk ? ee : es + kChunk;
 
-        Cuckoo32 ck{smem_addr(ctab), 4 * nh < cap ? 4 * nh : cap, 0, 0};
+        Cuckoo32 ck{smem_addr(ctab), 3 * nh < cap ? 3 * nh : cap, 0, 0};
         if (nh) {
             for (uint32_t seed = 0;; ++seed) {
                 if (seed == 32) __trap();  // cannot happen at load <= 1/4; never miscount
@@ -1821,7 +1821,7 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
                   (vm_env == 1 || (g.m >= (1ull << 27) && g.max_out > 256));
     for (int c = 0; c < kClasses && vmajor; ++c)
         if (g.max_out > lower[c] &&
-            4 * ((size_t)g.hwp + 4 * (g.max_out < kClassMax[c] ? g.max_out : kClassMax[c])) > 200 * 1024)
+            4 * ((size_t)g.hwp + 3 * (g.max_out < kClassMax[c] ? g.max_out : kClassMax[c])) > 200 * 1024)
             vmajor = false;
     if (g.max_out > (uint32_t)kLightMax) {
         k_classify<OffT><<<grid_for(nverts, 256, kSMs * 8), 256, 0, s>>>(
@@ -1850,7 +1850,8 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
         const unsigned *nt_c = counters + c;
         unsigned *next_c = counters + kClasses + c;
         int rc = 0;
-        const uint32_t hub_cap = 4 * (g.max_out < kClassMax[c] ? g.max_out : kClassMax[c]);
+        // non-hub part of adj(u) in a cuckoo table at load <= 1/3 (smem: bitmap + table)
+        const uint32_t hub_cap = 3 * (g.max_out < kClassMax[c] ? g.max_out : kClassMax[c]);
         const size_t hub_sm = 4 * ((size_t)g.hwp + hub_cap);
         static const int midwarp = getenv("TC_MIDWARP") ? atoi(getenv("TC_MIDWARP")) : 1;
         // with v-major on, the hub heads' dense edges are gone and the class-0 tasks are
