@@ -117,6 +117,28 @@ def measured_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def dominant_kernel_from_profiles(peak: float):
+    """The count's largest kernel in the committed ncu capture (time and DRAM bytes per launch,
+    cold-cache / serialised under ncu) -- the kernel-level roofline beside the phase-level one."""
+    import csv
+    path = os.path.join(ROOT, "profiles", "r01_dram_count_s26_vmajor.csv")
+    try:
+        rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+    except OSError:
+        return None
+    h = rows[0]
+    ki, mi, vi, ii = (h.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "ID"))
+    per = {}
+    for r in rows[1:]:
+        per.setdefault((int(r[ii]), r[ki]), {})[r[mi]] = float(r[vi].replace(",", ""))
+    (_, name), d = max(per.items(), key=lambda kv: kv[1].get("gpu__time_duration.sum", 0))
+    ms = d["gpu__time_duration.sum"] / 1e6
+    b = d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
+    return {"name": name.split("(")[0].replace("void ", ""), "ncu_ms": round(ms, 3),
+            "dram_bytes": b, "dram_gbs": round(b / ms / 1e6, 1), "dram_frac": round(b / ms / 1e6 / peak, 4),
+            "source": "profiles/r01_dram_count_s26_vmajor.csv (ncu, one count call)"}
+
+
 def traffic_from_profiles(workload: str):
     """dram read+write bytes per count call from the committed ncu capture, if any."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
@@ -292,7 +314,8 @@ def main():
                 "kernel": "count phase (k_classify + k_vin_* hub-head index + k_count_vmajor + "
                           "k_count_hub + k_count_light_tpe)",
                 "algorithmic_bytes_per_launch": alg_bytes, "launch_ms": round(count_ms, 3),
-                "peak_source": peak_src}
+                "peak_source": peak_src,
+                "dominant_kernel": dominant_kernel_from_profiles(peak) if workload == "rmat_s26_ef16_seed0" else None}
 
     # ------------------------------------------------------------ timed: e2e ---
     e2e = None
