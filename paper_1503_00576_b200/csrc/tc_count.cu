@@ -1276,8 +1276,13 @@ __global__ void k_vin_tasks(const uint32_t *__restrict__ start, const uint32_t *
     }
 }
 
+#ifndef TC_VM_MINB
+#define TC_VM_BOUNDS(nt) __launch_bounds__(nt)
+#else
+#define TC_VM_BOUNDS(nt) __launch_bounds__(nt, TC_VM_MINB)
+#endif
 template <int NT, int U>
-__global__ void __launch_bounds__(NT)
+__global__ void TC_VM_BOUNDS(NT)
     k_count_vmajor(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
                    const uint32_t *__restrict__ off, const uint32_t *__restrict__ hubstart,
                    uint32_t z0, uint32_t hz, uint32_t hwp, uint32_t cap,
