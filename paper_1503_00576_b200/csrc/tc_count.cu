@@ -481,6 +481,8 @@ __global__ void __launch_bounds__(NT)
 // v's data (dense bitmap words, or adj(v) as 16-byte chunks).  Every kernel evaluates the
 // same predicate, so each edge is counted exactly once.  Edges with an empty suffix or
 // an empty adj(v) close no triangle and are skipped by everyone.
+constexpr uint32_t kVBigNonHub = 4096;  // v-major heads below hz with long lists: non-hub cap
+
 struct VSplit {
     uint32_t z0, hz, vt, hwp, factor, nhcap;  // v-major zone [z0, n); z0 = ~0: v-major off
     uint32_t bias;                            // v-major iff bias/4 * vcost < ucost
@@ -498,9 +500,11 @@ __device__ __forceinline__ bool vmajor_edge(const VSplit &vp, uint32_t e, uint32
         const bool dense = v >= vp.vt && (vp.hwp - ws) < vp.factor * (ve - vs);
         ucost = dense ? 4 * (vp.hwp - ws) : 16 * ((ve - (vs & ~3u) + 3) >> 2);
     } else {
-        // below the hub zone: adj(v) goes into a per-warp cuckoo table (k_count_vlow_warp),
-        // so it must fit; by default only short suffixes (light sources) go there
-        if (ve - vs > vp.nhcap || (!vp.lowall && eu - e - 1 >= 32)) return false;
+        // below the hub zone: adj(v) goes into a per-warp cuckoo table (k_count_vlow_warp) when
+        // |adj(v)| <= nhcap; longer lists run as CTA tasks (hub part as a bitmap, non-hub part
+        // in a cuckoo table of at most kVBigNonHub keys)
+        if (!vp.lowall && eu - e - 1 >= 32) return false;
+        if (ve - vs > vp.nhcap && __ldg(vp.hubstart + v) - vs > kVBigNonHub) return false;
         ucost = 16 * ((ve - (vs & ~3u) + 3) >> 2) + 16;
     }
     return (uint64_t)(4 * (eu - e - 1) + 8) * vp.bias < (uint64_t)ucost * 4;
@@ -1267,12 +1271,20 @@ __global__ void k_vin_capacity(const uint32_t *__restrict__ deg_by_rank, const u
     }
 }
 
+// Tasks in head order; heads below the hub zone (h < hb) whose list exceeds `small` are
+// also appended to `big` (they run as CTA tasks, the warp kernel skips them).
 __global__ void k_vin_tasks(const uint32_t *__restrict__ start, const uint32_t *__restrict__ tstart,
-                            uint32_t nh, uint2 *__restrict__ tasks) {
+                            uint32_t nh, uint2 *__restrict__ tasks, const uint32_t *__restrict__ off,
+                            uint32_t z0, uint32_t hb, uint32_t small, uint2 *__restrict__ big,
+                            unsigned *__restrict__ nbig) {
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += stride) {
         const uint32_t t0 = tstart[h], t1 = tstart[h + 1];
         for (uint32_t t = t0; t < t1; ++t) tasks[t] = make_uint2(h, t - t0);
+        if (h < hb && t1 > t0 && off[z0 + h + 1] - off[z0 + h] > small) {
+            const unsigned b = atomicAdd(nbig, t1 - t0);
+            for (uint32_t t = t0; t < t1; ++t) big[b + t - t0] = make_uint2(h, t - t0);
+        }
     }
 }
 
@@ -1367,11 +1379,11 @@ __global__ void TC_VM_BOUNDS(NT)
             if (c0 < c1) {
                 // suffix items are > v: hub items hit words >= ws (staged); non-hub items
                 // (only when v < hz) are looked up in the cuckoo table
-                if (nh) {
+                if (v < hz) {  // suffix items below hz exist: bitmap or cuckoo per item
                     acc += sweep<uint32_t, false, U>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t) {
                         const uint32_t r = w - hz;
                         const bool b = ((lds32(bm + 4 * min(r >> 5, hwp - 1)) >> (r & 31)) & 1u) != 0u;
-                        return w >= hz ? b : ck.contains(w);
+                        return w >= hz ? b : (nh != 0 && ck.contains(w));
                     });
                 } else {
                     // suffix items exceed v >= hz: every valid item is a hub item
@@ -1607,6 +1619,7 @@ __global__ void __launch_bounds__(32 * kVlWarps)
         const uint2 task = tasks[t];
         const uint32_t h = task.x, v = z0 + h;
         const uint32_t vs = __ldg(off + v), ve = __ldg(off + v + 1), d = ve - vs;
+        if (d > kVNonHubCap) continue;  // long list: a CTA task (warp-uniform)
         Cuckoo32 ck{smem_addr(tab), 3 * d < kVlSlots ? 3 * d : kVlSlots, 0, 0};
         for (uint32_t seed = 0;; ++seed) {
             if (seed == 32) __trap();  // cannot happen at load <= 1/4; never miscount
@@ -1656,6 +1669,7 @@ __global__ void __launch_bounds__(32 * kVlWarps)
 struct VmajorState {
     uint32_t *cnt = nullptr, *start = nullptr, *tstart = nullptr;
     uint2 *in_e = nullptr;  // (edge, off[u+1]) per indexed in-edge
+    uint2 *big = nullptr;   // CTA tasks of long-list heads below hz
     bool capl = false;      // capacity layout used (overflow flag in next[2])
     unsigned *next = nullptr;
     uint2 *tasks = nullptr;
@@ -1677,9 +1691,11 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
     const uint64_t ie = capl ? (g.vin_total > span ? g.vin_total : span) : span;
     TC_CHECK(dalloc_t(&st->in_e, ie ? ie : 1, s));
     TC_CHECK(dalloc_t(&st->tasks, (size_t)nh + span / kVChunk + 1, s));
-    TC_CHECK(dalloc_t(&st->next, 3, s));  // [0], [1] task cursors, [2] capacity overflow flag
+    // [0], [1] task cursors, [2] capacity overflow flag, [3] big-task count, [4] zero, [5] big cursor
+    TC_CHECK(dalloc_t(&st->next, 6, s));
+    TC_CHECK(dalloc_t(&st->big, (size_t)nh + span / kVChunk + 1, s));
     TC_CUDA(cudaMemsetAsync(st->cnt, 0, (size_t)nh * sizeof(uint32_t), s));
-    TC_CUDA(cudaMemsetAsync(st->next, 0, 3 * sizeof(unsigned), s));
+    TC_CUDA(cudaMemsetAsync(st->next, 0, 6 * sizeof(unsigned), s));
     st->capl = capl;
     // everything below runs on s2 (the index build too, so that with s2 != s it overlaps
     // the u-major kernels on s)
@@ -1703,7 +1719,9 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
                                            capl ? st->next + 2 : nullptr);
     TC_LAUNCHED();
     TC_CHECK(vin_scan<true>(st->cnt, nh, st->tstart, s2));  // tasks from the fill counts
-    k_vin_tasks<<<grid_for(nh, 256, kSMs * 4), 256, 0, s2>>>(startp, st->tstart, nh, st->tasks);
+    const uint32_t hb = (uint32_t)(g.hz - z0);  // first hub-zone head: tasks [tstart[hb], ...)
+    k_vin_tasks<<<grid_for(nh, 256, kSMs * 4), 256, 0, s2>>>(startp, st->tstart, nh, st->tasks, g.off32, z0, hb,
+                                                             kVNonHubCap, st->big, st->next + 3);
     TC_LAUNCHED();
     constexpr int NT = 256;
     auto kern = k_count_vmajor<NT, 4>;
@@ -1714,7 +1732,6 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
     TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, sm));
     per_sm = per_sm / share;
     if (per_sm < 1) per_sm = 1;
-    const uint32_t hb = (uint32_t)(g.hz - z0);  // first hub-zone head: tasks [tstart[hb], ...)
     if (hb) {
         const size_t wsm = (size_t)4 * kVlSlots * kVlWarps;
         TC_CUDA(cudaFuncSetAttribute(k_count_vlow_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
@@ -1726,6 +1743,19 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
                                                                  d_total);
         TC_LAUNCHED();
     }
+    if (hb) {  // long-list heads below hz: CTA tasks with bitmap + non-hub cuckoo (load <= 1/4)
+        const uint32_t bcap = 4 * kVBigNonHub;
+        const size_t bsm = 4 * ((size_t)g.hwp + bcap);
+        TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+        int bper = 1;
+        TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bper, kern, NT, bsm));
+        if (bper < 1) bper = 1;
+        kern<<<kSMs * bper, NT, bsm, s2>>>(g.src, g.dst, g.off32, g.hubstart, z0, g.hz, g.hwp, bcap, startp,
+                                           st->cnt, st->in_e, st->big, st->next + 4, st->next + 3, st->next + 5,
+                                           d_total);
+        TC_LAUNCHED();
+    }
+    TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     kern<<<kSMs * per_sm, NT, sm, s2>>>(g.src, g.dst, g.off32, g.hubstart, z0, g.hz, g.hwp, cap,
                                         startp, st->cnt, st->in_e, st->tasks, st->tstart + hb, st->tstart + nh,
                                         st->next, d_total);
@@ -1757,6 +1787,7 @@ int vmajor_finish(VmajorState *st, cudaStream_t s, CountStats *stats, bool *over
     dfree(st->tstart, s);
     dfree(st->in_e, s);
     dfree(st->tasks, s);
+    dfree(st->big, s);
     dfree(st->next, s);
     *st = VmajorState{};
     return 0;
