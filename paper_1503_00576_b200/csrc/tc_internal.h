@@ -126,10 +126,10 @@ struct DeviceGraph {
     uint64_t vin_total = 0;  // vin_cap[n - vin_z0]
 };
 
-// First vertex of the v-major zone: the top 2^TC_VZONE_LOG2 ranks (default 2^20), never
+// First vertex of the v-major zone: the top 2^TC_VZONE_LOG2 ranks (default 2^22), never
 // above the hub zone start hz.
 inline uint32_t vzone_start_of(uint64_t n, uint32_t hz) {
-    static const int lg = getenv("TC_VZONE_LOG2") ? atoi(getenv("TC_VZONE_LOG2")) : 20;
+    static const int lg = getenv("TC_VZONE_LOG2") ? atoi(getenv("TC_VZONE_LOG2")) : 22;
     const uint64_t Z = 1ull << (lg < 18 ? 18 : lg > 31 ? 31 : lg);
     const uint64_t z0 = n > Z ? n - Z : 0;
     return (uint32_t)(z0 < hz ? z0 : hz);
