@@ -481,7 +481,10 @@ __global__ void __launch_bounds__(NT)
 // v's data (dense bitmap words, or adj(v) as 16-byte chunks).  Every kernel evaluates the
 // same predicate, so each edge is counted exactly once.  Edges with an empty suffix or
 // an empty adj(v) close no triangle and are skipped by everyone.
-constexpr uint32_t kVBigNonHub = 4096;  // v-major heads below hz with long lists: non-hub cap
+#ifndef TC_VBIG
+#define TC_VBIG 256  // 256 / 512 / 1K / 2K / 4K / 8K: s26 count 210 / 210 / 213 / 216 / 222 / 236 ms
+#endif
+constexpr uint32_t kVBigNonHub = TC_VBIG;  // v-major heads below hz with long lists: non-hub cap
 
 struct VSplit {
     uint32_t z0, hz, vt, hwp, factor, nhcap;  // v-major zone [z0, n); z0 = ~0: v-major off
