@@ -1492,7 +1492,10 @@ size_t heavy_smem(int cls, uint32_t max_out) {
     return (size_t)4 * slots;
 }
 
-constexpr uint32_t kVNonHubCap = 512;  // v-major below hz: max |adj(v)| (per-warp cuckoo slots / 4)
+#ifndef TC_VLCAP
+#define TC_VLCAP 512
+#endif
+constexpr uint32_t kVNonHubCap = TC_VLCAP;  // v-major below hz: max |adj(v)| of the warp tasks
 
 static uint32_t vm_lowall_env() {
     static const uint32_t b = getenv("TC_VLOW_ALL") ? (uint32_t)atoi(getenv("TC_VLOW_ALL")) : 1u;
