@@ -98,6 +98,20 @@ struct Cuckoo32 {
     }
 };
 
+// Membership in a sorted list (global memory): the fallback probe when a cuckoo table
+// cannot be built within kCuckooSeeds seeds (pathological key sets) -- slower, never wrong,
+// never a trap.
+constexpr uint32_t kCuckooSeeds = 16;
+
+__device__ __forceinline__ bool sorted_contains(const uint32_t *__restrict__ a, uint32_t n, uint32_t w) {
+    uint32_t lo = 0, len = n;
+    while (len > 0) {
+        const uint32_t h = len >> 1;
+        if (__ldg(a + lo + h) < w) { lo += h + 1; len -= h + 1; } else len = h;
+    }
+    return lo < n && __ldg(a + lo) == w;
+}
+
 // Insert `key` into a 32-bit cuckoo table; returns false after too many evictions.
 __device__ __forceinline__ bool cuckoo_insert32(uint32_t *tab, const Cuckoo32 &c, uint32_t key) {
     uint32_t h = c.h1(key);
@@ -831,9 +845,10 @@ __global__ void __launch_bounds__(NT)
         ee = ee < es + kChunk ? ee : es + kChunk;
 
         Cuckoo32 ck{smem_addr(table), 4 * d < cap ? 4 * d : cap, 0, 0};
+        bool tab_ok = true;
         if (MODE == 0) {
-            for (uint32_t seed = 0;; ++seed) {
-                if (seed == 32) __trap();  // cannot happen at load <= 1/3; never miscount
+            tab_ok = false;
+            for (uint32_t seed = 0; seed < kCuckooSeeds && !tab_ok; ++seed) {
                 ck.c1 = seed_mult(seed, 0);
                 ck.c2 = seed_mult(seed, 1);
                 for (uint32_t i = threadIdx.x; i < ck.T; i += NT) table[i] = kEmpty;
@@ -842,9 +857,8 @@ __global__ void __launch_bounds__(NT)
                 for (uint32_t i = threadIdx.x; i < d; i += NT)
                     if (!cuckoo_insert32(table, ck, __ldg(dst + s + i))) s_fail = 1;
                 __syncthreads();
-                const bool failed = s_fail != 0;
+                tab_ok = s_fail == 0;
                 __syncthreads();
-                if (!failed) break;
             }
         } else {
             for (uint32_t i = threadIdx.x; i < d; i += NT) table[i] = __ldg(dst + s + i);
@@ -874,9 +888,12 @@ __global__ void __launch_bounds__(NT)
             const uint32_t c0 = (uint32_t)((uint64_t)tot * warp / NW);
             const uint32_t c1 = (uint32_t)((uint64_t)tot * (warp + 1) / NW);
             if (c0 < c1) {
-                if (MODE == 0) {
+                if (MODE == 0 && tab_ok) {
                     acc += sweep<OffT, false>(dst, et, nwin, c0, c1,
                                               [&](uint32_t w, uint32_t) { return ck.contains(w); });
+                } else if (MODE == 0) {
+                    acc += sweep<OffT, false>(dst, et, nwin, c0, c1,
+                                              [&](uint32_t w, uint32_t) { return sorted_contains(dst + s, d, w); });
                 } else {
                     acc += sweep<OffT, false>(dst, et, nwin, c0, c1, [&](uint32_t w, uint32_t) {
                         uint32_t a = 0, n = d;
@@ -946,9 +963,10 @@ __global__ void TC_HUB_BOUNDS(NT)
         ee = ee < es + kChunk ? ee : es + kChunk;
 
         Cuckoo32 ck{smem_addr(ctab), 3 * nh < cap ? 3 * nh : cap, 0, 0};
+        bool tab_ok = true;
         if (nh) {
-            for (uint32_t seed = 0;; ++seed) {
-                if (seed == 32) __trap();  // cannot happen at load <= 1/4; never miscount
+            tab_ok = false;
+            for (uint32_t seed = 0; seed < kCuckooSeeds && !tab_ok; ++seed) {
                 ck.c1 = seed_mult(seed, 0);
                 ck.c2 = seed_mult(seed, 1);
                 for (uint32_t i = threadIdx.x; i < ck.T; i += NT) ctab[i] = kEmpty;
@@ -957,9 +975,8 @@ __global__ void TC_HUB_BOUNDS(NT)
                 for (uint32_t i = threadIdx.x; i < nh; i += NT)
                     if (!cuckoo_insert32(ctab, ck, __ldg(dst + s + i))) s_fail = 1;
                 __syncthreads();
-                const bool failed = s_fail != 0;
+                tab_ok = s_fail == 0;
                 __syncthreads();
-                if (!failed) break;
             }
         }
         for (uint32_t i = nh + threadIdx.x; i < e - s; i += NT) {
@@ -1025,9 +1042,13 @@ __global__ void TC_HUB_BOUNDS(NT)
                     } else if (pass == 0) {
                         // hub suffixes [hubstart[v], ve): every valid item is >= hz
                         acc += sweep_bits<U>(dst, et, NT, c0, c1, bitmap, hz);
-                    } else {
+                    } else if (tab_ok) {
                         acc += sweep<uint32_t, false>(dst, et, NT, c0, c1,
                                                       [&](uint32_t w, uint32_t) { return ck.contains(w); });
+                    } else {
+                        acc += sweep<uint32_t, false>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t) {
+                            return sorted_contains(dst + s, nh, w);
+                        });
                     }
                 }
                 __syncthreads();
@@ -1080,8 +1101,8 @@ __global__ void __launch_bounds__(32 * WARPS)
         es += (uint64_t)task.y * kChunk;
         ee = ee < es + kChunk ? ee : es + kChunk;
         Cuckoo32 ck{smem_addr(tab), LOADINV * d < SLOTS ? LOADINV * d : SLOTS, 0, 0};
-        for (uint32_t seed = 0;; ++seed) {
-            if (seed == 32) __trap();  // cannot happen at load <= 1/4; never miscount
+        bool tab_ok = false;
+        for (uint32_t seed = 0; seed < kCuckooSeeds && !tab_ok; ++seed) {
             ck.c1 = seed_mult(seed, 0);
             ck.c2 = seed_mult(seed, 1);
             for (uint32_t i = lane; i < ck.T; i += 32) tab[i] = kEmpty;
@@ -1090,7 +1111,7 @@ __global__ void __launch_bounds__(32 * WARPS)
             for (uint32_t i = lane; i < d; i += 32)
                 if (!cuckoo_insert32(tab, ck, __ldg(dst + s + i))) fail = true;
             __syncwarp();
-            if (!__any_sync(TC_FULL_MASK, fail)) break;
+            tab_ok = !__any_sync(TC_FULL_MASK, fail);
         }
         for (uint64_t ws = es; ws < ee; ws += 32) {
             uint32_t vs = 0, ve = 0, chunks = 0;
@@ -1114,8 +1135,13 @@ __global__ void __launch_bounds__(32 * WARPS)
             s_cst[wp][lane] = cst;
             if (lane == 0) s_cst[wp][32] = tot;
             __syncwarp();
-            acc += sweep<uint32_t, false, 2>(dst, et, 32, 0, tot,
-                                            [&](uint32_t w, uint32_t) { return ck.contains(w); });
+            if (tab_ok)
+                acc += sweep<uint32_t, false, 2>(dst, et, 32, 0, tot,
+                                                [&](uint32_t w, uint32_t) { return ck.contains(w); });
+            else
+                acc += sweep<uint32_t, false, 2>(dst, et, 32, 0, tot, [&](uint32_t w, uint32_t) {
+                    return sorted_contains(dst + s, d, w);
+                });
             __syncwarp();
         }
     }
@@ -1335,9 +1361,10 @@ __global__ void TC_VM_BOUNDS(NT)
         for (uint32_t i = ws + 4 * threadIdx.x; i < hwp; i += 4 * NT)
             *reinterpret_cast<uint4 *>(bitmap + i) = make_uint4(0, 0, 0, 0);
         Cuckoo32 ck{smem_addr(ctab), 4 * nh < cap ? 4 * nh : cap, 0, 0};
+        bool tab_ok = true;
         if (nh) {
-            for (uint32_t seed = 0;; ++seed) {
-                if (seed == 32) __trap();  // cannot happen at load <= 1/4; never miscount
+            tab_ok = false;
+            for (uint32_t seed = 0; seed < kCuckooSeeds && !tab_ok; ++seed) {
                 ck.c1 = seed_mult(seed, 0);
                 ck.c2 = seed_mult(seed, 1);
                 for (uint32_t i = threadIdx.x; i < ck.T; i += NT) ctab[i] = kEmpty;
@@ -1346,9 +1373,8 @@ __global__ void TC_VM_BOUNDS(NT)
                 for (uint32_t i = vs + threadIdx.x; i < hs; i += NT)
                     if (!cuckoo_insert32(ctab, ck, __ldg(dst + i))) s_fail = 1;
                 __syncthreads();
-                const bool failed = s_fail != 0;
+                tab_ok = s_fail == 0;
                 __syncthreads();
-                if (!failed) break;
             }
         }
         __syncthreads();
@@ -1382,11 +1408,17 @@ __global__ void TC_VM_BOUNDS(NT)
             if (c0 < c1) {
                 // suffix items are > v: hub items hit words >= ws (staged); non-hub items
                 // (only when v < hz) are looked up in the cuckoo table
-                if (v < hz) {  // suffix items below hz exist: bitmap or cuckoo per item
+                if (v < hz && tab_ok) {  // suffix items below hz exist: bitmap or cuckoo per item
                     acc += sweep<uint32_t, false, U>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t) {
                         const uint32_t r = w - hz;
                         const bool b = ((lds32(bm + 4 * min(r >> 5, hwp - 1)) >> (r & 31)) & 1u) != 0u;
                         return w >= hz ? b : (nh != 0 && ck.contains(w));
+                    });
+                } else if (v < hz) {  // cuckoo build failed: binary search of the non-hub part
+                    acc += sweep<uint32_t, false, U>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t) {
+                        const uint32_t r = w - hz;
+                        const bool b = ((lds32(bm + 4 * min(r >> 5, hwp - 1)) >> (r & 31)) & 1u) != 0u;
+                        return w >= hz ? b : sorted_contains(dst + vs, nh, w);
                     });
                 } else {
                     // suffix items exceed v >= hz: every valid item is a hub item
@@ -1627,8 +1659,8 @@ __global__ void __launch_bounds__(32 * kVlWarps)
         const uint32_t vs = __ldg(off + v), ve = __ldg(off + v + 1), d = ve - vs;
         if (d > kVNonHubCap) continue;  // long list: a CTA task (warp-uniform)
         Cuckoo32 ck{smem_addr(tab), 3 * d < kVlSlots ? 3 * d : kVlSlots, 0, 0};
-        for (uint32_t seed = 0;; ++seed) {
-            if (seed == 32) __trap();  // cannot happen at load <= 1/4; never miscount
+        bool tab_ok = false;
+        for (uint32_t seed = 0; seed < kCuckooSeeds && !tab_ok; ++seed) {
             ck.c1 = seed_mult(seed, 0);
             ck.c2 = seed_mult(seed, 1);
             for (uint32_t i = lane; i < ck.T; i += 32) tab[i] = kEmpty;
@@ -1637,7 +1669,7 @@ __global__ void __launch_bounds__(32 * kVlWarps)
             for (uint32_t i = lane; i < d; i += 32)
                 if (!cuckoo_insert32(tab, ck, __ldg(dst + vs + i))) fail = true;
             __syncwarp();
-            if (!__any_sync(TC_FULL_MASK, fail)) break;
+            tab_ok = !__any_sync(TC_FULL_MASK, fail);
         }
         const uint32_t p0 = __ldg(start + h) + task.y * kVChunk;
         // fill count, clamped to the slot range (an overflowed capacity layout is recounted)
@@ -1659,9 +1691,13 @@ __global__ void __launch_bounds__(32 * kVlWarps)
             s_cst[wp][lane] = cst;
             if (lane == 0) s_cst[wp][32] = tot;
             __syncwarp();
-            if (tot)
+            if (tot && tab_ok)
                 acc += sweep<uint32_t, false, 2>(dst, et, 32, 0, tot,
                                                 [&](uint32_t w, uint32_t) { return ck.contains(w); });
+            else if (tot)
+                acc += sweep<uint32_t, false, 2>(dst, et, 32, 0, tot, [&](uint32_t w, uint32_t) {
+                    return sorted_contains(dst + vs, d, w);
+                });
             __syncwarp();
         }
     }
