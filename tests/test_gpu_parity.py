@@ -350,3 +350,35 @@ def test_count_schedules_agree(env, golden, golden_big):
     for scale, counts in got.items():
         ref = want[int(scale)] or oracle.count(*oracle.preprocess(oracle.symmetrize(oracle.rmat_pairs(int(scale), 16, seed=0))))
         assert counts == [ref, ref, ref], (scale, counts, ref)
+
+
+def test_forced_vmajor_without_hubs():
+    """v-major forced on graphs without hubs (BA 10^7, RGG 2*10^7: the zone lies below the
+    hub zone, thousands of small warp tasks, cuckoo tables at load 1/3 -- RGG produced key
+    sets on which 32 cuckoo seeds failed, now a binary-search fallback): same counts as
+    the default schedule."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = r"""
+import json, sys
+sys.path.insert(0, ".")
+import paper_1503_00576_b200 as tcb
+from scripts.step import make
+out = {}
+for cfg in ("ba1e7", "rgg2e7"):
+    g = make(cfg)
+    out[cfg] = tcb.count_with_timings_device(g)[0]
+    g.free()
+print(json.dumps(out))
+"""
+    got = {}
+    for env in ({"TC_VMAJOR": "1"}, {"TC_VMAJOR": "0"}):
+        r = subprocess.run([sys.executable, "-c", script], cwd=root, capture_output=True, text=True,
+                           env={**os.environ, **env}, timeout=900)
+        assert r.returncode == 0, r.stderr[-2000:]
+        got[env["TC_VMAJOR"]] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert got["1"] == got["0"], got
+    assert got["0"]["ba1e7"] == 65054  # golden: reference count of barabasi_albert(10^7, 9, 0)
