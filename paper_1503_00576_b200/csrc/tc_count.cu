@@ -1635,41 +1635,55 @@ static void clear_l2_window(cudaStream_t s) {
 constexpr int kVlWarps = 8;
 constexpr uint32_t kVlSlots = 3 * kVNonHubCap;  // cuckoo load <= 1/3: 4 CTAs per SM
 
+// FB = false: the cuckoo path; a task whose table cannot be built is deferred (its index
+// appended to `defer`).  FB = true: the deferred tasks, probed by binary search of the sorted
+// adj(v) -- a separate instantiation so the hot kernel carries no fallback code.
+template <bool FB>
 __global__ void __launch_bounds__(32 * kVlWarps)
     k_count_vlow_warp(const uint32_t *__restrict__ dst, const uint32_t *__restrict__ off, uint32_t z0,
                       const uint32_t *__restrict__ start, const uint32_t *__restrict__ fillc,
                       const uint2 *__restrict__ in_e,
                       const uint2 *__restrict__ tasks, const uint32_t *__restrict__ ntasks,
-                      unsigned *__restrict__ next, unsigned long long *__restrict__ total) {
+                      unsigned *__restrict__ next, uint32_t *__restrict__ defer,
+                      unsigned *__restrict__ ndefer, unsigned long long *__restrict__ total) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t s_cb[kVlWarps][32], s_vs[kVlWarps][32], s_ve[kVlWarps][32];
     __shared__ uint32_t s_cst[kVlWarps][36];
     const unsigned lane = lane_id(), wp = threadIdx.x >> 5;
     uint32_t *tab = reinterpret_cast<uint32_t *>(smem) + wp * kVlSlots;
     const EdgeTable<uint32_t> et{s_cb[wp], s_vs[wp], s_ve[wp], s_cst[wp], nullptr};
-    const unsigned nt = *ntasks;
+    const unsigned nt = FB ? *ndefer : *ntasks;
     uint32_t acc = 0;
     for (;;) {
         unsigned t = 0;
         if (lane == 0) t = atomicAdd(next, 1u);
         t = __shfl_sync(TC_FULL_MASK, t, 0);
         if (t >= nt) break;
+        if (FB) t = defer[t];
         const uint2 task = tasks[t];
         const uint32_t h = task.x, v = z0 + h;
         const uint32_t vs = __ldg(off + v), ve = __ldg(off + v + 1), d = ve - vs;
         if (d > kVNonHubCap) continue;  // long list: a CTA task (warp-uniform)
         Cuckoo32 ck{smem_addr(tab), 3 * d < kVlSlots ? 3 * d : kVlSlots, 0, 0};
-        bool tab_ok = false;
-        for (uint32_t seed = 0; seed < kCuckooSeeds && !tab_ok; ++seed) {
-            ck.c1 = seed_mult(seed, 0);
-            ck.c2 = seed_mult(seed, 1);
-            for (uint32_t i = lane; i < ck.T; i += 32) tab[i] = kEmpty;
-            __syncwarp();
-            bool fail = false;
-            for (uint32_t i = lane; i < d; i += 32)
-                if (!cuckoo_insert32(tab, ck, __ldg(dst + vs + i))) fail = true;
-            __syncwarp();
-            tab_ok = !__any_sync(TC_FULL_MASK, fail);
+        if (!FB) {
+            bool deferred = false;
+            for (uint32_t seed = 0;; ++seed) {
+                if (__builtin_expect(seed == kCuckooSeeds, 0)) {  // warp-uniform, practically never
+                    if (lane == 0) defer[atomicAdd(ndefer, 1u)] = t;
+                    deferred = true;
+                    break;
+                }
+                ck.c1 = seed_mult(seed, 0);
+                ck.c2 = seed_mult(seed, 1);
+                for (uint32_t i = lane; i < ck.T; i += 32) tab[i] = kEmpty;
+                __syncwarp();
+                bool fail = false;
+                for (uint32_t i = lane; i < d; i += 32)
+                    if (!cuckoo_insert32(tab, ck, __ldg(dst + vs + i))) fail = true;
+                __syncwarp();
+                if (!__any_sync(TC_FULL_MASK, fail)) break;
+            }
+            if (deferred) continue;
         }
         const uint32_t p0 = __ldg(start + h) + task.y * kVChunk;
         // fill count, clamped to the slot range (an overflowed capacity layout is recounted)
@@ -1691,12 +1705,9 @@ __global__ void __launch_bounds__(32 * kVlWarps)
             s_cst[wp][lane] = cst;
             if (lane == 0) s_cst[wp][32] = tot;
             __syncwarp();
-            if (tot && tab_ok)
-                acc += sweep<uint32_t, false, 2>(dst, et, 32, 0, tot,
-                                                [&](uint32_t w, uint32_t) { return ck.contains(w); });
-            else if (tot)
+            if (tot)
                 acc += sweep<uint32_t, false, 2>(dst, et, 32, 0, tot, [&](uint32_t w, uint32_t) {
-                    return sorted_contains(dst + vs, d, w);
+                    return FB ? sorted_contains(dst + vs, d, w) : ck.contains(w);
                 });
             __syncwarp();
         }
@@ -1712,6 +1723,7 @@ struct VmajorState {
     uint32_t *cnt = nullptr, *start = nullptr, *tstart = nullptr;
     uint2 *in_e = nullptr;  // (edge, off[u+1]) per indexed in-edge
     uint2 *big = nullptr;   // CTA tasks of long-list heads below hz
+    uint32_t *defer = nullptr;  // warp tasks whose cuckoo build failed (binary-search rerun)
     bool capl = false;      // capacity layout used (overflow flag in next[2])
     unsigned *next = nullptr;
     uint2 *tasks = nullptr;
@@ -1733,11 +1745,13 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
     const uint64_t ie = capl ? (g.vin_total > span ? g.vin_total : span) : span;
     TC_CHECK(dalloc_t(&st->in_e, ie ? ie : 1, s));
     TC_CHECK(dalloc_t(&st->tasks, (size_t)nh + span / kVChunk + 1, s));
-    // [0], [1] task cursors, [2] capacity overflow flag, [3] big-task count, [4] zero, [5] big cursor
-    TC_CHECK(dalloc_t(&st->next, 6, s));
+    // [0], [1] task cursors, [2] capacity overflow flag, [3] big-task count, [4] zero,
+    // [5] big cursor, [6] deferred-task count, [7] deferred cursor
+    TC_CHECK(dalloc_t(&st->next, 8, s));
     TC_CHECK(dalloc_t(&st->big, (size_t)nh + span / kVChunk + 1, s));
+    TC_CHECK(dalloc_t(&st->defer, (size_t)nh + span / kVChunk + 1, s));
     TC_CUDA(cudaMemsetAsync(st->cnt, 0, (size_t)nh * sizeof(uint32_t), s));
-    TC_CUDA(cudaMemsetAsync(st->next, 0, 6 * sizeof(unsigned), s));
+    TC_CUDA(cudaMemsetAsync(st->next, 0, 8 * sizeof(unsigned), s));
     st->capl = capl;
     // everything below runs on s2 (the index build too, so that with s2 != s it overlaps
     // the u-major kernels on s)
@@ -1776,13 +1790,19 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
     if (per_sm < 1) per_sm = 1;
     if (hb) {
         const size_t wsm = (size_t)4 * kVlSlots * kVlWarps;
-        TC_CUDA(cudaFuncSetAttribute(k_count_vlow_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+        TC_CUDA(cudaFuncSetAttribute(k_count_vlow_warp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
         int wper = 1;
-        TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wper, k_count_vlow_warp, 32 * kVlWarps, wsm));
+        TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wper, k_count_vlow_warp<false>, 32 * kVlWarps, wsm));
         if (wper < 1) wper = 1;
-        k_count_vlow_warp<<<kSMs * wper, 32 * kVlWarps, wsm, s2>>>(g.dst, g.off32, z0, startp, st->cnt, st->in_e,
-                                                                 st->tasks, st->tstart + hb, st->next + 1,
-                                                                 d_total);
+        k_count_vlow_warp<false><<<kSMs * wper, 32 * kVlWarps, wsm, s2>>>(
+            g.dst, g.off32, z0, startp, st->cnt, st->in_e, st->tasks, st->tstart + hb, st->next + 1,
+            st->defer, st->next + 6, d_total);
+        TC_LAUNCHED();
+        // deferred tasks (cuckoo build failed; normally none): binary-search probes
+        TC_CUDA(cudaFuncSetAttribute(k_count_vlow_warp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+        k_count_vlow_warp<true><<<kSMs, 32 * kVlWarps, wsm, s2>>>(
+            g.dst, g.off32, z0, startp, st->cnt, st->in_e, st->tasks, st->tstart + hb, st->next + 7,
+            st->defer, st->next + 6, d_total);
         TC_LAUNCHED();
     }
     if (hb) {  // long-list heads below hz: CTA tasks with bitmap + non-hub cuckoo (load <= 1/4)
@@ -1830,6 +1850,7 @@ int vmajor_finish(VmajorState *st, cudaStream_t s, CountStats *stats, bool *over
     dfree(st->in_e, s);
     dfree(st->tasks, s);
     dfree(st->big, s);
+    dfree(st->defer, s);
     dfree(st->next, s);
     *st = VmajorState{};
     return 0;
