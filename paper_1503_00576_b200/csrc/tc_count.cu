@@ -1159,7 +1159,10 @@ __global__ void __launch_bounds__(32 * WARPS)
 //
 // Index: in-edges of each hub head, counting sort by v (only edges whose suffix and adj(v)
 // are both non-empty); tasks = (v, chunk of kVChunk in-edges) in v order.
-constexpr uint32_t kVChunk = 2048;
+#ifndef TC_VCHUNK
+#define TC_VCHUNK 2048
+#endif
+constexpr uint32_t kVChunk = TC_VCHUNK;
 
 // Both index passes evaluate the v-major predicate of every edge; each thread keeps
 // kVinPP edges in flight (all loads of a stage issued before any is used): the passes are
