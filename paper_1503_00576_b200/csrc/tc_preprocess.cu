@@ -985,7 +985,10 @@ __global__ void __launch_bounds__(256)
 }
 
 // 257..4096: CTA per list, shared-memory bitonic over the next power of two.
-__global__ void __launch_bounds__(256)
+#ifndef TC_SORT4K_NT
+#define TC_SORT4K_NT 256
+#endif
+__global__ void __launch_bounds__(TC_SORT4K_NT)
     k_seg_sort4k(const uint32_t *__restrict__ off32, const uint32_t *__restrict__ list,
                  const unsigned *__restrict__ count, uint32_t *__restrict__ dst, uint32_t hz,
                  uint32_t *__restrict__ hs) {
@@ -1131,7 +1134,7 @@ static int bucket_csr_dev(const uint64_t *keys, uint64_t m, uint64_t n, int vb, 
     TC_LAUNCHED();
     k_seg_sort_warp<32><<<kSMs * 8, 256, 0, s>>>(out->off32, w1k, counts + 4, out->dst, hz, hs);
     TC_LAUNCHED();
-    k_seg_sort4k<<<kSMs * 8, 256, 0, s>>>(out->off32, mid, counts + 1, out->dst, hz, hs);
+    k_seg_sort4k<<<kSMs * 8 * 256 / TC_SORT4K_NT, TC_SORT4K_NT, 0, s>>>(out->off32, mid, counts + 1, out->dst, hz, hs);
     TC_LAUNCHED();
     unsigned nbig = 0;
     TC_CUDA(cudaMemcpyAsync(&nbig, counts + 2, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
