@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define TC_ABI_VERSION 1
+#define TC_ABI_VERSION 2  /* 2: tc_times gained vmajor_ms */
 
 typedef struct tc_graph tc_graph; /* device-resident OrientedGraph */
 

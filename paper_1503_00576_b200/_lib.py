@@ -19,6 +19,9 @@ ALGO_MERGE_THREAD = 1
 PREPROCESS_RANK_SPACE = 1
 
 
+ABI_VERSION = 2  # include/tricount_b200.h TC_ABI_VERSION
+
+
 class TcTimes(ctypes.Structure):
     _fields_ = [
         ("h2d_ms", ctypes.c_double),
@@ -134,6 +137,9 @@ def load(init: bool = False):
                 fn = getattr(lib, name)
                 fn.argtypes = args
                 fn.restype = res
+            if lib.tc_abi_version() != ABI_VERSION:  # TcTimes layout and signatures below
+                raise ImportError(f"{LIB_PATH} has ABI {lib.tc_abi_version()}, this binding expects "
+                                  f"{ABI_VERSION}: rebuild with `python __graft_entry__.py build`")
             _lib = lib
         if init and not _initialised:
             dev = int(os.environ.get("LOCAL_RANK", "0")) if "TC_DEVICE" not in os.environ \

@@ -34,7 +34,7 @@ def test_library_exports_every_declared_symbol():
     for name in _declared():
         assert hasattr(L, name), name
         assert name in _lib.EXPORTED, f"{name} has no ctypes signature"
-    assert L.tc_abi_version() == 1
+    assert L.tc_abi_version() == 2
 
 
 def test_library_is_sm100a_only():
