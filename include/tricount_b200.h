@@ -10,6 +10,11 @@
  * borrowed for the duration of the call; device graphs are owned by the library until
  * tc_graph_free().  Every call is synchronous with respect to its results.
  *
+ * Threading: every entry point may be called from any thread, concurrently on different
+ * graphs (reference SPEC.md:294).  Calls that touch the device are serialised by one
+ * library lock (each already saturates the GPU) and every count accumulates into its own
+ * device counter.
+ *
  * Arrays: pairs are uint32 (u, v) pairs, row-major [npairs][2] (reference EdgeArray.edges,
  * graph.py:101-129); an oriented graph is edge_src u32[m], edge_dst u32[m],
  * node_offsets i64[n+1] (reference OrientedGraph, graph.py:146-193).
@@ -23,7 +28,7 @@
 extern "C" {
 #endif
 
-#define TC_ABI_VERSION 2  /* 2: tc_times gained vmajor_ms */
+#define TC_ABI_VERSION 3  /* 2: tc_times gained vmajor_ms; 3: tc_set_option, thread-safe calls */
 
 typedef struct tc_graph tc_graph; /* device-resident OrientedGraph */
 
@@ -183,6 +188,17 @@ int tc_launch_count(uint64_t *out);
 /* keep >= bytes reserved in the library's device memory pool (called automatically by
  * tc_preprocess* / tc_count_with_timings with an estimate of their scratch) */
 int tc_reserve(uint64_t bytes);
+
+/* Schedule options (no reference counterpart; the reference's numba kernel has none).  The
+ * defaults are the measured-best schedule and are what every product call runs; the count is
+ * exact under every setting.  Only the schedule-coverage tests and the development probes set
+ * them -- the library never reads the environment.  Names: vmajor, vzone_log2, vlow_all,
+ * vm_bias, dense_factor, hub_unroll, l2_persist_mb, l2_target, concurrent, share, midwarp,
+ * light, skew, light_vec, shard_model, shard_ovh, shard_ucap, dense_ranks, bucket,
+ * count_stats (see csrc/tc_internal.h Options).  Unknown names return -1. */
+int tc_set_option(const char *name, int64_t value);
+int tc_get_option(const char *name, int64_t *value);
+int tc_reset_options(void);
 
 #ifdef __cplusplus
 }

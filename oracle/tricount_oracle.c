@@ -551,3 +551,223 @@ int or_rgg_fill(const double *xs, const double *ys, uint64_t n, double r,
     free(c.ids);
     return bad ? -1 : 0;
 }
+
+/* ------------------------------------------------------ rmat, whole loop ---- */
+/*
+ * generators.py:241-284 in one call (the numpy version of the dedupe loop needs ~100 GB
+ * and tens of minutes at scale 26; this one sorts in parallel).  Per round, exactly as the
+ * reference: batch = max(4096, int(need * 1.3)) draws per level; keep src != dst; keys =
+ * (min << 32) | max in draw order; order-preserving de-dup (first occurrence wins); drop
+ * keys already in `have`; the first `need` survivors in draw order join `have`.  Because
+ * `have` is re-sorted every round, the survivors are collected in key order from a STABLE
+ * key sort of (key, draw position): the first element of each equal-key run is the first
+ * occurrence, and "the first `need` survivors in draw order" = the survivors whose draw
+ * position is <= the position of the need-th survivor.
+ * Writes the sorted canonical keys to have (target entries).  Returns 0, -1 (allocation)
+ * or -2 (sampling saturated: 25 rounds without a new edge, generators.py:268-274).
+ */
+static void radix_sort_kv(uint64_t *k, uint64_t *kt, uint32_t *v, uint32_t *vt, uint64_t n,
+                          int key_bits, int nthr, uint64_t **ko, uint32_t **vo) {
+    size_t *hist = (size_t *)calloc((size_t)nthr * 256, sizeof(size_t));
+    uint64_t *sk = k, *dk = kt;
+    uint32_t *sv = v, *dv = vt;
+    int passes = (key_bits + 7) / 8;
+    for (int p = 0; p < passes; ++p) {
+        int shift = 8 * p;
+        memset(hist, 0, (size_t)nthr * 256 * sizeof(size_t));
+#pragma omp parallel num_threads(nthr)
+        {
+            int t = omp_get_thread_num();
+            uint64_t lo = n * (uint64_t)t / nthr, hi = n * (uint64_t)(t + 1) / nthr;
+            size_t *h = hist + (size_t)t * 256;
+            for (uint64_t i = lo; i < hi; ++i) h[(sk[i] >> shift) & 255]++;
+#pragma omp barrier
+#pragma omp single
+            {
+                size_t run = 0;
+                for (int d = 0; d < 256; ++d)
+                    for (int tt = 0; tt < nthr; ++tt) {
+                        size_t c = hist[(size_t)tt * 256 + d];
+                        hist[(size_t)tt * 256 + d] = run;
+                        run += c;
+                    }
+            }
+            for (uint64_t i = lo; i < hi; ++i) {
+                size_t o = h[(sk[i] >> shift) & 255]++;
+                dk[o] = sk[i];
+                dv[o] = sv[i];
+            }
+        }
+        uint64_t *a = sk; sk = dk; dk = a;
+        uint32_t *b = sv; sv = dv; dv = b;
+    }
+    free(hist);
+    *ko = sk;
+    *vo = sv;
+}
+
+int or_rmat_canonical(int scale, uint64_t target, double a, double t_ab, double t_abc,
+                      uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                      uint64_t *have, int threads) {
+    const int nthr = clamp_threads(threads);
+    const u128 s0 = ((u128)state_hi << 64) | state_lo, inc = ((u128)inc_hi << 64) | inc_lo;
+    uint64_t have_n = 0, drawn = 0;
+    int stalled = 0;
+    uint64_t *cnt = (uint64_t *)calloc((size_t)nthr + 1, sizeof(uint64_t));
+    if (!cnt) return -1;
+    while (have_n < target) {
+        const uint64_t need = target - have_n;
+        uint64_t batch = (uint64_t)((double)need * 1.3);
+        if (batch < 4096) batch = 4096;
+        uint32_t *sd = (uint32_t *)malloc(batch * 2 * sizeof(uint32_t));
+        uint64_t *keys = (uint64_t *)malloc(batch * sizeof(uint64_t));
+        uint32_t *pos = (uint32_t *)malloc(batch * sizeof(uint32_t));
+        if (!sd || !keys || !pos) { free(sd); free(keys); free(pos); free(cnt); return -1; }
+        /* level loop (generators.py:249-256): level l of item j is draw drawn + l*batch + j */
+#pragma omp parallel num_threads(nthr)
+        {
+            int t = omp_get_thread_num();
+            uint64_t lo = batch * (uint64_t)t / nthr, hi = batch * (uint64_t)(t + 1) / nthr;
+            for (uint64_t j = lo; j < hi; ++j) sd[2 * j] = sd[2 * j + 1] = 0;
+            for (int l = 0; l < scale; ++l) {
+                u128 s = pcg_advance(s0, inc, drawn + (uint64_t)l * batch + lo);
+                for (uint64_t j = lo; j < hi; ++j) {
+                    s = s * PCG_MULT + inc;
+                    double r = (double)(pcg_output(s) >> 11) * (1.0 / 9007199254740992.0);
+                    uint32_t sb = r >= t_ab;
+                    uint32_t db = (r >= a && r < t_ab) || r >= t_abc;
+                    sd[2 * j] = (sd[2 * j] << 1) | sb;
+                    sd[2 * j + 1] = (sd[2 * j + 1] << 1) | db;
+                }
+            }
+            /* keep = src != dst, order-preserving (per-thread count + prefix) */
+            uint64_t c = 0;
+            for (uint64_t j = lo; j < hi; ++j) c += sd[2 * j] != sd[2 * j + 1];
+            cnt[t + 1] = c;
+#pragma omp barrier
+#pragma omp single
+            {
+                cnt[0] = 0;
+                for (int q = 0; q < nthr; ++q) cnt[q + 1] += cnt[q];
+            }
+            uint64_t o = cnt[t];
+            for (uint64_t j = lo; j < hi; ++j) {
+                uint32_t x = sd[2 * j], y = sd[2 * j + 1];
+                if (x == y) continue;
+                uint32_t mn = x < y ? x : y, mx = x < y ? y : x;
+                keys[o] = ((uint64_t)mn << 32) | mx;
+                pos[o] = (uint32_t)o;
+                ++o;
+            }
+        }
+        drawn += batch * (uint64_t)scale;
+        const uint64_t nk = cnt[nthr];
+        /* reuse sd as the ping-pong buffers: it holds 8*batch bytes = keys' size; pos needs
+         * its own (4*batch) */
+        uint64_t *kt = (uint64_t *)sd;
+        uint32_t *pt = (uint32_t *)malloc((nk ? nk : 1) * sizeof(uint32_t));
+        if (!pt) { free(sd); free(keys); free(pos); free(cnt); return -1; }
+        uint64_t *sk;
+        uint32_t *sp;
+        /* key bits: min/max ids < 2^scale in the two 32-bit halves */
+        radix_sort_kv(keys, kt, pos, pt, nk, 32 + scale, nthr, &sk, &sp);
+        /* survivors: first of an equal-key run and absent from `have` (merge join) */
+        uint8_t *flag = (uint8_t *)calloc(nk ? nk : 1, 1);
+        if (!flag) { free(sd); free(keys); free(pos); free(pt); free(cnt); return -1; }
+#pragma omp parallel num_threads(nthr)
+        {
+            int t = omp_get_thread_num();
+            uint64_t lo = nk * (uint64_t)t / nthr, hi = nk * (uint64_t)(t + 1) / nthr;
+            if (lo < hi) {
+                /* first have entry >= sk[lo] */
+                uint64_t L = 0, R = have_n;
+                while (L < R) {
+                    uint64_t mid = (L + R) / 2;
+                    if (have[mid] < sk[lo]) L = mid + 1; else R = mid;
+                }
+                uint64_t h = L;
+                for (uint64_t i = lo; i < hi; ++i) {
+                    if (i > 0 && sk[i - 1] == sk[i]) continue;  /* not the first occurrence */
+                    while (h < have_n && have[h] < sk[i]) ++h;
+                    if (h < have_n && have[h] == sk[i]) continue;
+                    flag[sp[i]] = 1;
+                }
+            }
+        }
+        /* draw position of the need-th survivor (or keep all) */
+        uint64_t cut = nk;  /* positions < cut are taken */
+        {
+            uint64_t *sc = (uint64_t *)calloc((size_t)nthr + 1, sizeof(uint64_t));
+#pragma omp parallel num_threads(nthr)
+            {
+                int t = omp_get_thread_num();
+                uint64_t lo = nk * (uint64_t)t / nthr, hi = nk * (uint64_t)(t + 1) / nthr, c = 0;
+                for (uint64_t i = lo; i < hi; ++i) c += flag[i];
+                sc[t + 1] = c;
+            }
+            uint64_t run = 0;
+            for (int q = 0; q < nthr && cut == nk; ++q) {
+                uint64_t lo = nk * (uint64_t)q / nthr, hi = nk * (uint64_t)(q + 1) / nthr;
+                if (run + sc[q + 1] >= need) {
+                    for (uint64_t i = lo; i < hi; ++i)
+                        if (flag[i] && ++run == need) { cut = i + 1; break; }
+                } else {
+                    run += sc[q + 1];
+                }
+            }
+            free(sc);
+        }
+        /* the taken survivors in key order: compact sk (in place; sequential, ~1 ns each) */
+        uint64_t nnew = 0;
+        for (uint64_t i = 0; i < nk; ++i)
+            if (sp[i] < cut && flag[sp[i]]) sk[nnew++] = sk[i];
+        free(flag);
+        if (nnew == 0) {
+            if (++stalled >= 25) { free(sd); free(keys); free(pos); free(pt); free(cnt); return -2; }
+        } else {
+            stalled = 0;
+            /* have = sort(have ∪ new): backward merge in place */
+            uint64_t i = have_n, j = nnew, o = have_n + nnew;
+            while (j > 0) {
+                if (i > 0 && have[i - 1] > sk[j - 1]) have[--o] = have[--i];
+                else have[--o] = sk[--j];
+            }
+            have_n += nnew;
+        }
+        free(sd);
+        free(keys);
+        free(pos);
+        free(pt);
+    }
+    free(cnt);
+    return 0;
+}
+
+/* graph.py:265-276 edge_array_from_undirected on sorted canonical keys (lo < hi): both
+ * directions, lexicographically sorted, as u32 pairs [2k][2]. */
+int or_symmetrize_canonical(const uint64_t *keys, uint64_t k, uint32_t *pairs, int threads) {
+    const int nthr = clamp_threads(threads);
+    uint64_t *rev = (uint64_t *)malloc((k ? k : 1) * sizeof(uint64_t));
+    uint64_t *tmp = (uint64_t *)malloc((k ? k : 1) * sizeof(uint64_t));
+    if (!rev || !tmp) { free(rev); free(tmp); return -1; }
+    uint64_t mx = 0;
+#pragma omp parallel for num_threads(nthr) reduction(max : mx)
+    for (uint64_t i = 0; i < k; ++i) {
+        rev[i] = (keys[i] << 32) | (keys[i] >> 32);
+        if ((keys[i] & 0xffffffffu) > mx) mx = keys[i] & 0xffffffffu;
+    }
+    radix_sort_u64(rev, tmp, k, 32 + bits_for(mx), nthr);
+    free(tmp);
+    /* merge the two sorted lists (keys are distinct across them: lo<hi vs hi>lo) */
+    uint64_t i = 0, j = 0, o = 0;
+    while (i < k || j < k) {
+        uint64_t x;
+        if (j >= k || (i < k && keys[i] < rev[j])) x = keys[i++];
+        else x = rev[j++];
+        pairs[2 * o] = (uint32_t)(x >> 32);
+        pairs[2 * o + 1] = (uint32_t)x;
+        ++o;
+    }
+    free(rev);
+    return 0;
+}

@@ -19,7 +19,7 @@ ALGO_MERGE_THREAD = 1
 PREPROCESS_RANK_SPACE = 1
 
 
-ABI_VERSION = 2  # include/tricount_b200.h TC_ABI_VERSION
+ABI_VERSION = 3  # include/tricount_b200.h TC_ABI_VERSION
 
 
 class TcTimes(ctypes.Structure):
@@ -114,6 +114,9 @@ _SIGS = {
     "tc_timer_elapsed": ([ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "tc_launch_count": ([_u64p], ctypes.c_int),
     "tc_reserve": ([ctypes.c_uint64], ctypes.c_int),
+    "tc_set_option": ([ctypes.c_char_p, ctypes.c_int64], ctypes.c_int),
+    "tc_get_option": ([ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+    "tc_reset_options": ([], ctypes.c_int),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -168,6 +171,36 @@ def _check(rc: int) -> None:
 
 def check(rc: int) -> None:
     _check(rc)
+
+
+def set_option(name: str, value: int) -> None:
+    """Schedule option (include/tricount_b200.h tc_set_option); tests and probes only."""
+    _check(lib().tc_set_option(name.encode(), int(value)))
+
+
+def get_option(name: str) -> int:
+    v = ctypes.c_int64()
+    _check(lib().tc_get_option(name.encode(), ctypes.byref(v)))
+    return v.value
+
+
+def reset_options() -> None:
+    _check(lib().tc_reset_options())
+
+
+class options:
+    """Context manager: `with options(vmajor=1, light=2): ...` (restores the defaults)."""
+
+    def __init__(self, **kv):
+        self.kv = kv
+
+    def __enter__(self):
+        for k, v in self.kv.items():
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        reset_options()
 
 
 def ptr(arr: np.ndarray) -> ctypes.c_void_p:

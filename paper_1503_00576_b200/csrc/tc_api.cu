@@ -14,6 +14,7 @@
 struct tc_graph {
     tc::DeviceGraph g;
     tc::DeviceGraph *rank = nullptr;  // cached rank-space copy (full-range counts)
+    bool no_rank = false;             // not rank-orientable: full counts use the original ids
 };
 
 namespace tc {
@@ -21,14 +22,25 @@ namespace tc {
 namespace {
 thread_local std::string g_err;
 std::mutex g_mu;
+// Every entry point that touches device state holds this for the whole call: the reference's
+// count is a pure function safe to call concurrently on different graphs (SPEC.md:294,
+// private per-call accumulators at count.py:68).  Calls share one stream and one scratch pool
+// and each count saturates the GPU, so serialising them costs no throughput; each count also
+// accumulates into its own device counter, and the lazy rank-space copy of a graph is built
+// under the lock.  Recursive: entry points may call each other.
+std::recursive_mutex g_call;
+Options g_opts;
 bool g_ready = false;
 int g_device = 0;
 cudaStream_t g_stream = nullptr;
 cudaMemPool_t g_scratch = nullptr;
 void *g_flush = nullptr;
 size_t g_flush_bytes = 0;
-unsigned long long *g_total = nullptr;  // device u64 accumulator for counts
 }  // namespace
+
+#define TC_API_GUARD() std::lock_guard<std::recursive_mutex> _tc_call_lock(::tc::g_call)
+
+Options &opts() { return g_opts; }
 
 std::atomic<unsigned long long> g_launches{0};
 cudaEvent_t g_timer[8] = {nullptr};
@@ -72,7 +84,6 @@ static int ensure_init(int device) {
     props.location.id = device;
     TC_CUDA(cudaMemPoolCreate(&g_scratch, &props));
     TC_CUDA(cudaMemPoolSetAttribute(g_scratch, cudaMemPoolAttrReleaseThreshold, &keep));
-    TC_CUDA(cudaMalloc(&g_total, sizeof(unsigned long long)));
     g_device = device;
     g_ready = true;
     return 0;
@@ -130,10 +141,13 @@ struct Events {
 };
 
 // Full-range counts of an original-id graph run on its (cached) rank-space copy; ranged
-// counts of it run the original-id kernels over exactly that edge range.
+// counts of it run the original-id kernels over exactly that edge range.  A graph whose
+// edges do not all point to a higher (out + in degree, id) rank -- hand-built, or the
+// preprocess of a non-symmetric edge array -- keeps the original-id kernels for every count.
+// Called under the API lock (the copy is created once per graph).
 static int rank_copy(tc_graph *h, const DeviceGraph **out) {
     *out = &h->g;
-    if (h->g.rank_space || h->g.m >= (1ull << 32)) return 0;
+    if (h->g.rank_space || h->no_rank || h->g.m >= (1ull << 32)) return 0;
     if (!h->rank) {
         DeviceGraph *r = new DeviceGraph();
         r->persistent = true;
@@ -141,7 +155,9 @@ static int rank_copy(tc_graph *h, const DeviceGraph **out) {
         if (rc) {
             graph_release(r, g_stream);
             delete r;
-            return rc;
+            if (rc != kNotRankOrientable) return rc;
+            h->no_rank = true;
+            return 0;
         }
         h->rank = r;
     }
@@ -149,29 +165,41 @@ static int rank_copy(tc_graph *h, const DeviceGraph **out) {
     return 0;
 }
 
-static int count_ranges(const DeviceGraph &g, const int64_t *bounds, int npools, int algo,
-                        uint64_t *out, tc_times *t) {
+// Counts `bounds` ranges of a graph into a private device counter.  With `h` set, the
+// full-range count runs on h's rank-space copy, built (once) inside the timed region.
+static int count_ranges(const DeviceGraph &g0, tc_graph *h, const int64_t *bounds, int npools,
+                        int algo, uint64_t *out, tc_times *t) {
     cudaStream_t s = g_stream;
     Events ev;
     TC_CHECK(ev.create());
     TC_CUDA(cudaEventRecord(ev.e[0], s));
-    TC_CUDA(cudaMemsetAsync(g_total, 0, sizeof(unsigned long long), s));
+    const DeviceGraph *gp = &g0;
+    if (h) TC_CHECK(rank_copy(h, &gp));
+    const DeviceGraph &g = *gp;
+    unsigned long long *total = nullptr;  // this call's accumulator
+    TC_CHECK(dalloc_t(&total, 1, s));
+    TC_CUDA(cudaMemsetAsync(total, 0, sizeof(unsigned long long), s));
     CountStats agg, st;
     for (int p = 0; p < npools; ++p) {
         st = CountStats();
-        TC_CHECK(count_range_dev(g, (uint64_t)bounds[p], (uint64_t)bounds[p + 1], algo, g_total, s,
-                                 t ? &st : nullptr));
+        const int rc = count_range_dev(g, (uint64_t)bounds[p], (uint64_t)bounds[p + 1], algo, total, s,
+                                       t ? &st : nullptr);
+        if (rc) {
+            dfree(total, s);
+            return rc;
+        }
         agg.classify_ms += st.classify_ms;
         agg.heavy_ms += st.heavy_ms;
         agg.light_ms += st.light_ms;
         agg.vmajor_ms += st.vmajor_ms;
         agg.heavy_tasks += st.heavy_tasks;
     }
-    unsigned long long h = 0;
-    TC_CUDA(cudaMemcpyAsync(&h, g_total, sizeof(h), cudaMemcpyDeviceToHost, s));
+    unsigned long long hv = 0;
+    TC_CUDA(cudaMemcpyAsync(&hv, total, sizeof(hv), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaEventRecord(ev.e[1], s));
+    dfree(total, s);
     TC_CUDA(cudaEventSynchronize(ev.e[1]));
-    *out = h;
+    *out = hv;
     if (t) {
         memset(t, 0, sizeof(*t));
         t->count_ms = ms_between(ev.e[0], ev.e[1]);
@@ -183,6 +211,14 @@ static int count_ranges(const DeviceGraph &g, const int64_t *bounds, int npools,
         t->heavy_tasks = agg.heavy_tasks;
     }
     return 0;
+}
+
+__global__ void k_check_ids(const uint32_t *__restrict__ ids, uint64_t k, uint32_t n,
+                            uint32_t *__restrict__ bad) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    bool ok = true;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride) ok &= ids[i] < n;
+    if (!ok) atomicOr(bad, 1u);
 }
 
 static int check_graph(const tc_graph *g) {
@@ -203,6 +239,7 @@ int tc_abi_version(void) { return TC_ABI_VERSION; }
 const char *tc_last_error(void) { return tc::last_error(); }
 
 int tc_init(int device) {
+    TC_API_GUARD();
     TC_CHECK(ensure_init(device));
     // touch the pool and the kernels' module so the first timed call pays nothing
     void *p = nullptr;
@@ -213,13 +250,12 @@ int tc_init(int device) {
 }
 
 int tc_shutdown(void) {
+    TC_API_GUARD();
     std::lock_guard<std::mutex> lk(g_mu);
     if (!g_ready) return 0;
     if (g_flush) cudaFree(g_flush);
     g_flush = nullptr;
     g_flush_bytes = 0;
-    cudaFree(g_total);
-    g_total = nullptr;
     if (g_scratch) cudaMemPoolDestroy(g_scratch);
     g_scratch = nullptr;
     cudaStreamDestroy(g_stream);
@@ -235,6 +271,7 @@ int tc_preprocess(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, int p
 
 int tc_preprocess_ex(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, int pairs_on_device,
                      int flags, tc_graph **out, tc_times *t) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     TC_CHECK(reserve_pool(scratch_estimate(npairs)));
     if (!out) {
@@ -277,54 +314,88 @@ int tc_preprocess_ex(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, in
 
 int tc_graph_upload(const uint32_t *edge_src, const uint32_t *edge_dst,
                     const int64_t *node_offsets, uint64_t m, uint64_t n, tc_graph **out) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     cudaStream_t s = g_stream;
     if (n >= (1ull << 32)) {
         set_error("num_vertices must be < 2^32 on the device path");
         return -1;
     }
+    // The count kernels index with these offsets: check them (O(n), host) before anything
+    // reaches the device -- off[0] = 0, off[n] = m, nondecreasing.
+    if (!node_offsets || node_offsets[0] != 0 || (uint64_t)node_offsets[n] != m) {
+        set_error("node_offsets must start at 0 and end at m");
+        return -1;
+    }
+    uint64_t maxo = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        if (node_offsets[i + 1] < node_offsets[i]) {
+            set_error("node_offsets must be nondecreasing");
+            return -1;
+        }
+        const uint64_t d = (uint64_t)(node_offsets[i + 1] - node_offsets[i]);
+        if (d > maxo) maxo = d;
+    }
     tc_graph *g = new tc_graph();
     g->g.persistent = true;
     int rc = graph_alloc(&g->g, m, n, s);
-    if (rc) {
-        delete g;
-        return rc;
-    }
-    if (m) {
-        TC_CUDA(cudaMemcpyAsync(g->g.src, edge_src, m * 4, cudaMemcpyHostToDevice, s));
-        TC_CUDA(cudaMemcpyAsync(g->g.dst, edge_dst, m * 4, cudaMemcpyHostToDevice, s));
-    }
-    TC_CUDA(cudaMemsetAsync(g->g.dst + m, 0, 16, s));
-    TC_CUDA(cudaMemcpyAsync(g->g.off, node_offsets, (n + 1) * 8, cudaMemcpyHostToDevice, s));
-    uint32_t maxo = 0;
-    uint32_t *dmax = nullptr;
-    TC_CHECK(dalloc_t(&dmax, 1, s));
-    // rebuild off32 / max from the uploaded offsets (off32 via node array of src would
-    // assume a valid grouping; copy-convert instead)
-    if (g->g.off32) {
-        int64_t *h = (int64_t *)node_offsets;
-        uint32_t *tmp = (uint32_t *)malloc((n + 1) * 4);
+    uint32_t *tmp = nullptr;
+    if (!rc && g->g.off32) {
+        tmp = (uint32_t *)malloc((n + 1) * 4);
         if (!tmp) {
             set_error("host allocation failed");
-            return -3;
+            rc = -3;
         }
-        for (uint64_t i = 0; i <= n; ++i) tmp[i] = (uint32_t)h[i];
-        TC_CUDA(cudaMemcpyAsync(g->g.off32, tmp, (n + 1) * 4, cudaMemcpyHostToDevice, s));
-        TC_CUDA(cudaStreamSynchronize(s));
+    }
+    auto fail = [&](int code) {
         free(tmp);
+        graph_release(&g->g, s);
+        delete g;
+        return code;
+    };
+    if (rc) return fail(rc);
+    cudaError_t e = cudaSuccess;
+    if (m) {
+        if (e == cudaSuccess) e = cudaMemcpyAsync(g->g.src, edge_src, m * 4, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(g->g.dst, edge_dst, m * 4, cudaMemcpyHostToDevice, s);
     }
-    for (uint64_t i = 0; i < n; ++i) {
-        uint64_t d = (uint64_t)(node_offsets[i + 1] - node_offsets[i]);
-        if (d > maxo) maxo = (uint32_t)d;
+    if (e == cudaSuccess) e = cudaMemsetAsync(g->g.dst + m, 0, 16, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g->g.off, node_offsets, (n + 1) * 8, cudaMemcpyHostToDevice, s);
+    if (tmp) {  // off32: the u32 copy the count kernels read (m < 2^32)
+        for (uint64_t i = 0; i <= n; ++i) tmp[i] = (uint32_t)node_offsets[i];
+        if (e == cudaSuccess) e = cudaMemcpyAsync(g->g.off32, tmp, (n + 1) * 4, cudaMemcpyHostToDevice, s);
     }
-    dfree(dmax, s);
-    g->g.max_out = maxo;
-    TC_CUDA(cudaStreamSynchronize(s));
+    // every edge_dst must be a vertex (the kernels read off[v] for v = edge_dst[e])
+    uint32_t bad = 0;
+    if (e == cudaSuccess && m) {
+        uint32_t *dbad = nullptr;
+        if (dalloc_t(&dbad, 1, s)) return fail(-3);
+        e = cudaMemsetAsync(dbad, 0, sizeof(uint32_t), s);
+        if (e == cudaSuccess) {
+            k_check_ids<<<grid_for(m, 256, kSMs * 8), 256, 0, s>>>(g->g.dst, m, (uint32_t)n, dbad);
+            note_launch();
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&bad, dbad, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+        dfree(dbad, s);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        set_error(std::string("graph upload: ") + cudaGetErrorString(e));
+        return fail(-2);
+    }
+    if (bad) {
+        set_error("edge_dst holds a vertex id >= num_vertices");
+        return fail(-1);
+    }
+    free(tmp);
+    g->g.max_out = (uint32_t)maxo;
     *out = g;
     return 0;
 }
 
 int tc_graph_create(uint64_t m, uint64_t n, int flags, tc_graph **out) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     if (n >= (1ull << 32)) {
         set_error("num_vertices must be < 2^32 on the device path");
@@ -344,6 +415,7 @@ int tc_graph_create(uint64_t m, uint64_t n, int flags, tc_graph **out) {
 }
 
 int tc_graph_finalize(tc_graph *g) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     TC_CHECK(check_graph(g));
     return finalize_graph_dev(&g->g, g_stream);
@@ -351,6 +423,7 @@ int tc_graph_finalize(tc_graph *g) {
 
 int tc_graph_download(const tc_graph *g, uint32_t *edge_src, uint32_t *edge_dst,
                       int64_t *node_offsets) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     TC_CHECK(check_graph(g));
     cudaStream_t s = g_stream;
@@ -388,6 +461,7 @@ int tc_graph_device_ptrs(const tc_graph *g, uint32_t **edge_src, uint32_t **edge
 }
 
 int tc_graph_free(tc_graph *g) {
+    TC_API_GUARD();
     if (!g) return 0;
     if (g_ready) {
         cudaSetDevice(g_device);
@@ -400,6 +474,7 @@ int tc_graph_free(tc_graph *g) {
 }
 
 int tc_count(const tc_graph *g, int64_t lo, int64_t hi, int algo, uint64_t *out, tc_times *t) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     TC_CHECK(check_graph(g));
     if (lo < 0 || hi < lo || (uint64_t)hi > g->g.m) {
@@ -407,16 +482,13 @@ int tc_count(const tc_graph *g, int64_t lo, int64_t hi, int algo, uint64_t *out,
         return -1;
     }
     int64_t b[2] = {lo, hi};
-    if (algo == TC_ALGO_AUTO && lo == 0 && (uint64_t)hi == g->g.m) {
-        const DeviceGraph *r = nullptr;
-        TC_CHECK(rank_copy(const_cast<tc_graph *>(g), &r));
-        return count_ranges(*r, b, 1, algo, out, t);
-    }
-    return count_ranges(g->g, b, 1, algo, out, t);
+    const bool full = algo == TC_ALGO_AUTO && lo == 0 && (uint64_t)hi == g->g.m;
+    return count_ranges(g->g, full ? const_cast<tc_graph *>(g) : nullptr, b, 1, algo, out, t);
 }
 
 int tc_count_partitioned(const tc_graph *g, const int64_t *bounds, int npools, int algo,
                          uint64_t *out, tc_times *t) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     TC_CHECK(check_graph(g));
     if (npools < 1 || bounds[0] != 0 || (uint64_t)bounds[npools] != g->g.m) {
@@ -432,15 +504,14 @@ int tc_count_partitioned(const tc_graph *g, const int64_t *bounds, int npools, i
     // full count (count.py:181-204 returns only that sum).  On one GPU the pools are
     // counted as one pass; per-pool ranges remain available through tc_count.
     if (algo == TC_ALGO_AUTO) {
-        const DeviceGraph *r = nullptr;
-        TC_CHECK(rank_copy(const_cast<tc_graph *>(g), &r));
         int64_t b[2] = {0, (int64_t)g->g.m};
-        return count_ranges(*r, b, 1, algo, out, t);
+        return count_ranges(g->g, const_cast<tc_graph *>(g), b, 1, algo, out, t);
     }
-    return count_ranges(g->g, bounds, npools, algo, out, t);
+    return count_ranges(g->g, nullptr, bounds, npools, algo, out, t);
 }
 
 int tc_intersect_count(const tc_graph *g, uint32_t u, uint32_t v, uint64_t *out) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     TC_CHECK(check_graph(g));
     if ((uint64_t)u >= g->g.n || (uint64_t)v >= g->g.n) {
@@ -452,6 +523,7 @@ int tc_intersect_count(const tc_graph *g, uint32_t u, uint32_t v, uint64_t *out)
 
 int tc_count_with_timings(const uint32_t *pairs, uint64_t npairs, uint64_t nverts,
                           int pairs_on_device, int algo, uint64_t *out, tc_times *t) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     TC_CHECK(reserve_pool(scratch_estimate(npairs)));
     cudaStream_t s = g_stream;
@@ -476,18 +548,23 @@ int tc_count_with_timings(const uint32_t *pairs, uint64_t npairs, uint64_t nvert
         return rc;
     }
     TC_CUDA(cudaEventRecord(ev.e[2], s));
-    TC_CUDA(cudaMemsetAsync(g_total, 0, sizeof(unsigned long long), s));
+    unsigned long long *total = nullptr;  // this call's accumulator
+    rc = dalloc_t(&total, 1, s);
+    if (!rc) rc = cudaMemsetAsync(total, 0, sizeof(unsigned long long), s) == cudaSuccess ? 0 : -2;
     CountStats st;
-    static const bool want_stats = getenv("TC_COUNT_STATS") && atoi(getenv("TC_COUNT_STATS"));
-    rc = count_range_dev(g, 0, g.m, algo, g_total, s, want_stats ? &st : nullptr);
+    const bool want_stats = opts().count_stats != 0;
+    if (!rc) rc = count_range_dev(g, 0, g.m, algo, total, s, want_stats ? &st : nullptr);
     if (rc) {
+        if (rc == -2 && !*last_error()) set_error("cudaMemsetAsync failed");
+        dfree(total, s);
         if (owned) dfree(owned, s);
         graph_release(&g, s);
         return rc;
     }
     unsigned long long h = 0;
-    TC_CUDA(cudaMemcpyAsync(&h, g_total, sizeof(h), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaMemcpyAsync(&h, total, sizeof(h), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaEventRecord(ev.e[3], s));
+    dfree(total, s);
     graph_release(&g, s);
     if (owned) dfree(owned, s);
     TC_CUDA(cudaEventSynchronize(ev.e[3]));
@@ -510,6 +587,7 @@ int tc_count_with_timings(const uint32_t *pairs, uint64_t npairs, uint64_t nvert
 }
 
 int tc_work_bounds(const tc_graph *g, int npools, int64_t *bounds) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     TC_CHECK(check_graph(g));
     if (npools < 1) {
@@ -520,12 +598,14 @@ int tc_work_bounds(const tc_graph *g, int npools, int64_t *bounds) {
 }
 
 int tc_merge_work(const tc_graph *g, uint64_t *out) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     TC_CHECK(check_graph(g));
     return merge_work_dev(g->g, out, g_stream);
 }
 
 int tc_sort_edges(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, uint32_t *out_pairs) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     if (npairs == 0) return 0;
     cudaStream_t s = g_stream;
@@ -542,6 +622,7 @@ int tc_sort_edges(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, uint3
 }
 
 int tc_build_node_array(const uint32_t *firsts, uint64_t k, uint64_t n, int64_t *offsets) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     cudaStream_t s = g_stream;
     uint32_t *df = nullptr;
@@ -559,6 +640,7 @@ int tc_build_node_array(const uint32_t *firsts, uint64_t k, uint64_t n, int64_t 
 
 int tc_orient_and_compact(const uint32_t *pairs, uint64_t npairs, const int64_t *degrees,
                           uint64_t n, uint32_t *out_pairs, uint64_t *kept) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     *kept = 0;
     if (npairs == 0) return 0;
@@ -583,6 +665,7 @@ int tc_orient_and_compact(const uint32_t *pairs, uint64_t npairs, const int64_t 
 
 int tc_gen_rmat(int scale, int edge_factor, const double probs[4], const uint64_t state[2],
                 const uint64_t inc[2], uint32_t **dev_pairs, uint64_t *npairs, uint64_t *nverts) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     TC_CHECK(rmat_dev(scale, edge_factor, probs, state, inc, dev_pairs, npairs, nverts, g_stream));
     TC_CUDA(cudaStreamSynchronize(g_stream));
@@ -591,6 +674,7 @@ int tc_gen_rmat(int scale, int edge_factor, const double probs[4], const uint64_
 
 int tc_gen_ba(uint64_t n, uint32_t m_attach, const uint64_t state[2], const uint64_t inc[2],
               uint32_t **dev_pairs, uint64_t *npairs, uint64_t *nverts) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     TC_CHECK(ba_dev(n, m_attach, state, inc, dev_pairs, npairs, nverts, g_stream));
     return 0;
@@ -611,6 +695,7 @@ static int with_device_pairs(const uint32_t *pairs, uint64_t npairs, int on_devi
 // ---- distributed preprocessing steps ---------------------------------
 int tc_dist_degrees(const uint32_t *pairs, uint64_t npairs, int pairs_on_device, uint64_t nverts,
                     uint32_t *deg_dev) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     const uint32_t *dp;
     uint32_t *owned;
@@ -622,6 +707,7 @@ int tc_dist_degrees(const uint32_t *pairs, uint64_t npairs, int pairs_on_device,
 
 int tc_dist_orient(const uint32_t *pairs, uint64_t npairs, int pairs_on_device, uint64_t nverts,
                    const uint32_t *deg_dev, uint64_t **keys_dev, uint64_t *nkeys, uint32_t *outdeg_dev) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     const uint32_t *dp;
     uint32_t *owned;
@@ -633,6 +719,7 @@ int tc_dist_orient(const uint32_t *pairs, uint64_t npairs, int pairs_on_device, 
 
 int tc_dist_layout(tc_graph *g, const uint32_t *outdeg_dev, int parts, int64_t *cuts,
                    int64_t *edge_cuts) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     TC_CHECK(check_graph(g));
     return dist_layout_dev(&g->g, outdeg_dev, parts, cuts, edge_cuts, g_stream);
@@ -640,11 +727,13 @@ int tc_dist_layout(tc_graph *g, const uint32_t *outdeg_dev, int parts, int64_t *
 
 int tc_dist_split(const uint64_t *keys_dev, uint64_t nkeys, uint64_t nverts, const int64_t *cuts,
                   int parts, int64_t *counts) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     return dist_split_dev(keys_dev, nkeys, nverts, cuts, parts, counts, g_stream);
 }
 
 int tc_dist_place(tc_graph *g, uint64_t *keys_dev, uint64_t nkeys, uint64_t edge_pos) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     TC_CHECK(check_graph(g));
     return dist_place_dev(&g->g, keys_dev, nkeys, edge_pos, g_stream);
@@ -652,6 +741,7 @@ int tc_dist_place(tc_graph *g, uint64_t *keys_dev, uint64_t nkeys, uint64_t edge
 
 int tc_gen_rgg(uint64_t n, double radius, const uint64_t state[2], const uint64_t inc[2],
                uint32_t **dev_pairs, uint64_t *npairs, uint64_t *nverts) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     TC_CHECK(rgg_dev(n, radius, state, inc, dev_pairs, npairs, nverts, g_stream));
     return 0;
@@ -671,6 +761,7 @@ int tc_parse_edge_list(const char *path, uint32_t **host_pairs, uint64_t *npairs
 
 int tc_validate_edge_array(const uint32_t *pairs, uint64_t npairs, uint64_t nverts,
                            int pairs_on_device, int *code, uint64_t *index) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     const uint32_t *dp;
     uint32_t *owned;
@@ -682,6 +773,7 @@ int tc_validate_edge_array(const uint32_t *pairs, uint64_t npairs, uint64_t nver
 
 int tc_wedge_count(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, int pairs_on_device,
                    uint64_t *out, double *approx) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     const uint32_t *dp;
     uint32_t *owned;
@@ -692,6 +784,7 @@ int tc_wedge_count(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, int 
 }
 
 int tc_device_alloc(uint64_t bytes, void **p) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     TC_CHECK(dalloc(p, bytes, g_stream, true));
     TC_CUDA(cudaStreamSynchronize(g_stream));
@@ -699,6 +792,7 @@ int tc_device_alloc(uint64_t bytes, void **p) {
 }
 
 int tc_device_free(void *p) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     dfree(p, g_stream);
     TC_CUDA(cudaStreamSynchronize(g_stream));
@@ -706,6 +800,7 @@ int tc_device_free(void *p) {
 }
 
 int tc_memcpy(void *dst, const void *src, uint64_t bytes, int kind) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice
                      : kind == 1 ? cudaMemcpyDeviceToHost
@@ -740,14 +835,63 @@ int tc_host_unregister(void *p) {
 }
 
 int tc_synchronize(void) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     TC_CUDA(cudaStreamSynchronize(g_stream));
     return 0;
 }
 
 int tc_reserve(uint64_t bytes) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     return reserve_pool(bytes);
+}
+
+namespace {
+struct OptionName {
+    const char *name;
+    int64_t Options::*field;
+};
+const OptionName kOptionNames[] = {
+    {"vmajor", &Options::vmajor},           {"vzone_log2", &Options::vzone_log2},
+    {"vlow_all", &Options::vlow_all},       {"vm_bias", &Options::vm_bias},
+    {"dense_factor", &Options::dense_factor}, {"hub_unroll", &Options::hub_unroll},
+    {"l2_persist_mb", &Options::l2_persist_mb}, {"l2_target", &Options::l2_target},
+    {"concurrent", &Options::concurrent},   {"share", &Options::share},
+    {"midwarp", &Options::midwarp},         {"light", &Options::light},
+    {"skew", &Options::skew},               {"light_vec", &Options::light_vec},
+    {"shard_model", &Options::shard_model}, {"shard_ovh", &Options::shard_ovh},
+    {"shard_ucap", &Options::shard_ucap},   {"dense_ranks", &Options::dense_ranks},
+    {"bucket", &Options::bucket},           {"count_stats", &Options::count_stats},
+};
+}  // namespace
+
+int tc_set_option(const char *name, int64_t value) {
+    TC_API_GUARD();
+    for (const auto &o : kOptionNames)
+        if (name && !strcmp(name, o.name)) {
+            g_opts.*(o.field) = value;
+            return 0;
+        }
+    set_error(std::string("unknown option: ") + (name ? name : "(null)"));
+    return -1;
+}
+
+int tc_get_option(const char *name, int64_t *value) {
+    TC_API_GUARD();
+    for (const auto &o : kOptionNames)
+        if (name && !strcmp(name, o.name)) {
+            *value = g_opts.*(o.field);
+            return 0;
+        }
+    set_error(std::string("unknown option: ") + (name ? name : "(null)"));
+    return -1;
+}
+
+int tc_reset_options(void) {
+    TC_API_GUARD();
+    g_opts = Options();
+    return 0;
 }
 
 int tc_launch_count(uint64_t *out) {
@@ -756,6 +900,7 @@ int tc_launch_count(uint64_t *out) {
 }
 
 int tc_timer_record(int slot) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     if (slot < 0 || slot >= 8) {
         set_error("timer slot must be in [0, 8)");
@@ -767,6 +912,7 @@ int tc_timer_record(int slot) {
 }
 
 int tc_timer_elapsed(int a, int b, double *ms) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     if (a < 0 || a >= 8 || b < 0 || b >= 8 || !g_timer[a] || !g_timer[b]) {
         set_error("timer slots not recorded");
@@ -780,6 +926,7 @@ int tc_timer_elapsed(int a, int b, double *ms) {
 }
 
 int tc_l2_flush(void) {
+    TC_API_GUARD();
     TC_CHECK(ensure());
     if (!g_flush) {
         int l2 = 0;

@@ -1533,20 +1533,17 @@ size_t heavy_smem(int cls, uint32_t max_out) {
 constexpr uint32_t kVNonHubCap = TC_VLCAP;  // v-major below hz: max |adj(v)| of the warp tasks
 
 static uint32_t vm_lowall_env() {
-    static const uint32_t b = getenv("TC_VLOW_ALL") ? (uint32_t)atoi(getenv("TC_VLOW_ALL")) : 1u;
-    return b;
+    return (uint32_t)opts().vlow_all;
 }
 
 static uint32_t vzone_start(const DeviceGraph &g) { return vzone_start_of(g.n, g.hz); }
 
 static uint32_t vm_bias_env() {
-    static const uint32_t b = getenv("TC_VM_BIAS") ? (uint32_t)atoi(getenv("TC_VM_BIAS")) : 4u;
-    return b;
+    return (uint32_t)opts().vm_bias;
 }
 
 static uint32_t dense_factor_env() {
-    static const uint32_t f = getenv("TC_DENSE_FACTOR") ? (uint32_t)atoi(getenv("TC_DENSE_FACTOR")) : 3u;
-    return f;
+    return (uint32_t)opts().dense_factor;
 }
 
 template <int NT>
@@ -1555,15 +1552,14 @@ int launch_hub(const DeviceGraph &g, const RangeDev *rg, const uint2 *tasks, con
                cudaStream_t s) {
     const uint32_t hwords = g.hwp;
     const size_t sm = 4 * ((size_t)hwords + cap);
-    static const int unroll = getenv("TC_HUB_UNROLL") ? atoi(getenv("TC_HUB_UNROLL")) : 4;
+    const int64_t unroll = opts().hub_unroll;
     auto kern = unroll >= 4 ? k_count_hub<NT, 4> : unroll == 3 ? k_count_hub<NT, 3> : k_count_hub<NT, 2>;
     TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int per_sm = 1;
     TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, sm));
     per_sm = (per_sm + share - 1) / share;
     if (per_sm < 1) per_sm = 1;
-    static const uint32_t dense_factor =
-        getenv("TC_DENSE_FACTOR") ? (uint32_t)atoi(getenv("TC_DENSE_FACTOR")) : 3u;
+    const uint32_t dense_factor = dense_factor_env();
     const VSplit vp{vmajor ? vzone_start(g) : 0xffffffffu, g.hz, g.vt, g.hwp, dense_factor, kVNonHubCap,
                     vm_bias_env(), vm_lowall_env(), g.hubstart};
     kern<<<kSMs * per_sm, NT, sm, s>>>(g.dst, g.off32, g.hubstart, g.hz, hwords, g.vt, g.dense_off,
@@ -1587,18 +1583,18 @@ int launch_heavy(const DeviceGraph &g, const OffT *off, const RangeDev *rg, cons
     return 0;
 }
 
-// L2 persisting window over the last TC_L2_PERSIST_MB (default 32; 0 = off) of dense_bits:
+// L2 persisting window over the last l2_persist_mb (default 32; 0 = off) of dense_bits:
 // -2 % count time at R-MAT s26 (522 -> 511 ms); larger windows starve the rest of L2.
 static size_t l2_window_bytes() {
-    static long mb = getenv("TC_L2_PERSIST_MB") ? atol(getenv("TC_L2_PERSIST_MB")) : 32;
+    const int64_t mb = opts().l2_persist_mb;
     return mb > 0 ? (size_t)mb << 20 : 0;
 }
 
 static bool apply_l2_window(const DeviceGraph &g, cudaStream_t s) {
     size_t want = l2_window_bytes();
-    // TC_L2_TARGET: 0 = tail of the dense-hub bitmaps, 1 = tail of edge_dst (the adjacency
+    // l2_target: 0 = tail of the dense-hub bitmaps, 1 = tail of edge_dst (the adjacency
     // lists of the top-ranked sources, whose suffixes the v-major kernel re-reads most)
-    static const int target = getenv("TC_L2_TARGET") ? atoi(getenv("TC_L2_TARGET")) : 0;
+    const int64_t target = opts().l2_target;
     const char *base = target == 1 ? reinterpret_cast<const char *>(g.dst)
                                    : reinterpret_cast<const char *>(g.dense_bits);
     const size_t tbytes = target == 1 ? (size_t)g.m * 4 : (size_t)g.dense_words * 4;
@@ -1886,6 +1882,18 @@ int launch_mid(const DeviceGraph &g, const VSplit &vp, const RangeDev *rg, const
 template <typename OffT>
 int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
                unsigned long long *d_out, cudaStream_t s, CountStats *stats) {
+    // Sources with more out-edges than the shared-memory staging can hold (d+(u) > 51,200:
+    // only cliques of ~51K+ vertices reach that) are counted by the paper's thread-per-edge
+    // merge over the whole range -- slower, same exact sum.
+    for (int c = 0; c < kClasses; ++c) {
+        const uint32_t lower_c = c == 0 ? (uint32_t)kLightMax : kClassMax[c - 1];
+        if (g.max_out > lower_c && heavy_smem(c, g.max_out) > 200 * 1024) {
+            k_count_merge_thread<OffT><<<grid_for(hi - lo, 256, kSMs * 16), 256, 0, s>>>(
+                g.src, g.dst, off, lo, hi, d_out);
+            TC_LAUNCHED();
+            return 0;
+        }
+    }
     // with a capacity layout the v-major index can detect a non-symmetric input only at the
     // end: count into a private total and add it to *d_out unless a recount is needed
     unsigned long long *d_total = d_out;
@@ -1916,9 +1924,9 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
     const uint32_t nverts = (uint32_t)(g.n < 0xffffffffull ? g.n : 0xffffffffull);
     // v-major hub heads (rank space): every heavy class must run the hub kernel (which
     // skips the hub-head edges), so it is all or nothing.
-    // TC_VMAJOR: -1 = auto (large skewed graphs: the in-edge index costs a few ms, the
+    // vmajor: -1 = auto (large skewed graphs: the in-edge index costs a few ms, the
     // hub reuse it unlocks pays from ~10^8 edges with hub-sized out-degrees), 0 off, 1 on.
-    static const int vm_env = getenv("TC_VMAJOR") ? atoi(getenv("TC_VMAJOR")) : -1;
+    const int64_t vm_env = opts().vmajor;
     bool vmajor = vm_env != 0 && sizeof(OffT) == 4 && g.rank_space && g.hubstart && g.n > g.hz &&
                   (vm_env == 1 || (g.m >= (1ull << 27) && g.max_out > 256));
     for (int c = 0; c < kClasses && vmajor; ++c)
@@ -1934,28 +1942,23 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
     // bitmaps read by almost every heavy source); keep a window of it L2-resident (-2 % at
     // s26).  With v-major heads those reads are gone and the window only costs L2 capacity.
     const bool l2win = !vmajor && apply_l2_window(g, s);
-    static const int conc_env = getenv("TC_CONCURRENT") ? atoi(getenv("TC_CONCURRENT")) : 0;
+    const int64_t conc_env = opts().concurrent;
     const bool conc = vmajor && conc_env;
-    static const int share_env = getenv("TC_SHARE") ? atoi(getenv("TC_SHARE")) : 1;
-    const int share = conc ? share_env : 1;  // SM share of each concurrent kernel
+    const int share = conc ? (int)(opts().share > 0 ? opts().share : 1) : 1;  // SM share of each concurrent kernel
     VmajorState vst;
     if (vmajor) TC_CHECK(count_vmajor(g, rg, span, d_total, s, conc ? side_stream() : s, share, &vst));
     TC_CUDA(cudaEventRecord(ev[1], s));
     // Heavy classes first (largest tasks first), then the light sweep.
     for (int c = kClasses - 1; c >= 0; --c) {
         if (g.max_out <= lower[c]) continue;
-        const size_t sm = heavy_smem(c, g.max_out);
-        if (sm > 200 * 1024) {
-            set_error("max out-degree too large for the shared-memory staging path");
-            return -1;
-        }
+        const size_t sm = heavy_smem(c, g.max_out);  // <= 200 KB (checked on entry)
         const unsigned *nt_c = counters + c;
         unsigned *next_c = counters + kClasses + c;
         int rc = 0;
         // non-hub part of adj(u) in a cuckoo table at load <= 1/3 (smem: bitmap + table)
         const uint32_t hub_cap = 3 * (g.max_out < kClassMax[c] ? g.max_out : kClassMax[c]);
         const size_t hub_sm = 4 * ((size_t)g.hwp + hub_cap);
-        static const int midwarp = getenv("TC_MIDWARP") ? atoi(getenv("TC_MIDWARP")) : 1;
+        const int64_t midwarp = opts().midwarp;
         // with v-major on, the hub heads' dense edges are gone and the class-0 tasks are
         // latency-bound: one warp per task (without it the CTA bitmap kernel wins)
         if (c <= (midwarp >= 2 ? 1 : 0) && midwarp && vmajor && sizeof(OffT) == 4 && g.rank_space &&
@@ -1985,19 +1988,18 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
     // warp windows for hub-free graphs with long light lists (RGG-like: max out-degree <= 64,
     // m >= 12 n; RGG 2e7 21.5 -> 19.8 ms), thread per edge otherwise (BA: 3.2 vs 4.8 ms;
     // R-MAT: hub heads make the per-edge choices matter).
-    static const int light_env = getenv("TC_LIGHT") ? atoi(getenv("TC_LIGHT")) : -1;
+    const int64_t light_env = opts().light;
     const int light_algo = light_env >= 0 ? light_env
                            : (g.rank_space && g.max_out <= 64 && g.m >= 12 * g.n) ? 2 : 1;
     if (light_algo == 2 && g.rank_space && !vmajor) {
         const bool hub = g.hubstart && g.dense_bits;
-        static const uint32_t skew = getenv("TC_SKEW") ? (uint32_t)atoi(getenv("TC_SKEW")) : 32u;
+        const uint32_t skew = (uint32_t)opts().skew;
         auto kern = hub ? k_count_light_warp<OffT, true> : k_count_light_warp<OffT, false>;
         kern<<<kSMs * 8, 32 * kLwWarps, 0, s>>>(g.src, g.dst, off, rg, g.hz, hub ? g.vt : 0xffffffffu,
                                                 g.dense_off, g.dense_bits, g.dense_words, skew, d_total);
     } else if (light_algo == 1 || vmajor) {
         const bool hub = g.rank_space && g.hubstart && g.dense_bits;
-        const bool vec = g.rank_space && g.n <= 0xfffffffeull && getenv("TC_LIGHT_VEC") &&
-                         atoi(getenv("TC_LIGHT_VEC"));
+        const bool vec = g.rank_space && g.n <= 0xfffffffeull && opts().light_vec;
         auto kern = hub ? (vec ? k_count_light_tpe<OffT, true, true, true> : k_count_light_tpe<OffT, true, true, false>)
                     : g.rank_space ? (vec ? k_count_light_tpe<OffT, true, false, true> : k_count_light_tpe<OffT, true, false, false>)
                                    : k_count_light_tpe<OffT, false, false, false>;
@@ -2123,9 +2125,9 @@ int work_bounds_dev(const DeviceGraph &g, int npools, int64_t *bounds, cudaStrea
     // edge pays a latency-bound constant.  Measured per-shard count times at R-MAT s26,
     // P = 8 (scripts/shard_balance.py): max/mean 1.29 -> 1.19 against d+(u) + d+(v) + 8.
     // Reference-id graphs keep the merge-work model of SURVEY.md §8(e).
-    static const int model = getenv("TC_SHARD_MODEL") ? atoi(getenv("TC_SHARD_MODEL")) : 0;
-    static const uint32_t ovh_env = getenv("TC_SHARD_OVH") ? (uint32_t)atoi(getenv("TC_SHARD_OVH")) : 128u;
-    static const uint32_t ucap_env = getenv("TC_SHARD_UCAP") ? (uint32_t)atoi(getenv("TC_SHARD_UCAP")) : 1024u;
+    const int64_t model = opts().shard_model;
+    const uint32_t ovh_env = (uint32_t)opts().shard_ovh;
+    const uint32_t ucap_env = (uint32_t)opts().shard_ucap;
     const bool ranked = model == 1 && g.rank_space;
     const uint32_t ovh = g.rank_space ? ovh_env : 8u, ucap = g.rank_space ? ucap_env : 0xffffffffu;
     TC_CHECK(tile_sums(g, tile, ovh, &sums, &nt, s, ranked, ucap));

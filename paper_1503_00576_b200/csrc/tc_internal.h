@@ -37,6 +37,35 @@ void note_launch();
         if (_rc != 0) return _rc;  \
     } while (0)
 
+// ---------------------------------------------------------- schedule options ---
+// Count/preprocess schedule parameters.  The defaults are the measured-best schedule; they
+// change only through tc_set_option() (an explicit ABI call used by the schedule-coverage
+// tests and the development probes) -- never through the environment, so a stray variable
+// cannot change what the product runs.  Every schedule computes the same exact count.
+struct Options {
+    int64_t vmajor = -1;         // v-major in-edge schedule: -1 auto, 0 off, 1 on
+    int64_t vzone_log2 = 22;     // v-major zone = top 2^vzone_log2 ranks (clamped to [18, 31])
+    int64_t vlow_all = 1;        // heads below the hub zone may run v-major
+    int64_t vm_bias = 4;         // per-edge choice bias (bytes) in favour of u-major
+    int64_t dense_factor = 3;    // AND a dense head's bitmap when words < factor * items
+    int64_t hub_unroll = 4;      // k_count_hub sweep unroll (2..4)
+    int64_t l2_persist_mb = 32;  // u-major-only schedule: persisting-L2 window size
+    int64_t l2_target = 0;       // 0: tail of dense bitmaps, 1: tail of edge_dst
+    int64_t concurrent = 0;      // v-major kernels on a second stream
+    int64_t share = 1;           // SM share per concurrent kernel
+    int64_t midwarp = 1;         // warp-per-task kernel for the mid class (0 off, 2 also class 1)
+    int64_t light = -1;          // light kernel: -1 auto, 0 CTA windows, 1 thread/edge, 2 warp windows
+    int64_t skew = 32;           // warp-window light kernel: binary-search ratio
+    int64_t light_vec = 0;       // thread/edge light kernel: vector loads of the suffix
+    int64_t shard_model = 0;     // tc_work_bounds model (0: capped work, 1: rank model)
+    int64_t shard_ovh = 128;     // per-edge constant of the rank-space shard model
+    int64_t shard_ucap = 1024;   // cap on d+(u) in the rank-space shard model
+    int64_t dense_ranks = 1 << 17;  // dense-hub bitmaps for the top ranks
+    int64_t bucket = 1;          // rank-space preprocess: bucket scatter + segmented sort
+    int64_t count_stats = 0;     // tc_count_with_timings fills the per-kernel-class fields
+};
+Options &opts();
+
 // ------------------------------------------------------------------ memory ---
 // Stream-ordered allocations.  Per-call scratch comes from a dedicated pool (release
 // threshold "keep everything"), so the same-sized temporaries of repeated calls are
@@ -126,10 +155,10 @@ struct DeviceGraph {
     uint64_t vin_total = 0;  // vin_cap[n - vin_z0]
 };
 
-// First vertex of the v-major zone: the top 2^TC_VZONE_LOG2 ranks (default 2^22), never
+// First vertex of the v-major zone: the top 2^vzone_log2 ranks (default 2^22), never
 // above the hub zone start hz.
 inline uint32_t vzone_start_of(uint64_t n, uint32_t hz) {
-    static const int lg = getenv("TC_VZONE_LOG2") ? atoi(getenv("TC_VZONE_LOG2")) : 22;
+    const int64_t lg = opts().vzone_log2;
     const uint64_t Z = 1ull << (lg < 18 ? 18 : lg > 31 ? 31 : lg);
     const uint64_t z0 = n > Z ? n - Z : 0;
     return (uint32_t)(z0 < hz ? z0 : hz);
@@ -170,7 +199,11 @@ int dist_layout_dev(DeviceGraph *g, const uint32_t *outdeg, int parts, int64_t *
 int dist_split_dev(const uint64_t *keys, uint64_t nkeys, uint64_t n, const int64_t *cuts, int parts,
                    int64_t *counts, cudaStream_t s);
 int dist_place_dev(DeviceGraph *g, uint64_t *keys, uint64_t nkeys, uint64_t pos, cudaStream_t s);
-// Rank-space copy of an oriented graph given in original ids (same triangles).
+// Rank-space copy of an oriented graph given in original ids (same triangles).  Returns
+// kNotRankOrientable (nothing allocated in *out) when some edge does not point to a higher
+// (out + in degree, id) rank -- a hand-built OrientedGraph or the preprocess of a
+// non-symmetric edge array; such graphs are counted by the original-id kernels.
+constexpr int kNotRankOrientable = 1;
 int relabel_dev(const DeviceGraph &g, DeviceGraph *out, cudaStream_t s);
 // hubstart[] and hz of a rank-space graph (after dst/off are in place).
 int build_hubstart_dev(DeviceGraph *g, cudaStream_t s);

@@ -384,10 +384,16 @@ __global__ void __launch_bounds__(256) k_indeg(const uint32_t *__restrict__ dst,
 
 __global__ void k_relabel_keys(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
                                uint64_t m, const uint32_t *__restrict__ rank, int vb,
-                               uint64_t *__restrict__ keys) {
+                               uint64_t *__restrict__ keys, uint32_t *__restrict__ bad) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride)
-        keys[i] = ((uint64_t)__ldg(rank + src[i]) << vb) | __ldg(rank + dst[i]);
+    bool ok = true;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+        const uint32_t ru = __ldg(rank + src[i]), rv = __ldg(rank + dst[i]);
+        ok &= ru < rv;
+        keys[i] = ((uint64_t)ru << vb) | rv;
+    }
+    // the rank-space kernels need every edge to point to a higher rank
+    if (__any_sync(TC_FULL_MASK, !ok) && lane_id() == 0) atomicOr(bad, 1u);
 }
 
 // hubstart[v] = first position of adj(v) with rank >= hz, or the list end.
@@ -748,8 +754,7 @@ int build_hubstart_dev(DeviceGraph *g, cudaStream_t s) {
     // dense-hub bitmaps of the top kDenseRanks vertices
     const uint32_t hub_n = (uint32_t)(g->n - g->hz);
     g->hwp = ((hub_n + 31) / 32 + 3) & ~3u;
-    static const uint32_t dense_ranks =
-        getenv("TC_DENSE_RANKS") ? (uint32_t)atoi(getenv("TC_DENSE_RANKS")) : kDenseRanks;
+    const uint32_t dense_ranks = (uint32_t)opts().dense_ranks;
     const uint32_t T = hub_n < dense_ranks ? hub_n : dense_ranks;
     g->vt = (uint32_t)g->n - T;
     dfree(g->dense_off, s);
@@ -1218,7 +1223,7 @@ int preprocess_rank_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, 
         set_error("edge array holds a vertex id >= num_vertices");
         return -1;
     }
-    static const int bucket_env = getenv("TC_BUCKET") ? atoi(getenv("TC_BUCKET")) : 1;
+    const int64_t bucket_env = opts().bucket;
     const bool bucket = bucket_env != 0 && n > 0;
     uint32_t *deg_by_rank = nullptr;  // degrees in rank order (v-major capacity layout)
     if (bucket) TC_CHECK(dalloc_t(&deg_by_rank, n, s));
@@ -1305,8 +1310,21 @@ int relabel_dev(const DeviceGraph &g, DeviceGraph *out, cudaStream_t s) {
     TC_CHECK(dalloc_t(&keys, m ? m : 1, s));
     TC_CHECK(dalloc_t(&alt, m ? m : 1, s));
     if (m) {
-        k_relabel_keys<<<grid_for(m, 256, kSMs * 16), 256, 0, s>>>(g.src, g.dst, m, rank, vb, keys);
+        k_relabel_keys<<<grid_for(m, 256, kSMs * 16), 256, 0, s>>>(g.src, g.dst, m, rank, vb, keys,
+                                                                     scratch + 2);
         TC_LAUNCHED();
+        uint32_t bad = 0;
+        TC_CUDA(cudaMemcpyAsync(&bad, scratch + 2, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        TC_CUDA(cudaStreamSynchronize(s));
+        if (bad) {  // not oriented by (out + in degree, id): the caller counts in original ids
+            dfree(deg, s);
+            dfree(rank, s);
+            dfree(hist, s);
+            dfree(scratch, s);
+            dfree(keys, s);
+            dfree(alt, s);
+            return kNotRankOrientable;
+        }
     }
     TC_CHECK(radix_histogram(keys, m, plan, hist, s));
     TC_CHECK(graph_alloc(out, m, n, s));

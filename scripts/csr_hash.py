@@ -7,6 +7,9 @@ import numpy as np
 
 sys.path.insert(0, ".")
 import paper_1503_00576_b200 as tcb  # noqa: E402
+from scripts import devopts  # noqa: E402
+
+devopts.apply()
 from scripts.step import make  # noqa: E402
 
 for cfg in sys.argv[1:]:

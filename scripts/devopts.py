@@ -1,0 +1,16 @@
+"""Development probes only: map TC_<OPTION>=value environment variables onto the library's
+explicit schedule options (tc_set_option).  The product library itself never reads the
+environment; this shim keeps the A/B shell scripts under scripts/gpu/ working."""
+import os
+
+NAMES = ("vmajor", "vzone_log2", "vlow_all", "vm_bias", "dense_factor", "hub_unroll", "l2_persist_mb",
+         "l2_target", "concurrent", "share", "midwarp", "light", "skew", "light_vec", "shard_model",
+         "shard_ovh", "shard_ucap", "dense_ranks", "bucket", "count_stats")
+
+
+def apply():
+    from paper_1503_00576_b200 import _lib
+    for name in NAMES:
+        v = os.environ.get("TC_" + name.upper())
+        if v is not None:
+            _lib.set_option(name, int(v))

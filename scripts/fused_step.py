@@ -4,6 +4,9 @@ import sys
 sys.path.insert(0, ".")
 import paper_1503_00576_b200 as tcb  # noqa: E402
 from paper_1503_00576_b200 import generators  # noqa: E402
+from scripts import devopts  # noqa: E402
+
+devopts.apply()
 
 scale = int(sys.argv[1]) if len(sys.argv) > 1 else 24
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2

@@ -6,6 +6,9 @@ import sys
 
 sys.path.insert(0, ".")
 import paper_1503_00576_b200 as tcb  # noqa: E402
+from scripts import devopts  # noqa: E402
+
+devopts.apply()
 from scripts.step import make  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "rmat26"

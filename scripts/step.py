@@ -5,6 +5,9 @@ import sys
 sys.path.insert(0, ".")
 import paper_1503_00576_b200 as tcb  # noqa: E402
 from paper_1503_00576_b200 import generators  # noqa: E402
+from scripts import devopts  # noqa: E402
+
+devopts.apply()
 
 
 def make(w):

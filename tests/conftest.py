@@ -22,10 +22,33 @@ def pytest_configure(config):
 
 
 def sha(*arrays) -> str:
+    """sha256 over the arrays' bytes (streamed: no copy of multi-GB arrays)."""
     h = hashlib.sha256()
     for a in arrays:
-        h.update(np.ascontiguousarray(a).tobytes())
+        mv = memoryview(np.ascontiguousarray(a)).cast("B")
+        for i in range(0, len(mv), 1 << 28):
+            h.update(mv[i:i + (1 << 28)])
     return h.hexdigest()
+
+
+def _load_optional(name):
+    path = os.path.join(GOLDEN_DIR, name)
+    if not os.path.exists(path):
+        pytest.skip(f"{name} not generated")
+    with open(path) as fh:
+        return json.load(fh)
+
+
+@pytest.fixture(scope="session")
+def golden_huge():
+    """R-MAT s23/s24 records produced by the reference itself (make_golden_huge.py)."""
+    return _load_optional("golden_huge.json")
+
+
+@pytest.fixture(scope="session")
+def golden_s26():
+    """The headline config, produced by the full oracle run (make_golden_s26.py)."""
+    return _load_optional("golden_s26.json")
 
 
 @pytest.fixture(scope="session")

@@ -34,7 +34,7 @@ def test_library_exports_every_declared_symbol():
     for name in _declared():
         assert hasattr(L, name), name
         assert name in _lib.EXPORTED, f"{name} has no ctypes signature"
-    assert L.tc_abi_version() == 2
+    assert L.tc_abi_version() == _lib.ABI_VERSION == 3
 
 
 def test_library_is_sm100a_only():
@@ -61,3 +61,12 @@ def test_no_gpu_raises_loudly():
     L = _lib.load(init=False)
     assert L.tc_init(0) != 0
     assert L.tc_last_error()
+
+
+def test_product_sources_never_read_the_environment():
+    """Schedule options change only through tc_set_option: no getenv in the library sources
+    (VERDICT r1 weak #9); the static CUDA runtime's own getenv use is outside our code."""
+    csrc = os.path.join(ROOT, "paper_1503_00576_b200", "csrc")
+    for name in os.listdir(csrc):
+        if name.endswith((".cu", ".cuh", ".h", ".cpp")):
+            assert "getenv" not in open(os.path.join(csrc, name)).read(), name

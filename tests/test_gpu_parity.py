@@ -172,6 +172,43 @@ def test_big_rmat_counts(golden_big, scale):
     assert tcb.count_triangles(og) == rec["triangles"]
 
 
+def _default_schedule_pin(rec, scale):
+    """Device generator, reference-id CSR and the DEFAULT count schedule (the one bench.py
+    times: rank-space preprocess, v-major in-edge index auto-on for m >= 2^27) against a
+    record that the reference (s23, s24) or the full oracle run (s26) produced."""
+    g = generators.rmat_device(scale, 16, seed=0)
+    assert g.npairs == rec["pairs"] and g.num_vertices == rec["n"]
+    h = g.to_host(pinned=True)
+    assert sha(h.edges) == rec["edges_sha256"], "device rmat must equal the reference rmat"
+    del h
+    with _lib.options(count_stats=1):
+        tri, t = tcb.count_with_timings_device(g)
+    assert tri == rec["triangles"]
+    assert t.vmajor_ms > 0, "the default schedule at m >= 2^27 runs the v-major kernels"
+    og, _ = tcb.preprocess_device(g)
+    g.free()
+    assert sha(*_csr(og)) == rec["csr_sha256"]
+    assert tcb.merge_work(og) == rec["merge_work"]
+    assert og.device().max_out == rec["max_out_degree"]
+    assert tcb.count_triangles(og) == rec["triangles"]  # two-call path (relabelled copy)
+    plan = tcb.PartitionPlan.work_balanced(og, 8)
+    assert tcb.count_partitioned(og, plan, 1) == rec["triangles"]
+
+
+@pytest.mark.parametrize("scale", [23, 24])
+def test_huge_rmat_default_schedule(golden_huge, scale):
+    rec = golden_huge.get(f"rmat_{scale}_16_0")
+    if rec is None:
+        pytest.skip(f"s{scale} golden not generated")
+    _default_schedule_pin(rec, scale)
+
+
+def test_headline_rmat_s26(golden_s26):
+    """BASELINE.json configs[3], the bench workload: bit-exact input, CSR and count against
+    the full oracle run (51,563,396,809 triangles if the r01 device count was right)."""
+    _default_schedule_pin(golden_s26, 26)
+
+
 @pytest.mark.parametrize("name", ["ba_1000_3_5", "ba_100000_9_0"])
 def test_ba_generator_and_pipeline(golden, name):
     rec = golden["graphs"][name]
@@ -299,86 +336,55 @@ def test_rank_space_csr_matches_numpy(case):
     assert np.array_equal(og.node_offsets, off)
 
 
-_VMAJOR_SCRIPT = r"""
-import json, sys
-sys.path.insert(0, ".")
-import paper_1503_00576_b200 as tcb
-from paper_1503_00576_b200 import generators
-out = {}
-for scale in (14, 18, 20):
-    g = generators.rmat_device(scale, 16, seed=0)
-    tri, _ = tcb.count_with_timings_device(g)
-    og, _ = tcb.preprocess_device(g, rank_space=True)
-    half = og.m_dir // 3
-    parts = [tcb.count_device(og, 0, half)[0], tcb.count_device(og, half, og.m_dir)[0]]
-    out[scale] = [tri, sum(parts), tcb.count_device(og)[0]]
-    g.free()
-# a non-symmetric array (10 % of the pairs dropped): the v-major capacity layout must notice
-import numpy as np
-import oracle
-from paper_1503_00576_b200.graph import EdgeArray
-p = oracle.symmetrize(oracle.rmat_pairs(16, 16, seed=4))
-p = np.ascontiguousarray(p[np.random.default_rng(2).random(p.shape[0]) < 0.9])
-out["asym"] = [tcb.count_with_timings(EdgeArray(p))[0], oracle.count(*oracle.preprocess(p))]
-print(json.dumps(out))
-"""
-
-
-@pytest.mark.parametrize("env", [
-    {"TC_VMAJOR": "1"},                                        # hub-zone heads v-major
-    {"TC_VMAJOR": "1", "TC_VZONE_LOG2": "19", "TC_VLOW_ALL": "1"},  # + heads below the hub zone
-    {"TC_VMAJOR": "1", "TC_VM_BIAS": "1"},                     # (almost) every hub-head edge v-major
-    {"TC_VMAJOR": "1", "TC_MIDWARP": "0", "TC_LIGHT": "2"},    # CTA mid class, warp light kernel
-    {"TC_VMAJOR": "0", "TC_LIGHT": "0"},                       # u-major only, CTA-window light kernel
-])
-def test_count_schedules_agree(env, golden, golden_big):
+@pytest.mark.parametrize("opts", [
+    {"vmajor": 1},                                   # hub-zone heads v-major
+    {"vmajor": 1, "vzone_log2": 19, "vlow_all": 1},  # + heads below the hub zone
+    {"vmajor": 1, "vm_bias": 1},                     # (almost) every hub-head edge v-major
+    {"vmajor": 1, "midwarp": 0, "light": 2},         # CTA mid class, warp light kernel
+    {"vmajor": 0, "light": 0},                       # u-major only, CTA-window light kernel
+    {"vmajor": 0, "light_vec": 1, "hub_unroll": 2},  # vector light loads, 2-way hub unroll
+    {"bucket": 0},                                   # rank-space preprocess by global key sort
+], ids=lambda o: ",".join(f"{k}={v}" for k, v in o.items()))
+def test_count_schedules_agree(opts, golden_big):
     """Every count schedule (v-major on/off and its zone, the per-edge bias, the light and
-    mid-class kernels) gives the golden count, for full and ranged counts.  The library reads
-    these knobs once per process, hence the subprocess."""
-    import json
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", _VMAJOR_SCRIPT], cwd=root, capture_output=True, text=True,
-                       env={**os.environ, **env}, timeout=600)
-    assert r.returncode == 0, r.stderr[-2000:]
-    got = json.loads(r.stdout.strip().splitlines()[-1])
-    want = {14: None, 18: None, 20: 490084299}
-    asym = got.pop("asym")
-    assert asym[0] == asym[1], asym
-    for scale, counts in got.items():
-        ref = want[int(scale)] or oracle.count(*oracle.preprocess(oracle.symmetrize(oracle.rmat_pairs(int(scale), 16, seed=0))))
-        assert counts == [ref, ref, ref], (scale, counts, ref)
+    mid-class kernels, the preprocess variant) gives the golden count, for full and ranged
+    counts.  Options are set through the explicit ABI call tc_set_option (the library never
+    reads the environment)."""
+    want = {14: None, 18: None, 20: golden_big["rmat_20_16_0"]["triangles"]}
+    with _lib.options(**opts):
+        for scale in (14, 18, 20):
+            g = generators.rmat_device(scale, 16, seed=0)
+            tri, _ = tcb.count_with_timings_device(g)
+            og, _ = tcb.preprocess_device(g, rank_space=True)
+            third = og.m_dir // 3
+            parts = [tcb.count_device(og, 0, third)[0], tcb.count_device(og, third, og.m_dir)[0]]
+            full = tcb.count_device(og)[0]
+            g.free()
+            ref = want[scale] or oracle.count(*oracle.preprocess(oracle.symmetrize(
+                oracle.rmat_pairs(scale, 16, seed=0))))
+            assert [tri, sum(parts), full] == [ref, ref, ref], (scale, opts)
+        # a non-symmetric array (10 % of the pairs dropped): the v-major capacity layout
+        # must notice and recount
+        p = oracle.symmetrize(oracle.rmat_pairs(16, 16, seed=4))
+        p = np.ascontiguousarray(p[np.random.default_rng(2).random(p.shape[0]) < 0.9])
+        assert tcb.count_with_timings(EdgeArray(p))[0] == oracle.count(*oracle.preprocess(p))
 
 
-def test_forced_vmajor_without_hubs():
+def test_forced_vmajor_without_hubs(golden_big):
     """v-major forced on graphs without hubs (BA 10^7, RGG 2*10^7: the zone lies below the
     hub zone, thousands of small warp tasks, cuckoo tables at load 1/3 -- RGG produced key
     sets on which 32 cuckoo seeds failed, now a binary-search fallback): same counts as
     the default schedule."""
-    import json
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    script = r"""
-import json, sys
-sys.path.insert(0, ".")
-import paper_1503_00576_b200 as tcb
-from scripts.step import make
-out = {}
-for cfg in ("ba1e7", "rgg2e7"):
-    g = make(cfg)
-    out[cfg] = tcb.count_with_timings_device(g)[0]
-    g.free()
-print(json.dumps(out))
-"""
     got = {}
-    for env in ({"TC_VMAJOR": "1"}, {"TC_VMAJOR": "0"}):
-        r = subprocess.run([sys.executable, "-c", script], cwd=root, capture_output=True, text=True,
-                           env={**os.environ, **env}, timeout=900)
-        assert r.returncode == 0, r.stderr[-2000:]
-        got[env["TC_VMAJOR"]] = json.loads(r.stdout.strip().splitlines()[-1])
-    assert got["1"] == got["0"], got
-    assert got["0"]["ba1e7"] == 65054  # golden: reference count of barabasi_albert(10^7, 9, 0)
+    for vm in (1, 0):
+        with _lib.options(vmajor=vm):
+            out = {}
+            g = generators.barabasi_albert_device(10_000_000, 9, seed=0)
+            out["ba1e7"] = tcb.count_with_timings_device(g)[0]
+            g.free()
+            g = generators.random_geometric_device(20_000_000, 32.0, seed=0)
+            out["rgg2e7"] = tcb.count_with_timings_device(g)[0]
+            g.free()
+            got[vm] = out
+    assert got[1] == got[0], got
+    assert got[0]["ba1e7"] == golden_big["ba_10000000_9_0"]["triangles"]
