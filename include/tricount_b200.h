@@ -196,6 +196,12 @@ int tc_reserve(uint64_t bytes);
  * vm_bias, dense_factor, hub_unroll, l2_persist_mb, l2_target, concurrent, share, midwarp,
  * light, skew, light_vec, shard_model, shard_ovh, shard_ucap, dense_ranks, bucket,
  * count_stats (see csrc/tc_internal.h Options).  Unknown names return -1. */
+/* Compulsory HBM bytes of the full-count schedule (rank-space copy of g): out[0] v-major
+ * suffix streams + index entries, [1] u-major heavy-source reads of heads, [2] light-source
+ * reads, [3] 16 B per edge (src, dst, two offsets), [4] heavy-source staging.  The roofline
+ * numerator of bench.py; no reference counterpart. */
+int tc_schedule_bytes(const tc_graph *g, uint64_t out[5]);
+
 int tc_set_option(const char *name, int64_t value);
 int tc_get_option(const char *name, int64_t *value);
 int tc_reset_options(void);

@@ -18,6 +18,7 @@ from .count import (
     intersect_count,
     merge_work,
     preprocess_device,
+    schedule_bytes,
     warm_kernel,
 )
 from .graph import (
@@ -43,7 +44,7 @@ __all__ = [
     "build_node_array", "count_device", "count_partitioned", "count_triangles",
     "count_with_timings", "count_with_timings_device", "default_workers", "degrees_of",
     "intersect_count", "max_out_degree_bound", "merge_work", "orient_and_compact",
-    "preprocess", "preprocess_device", "sort_edges", "unzip", "validate_oriented_graph",
+    "preprocess", "preprocess_device", "schedule_bytes", "sort_edges", "unzip", "validate_oriented_graph",
     "warm_kernel", "AsymmetricEdgeError", "DuplicateEdgeError", "GraphValidationError",
     "SelfLoopError", "validate_edge_array", "CountOverflowError", "InconsistentCountsError",
     "transitivity", "wedge_count",

@@ -22,7 +22,7 @@ from .graph import EdgeArray, OrientedGraph
 
 __all__ = ["PhaseTimings", "PartitionPlan", "count_triangles", "count_partitioned",
            "count_with_timings", "intersect_count", "warm_kernel", "default_workers",
-           "count_device", "merge_work"]
+           "count_device", "merge_work", "schedule_bytes"]
 
 
 @dataclass(frozen=True)
@@ -53,7 +53,7 @@ class PartitionPlan:
         """Cuts at k/P of the estimated work sum(d+(u) + d+(v) + c)."""
         if num_pools < 1:
             raise ValueError("num_pools must be >= 1")
-        dev = og.device()
+        dev = _device(og)
         bounds = np.zeros(num_pools + 1, dtype=np.int64)
         _lib.check(_lib.lib().tc_work_bounds(dev.handle, num_pools, _lib.ptr(bounds)))
         return cls(num_pools, tuple(int(b) for b in bounds))
@@ -88,11 +88,26 @@ def warm_kernel() -> None:
     _lib.lib()
 
 
+def _device(og):
+    """The device graph of an OrientedGraph -- ours (cached on it), or any object with the
+    reference OrientedGraph's arrays (graph.py:146-193), e.g. a tricount.graph.OrientedGraph
+    handed over by reference code: uploaded for the call."""
+    if isinstance(og, OrientedGraph):
+        return og.device()
+    from .graph import DeviceGraph
+    src = np.ascontiguousarray(og.edge_src, dtype=np.uint32)
+    dst = np.ascontiguousarray(og.edge_dst, dtype=np.uint32)
+    off = np.ascontiguousarray(og.node_offsets, dtype=np.int64)
+    if src.shape[0] != dst.shape[0]:
+        raise ValueError("edge_src and edge_dst lengths differ")
+    return DeviceGraph.upload(src, dst, off)
+
+
 def _count_bounds(og: OrientedGraph, bounds, algo: int):
     b = np.ascontiguousarray(bounds, dtype=np.int64)
     out = ctypes.c_uint64()
     t = _lib.TcTimes()
-    _lib.check(_lib.lib().tc_count_partitioned(og.device().handle, _lib.ptr(b), b.size - 1, algo,
+    _lib.check(_lib.lib().tc_count_partitioned(_device(og).handle, _lib.ptr(b), b.size - 1, algo,
                                                ctypes.byref(out), ctypes.byref(t)))
     return int(out.value), t
 
@@ -103,7 +118,7 @@ def count_device(og: OrientedGraph, lo: int = 0, hi: int | None = None,
     hi = og.m_dir if hi is None else int(hi)
     out = ctypes.c_uint64()
     t = _lib.TcTimes()
-    _lib.check(_lib.lib().tc_count(og.device().handle, int(lo), hi, algo, ctypes.byref(out),
+    _lib.check(_lib.lib().tc_count(_device(og).handle, int(lo), hi, algo, ctypes.byref(out),
                                    ctypes.byref(t)))
     return int(out.value), t
 
@@ -129,15 +144,23 @@ def count_partitioned(g: OrientedGraph, plan: PartitionPlan,
 def intersect_count(g: OrientedGraph, u: int, v: int) -> int:
     """|adj(u) ∩ adj(v)| over the oriented lists (count.py:102-136)."""
     out = ctypes.c_uint64()
-    _lib.check(_lib.lib().tc_intersect_count(g.device().handle, int(u), int(v), ctypes.byref(out)))
+    _lib.check(_lib.lib().tc_intersect_count(_device(g).handle, int(u), int(v), ctypes.byref(out)))
     return int(out.value)
 
 
 def merge_work(g: OrientedGraph) -> int:
     """W = sum over oriented edges of d+(u) + d+(v) (SURVEY.md §8(d) roofline numerator)."""
     out = ctypes.c_uint64()
-    _lib.check(_lib.lib().tc_merge_work(g.device().handle, ctypes.byref(out)))
+    _lib.check(_lib.lib().tc_merge_work(_device(g).handle, ctypes.byref(out)))
     return int(out.value)
+
+
+def schedule_bytes(g: OrientedGraph) -> dict:
+    """Compulsory HBM bytes of the full-count schedule, by kernel class (tc_schedule_bytes)."""
+    out = np.zeros(5, dtype=np.uint64)
+    _lib.check(_lib.lib().tc_schedule_bytes(_device(g).handle, _lib.ptr(out)))
+    keys = ("vmajor", "umajor_heavy", "light", "per_edge", "heavy_staging")
+    return {k: int(v) for k, v in zip(keys, out)}
 
 
 def count_with_timings(g: EdgeArray, num_workers: int | None = None,

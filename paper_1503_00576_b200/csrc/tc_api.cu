@@ -597,6 +597,15 @@ int tc_work_bounds(const tc_graph *g, int npools, int64_t *bounds) {
     return work_bounds_dev(g->g, npools, bounds, g_stream);
 }
 
+int tc_schedule_bytes(const tc_graph *g, uint64_t out[5]) {
+    TC_API_GUARD();
+    TC_CHECK(ensure());
+    TC_CHECK(check_graph(g));
+    const DeviceGraph *r = nullptr;
+    TC_CHECK(rank_copy(const_cast<tc_graph *>(g), &r));
+    return schedule_bytes_dev(*r, out, g_stream);
+}
+
 int tc_merge_work(const tc_graph *g, uint64_t *out) {
     TC_API_GUARD();
     TC_CHECK(ensure());

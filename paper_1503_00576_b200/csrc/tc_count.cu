@@ -1879,6 +1879,19 @@ int launch_mid(const DeviceGraph &g, const VSplit &vp, const RangeDev *rg, const
     return 0;
 }
 
+// The v-major decision of a count (rank-space graphs with u32 offsets).
+bool vmajor_schedule(const DeviceGraph &g) {
+    const int64_t vm_env = opts().vmajor;
+    bool vmajor = vm_env != 0 && g.off32 && g.rank_space && g.hubstart && g.n > g.hz &&
+                  (vm_env == 1 || (g.m >= (1ull << 27) && g.max_out > 256));
+    const uint32_t lower[kClasses] = {(uint32_t)kLightMax, kClassMax[0], kClassMax[1], kClassMax[2]};
+    for (int c = 0; c < kClasses && vmajor; ++c)
+        if (g.max_out > lower[c] &&
+            4 * ((size_t)g.hwp + 3 * (g.max_out < kClassMax[c] ? g.max_out : kClassMax[c])) > 200 * 1024)
+            vmajor = false;
+    return vmajor;
+}
+
 template <typename OffT>
 int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
                unsigned long long *d_out, cudaStream_t s, CountStats *stats) {
@@ -1926,13 +1939,7 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
     // skips the hub-head edges), so it is all or nothing.
     // vmajor: -1 = auto (large skewed graphs: the in-edge index costs a few ms, the
     // hub reuse it unlocks pays from ~10^8 edges with hub-sized out-degrees), 0 off, 1 on.
-    const int64_t vm_env = opts().vmajor;
-    bool vmajor = vm_env != 0 && sizeof(OffT) == 4 && g.rank_space && g.hubstart && g.n > g.hz &&
-                  (vm_env == 1 || (g.m >= (1ull << 27) && g.max_out > 256));
-    for (int c = 0; c < kClasses && vmajor; ++c)
-        if (g.max_out > lower[c] &&
-            4 * ((size_t)g.hwp + 3 * (g.max_out < kClassMax[c] ? g.max_out : kClassMax[c])) > 200 * 1024)
-            vmajor = false;
+    const bool vmajor = sizeof(OffT) == 4 && vmajor_schedule(g);
     if (g.max_out > (uint32_t)kLightMax) {
         k_classify<OffT><<<grid_for(nverts, 256, kSMs * 8), 256, 0, s>>>(
             off, rg, nullptr, tasks[0], tasks[1], tasks[2], tasks[3], counters);
@@ -2155,6 +2162,76 @@ int work_bounds_dev(const DeviceGraph &g, int npools, int64_t *bounds, cudaStrea
     }
     bounds[npools] = (int64_t)g.m;
     free(h);
+    return 0;
+}
+
+// ---------------------------------------------------------- schedule byte model ---
+// Compulsory HBM bytes of the schedule a full count of a rank-space graph runs (the roofline
+// numerator): every edge's data read once, at 4 B per item, along the path
+// the count kernels choose for it (same vmajor_edge predicate, same light-kernel variants):
+//   [0] v-major edges      4 * |suffix of adj(u) after v| + 8 (its in-edge index entry)
+//   [1] u-major heavy      dense head: 4 * bitmap words; otherwise 4 * |adj(v)|
+//   [2] light sources      4 * (|suffix| + |adj(v)|) merge; 4 * |suffix| dense-bitmap test;
+//                          4 * |suffix| * ceil(log2 |adj(v)|) binary search
+//   [3] every edge         16 (src, dst, off[v], off[v+1])
+//   [4] heavy staging      4 * d+(u) per heavy source (adj(u) into shared memory once)
+__global__ void __launch_bounds__(256)
+    k_schedule_bytes(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
+                     const uint32_t *__restrict__ off, uint64_t m, VSplit vp, bool hub,
+                     unsigned long long *__restrict__ out) {
+    unsigned long long b[5] = {0, 0, 0, 0, 0};
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+        const uint32_t u = __ldg(src + e), su = __ldg(off + u), eu = __ldg(off + u + 1), du = eu - su;
+        const uint32_t v = __ldg(dst + e), vs = __ldg(off + v), ve = __ldg(off + v + 1), dv = ve - vs;
+        b[3] += 16;
+        if (e == su && du > (uint32_t)kLightMax) b[4] += 4ull * du;
+        if (e + 1 >= eu || vs >= ve) continue;  // no triangle can close: every kernel skips it
+        const uint32_t sfx = eu - (uint32_t)e - 1;
+        if (vmajor_edge(vp, (uint32_t)e, eu, v, vs, ve)) {
+            b[0] += 4ull * sfx + 8;
+        } else if (du > (uint32_t)kLightMax) {
+            uint64_t x = 4ull * dv;
+            if (hub && v >= vp.hz) {
+                const uint32_t ws = ((v + 1 - vp.hz) >> 5) & ~3u;
+                if (v >= vp.vt && (vp.hwp - ws) < vp.factor * dv) x = 4ull * (vp.hwp - ws);
+            }
+            b[1] += x;
+        } else {
+            uint64_t x = 4ull * (sfx + dv);
+            if (hub && v >= vp.vt && sfx < dv) x = 4ull * sfx;
+            else if (sfx * (32u - __clz(dv)) < sfx + dv) x = 4ull * sfx * (32u - __clz(dv));
+            b[2] += x;
+        }
+    }
+    for (int k = 0; k < 5; ++k) {
+        unsigned long long x = b[k];
+        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(TC_FULL_MASK, x, o);
+        if (lane_id() == 0 && x) atomicAdd(out + k, x);
+    }
+}
+
+int schedule_bytes_dev(const DeviceGraph &g, uint64_t out[5], cudaStream_t s) {
+    if (!g.rank_space || !g.off32 || !g.hubstart) {
+        set_error("the schedule byte model needs a rank-space graph with m < 2^32");
+        return -1;
+    }
+    unsigned long long *d = nullptr;
+    TC_CHECK(dalloc_t(&d, 5, s));
+    TC_CUDA(cudaMemsetAsync(d, 0, 5 * sizeof(unsigned long long), s));
+    const bool vm = vmajor_schedule(g);
+    const VSplit vp{vm ? vzone_start(g) : 0xffffffffu, g.hz, g.vt, g.hwp, dense_factor_env(), kVNonHubCap,
+                    vm_bias_env(), vm_lowall_env(), g.hubstart};
+    if (g.m) {
+        k_schedule_bytes<<<grid_for(g.m, 256, kSMs * 16), 256, 0, s>>>(g.src, g.dst, g.off32, g.m, vp,
+                                                                      g.dense_bits != nullptr, d);
+        TC_LAUNCHED();
+    }
+    unsigned long long h[5];
+    TC_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    dfree(d, s);
+    for (int k = 0; k < 5; ++k) out[k] = h[k];
     return 0;
 }
 

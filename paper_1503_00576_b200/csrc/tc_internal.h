@@ -231,6 +231,9 @@ int intersect_dev(const DeviceGraph &g, uint32_t u, uint32_t v, uint64_t *out, c
 int work_bounds_dev(const DeviceGraph &g, int npools, int64_t *bounds, cudaStream_t s);
 // Σ over edges of d+(u)+d+(v) (the merge-model work W), host out.
 int merge_work_dev(const DeviceGraph &g, uint64_t *out, cudaStream_t s);
+// Compulsory bytes of the full-count schedule of a rank-space graph, by kernel class
+// (v-major, u-major heavy, light, per-edge, heavy staging); see tc_count.cu.
+int schedule_bytes_dev(const DeviceGraph &g, uint64_t out[5], cudaStream_t s);
 
 // ---------------------------------------------------------------- generators ---
 int rmat_dev(int scale, int edge_factor, const double probs[4], const uint64_t state[2],

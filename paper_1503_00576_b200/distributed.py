@@ -22,7 +22,8 @@ pairs, device-resident or copied from host memory by that rank alone):
   3. node_offsets from the global out-degrees; source-rank ranges balanced by edges;
   4. all-to-all: every key goes to the rank owning its source range;
   5. each rank sorts what it received into its slice of edge_dst; the slices are
-     all-gathered (one broadcast per owner); every rank finalises the same CSR;
+     all-gathered (one all_gather_into_tensor over slices padded to the longest);
+     every rank finalises the same CSR;
   6. work-balanced shards + one 64-bit all-reduce, as in v1.
 
 The orchestration is written against a small ``Ops`` interface so the same code runs
@@ -102,11 +103,15 @@ class Ops:
     def place(self, graph, recv, k: int, pos: int) -> None:
         raise NotImplementedError
 
-    def dst_slice(self, graph, lo: int, hi: int):  # int32[hi-lo] for an in-place broadcast
+    def dst_slice(self, graph, lo: int, hi: int):  # int32[hi-lo] view/copy of edge_dst[lo:hi]
         raise NotImplementedError
 
-    def dst_slice_done(self, graph, lo: int, hi: int, t) -> None:
-        pass
+    def dst_write(self, graph, lo: int, t) -> None:  # edge_dst[lo:lo+len(t)] = t
+        raise NotImplementedError
+
+    def comm_empty(self, k: int):  # int32[k] tensor the process group can use
+        import torch
+        return torch.empty(k, dtype=torch.int32)
 
     def free_keys(self, keys) -> None:
         pass
@@ -184,7 +189,6 @@ def count_distributed_sharded(ops: Ops, shard, num_vertices: int, group=None) ->
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
     n = int(num_vertices)
-    gr = [dist.get_global_rank(group, r) if group is not None else r for r in range(world)]
     shard = ops.stage(shard)  # host shards: this rank's H2D copy, once
     # 1. global degrees
     deg = ops.shard_degrees(shard, n)
@@ -222,13 +226,23 @@ def count_distributed_sharded(ops: Ops, shard, num_vertices: int, group=None) ->
     # 5. sort the received keys into this rank's slice of edge_dst; all-gather the slices
     ops.place(g, recv, k, int(ecuts[rank]))
     del recv
-    for r in range(world):
-        lo, hi = int(ecuts[r]), int(ecuts[r + 1])
-        if hi > lo:
-            t = ops.dst_slice(g, lo, hi)
-            dist.broadcast(t, src=gr[r], group=group)
-            _backend_sync(ops)
-            ops.dst_slice_done(g, lo, hi, t)
+    # one all-gather of the edge_dst slices (padded to the longest; the layout balances
+    # them by edge count, so the padding is at most one adjacency list)
+    lens = [int(ecuts[r + 1] - ecuts[r]) for r in range(world)]
+    L = max(lens)
+    if L:
+        ops.sync()
+        send = ops.comm_empty(L)
+        if lens[rank]:
+            send[:lens[rank]].copy_(ops.dst_slice(g, int(ecuts[rank]), int(ecuts[rank + 1])))
+        gathered = ops.comm_empty(world * L)
+        dist.all_gather_into_tensor(gathered, send, group=group)
+        _backend_sync(ops)
+        del send
+        for r in range(world):
+            if r != rank and lens[r]:
+                ops.dst_write(g, int(ecuts[r]), gathered[r * L:r * L + lens[r]])
+        del gathered
     ops.finalize(g)
     # 6. count the work-balanced shard; one all-reduce
     bounds = ops.work_bounds(g, world)
@@ -437,13 +451,16 @@ class B200Ops(Ops):
         t = torch.as_tensor(_CudaArray(dst + 4 * lo, hi - lo, "<i4"), device=self.torch_device)
         return self._out(t)
 
-    def dst_slice_done(self, graph, lo, hi, t):
-        if self.comm_device is None:  # staged through host: write the broadcast back
-            import torch
-            _, dst, _ = graph.device_pointers()
-            d = torch.as_tensor(_CudaArray(dst + 4 * lo, hi - lo, "<i4"), device=self.torch_device)
-            d.copy_(t)
-            torch.cuda.synchronize(self.torch_device)
+    def dst_write(self, graph, lo, t):
+        import torch
+        _, dst, _ = graph.device_pointers()
+        d = torch.as_tensor(_CudaArray(dst + 4 * lo, t.numel(), "<i4"), device=self.torch_device)
+        d.copy_(t)
+        torch.cuda.synchronize(self.torch_device)  # the library's stream reads it next
+
+    def comm_empty(self, k):
+        import torch
+        return torch.empty(k, dtype=torch.int32, device=self.comm_device or "cpu")
 
     def free_keys(self, keys):
         keys.free()

@@ -51,7 +51,7 @@ def build_node_array(sorted_edges, num_vertices: int) -> np.ndarray:
 
     Accepts a sorted EdgeArray, a (k, 2) pair array or a bare first-vertex column.
     """
-    if isinstance(sorted_edges, EdgeArray):
+    if hasattr(sorted_edges, "edges"):  # an EdgeArray (ours or the reference's)
         sorted_edges = sorted_edges.edges
     arr = np.asarray(sorted_edges)
     firsts = np.ascontiguousarray(arr[:, 0] if arr.ndim == 2 else arr, dtype=np.uint32)

@@ -25,7 +25,10 @@ def sha(*arrays) -> str:
     """sha256 over the arrays' bytes (streamed: no copy of multi-GB arrays)."""
     h = hashlib.sha256()
     for a in arrays:
-        mv = memoryview(np.ascontiguousarray(a)).cast("B")
+        a = np.ascontiguousarray(a)
+        if a.size == 0:
+            continue
+        mv = memoryview(a).cast("B")
         for i in range(0, len(mv), 1 << 28):
             h.update(mv[i:i + (1 << 28)])
     return h.hexdigest()

@@ -35,6 +35,8 @@ def sha(*arrays) -> str:
     h = hashlib.sha256()
     for a in arrays:
         a = np.ascontiguousarray(a)
+        if a.size == 0:
+            continue
         mv = memoryview(a).cast("B")
         for i in range(0, len(mv), 1 << 28):
             h.update(mv[i:i + (1 << 28)])

@@ -7,6 +7,9 @@ the small case, and the triangles are counted by the REFERENCE counter
 (tricount.preprocess + count_triangles).
 
     PYTHONPATH=/root/reference/pkg/src:. python tests/golden/make_rgg_golden.py
+    PYTHONPATH=/root/reference/pkg/src:. python tests/golden/make_rgg_golden.py --full
+        (adds BASELINE config 5 at full size, n = 2*10^7: the reference counter on the
+        6.4*10^8-pair oracle-generated graph, ~30 GB RAM, a few minutes on 8 cores)
 """
 from __future__ import annotations
 
@@ -45,22 +48,30 @@ def brute(n, seed, r):
     return np.concatenate(out).astype(np.uint32)
 
 
-def main():
-    cases = []
-    for n, k, seed in ((2_000, 32.0, 3), (20_000, 32.0, 0), (200_000, 32.0, 0), (2_000_000, 32.0, 0),
-                       (50_000, 200.0, 1)):
+def main(full: bool):
+    path = os.path.join(HERE, "golden_rgg.json")
+    if full:
+        cases = json.load(open(path))["rgg"]
+        params = ((20_000_000, 32.0, 0),)
+    else:
+        cases = []
+        params = ((2_000, 32.0, 3), (20_000, 32.0, 0), (200_000, 32.0, 0), (2_000_000, 32.0, 0),
+                  (50_000, 200.0, 1))
+    for n, k, seed in params:
         r = math.sqrt(k / (math.pi * n))
         pairs = oracle.rgg_pairs(n, k, seed)
         if n <= 50_000:
             assert np.array_equal(pairs, brute(n, seed, r)), n
         g = EdgeArray(pairs)
-        t = count_triangles(preprocess(g), 8)
+        del pairs
+        t = count_triangles(preprocess(g), os.cpu_count())
+        pairs = g.edges
         cases.append({"n": n, "avg_degree": k, "seed": seed, "radius": r, "pairs": int(pairs.shape[0]),
                       "num_vertices": int(g.num_vertices), "edges_sha256": sha(pairs), "triangles": int(t)})
         print(cases[-1], file=sys.stderr)
-    with open(os.path.join(HERE, "golden_rgg.json"), "w") as fh:
+    with open(path, "w") as fh:
         json.dump({"rgg": cases}, fh, indent=1)
 
 
 if __name__ == "__main__":
-    main()
+    main("--full" in sys.argv)

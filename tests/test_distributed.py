@@ -103,6 +103,9 @@ class OracleOps(Ops):
     def dst_slice(self, g, lo, hi):
         return torch.from_numpy(g["dst"][lo:hi].view(np.int32))
 
+    def dst_write(self, g, lo, t):
+        g["dst"][lo:lo + t.numel()] = t.numpy().view(np.uint32)
+
 
 def _rank_space_csr(pairs):
     """Single-process restatement of the rank-space CSR the sharded path must rebuild."""

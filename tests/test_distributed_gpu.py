@@ -93,3 +93,42 @@ def test_sharded_preprocess_one_gpu_big():
         p.join(timeout=60)
     assert {r[1] for r in res} == {want}, res
     assert all(r[4] for r in res)
+
+
+def _nccl_worker(port, q):
+    """One rank over NCCL (world 1: NCCL refuses two ranks on one GPU): the v2 collectives
+    (all-reduce of degrees / out-degrees / m, the key all-to-all, the edge_dst all-gather,
+    the count all-reduce) run on device tensors that alias library-owned HBM."""
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), TC_DEVICE="0")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        import paper_1503_00576_b200 as tcb
+        from paper_1503_00576_b200 import generators
+        from paper_1503_00576_b200.distributed import (B200Ops, count_distributed,
+                                                       count_distributed_sharded)
+        ops = B200Ops(0, comm="cuda")
+        dev = generators.rmat_device(16, 16, seed=0)
+        a = count_distributed_sharded(ops, dev, dev.num_vertices).triangles
+        b = count_distributed_sharded(ops, dev.to_host().edges, dev.num_vertices).triangles
+        c = count_distributed(ops, dev).triangles
+        ref = tcb.count_with_timings_device(dev)[0]
+        q.put((a, b, c, ref, dist.get_backend()))
+    except Exception as e:  # noqa: BLE001
+        q.put((repr(e), None, None, None, None))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_transport_world1():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(_free_port(), q))
+    p.start()
+    res = q.get(timeout=300)
+    p.join(timeout=60)
+    assert p.exitcode == 0, res
+    a, b, c, ref, backend = res
+    assert backend == "nccl"
+    assert a == b == c == ref, res

@@ -98,3 +98,38 @@ def test_rgg_oracle_matches_definition():
         assert sha(pairs) == c["edges_sha256"]
         og = oracle.preprocess(pairs)
         assert oracle.count(*og) == c["triangles"]
+
+
+@pytest.mark.parametrize("name", ["rmat_8_4_1", "rmat_10_8_7", "rmat_12_16_99", "rmat_16_76_20240616"])
+def test_fast_rmat_matches_reference(golden, name):
+    """oracle.rmat_edges (the whole reference rmat loop in C, used for s23-s26 and by the
+    reference arm of bench.py) == the reference generator's output, byte for byte."""
+    rec = golden["graphs"][name]
+    e = oracle.rmat_edges(rec["scale"], rec["edge_factor"], seed=rec["seed"])
+    assert sha(e) == rec["edges_sha256"]
+
+
+def test_fast_rmat_matches_reference_s20_s22(golden_big):
+    for scale in (20, 22):
+        rec = golden_big[f"rmat_{scale}_16_0"]
+        assert sha(oracle.rmat_edges(scale, 16, seed=0)) == rec["edges_sha256"], scale
+
+
+def test_fast_rmat_matches_reference_s23(golden_huge):
+    """s23 (m = 2^27, 2 GB of pairs; ~20 s): the reference's own s23 output, and the oracle's
+    CSR + count of it == the reference's (the default GPU schedule turns v-major on here)."""
+    rec = golden_huge["rmat_23_16_0"]
+    e = oracle.rmat_edges(23, 16, seed=0)
+    assert sha(e) == rec["edges_sha256"]
+    src, dst, off = oracle.preprocess(e, num_vertices=rec["n"])
+    del e
+    assert sha(src, dst, off) == rec["csr_sha256"]
+    assert oracle.count(src, dst, off) == rec["triangles"]
+
+
+def test_headline_golden_consistent(golden_s26, golden_big, golden_huge):
+    """The s26 record (full oracle run on the GPU host) continues the reference-produced
+    s20-s24 series: same generator parameters, n and m per scale, triangles growing."""
+    assert golden_s26["m"] == 16 << 26 and golden_s26["pairs"] == 32 << 26
+    assert golden_s26["triangles"] == 51_563_396_809
+    assert golden_huge["rmat_24_16_0"]["triangles"] < golden_s26["triangles"]
