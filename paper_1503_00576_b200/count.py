@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -88,12 +89,30 @@ def warm_kernel() -> None:
     _lib.lib()
 
 
+_foreign = weakref.WeakKeyDictionary()
+
+
 def _device(og):
     """The device graph of an OrientedGraph -- ours (cached on it), or any object with the
     reference OrientedGraph's arrays (graph.py:146-193), e.g. a tricount.graph.OrientedGraph
-    handed over by reference code: uploaded for the call."""
+    handed over by reference code: uploaded once and cached for the object's lifetime
+    (its arrays are read-only).  Callers keep the returned handle alive for the call."""
     if isinstance(og, OrientedGraph):
         return og.device()
+    try:
+        dev = _foreign.get(og)
+    except TypeError:  # not weak-referenceable: upload for this call only
+        dev = None
+    if dev is None:
+        dev = _upload_foreign(og)
+        try:
+            _foreign[og] = dev
+        except TypeError:
+            pass
+    return dev
+
+
+def _upload_foreign(og):
     from .graph import DeviceGraph
     src = np.ascontiguousarray(og.edge_src, dtype=np.uint32)
     dst = np.ascontiguousarray(og.edge_dst, dtype=np.uint32)
@@ -107,7 +126,8 @@ def _count_bounds(og: OrientedGraph, bounds, algo: int):
     b = np.ascontiguousarray(bounds, dtype=np.int64)
     out = ctypes.c_uint64()
     t = _lib.TcTimes()
-    _lib.check(_lib.lib().tc_count_partitioned(_device(og).handle, _lib.ptr(b), b.size - 1, algo,
+    dev = _device(og)  # keeps the device graph alive across the call
+    _lib.check(_lib.lib().tc_count_partitioned(dev.handle, _lib.ptr(b), b.size - 1, algo,
                                                ctypes.byref(out), ctypes.byref(t)))
     return int(out.value), t
 
@@ -118,7 +138,8 @@ def count_device(og: OrientedGraph, lo: int = 0, hi: int | None = None,
     hi = og.m_dir if hi is None else int(hi)
     out = ctypes.c_uint64()
     t = _lib.TcTimes()
-    _lib.check(_lib.lib().tc_count(_device(og).handle, int(lo), hi, algo, ctypes.byref(out),
+    dev = _device(og)
+    _lib.check(_lib.lib().tc_count(dev.handle, int(lo), hi, algo, ctypes.byref(out),
                                    ctypes.byref(t)))
     return int(out.value), t
 
@@ -144,21 +165,24 @@ def count_partitioned(g: OrientedGraph, plan: PartitionPlan,
 def intersect_count(g: OrientedGraph, u: int, v: int) -> int:
     """|adj(u) ∩ adj(v)| over the oriented lists (count.py:102-136)."""
     out = ctypes.c_uint64()
-    _lib.check(_lib.lib().tc_intersect_count(_device(g).handle, int(u), int(v), ctypes.byref(out)))
+    dev = _device(g)
+    _lib.check(_lib.lib().tc_intersect_count(dev.handle, int(u), int(v), ctypes.byref(out)))
     return int(out.value)
 
 
 def merge_work(g: OrientedGraph) -> int:
     """W = sum over oriented edges of d+(u) + d+(v) (SURVEY.md §8(d) roofline numerator)."""
     out = ctypes.c_uint64()
-    _lib.check(_lib.lib().tc_merge_work(_device(g).handle, ctypes.byref(out)))
+    dev = _device(g)
+    _lib.check(_lib.lib().tc_merge_work(dev.handle, ctypes.byref(out)))
     return int(out.value)
 
 
 def schedule_bytes(g: OrientedGraph) -> dict:
     """Compulsory HBM bytes of the full-count schedule, by kernel class (tc_schedule_bytes)."""
     out = np.zeros(5, dtype=np.uint64)
-    _lib.check(_lib.lib().tc_schedule_bytes(_device(g).handle, _lib.ptr(out)))
+    dev = _device(g)
+    _lib.check(_lib.lib().tc_schedule_bytes(dev.handle, _lib.ptr(out)))
     keys = ("vmajor", "umajor_heavy", "light", "per_edge", "heavy_staging")
     return {k: int(v) for k, v in zip(keys, out)}
 

@@ -872,6 +872,7 @@ const OptionName kOptionNames[] = {
     {"shard_model", &Options::shard_model}, {"shard_ovh", &Options::shard_ovh},
     {"shard_ucap", &Options::shard_ucap},   {"dense_ranks", &Options::dense_ranks},
     {"bucket", &Options::bucket},           {"count_stats", &Options::count_stats},
+    {"hubpack", &Options::hubpack},
 };
 }  // namespace
 

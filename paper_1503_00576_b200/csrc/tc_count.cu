@@ -275,6 +275,88 @@ __device__ __forceinline__ uint32_t sweep_bits(const uint32_t *__restrict__ dst,
     return found;
 }
 
+// Hub items packed to 18 bits (2.25 B per item instead of 4): position p of edge_dst holds
+// r = dst[p] - hz as lo16[p] (u16) plus 2 high bits in hi2[p / 4] (bits 2i..2i+1 for the i-th
+// item of the aligned group of 4).  A 16-byte chunk of 4 items becomes one 8-byte + one
+// 1-byte load.  Only positions holding hub items (>= hz) are meaningful; the sweeps read
+// lists whose valid items are all hub items (suffixes after a hub head).
+struct HubPack {
+    const uint16_t *lo16;
+    const uint8_t *hi2;
+};
+
+template <int U>
+__device__ __forceinline__ uint32_t sweep_bits18(const HubPack hp, const EdgeTable<uint32_t> &et,
+                                                 uint32_t nwin, uint32_t c0, uint32_t c1,
+                                                 const uint32_t *bitmap) {
+    const unsigned lane = lane_id();
+    uint32_t k = 0;
+    {
+        const uint32_t c = c0 + lane < c1 ? c0 + lane : c1 - 1;
+        uint32_t a = 0, b = nwin;
+        while (b - a > 1) {
+            const uint32_t mid = (a + b) >> 1;
+            if (et.cst[mid] <= c) a = mid; else b = mid;
+        }
+        k = a;
+    }
+    uint32_t nextb = et.cst[k + 1];
+    uint32_t cb = et.cb[k], lo = et.vs[k];
+    uint32_t span = et.ve[k] - lo;
+    uint32_t found = 0;
+    for (uint32_t base = c0; base < c1; base += 32 * U) {
+        uint2 q[U];
+        uint32_t hb[U], rel[U], sp[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            uint32_t c = base + j * 32 + lane;
+            const bool live = c < c1;
+            c = live ? c : c1 - 1;
+            if (c >= nextb) {
+                do { nextb = et.cst[++k + 1]; } while (c >= nextb);
+                cb = et.cb[k];
+                lo = et.vs[k];
+                span = et.ve[k] - lo;
+            }
+            const uint32_t p = cb + 4 * c;
+            q[j] = __ldg(reinterpret_cast<const uint2 *>(hp.lo16 + p));
+            hb[j] = __ldg(hp.hi2 + (p >> 2));
+            rel[j] = p - lo;
+            sp[j] = live ? span : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const uint32_t r4[4] = {(q[j].x & 0xffffu) | ((hb[j] & 3u) << 16),
+                                    (q[j].x >> 16) | (((hb[j] >> 2) & 3u) << 16),
+                                    (q[j].y & 0xffffu) | (((hb[j] >> 4) & 3u) << 16),
+                                    (q[j].y >> 16) | (((hb[j] >> 6) & 3u) << 16)};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t ok = (rel[j] + i < sp[j]) ? 1u : 0u;
+                const uint32_t r = ok ? r4[i] : 0u;
+                found += (bitmap[r >> 5] >> (r & 31)) & ok;
+            }
+        }
+    }
+    return found;
+}
+
+// Builds the packed hub representation of edge_dst: one thread per aligned group of 4.
+__global__ void __launch_bounds__(256) k_pack_hub(const uint32_t *__restrict__ dst, uint64_t m, uint32_t hz,
+                                                  uint16_t *__restrict__ lo16, uint8_t *__restrict__ hi2) {
+    const uint64_t ng = (m + 3) / 4;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += stride) {
+        const uint4 w = __ldg(reinterpret_cast<const uint4 *>(dst) + g);  // dst is padded
+        const uint32_t r0 = w.x >= hz ? w.x - hz : 0u, r1 = w.y >= hz ? w.y - hz : 0u;
+        const uint32_t r2 = w.z >= hz ? w.z - hz : 0u, r3 = w.w >= hz ? w.w - hz : 0u;
+        reinterpret_cast<uint2 *>(lo16)[g] =
+            make_uint2((r0 & 0xffffu) | (r1 << 16), (r2 & 0xffffu) | (r3 << 16));
+        hi2[g] = (uint8_t)(((r0 >> 16) & 3u) | (((r1 >> 16) & 3u) << 2) | (((r2 >> 16) & 3u) << 4) |
+                           (((r3 >> 16) & 3u) << 6));
+    }
+}
+
 // Dense edges of a heavy source: |adj(u) ∩ adj(v)| = popcount(B_u & B_v) over the hub
 // words v can reach.  Chunk c of edge k reads 4 words of B_v at global word cb_k + 4c and
 // 4 words of the shared-memory B_u at word vs_k + 4c (both 16-byte aligned).
@@ -505,6 +587,7 @@ struct VSplit {
     uint32_t bias;                            // v-major iff bias/4 * vcost < ucost
     uint32_t lowall;                          // below hz: 0 = short suffixes only, 1 = by bytes
     const uint32_t *hubstart;
+    uint32_t packed = 0;                      // hub-head suffixes read from the 18-bit copy
 };
 
 __device__ __forceinline__ bool vmajor_edge(const VSplit &vp, uint32_t e, uint32_t eu, uint32_t v,
@@ -515,7 +598,9 @@ __device__ __forceinline__ bool vmajor_edge(const VSplit &vp, uint32_t e, uint32
     if (v >= vp.hz) {
         const uint32_t ws = ((v + 1 - vp.hz) >> 5) & ~3u;
         const bool dense = v >= vp.vt && (vp.hwp - ws) < vp.factor * (ve - vs);
-        ucost = dense ? 4 * (vp.hwp - ws) : 16 * ((ve - (vs & ~3u) + 3) >> 2);
+        ucost = dense ? 4 * (vp.hwp - ws) : (vp.packed ? 9 : 16) * ((ve - (vs & ~3u) + 3) >> 2);
+        // the suffix is read from the packed hub copy: 9 bytes per 4 items
+        if (vp.packed) return (uint64_t)(9 * ((eu - e - 1 + 3) >> 2) + 8) * vp.bias < (uint64_t)ucost * 4;
     } else {
         // below the hub zone: adj(v) goes into a per-warp cuckoo table (k_count_vlow_warp) when
         // |adj(v)| <= nhcap; longer lists run as CTA tasks (hub part as a bitmap, non-hub part
@@ -932,7 +1017,7 @@ __global__ void TC_HUB_BOUNDS(NT)
                 const uint32_t *__restrict__ dense_bits, uint32_t dense_factor, VSplit vp,
                 const RangeDev *__restrict__ rg, const uint2 *__restrict__ tasks,
                 const unsigned *__restrict__ ntasks, unsigned *__restrict__ next, uint32_t cap,
-                unsigned long long *__restrict__ total) {
+                const HubPack hp, unsigned long long *__restrict__ total) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t *bitmap = reinterpret_cast<uint32_t *>(smem);  // hwords
     uint32_t *ctab = bitmap + hwords;                        // cap slots
@@ -1041,7 +1126,8 @@ __global__ void TC_HUB_BOUNDS(NT)
                         acc += sweep_and<U>(dense_bits, et, NT, c0, c1, bm);
                     } else if (pass == 0) {
                         // hub suffixes [hubstart[v], ve): every valid item is >= hz
-                        acc += sweep_bits<U>(dst, et, NT, c0, c1, bitmap, hz);
+                        if (hp.lo16) acc += sweep_bits18<U>(hp, et, NT, c0, c1, bitmap);
+                        else acc += sweep_bits<U>(dst, et, NT, c0, c1, bitmap, hz);
                     } else if (tab_ok) {
                         acc += sweep<uint32_t, false>(dst, et, NT, c0, c1,
                                                       [&](uint32_t w, uint32_t) { return ck.contains(w); });
@@ -1334,7 +1420,7 @@ __global__ void TC_VM_BOUNDS(NT)
                    const uint2 *__restrict__ in_e,
                    const uint2 *__restrict__ tasks, const uint32_t *__restrict__ tlo,
                    const uint32_t *__restrict__ ntasks, unsigned *__restrict__ next,
-                   unsigned long long *__restrict__ total) {
+                   const HubPack hp, unsigned long long *__restrict__ total) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t *bitmap = reinterpret_cast<uint32_t *>(smem);  // hwp words
     uint32_t *ctab = bitmap + hwp;                           // cap slots (v below hz)
@@ -1423,8 +1509,11 @@ __global__ void TC_VM_BOUNDS(NT)
                         const bool b = ((lds32(bm + 4 * min(r >> 5, hwp - 1)) >> (r & 31)) & 1u) != 0u;
                         return w >= hz ? b : sorted_contains(dst + vs, nh, w);
                     });
+                } else if (hp.lo16) {
+                    // suffix items exceed v >= hz: every valid item is a hub item, read from
+                    // the 18-bit packed copy (2.25 B per item)
+                    acc += sweep_bits18<U>(hp, et, NT, c0, c1, bitmap);
                 } else {
-                    // suffix items exceed v >= hz: every valid item is a hub item
                     acc += sweep_bits<U>(dst, et, NT, c0, c1, bitmap, hz);
                 }
             }
@@ -1546,10 +1635,19 @@ static uint32_t dense_factor_env() {
     return (uint32_t)opts().dense_factor;
 }
 
+// The v-major split every kernel of one count evaluates (the same predicate everywhere, so
+// each edge is counted exactly once).
+static VSplit make_vsplit(const DeviceGraph &g, bool vmajor) {
+    VSplit vp{vmajor ? vzone_start(g) : 0xffffffffu, g.hz, g.vt, g.hwp, dense_factor_env(), kVNonHubCap,
+              vm_bias_env(), vm_lowall_env(), g.hubstart};
+    vp.packed = vmajor && opts().hubpack ? 1u : 0u;
+    return vp;
+}
+
 template <int NT>
 int launch_hub(const DeviceGraph &g, const RangeDev *rg, const uint2 *tasks, const unsigned *ntasks,
-               unsigned *next, uint32_t cap, bool vmajor, int share, unsigned long long *d_total,
-               cudaStream_t s) {
+               unsigned *next, uint32_t cap, bool vmajor, int share, HubPack hp,
+               unsigned long long *d_total, cudaStream_t s) {
     const uint32_t hwords = g.hwp;
     const size_t sm = 4 * ((size_t)hwords + cap);
     const int64_t unroll = opts().hub_unroll;
@@ -1560,11 +1658,10 @@ int launch_hub(const DeviceGraph &g, const RangeDev *rg, const uint2 *tasks, con
     per_sm = (per_sm + share - 1) / share;
     if (per_sm < 1) per_sm = 1;
     const uint32_t dense_factor = dense_factor_env();
-    const VSplit vp{vmajor ? vzone_start(g) : 0xffffffffu, g.hz, g.vt, g.hwp, dense_factor, kVNonHubCap,
-                    vm_bias_env(), vm_lowall_env(), g.hubstart};
+    const VSplit vp = make_vsplit(g, vmajor);
     kern<<<kSMs * per_sm, NT, sm, s>>>(g.dst, g.off32, g.hubstart, g.hz, hwords, g.vt, g.dense_off,
                                        g.dense_bits, dense_factor, vp, rg, tasks, ntasks, next, cap,
-                                       d_total);
+                                       vp.packed ? hp : HubPack{nullptr, nullptr}, d_total);
     TC_LAUNCHED();
     return 0;
 }
@@ -1723,6 +1820,8 @@ struct VmajorState {
     uint2 *in_e = nullptr;  // (edge, off[u+1]) per indexed in-edge
     uint2 *big = nullptr;   // CTA tasks of long-list heads below hz
     uint32_t *defer = nullptr;  // warp tasks whose cuckoo build failed (binary-search rerun)
+    uint16_t *lo16 = nullptr;   // packed hub copy of edge_dst (HubPack)
+    uint8_t *hi2 = nullptr;
     bool capl = false;      // capacity layout used (overflow flag in next[2])
     unsigned *next = nullptr;
     uint2 *tasks = nullptr;
@@ -1761,7 +1860,7 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
     TC_CUDA(cudaEventRecord(st->e0, s));
     if (s2 != s) TC_CUDA(cudaStreamWaitEvent(s2, st->e0, 0));
     const unsigned grid = grid_for(span, 256 * kVinPP, kSMs * 8);
-    const VSplit vp{z0, g.hz, g.vt, g.hwp, dense_factor_env(), kVNonHubCap, vm_bias_env(), vm_lowall_env(), g.hubstart};
+    const VSplit vp = make_vsplit(g, true);
     const uint32_t *startp = g.vin_cap;
     if (!capl) {
         k_vin_pass<false><<<grid, 256, 0, s2>>>(g.src, g.dst, g.off32, rg, vp, nullptr, st->cnt, nullptr,
@@ -1778,6 +1877,17 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
     k_vin_tasks<<<grid_for(nh, 256, kSMs * 4), 256, 0, s2>>>(startp, st->tstart, nh, st->tasks, g.off32, z0, hb,
                                                              kVNonHubCap, st->big, st->next + 3);
     TC_LAUNCHED();
+    HubPack hp{nullptr, nullptr};
+    if (vp.packed) {
+        const uint64_t ng = (g.m + 3) / 4;
+        TC_CHECK(dalloc_t(&st->lo16, 4 * ng + 16, s2));
+        TC_CHECK(dalloc_t(&st->hi2, ng + 16, s2));
+        TC_CUDA(cudaMemsetAsync(st->lo16 + 4 * ng, 0, 32, s2));
+        TC_CUDA(cudaMemsetAsync(st->hi2 + ng, 0, 16, s2));
+        k_pack_hub<<<grid_for(ng, 256, kSMs * 8), 256, 0, s2>>>(g.dst, g.m, g.hz, st->lo16, st->hi2);
+        TC_LAUNCHED();
+        hp = HubPack{st->lo16, st->hi2};
+    }
     constexpr int NT = 256;
     auto kern = k_count_vmajor<NT, 4>;
     const uint32_t cap = 0;  // heads below hz run in k_count_vlow_warp
@@ -1813,13 +1923,13 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
         if (bper < 1) bper = 1;
         kern<<<kSMs * bper, NT, bsm, s2>>>(g.src, g.dst, g.off32, g.hubstart, z0, g.hz, g.hwp, bcap, startp,
                                            st->cnt, st->in_e, st->big, st->next + 4, st->next + 3, st->next + 5,
-                                           d_total);
+                                           hp, d_total);
         TC_LAUNCHED();
     }
     TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     kern<<<kSMs * per_sm, NT, sm, s2>>>(g.src, g.dst, g.off32, g.hubstart, z0, g.hz, g.hwp, cap,
                                         startp, st->cnt, st->in_e, st->tasks, st->tstart + hb, st->tstart + nh,
-                                        st->next, d_total);
+                                        st->next, hp, d_total);
     TC_LAUNCHED();
     TC_CUDA(cudaEventRecord(st->e1, s2));
     TC_CUDA(cudaEventRecord(st->done, s2));
@@ -1851,6 +1961,8 @@ int vmajor_finish(VmajorState *st, cudaStream_t s, CountStats *stats, bool *over
     dfree(st->big, s);
     dfree(st->defer, s);
     dfree(st->next, s);
+    dfree(st->lo16, s);
+    dfree(st->hi2, s);
     *st = VmajorState{};
     return 0;
 }
@@ -1970,8 +2082,7 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
         // latency-bound: one warp per task (without it the CTA bitmap kernel wins)
         if (c <= (midwarp >= 2 ? 1 : 0) && midwarp && vmajor && sizeof(OffT) == 4 && g.rank_space &&
             g.hubstart) {
-            const VSplit vp{vmajor ? vzone_start(g) : 0xffffffffu, g.hz, g.vt, g.hwp, dense_factor_env(),
-                            kVNonHubCap, vm_bias_env(), vm_lowall_env(), g.hubstart};
+            const VSplit vp = make_vsplit(g, vmajor);
             // cuckoo load <= 1/3: 6 KB per warp, 4 CTAs (32 warps) per SM (load 1/4: 3 CTAs, +12 %)
             if (c == 0) TC_CHECK((launch_mid<kMidWarps, kMidSlots, 3>(g, vp, rg, tasks[c], nt_c, next_c, d_total, s)));
             else TC_CHECK((launch_mid<4, 3 * 2048, 3>(g, vp, rg, tasks[c], nt_c, next_c, d_total, s)));
@@ -1979,8 +2090,10 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
         }
         if (sizeof(OffT) == 4 && g.rank_space && g.hubstart && hub_sm <= 200 * 1024) {
             const int ntc = c == 2 ? 512 : 256;
-            rc = ntc == 512 ? launch_hub<512>(g, rg, tasks[c], nt_c, next_c, hub_cap, vmajor, share, d_total, s)
-                            : launch_hub<256>(g, rg, tasks[c], nt_c, next_c, hub_cap, vmajor, share, d_total, s);
+            // the packed copy is built on the v-major stream: usable once that phase is joined
+            const HubPack hp = conc ? HubPack{nullptr, nullptr} : HubPack{vst.lo16, vst.hi2};
+            rc = ntc == 512 ? launch_hub<512>(g, rg, tasks[c], nt_c, next_c, hub_cap, vmajor, share, hp, d_total, s)
+                            : launch_hub<256>(g, rg, tasks[c], nt_c, next_c, hub_cap, vmajor, share, hp, d_total, s);
             if (rc) return rc;
             continue;
         }
@@ -2012,9 +2125,7 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
                                    : k_count_light_tpe<OffT, false, false, false>;
         kern<<<kSMs * 8, 256, 0, s>>>(g.src, g.dst, off, rg, g.hz, hub ? g.vt : 0xffffffffu,
                                       g.dense_off, g.dense_bits, g.dense_words,
-                                      VSplit{vmajor ? vzone_start(g) : 0xffffffffu, g.hz, g.vt, g.hwp,
-                                             dense_factor_env(), kVNonHubCap, vm_bias_env(), vm_lowall_env(), g.hubstart},
-                                      d_total);
+                                      make_vsplit(g, vmajor), d_total);
     } else {
         const bool hub = g.rank_space && g.hubstart;
         const uint32_t hwords = hub ? (uint32_t)((g.n - g.hz + 31) / 32) + 1 : 0u;
@@ -2189,12 +2300,13 @@ __global__ void __launch_bounds__(256)
         if (e + 1 >= eu || vs >= ve) continue;  // no triangle can close: every kernel skips it
         const uint32_t sfx = eu - (uint32_t)e - 1;
         if (vmajor_edge(vp, (uint32_t)e, eu, v, vs, ve)) {
-            b[0] += 4ull * sfx + 8;
+            b[0] += (vp.packed && v >= vp.hz ? 9ull * ((sfx + 3) / 4) : 4ull * sfx) + 8;
         } else if (du > (uint32_t)kLightMax) {
             uint64_t x = 4ull * dv;
             if (hub && v >= vp.hz) {
                 const uint32_t ws = ((v + 1 - vp.hz) >> 5) & ~3u;
                 if (v >= vp.vt && (vp.hwp - ws) < vp.factor * dv) x = 4ull * (vp.hwp - ws);
+                else if (vp.packed) x = 9ull * ((dv + 3) / 4);
             }
             b[1] += x;
         } else {
@@ -2220,8 +2332,7 @@ int schedule_bytes_dev(const DeviceGraph &g, uint64_t out[5], cudaStream_t s) {
     TC_CHECK(dalloc_t(&d, 5, s));
     TC_CUDA(cudaMemsetAsync(d, 0, 5 * sizeof(unsigned long long), s));
     const bool vm = vmajor_schedule(g);
-    const VSplit vp{vm ? vzone_start(g) : 0xffffffffu, g.hz, g.vt, g.hwp, dense_factor_env(), kVNonHubCap,
-                    vm_bias_env(), vm_lowall_env(), g.hubstart};
+    const VSplit vp = make_vsplit(g, vm);
     if (g.m) {
         k_schedule_bytes<<<grid_for(g.m, 256, kSMs * 16), 256, 0, s>>>(g.src, g.dst, g.off32, g.m, vp,
                                                                       g.dense_bits != nullptr, d);

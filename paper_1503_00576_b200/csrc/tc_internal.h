@@ -63,6 +63,7 @@ struct Options {
     int64_t dense_ranks = 1 << 17;  // dense-hub bitmaps for the top ranks
     int64_t bucket = 1;          // rank-space preprocess: bucket scatter + segmented sort
     int64_t count_stats = 0;     // tc_count_with_timings fills the per-kernel-class fields
+    int64_t hubpack = 1;         // v-major hub-head suffixes read from an 18-bit packed copy
 };
 Options &opts();
 

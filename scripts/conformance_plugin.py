@@ -18,9 +18,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
 
+import importlib  # noqa: E402
+
 import tricount  # noqa: E402  (the reference package)
-from paper_1503_00576_b200 import count as _count  # noqa: E402
-from paper_1503_00576_b200 import preprocess as _preprocess  # noqa: E402
+
+# the package re-exports functions named like its modules: import the modules explicitly
+_count = importlib.import_module("paper_1503_00576_b200.count")
+_preprocess = importlib.import_module("paper_1503_00576_b200.preprocess")
 
 sys.modules["tricount.count"] = _count
 sys.modules["tricount.preprocess"] = _preprocess

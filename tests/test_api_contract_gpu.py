@@ -185,3 +185,32 @@ def test_options_api():
     assert _lib.get_option("vmajor") == -1 and _lib.get_option("light") == -1
     with pytest.raises(ValueError):
         _lib.set_option("no_such_option", 1)
+
+
+def test_foreign_oriented_graph_objects():
+    """An object carrying the reference OrientedGraph's arrays (a tricount.graph.OrientedGraph
+    handed over by reference code, graph.py:146-193) is accepted by every counting entry
+    point; its device copy lives as long as the object (reference test_count.py:39-45)."""
+    import gc
+
+    class RefOG:  # duck-typed stand-in: frozen arrays + m_dir / num_vertices
+        def __init__(self, src, dst, off):
+            self.edge_src, self.edge_dst, self.node_offsets = src, dst, off
+            self.m_dir, self.num_vertices = int(dst.size), int(off.size) - 1
+
+    src = np.array([0, 0, 0, 0, 1, 1, 1], np.uint32)
+    dst = np.array([2, 4, 6, 8, 4, 8, 9], np.uint32)
+    off = np.array([0, 4, 7, 7, 7, 7, 7, 7, 7, 7, 7], np.int64)
+    for _ in range(3):
+        og = RefOG(src, dst, off)
+        assert tcb.intersect_count(og, 0, 1) == 2
+        assert tcb.count_triangles(og) == 0
+        assert tcb.count_partitioned(og, tcb.PartitionPlan.even(2, og.m_dir), 1) == 0
+        del og
+        gc.collect()
+    pairs = oracle.symmetrize(oracle.rmat_pairs(10, 8, seed=7))
+    s, d, o = oracle.preprocess(pairs)
+    og = RefOG(s, d, o)
+    assert tcb.count_triangles(og) == oracle.count(s, d, o)
+    assert sum(tcb.intersect_count(og, int(u), int(v)) for u, v in zip(s[:200], d[:200])) == \
+        sum(oracle.intersect_count(d, o, int(u), int(v)) for u, v in zip(s[:200], d[:200]))
