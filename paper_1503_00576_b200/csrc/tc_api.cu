@@ -4,17 +4,27 @@
 #include <string.h>
 
 #include <atomic>
+#include <condition_variable>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "../../include/tricount_b200.h"
 #include "tc_common.cuh"
 #include "tc_internal.h"
 
+// A device OrientedGraph.  `g` is the reference-id CSR (reference graph.py:146-193): what
+// downloads, ranged counts and partition bounds see.  `rank` is the count-ready rank-space
+// copy.  tc_preprocess builds the rank copy directly (the fused path's preprocessing) and
+// keeps `id_of_rank`; `g` is then materialised from it on first use (ref_ready false) --
+// the same arrays the reference produces, built only when something asks for them.
 struct tc_graph {
     tc::DeviceGraph g;
     tc::DeviceGraph *rank = nullptr;  // cached rank-space copy (full-range counts)
     bool no_rank = false;             // not rank-orientable: full counts use the original ids
+    bool ref_ready = true;            // g's arrays exist
+    uint32_t *id_of_rank = nullptr;   // rank -> reference id (graphs from tc_preprocess)
 };
 
 namespace tc {
@@ -115,6 +125,123 @@ static int reserve_pool(uint64_t bytes) {
     return 0;
 }
 
+// ---- host -> device copies of caller buffers ---------------------------------------------
+// Pinned (page-locked or cudaHostRegister'ed) buffers go straight to the copy engine.  An
+// ordinary pageable buffer -- a plain numpy array, what a reference EdgeArray holds -- would
+// go through the driver's single-threaded staging (~10 GB/s measured); instead it is
+// streamed through kStageBufs pinned staging buffers: host threads copy chunk k into one
+// while the copy engine moves chunk k-1 out of another (PCIe rate when the host copy keeps up).
+constexpr int kStageBufs = 3;
+constexpr size_t kStageBytes = 128ull << 20;
+void *g_stage[kStageBufs] = {nullptr};
+cudaEvent_t g_stage_ev[kStageBufs] = {nullptr};
+
+static bool is_pageable(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
+// A small persistent pool of host threads for the staged copies (created on first use).
+class CopyPool {
+  public:
+    explicit CopyPool(int n) : n_(n) {
+        for (int t = 0; t < n_; ++t) th_.emplace_back([this, t] { run(t); });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto &t : th_) t.join();
+    }
+    void copy(void *dst, const void *src, size_t bytes) {
+        std::unique_lock<std::mutex> lk(mu_);
+        dst_ = (char *)dst;
+        src_ = (const char *)src;
+        bytes_ = bytes;
+        left_ = n_;
+        ++gen_;
+        cv_.notify_all();
+        done_.wait(lk, [this] { return left_ == 0; });
+    }
+
+  private:
+    void run(int t) {
+        uint64_t seen = 0;
+        for (;;) {
+            char *d;
+            const char *sp;
+            size_t b;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+                d = dst_;
+                sp = src_;
+                b = bytes_;
+            }
+            const size_t part = ((b / n_) + 4095) & ~(size_t)4095;
+            const size_t lo = part * t;
+            if (lo < b) memcpy(d + lo, sp + lo, b - lo < part ? b - lo : part);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--left_ == 0) done_.notify_one();
+        }
+    }
+    int n_;
+    std::vector<std::thread> th_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+    char *dst_ = nullptr;
+    const char *src_ = nullptr;
+    size_t bytes_ = 0;
+    int left_ = 0;
+};
+CopyPool *g_copy_pool = nullptr;
+
+static void parallel_memcpy(void *dst, const void *src, size_t bytes, int threads) {
+    if (threads <= 1 || bytes < (8u << 20)) {
+        memcpy(dst, src, bytes);
+        return;
+    }
+    if (!g_copy_pool) g_copy_pool = new CopyPool(threads);
+    g_copy_pool->copy(dst, src, bytes);
+}
+
+static int h2d(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+    if (!bytes) return 0;
+    if (bytes < (32u << 20) || !is_pageable(src)) {
+        TC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        return 0;
+    }
+    if (!g_stage[0])
+        for (int b = 0; b < kStageBufs; ++b) {
+            TC_CUDA(cudaHostAlloc(&g_stage[b], kStageBytes, cudaHostAllocDefault));
+            TC_CUDA(cudaEventCreateWithFlags(&g_stage_ev[b], cudaEventDisableTiming));
+        }
+    const unsigned hc = std::thread::hardware_concurrency();
+    const int threads = hc >= 16 ? 8 : hc >= 4 ? (int)hc / 2 : 1;
+    size_t off = 0;
+    for (int k = 0; off < bytes; ++k) {
+        const int b = k % kStageBufs;
+        const size_t len = bytes - off < kStageBytes ? bytes - off : kStageBytes;
+        TC_CUDA(cudaEventSynchronize(g_stage_ev[b]));  // the copy out of this buffer finished
+        parallel_memcpy(g_stage[b], (const char *)src + off, len, threads);
+        TC_CUDA(cudaMemcpyAsync((char *)dst + off, g_stage[b], len, cudaMemcpyHostToDevice, s));
+        TC_CUDA(cudaEventRecord(g_stage_ev[b], s));
+        off += len;
+    }
+    return 0;
+}
+
 // Peak scratch of preprocess + count, ~14 B per input pair at R-MAT s26.
 static uint64_t scratch_estimate(uint64_t npairs) { return 16ull * npairs + (256ull << 20); }
 
@@ -162,6 +289,22 @@ static int rank_copy(tc_graph *h, const DeviceGraph **out) {
         h->rank = r;
     }
     *out = h->rank;
+    return 0;
+}
+
+// The reference-id arrays of a graph whose preprocessing produced only the rank-space copy.
+// Called under the API lock.
+static int ensure_ref(tc_graph *h) {
+    if (h->ref_ready) return 0;
+    DeviceGraph g;
+    g.persistent = true;
+    int rc = derank_dev(*h->rank, h->id_of_rank, &g, g_stream);
+    if (rc) {
+        graph_release(&g, g_stream);
+        return rc;
+    }
+    h->g = g;
+    h->ref_ready = true;
     return 0;
 }
 
@@ -253,6 +396,14 @@ int tc_shutdown(void) {
     TC_API_GUARD();
     std::lock_guard<std::mutex> lk(g_mu);
     if (!g_ready) return 0;
+    for (int b = 0; b < kStageBufs; ++b) {
+        if (g_stage[b]) cudaFreeHost(g_stage[b]);
+        if (g_stage_ev[b]) cudaEventDestroy(g_stage_ev[b]);
+        g_stage[b] = nullptr;
+        g_stage_ev[b] = nullptr;
+    }
+    delete g_copy_pool;
+    g_copy_pool = nullptr;
     if (g_flush) cudaFree(g_flush);
     g_flush = nullptr;
     g_flush_bytes = 0;
@@ -286,17 +437,39 @@ int tc_preprocess_ex(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, in
     uint32_t *owned = nullptr;  // staging copy: default pool, freed at the end of the call
     if (!pairs_on_device && npairs) {
         TC_CHECK(dalloc_t(&owned, 2 * npairs, s, true));
-        TC_CUDA(cudaMemcpyAsync(owned, pairs, npairs * 8, cudaMemcpyHostToDevice, s));
+        TC_CHECK(h2d(owned, pairs, npairs * 8, s));
         dpairs = owned;
     }
     TC_CUDA(cudaEventRecord(ev.e[1], s));
     tc_graph *g = new tc_graph();
     g->g.persistent = true;
-    int rc = (flags & TC_PREPROCESS_RANK_SPACE) ? preprocess_rank_dev(dpairs, npairs, nverts, &g->g, s)
-                                               : preprocess_dev(dpairs, npairs, nverts, &g->g, s);
+    int rc;
+    if (flags & TC_PREPROCESS_RANK_SPACE) {
+        rc = preprocess_rank_dev(dpairs, npairs, nverts, &g->g, s);
+    } else if (npairs / 2 < (1ull << 32) && nverts < (1ull << 32) && opts().rank_primary) {
+        // the count-ready rank-space CSR is built (as the fused path does) and the reference-id
+        // CSR only on demand
+        g->rank = new DeviceGraph();
+        g->rank->persistent = true;
+        rc = dalloc_t(&g->id_of_rank, nverts ? nverts : 1, s, true);
+        if (!rc) rc = preprocess_rank_dev(dpairs, npairs, nverts, g->rank, s, g->id_of_rank);
+        if (!rc) {
+            g->g.m = g->rank->m;
+            g->g.n = g->rank->n;
+            g->g.max_out = g->rank->max_out;
+            g->ref_ready = false;
+        } else {
+            graph_release(g->rank, s);
+            delete g->rank;
+            g->rank = nullptr;
+        }
+    } else {
+        rc = preprocess_dev(dpairs, npairs, nverts, &g->g, s);
+    }
     if (owned) dfree(owned, s);
     if (rc) {
         graph_release(&g->g, s);
+        dfree(g->id_of_rank, s);
         delete g;
         return rc;
     }
@@ -356,8 +529,7 @@ int tc_graph_upload(const uint32_t *edge_src, const uint32_t *edge_dst,
     if (rc) return fail(rc);
     cudaError_t e = cudaSuccess;
     if (m) {
-        if (e == cudaSuccess) e = cudaMemcpyAsync(g->g.src, edge_src, m * 4, cudaMemcpyHostToDevice, s);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(g->g.dst, edge_dst, m * 4, cudaMemcpyHostToDevice, s);
+        if (h2d(g->g.src, edge_src, m * 4, s) || h2d(g->g.dst, edge_dst, m * 4, s)) return fail(-2);
     }
     if (e == cudaSuccess) e = cudaMemsetAsync(g->g.dst + m, 0, 16, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(g->g.off, node_offsets, (n + 1) * 8, cudaMemcpyHostToDevice, s);
@@ -426,6 +598,7 @@ int tc_graph_download(const tc_graph *g, uint32_t *edge_src, uint32_t *edge_dst,
     TC_API_GUARD();
     TC_CHECK(ensure());
     TC_CHECK(check_graph(g));
+    TC_CHECK(ensure_ref(const_cast<tc_graph *>(g)));
     cudaStream_t s = g_stream;
     if (g->g.m) {
         if (edge_src) TC_CUDA(cudaMemcpyAsync(edge_src, g->g.src, g->g.m * 4, cudaMemcpyDeviceToHost, s));
@@ -453,7 +626,9 @@ int tc_graph_flags(const tc_graph *g, int *flags) {
 
 int tc_graph_device_ptrs(const tc_graph *g, uint32_t **edge_src, uint32_t **edge_dst,
                          int64_t **node_offsets) {
+    TC_API_GUARD();
     TC_CHECK(check_graph(g));
+    TC_CHECK(ensure_ref(const_cast<tc_graph *>(g)));
     if (edge_src) *edge_src = g->g.src;
     if (edge_dst) *edge_dst = g->g.dst;
     if (node_offsets) *node_offsets = g->g.off;
@@ -467,6 +642,7 @@ int tc_graph_free(tc_graph *g) {
         cudaSetDevice(g_device);
         graph_release(&g->g, g_stream);
         if (g->rank) graph_release(g->rank, g_stream);
+        dfree(g->id_of_rank, g_stream);
     }
     delete g->rank;
     delete g;
@@ -483,6 +659,7 @@ int tc_count(const tc_graph *g, int64_t lo, int64_t hi, int algo, uint64_t *out,
     }
     int64_t b[2] = {lo, hi};
     const bool full = algo == TC_ALGO_AUTO && lo == 0 && (uint64_t)hi == g->g.m;
+    if (!full) TC_CHECK(ensure_ref(const_cast<tc_graph *>(g)));  // ranges are in reference edge order
     return count_ranges(g->g, full ? const_cast<tc_graph *>(g) : nullptr, b, 1, algo, out, t);
 }
 
@@ -507,6 +684,7 @@ int tc_count_partitioned(const tc_graph *g, const int64_t *bounds, int npools, i
         int64_t b[2] = {0, (int64_t)g->g.m};
         return count_ranges(g->g, const_cast<tc_graph *>(g), b, 1, algo, out, t);
     }
+    TC_CHECK(ensure_ref(const_cast<tc_graph *>(g)));
     return count_ranges(g->g, nullptr, bounds, npools, algo, out, t);
 }
 
@@ -518,6 +696,7 @@ int tc_intersect_count(const tc_graph *g, uint32_t u, uint32_t v, uint64_t *out)
         set_error("vertex id out of range");
         return -1;
     }
+    TC_CHECK(ensure_ref(const_cast<tc_graph *>(g)));
     return intersect_dev(g->g, u, v, out, g_stream);
 }
 
@@ -534,7 +713,7 @@ int tc_count_with_timings(const uint32_t *pairs, uint64_t npairs, uint64_t nvert
     uint32_t *owned = nullptr;  // staging copy: default pool, freed at the end of the call
     if (!pairs_on_device && npairs) {
         TC_CHECK(dalloc_t(&owned, 2 * npairs, s, true));
-        TC_CUDA(cudaMemcpyAsync(owned, pairs, npairs * 8, cudaMemcpyHostToDevice, s));
+        TC_CHECK(h2d(owned, pairs, npairs * 8, s));
         dpairs = owned;
     }
     TC_CUDA(cudaEventRecord(ev.e[1], s));
@@ -594,6 +773,7 @@ int tc_work_bounds(const tc_graph *g, int npools, int64_t *bounds) {
         set_error("num_pools must be >= 1");
         return -1;
     }
+    TC_CHECK(ensure_ref(const_cast<tc_graph *>(g)));  // bounds are reference edge indices
     return work_bounds_dev(g->g, npools, bounds, g_stream);
 }
 
@@ -610,7 +790,8 @@ int tc_merge_work(const tc_graph *g, uint64_t *out) {
     TC_API_GUARD();
     TC_CHECK(ensure());
     TC_CHECK(check_graph(g));
-    return merge_work_dev(g->g, out, g_stream);
+    // W is label-independent: use whichever copy exists
+    return merge_work_dev(g->ref_ready ? g->g : *g->rank, out, g_stream);
 }
 
 int tc_sort_edges(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, uint32_t *out_pairs) {
@@ -621,7 +802,7 @@ int tc_sort_edges(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, uint3
     uint32_t *din = nullptr, *dout = nullptr;
     TC_CHECK(dalloc_t(&din, 2 * npairs, s));
     TC_CHECK(dalloc_t(&dout, 2 * npairs, s));
-    TC_CUDA(cudaMemcpyAsync(din, pairs, npairs * 8, cudaMemcpyHostToDevice, s));
+    TC_CHECK(h2d(din, pairs, npairs * 8, s));
     TC_CHECK(sort_pairs_dev(din, npairs, nverts, dout, s));
     TC_CUDA(cudaMemcpyAsync(out_pairs, dout, npairs * 8, cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));
@@ -659,7 +840,7 @@ int tc_orient_and_compact(const uint32_t *pairs, uint64_t npairs, const int64_t 
     TC_CHECK(dalloc_t(&din, 2 * npairs, s));
     TC_CHECK(dalloc_t(&dout, 2 * npairs, s));
     TC_CHECK(dalloc_t(&ddeg, n ? n : 1, s));
-    TC_CUDA(cudaMemcpyAsync(din, pairs, npairs * 8, cudaMemcpyHostToDevice, s));
+    TC_CHECK(h2d(din, pairs, npairs * 8, s));
     if (n) TC_CUDA(cudaMemcpyAsync(ddeg, degrees, n * 8, cudaMemcpyHostToDevice, s));
     uint64_t k = 0;
     TC_CHECK(orient_compact_dev(din, npairs, ddeg, n, dout, &k, s));
@@ -695,7 +876,7 @@ static int with_device_pairs(const uint32_t *pairs, uint64_t npairs, int on_devi
     *owned = nullptr;
     if (!on_device && npairs) {
         TC_CHECK(dalloc_t(owned, 2 * npairs, g_stream, true));
-        TC_CUDA(cudaMemcpyAsync(*owned, pairs, npairs * 8, cudaMemcpyHostToDevice, g_stream));
+        TC_CHECK(h2d(*owned, pairs, npairs * 8, g_stream));
         *dp = *owned;
     }
     return 0;
@@ -872,7 +1053,7 @@ const OptionName kOptionNames[] = {
     {"shard_model", &Options::shard_model}, {"shard_ovh", &Options::shard_ovh},
     {"shard_ucap", &Options::shard_ucap},   {"dense_ranks", &Options::dense_ranks},
     {"bucket", &Options::bucket},           {"count_stats", &Options::count_stats},
-    {"hubpack", &Options::hubpack},
+    {"hubpack", &Options::hubpack},         {"rank_primary", &Options::rank_primary},
 };
 }  // namespace
 

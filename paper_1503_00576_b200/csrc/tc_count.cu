@@ -588,6 +588,7 @@ struct VSplit {
     uint32_t lowall;                          // below hz: 0 = short suffixes only, 1 = by bytes
     const uint32_t *hubstart;
     uint32_t packed = 0;                      // hub-head suffixes read from the 18-bit copy
+    uint32_t packed_cost = 0;                 // the per-edge choice charges packed bytes
 };
 
 __device__ __forceinline__ bool vmajor_edge(const VSplit &vp, uint32_t e, uint32_t eu, uint32_t v,
@@ -598,9 +599,9 @@ __device__ __forceinline__ bool vmajor_edge(const VSplit &vp, uint32_t e, uint32
     if (v >= vp.hz) {
         const uint32_t ws = ((v + 1 - vp.hz) >> 5) & ~3u;
         const bool dense = v >= vp.vt && (vp.hwp - ws) < vp.factor * (ve - vs);
-        ucost = dense ? 4 * (vp.hwp - ws) : (vp.packed ? 9 : 16) * ((ve - (vs & ~3u) + 3) >> 2);
+        ucost = dense ? 4 * (vp.hwp - ws) : (vp.packed_cost ? 9 : 16) * ((ve - (vs & ~3u) + 3) >> 2);
         // the suffix is read from the packed hub copy: 9 bytes per 4 items
-        if (vp.packed) return (uint64_t)(9 * ((eu - e - 1 + 3) >> 2) + 8) * vp.bias < (uint64_t)ucost * 4;
+        if (vp.packed_cost) return (uint64_t)(9 * ((eu - e - 1 + 3) >> 2) + 8) * vp.bias < (uint64_t)ucost * 4;
     } else {
         // below the hub zone: adj(v) goes into a per-warp cuckoo table (k_count_vlow_warp) when
         // |adj(v)| <= nhcap; longer lists run as CTA tasks (hub part as a bitmap, non-hub part
@@ -1641,6 +1642,7 @@ static VSplit make_vsplit(const DeviceGraph &g, bool vmajor) {
     VSplit vp{vmajor ? vzone_start(g) : 0xffffffffu, g.hz, g.vt, g.hwp, dense_factor_env(), kVNonHubCap,
               vm_bias_env(), vm_lowall_env(), g.hubstart};
     vp.packed = vmajor && opts().hubpack ? 1u : 0u;
+    vp.packed_cost = vmajor && opts().hubpack == 1 ? 1u : 0u;  // 2: packed reads, 4-byte costs
     return vp;
 }
 

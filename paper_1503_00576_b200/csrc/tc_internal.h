@@ -64,6 +64,7 @@ struct Options {
     int64_t bucket = 1;          // rank-space preprocess: bucket scatter + segmented sort
     int64_t count_stats = 0;     // tc_count_with_timings fills the per-kernel-class fields
     int64_t hubpack = 1;         // v-major hub-head suffixes read from an 18-bit packed copy
+    int64_t rank_primary = 1;    // tc_preprocess builds the rank-space CSR, reference ids lazily
 };
 Options &opts();
 
@@ -188,9 +189,12 @@ int finalize_graph_dev(DeviceGraph *g, cudaStream_t s);
 // Full reference preprocess on device-resident pairs (reference preprocess.py:74-84).
 int preprocess_dev(const uint32_t *pairs, uint64_t npairs, uint64_t n, DeviceGraph *out,
                    cudaStream_t s);
-// The same pipeline producing the rank-space oriented CSR (+ hubstart) directly.
+// The same pipeline producing the rank-space oriented CSR (+ hubstart) directly; with
+// id_of_rank (u32[n], caller-allocated) also the inverse relabelling.
 int preprocess_rank_dev(const uint32_t *pairs, uint64_t npairs, uint64_t n, DeviceGraph *out,
-                        cudaStream_t s);
+                        cudaStream_t s, uint32_t *id_of_rank = nullptr);
+// Reference-id CSR of a preprocess_rank_dev graph (exact inverse relabelling + sort).
+int derank_dev(const DeviceGraph &r, const uint32_t *id_of_rank, DeviceGraph *out, cudaStream_t s);
 // Distributed preprocessing steps (tc_preprocess.cu).
 int dist_degrees_dev(const uint32_t *pairs, uint64_t npairs, uint64_t n, uint32_t *deg, cudaStream_t s);
 int dist_orient_dev(const uint32_t *pairs, uint64_t npairs, uint64_t n, const uint32_t *deg,

@@ -382,6 +382,11 @@ __global__ void __launch_bounds__(256) k_indeg(const uint32_t *__restrict__ dst,
     }
 }
 
+__global__ void k_invert_perm(const uint32_t *__restrict__ perm, uint64_t n, uint32_t *__restrict__ inv) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) inv[perm[i]] = (uint32_t)i;
+}
+
 __global__ void k_relabel_keys(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
                                uint64_t m, const uint32_t *__restrict__ rank, int vb,
                                uint64_t *__restrict__ keys, uint32_t *__restrict__ bad) {
@@ -1192,7 +1197,7 @@ static int bucket_csr_dev(const uint64_t *keys, uint64_t m, uint64_t n, int vb, 
 }
 
 int preprocess_rank_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, DeviceGraph *out,
-                        cudaStream_t s) {
+                        cudaStream_t s, uint32_t *id_of_rank) {
     const uint2 *pairs = reinterpret_cast<const uint2 *>(pairs_u32);
     if (n >= (1ull << 32) || npairs / 2 >= (1ull << 32)) {
         set_error("rank-space preprocessing needs num_vertices < 2^32 and m < 2^32");
@@ -1271,6 +1276,10 @@ int preprocess_rank_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, 
         dfree(deg_by_rank, s);
     }
     TC_CUDA(cudaMemcpyAsync(&out->max_out, scratch + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    if (id_of_rank && n) {  // the inverse of the relabelling (lazy reference-id CSR)
+        k_invert_perm<<<grid_for(n, 256, kSMs * 8), 256, 0, s>>>(rank, n, id_of_rank);
+        TC_LAUNCHED();
+    }
     dfree(deg, s);
     dfree(rank, s);
     dfree(hist, s);
@@ -1279,6 +1288,42 @@ int preprocess_rank_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, 
     dfree(alt, s);
     dfree(scratch, s);
     TC_CUDA(cudaStreamSynchronize(s));
+    return 0;
+}
+
+// The reference-id CSR of a rank-space graph from preprocess_rank_dev (its exact relabelling:
+// same orientation, ranks replaced by ids): keys (id(u) << vb) | id(v), radix sorted, node
+// array -- the arrays reference preprocess.py:74-84 returns, built only when asked for.
+int derank_dev(const DeviceGraph &r, const uint32_t *id_of_rank, DeviceGraph *out, cudaStream_t s) {
+    const uint64_t n = r.n, m = r.m;
+    const int vb = n > 1 ? bits_for(n - 1) : 1;
+    const RadixPlan plan = make_radix_plan(2 * vb);
+    uint32_t *hist = nullptr, *scratch = nullptr;
+    uint64_t *keys = nullptr, *alt = nullptr;
+    TC_CHECK(dalloc_t(&scratch, 4, s));
+    TC_CHECK(dalloc_t(&hist, kMaxPasses * kRadix, s));
+    TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
+    TC_CUDA(cudaMemsetAsync(scratch, 0, 4 * sizeof(uint32_t), s));
+    TC_CHECK(dalloc_t(&keys, m ? m : 1, s));
+    TC_CHECK(dalloc_t(&alt, m ? m : 1, s));
+    if (m) {
+        // scratch[2]: the ordering flag of k_relabel_keys, meaningless here (ids are unordered)
+        k_relabel_keys<<<grid_for(m, 256, kSMs * 16), 256, 0, s>>>(r.src, r.dst, m, id_of_rank, vb, keys,
+                                                                     scratch + 2);
+        TC_LAUNCHED();
+    }
+    TC_CHECK(radix_histogram(keys, m, plan, hist, s));
+    TC_CHECK(graph_alloc(out, m, n, s));
+    TC_CHECK(radix_sort(keys, alt, nullptr, nullptr, m, plan, hist, kOutSoA, out->src, out->dst, vb,
+                        nullptr, nullptr, s));
+    TC_CUDA(cudaMemsetAsync(out->dst + m, 0, 8 * sizeof(uint32_t), s));
+    TC_CHECK(build_node_array_dev(out->src, m, n, out->off, out->off32, scratch + 1, s));
+    TC_CUDA(cudaMemcpyAsync(&out->max_out, scratch + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    dfree(hist, s);
+    dfree(scratch, s);
+    dfree(keys, s);
+    dfree(alt, s);
     return 0;
 }
 
