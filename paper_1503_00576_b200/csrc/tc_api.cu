@@ -1052,6 +1052,7 @@ const OptionName kOptionNames[] = {
     {"skew", &Options::skew},               {"light_vec", &Options::light_vec},
     {"shard_model", &Options::shard_model}, {"shard_ovh", &Options::shard_ovh},
     {"shard_ucap", &Options::shard_ucap},   {"dense_ranks", &Options::dense_ranks},
+    {"shard_ovh2", &Options::shard_ovh2},
     {"bucket", &Options::bucket},           {"count_stats", &Options::count_stats},
     {"hubpack", &Options::hubpack},         {"rank_primary", &Options::rank_primary},
 };

@@ -280,6 +280,9 @@ __device__ __forceinline__ uint32_t sweep_bits(const uint32_t *__restrict__ dst,
 // item of the aligned group of 4).  A 16-byte chunk of 4 items becomes one 8-byte + one
 // 1-byte load.  Only positions holding hub items (>= hz) are meaningful; the sweeps read
 // lists whose valid items are all hub items (suffixes after a hub head).
+#ifndef TC_PACK_U
+#define TC_PACK_U 8  // chunks in flight per lane in the packed sweep (9 B each: keep bytes in flight)
+#endif
 struct HubPack {
     const uint16_t *lo16;
     const uint8_t *hi2;
@@ -1513,7 +1516,7 @@ __global__ void TC_VM_BOUNDS(NT)
                 } else if (hp.lo16) {
                     // suffix items exceed v >= hz: every valid item is a hub item, read from
                     // the 18-bit packed copy (2.25 B per item)
-                    acc += sweep_bits18<U>(hp, et, NT, c0, c1, bitmap);
+                    acc += sweep_bits18<TC_PACK_U>(hp, et, NT, c0, c1, bitmap);
                 } else {
                     acc += sweep_bits<U>(dst, et, NT, c0, c1, bitmap, hz);
                 }
@@ -2232,6 +2235,10 @@ int tile_sums(const DeviceGraph &g, uint64_t tile, uint32_t overhead, unsigned l
 }
 }  // namespace
 
+__global__ void k_tile_sched(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
+                             const uint32_t *__restrict__ off, uint64_t m, uint64_t tile, uint32_t overhead,
+                             VSplit vp, bool hub, unsigned long long *__restrict__ sums);
+
 int work_bounds_dev(const DeviceGraph &g, int npools, int64_t *bounds, cudaStream_t s) {
     // Per-edge estimated work d+(u) + d+(v) + c; cuts at k*W/P with a
     // tile granularity fine enough that rounding is negligible against m/P.
@@ -2250,7 +2257,20 @@ int work_bounds_dev(const DeviceGraph &g, int npools, int64_t *bounds, cudaStrea
     const uint32_t ucap_env = (uint32_t)opts().shard_ucap;
     const bool ranked = model == 1 && g.rank_space;
     const uint32_t ovh = g.rank_space ? ovh_env : 8u, ucap = g.rank_space ? ucap_env : 0xffffffffu;
-    TC_CHECK(tile_sums(g, tile, ovh, &sums, &nt, s, ranked, ucap));
+    if (model == 2 && g.rank_space && g.off32 && g.hubstart) {
+        // compulsory bytes of the schedule the ranged count will run, per edge, + overhead
+        const uint64_t ntl = (g.m + tile - 1) / tile;
+        TC_CHECK(dalloc_t(&sums, ntl ? ntl : 1, s));
+        if (ntl) {
+            k_tile_sched<<<(unsigned)ntl, 256, 0, s>>>(g.src, g.dst, g.off32, g.m, tile, (uint32_t)opts().shard_ovh2,
+                                                      make_vsplit(g, vmajor_schedule(g)), g.dense_bits != nullptr,
+                                                      sums);
+            TC_LAUNCHED();
+        }
+        nt = ntl;
+    } else {
+        TC_CHECK(tile_sums(g, tile, ovh, &sums, &nt, s, ranked, ucap));
+    }
     std::string err;
     unsigned long long *h = (unsigned long long *)malloc((nt ? nt : 1) * sizeof(unsigned long long));
     if (!h) { set_error("host allocation failed"); return -3; }
@@ -2288,6 +2308,37 @@ int work_bounds_dev(const DeviceGraph &g, int npools, int64_t *bounds, cudaStrea
 //                          4 * |suffix| * ceil(log2 |adj(v)|) binary search
 //   [3] every edge         16 (src, dst, off[v], off[v+1])
 //   [4] heavy staging      4 * d+(u) per heavy source (adj(u) into shared memory once)
+// Bytes of edge e under the schedule; *cls = 0..3 (v-major, u-major heavy, light, none).
+__device__ __forceinline__ uint64_t edge_bytes(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
+                                               const uint32_t *__restrict__ off, uint64_t e, const VSplit &vp,
+                                               bool hub, int *cls, uint32_t *stage) {
+    const uint32_t u = __ldg(src + e), su = __ldg(off + u), eu = __ldg(off + u + 1), du = eu - su;
+    const uint32_t v = __ldg(dst + e), vs = __ldg(off + v), ve = __ldg(off + v + 1), dv = ve - vs;
+    *stage = e == su && du > (uint32_t)kLightMax ? 4u * du : 0u;
+    *cls = 3;
+    if (e + 1 >= eu || vs >= ve) return 0;  // no triangle can close: every kernel skips it
+    const uint32_t sfx = eu - (uint32_t)e - 1;
+    if (vmajor_edge(vp, (uint32_t)e, eu, v, vs, ve)) {
+        *cls = 0;
+        return (vp.packed && v >= vp.hz ? 9ull * ((sfx + 3) / 4) : 4ull * sfx) + 8;
+    }
+    if (du > (uint32_t)kLightMax) {
+        *cls = 1;
+        uint64_t x = 4ull * dv;
+        if (hub && v >= vp.hz) {
+            const uint32_t ws = ((v + 1 - vp.hz) >> 5) & ~3u;
+            if (v >= vp.vt && (vp.hwp - ws) < vp.factor * dv) x = 4ull * (vp.hwp - ws);
+            else if (vp.packed) x = 9ull * ((dv + 3) / 4);
+        }
+        return x;
+    }
+    *cls = 2;
+    uint64_t x = 4ull * (sfx + dv);
+    if (hub && v >= vp.vt && sfx < dv) x = 4ull * sfx;
+    else if (sfx * (32u - __clz(dv)) < sfx + dv) x = 4ull * sfx * (32u - __clz(dv));
+    return x;
+}
+
 __global__ void __launch_bounds__(256)
     k_schedule_bytes(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
                      const uint32_t *__restrict__ off, uint64_t m, VSplit vp, bool hub,
@@ -2295,33 +2346,41 @@ __global__ void __launch_bounds__(256)
     unsigned long long b[5] = {0, 0, 0, 0, 0};
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
-        const uint32_t u = __ldg(src + e), su = __ldg(off + u), eu = __ldg(off + u + 1), du = eu - su;
-        const uint32_t v = __ldg(dst + e), vs = __ldg(off + v), ve = __ldg(off + v + 1), dv = ve - vs;
+        int cls;
+        uint32_t stage;
+        const uint64_t x = edge_bytes(src, dst, off, e, vp, hub, &cls, &stage);
         b[3] += 16;
-        if (e == su && du > (uint32_t)kLightMax) b[4] += 4ull * du;
-        if (e + 1 >= eu || vs >= ve) continue;  // no triangle can close: every kernel skips it
-        const uint32_t sfx = eu - (uint32_t)e - 1;
-        if (vmajor_edge(vp, (uint32_t)e, eu, v, vs, ve)) {
-            b[0] += (vp.packed && v >= vp.hz ? 9ull * ((sfx + 3) / 4) : 4ull * sfx) + 8;
-        } else if (du > (uint32_t)kLightMax) {
-            uint64_t x = 4ull * dv;
-            if (hub && v >= vp.hz) {
-                const uint32_t ws = ((v + 1 - vp.hz) >> 5) & ~3u;
-                if (v >= vp.vt && (vp.hwp - ws) < vp.factor * dv) x = 4ull * (vp.hwp - ws);
-                else if (vp.packed) x = 9ull * ((dv + 3) / 4);
-            }
-            b[1] += x;
-        } else {
-            uint64_t x = 4ull * (sfx + dv);
-            if (hub && v >= vp.vt && sfx < dv) x = 4ull * sfx;
-            else if (sfx * (32u - __clz(dv)) < sfx + dv) x = 4ull * sfx * (32u - __clz(dv));
-            b[2] += x;
-        }
+        b[4] += stage;
+        if (cls < 3) b[cls] += x;
     }
     for (int k = 0; k < 5; ++k) {
         unsigned long long x = b[k];
         for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(TC_FULL_MASK, x, o);
         if (lane_id() == 0 && x) atomicAdd(out + k, x);
+    }
+}
+
+// Per-tile sums of the schedule's bytes + `overhead` per edge (the rank-space shard model).
+__global__ void __launch_bounds__(256)
+    k_tile_sched(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
+                 const uint32_t *__restrict__ off, uint64_t m, uint64_t tile, uint32_t overhead, VSplit vp,
+                 bool hub, unsigned long long *__restrict__ sums) {
+    const uint64_t b = (uint64_t)blockIdx.x * tile;
+    const uint64_t e1 = b + tile < m ? b + tile : m;
+    unsigned long long acc = 0;
+    for (uint64_t e = b + threadIdx.x; e < e1; e += blockDim.x) {
+        int cls;
+        uint32_t stage;
+        acc += edge_bytes(src, dst, off, e, vp, hub, &cls, &stage) + stage + overhead;
+    }
+    __shared__ unsigned long long s_red[32];
+    acc = warp_sum(acc);
+    if (lane_id() == 0) s_red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        unsigned long long y = threadIdx.x < (blockDim.x >> 5) ? s_red[threadIdx.x] : 0ull;
+        y = warp_sum(y);
+        if (threadIdx.x == 0) sums[blockIdx.x] = y;
     }
 }
 

@@ -60,6 +60,7 @@ struct Options {
     int64_t shard_model = 0;     // tc_work_bounds model (0: capped work, 1: rank model)
     int64_t shard_ovh = 128;     // per-edge constant of the rank-space shard model
     int64_t shard_ucap = 1024;   // cap on d+(u) in the rank-space shard model
+    int64_t shard_ovh2 = 256;    // per-edge byte-equivalent overhead of shard model 2
     int64_t dense_ranks = 1 << 17;  // dense-hub bitmaps for the top ranks
     int64_t bucket = 1;          // rank-space preprocess: bucket scatter + segmented sort
     int64_t count_stats = 0;     // tc_count_with_timings fills the per-kernel-class fields
