@@ -201,6 +201,8 @@ int tc_reserve(uint64_t bytes);
  * reads, [3] 16 B per edge (src, dst, two offsets), [4] heavy-source staging.  The roofline
  * numerator of bench.py; no reference counterpart. */
 int tc_schedule_bytes(const tc_graph *g, uint64_t out[5]);
+/* The same over oriented edges [lo, hi) of a rank-space graph (shard cost calibration). */
+int tc_schedule_bytes_range(const tc_graph *g, int64_t lo, int64_t hi, uint64_t out[5]);
 
 int tc_set_option(const char *name, int64_t value);
 int tc_get_option(const char *name, int64_t *value);

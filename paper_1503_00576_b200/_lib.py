@@ -115,6 +115,7 @@ _SIGS = {
     "tc_launch_count": ([_u64p], ctypes.c_int),
     "tc_reserve": ([ctypes.c_uint64], ctypes.c_int),
     "tc_schedule_bytes": ([_graph_p, _vp], ctypes.c_int),
+    "tc_schedule_bytes_range": ([_graph_p, ctypes.c_int64, ctypes.c_int64, _vp], ctypes.c_int),
     "tc_set_option": ([ctypes.c_char_p, ctypes.c_int64], ctypes.c_int),
     "tc_get_option": ([ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
     "tc_reset_options": ([], ctypes.c_int),

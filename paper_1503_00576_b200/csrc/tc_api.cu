@@ -160,6 +160,7 @@ class CopyPool {
         cv_.notify_all();
         for (auto &t : th_) t.join();
     }
+    int size() const { return n_; }
     void copy(void *dst, const void *src, size_t bytes) {
         std::unique_lock<std::mutex> lk(mu_);
         dst_ = (char *)dst;
@@ -212,6 +213,10 @@ static void parallel_memcpy(void *dst, const void *src, size_t bytes, int thread
         memcpy(dst, src, bytes);
         return;
     }
+    if (g_copy_pool && g_copy_pool->size() != threads) {
+        delete g_copy_pool;
+        g_copy_pool = nullptr;
+    }
     if (!g_copy_pool) g_copy_pool = new CopyPool(threads);
     g_copy_pool->copy(dst, src, bytes);
 }
@@ -228,7 +233,8 @@ static int h2d(void *dst, const void *src, size_t bytes, cudaStream_t s) {
             TC_CUDA(cudaEventCreateWithFlags(&g_stage_ev[b], cudaEventDisableTiming));
         }
     const unsigned hc = std::thread::hardware_concurrency();
-    const int threads = hc >= 16 ? 8 : hc >= 4 ? (int)hc / 2 : 1;
+    const int threads = opts().copy_threads > 0 ? (int)opts().copy_threads
+                        : hc >= 16 ? 8 : hc >= 4 ? (int)hc / 2 : 1;
     size_t off = 0;
     for (int k = 0; off < bytes; ++k) {
         const int b = k % kStageBufs;
@@ -783,7 +789,22 @@ int tc_schedule_bytes(const tc_graph *g, uint64_t out[5]) {
     TC_CHECK(check_graph(g));
     const DeviceGraph *r = nullptr;
     TC_CHECK(rank_copy(const_cast<tc_graph *>(g), &r));
-    return schedule_bytes_dev(*r, out, g_stream);
+    return schedule_bytes_dev(*r, 0, r->m, out, g_stream);
+}
+
+int tc_schedule_bytes_range(const tc_graph *g, int64_t lo, int64_t hi, uint64_t out[5]) {
+    TC_API_GUARD();
+    TC_CHECK(ensure());
+    TC_CHECK(check_graph(g));
+    if (!g->g.rank_space) {
+        set_error("ranged schedule bytes need a rank-space graph (tc_preprocess_ex RANK_SPACE)");
+        return -1;
+    }
+    if (lo < 0 || hi < lo || (uint64_t)hi > g->g.m) {
+        set_error("edge range outside [0, m]");
+        return -1;
+    }
+    return schedule_bytes_dev(g->g, (uint64_t)lo, (uint64_t)hi, out, g_stream);
 }
 
 int tc_merge_work(const tc_graph *g, uint64_t *out) {
@@ -1052,7 +1073,7 @@ const OptionName kOptionNames[] = {
     {"skew", &Options::skew},               {"light_vec", &Options::light_vec},
     {"shard_model", &Options::shard_model}, {"shard_ovh", &Options::shard_ovh},
     {"shard_ucap", &Options::shard_ucap},   {"dense_ranks", &Options::dense_ranks},
-    {"shard_ovh2", &Options::shard_ovh2},
+    {"shard_ovh2", &Options::shard_ovh2},   {"copy_threads", &Options::copy_threads},
     {"bucket", &Options::bucket},           {"count_stats", &Options::count_stats},
     {"hubpack", &Options::hubpack},         {"rank_primary", &Options::rank_primary},
 };

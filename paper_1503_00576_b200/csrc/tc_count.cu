@@ -2341,11 +2341,11 @@ __device__ __forceinline__ uint64_t edge_bytes(const uint32_t *__restrict__ src,
 
 __global__ void __launch_bounds__(256)
     k_schedule_bytes(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
-                     const uint32_t *__restrict__ off, uint64_t m, VSplit vp, bool hub,
+                     const uint32_t *__restrict__ off, uint64_t lo, uint64_t m, VSplit vp, bool hub,
                      unsigned long long *__restrict__ out) {
     unsigned long long b[5] = {0, 0, 0, 0, 0};
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+    for (uint64_t e = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
         int cls;
         uint32_t stage;
         const uint64_t x = edge_bytes(src, dst, off, e, vp, hub, &cls, &stage);
@@ -2384,7 +2384,7 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-int schedule_bytes_dev(const DeviceGraph &g, uint64_t out[5], cudaStream_t s) {
+int schedule_bytes_dev(const DeviceGraph &g, uint64_t lo, uint64_t hi, uint64_t out[5], cudaStream_t s) {
     if (!g.rank_space || !g.off32 || !g.hubstart) {
         set_error("the schedule byte model needs a rank-space graph with m < 2^32");
         return -1;
@@ -2394,9 +2394,10 @@ int schedule_bytes_dev(const DeviceGraph &g, uint64_t out[5], cudaStream_t s) {
     TC_CUDA(cudaMemsetAsync(d, 0, 5 * sizeof(unsigned long long), s));
     const bool vm = vmajor_schedule(g);
     const VSplit vp = make_vsplit(g, vm);
-    if (g.m) {
-        k_schedule_bytes<<<grid_for(g.m, 256, kSMs * 16), 256, 0, s>>>(g.src, g.dst, g.off32, g.m, vp,
-                                                                      g.dense_bits != nullptr, d);
+    if (hi > g.m) hi = g.m;
+    if (lo < hi) {
+        k_schedule_bytes<<<grid_for(hi - lo, 256, kSMs * 16), 256, 0, s>>>(g.src, g.dst, g.off32, lo, hi, vp,
+                                                                          g.dense_bits != nullptr, d);
         TC_LAUNCHED();
     }
     unsigned long long h[5];

@@ -61,10 +61,11 @@ struct Options {
     int64_t shard_ovh = 128;     // per-edge constant of the rank-space shard model
     int64_t shard_ucap = 1024;   // cap on d+(u) in the rank-space shard model
     int64_t shard_ovh2 = 256;    // per-edge byte-equivalent overhead of shard model 2
+    int64_t copy_threads = 0;    // host threads of the staged pageable H2D copy (0: auto)
     int64_t dense_ranks = 1 << 17;  // dense-hub bitmaps for the top ranks
     int64_t bucket = 1;          // rank-space preprocess: bucket scatter + segmented sort
     int64_t count_stats = 0;     // tc_count_with_timings fills the per-kernel-class fields
-    int64_t hubpack = 1;         // v-major hub-head suffixes read from an 18-bit packed copy
+    int64_t hubpack = 0;         // 1: hub-head suffixes read from an 18-bit packed copy (slower)
     int64_t rank_primary = 1;    // tc_preprocess builds the rank-space CSR, reference ids lazily
 };
 Options &opts();
@@ -239,7 +240,7 @@ int work_bounds_dev(const DeviceGraph &g, int npools, int64_t *bounds, cudaStrea
 int merge_work_dev(const DeviceGraph &g, uint64_t *out, cudaStream_t s);
 // Compulsory bytes of the full-count schedule of a rank-space graph, by kernel class
 // (v-major, u-major heavy, light, per-edge, heavy staging); see tc_count.cu.
-int schedule_bytes_dev(const DeviceGraph &g, uint64_t out[5], cudaStream_t s);
+int schedule_bytes_dev(const DeviceGraph &g, uint64_t lo, uint64_t hi, uint64_t out[5], cudaStream_t s);
 
 // ---------------------------------------------------------------- generators ---
 int rmat_dev(int scale, int edge_factor, const double probs[4], const uint64_t state[2],

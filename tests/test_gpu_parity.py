@@ -348,7 +348,8 @@ def test_rank_space_csr_matches_numpy(case):
     {"vmajor": 0, "light": 0},                       # u-major only, CTA-window light kernel
     {"vmajor": 0, "light_vec": 1, "hub_unroll": 2},  # vector light loads, 2-way hub unroll
     {"bucket": 0},                                   # rank-space preprocess by global key sort
-    {"vmajor": 1, "hubpack": 0},                     # hub suffixes from the 32-bit edge_dst
+    {"vmajor": 1, "hubpack": 1},                     # hub suffixes from the 18-bit packed copy
+    {"vmajor": 1, "hubpack": 2},                     # packed reads, 4-byte cost model
 ], ids=lambda o: ",".join(f"{k}={v}" for k, v in o.items()))
 def test_count_schedules_agree(opts, golden_big):
     """Every count schedule (v-major on/off and its zone, the per-edge bias, the light and
