@@ -95,6 +95,15 @@ int tc_count_with_timings(const uint32_t *pairs, uint64_t npairs, uint64_t nvert
 
 /* ---- multi-GPU sharding: estimated-work bounds[npools+1] ---------- */
 int tc_work_bounds(const tc_graph *g, int npools, int64_t *bounds);
+/* Multi-GPU shard plan of a full count (rank-space copy of g): shard r
+ * counts the edges [edge_bounds[r], edge_bounds[r+1]) that are not v-major plus the v-major
+ * edges of the whole graph whose head lies in [head_bounds[r], head_bounds[r+1]).  Edge
+ * bounds balance the u-major + light bytes, head bounds the v-major bytes, so every shard
+ * gets 1/parts of both, and each head's bitmap is built by one shard only.  Both arrays
+ * hold parts + 1 entries; the shard counts sum to the full count. */
+int tc_shard_plan(const tc_graph *g, int parts, int64_t *edge_bounds, int64_t *head_bounds);
+int tc_count_shard(const tc_graph *g, int64_t lo, int64_t hi, int64_t head_lo, int64_t head_hi,
+                   uint64_t *out, tc_times *t);
 /* merge-model work W = sum over oriented edges of d+(u) + d+(v) (roofline numerator) */
 int tc_merge_work(const tc_graph *g, uint64_t *out);
 

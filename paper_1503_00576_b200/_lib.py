@@ -78,6 +78,9 @@ _SIGS = {
                                _u64p, ctypes.POINTER(TcTimes)], ctypes.c_int),
     "tc_work_bounds": ([_graph_p, ctypes.c_int, _vp], ctypes.c_int),
     "tc_merge_work": ([_graph_p, _u64p], ctypes.c_int),
+    "tc_shard_plan": ([_graph_p, ctypes.c_int, _vp, _vp], ctypes.c_int),
+    "tc_count_shard": ([_graph_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _u64p,
+                        ctypes.POINTER(TcTimes)], ctypes.c_int),
     "tc_sort_edges": ([_vp, ctypes.c_uint64, ctypes.c_uint64, _vp], ctypes.c_int),
     "tc_build_node_array": ([_vp, ctypes.c_uint64, ctypes.c_uint64, _vp], ctypes.c_int),
     "tc_orient_and_compact": ([_vp, ctypes.c_uint64, _vp, ctypes.c_uint64, _vp, _u64p],

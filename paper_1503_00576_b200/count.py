@@ -23,7 +23,7 @@ from .graph import EdgeArray, OrientedGraph
 
 __all__ = ["PhaseTimings", "PartitionPlan", "count_triangles", "count_partitioned",
            "count_with_timings", "intersect_count", "warm_kernel", "default_workers",
-           "count_device", "merge_work", "schedule_bytes"]
+           "count_device", "merge_work", "schedule_bytes", "shard_plan", "count_shard"]
 
 
 @dataclass(frozen=True)
@@ -176,6 +176,29 @@ def merge_work(g: OrientedGraph) -> int:
     dev = _device(g)
     _lib.check(_lib.lib().tc_merge_work(dev.handle, ctypes.byref(out)))
     return int(out.value)
+
+
+def shard_plan(g: OrientedGraph, parts: int):
+    """Multi-GPU shard plan of a full count (tc_shard_plan): (edge_bounds, head_bounds) of the
+    rank-space copy.  Shard r = non-v-major edges in its edge range + v-major edges whose
+    head is in its head range; count_shard(g, r-th bounds) summed over r is the count."""
+    if parts < 1:
+        raise ValueError("parts must be >= 1")
+    eb = np.zeros(parts + 1, dtype=np.int64)
+    hb = np.zeros(parts + 1, dtype=np.int64)
+    dev = _device(g)
+    _lib.check(_lib.lib().tc_shard_plan(dev.handle, int(parts), _lib.ptr(eb), _lib.ptr(hb)))
+    return eb, hb
+
+
+def count_shard(g: OrientedGraph, lo: int, hi: int, head_lo: int, head_hi: int):
+    """One shard of a shard_plan (triangles, library timings)."""
+    out = ctypes.c_uint64()
+    t = _lib.TcTimes()
+    dev = _device(g)
+    _lib.check(_lib.lib().tc_count_shard(dev.handle, int(lo), int(hi), int(head_lo), int(head_hi),
+                                         ctypes.byref(out), ctypes.byref(t)))
+    return int(out.value), t
 
 
 def schedule_bytes(g: OrientedGraph) -> dict:

@@ -807,6 +807,62 @@ int tc_schedule_bytes_range(const tc_graph *g, int64_t lo, int64_t hi, uint64_t 
     return schedule_bytes_dev(g->g, (uint64_t)lo, (uint64_t)hi, out, g_stream);
 }
 
+int tc_shard_plan(const tc_graph *g, int parts, int64_t *edge_bounds, int64_t *head_bounds) {
+    TC_API_GUARD();
+    TC_CHECK(ensure());
+    TC_CHECK(check_graph(g));
+    if (parts < 1) {
+        set_error("parts must be >= 1");
+        return -1;
+    }
+    const DeviceGraph *r = nullptr;
+    TC_CHECK(rank_copy(const_cast<tc_graph *>(g), &r));
+    return shard_plan_dev(*r, parts, edge_bounds, head_bounds, g_stream);
+}
+
+int tc_count_shard(const tc_graph *g, int64_t lo, int64_t hi, int64_t hlo, int64_t hhi, uint64_t *out,
+                   tc_times *t) {
+    TC_API_GUARD();
+    TC_CHECK(ensure());
+    TC_CHECK(check_graph(g));
+    const DeviceGraph *r = nullptr;
+    TC_CHECK(rank_copy(const_cast<tc_graph *>(g), &r));
+    if (lo < 0 || hi < lo || (uint64_t)hi > r->m || hlo < 0 || hhi < hlo || (uint64_t)hhi > r->n) {
+        set_error("shard outside [0, m) x [0, n)");
+        return -1;
+    }
+    cudaStream_t s = g_stream;
+    Events ev;
+    TC_CHECK(ev.create());
+    TC_CUDA(cudaEventRecord(ev.e[0], s));
+    unsigned long long *total = nullptr;
+    TC_CHECK(dalloc_t(&total, 1, s));
+    TC_CUDA(cudaMemsetAsync(total, 0, sizeof(unsigned long long), s));
+    CountStats st;
+    const int rc = count_shard_dev(*r, (uint64_t)lo, (uint64_t)hi, (uint32_t)hlo, (uint32_t)hhi, total, s,
+                                   t ? &st : nullptr);
+    if (rc) {
+        dfree(total, s);
+        return rc;
+    }
+    unsigned long long hv = 0;
+    TC_CUDA(cudaMemcpyAsync(&hv, total, sizeof(hv), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaEventRecord(ev.e[1], s));
+    dfree(total, s);
+    TC_CUDA(cudaEventSynchronize(ev.e[1]));
+    *out = hv;
+    if (t) {
+        memset(t, 0, sizeof(*t));
+        t->count_ms = t->total_ms = ms_between(ev.e[0], ev.e[1]);
+        t->classify_ms = st.classify_ms;
+        t->heavy_ms = st.heavy_ms;
+        t->light_ms = st.light_ms;
+        t->vmajor_ms = st.vmajor_ms;
+        t->heavy_tasks = st.heavy_tasks;
+    }
+    return 0;
+}
+
 int tc_merge_work(const tc_graph *g, uint64_t *out) {
     TC_API_GUARD();
     TC_CHECK(ensure());

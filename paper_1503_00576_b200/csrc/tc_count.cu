@@ -1074,14 +1074,34 @@ __global__ void TC_HUB_BOUNDS(NT)
         }
         __syncthreads();
 
+        // Window metadata is software-pipelined: the head v of window k+2 and the offsets /
+        // hubstart / dense offset of window k+1 are loaded while window k is swept, so the
+        // dependent chain edge -> v -> off[v] is off the critical path.
+        auto load_v = [&](uint64_t w) -> uint32_t {
+            return w + threadIdx.x < ee ? __ldg(dst + w + threadIdx.x) : 0xffffffffu;
+        };
+        auto load_meta = [&](uint32_t x, uint32_t &a0, uint32_t &a1, uint32_t &a2, uint32_t &a3) {
+            if (x != 0xffffffffu) {
+                a0 = __ldg(off + x);
+                a1 = __ldg(off + x + 1);
+                a2 = __ldg(hubstart + x);
+                a3 = x >= vt ? __ldg(dense_off + (x - vt)) : 0u;
+            }
+        };
+        uint32_t v_n = load_v(es), v_nn = load_v(es + NT);
+        uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+        load_meta(v_n, m0, m1, m2, m3);
         for (uint64_t ws = es; ws < ee; ws += NT) {
             const uint32_t nwin = (uint32_t)(ee - ws < (uint64_t)NT ? ee - ws : (uint64_t)NT);
-            uint32_t v = 0, vs = 0, ve = 0, hv = 0, dgo = 0, dws = 0;
+            uint32_t v = v_n, vs = m0, ve = m1, hv = 0, dgo = 0, dws = 0;
+            const uint32_t hv_l = m2, dgo_l = m3;
             bool dense = false;
+            // next window's metadata (its head arrived one window ago), head of the one after
+            v_n = v_nn;
+            m0 = m1 = m2 = m3 = 0;
+            load_meta(v_n, m0, m1, m2, m3);
+            v_nn = load_v(ws + 2 * (uint64_t)NT);
             if (threadIdx.x < nwin) {
-                v = __ldg(dst + ws + threadIdx.x);
-                vs = __ldg(off + v);
-                ve = __ldg(off + v + 1);
                 if (vmajor_edge(vp, (uint32_t)(ws + threadIdx.x), e, v, vs, ve)) {
                     vs = ve = 0;  // counted by k_count_vmajor
                 } else {
@@ -1090,11 +1110,13 @@ __global__ void TC_HUB_BOUNDS(NT)
                     if (v >= vt) {
                         dws = ((v + 1 - hz) >> 5) & ~3u;
                         dense = (hwords - dws) < dense_factor * (ve - vs);
-                        if (dense) dgo = __ldg(dense_off + (v - vt));
+                        if (dense) dgo = dgo_l;
                     }
                     if (dense) vs = ve = 0;
-                    else hv = __ldg(hubstart + v);
+                    else hv = hv_l;
                 }
+            } else {
+                v = vs = ve = 0;
             }
             // pass 0: hub suffixes [hv, ve) of sparse edges against the bitmap;
             // pass 1: non-hub prefixes [vs, hv) against the cuckoo table (only if adj(u)
@@ -1264,7 +1286,7 @@ __global__ void __launch_bounds__(256)
     k_vin_pass(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
                const uint32_t *__restrict__ off, const RangeDev *__restrict__ rg, VSplit vp,
                const uint32_t *__restrict__ start, uint32_t *__restrict__ cnt,
-               uint2 *__restrict__ in_e, uint32_t *__restrict__ capflag) {
+               uint2 *__restrict__ in_e, uint32_t *__restrict__ capflag, uint32_t hlo, uint32_t hhi) {
     const uint64_t lo = rg->lo, hi = rg->hi;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * kVinPP;
     for (uint64_t b = lo + ((uint64_t)blockIdx.x * blockDim.x) * kVinPP + threadIdx.x; b < hi; b += stride) {
@@ -1279,7 +1301,8 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int i = 0; i < kVinPP; ++i) {
             const uint64_t e = b + (uint64_t)i * blockDim.x;
-            const bool cand = e < hi && v[i] >= vp.z0;
+            // head filter [hlo, hhi): a shard counts the v-major edges of its own heads
+            const bool cand = e < hi && v[i] >= vp.z0 && v[i] >= hlo && v[i] < hhi;
             eu[i] = cand ? __ldg(off + u[i] + 1) : 0u;
             vs[i] = cand ? __ldg(off + v[i]) : 0u;
             ve[i] = cand ? __ldg(off + v[i] + 1) : 0u;
@@ -1290,6 +1313,7 @@ __global__ void __launch_bounds__(256)
         for (int i = 0; i < kVinPP; ++i) {
             const uint32_t e = (uint32_t)(b + (uint64_t)i * blockDim.x);
             pos[i] = 0xffffffffu;
+            if (v[i] < vp.z0 || v[i] < hlo || v[i] >= hhi) continue;
             if (e + 1 >= eu[i] || vs[i] >= ve[i] || !vmajor_edge(vp, e, eu[i], v[i], vs[i], ve[i])) continue;
             const uint32_t h = v[i] - vp.z0;
             if (FILL) {
@@ -1836,7 +1860,7 @@ struct VmajorState {
 
 int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
                  unsigned long long *d_total, cudaStream_t s, cudaStream_t s2, int share,
-                 VmajorState *st) {
+                 VmajorState *st, uint32_t hlo = 0, uint32_t hhi = 0xffffffffu) {
     const uint32_t z0 = vzone_start(g);
     const uint32_t nh = (uint32_t)(g.n - z0);  // v-major zone size
     TC_CHECK(dalloc_t(&st->cnt, nh, s));
@@ -1869,13 +1893,13 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
     const uint32_t *startp = g.vin_cap;
     if (!capl) {
         k_vin_pass<false><<<grid, 256, 0, s2>>>(g.src, g.dst, g.off32, rg, vp, nullptr, st->cnt, nullptr,
-                                                nullptr);
+                                                nullptr, hlo, hhi);
         TC_LAUNCHED();
         TC_CHECK(vin_scan<false>(st->cnt, nh, st->start, s2));  // exact layout, cursors zeroed
         startp = st->start;
     }
     k_vin_pass<true><<<grid, 256, 0, s2>>>(g.src, g.dst, g.off32, rg, vp, startp, st->cnt, st->in_e,
-                                           capl ? st->next + 2 : nullptr);
+                                           capl ? st->next + 2 : nullptr, hlo, hhi);
     TC_LAUNCHED();
     TC_CHECK(vin_scan<true>(st->cnt, nh, st->tstart, s2));  // tasks from the fill counts
     const uint32_t hb = (uint32_t)(g.hz - z0);  // first hub-zone head: tasks [tstart[hb], ...)
@@ -2009,9 +2033,17 @@ bool vmajor_schedule(const DeviceGraph &g) {
     return vmajor;
 }
 
+// Shard of a multi-GPU count: the non-v-major edges of [lo, hi) plus the v-major edges (of
+// the whole graph) whose head lies in [hlo, hhi).  Over a covering set of shards every edge
+// is counted exactly once, and every head's bitmap is built once in total.
+struct ShardSpec {
+    uint32_t hlo, hhi;
+};
+
 template <typename OffT>
 int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
-               unsigned long long *d_out, cudaStream_t s, CountStats *stats) {
+               unsigned long long *d_out, cudaStream_t s, CountStats *stats,
+               const ShardSpec *shard = nullptr) {
     // Sources with more out-edges than the shared-memory staging can hold (d+(u) > 51,200:
     // only cliques of ~51K+ vertices reach that) are counted by the paper's thread-per-edge
     // merge over the whole range -- slower, same exact sum.
@@ -2070,7 +2102,16 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
     const bool conc = vmajor && conc_env;
     const int share = conc ? (int)(opts().share > 0 ? opts().share : 1) : 1;  // SM share of each concurrent kernel
     VmajorState vst;
-    if (vmajor) TC_CHECK(count_vmajor(g, rg, span, d_total, s, conc ? side_stream() : s, share, &vst));
+    RangeDev *rg_all = nullptr;  // shard mode: the v-major index scans every edge for its heads
+    if (vmajor && shard) {
+        TC_CHECK(dalloc_t(&rg_all, 1, s));
+        k_range_init<<<1, 1, 0, s>>>(g.src, 0, g.m, g.m, rg_all);
+        TC_LAUNCHED();
+        TC_CHECK(count_vmajor(g, rg_all, g.m, d_total, s, conc ? side_stream() : s, share, &vst, shard->hlo,
+                              shard->hhi));
+    } else if (vmajor) {
+        TC_CHECK(count_vmajor(g, rg, span, d_total, s, conc ? side_stream() : s, share, &vst));
+    }
     TC_CUDA(cudaEventRecord(ev[1], s));
     // Heavy classes first (largest tasks first), then the light sweep.
     for (int c = kClasses - 1; c >= 0; --c) {
@@ -2152,10 +2193,11 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
         g2.vin_cap = nullptr;
         for (auto &e : ev) cudaEventDestroy(e);
         for (int c = 0; c < kClasses; ++c) dfree(tasks[c], s);
+        dfree(rg_all, s);
         dfree(rg, s);
         dfree(counters, s);
         dfree(d_total, s);
-        return count_impl<OffT>(g2, off, lo, hi, d_out, s, stats);
+        return count_impl<OffT>(g2, off, lo, hi, d_out, s, stats, shard);
     }
     TC_CUDA(cudaEventRecord(ev[3], s));
     if (stats) {
@@ -2170,6 +2212,7 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
     for (auto &e : ev) cudaEventDestroy(e);
     if (l2win) clear_l2_window(s);
     for (int c = 0; c < kClasses; ++c) dfree(tasks[c], s);
+    dfree(rg_all, s);
     dfree(rg, s);
     dfree(counters, s);
     if (d_total != d_out) {
@@ -2199,6 +2242,15 @@ int count_range_dev(const DeviceGraph &g, uint64_t lo, uint64_t hi, int algo,
     }
     if (g.off32) return count_impl<uint32_t>(g, g.off32, lo, hi, d_total, s, stats);
     return count_impl<int64_t>(g, g.off, lo, hi, d_total, s, stats);
+}
+
+int count_shard_dev(const DeviceGraph &g, uint64_t lo, uint64_t hi, uint32_t hlo, uint32_t hhi,
+                    unsigned long long *d_total, cudaStream_t s, CountStats *stats) {
+    if (hi > g.m) hi = g.m;
+    if (!g.off32 || !vmajor_schedule(g)) return count_range_dev(g, lo, hi, kAlgoAuto, d_total, s, stats);
+    const ShardSpec sh{hlo, hhi};
+    // an empty edge range may still own heads: run the v-major part over them
+    return count_impl<uint32_t>(g, g.off32, lo, hi > lo ? hi : lo, d_total, s, stats, &sh);
 }
 
 int intersect_dev(const DeviceGraph &g, uint32_t u, uint32_t v, uint64_t *out, cudaStream_t s) {
@@ -2405,6 +2457,126 @@ int schedule_bytes_dev(const DeviceGraph &g, uint64_t lo, uint64_t hi, uint64_t 
     TC_CUDA(cudaStreamSynchronize(s));
     dfree(d, s);
     for (int k = 0; k < 5; ++k) out[k] = h[k];
+    return 0;
+}
+
+// ---------------------------------------------------------------- shard plan ---
+// Edge side: per-tile bytes of the NON-v-major edges (u-major heavy, light, per-edge, staging).
+__global__ void __launch_bounds__(256)
+    k_tile_edge_side(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
+                     const uint32_t *__restrict__ off, uint64_t m, uint64_t tile, VSplit vp, bool hub,
+                     unsigned long long *__restrict__ sums) {
+    const uint64_t b = (uint64_t)blockIdx.x * tile;
+    const uint64_t e1 = b + tile < m ? b + tile : m;
+    unsigned long long acc = 0;
+    for (uint64_t e = b + threadIdx.x; e < e1; e += blockDim.x) {
+        int cls;
+        uint32_t stage;
+        const uint64_t x = edge_bytes(src, dst, off, e, vp, hub, &cls, &stage);
+        acc += (cls == 0 ? 0ull : x) + stage + 16;
+    }
+    __shared__ unsigned long long s_red[32];
+    acc = warp_sum(acc);
+    if (lane_id() == 0) s_red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        unsigned long long y = threadIdx.x < (blockDim.x >> 5) ? s_red[threadIdx.x] : 0ull;
+        y = warp_sum(y);
+        if (threadIdx.x == 0) sums[blockIdx.x] = y;
+    }
+}
+
+// Head side: v-major bytes per head of the zone [z0, n) (suffix streams + index entries).
+__global__ void __launch_bounds__(256)
+    k_head_side(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
+                const uint32_t *__restrict__ off, uint64_t m, VSplit vp, bool hub,
+                unsigned long long *__restrict__ hb) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+        const uint32_t v = __ldg(dst + e);
+        if (v < vp.z0) continue;
+        int cls;
+        uint32_t stage;
+        const uint64_t x = edge_bytes(src, dst, off, e, vp, hub, &cls, &stage);
+        if (cls == 0) atomicAdd(hb + (v - vp.z0), (unsigned long long)x);
+    }
+}
+
+// + the per-task cost of a head that has v-major in-edges: zeroing its bitmap words and
+// staging adj(v).
+__global__ void k_head_fixed(const uint32_t *__restrict__ off, uint32_t z0, uint32_t nz, VSplit vp,
+                             unsigned long long *__restrict__ hb) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < nz; h += stride) {
+        if (!hb[h]) continue;
+        const uint32_t v = z0 + h;
+        const uint32_t ws = v >= vp.hz ? ((v + 1 - vp.hz) >> 5) & ~3u : 0u;
+        hb[h] += 4ull * (vp.hwp - ws) + 4ull * (off[v + 1] - off[v]);
+    }
+}
+
+static void cut_prefix(const unsigned long long *h, uint64_t nt, int parts, uint64_t unit, uint64_t cap,
+                       int64_t *bounds, int64_t base) {
+    unsigned long long W = 0;
+    for (uint64_t i = 0; i < nt; ++i) W += h[i];
+    bounds[0] = base;
+    unsigned long long run = 0;
+    uint64_t t = 0;
+    for (int p = 1; p < parts; ++p) {
+        const long double target = (long double)W * p / parts;
+        while (t < nt && (long double)(run + h[t]) <= target) run += h[t++];
+        uint64_t cut = t;
+        if (t < nt && (long double)(run + h[t]) - target < target - (long double)run) cut = t + 1;
+        uint64_t b = cut * unit;
+        if (b > cap) b = cap;
+        int64_t bb = base + (int64_t)b;
+        if (bb < bounds[p - 1]) bb = bounds[p - 1];
+        bounds[p] = bb;
+    }
+}
+
+int shard_plan_dev(const DeviceGraph &g, int parts, int64_t *ebounds, int64_t *hbounds, cudaStream_t s) {
+    const bool vm = g.off32 && vmajor_schedule(g);
+    for (int p = 0; p <= parts; ++p) hbounds[p] = p == 0 ? 0 : (int64_t)g.n;
+    if (!vm) return work_bounds_dev(g, parts, ebounds, s);
+    const VSplit vp = make_vsplit(g, true);
+    const bool hub = g.dense_bits != nullptr;
+    uint64_t tile = g.m / ((uint64_t)parts * 1024);
+    if (tile < 1) tile = 1;
+    if (tile > 4096) tile = 4096;
+    const uint64_t nt = (g.m + tile - 1) / tile;
+    const uint32_t z0 = vp.z0, nz = (uint32_t)(g.n - z0);
+    unsigned long long *sums = nullptr, *hb = nullptr;
+    TC_CHECK(dalloc_t(&sums, nt ? nt : 1, s));
+    TC_CHECK(dalloc_t(&hb, nz ? nz : 1, s));
+    TC_CUDA(cudaMemsetAsync(hb, 0, (nz ? nz : 1) * sizeof(unsigned long long), s));
+    if (nt) {
+        k_tile_edge_side<<<(unsigned)nt, 256, 0, s>>>(g.src, g.dst, g.off32, g.m, tile, vp, hub, sums);
+        TC_LAUNCHED();
+        k_head_side<<<grid_for(g.m, 256, kSMs * 16), 256, 0, s>>>(g.src, g.dst, g.off32, g.m, vp, hub, hb);
+        TC_LAUNCHED();
+    }
+    if (nz) {
+        k_head_fixed<<<grid_for(nz, 256, kSMs * 4), 256, 0, s>>>(g.off32, z0, nz, vp, hb);
+        TC_LAUNCHED();
+    }
+    unsigned long long *h = (unsigned long long *)malloc(((nt > nz ? nt : nz) + 1) * sizeof(unsigned long long));
+    if (!h) {
+        set_error("host allocation failed");
+        return -3;
+    }
+    TC_CUDA(cudaMemcpyAsync(h, sums, nt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    cut_prefix(h, nt, parts, tile, g.m, ebounds, 0);
+    ebounds[parts] = (int64_t)g.m;
+    TC_CUDA(cudaMemcpyAsync(h, hb, nz * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    cut_prefix(h, nz, parts, 1, nz, hbounds, (int64_t)z0);
+    hbounds[0] = 0;  // heads below the zone never run v-major: shard 0 owns them (no work)
+    hbounds[parts] = (int64_t)g.n;
+    free(h);
+    dfree(sums, s);
+    dfree(hb, s);
     return 0;
 }
 

@@ -236,6 +236,11 @@ int count_range_dev(const DeviceGraph &g, uint64_t lo, uint64_t hi, int algo,
 int intersect_dev(const DeviceGraph &g, uint32_t u, uint32_t v, uint64_t *out, cudaStream_t s);
 // Estimated-work partition of [0, m) into npools ranges (bounds[npools+1], host out).
 int work_bounds_dev(const DeviceGraph &g, int npools, int64_t *bounds, cudaStream_t s);
+// Multi-GPU shard plan (tc_shard_plan): edge bounds balancing the non-v-major work and head
+// bounds balancing the v-major work; count_shard_dev counts one shard of it.
+int shard_plan_dev(const DeviceGraph &g, int parts, int64_t *ebounds, int64_t *hbounds, cudaStream_t s);
+int count_shard_dev(const DeviceGraph &g, uint64_t lo, uint64_t hi, uint32_t hlo, uint32_t hhi,
+                    unsigned long long *d_total, cudaStream_t s, CountStats *stats);
 // Σ over edges of d+(u)+d+(v) (the merge-model work W), host out.
 int merge_work_dev(const DeviceGraph &g, uint64_t *out, cudaStream_t s);
 // Compulsory bytes of the full-count schedule of a rank-space graph, by kernel class

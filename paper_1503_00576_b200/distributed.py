@@ -67,6 +67,15 @@ class Ops:
     def count_range(self, graph, lo: int, hi: int) -> int:
         raise NotImplementedError
 
+    def shard_plan(self, graph, parts: int):
+        """(edge_bounds, head_bounds), parts + 1 entries each.  Default: work-balanced edge
+        ranges, every head in shard 0's head range (no v-major split)."""
+        _, n = self.graph_shape(graph)
+        return self.work_bounds(graph, parts), np.array([0] + [n] * parts, dtype=np.int64)
+
+    def count_shard(self, graph, lo: int, hi: int, hlo: int, hhi: int) -> int:
+        return self.count_range(graph, lo, hi) if hi > lo else 0
+
     def sync(self) -> None:
         pass
 
@@ -124,6 +133,7 @@ class ShardReport:
     bounds: tuple
     m: int
     n: int
+    head_bounds: tuple = ()
 
 
 def count_distributed(ops: Ops, edges=None, group=None, graph=None) -> ShardReport:
@@ -162,15 +172,9 @@ def count_distributed(ops: Ops, edges=None, group=None, graph=None) -> ShardRepo
     _backend_sync(ops)
     if rank != 0:
         ops.finalize(g)
-    # 3. identical work-balanced bounds on every rank; count the local shard
-    bounds = ops.work_bounds(g, world)
-    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
-    local = ops.count_range(g, lo, hi) if hi > lo else 0
-    # 4. one 64-bit all-reduce (counts < 2^63, so int64 sum == uint64 sum bit for bit)
-    t = _to_backend(ops.count_tensor(local), ops)
-    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-    total = int(t.cpu().item())
-    return ShardReport(total, local, tuple(int(b) for b in bounds), m, n)
+    # 3. identical shard plan on every rank (edge ranges for the u-major / light work, head
+    #    ranges for the v-major work); count the local shard
+    return _count_local_shard(ops, g, rank, world, group, m, n)
 
 
 def shard_bounds(npairs: int, world: int) -> list[int]:
@@ -244,14 +248,22 @@ def count_distributed_sharded(ops: Ops, shard, num_vertices: int, group=None) ->
                 ops.dst_write(g, int(ecuts[r]), gathered[r * L:r * L + lens[r]])
         del gathered
     ops.finalize(g)
-    # 6. count the work-balanced shard; one all-reduce
-    bounds = ops.work_bounds(g, world)
-    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
-    local = ops.count_range(g, lo, hi) if hi > lo else 0
+    # 6. count the local shard; one all-reduce
+    return _count_local_shard(ops, g, rank, world, group, m, n)
+
+
+def _count_local_shard(ops: Ops, g, rank: int, world: int, group, m: int, n: int) -> ShardReport:
+    """This rank's shard of the plan every rank computes identically, then one 64-bit
+    all-reduce (counts < 2^63, so the int64 sum equals the uint64 sum bit for bit)."""
+    import torch.distributed as dist
+    eb, hb = ops.shard_plan(g, world)
+    lo, hi = int(eb[rank]), int(eb[rank + 1])
+    hlo, hhi = int(hb[rank]), int(hb[rank + 1])
+    local = ops.count_shard(g, lo, hi, hlo, hhi)
     t = _to_backend(ops.count_tensor(local), ops)
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     total = int(t.cpu().item())
-    return ShardReport(total, local, tuple(int(b) for b in bounds), m, n)
+    return ShardReport(total, local, tuple(int(b) for b in eb), m, n, tuple(int(b) for b in hb))
 
 
 def _global_src(group) -> int:
@@ -360,6 +372,19 @@ class B200Ops(Ops):
 
     def sync(self):
         _lib.check(_lib.lib().tc_synchronize())
+
+    def shard_plan(self, graph, parts):
+        eb = np.zeros(parts + 1, dtype=np.int64)
+        hb = np.zeros(parts + 1, dtype=np.int64)
+        _lib.check(_lib.lib().tc_shard_plan(graph.handle, parts, _lib.ptr(eb), _lib.ptr(hb)))
+        return eb, hb
+
+    def count_shard(self, graph, lo, hi, hlo, hhi):
+        out = ctypes.c_uint64()
+        t = _lib.TcTimes()
+        _lib.check(_lib.lib().tc_count_shard(graph.handle, int(lo), int(hi), int(hlo), int(hhi),
+                                             ctypes.byref(out), ctypes.byref(t)))
+        return int(out.value)
 
     # ---- v2 -----------------------------------------------------------------------
     def _out(self, t):

@@ -16,15 +16,18 @@ P = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 g = make(cfg)
 og, _ = tcb.preprocess_device(g, rank_space=True)
 g.free()
-plan = tcb.PartitionPlan.work_balanced(og, P)
+from paper_1503_00576_b200.count import count_shard, shard_plan  # noqa: E402
+
+eb, hb = shard_plan(og, P)
 full = statistics.median(tcb.count_device(og)[1].count_ms for _ in range(3))
 times, tris = [], 0
 for p in range(P):
-    lo, hi = plan.pool_range(p)
-    tcb.count_device(og, lo, hi)
-    ts = [tcb.count_device(og, lo, hi) for _ in range(3)]
+    args = (og, eb[p], eb[p + 1], hb[p], hb[p + 1])
+    count_shard(*args)
+    ts = [count_shard(*args) for _ in range(3)]
     tris += ts[0][0]
     times.append(statistics.median(t[1].count_ms for t in ts))
 print(json.dumps({"config": cfg, "P": P, "full_ms": round(full, 2), "shard_ms": [round(t, 2) for t in times],
                   "max_over_mean": round(max(times) / statistics.mean(times), 3),
-                  "speedup_bound": round(full / max(times), 2), "triangles": tris}))
+                  "speedup_bound": round(full / max(times), 2), "sum_over_full": round(sum(times) / full, 3),
+                  "triangles": tris, "edge_bounds": [int(x) for x in eb], "head_bounds": [int(x) for x in hb]}))

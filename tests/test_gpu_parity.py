@@ -394,3 +394,37 @@ def test_forced_vmajor_without_hubs(golden_big):
             got[vm] = out
     assert got[1] == got[0], got
     assert got[0]["ba1e7"] == golden_big["ba_10000000_9_0"]["triangles"]
+
+
+@pytest.mark.parametrize("name", ["rmat23", "rmat16_forced", "rgg2e6"])
+def test_shard_plan_covers_every_edge_once(golden_huge, name):
+    """The multi-GPU shard plan (edge ranges for u-major/light work, head ranges for v-major
+    work): for P = 1..8 the shard counts sum to the full count, including empty shards."""
+    from paper_1503_00576_b200.count import count_shard, shard_plan
+    opts = {"vmajor": 1} if name == "rmat16_forced" else {}
+    with _lib.options(**opts):
+        if name == "rmat23":
+            g = generators.rmat_device(23, 16, seed=0)
+            want = golden_huge["rmat_23_16_0"]["triangles"]
+        elif name == "rmat16_forced":
+            g = generators.rmat_device(16, 16, seed=0)
+            want = None
+        else:
+            g = generators.random_geometric_device(2_000_000, 32.0, seed=0)
+            want = next(c for c in _golden_rgg() if c["n"] == 2_000_000)["triangles"]
+        og, _ = tcb.preprocess_device(g, rank_space=True)
+        full = tcb.count_device(og)[0]
+        if want is not None:
+            assert full == want
+        for P in (1, 2, 3, 8):
+            eb, hb = shard_plan(og, P)
+            assert eb[0] == 0 and eb[-1] == og.m_dir and hb[0] == 0 and hb[-1] == og.num_vertices
+            assert all(eb[i] <= eb[i + 1] for i in range(P)) and all(hb[i] <= hb[i + 1] for i in range(P))
+            parts = [count_shard(og, eb[r], eb[r + 1], hb[r], hb[r + 1])[0] for r in range(P)]
+            assert sum(parts) == full, (name, P, parts)
+        # degenerate shards: everything in one shard, nothing in the other
+        m, n = og.m_dir, og.num_vertices
+        assert count_shard(og, 0, m, 0, n)[0] == full
+        assert count_shard(og, 0, 0, 0, 0)[0] == 0
+        assert count_shard(og, 0, m, 0, 0)[0] + count_shard(og, m, m, 0, n)[0] == full
+        g.free()
