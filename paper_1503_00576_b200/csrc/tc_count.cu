@@ -2465,7 +2465,7 @@ int schedule_bytes_dev(const DeviceGraph &g, uint64_t lo, uint64_t hi, uint64_t 
 __global__ void __launch_bounds__(256)
     k_tile_edge_side(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
                      const uint32_t *__restrict__ off, uint64_t m, uint64_t tile, VSplit vp, bool hub,
-                     unsigned long long *__restrict__ sums) {
+                     uint32_t wlight, unsigned long long *__restrict__ sums) {
     const uint64_t b = (uint64_t)blockIdx.x * tile;
     const uint64_t e1 = b + tile < m ? b + tile : m;
     unsigned long long acc = 0;
@@ -2473,7 +2473,9 @@ __global__ void __launch_bounds__(256)
         int cls;
         uint32_t stage;
         const uint64_t x = edge_bytes(src, dst, off, e, vp, hub, &cls, &stage);
-        acc += (cls == 0 ? 0ull : x) + stage + 16;
+        // light-source bytes are random 32-byte sectors (~wlight x the time per byte of the
+        // streaming heavy-source kernels)
+        acc += (cls == 0 ? 0ull : cls == 2 ? x * wlight : x) + stage + 16;
     }
     __shared__ unsigned long long s_red[32];
     acc = warp_sum(acc);
@@ -2489,7 +2491,7 @@ __global__ void __launch_bounds__(256)
 // Head side: v-major bytes per head of the zone [z0, n) (suffix streams + index entries).
 __global__ void __launch_bounds__(256)
     k_head_side(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
-                const uint32_t *__restrict__ off, uint64_t m, VSplit vp, bool hub,
+                const uint32_t *__restrict__ off, uint64_t m, VSplit vp, bool hub, uint32_t wvlow,
                 unsigned long long *__restrict__ hb) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
@@ -2498,7 +2500,8 @@ __global__ void __launch_bounds__(256)
         int cls;
         uint32_t stage;
         const uint64_t x = edge_bytes(src, dst, off, e, vp, hub, &cls, &stage);
-        if (cls == 0) atomicAdd(hb + (v - vp.z0), (unsigned long long)x);
+        // heads below the hub zone run in the warp-task kernel (slower per byte)
+        if (cls == 0) atomicAdd(hb + (v - vp.z0), (unsigned long long)(v < vp.hz ? x * wvlow / 4 : x));
     }
 }
 
@@ -2551,9 +2554,11 @@ int shard_plan_dev(const DeviceGraph &g, int parts, int64_t *ebounds, int64_t *h
     TC_CHECK(dalloc_t(&hb, nz ? nz : 1, s));
     TC_CUDA(cudaMemsetAsync(hb, 0, (nz ? nz : 1) * sizeof(unsigned long long), s));
     if (nt) {
-        k_tile_edge_side<<<(unsigned)nt, 256, 0, s>>>(g.src, g.dst, g.off32, g.m, tile, vp, hub, sums);
+        k_tile_edge_side<<<(unsigned)nt, 256, 0, s>>>(g.src, g.dst, g.off32, g.m, tile, vp, hub,
+                                                     (uint32_t)opts().shard_wlight, sums);
         TC_LAUNCHED();
-        k_head_side<<<grid_for(g.m, 256, kSMs * 16), 256, 0, s>>>(g.src, g.dst, g.off32, g.m, vp, hub, hb);
+        k_head_side<<<grid_for(g.m, 256, kSMs * 16), 256, 0, s>>>(g.src, g.dst, g.off32, g.m, vp, hub,
+                                                                 (uint32_t)opts().shard_wvlow4, hb);
         TC_LAUNCHED();
     }
     if (nz) {

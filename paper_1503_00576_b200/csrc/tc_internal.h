@@ -62,6 +62,9 @@ struct Options {
     int64_t shard_ucap = 1024;   // cap on d+(u) in the rank-space shard model
     int64_t shard_ovh2 = 256;    // per-edge byte-equivalent overhead of shard model 2
     int64_t copy_threads = 0;    // host threads of the staged pageable H2D copy (0: auto)
+    int64_t seg_fork = 1;
+    int64_t shard_wlight = 16;   // shard plan: time weight of light-source bytes vs streamed bytes
+    int64_t shard_wvlow4 = 6;    // shard plan: weight x4 of v-major bytes of heads below the hub zone        // rank-space preprocess: size-class sorts on concurrent streams
     int64_t dense_ranks = 1 << 17;  // dense-hub bitmaps for the top ranks
     int64_t bucket = 1;          // rank-space preprocess: bucket scatter + segmented sort
     int64_t count_stats = 0;     // tc_count_with_timings fills the per-kernel-class fields

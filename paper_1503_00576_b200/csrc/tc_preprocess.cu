@@ -1107,6 +1107,13 @@ __global__ void __launch_bounds__(256)
 }  // namespace
 
 // keys: m oriented rank keys (u << vb | v), outdeg: per-source counts (consumed as cursors).
+// Side streams for independent kernels of one call (created once; callers hold the API lock).
+static cudaStream_t fork_stream(int i) {
+    static cudaStream_t ss[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (!ss[i]) cudaStreamCreateWithFlags(&ss[i], cudaStreamNonBlocking);
+    return ss[i];
+}
+
 static int bucket_csr_dev(const uint64_t *keys, uint64_t m, uint64_t n, int vb, uint32_t *outdeg,
                           DeviceGraph *out, uint32_t *max_out_dev, cudaStream_t s) {
     unsigned long long *sums = nullptr;
@@ -1136,16 +1143,38 @@ static int bucket_csr_dev(const uint64_t *keys, uint64_t m, uint64_t n, int vb, 
     const uint32_t hz = n > kHubRanks ? (uint32_t)(n - kHubRanks) : 0u;
     if (!out->hubstart) TC_CHECK(dalloc_t(&out->hubstart, n, s, out->persistent));
     uint32_t *hs = out->hubstart;
+    // The size classes sort disjoint lists: the five latency-bound sorts run concurrently
+    // (forked off s, joined back before the long-list radix pass reads `counts`).
+    const bool fork = opts().seg_fork != 0;
+    cudaEvent_t ev_fork = nullptr, ev_join[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaStream_t ss[4] = {s, s, s, s};
+    if (fork) {
+        TC_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+        TC_CUDA(cudaEventRecord(ev_fork, s));
+        for (int i = 0; i < 4; ++i) {
+            ss[i] = fork_stream(i);
+            TC_CUDA(cudaEventCreateWithFlags(&ev_join[i], cudaEventDisableTiming));
+            TC_CUDA(cudaStreamWaitEvent(ss[i], ev_fork, 0));
+        }
+    }
+    k_seg_sort4k<<<kSMs * 8 * 256 / TC_SORT4K_NT, TC_SORT4K_NT, 0, ss[0]>>>(out->off32, mid, counts + 1, out->dst, hz, hs);
+    TC_LAUNCHED();
+    k_seg_sort_warp<32><<<kSMs * 8, 256, 0, ss[1]>>>(out->off32, w1k, counts + 4, out->dst, hz, hs);
+    TC_LAUNCHED();
+    k_seg_sort_warp<8><<<kSMs * 8, 256, 0, ss[2]>>>(out->off32, w256, counts + 3, out->dst, hz, hs);
+    TC_LAUNCHED();
+    k_seg_sort64<<<kSMs * 8, 256, 0, ss[3]>>>(out->off32, warpl, counts + 0, out->dst, hz, hs);
+    TC_LAUNCHED();
     k_seg_sort16<<<grid_for(n, 256, kSMs * 16), 256, 0, s>>>(out->off32, n, out->dst, hz, hs);
     TC_LAUNCHED();
-    k_seg_sort64<<<kSMs * 8, 256, 0, s>>>(out->off32, warpl, counts + 0, out->dst, hz, hs);
-    TC_LAUNCHED();
-    k_seg_sort_warp<8><<<kSMs * 8, 256, 0, s>>>(out->off32, w256, counts + 3, out->dst, hz, hs);
-    TC_LAUNCHED();
-    k_seg_sort_warp<32><<<kSMs * 8, 256, 0, s>>>(out->off32, w1k, counts + 4, out->dst, hz, hs);
-    TC_LAUNCHED();
-    k_seg_sort4k<<<kSMs * 8 * 256 / TC_SORT4K_NT, TC_SORT4K_NT, 0, s>>>(out->off32, mid, counts + 1, out->dst, hz, hs);
-    TC_LAUNCHED();
+    if (fork) {
+        for (int i = 0; i < 4; ++i) {
+            TC_CUDA(cudaEventRecord(ev_join[i], ss[i]));
+            TC_CUDA(cudaStreamWaitEvent(s, ev_join[i], 0));
+            cudaEventDestroy(ev_join[i]);
+        }
+        cudaEventDestroy(ev_fork);
+    }
     unsigned nbig = 0;
     TC_CUDA(cudaMemcpyAsync(&nbig, counts + 2, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));

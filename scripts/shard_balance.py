@@ -20,14 +20,16 @@ from paper_1503_00576_b200.count import count_shard, shard_plan  # noqa: E402
 
 eb, hb = shard_plan(og, P)
 full = statistics.median(tcb.count_device(og)[1].count_ms for _ in range(3))
-times, tris = [], 0
+times, tris, phases = [], 0, []
 for p in range(P):
     args = (og, eb[p], eb[p + 1], hb[p], hb[p + 1])
     count_shard(*args)
     ts = [count_shard(*args) for _ in range(3)]
     tris += ts[0][0]
     times.append(statistics.median(t[1].count_ms for t in ts))
+    phases.append([round(statistics.median(getattr(t[1], k) for t in ts), 2)
+                   for k in ("vmajor_ms", "heavy_ms", "light_ms")])
 print(json.dumps({"config": cfg, "P": P, "full_ms": round(full, 2), "shard_ms": [round(t, 2) for t in times],
                   "max_over_mean": round(max(times) / statistics.mean(times), 3),
                   "speedup_bound": round(full / max(times), 2), "sum_over_full": round(sum(times) / full, 3),
-                  "triangles": tris, "edge_bounds": [int(x) for x in eb], "head_bounds": [int(x) for x in hb]}))
+                  "triangles": tris, "phases_vm_heavy_light": phases, "edge_bounds": [int(x) for x in eb], "head_bounds": [int(x) for x in hb]}))
