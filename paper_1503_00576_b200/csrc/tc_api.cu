@@ -1131,7 +1131,7 @@ const OptionName kOptionNames[] = {
     {"shard_ucap", &Options::shard_ucap},   {"dense_ranks", &Options::dense_ranks},
     {"shard_ovh2", &Options::shard_ovh2},   {"copy_threads", &Options::copy_threads},
     {"seg_fork", &Options::seg_fork},       {"shard_wlight", &Options::shard_wlight},
-    {"shard_wvlow4", &Options::shard_wvlow4},
+    {"shard_wvlow4", &Options::shard_wvlow4}, {"shard_wvedge", &Options::shard_wvedge},
     {"bucket", &Options::bucket},           {"count_stats", &Options::count_stats},
     {"hubpack", &Options::hubpack},         {"rank_primary", &Options::rank_primary},
 };

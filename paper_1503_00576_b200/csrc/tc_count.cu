@@ -2492,7 +2492,7 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     k_head_side(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
                 const uint32_t *__restrict__ off, uint64_t m, VSplit vp, bool hub, uint32_t wvlow,
-                unsigned long long *__restrict__ hb) {
+                uint32_t wvedge, unsigned long long *__restrict__ hb) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
         const uint32_t v = __ldg(dst + e);
@@ -2501,7 +2501,8 @@ __global__ void __launch_bounds__(256)
         uint32_t stage;
         const uint64_t x = edge_bytes(src, dst, off, e, vp, hub, &cls, &stage);
         // heads below the hub zone run in the warp-task kernel (slower per byte)
-        if (cls == 0) atomicAdd(hb + (v - vp.z0), (unsigned long long)(v < vp.hz ? x * wvlow / 4 : x));
+        // + wvedge per in-edge: the index fill's atomic + entry (serialised on hot heads)
+        if (cls == 0) atomicAdd(hb + (v - vp.z0), (unsigned long long)(v < vp.hz ? x * wvlow / 4 : x) + wvedge);
     }
 }
 
@@ -2558,7 +2559,8 @@ int shard_plan_dev(const DeviceGraph &g, int parts, int64_t *ebounds, int64_t *h
                                                      (uint32_t)opts().shard_wlight, sums);
         TC_LAUNCHED();
         k_head_side<<<grid_for(g.m, 256, kSMs * 16), 256, 0, s>>>(g.src, g.dst, g.off32, g.m, vp, hub,
-                                                                 (uint32_t)opts().shard_wvlow4, hb);
+                                                                 (uint32_t)opts().shard_wvlow4,
+                                                                 (uint32_t)opts().shard_wvedge, hb);
         TC_LAUNCHED();
     }
     if (nz) {

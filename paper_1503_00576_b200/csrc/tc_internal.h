@@ -64,7 +64,8 @@ struct Options {
     int64_t copy_threads = 0;    // host threads of the staged pageable H2D copy (0: auto)
     int64_t seg_fork = 1;
     int64_t shard_wlight = 16;   // shard plan: time weight of light-source bytes vs streamed bytes
-    int64_t shard_wvlow4 = 6;    // shard plan: weight x4 of v-major bytes of heads below the hub zone        // rank-space preprocess: size-class sorts on concurrent streams
+    int64_t shard_wvlow4 = 4;    // shard plan: weight x4 of v-major bytes of heads below the hub zone
+    int64_t shard_wvedge = 64;   // shard plan: byte-equivalent cost of one v-major in-edge        // rank-space preprocess: size-class sorts on concurrent streams
     int64_t dense_ranks = 1 << 17;  // dense-hub bitmaps for the top ranks
     int64_t bucket = 1;          // rank-space preprocess: bucket scatter + segmented sort
     int64_t count_stats = 0;     // tc_count_with_timings fills the per-kernel-class fields
