@@ -102,6 +102,9 @@ int tc_work_bounds(const tc_graph *g, int npools, int64_t *bounds);
  * gets 1/parts of both, and each head's bitmap is built by one shard only.  Both arrays
  * hold parts + 1 entries; the shard counts sum to the full count. */
 int tc_shard_plan(const tc_graph *g, int parts, int64_t *edge_bounds, int64_t *head_bounds);
+/* Cost features of one shard (calibration of the plan's weights; see csrc/tc_count.cu). */
+int tc_shard_stats(const tc_graph *g, int64_t lo, int64_t hi, int64_t head_lo, int64_t head_hi,
+                   uint64_t out[8]);
 int tc_count_shard(const tc_graph *g, int64_t lo, int64_t hi, int64_t head_lo, int64_t head_hi,
                    uint64_t *out, tc_times *t);
 /* merge-model work W = sum over oriented edges of d+(u) + d+(v) (roofline numerator) */

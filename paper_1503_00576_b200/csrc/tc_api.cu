@@ -820,6 +820,15 @@ int tc_shard_plan(const tc_graph *g, int parts, int64_t *edge_bounds, int64_t *h
     return shard_plan_dev(*r, parts, edge_bounds, head_bounds, g_stream);
 }
 
+int tc_shard_stats(const tc_graph *g, int64_t lo, int64_t hi, int64_t hlo, int64_t hhi, uint64_t out[8]) {
+    TC_API_GUARD();
+    TC_CHECK(ensure());
+    TC_CHECK(check_graph(g));
+    const DeviceGraph *r = nullptr;
+    TC_CHECK(rank_copy(const_cast<tc_graph *>(g), &r));
+    return shard_stats_dev(*r, (uint64_t)lo, (uint64_t)hi, (uint32_t)hlo, (uint32_t)hhi, out, g_stream);
+}
+
 int tc_count_shard(const tc_graph *g, int64_t lo, int64_t hi, int64_t hlo, int64_t hhi, uint64_t *out,
                    tc_times *t) {
     TC_API_GUARD();

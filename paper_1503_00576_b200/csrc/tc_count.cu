@@ -2519,6 +2519,68 @@ __global__ void k_head_fixed(const uint32_t *__restrict__ off, uint32_t z0, uint
     }
 }
 
+// Per-shard cost features (calibration of the shard plan's weights, scripts/shard_calib.py):
+// edge side over [lo, hi) non-v-major edges: [0] dense AND bytes, [1] sparse heavy item
+// bytes, [2] light bytes, [3] edges, [4] heavy staging bytes; head side over heads in
+// [hlo, hhi): [5] hub-head v-major bytes, [6] below-hub v-major bytes, [7] v-major edges.
+__global__ void __launch_bounds__(256)
+    k_shard_stats(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
+                  const uint32_t *__restrict__ off, uint64_t m, uint64_t lo, uint64_t hi, uint32_t hlo,
+                  uint32_t hhi, VSplit vp, bool hub, unsigned long long *__restrict__ out) {
+    unsigned long long b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+        int cls;
+        uint32_t stage;
+        const uint64_t x = edge_bytes(src, dst, off, e, vp, hub, &cls, &stage);
+        const uint32_t v = __ldg(dst + e);
+        if (cls == 0) {
+            if (v >= hlo && v < hhi) {
+                b[v >= vp.hz ? 5 : 6] += x;
+                b[7] += 1;
+            }
+        } else if (e >= lo && e < hi) {
+            b[3] += 1;
+            b[4] += stage;
+            if (cls == 2) b[2] += x;
+            else if (cls == 1) {
+                const uint32_t vs = __ldg(off + v), ve = __ldg(off + v + 1);
+                const uint32_t ws = ((v + 1 - vp.hz) >> 5) & ~3u;
+                const bool dense = hub && v >= vp.hz && v >= vp.vt && (vp.hwp - ws) < vp.factor * (ve - vs);
+                b[dense ? 0 : 1] += x;
+            }
+        }
+    }
+    for (int k = 0; k < 8; ++k) {
+        unsigned long long x = b[k];
+        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(TC_FULL_MASK, x, o);
+        if (lane_id() == 0 && x) atomicAdd(out + k, x);
+    }
+}
+
+int shard_stats_dev(const DeviceGraph &g, uint64_t lo, uint64_t hi, uint32_t hlo, uint32_t hhi, uint64_t out[8],
+                    cudaStream_t s) {
+    if (!g.off32 || !g.rank_space || !g.hubstart) {
+        set_error("shard stats need a rank-space graph with m < 2^32");
+        return -1;
+    }
+    unsigned long long *d = nullptr;
+    TC_CHECK(dalloc_t(&d, 8, s));
+    TC_CUDA(cudaMemsetAsync(d, 0, 8 * sizeof(unsigned long long), s));
+    if (g.m) {
+        k_shard_stats<<<grid_for(g.m, 256, kSMs * 16), 256, 0, s>>>(g.src, g.dst, g.off32, g.m, lo, hi, hlo, hhi,
+                                                                   make_vsplit(g, vmajor_schedule(g)),
+                                                                   g.dense_bits != nullptr, d);
+        TC_LAUNCHED();
+    }
+    unsigned long long h[8];
+    TC_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    dfree(d, s);
+    for (int k = 0; k < 8; ++k) out[k] = h[k];
+    return 0;
+}
+
 static void cut_prefix(const unsigned long long *h, uint64_t nt, int parts, uint64_t unit, uint64_t cap,
                        int64_t *bounds, int64_t base) {
     unsigned long long W = 0;

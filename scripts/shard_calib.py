@@ -1,7 +1,7 @@
-"""Development aid (GPU): per-shard count times beside the shard's schedule bytes by class,
-for several partitions of the R-MAT rank-space CSR -- the data the rank-space shard cost
-model is fitted to.  python scripts/shard_calib.py CFG > gpurun_out/shard_calib.jsonl"""
-import ctypes
+"""Development aid (GPU): per-shard cost features (tc_shard_stats) beside the measured
+per-phase times of tc_count_shard, over several shard plans of the R-MAT rank-space CSR --
+the data the shard plan's class weights are fitted to.
+    python scripts/shard_calib.py rmat26 > gpurun_out/shard_calib.jsonl"""
 import json
 import statistics
 import sys
@@ -11,6 +11,7 @@ import numpy as np
 sys.path.insert(0, ".")
 import paper_1503_00576_b200 as tcb  # noqa: E402
 from paper_1503_00576_b200 import _lib  # noqa: E402
+from paper_1503_00576_b200.count import count_shard, shard_plan  # noqa: E402
 from scripts import devopts  # noqa: E402
 
 devopts.apply()
@@ -20,25 +21,24 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "rmat26"
 g = make(cfg)
 og, _ = tcb.preprocess_device(g, rank_space=True)
 g.free()
-m = og.m_dir
 h = og.device().handle
-src = og.edge_src  # host copy for per-shard source counts
-plans = {"even16": np.linspace(0, m, 17).astype(np.int64),
-         "model0_16": np.array(tcb.PartitionPlan.work_balanced(og, 16).bounds, np.int64),
-         "even8": np.linspace(0, m, 9).astype(np.int64)}
-for name, b in plans.items():
-    for p in range(len(b) - 1):
-        lo, hi = int(b[p]), int(b[p + 1])
-        out = np.zeros(5, np.uint64)
-        _lib.check(_lib.lib().tc_schedule_bytes_range(h, lo, hi, _lib.ptr(out)))
+plans = []
+for P, wl, wv, we in ((8, 16, 6, 0), (8, 32, 4, 64), (8, 4, 8, 256), (4, 16, 4, 64), (16, 8, 4, 0)):
+    with _lib.options(shard_wlight=wl, shard_wvlow4=wv, shard_wvedge=we):
+        plans.append((f"P{P}_wl{wl}_wv{wv}_we{we}",) + shard_plan(og, P))
+for name, eb, hb in plans:
+    for p in range(len(eb) - 1):
+        a = (og, eb[p], eb[p + 1], hb[p], hb[p + 1])
+        out = np.zeros(8, np.uint64)
+        _lib.check(_lib.lib().tc_shard_stats(h, int(eb[p]), int(eb[p + 1]), int(hb[p]), int(hb[p + 1]),
+                                             _lib.ptr(out)))
         with _lib.options(count_stats=1):
-            tcb.count_device(og, lo, hi)
-            ts = [tcb.count_device(og, lo, hi)[1] for _ in range(3)]
-        rec = {"plan": name, "p": p, "lo": lo, "hi": hi, "edges": hi - lo,
-               "sources": int(src[hi - 1]) - int(src[lo]) + 1,
-               "bytes": [int(x) for x in out],
+            count_shard(*a)
+            ts = [count_shard(*a)[1] for _ in range(3)]
+        rec = {"plan": name, "p": p, "stats": [int(x) for x in out],
                "ms": statistics.median(t.count_ms for t in ts),
                "vmajor_ms": statistics.median(t.vmajor_ms for t in ts),
                "heavy_ms": statistics.median(t.heavy_ms for t in ts),
-               "light_ms": statistics.median(t.light_ms for t in ts)}
+               "light_ms": statistics.median(t.light_ms for t in ts),
+               "classify_ms": statistics.median(t.classify_ms for t in ts)}
         print(json.dumps(rec), flush=True)
