@@ -1139,8 +1139,11 @@ const OptionName kOptionNames[] = {
     {"shard_model", &Options::shard_model}, {"shard_ovh", &Options::shard_ovh},
     {"shard_ucap", &Options::shard_ucap},   {"dense_ranks", &Options::dense_ranks},
     {"shard_ovh2", &Options::shard_ovh2},   {"copy_threads", &Options::copy_threads},
-    {"seg_fork", &Options::seg_fork},       {"shard_wlight", &Options::shard_wlight},
-    {"shard_wvlow4", &Options::shard_wvlow4}, {"shard_wvedge", &Options::shard_wvedge},
+    {"seg_fork", &Options::seg_fork},
+    {"shard_w_dense", &Options::shard_w_dense}, {"shard_w_sparse", &Options::shard_w_sparse},
+    {"shard_w_light", &Options::shard_w_light}, {"shard_w_stage", &Options::shard_w_stage},
+    {"shard_w_edge", &Options::shard_w_edge},   {"shard_w_hub", &Options::shard_w_hub},
+    {"shard_w_vlow", &Options::shard_w_vlow},   {"shard_w_vedge", &Options::shard_w_vedge},
     {"bucket", &Options::bucket},           {"count_stats", &Options::count_stats},
     {"hubpack", &Options::hubpack},         {"rank_primary", &Options::rank_primary},
 };

@@ -2363,7 +2363,7 @@ int work_bounds_dev(const DeviceGraph &g, int npools, int64_t *bounds, cudaStrea
 // Bytes of edge e under the schedule; *cls = 0..3 (v-major, u-major heavy, light, none).
 __device__ __forceinline__ uint64_t edge_bytes(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
                                                const uint32_t *__restrict__ off, uint64_t e, const VSplit &vp,
-                                               bool hub, int *cls, uint32_t *stage) {
+                                               bool hub, int *cls, uint32_t *stage, bool *dense_out = nullptr) {
     const uint32_t u = __ldg(src + e), su = __ldg(off + u), eu = __ldg(off + u + 1), du = eu - su;
     const uint32_t v = __ldg(dst + e), vs = __ldg(off + v), ve = __ldg(off + v + 1), dv = ve - vs;
     *stage = e == su && du > (uint32_t)kLightMax ? 4u * du : 0u;
@@ -2379,8 +2379,12 @@ __device__ __forceinline__ uint64_t edge_bytes(const uint32_t *__restrict__ src,
         uint64_t x = 4ull * dv;
         if (hub && v >= vp.hz) {
             const uint32_t ws = ((v + 1 - vp.hz) >> 5) & ~3u;
-            if (v >= vp.vt && (vp.hwp - ws) < vp.factor * dv) x = 4ull * (vp.hwp - ws);
-            else if (vp.packed) x = 9ull * ((dv + 3) / 4);
+            if (v >= vp.vt && (vp.hwp - ws) < vp.factor * dv) {
+                x = 4ull * (vp.hwp - ws);
+                if (dense_out) *dense_out = true;
+            } else if (vp.packed) {
+                x = 9ull * ((dv + 3) / 4);
+            }
         }
         return x;
     }
@@ -2461,21 +2465,31 @@ int schedule_bytes_dev(const DeviceGraph &g, uint64_t lo, uint64_t hi, uint64_t 
 }
 
 // ---------------------------------------------------------------- shard plan ---
+// Time per byte of each class, in 1/1000 ps, fitted to per-shard phase times of R-MAT s26
+// shards on one B200 (scripts/shard_calib.py, profiles/r02_shard_calib_s26.jsonl; nnls,
+// max rel. error 0.27 edge side / 0.21 head side): dense-head ANDs stream L2-resident
+// bitmaps (0.118 ps/B), sparse heavy items 0.273, light sources pay random 32-byte sectors
+// (5.5), a heavy source's staging ~18 per staged byte (task setup); v-major suffix bytes
+// of hub heads 0.153, of heads below the hub zone (warp tasks) 0.30, plus 62 ps per in-edge
+// (index fill).  Each side is balanced separately, so every shard gets 1/P of both.
+struct ShardWeights {
+    uint64_t dense, sparse, light, stage, edge, hub, vlow, vedge;
+};
 // Edge side: per-tile bytes of the NON-v-major edges (u-major heavy, light, per-edge, staging).
 __global__ void __launch_bounds__(256)
     k_tile_edge_side(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
                      const uint32_t *__restrict__ off, uint64_t m, uint64_t tile, VSplit vp, bool hub,
-                     uint32_t wlight, unsigned long long *__restrict__ sums) {
+                     ShardWeights w, unsigned long long *__restrict__ sums) {
     const uint64_t b = (uint64_t)blockIdx.x * tile;
     const uint64_t e1 = b + tile < m ? b + tile : m;
     unsigned long long acc = 0;
     for (uint64_t e = b + threadIdx.x; e < e1; e += blockDim.x) {
         int cls;
         uint32_t stage;
-        const uint64_t x = edge_bytes(src, dst, off, e, vp, hub, &cls, &stage);
-        // light-source bytes are random 32-byte sectors (~wlight x the time per byte of the
-        // streaming heavy-source kernels)
-        acc += (cls == 0 ? 0ull : cls == 2 ? x * wlight : x) + stage + 16;
+        bool dense = false;
+        const uint64_t x = edge_bytes(src, dst, off, e, vp, hub, &cls, &stage, &dense);
+        acc += (cls == 1 ? x * (dense ? w.dense : w.sparse) : cls == 2 ? x * w.light : 0ull) +
+               (uint64_t)stage * w.stage + w.edge;
     }
     __shared__ unsigned long long s_red[32];
     acc = warp_sum(acc);
@@ -2491,8 +2505,8 @@ __global__ void __launch_bounds__(256)
 // Head side: v-major bytes per head of the zone [z0, n) (suffix streams + index entries).
 __global__ void __launch_bounds__(256)
     k_head_side(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
-                const uint32_t *__restrict__ off, uint64_t m, VSplit vp, bool hub, uint32_t wvlow,
-                uint32_t wvedge, unsigned long long *__restrict__ hb) {
+                const uint32_t *__restrict__ off, uint64_t m, VSplit vp, bool hub, ShardWeights w,
+                unsigned long long *__restrict__ hb) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
         const uint32_t v = __ldg(dst + e);
@@ -2501,21 +2515,21 @@ __global__ void __launch_bounds__(256)
         uint32_t stage;
         const uint64_t x = edge_bytes(src, dst, off, e, vp, hub, &cls, &stage);
         // heads below the hub zone run in the warp-task kernel (slower per byte)
-        // + wvedge per in-edge: the index fill's atomic + entry (serialised on hot heads)
-        if (cls == 0) atomicAdd(hb + (v - vp.z0), (unsigned long long)(v < vp.hz ? x * wvlow / 4 : x) + wvedge);
+        // + w.vedge per in-edge: the index fill's atomic + entry
+        if (cls == 0) atomicAdd(hb + (v - vp.z0), x * (v < vp.hz ? w.vlow : w.hub) + w.vedge);
     }
 }
 
 // + the per-task cost of a head that has v-major in-edges: zeroing its bitmap words and
 // staging adj(v).
 __global__ void k_head_fixed(const uint32_t *__restrict__ off, uint32_t z0, uint32_t nz, VSplit vp,
-                             unsigned long long *__restrict__ hb) {
+                             ShardWeights w, unsigned long long *__restrict__ hb) {
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < nz; h += stride) {
         if (!hb[h]) continue;
         const uint32_t v = z0 + h;
         const uint32_t ws = v >= vp.hz ? ((v + 1 - vp.hz) >> 5) & ~3u : 0u;
-        hb[h] += 4ull * (vp.hwp - ws) + 4ull * (off[v + 1] - off[v]);
+        hb[h] += (4ull * (vp.hwp - ws) + 4ull * (off[v + 1] - off[v])) * w.hub;
     }
 }
 
@@ -2607,6 +2621,10 @@ int shard_plan_dev(const DeviceGraph &g, int parts, int64_t *ebounds, int64_t *h
     if (!vm) return work_bounds_dev(g, parts, ebounds, s);
     const VSplit vp = make_vsplit(g, true);
     const bool hub = g.dense_bits != nullptr;
+    const Options &o = opts();
+    const ShardWeights w{(uint64_t)o.shard_w_dense, (uint64_t)o.shard_w_sparse, (uint64_t)o.shard_w_light,
+                         (uint64_t)o.shard_w_stage, (uint64_t)o.shard_w_edge, (uint64_t)o.shard_w_hub,
+                         (uint64_t)o.shard_w_vlow, (uint64_t)o.shard_w_vedge};
     uint64_t tile = g.m / ((uint64_t)parts * 1024);
     if (tile < 1) tile = 1;
     if (tile > 4096) tile = 4096;
@@ -2617,16 +2635,13 @@ int shard_plan_dev(const DeviceGraph &g, int parts, int64_t *ebounds, int64_t *h
     TC_CHECK(dalloc_t(&hb, nz ? nz : 1, s));
     TC_CUDA(cudaMemsetAsync(hb, 0, (nz ? nz : 1) * sizeof(unsigned long long), s));
     if (nt) {
-        k_tile_edge_side<<<(unsigned)nt, 256, 0, s>>>(g.src, g.dst, g.off32, g.m, tile, vp, hub,
-                                                     (uint32_t)opts().shard_wlight, sums);
+        k_tile_edge_side<<<(unsigned)nt, 256, 0, s>>>(g.src, g.dst, g.off32, g.m, tile, vp, hub, w, sums);
         TC_LAUNCHED();
-        k_head_side<<<grid_for(g.m, 256, kSMs * 16), 256, 0, s>>>(g.src, g.dst, g.off32, g.m, vp, hub,
-                                                                 (uint32_t)opts().shard_wvlow4,
-                                                                 (uint32_t)opts().shard_wvedge, hb);
+        k_head_side<<<grid_for(g.m, 256, kSMs * 16), 256, 0, s>>>(g.src, g.dst, g.off32, g.m, vp, hub, w, hb);
         TC_LAUNCHED();
     }
     if (nz) {
-        k_head_fixed<<<grid_for(nz, 256, kSMs * 4), 256, 0, s>>>(g.off32, z0, nz, vp, hb);
+        k_head_fixed<<<grid_for(nz, 256, kSMs * 4), 256, 0, s>>>(g.off32, z0, nz, vp, w, hb);
         TC_LAUNCHED();
     }
     unsigned long long *h = (unsigned long long *)malloc(((nt > nz ? nt : nz) + 1) * sizeof(unsigned long long));

@@ -62,15 +62,15 @@ struct Options {
     int64_t shard_ucap = 1024;   // cap on d+(u) in the rank-space shard model
     int64_t shard_ovh2 = 256;    // per-edge byte-equivalent overhead of shard model 2
     int64_t copy_threads = 0;    // host threads of the staged pageable H2D copy (0: auto)
-    int64_t seg_fork = 1;
-    int64_t shard_wlight = 16;   // shard plan: time weight of light-source bytes vs streamed bytes
-    int64_t shard_wvlow4 = 4;    // shard plan: weight x4 of v-major bytes of heads below the hub zone
-    int64_t shard_wvedge = 64;   // shard plan: byte-equivalent cost of one v-major in-edge        // rank-space preprocess: size-class sorts on concurrent streams
+    int64_t seg_fork = 1;        // rank-space preprocess: size-class sorts on concurrent streams
     int64_t dense_ranks = 1 << 17;  // dense-hub bitmaps for the top ranks
     int64_t bucket = 1;          // rank-space preprocess: bucket scatter + segmented sort
     int64_t count_stats = 0;     // tc_count_with_timings fills the per-kernel-class fields
     int64_t hubpack = 0;         // 1: hub-head suffixes read from an 18-bit packed copy (slower)
     int64_t rank_primary = 1;    // tc_preprocess builds the rank-space CSR, reference ids lazily
+    // shard plan class weights (1/1000 ps per byte; per edge / in-edge), fitted -- tc_count.cu
+    int64_t shard_w_dense = 118, shard_w_sparse = 273, shard_w_light = 5500, shard_w_stage = 18000;
+    int64_t shard_w_edge = 0, shard_w_hub = 153, shard_w_vlow = 300, shard_w_vedge = 62000;
 };
 Options &opts();
 

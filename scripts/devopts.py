@@ -5,7 +5,9 @@ import os
 
 NAMES = ("vmajor", "vzone_log2", "vlow_all", "vm_bias", "dense_factor", "hub_unroll", "l2_persist_mb",
          "l2_target", "concurrent", "share", "midwarp", "light", "skew", "light_vec", "shard_model",
-         "shard_ovh", "shard_ucap", "dense_ranks", "bucket", "count_stats", "hubpack", "rank_primary", "shard_ovh2", "copy_threads", "seg_fork", "shard_wlight", "shard_wvlow4", "shard_wvedge")
+         "shard_ovh", "shard_ucap", "dense_ranks", "bucket", "count_stats", "hubpack", "rank_primary",
+         "shard_ovh2", "copy_threads", "seg_fork", "shard_w_dense", "shard_w_sparse", "shard_w_light",
+         "shard_w_stage", "shard_w_edge", "shard_w_hub", "shard_w_vlow", "shard_w_vedge")
 
 
 def apply():

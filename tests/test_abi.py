@@ -70,3 +70,23 @@ def test_product_sources_never_read_the_environment():
     for name in os.listdir(csrc):
         if name.endswith((".cu", ".cuh", ".h", ".cpp")):
             assert "getenv" not in open(os.path.join(csrc, name)).read(), name
+
+
+def test_schedule_option_names():
+    """Every option the development probes know is accepted by tc_set_option (no GPU
+    needed); unknown names fail with -1 and defaults come back after tc_reset_options."""
+    import ctypes
+
+    from paper_1503_00576_b200 import _lib
+    from scripts import devopts
+
+    L = _lib.load(init=False)
+    for name in devopts.NAMES:
+        v = ctypes.c_int64()
+        assert L.tc_get_option(name.encode(), ctypes.byref(v)) == 0, name
+        default = v.value
+        assert L.tc_set_option(name.encode(), default + 1) == 0, name
+        assert L.tc_get_option(name.encode(), ctypes.byref(v)) == 0 and v.value == default + 1
+        assert L.tc_reset_options() == 0
+        assert L.tc_get_option(name.encode(), ctypes.byref(v)) == 0 and v.value == default
+    assert L.tc_set_option(b"no_such_option", 1) == -1
