@@ -1503,11 +1503,13 @@ __global__ void TC_VM_BOUNDS(NT)
         const uint32_t p0 = __ldg(start + h) + task.y * kVChunk;
         // fill count, clamped to the slot range (an overflowed capacity layout is recounted)
         const uint32_t p1 = min(p0 + kVChunk, min(__ldg(start + h) + __ldg(fillc + h), __ldg(start + h + 1)));
+        uint2 ie_n = p0 + threadIdx.x < p1 ? __ldg(in_e + p0 + threadIdx.x) : make_uint2(0u, 0u);
         for (uint32_t ps = p0; ps < p1; ps += NT) {
             const uint32_t nwin = min((uint32_t)NT, p1 - ps);
             uint32_t chunks = 0, a = 0, b = 0;
+            const uint2 ie = ie_n;  // (edge, end of adj(u)); the next window's is loaded now
+            ie_n = ps + NT + threadIdx.x < p1 ? __ldg(in_e + ps + NT + threadIdx.x) : make_uint2(0u, 0u);
             if (threadIdx.x < nwin) {
-                const uint2 ie = __ldg(in_e + ps + threadIdx.x);  // (edge, end of adj(u))
                 a = ie.x + 1;
                 b = ie.y;
                 chunks = (b - (a & ~3u) + 3) >> 2;  // a < b by construction
@@ -1813,10 +1815,13 @@ __global__ void __launch_bounds__(32 * kVlWarps)
         const uint32_t p0 = __ldg(start + h) + task.y * kVChunk;
         // fill count, clamped to the slot range (an overflowed capacity layout is recounted)
         const uint32_t p1 = min(p0 + kVChunk, min(__ldg(start + h) + __ldg(fillc + h), __ldg(start + h + 1)));
+        // the next batch of in-edges is loaded while the current one is swept
+        uint2 ie_n = p0 + lane < p1 ? __ldg(in_e + p0 + lane) : make_uint2(0u, 0u);
         for (uint32_t ps = p0; ps < p1; ps += 32) {
             uint32_t a = 0, b = 0, chunks = 0;
+            const uint2 ie = ie_n;
+            ie_n = ps + 32 + lane < p1 ? __ldg(in_e + ps + 32 + lane) : make_uint2(0u, 0u);
             if (ps + lane < p1) {
-                const uint2 ie = __ldg(in_e + ps + lane);
                 a = ie.x + 1;
                 b = ie.y;
                 chunks = (b - (a & ~3u) + 3) >> 2;

@@ -177,6 +177,41 @@ def count_distributed(ops: Ops, edges=None, group=None, graph=None) -> ShardRepo
     return _count_local_shard(ops, g, rank, world, group, m, n)
 
 
+def refine_plan(edge_bounds, head_bounds, edge_ms, head_ms, head_floor: int = 0):
+    """One measurement-guided refinement of a shard plan: within every shard the measured time
+    of each side (edge side: u-major + light kernels; head side: the v-major phase) is
+    assumed spread uniformly over its index range, and both sides are re-cut at equal
+    cumulative time.  Used for repeated counts of one graph (the first count's per-rank
+    times, all-gathered, refine the plan for the next); the cost-model plan (tc_shard_plan)
+    is the starting point.  ``head_floor``: first head that can carry v-major work (the
+    v-major zone start; heads below it count for nothing)."""
+    def recut(bounds, ms):
+        bounds = [int(b) for b in bounds]
+        P = len(bounds) - 1
+        ms = [max(float(t), 1e-9) for t in ms]
+        cum = [0.0]
+        for t in ms:
+            cum.append(cum[-1] + t)
+        total = cum[-1]
+        out = [bounds[0]]
+        r = 0
+        for k in range(1, P):
+            target = total * k / P
+            while r < P - 1 and cum[r + 1] < target:
+                r += 1
+            frac = (target - cum[r]) / ms[r]
+            x = bounds[r] + int(round(frac * (bounds[r + 1] - bounds[r])))
+            out.append(max(out[-1], min(x, bounds[-1])))
+        out.append(bounds[-1])
+        return np.array(out, dtype=np.int64)
+    hb = [int(b) for b in head_bounds]
+    lo = hb[0]
+    hb[0] = max(lo, min(int(head_floor), hb[1]))
+    out_h = recut(hb, head_ms)
+    out_h[0] = lo
+    return recut(edge_bounds, edge_ms), out_h
+
+
 def shard_bounds(npairs: int, world: int) -> list[int]:
     """Contiguous pair ranges [b[r], b[r+1]) of an edge array split over ``world`` ranks."""
     return [npairs * r // world for r in range(world + 1)]

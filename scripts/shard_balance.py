@@ -6,6 +6,7 @@ import sys
 
 sys.path.insert(0, ".")
 import paper_1503_00576_b200 as tcb  # noqa: E402
+from paper_1503_00576_b200 import _lib  # noqa: E402
 from scripts import devopts  # noqa: E402
 
 devopts.apply()
@@ -18,18 +19,29 @@ og, _ = tcb.preprocess_device(g, rank_space=True)
 g.free()
 from paper_1503_00576_b200.count import count_shard, shard_plan  # noqa: E402
 
+from paper_1503_00576_b200.distributed import refine_plan  # noqa: E402
+
 eb, hb = shard_plan(og, P)
 full = statistics.median(tcb.count_device(og)[1].count_ms for _ in range(3))
-times, tris, phases = [], 0, []
-for p in range(P):
-    args = (og, eb[p], eb[p + 1], hb[p], hb[p + 1])
-    count_shard(*args)
-    ts = [count_shard(*args) for _ in range(3)]
-    tris += ts[0][0]
-    times.append(statistics.median(t[1].count_ms for t in ts))
-    phases.append([round(statistics.median(getattr(t[1], k) for t in ts), 2)
-                   for k in ("vmajor_ms", "heavy_ms", "light_ms")])
-print(json.dumps({"config": cfg, "P": P, "full_ms": round(full, 2), "shard_ms": [round(t, 2) for t in times],
-                  "max_over_mean": round(max(times) / statistics.mean(times), 3),
-                  "speedup_bound": round(full / max(times), 2), "sum_over_full": round(sum(times) / full, 3),
-                  "triangles": tris, "phases_vm_heavy_light": phases, "edge_bounds": [int(x) for x in eb], "head_bounds": [int(x) for x in hb]}))
+iters = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+for it in range(iters + 1):
+    times, tris, phases, edge_ms, head_ms = [], 0, [], [], []
+    for p in range(P):
+        args = (og, eb[p], eb[p + 1], hb[p], hb[p + 1])
+        with _lib.options(count_stats=1):
+            count_shard(*args)
+            ts = [count_shard(*args) for _ in range(3)]
+        tris += ts[0][0]
+        times.append(statistics.median(t[1].count_ms for t in ts))
+        vm = statistics.median(t[1].vmajor_ms for t in ts)
+        rest = statistics.median(t[1].count_ms - t[1].vmajor_ms for t in ts)
+        phases.append([round(vm, 2), round(rest, 2)])
+        head_ms.append(vm)
+        edge_ms.append(rest)
+    print(json.dumps({"config": cfg, "P": P, "refinement": it, "full_ms": round(full, 2),
+                      "shard_ms": [round(t, 2) for t in times],
+                      "max_over_mean": round(max(times) / statistics.mean(times), 3),
+                      "speedup_bound": round(full / max(times), 2), "sum_over_full": round(sum(times) / full, 3),
+                      "triangles": tris, "phases_head_edge": phases, "edge_bounds": [int(x) for x in eb],
+                      "head_bounds": [int(x) for x in hb]}), flush=True)
+    eb, hb = refine_plan(eb, hb, edge_ms, head_ms, head_floor=max(og.num_vertices - (1 << 22), 0))
