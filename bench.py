@@ -41,6 +41,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["rmat", "er", "ba", "rgg"], default="rmat",
+                    help="BASELINE.json configs: rmat (--scale, default 26 = the metric's config; 20 = "
+                         "configs[1]), er = configs[0] G(10^4, p = 10^5 / C(10^4, 2)), ba = configs[2] "
+                         "BA(10^7, 9), rgg = configs[4] RGG(2*10^7, deg 32)")
     ap.add_argument("--scale", type=int, default=26)
     ap.add_argument("--edge-factor", type=int, default=16)
     ap.add_argument("--seed", type=int, default=0)
@@ -182,7 +186,7 @@ class CpuPath:
                 "sample": (f"oracle C port (reference preprocess.py:74-84 + count.py:63-99 restated), "
                            f"{self.threads} threads: preprocess of ALL {2 * self.m} pairs timed in full "
                            f"({self.preprocess_s:.1f} s); count of {len(self.samples)} random contiguous "
-                           f"chunks of {CPU_CHUNK} oriented edges ({e} edges, {100.0 * e / self.m:.2f} % of m, "
+                           f"chunks of {min(CPU_CHUNK, self.m)} oriented edges ({e} edges, {100.0 * e / self.m:.2f} % of m, "
                            f"{100.0 * w / self.W:.2f} % of the merge work W, {t:.1f} s) counted as the "
                            f"reference counts a range, extrapolated by merge work to {t_cnt:.1f} s")}
 
@@ -273,6 +277,49 @@ def roofline_block(sched: dict, med: dict, peak: float, peak_src: str, W: int, m
             "peak_source": peak_src}
 
 
+# --------------------------------------------------------------------- workloads ---
+ER_N, ER_M = 10_000, 100_000  # BASELINE configs[0]: G(n = 10^4, m = 10^5) -> gnp(n, m / C(n, 2))
+
+
+def rmat_params(args) -> dict:
+    return {"scale": args.scale, "edge_factor": args.edge_factor} if args.workload == "rmat" else {}
+
+
+def workload_name(args) -> str:
+    if args.workload == "er":
+        return f"er_n1e4_m1e5_seed{args.seed}"
+    if args.workload == "ba":
+        return f"ba_n1e7_m9_seed{args.seed}"
+    if args.workload == "rgg":
+        return f"rgg_n2e7_deg32_seed{args.seed}"
+    return f"rmat_s{args.scale}_ef{args.edge_factor}_seed{args.seed}"
+
+
+def device_input(args, generators):
+    """The workload's edge array in HBM, produced by the product's generators (bit-identical to
+    the reference generators / the oracle's RGG definition; untimed)."""
+    import math
+    if args.workload == "er":
+        return generators.to_device(generators.gnp(ER_N, ER_M / math.comb(ER_N, 2), seed=args.seed))
+    if args.workload == "ba":
+        return generators.barabasi_albert_device(10_000_000, 9, seed=args.seed)
+    if args.workload == "rgg":
+        return generators.random_geometric_device(20_000_000, 32.0, seed=args.seed)
+    return generators.rmat_device(args.scale, args.edge_factor, seed=args.seed)
+
+
+def oracle_input(args, oracle, threads):
+    """The same edge array from the oracle's restatements (reference arm: no product code)."""
+    import math
+    if args.workload == "er":
+        return oracle.gnp_pairs(ER_N, ER_M / math.comb(ER_N, 2), seed=args.seed)
+    if args.workload == "ba":
+        return oracle.ba_pairs(10_000_000, 9, seed=args.seed)
+    if args.workload == "rgg":
+        return oracle.rgg_pairs(20_000_000, 32.0, seed=args.seed)
+    return oracle.rmat_edges(args.scale, args.edge_factor, seed=args.seed, threads=threads)
+
+
 # ------------------------------------------------------------------------ main ---
 def main():
     args = parse()
@@ -282,7 +329,7 @@ def main():
     if args.share_gpu:
         local = 0
     os.environ.setdefault("TC_DEVICE", str(local))
-    workload = f"rmat_s{args.scale}_ef{args.edge_factor}_seed{args.seed}"
+    workload = workload_name(args)
 
     if args.impl == "reference":
         return reference_arm(args, world, rank, workload)
@@ -333,7 +380,7 @@ def main():
         return float(t.item())
 
     t0 = time.time()
-    dev_edges = generators.rmat_device(args.scale, args.edge_factor, seed=args.seed)
+    dev_edges = device_input(args, generators)
     gen_s = time.time() - t0
     npairs = dev_edges.npairs
     m = npairs // 2
@@ -455,7 +502,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u32/u64 (integer)", "data": "synthetic (reference rmat generator, device-reproduced)",
-            "config": {"workload": workload, "scale": args.scale, "edge_factor": args.edge_factor,
+            "config": {"workload": workload, **rmat_params(args),
                        "seed": args.seed, "num_vertices": dev_edges.num_vertices,
                        "undirected_edges": m, "pairs": npairs, "triangles": tri_ref,
                        "merge_work_W": W, "inputs_vs_L2": "inputs 8*pairs bytes >> 126 MB L2; no flush",
@@ -492,7 +539,7 @@ def reference_arm(args, world, rank, workload):
     assert "paper_1503_00576_b200" not in sys.modules
     threads = os.cpu_count() or 1
     t0 = time.perf_counter()
-    pairs = oracle.rmat_edges(args.scale, args.edge_factor, seed=args.seed, threads=threads)
+    pairs = oracle_input(args, oracle, threads)
     gen_s = time.perf_counter() - t0
     n = int(pairs.max()) + 1 if pairs.size else 0
     cp = CpuPath(pairs, n, threads)
@@ -517,7 +564,7 @@ def reference_arm(args, world, rank, workload):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u32/u64 (integer)",
             "data": "synthetic (reference rmat generator restated in the oracle, bit-identical)",
-            "config": {"workload": workload, "scale": args.scale, "edge_factor": args.edge_factor,
+            "config": {"workload": workload, **rmat_params(args),
                        "seed": args.seed, "num_vertices": n, "undirected_edges": cp.m,
                        "merge_work_W": cp.W, "threads": threads},
             "impl": "reference", "cpu_baseline": cpu,

@@ -191,3 +191,34 @@ def barabasi_albert(n: int, m_attach: int, seed: int = 0, pinned: bool = True) -
         return dev.to_host(pinned=pinned)
     finally:
         dev.free()
+
+
+def gnp(n: int, p: float, seed: int = 0) -> EdgeArray:
+    """Reference generators.py:186-200 (G(n, p) row by row from numpy default_rng(seed)):
+    for every u, the hits of rng.random(n - u - 1) < p are u's higher neighbours; both
+    directions, lexicographically sorted.  Host-side input production (BASELINE config 1 is
+    G(n = 10^4, p = 10^5 / C(n, 2))); the sort of the symmetrised pairs runs on the device."""
+    if n < 0 or not 0.0 <= p <= 1.0:
+        raise ValueError("gnp: n >= 0 and 0 <= p <= 1 required")
+    rng = np.random.default_rng(seed)
+    rows = []
+    for u in range(n - 1):
+        hits = np.flatnonzero(rng.random(n - u - 1) < p)
+        if hits.size:
+            rows.append(np.stack([np.full(hits.size, u, np.uint32), (hits + u + 1).astype(np.uint32)], axis=1))
+    if not rows:
+        return EdgeArray(np.zeros((0, 2), np.uint32), num_vertices=0)
+    canon = np.concatenate(rows)
+    both = np.ascontiguousarray(np.concatenate([canon, canon[:, ::-1]]))
+    from .preprocess import sort_edges
+    return sort_edges(EdgeArray(both))
+
+
+def to_device(g: EdgeArray) -> DeviceEdges:
+    """Copy a host edge array into library-owned HBM (untimed input staging)."""
+    e = np.ascontiguousarray(g.edges)
+    p = ctypes.c_void_p()
+    _lib.check(_lib.lib().tc_device_alloc(max(e.nbytes, 16), ctypes.byref(p)))
+    if e.size:
+        _lib.check(_lib.lib().tc_memcpy(p, _lib.ptr(e), e.nbytes, 0))
+    return DeviceEdges(p.value, e.shape[0], g.num_vertices)

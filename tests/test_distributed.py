@@ -207,3 +207,29 @@ def test_count_distributed_sharded_gloo(golden, world, shuffle):
     for r in res:
         assert r[4] == rec["m"]
         assert np.array_equal(r[6], dst) and np.array_equal(r[7], off)
+
+
+def test_refine_plan_equalises_measured_times():
+    """refine_plan re-cuts both sides at equal cumulative measured time (uniform within a
+    shard); a plan whose shards already take equal time is a fixed point; heads below the
+    floor carry no work."""
+    from paper_1503_00576_b200.distributed import refine_plan
+    eb, hb = [0, 100, 200, 300, 400], [0, 1000, 1010, 1020, 1030]
+    e2, h2 = refine_plan(eb, hb, [1, 1, 1, 1], [2, 2, 2, 2], head_floor=990)
+    assert list(e2) == eb
+    assert h2[0] == 0 and h2[-1] == 1030 and list(h2[2:]) == [1010, 1020, 1030]
+    e3, _ = refine_plan(eb, hb, [3, 1, 1, 3], [1, 1, 1, 1], head_floor=990)
+    assert e3[0] == 0 and e3[-1] == 400 and list(e3) == sorted(e3)
+    # equal time per shard under the uniform-density assumption
+    dens = [3 / 100, 1 / 100, 1 / 100, 3 / 100]
+
+    def t(a, b):
+        tot, x = 0.0, a
+        while x < b:
+            k = min(x // 100, 3)
+            nxt = min(b, (k + 1) * 100)
+            tot += (nxt - x) * dens[k]
+            x = nxt
+        return tot
+    parts = [t(e3[i], e3[i + 1]) for i in range(4)]
+    assert max(parts) - min(parts) < 0.05
