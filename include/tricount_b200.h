@@ -102,6 +102,12 @@ int tc_work_bounds(const tc_graph *g, int npools, int64_t *bounds);
  * gets 1/parts of both, and each head's bitmap is built by one shard only.  Both arrays
  * hold parts + 1 entries; the shard counts sum to the full count. */
 int tc_shard_plan(const tc_graph *g, int parts, int64_t *edge_bounds, int64_t *head_bounds);
+/* The plan's model costs, for measurement-guided refinement (distributed.ShardPlanner):
+ * per-tile edge-side costs (ntiles tiles of `tile` edges) and per-head head-side costs
+ * (nheads heads from head0), in the plan's time units. */
+int tc_shard_cost_sizes(const tc_graph *g, int parts, uint64_t *ntiles, uint64_t *tile, uint64_t *nheads,
+                        uint32_t *head0);
+int tc_shard_costs(const tc_graph *g, int parts, uint64_t *edge_tiles, uint64_t *head_costs);
 /* Cost features of one shard (calibration of the plan's weights; see csrc/tc_count.cu). */
 int tc_shard_stats(const tc_graph *g, int64_t lo, int64_t hi, int64_t head_lo, int64_t head_hi,
                    uint64_t out[8]);

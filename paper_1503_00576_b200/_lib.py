@@ -79,6 +79,9 @@ _SIGS = {
     "tc_work_bounds": ([_graph_p, ctypes.c_int, _vp], ctypes.c_int),
     "tc_merge_work": ([_graph_p, _u64p], ctypes.c_int),
     "tc_shard_plan": ([_graph_p, ctypes.c_int, _vp, _vp], ctypes.c_int),
+    "tc_shard_cost_sizes": ([_graph_p, ctypes.c_int, _u64p, _u64p, _u64p, ctypes.POINTER(ctypes.c_uint32)],
+                            ctypes.c_int),
+    "tc_shard_costs": ([_graph_p, ctypes.c_int, _vp, _vp], ctypes.c_int),
     "tc_shard_stats": ([_graph_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _vp],
                        ctypes.c_int),
     "tc_count_shard": ([_graph_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _u64p,

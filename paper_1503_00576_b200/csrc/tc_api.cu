@@ -820,6 +820,26 @@ int tc_shard_plan(const tc_graph *g, int parts, int64_t *edge_bounds, int64_t *h
     return shard_plan_dev(*r, parts, edge_bounds, head_bounds, g_stream);
 }
 
+int tc_shard_cost_sizes(const tc_graph *g, int parts, uint64_t *ntiles, uint64_t *tile, uint64_t *nheads,
+                        uint32_t *head0) {
+    TC_API_GUARD();
+    TC_CHECK(ensure());
+    TC_CHECK(check_graph(g));
+    const DeviceGraph *r = nullptr;
+    TC_CHECK(rank_copy(const_cast<tc_graph *>(g), &r));
+    shard_cost_sizes(*r, parts, ntiles, tile, nheads, head0);
+    return 0;
+}
+
+int tc_shard_costs(const tc_graph *g, int parts, uint64_t *edge_tiles, uint64_t *head_costs) {
+    TC_API_GUARD();
+    TC_CHECK(ensure());
+    TC_CHECK(check_graph(g));
+    const DeviceGraph *r = nullptr;
+    TC_CHECK(rank_copy(const_cast<tc_graph *>(g), &r));
+    return shard_costs_dev(*r, parts, (unsigned long long *)edge_tiles, (unsigned long long *)head_costs, g_stream);
+}
+
 int tc_shard_stats(const tc_graph *g, int64_t lo, int64_t hi, int64_t hlo, int64_t hhi, uint64_t out[8]) {
     TC_API_GUARD();
     TC_CHECK(ensure());

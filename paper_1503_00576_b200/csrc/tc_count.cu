@@ -2620,21 +2620,35 @@ static void cut_prefix(const unsigned long long *h, uint64_t nt, int parts, uint
     }
 }
 
-int shard_plan_dev(const DeviceGraph &g, int parts, int64_t *ebounds, int64_t *hbounds, cudaStream_t s) {
+// Model costs of the plan: per-tile edge-side costs (nt tiles of `tile` edges) and per-head
+// head-side costs (nz heads from z0).  Host arrays; sizes from shard_cost_sizes.
+void shard_cost_sizes(const DeviceGraph &g, int parts, uint64_t *nt, uint64_t *tile, uint64_t *nz, uint32_t *z0) {
+    uint64_t t = g.m / ((uint64_t)(parts > 0 ? parts : 1) * 1024);
+    if (t < 1) t = 1;
+    if (t > 4096) t = 4096;
+    *tile = t;
+    *nt = (g.m + t - 1) / t;
     const bool vm = g.off32 && vmajor_schedule(g);
-    for (int p = 0; p <= parts; ++p) hbounds[p] = p == 0 ? 0 : (int64_t)g.n;
-    if (!vm) return work_bounds_dev(g, parts, ebounds, s);
+    *z0 = vm ? vzone_start(g) : (uint32_t)g.n;
+    *nz = g.n - *z0;
+}
+
+int shard_costs_dev(const DeviceGraph &g, int parts, unsigned long long *edge_tiles, unsigned long long *head_costs,
+                    cudaStream_t s) {
+    uint64_t nt, tile, nz;
+    uint32_t z0;
+    shard_cost_sizes(g, parts, &nt, &tile, &nz, &z0);
+    const bool vm = g.off32 && vmajor_schedule(g);
+    if (!vm) {
+        set_error("shard costs need a v-major (rank-space, m >= 2^27 or forced) schedule");
+        return -1;
+    }
     const VSplit vp = make_vsplit(g, true);
     const bool hub = g.dense_bits != nullptr;
     const Options &o = opts();
     const ShardWeights w{(uint64_t)o.shard_w_dense, (uint64_t)o.shard_w_sparse, (uint64_t)o.shard_w_light,
                          (uint64_t)o.shard_w_stage, (uint64_t)o.shard_w_edge, (uint64_t)o.shard_w_hub,
                          (uint64_t)o.shard_w_vlow, (uint64_t)o.shard_w_vedge};
-    uint64_t tile = g.m / ((uint64_t)parts * 1024);
-    if (tile < 1) tile = 1;
-    if (tile > 4096) tile = 4096;
-    const uint64_t nt = (g.m + tile - 1) / tile;
-    const uint32_t z0 = vp.z0, nz = (uint32_t)(g.n - z0);
     unsigned long long *sums = nullptr, *hb = nullptr;
     TC_CHECK(dalloc_t(&sums, nt ? nt : 1, s));
     TC_CHECK(dalloc_t(&hb, nz ? nz : 1, s));
@@ -2646,27 +2660,43 @@ int shard_plan_dev(const DeviceGraph &g, int parts, int64_t *ebounds, int64_t *h
         TC_LAUNCHED();
     }
     if (nz) {
-        k_head_fixed<<<grid_for(nz, 256, kSMs * 4), 256, 0, s>>>(g.off32, z0, nz, vp, w, hb);
+        k_head_fixed<<<grid_for(nz, 256, kSMs * 4), 256, 0, s>>>(g.off32, z0, (uint32_t)nz, vp, w, hb);
         TC_LAUNCHED();
     }
-    unsigned long long *h = (unsigned long long *)malloc(((nt > nz ? nt : nz) + 1) * sizeof(unsigned long long));
-    if (!h) {
-        set_error("host allocation failed");
-        return -3;
-    }
-    TC_CUDA(cudaMemcpyAsync(h, sums, nt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    if (nt) TC_CUDA(cudaMemcpyAsync(edge_tiles, sums, nt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    if (nz) TC_CUDA(cudaMemcpyAsync(head_costs, hb, nz * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));
-    cut_prefix(h, nt, parts, tile, g.m, ebounds, 0);
-    ebounds[parts] = (int64_t)g.m;
-    TC_CUDA(cudaMemcpyAsync(h, hb, nz * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    TC_CUDA(cudaStreamSynchronize(s));
-    cut_prefix(h, nz, parts, 1, nz, hbounds, (int64_t)z0);
-    hbounds[0] = 0;  // heads below the zone never run v-major: shard 0 owns them (no work)
-    hbounds[parts] = (int64_t)g.n;
-    free(h);
     dfree(sums, s);
     dfree(hb, s);
     return 0;
+}
+
+int shard_plan_dev(const DeviceGraph &g, int parts, int64_t *ebounds, int64_t *hbounds, cudaStream_t s) {
+    const bool vm = g.off32 && vmajor_schedule(g);
+    for (int p = 0; p <= parts; ++p) hbounds[p] = p == 0 ? 0 : (int64_t)g.n;
+    if (!vm) return work_bounds_dev(g, parts, ebounds, s);
+    uint64_t nt, tile, nz;
+    uint32_t z0;
+    shard_cost_sizes(g, parts, &nt, &tile, &nz, &z0);
+    unsigned long long *e = (unsigned long long *)malloc((nt + 1) * sizeof(unsigned long long));
+    unsigned long long *h = (unsigned long long *)malloc((nz + 1) * sizeof(unsigned long long));
+    if (!e || !h) {
+        free(e);
+        free(h);
+        set_error("host allocation failed");
+        return -3;
+    }
+    const int rc = shard_costs_dev(g, parts, e, h, s);
+    if (!rc) {
+        cut_prefix(e, nt, parts, tile, g.m, ebounds, 0);
+        ebounds[parts] = (int64_t)g.m;
+        cut_prefix(h, nz, parts, 1, nz, hbounds, (int64_t)z0);
+        hbounds[0] = 0;  // heads below the zone never run v-major: shard 0 owns them (no work)
+        hbounds[parts] = (int64_t)g.n;
+    }
+    free(e);
+    free(h);
+    return rc;
 }
 
 int vin_capacity_dev(DeviceGraph *g, const uint32_t *deg_by_rank, cudaStream_t s) {

@@ -243,6 +243,9 @@ int work_bounds_dev(const DeviceGraph &g, int npools, int64_t *bounds, cudaStrea
 // Multi-GPU shard plan (tc_shard_plan): edge bounds balancing the non-v-major work and head
 // bounds balancing the v-major work; count_shard_dev counts one shard of it.
 int shard_plan_dev(const DeviceGraph &g, int parts, int64_t *ebounds, int64_t *hbounds, cudaStream_t s);
+void shard_cost_sizes(const DeviceGraph &g, int parts, uint64_t *nt, uint64_t *tile, uint64_t *nz, uint32_t *z0);
+int shard_costs_dev(const DeviceGraph &g, int parts, unsigned long long *edge_tiles, unsigned long long *head_costs,
+                    cudaStream_t s);
 int shard_stats_dev(const DeviceGraph &g, uint64_t lo, uint64_t hi, uint32_t hlo, uint32_t hhi, uint64_t out[8],
                     cudaStream_t s);
 int count_shard_dev(const DeviceGraph &g, uint64_t lo, uint64_t hi, uint32_t hlo, uint32_t hhi,

@@ -212,6 +212,62 @@ def refine_plan(edge_bounds, head_bounds, edge_ms, head_ms, head_floor: int = 0)
     return recut(edge_bounds, edge_ms), out_h
 
 
+class ShardPlanner:
+    """The shard plan of tc_shard_plan, held on the host as its model costs (per-tile edge-side
+    costs, per-head head-side costs) so it can be refined by measurement: after a count, each
+    shard's measured time per side (minus a fixed per-shard cost) over its model cost gives a
+    correction factor applied to that shard's cost range, and both sides are re-cut at equal
+    corrected cost.  Identical inputs give identical plans on every rank (the measured times
+    are all-gathered first).  For repeated counts of one graph (bench steps, a service)."""
+
+    def __init__(self, graph, parts: int, head_fixed_ms: float = 2.9, edge_fixed_ms: float = 0.1):
+        h = graph.handle
+        L = _lib.lib()
+        nt, tile, nz = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        z0 = ctypes.c_uint32()
+        _lib.check(L.tc_shard_cost_sizes(h, parts, ctypes.byref(nt), ctypes.byref(tile), ctypes.byref(nz),
+                                         ctypes.byref(z0)))
+        et = np.zeros(max(nt.value, 1), np.uint64)
+        hc = np.zeros(max(nz.value, 1), np.uint64)
+        _lib.check(L.tc_shard_costs(h, parts, _lib.ptr(et), _lib.ptr(hc)))
+        self.parts, self.tile, self.z0 = parts, tile.value, z0.value
+        self.m, self.n = graph.m, graph.n
+        self.ecost = et[:nt.value].astype(np.float64)
+        self.hcost = hc[:nz.value].astype(np.float64)
+        self.hfix, self.efix = head_fixed_ms, edge_fixed_ms
+        self.ecut = self._cut(self.ecost)
+        self.hcut = self._cut(self.hcost)
+
+    def _cut(self, cost):
+        P = self.parts
+        c = np.cumsum(cost)
+        total = c[-1] if c.size else 0.0
+        cut = [0]
+        for k in range(1, P):
+            i = int(np.searchsorted(c, total * k / P, side="left")) + 1 if total > 0 else cost.size
+            cut.append(min(max(i, cut[-1]), cost.size))
+        cut.append(cost.size)
+        return cut
+
+    def bounds(self):
+        eb = np.array([min(i * self.tile, self.m) for i in self.ecut], dtype=np.int64)
+        hb = np.array([self.z0 + i for i in self.hcut], dtype=np.int64)
+        hb[0], hb[-1] = 0, self.n
+        return eb, hb
+
+    def refine(self, edge_ms, head_ms):
+        for cost, cut, ms, fix in ((self.ecost, self.ecut, edge_ms, self.efix),
+                                   (self.hcost, self.hcut, head_ms, self.hfix)):
+            for r in range(self.parts):
+                a, b = cut[r], cut[r + 1]
+                model = cost[a:b].sum()
+                if b > a and model > 0:
+                    cost[a:b] *= max(float(ms[r]) - fix, 1e-3) / model
+        self.ecut = self._cut(self.ecost)
+        self.hcut = self._cut(self.hcost)
+        return self.bounds()
+
+
 def shard_bounds(npairs: int, world: int) -> list[int]:
     """Contiguous pair ranges [b[r], b[r+1]) of an edge array split over ``world`` ranks."""
     return [npairs * r // world for r in range(world + 1)]

@@ -19,9 +19,10 @@ og, _ = tcb.preprocess_device(g, rank_space=True)
 g.free()
 from paper_1503_00576_b200.count import count_shard, shard_plan  # noqa: E402
 
-from paper_1503_00576_b200.distributed import refine_plan  # noqa: E402
+from paper_1503_00576_b200.distributed import ShardPlanner  # noqa: E402
 
-eb, hb = shard_plan(og, P)
+planner = ShardPlanner(og.device(), P)
+eb, hb = planner.bounds()
 full = statistics.median(tcb.count_device(og)[1].count_ms for _ in range(3))
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 for it in range(iters + 1):
@@ -44,4 +45,4 @@ for it in range(iters + 1):
                       "speedup_bound": round(full / max(times), 2), "sum_over_full": round(sum(times) / full, 3),
                       "triangles": tris, "phases_head_edge": phases, "edge_bounds": [int(x) for x in eb],
                       "head_bounds": [int(x) for x in hb]}), flush=True)
-    eb, hb = refine_plan(eb, hb, edge_ms, head_ms, head_floor=max(og.num_vertices - (1 << 22), 0))
+    eb, hb = planner.refine(edge_ms, head_ms)
