@@ -392,14 +392,18 @@ def main():
     sb = shard_bounds(npairs, world)
     shard = generators.DeviceEdgesView(dev_edges, sb[rank], sb[rank + 1])
 
+    # multi-GPU: the shard plan is refined from every count's per-rank phase times (the
+    # warm-up steps calibrate it; ShardPlanner in distributed.py)
+    plans = {}
+
     def step_device():
         if world == 1:
             tri, t = tcb.count_with_timings_device(dev_edges)
             return tri, t.preprocess_ms, t.count_ms
         if args.dist == "v1":
-            rep = count_distributed(ops, dev_edges if rank == 0 else None)
+            rep = count_distributed(ops, dev_edges if rank == 0 else None, plans=plans)
         else:
-            rep = count_distributed_sharded(ops, shard, dev_edges.num_vertices)
+            rep = count_distributed_sharded(ops, shard, dev_edges.num_vertices, plans=plans)
         return rep.triangles, None, None
 
     for _ in range(args.warmup):
@@ -473,11 +477,11 @@ def main():
         host_shard = generators.pinned_empty((shard.npairs, 2), np.uint32)
         if shard.npairs:
             _lib.check(L.tc_memcpy(_lib.ptr(host_shard), ctypes.c_void_p(shard.ptr), shard.nbytes, 1))
-        count_distributed_sharded(ops, host_shard, dev_edges.num_vertices)  # warm
+        count_distributed_sharded(ops, host_shard, dev_edges.num_vertices, plans=plans)  # warm
         barrier()
         timer(2)
         for _ in range(e2e_steps):
-            rep = count_distributed_sharded(ops, host_shard, dev_edges.num_vertices)
+            rep = count_distributed_sharded(ops, host_shard, dev_edges.num_vertices, plans=plans)
             if rep.triangles != tri_ref:
                 raise RuntimeError("e2e count differs")
         timer(3)

@@ -76,6 +76,14 @@ class Ops:
     def count_shard(self, graph, lo: int, hi: int, hlo: int, hhi: int) -> int:
         return self.count_range(graph, lo, hi) if hi > lo else 0
 
+    def count_shard_timed(self, graph, lo: int, hi: int, hlo: int, hhi: int):
+        """(count, edge-side ms, head-side ms) of one shard."""
+        return self.count_shard(graph, lo, hi, hlo, hhi), 0.0, 0.0
+
+    def make_planner(self, graph, parts: int):
+        """A ShardPlanner for repeated counts of this graph, or None (static plan only)."""
+        return None
+
     def sync(self) -> None:
         pass
 
@@ -136,7 +144,7 @@ class ShardReport:
     head_bounds: tuple = ()
 
 
-def count_distributed(ops: Ops, edges=None, group=None, graph=None) -> ShardReport:
+def count_distributed(ops: Ops, edges=None, group=None, graph=None, plans: dict | None = None) -> ShardReport:
     """Count triangles of ``edges`` (held by rank 0) across all ranks of ``group``.
 
     Every rank must call it; only rank 0 needs ``edges`` (or an existing ``graph``).
@@ -174,7 +182,7 @@ def count_distributed(ops: Ops, edges=None, group=None, graph=None) -> ShardRepo
         ops.finalize(g)
     # 3. identical shard plan on every rank (edge ranges for the u-major / light work, head
     #    ranges for the v-major work); count the local shard
-    return _count_local_shard(ops, g, rank, world, group, m, n)
+    return _count_local_shard(ops, g, rank, world, group, m, n, plans)
 
 
 def refine_plan(edge_bounds, head_bounds, edge_ms, head_ms, head_floor: int = 0):
@@ -220,7 +228,18 @@ class ShardPlanner:
     corrected cost.  Identical inputs give identical plans on every rank (the measured times
     are all-gathered first).  For repeated counts of one graph (bench steps, a service)."""
 
-    def __init__(self, graph, parts: int, head_fixed_ms: float = 2.9, edge_fixed_ms: float = 0.1):
+    def __init__(self, ecost, tile: int, hcost, z0: int, m: int, n: int, parts: int,
+                 head_fixed_ms: float = 2.9, edge_fixed_ms: float = 0.1):
+        self.parts, self.tile, self.z0, self.m, self.n = parts, int(tile), int(z0), int(m), int(n)
+        self.ecost = np.asarray(ecost, dtype=np.float64).copy()
+        self.hcost = np.asarray(hcost, dtype=np.float64).copy()
+        self.hfix, self.efix = head_fixed_ms, edge_fixed_ms
+        self.ecut = self._cut(self.ecost)
+        self.hcut = self._cut(self.hcost)
+
+    @classmethod
+    def from_device(cls, graph, parts: int) -> "ShardPlanner":
+        """From a device graph's model costs (tc_shard_costs); graph has .handle, .m, .n."""
         h = graph.handle
         L = _lib.lib()
         nt, tile, nz = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
@@ -230,13 +249,7 @@ class ShardPlanner:
         et = np.zeros(max(nt.value, 1), np.uint64)
         hc = np.zeros(max(nz.value, 1), np.uint64)
         _lib.check(L.tc_shard_costs(h, parts, _lib.ptr(et), _lib.ptr(hc)))
-        self.parts, self.tile, self.z0 = parts, tile.value, z0.value
-        self.m, self.n = graph.m, graph.n
-        self.ecost = et[:nt.value].astype(np.float64)
-        self.hcost = hc[:nz.value].astype(np.float64)
-        self.hfix, self.efix = head_fixed_ms, edge_fixed_ms
-        self.ecut = self._cut(self.ecost)
-        self.hcut = self._cut(self.hcost)
+        return cls(et[:nt.value], tile.value, hc[:nz.value], z0.value, graph.m, graph.n, parts)
 
     def _cut(self, cost):
         P = self.parts
@@ -273,7 +286,8 @@ def shard_bounds(npairs: int, world: int) -> list[int]:
     return [npairs * r // world for r in range(world + 1)]
 
 
-def count_distributed_sharded(ops: Ops, shard, num_vertices: int, group=None) -> ShardReport:
+def count_distributed_sharded(ops: Ops, shard, num_vertices: int, group=None,
+                              plans: dict | None = None) -> ShardReport:
     """Triangles of the edge array whose shards the ranks of ``group`` hold (v2: sharded
     preprocessing, no serial step).  ``shard`` is this rank's slice of the pairs (any
     split works: the result does not depend on it); ``num_vertices`` is the global
@@ -340,20 +354,37 @@ def count_distributed_sharded(ops: Ops, shard, num_vertices: int, group=None) ->
         del gathered
     ops.finalize(g)
     # 6. count the local shard; one all-reduce
-    return _count_local_shard(ops, g, rank, world, group, m, n)
+    return _count_local_shard(ops, g, rank, world, group, m, n, plans)
 
 
-def _count_local_shard(ops: Ops, g, rank: int, world: int, group, m: int, n: int) -> ShardReport:
+def _count_local_shard(ops: Ops, g, rank: int, world: int, group, m: int, n: int,
+                       plans: dict | None = None) -> ShardReport:
     """This rank's shard of the plan every rank computes identically, then one 64-bit
-    all-reduce (counts < 2^63, so the int64 sum equals the uint64 sum bit for bit)."""
+    all-reduce (counts < 2^63, so the int64 sum equals the uint64 sum bit for bit).  With
+    ``plans`` (a dict the caller keeps across counts of the same graph) the plan is a
+    ShardPlanner refined after every count by the all-gathered per-rank phase times."""
+    import torch
     import torch.distributed as dist
-    eb, hb = ops.shard_plan(g, world)
+    key = (m, n, world)
+    planner = None
+    if plans is not None:
+        if key not in plans:
+            plans[key] = ops.make_planner(g, world)
+        planner = plans[key]
+    eb, hb = planner.bounds() if planner is not None else ops.shard_plan(g, world)
     lo, hi = int(eb[rank]), int(eb[rank + 1])
     hlo, hhi = int(hb[rank]), int(hb[rank + 1])
-    local = ops.count_shard(g, lo, hi, hlo, hhi)
+    local, edge_ms, head_ms = ops.count_shard_timed(g, lo, hi, hlo, hhi)
     t = _to_backend(ops.count_tensor(local), ops)
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     total = int(t.cpu().item())
+    if planner is not None:
+        times = torch.zeros(2 * world, dtype=torch.float64)
+        times[2 * rank], times[2 * rank + 1] = edge_ms, head_ms
+        times = _to_backend(times, ops)
+        dist.all_reduce(times, op=dist.ReduceOp.SUM, group=group)
+        tt = times.cpu().numpy()
+        planner.refine(tt[0::2], tt[1::2])
     return ShardReport(total, local, tuple(int(b) for b in eb), m, n, tuple(int(b) for b in hb))
 
 
@@ -471,11 +502,20 @@ class B200Ops(Ops):
         return eb, hb
 
     def count_shard(self, graph, lo, hi, hlo, hhi):
+        return self.count_shard_timed(graph, lo, hi, hlo, hhi)[0]
+
+    def count_shard_timed(self, graph, lo, hi, hlo, hhi):
         out = ctypes.c_uint64()
         t = _lib.TcTimes()
         _lib.check(_lib.lib().tc_count_shard(graph.handle, int(lo), int(hi), int(hlo), int(hhi),
                                              ctypes.byref(out), ctypes.byref(t)))
-        return int(out.value)
+        return int(out.value), t.count_ms - t.vmajor_ms, t.vmajor_ms
+
+    def make_planner(self, graph, parts):
+        try:
+            return ShardPlanner.from_device(graph, parts)
+        except ValueError:  # no v-major split for this graph: the static plan
+            return None
 
     # ---- v2 -----------------------------------------------------------------------
     def _out(self, t):

@@ -21,7 +21,7 @@ from paper_1503_00576_b200.count import count_shard, shard_plan  # noqa: E402
 
 from paper_1503_00576_b200.distributed import ShardPlanner  # noqa: E402
 
-planner = ShardPlanner(og.device(), P)
+planner = ShardPlanner.from_device(og.device(), P)
 eb, hb = planner.bounds()
 full = statistics.median(tcb.count_device(og)[1].count_ms for _ in range(3))
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 0

@@ -233,3 +233,31 @@ def test_refine_plan_equalises_measured_times():
         return tot
     parts = [t(e3[i], e3[i + 1]) for i in range(4)]
     assert max(parts) - min(parts) < 0.05
+
+
+def test_shard_planner_refinement_converges():
+    """ShardPlanner (pure host logic): with a hidden true cost per tile/head that differs
+    from the model by a smooth factor, two refinements bring every shard within 2 % of the
+    mean."""
+    from paper_1503_00576_b200.distributed import ShardPlanner
+    rng = np.random.default_rng(3)
+    ecost = rng.random(4096) + 0.1
+    hcost = rng.random(2048) ** 3
+    etrue = ecost * np.linspace(0.5, 3.0, ecost.size)
+    htrue = hcost * np.linspace(2.0, 0.4, hcost.size)
+    P = 8
+    pl = ShardPlanner(ecost, 16, hcost, 1000, 16 * 4096, 1000 + 2048, P, head_fixed_ms=0.0, edge_fixed_ms=0.0)
+
+    def measure():
+        e = [etrue[pl.ecut[r]:pl.ecut[r + 1]].sum() for r in range(P)]
+        h = [htrue[pl.hcut[r]:pl.hcut[r + 1]].sum() for r in range(P)]
+        return np.array(e), np.array(h)
+    e0, h0 = measure()
+    for _ in range(2):
+        pl.refine(*measure())
+    e2, h2 = measure()
+    assert e2.max() / e2.mean() < 1.02 and h2.max() / h2.mean() < 1.02
+    assert e0.max() / e0.mean() > 1.1
+    eb, hb = pl.bounds()
+    assert eb[0] == 0 and eb[-1] == 16 * 4096 and hb[0] == 0 and hb[-1] == 3048
+    assert all(np.diff(eb) >= 0) and all(np.diff(hb) >= 0)

@@ -112,7 +112,10 @@ def _nccl_worker(port, q):
         a = count_distributed_sharded(ops, dev, dev.num_vertices).triangles
         b = count_distributed_sharded(ops, dev.to_host().edges, dev.num_vertices).triangles
         c = count_distributed(ops, dev).triangles
+        plans = {}
+        d = [count_distributed_sharded(ops, dev, dev.num_vertices, plans=plans).triangles for _ in range(2)]
         ref = tcb.count_with_timings_device(dev)[0]
+        assert d == [ref, ref], d
         q.put((a, b, c, ref, dist.get_backend()))
     except Exception as e:  # noqa: BLE001
         q.put((repr(e), None, None, None, None))
