@@ -110,7 +110,7 @@ int tc_shard_cost_sizes(const tc_graph *g, int parts, uint64_t *ntiles, uint64_t
 int tc_shard_costs(const tc_graph *g, int parts, uint64_t *edge_tiles, uint64_t *head_costs);
 /* Cost features of one shard (calibration of the plan's weights; see csrc/tc_count.cu). */
 int tc_shard_stats(const tc_graph *g, int64_t lo, int64_t hi, int64_t head_lo, int64_t head_hi,
-                   uint64_t out[8]);
+                   uint64_t out[9]);
 int tc_count_shard(const tc_graph *g, int64_t lo, int64_t hi, int64_t head_lo, int64_t head_hi,
                    uint64_t *out, tc_times *t);
 /* merge-model work W = sum over oriented edges of d+(u) + d+(v) (roofline numerator) */

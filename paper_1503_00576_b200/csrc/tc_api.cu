@@ -840,7 +840,7 @@ int tc_shard_costs(const tc_graph *g, int parts, uint64_t *edge_tiles, uint64_t 
     return shard_costs_dev(*r, parts, (unsigned long long *)edge_tiles, (unsigned long long *)head_costs, g_stream);
 }
 
-int tc_shard_stats(const tc_graph *g, int64_t lo, int64_t hi, int64_t hlo, int64_t hhi, uint64_t out[8]) {
+int tc_shard_stats(const tc_graph *g, int64_t lo, int64_t hi, int64_t hlo, int64_t hhi, uint64_t out[9]) {
     TC_API_GUARD();
     TC_CHECK(ensure());
     TC_CHECK(check_graph(g));

@@ -2541,18 +2541,20 @@ __global__ void k_head_fixed(const uint32_t *__restrict__ off, uint32_t z0, uint
 // Per-shard cost features (calibration of the shard plan's weights, scripts/shard_calib.py):
 // edge side over [lo, hi) non-v-major edges: [0] dense AND bytes, [1] sparse heavy item
 // bytes, [2] light bytes, [3] edges, [4] heavy staging bytes; head side over heads in
-// [hlo, hhi): [5] hub-head v-major bytes, [6] below-hub v-major bytes, [7] v-major edges.
+// [hlo, hhi): [5] hub-head v-major bytes, [6] below-hub v-major bytes, [7] v-major edges;
+// [8] v-major bytes of the edges in [lo, hi) (by source position: suffix locality probes).
 __global__ void __launch_bounds__(256)
     k_shard_stats(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
                   const uint32_t *__restrict__ off, uint64_t m, uint64_t lo, uint64_t hi, uint32_t hlo,
                   uint32_t hhi, VSplit vp, bool hub, unsigned long long *__restrict__ out) {
-    unsigned long long b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long b[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
         int cls;
         uint32_t stage;
         const uint64_t x = edge_bytes(src, dst, off, e, vp, hub, &cls, &stage);
         const uint32_t v = __ldg(dst + e);
+        if (cls == 0 && e >= lo && e < hi) b[8] += x;
         if (cls == 0) {
             if (v >= hlo && v < hhi) {
                 b[v >= vp.hz ? 5 : 6] += x;
@@ -2570,33 +2572,33 @@ __global__ void __launch_bounds__(256)
             }
         }
     }
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < 9; ++k) {
         unsigned long long x = b[k];
         for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(TC_FULL_MASK, x, o);
         if (lane_id() == 0 && x) atomicAdd(out + k, x);
     }
 }
 
-int shard_stats_dev(const DeviceGraph &g, uint64_t lo, uint64_t hi, uint32_t hlo, uint32_t hhi, uint64_t out[8],
+int shard_stats_dev(const DeviceGraph &g, uint64_t lo, uint64_t hi, uint32_t hlo, uint32_t hhi, uint64_t out[9],
                     cudaStream_t s) {
     if (!g.off32 || !g.rank_space || !g.hubstart) {
         set_error("shard stats need a rank-space graph with m < 2^32");
         return -1;
     }
     unsigned long long *d = nullptr;
-    TC_CHECK(dalloc_t(&d, 8, s));
-    TC_CUDA(cudaMemsetAsync(d, 0, 8 * sizeof(unsigned long long), s));
+    TC_CHECK(dalloc_t(&d, 9, s));
+    TC_CUDA(cudaMemsetAsync(d, 0, 9 * sizeof(unsigned long long), s));
     if (g.m) {
         k_shard_stats<<<grid_for(g.m, 256, kSMs * 16), 256, 0, s>>>(g.src, g.dst, g.off32, g.m, lo, hi, hlo, hhi,
                                                                    make_vsplit(g, vmajor_schedule(g)),
                                                                    g.dense_bits != nullptr, d);
         TC_LAUNCHED();
     }
-    unsigned long long h[8];
+    unsigned long long h[9];
     TC_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));
     dfree(d, s);
-    for (int k = 0; k < 8; ++k) out[k] = h[k];
+    for (int k = 0; k < 9; ++k) out[k] = h[k];
     return 0;
 }
 

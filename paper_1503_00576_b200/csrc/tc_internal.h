@@ -246,7 +246,7 @@ int shard_plan_dev(const DeviceGraph &g, int parts, int64_t *ebounds, int64_t *h
 void shard_cost_sizes(const DeviceGraph &g, int parts, uint64_t *nt, uint64_t *tile, uint64_t *nz, uint32_t *z0);
 int shard_costs_dev(const DeviceGraph &g, int parts, unsigned long long *edge_tiles, unsigned long long *head_costs,
                     cudaStream_t s);
-int shard_stats_dev(const DeviceGraph &g, uint64_t lo, uint64_t hi, uint32_t hlo, uint32_t hhi, uint64_t out[8],
+int shard_stats_dev(const DeviceGraph &g, uint64_t lo, uint64_t hi, uint32_t hlo, uint32_t hhi, uint64_t out[9],
                     cudaStream_t s);
 int count_shard_dev(const DeviceGraph &g, uint64_t lo, uint64_t hi, uint32_t hlo, uint32_t hhi,
                     unsigned long long *d_total, cudaStream_t s, CountStats *stats);

@@ -13,7 +13,7 @@ g = make(sys.argv[1] if len(sys.argv) > 1 else "rmat26")
 og, _ = tcb.preprocess_device(g, rank_space=True)
 g.free()
 h, n, m = og.device().handle, og.num_vertices, og.m_dir
-out = np.zeros(8, np.uint64)
+out = np.zeros(9, np.uint64)
 _lib.check(_lib.lib().tc_shard_stats(h, 0, 0, 0, n, _lib.ptr(out)))
 tot_b, tot_e = int(out[5] + out[6]), int(out[7])
 print("total v-major bytes", tot_b / 1e9, "GB, in-edges", tot_e)

@@ -29,7 +29,7 @@ for P, wl, wv, we in ((8, 16, 6, 0), (8, 32, 4, 64), (8, 4, 8, 256), (4, 16, 4, 
 for name, eb, hb in plans:
     for p in range(len(eb) - 1):
         a = (og, eb[p], eb[p + 1], hb[p], hb[p + 1])
-        out = np.zeros(8, np.uint64)
+        out = np.zeros(9, np.uint64)
         _lib.check(_lib.lib().tc_shard_stats(h, int(eb[p]), int(eb[p + 1]), int(hb[p]), int(hb[p + 1]),
                                              _lib.ptr(out)))
         with _lib.options(count_stats=1):
