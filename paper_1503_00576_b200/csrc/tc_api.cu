@@ -1160,6 +1160,13 @@ const OptionName kOptionNames[] = {
     {"shard_ucap", &Options::shard_ucap},   {"dense_ranks", &Options::dense_ranks},
     {"shard_ovh2", &Options::shard_ovh2},   {"copy_threads", &Options::copy_threads},
     {"seg_fork", &Options::seg_fork},
+    {"vin_overlap", &Options::vin_overlap},
+    {"vin_grid", &Options::vin_grid},
+    {"seg_k16", &Options::seg_k16},
+    {"seg_w2k", &Options::seg_w2k},
+    {"vhub", &Options::vhub},
+    {"vhub_unroll", &Options::vhub_unroll},
+    {"vhub_blocks", &Options::vhub_blocks},
     {"shard_w_dense", &Options::shard_w_dense}, {"shard_w_sparse", &Options::shard_w_sparse},
     {"shard_w_light", &Options::shard_w_light}, {"shard_w_stage", &Options::shard_w_stage},
     {"shard_w_edge", &Options::shard_w_edge},   {"shard_w_hub", &Options::shard_w_hub},

@@ -1553,6 +1553,301 @@ __global__ void TC_VM_BOUNDS(NT)
     block_add_total(acc, total);
 }
 
+// ------------------------------------------------------- v-major, hub heads ---
+// Hub heads v >= hz: the same per-head schedule as k_count_vmajor, with a leaner item sweep.
+//  * No per-item bounds: every lane tests all items of its aligned 16-byte chunks.  The items
+//    of an in-edge's first and last chunk that lie outside its suffix [a, b) are tested a
+//    second time by the thread that owns the in-edge and subtracted (at most 3 + 3 items, or
+//    7 + 7 in 16-bit chunks), so the hot loop is load, shift, mask, LDS, shift, add.  Those
+//    outside items can be any vertex: the 32-bit probe masks the word address into the
+//    power-of-two bitmap allocation, which keeps every access in bounds and deterministic
+//    (the subtraction re-reads exactly what the sweep read).
+//  * Heads in the top 2^16 ranks (t16 = n - 2^16): every suffix item after v lies in
+//    [t16, n), so the suffixes are read from a 16-bit copy of edge_dst (lo16[p] = dst[p] -
+//    t16; 2 B per item, 8 items per 16-byte chunk) against a 2^16-bit bitmap (8 KB).  At
+//    R-MAT s26 these heads carry 52 % of the hub-head suffix items (scripts/hub16_stats.py).
+constexpr uint32_t kT16 = 1u << 16;
+
+__device__ __forceinline__ uint32_t bit16(const unsigned char *bm, uint32_t x) {
+    // item x (16-bit): word x >> 5 at byte (x >> 3) & ~3 (x < 2^16), bit x & 31
+    return (*reinterpret_cast<const uint32_t *>(bm + ((x >> 3) & 0x1ffcu)) >> (x & 31u)) & 1u;
+}
+
+__device__ __forceinline__ uint32_t bit32(const unsigned char *bm, uint32_t w, uint32_t hz, uint32_t amask) {
+    const uint32_t r = w - hz;
+    return (*reinterpret_cast<const uint32_t *>(bm + ((r >> 3) & amask)) >> (r & 31u)) & 1u;
+}
+
+// Chunk c of the window belongs to the in-edge k with cst[k] <= c < cst[k+1]; its items are
+// at element cb[k] + E c (E = items per 16-byte chunk).  Lanes past c1 count nothing.
+// Software-pipelined: the U chunks of the next round are in flight while this round's items
+// are probed, and all shared-memory probes of a round are issued before their results are
+// used (the probe chain LDS -> shift -> add is latency-bound otherwise).
+template <int U, bool B16>
+__device__ __forceinline__ uint32_t sweep_nomask(const void *__restrict__ arr, const uint32_t *s_cb,
+                                                 const uint32_t *s_cst, uint32_t nwin, uint32_t c0, uint32_t c1,
+                                                 const unsigned char *bm, uint32_t hz, uint32_t amask) {
+    constexpr uint32_t E = B16 ? 8u : 4u;
+    constexpr int NI = B16 ? 8 * U : 4 * U;  // items per lane per round
+    const unsigned lane = lane_id();
+    uint32_t k = 0;
+    {
+        const uint32_t c = c0 + lane < c1 ? c0 + lane : c1 - 1;
+        uint32_t a = 0, b = nwin;
+        while (b - a > 1) {
+            const uint32_t mid = (a + b) >> 1;
+            if (s_cst[mid] <= c) a = mid; else b = mid;
+        }
+        k = a;
+    }
+    uint32_t nextb = s_cst[k + 1], cb = s_cb[k];
+    auto fetch = [&](uint32_t base, uint4 (&q)[U], uint32_t &live) {
+        live = 0;
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            uint32_t c = base + j * 32 + lane;
+            live |= (c < c1 ? 1u : 0u) << j;
+            c = c < c1 ? c : c1 - 1;
+            if (c >= nextb) {
+                do { nextb = s_cst[++k + 1]; } while (c >= nextb);
+                cb = s_cb[k];
+            }
+            const uint32_t p = cb + E * c;
+            if (B16) q[j] = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(arr) + p));
+            else q[j] = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(arr) + p));
+        }
+    };
+    auto probe = [&](const uint4 (&q)[U], uint32_t live) -> uint32_t {
+        uint32_t ad[NI], sh[NI], wd[NI];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const uint32_t x4[4] = {q[j].x, q[j].y, q[j].z, q[j].w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                if (B16) {
+                    ad[8 * j + 2 * i] = (x4[i] >> 3) & 0x1ffcu;
+                    sh[8 * j + 2 * i] = x4[i];
+                    ad[8 * j + 2 * i + 1] = (x4[i] >> 19) & 0x1ffcu;
+                    sh[8 * j + 2 * i + 1] = x4[i] >> 16;
+                } else {
+                    const uint32_t r = x4[i] - hz;
+                    ad[4 * j + i] = (r >> 3) & amask;
+                    sh[4 * j + i] = r;
+                }
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < NI; ++t) wd[t] = *reinterpret_cast<const uint32_t *>(bm + ad[t]);
+        uint32_t f = 0;
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            uint32_t h = 0;
+#pragma unroll
+            for (int t = 0; t < NI / U; ++t) h += (wd[j * (NI / U) + t] >> (sh[j * (NI / U) + t] & 31u)) & 1u;
+            f += ((live >> j) & 1u) ? h : 0u;
+        }
+        return f;
+    };
+    uint32_t found = 0;
+    uint4 qa[U], qb[U];
+    uint32_t la = 0, lb = 0;
+    fetch(c0, qa, la);
+    for (uint32_t base = c0;;) {
+        const uint32_t nb = base + 32 * U;
+        if (nb < c1) fetch(nb, qb, lb);  // warp-uniform
+        found += probe(qa, la);
+        if (nb >= c1) break;
+        base = nb + 32 * U;
+        if (base < c1) fetch(base, qa, la);
+        found += probe(qb, lb);
+        if (base >= c1) break;
+    }
+    return found;
+}
+
+// The items of [F, F + E * chunks) outside [a, b): positions < a in the first chunk and
+// positions >= b in the last one (same chunk when chunks == 1).
+template <bool B16>
+__device__ __forceinline__ uint32_t edge_outside(const void *__restrict__ arr, uint32_t a, uint32_t b,
+                                                 uint32_t F, uint32_t chunks, const unsigned char *bm,
+                                                 uint32_t hz, uint32_t amask) {
+    constexpr uint32_t E = B16 ? 8u : 4u;
+    const uint32_t L = F + E * (chunks - 1);
+    uint32_t x = 0;
+    if (B16) {
+        const uint4 qf = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(arr) + F));
+        const uint4 ql = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(arr) + L));
+        const uint32_t f4[4] = {qf.x, qf.y, qf.z, qf.w}, l4[4] = {ql.x, ql.y, ql.z, ql.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            x += (F + 2 * i < a ? bit16(bm, f4[i] & 0xffffu) : 0u) + (F + 2 * i + 1 < a ? bit16(bm, f4[i] >> 16) : 0u);
+            x += (L + 2 * i >= b ? bit16(bm, l4[i] & 0xffffu) : 0u) + (L + 2 * i + 1 >= b ? bit16(bm, l4[i] >> 16) : 0u);
+        }
+    } else {
+        const uint4 qf = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(arr) + F));
+        const uint4 ql = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(arr) + L));
+        const uint32_t f4[4] = {qf.x, qf.y, qf.z, qf.w}, l4[4] = {ql.x, ql.y, ql.z, ql.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            x += F + i < a ? bit32(bm, f4[i], hz, amask) : 0u;
+            x += L + i >= b ? bit32(bm, l4[i], hz, amask) : 0u;
+        }
+    }
+    return x;
+}
+
+// BT: tasks are (head, first, end) index ranges (the source-blocked top-band tasks);
+// otherwise (head, chunk) as in k_count_vmajor.
+template <int NT, int U, bool BT>
+__global__ void __launch_bounds__(NT)
+    k_count_vhub(const uint32_t *__restrict__ dst, const uint16_t *__restrict__ lo16,
+                 const uint32_t *__restrict__ off, uint32_t z0, uint32_t hz, uint32_t t16, uint32_t hwp,
+                 uint32_t amask, const uint32_t *__restrict__ start, const uint32_t *__restrict__ fillc,
+                 const uint2 *__restrict__ in_e, const void *__restrict__ tasks,
+                 const uint32_t *__restrict__ tlo, const uint32_t *__restrict__ ntasks,
+                 unsigned *__restrict__ next, unsigned long long *__restrict__ total) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t *bitmap = reinterpret_cast<uint32_t *>(smem);  // (amask + 4) / 4 words
+    __shared__ uint32_t s_cb[NT];
+    __shared__ uint32_t s_cst[NT + 4];
+    __shared__ uint32_t s_scan[32];
+    __shared__ unsigned s_task;
+    constexpr int NW = NT / 32;
+    const unsigned warp = threadIdx.x >> 5;
+    const unsigned nt = *ntasks, t0 = *tlo;
+    // the probes of outside items may read any word of the allocation: define them all
+    for (uint32_t i = threadIdx.x; i < (amask + 4) / 4 || i < kT16 / 32; i += NT) bitmap[i] = 0;
+    unsigned long long acc = 0;
+    for (;;) {
+        if (threadIdx.x == 0) s_task = t0 + atomicAdd(next, 1u);
+        __syncthreads();
+        const unsigned t = s_task;
+        if (t >= nt) break;
+        uint32_t h, p0, p1;
+        if (BT) {
+            const uint4 task = static_cast<const uint4 *>(tasks)[t];
+            h = task.x;
+            p0 = task.y;
+            p1 = task.z;
+        } else {
+            const uint2 task = static_cast<const uint2 *>(tasks)[t];
+            h = task.x;
+            p0 = __ldg(start + h) + task.y * kVChunk;
+            // fill count, clamped to the slot range (an overflowed capacity layout is recounted)
+            p1 = min(p0 + kVChunk, min(__ldg(start + h) + __ldg(fillc + h), __ldg(start + h + 1)));
+        }
+        const uint32_t v = z0 + h;
+        const uint32_t vs = __ldg(off + v), ve = __ldg(off + v + 1);
+        const bool b16 = v >= t16;  // block-uniform
+        const uint32_t base = b16 ? t16 : hz;
+        const uint32_t wend = b16 ? kT16 / 32 : hwp;
+        const uint32_t ws = ((v + 1 - base) >> 5) & ~3u;
+        for (uint32_t i = ws + 4 * threadIdx.x; i < wend; i += 4 * NT)
+            *reinterpret_cast<uint4 *>(bitmap + i) = make_uint4(0, 0, 0, 0);
+        __syncthreads();
+        for (uint32_t i = vs + threadIdx.x; i < ve; i += NT) {
+            const uint32_t r = __ldg(dst + i) - base;
+            atomicOr(bitmap + (r >> 5), 1u << (r & 31));
+        }
+        __syncthreads();
+        uint2 ie_n = p0 + threadIdx.x < p1 ? __ldg(in_e + p0 + threadIdx.x) : make_uint2(0u, 0u);
+        for (uint32_t ps = p0; ps < p1; ps += NT) {
+            const uint32_t nwin = min((uint32_t)NT, p1 - ps);
+            uint32_t chunks = 0, F = 0;
+            const uint2 ie = ie_n;  // (edge, end of adj(u)); the next window's is loaded now
+            ie_n = ps + NT + threadIdx.x < p1 ? __ldg(in_e + ps + NT + threadIdx.x) : make_uint2(0u, 0u);
+            if (threadIdx.x < nwin) {
+                const uint32_t a = ie.x + 1, b = ie.y;  // a < b by construction
+                if (b16) {
+                    F = a & ~7u;
+                    chunks = (b - F + 7) >> 3;
+                    acc -= edge_outside<true>(lo16, a, b, F, chunks, smem, hz, amask);
+                } else {
+                    F = a & ~3u;
+                    chunks = (b - F + 3) >> 2;
+                    acc -= edge_outside<false>(dst, a, b, F, chunks, smem, hz, amask);
+                }
+            }
+            uint32_t tot;
+            const uint32_t cst = block_exclusive_scan<uint32_t>(chunks, s_scan, &tot);
+            s_cb[threadIdx.x] = F - (b16 ? 8u : 4u) * cst;
+            s_cst[threadIdx.x] = cst;
+            if (threadIdx.x == 0) s_cst[NT] = tot;
+            __syncthreads();
+            const uint32_t c0 = (uint32_t)((uint64_t)tot * warp / NW);
+            const uint32_t c1 = (uint32_t)((uint64_t)tot * (warp + 1) / NW);
+            if (c0 < c1) {
+                if (b16) acc += sweep_nomask<U, true>(lo16, s_cb, s_cst, NT, c0, c1, smem, hz, amask);
+                else acc += sweep_nomask<U, false>(dst, s_cb, s_cst, NT, c0, c1, smem, hz, amask);
+            }
+            __syncthreads();
+        }
+    }
+    block_add_total(acc, total);
+}
+
+// Source blocks for the top-band heads.  Their suffix streams (2 B per item) re-read each
+// source's band items once per head it points to (R-MAT s26: ~140 reads per item).  Tasks
+// ordered (source block, head) keep the streams of one block of edge_dst -- ~1/nb of the
+// band data -- in L2 while every head's bitmap is staged once per block.  The fill appends
+// in-edges roughly in edge order (grid-stride over edges), so a head's list is split at the
+// block bounds by binary search on the edge index; splits are made monotone, so the tasks
+// partition every list whatever the order (exactness never depends on it).
+__global__ void k_band_splits(const uint32_t *__restrict__ start, const uint32_t *__restrict__ fillc,
+                              const uint2 *__restrict__ in_e, uint32_t h16, uint32_t nb16, uint32_t nb,
+                              uint64_t bsize, uint32_t *__restrict__ spl, uint32_t *__restrict__ cnt) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb16; i += stride) {
+        const uint32_t h = h16 + i;
+        const uint32_t P0 = start[h], P1 = min(start[h] + fillc[h], start[h + 1]);
+        uint32_t prev = P0;
+        spl[(size_t)i * (nb + 1)] = P0;
+        for (uint32_t S = 1; S <= nb; ++S) {
+            uint32_t q = P1;
+            if (S < nb) {
+                const uint64_t E = (uint64_t)S * bsize;
+                uint32_t a = prev, n2 = P1 - prev;  // first position with edge >= E
+                while (n2 > 0) {
+                    const uint32_t hh = n2 >> 1;
+                    if ((uint64_t)in_e[a + hh].x < E) { a += hh + 1; n2 -= hh + 1; } else n2 = hh;
+                }
+                q = a;
+            }
+            spl[(size_t)i * (nb + 1) + S] = q;
+            cnt[(size_t)(S - 1) * nb16 + i] = (q - prev + kVChunk - 1) / kVChunk;
+            prev = q;
+        }
+    }
+}
+
+// tasks (head, first, end, 0) in (block, head) order from the scanned counts
+__global__ void k_band_tasks(const uint32_t *__restrict__ spl, const uint32_t *__restrict__ tst,
+                             uint32_t h16, uint32_t nb16, uint32_t nb, uint4 *__restrict__ tasks) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t N = nb16 * nb;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += stride) {
+        const uint32_t S = j / nb16, i = j - S * nb16;
+        const uint32_t lo = spl[(size_t)i * (nb + 1) + S], hi = spl[(size_t)i * (nb + 1) + S + 1];
+        for (uint32_t t = tst[j]; t < tst[j + 1]; ++t) {
+            const uint32_t a = lo + (t - tst[j]) * kVChunk;
+            tasks[t] = make_uint4(h16 + i, a, min(a + kVChunk, hi), 0u);
+        }
+    }
+}
+
+// 16-bit copy of edge_dst for the top-2^16 heads: lo16[p] = dst[p] - t16 (mod 2^16; only
+// items >= t16 are ever counted).  dst is padded to a multiple of 4 + 4.
+__global__ void __launch_bounds__(256) k_pack16(const uint32_t *__restrict__ dst, uint64_t m, uint32_t t16,
+                                                uint16_t *__restrict__ lo16) {
+    const uint64_t ng = (m + 3) / 4;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += stride) {
+        const uint4 w = __ldg(reinterpret_cast<const uint4 *>(dst) + g);
+        reinterpret_cast<uint2 *>(lo16)[g] = make_uint2(((w.x - t16) & 0xffffu) | ((w.y - t16) << 16),
+                                                       ((w.z - t16) & 0xffffu) | ((w.w - t16) << 16));
+    }
+}
+
 // ------------------------------------------------------- paper baseline ---
 // Thread per oriented edge, grid-stride, bounds checked like the
 // reference (count.py:69-98).
@@ -1855,16 +2150,23 @@ struct VmajorState {
     uint2 *big = nullptr;   // CTA tasks of long-list heads below hz
     uint32_t *defer = nullptr;  // warp tasks whose cuckoo build failed (binary-search rerun)
     uint16_t *lo16 = nullptr;   // packed hub copy of edge_dst (HubPack)
+    uint16_t *lo16t = nullptr;  // 16-bit copy of edge_dst relative to t16 (k_count_vhub)
+    uint4 *btasks = nullptr;    // source-blocked top-band tasks (k_count_vhub<.., true>)
+    uint32_t *bspl = nullptr, *bcnt = nullptr, *btst = nullptr;
+    uint32_t nbands = 0, nb16 = 0;
     uint8_t *hi2 = nullptr;
     bool capl = false;      // capacity layout used (overflow flag in next[2])
     unsigned *next = nullptr;
     uint2 *tasks = nullptr;
+    HubPack hp{nullptr, nullptr};
     cudaEvent_t e0 = nullptr, e1 = nullptr, done = nullptr;
     cudaStream_t s2 = nullptr;
 };
 
-int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
-                 unsigned long long *d_total, cudaStream_t s, cudaStream_t s2, int share,
+// v-major part 1: the in-edge index and the task lists, on s2 (forked from s).  With s2 != s
+// it overlaps the u-major kernels: the fill is bound by L2 atomics, the u-major kernels by
+// dependent-load latency, and neither depends on the other.
+int vmajor_index(const DeviceGraph &g, const RangeDev *rg, uint64_t span, cudaStream_t s, cudaStream_t s2,
                  VmajorState *st, uint32_t hlo = 0, uint32_t hhi = 0xffffffffu) {
     const uint32_t z0 = vzone_start(g);
     const uint32_t nh = (uint32_t)(g.n - z0);  // v-major zone size
@@ -1879,11 +2181,11 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
     TC_CHECK(dalloc_t(&st->tasks, (size_t)nh + span / kVChunk + 1, s));
     // [0], [1] task cursors, [2] capacity overflow flag, [3] big-task count, [4] zero,
     // [5] big cursor, [6] deferred-task count, [7] deferred cursor
-    TC_CHECK(dalloc_t(&st->next, 8, s));
+    TC_CHECK(dalloc_t(&st->next, 10, s));
     TC_CHECK(dalloc_t(&st->big, (size_t)nh + span / kVChunk + 1, s));
     TC_CHECK(dalloc_t(&st->defer, (size_t)nh + span / kVChunk + 1, s));
     TC_CUDA(cudaMemsetAsync(st->cnt, 0, (size_t)nh * sizeof(uint32_t), s));
-    TC_CUDA(cudaMemsetAsync(st->next, 0, 8 * sizeof(unsigned), s));
+    TC_CUDA(cudaMemsetAsync(st->next, 0, 10 * sizeof(unsigned), s));
     st->capl = capl;
     // everything below runs on s2 (the index build too, so that with s2 != s it overlaps
     // the u-major kernels on s)
@@ -1891,9 +2193,14 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
     TC_CUDA(cudaEventCreateWithFlags(&st->done, cudaEventDisableTiming));
     TC_CUDA(cudaEventCreate(&st->e0));
     TC_CUDA(cudaEventCreate(&st->e1));
-    TC_CUDA(cudaEventRecord(st->e0, s));
-    if (s2 != s) TC_CUDA(cudaStreamWaitEvent(s2, st->e0, 0));
-    const unsigned grid = grid_for(span, 256 * kVinPP, kSMs * 8);
+    if (s2 != s) {
+        TC_CUDA(cudaEventRecord(st->done, s));
+        TC_CUDA(cudaStreamWaitEvent(s2, st->done, 0));
+    }
+    // beside the u-major kernels the fill keeps a small grid (it needs atomics in flight,
+    // not SM slots)
+    const int64_t vg = opts().vin_grid;
+    const unsigned grid = grid_for(span, 256 * kVinPP, kSMs * (unsigned)(s2 != s && vg > 0 ? vg : 8));
     const VSplit vp = make_vsplit(g, true);
     const uint32_t *startp = g.vin_cap;
     if (!capl) {
@@ -1922,6 +2229,50 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
         TC_LAUNCHED();
         hp = HubPack{st->lo16, st->hi2};
     }
+    st->hp = hp;
+    if (!vp.packed && opts().vhub) {
+        // 16-bit copy of edge_dst for the top-2^16 heads of k_count_vhub
+        const uint64_t ng = (g.m + 3) / 4;
+        const uint32_t t16 = g.n - g.hz > kT16 ? (uint32_t)(g.n - kT16) : g.hz;
+        TC_CHECK(dalloc_t(&st->lo16t, 4 * ng + 32, s2));
+        TC_CUDA(cudaMemsetAsync(st->lo16t + 4 * ng, 0, 64, s2));
+        k_pack16<<<grid_for(ng, 256, kSMs * 8), 256, 0, s2>>>(g.dst, g.m, t16, st->lo16t);
+        TC_LAUNCHED();
+        const int64_t nbo = opts().vhub_blocks;
+        if (nbo > 1) {
+            const uint32_t nb = (uint32_t)(nbo < 256 ? nbo : 256);
+            const uint32_t h16 = t16 - z0, nb16 = nh - h16;
+            const uint64_t bsize = (g.m + nb - 1) / nb;
+            const size_t N = (size_t)nb16 * nb;
+            TC_CHECK(dalloc_t(&st->bspl, (size_t)nb16 * (nb + 1), s2));
+            TC_CHECK(dalloc_t(&st->bcnt, N, s2));
+            TC_CHECK(dalloc_t(&st->btst, N + 1, s2));
+            TC_CHECK(dalloc_t(&st->btasks, span / kVChunk + N + 1, s2));
+            k_band_splits<<<grid_for(nb16, 256, kSMs * 4), 256, 0, s2>>>(startp, st->cnt, st->in_e, h16, nb16, nb,
+                                                                        bsize, st->bspl, st->bcnt);
+            TC_LAUNCHED();
+            TC_CHECK(vin_scan<false>(st->bcnt, (uint32_t)N, st->btst, s2));
+            k_band_tasks<<<grid_for(N, 256, kSMs * 8), 256, 0, s2>>>(st->bspl, st->btst, h16, nb16, nb, st->btasks);
+            TC_LAUNCHED();
+            st->nbands = nb;
+            st->nb16 = nb16;
+        }
+    }
+    return 0;
+}
+
+// v-major part 2: the count kernels on st->s2, after `gate` (recorded on s once the u-major
+// kernels are queued; nullptr = right away).  The v-major phase time is e0 -> e1.
+int vmajor_count(const DeviceGraph &g, unsigned long long *d_total, cudaStream_t s, int share, VmajorState *st,
+                 cudaEvent_t gate) {
+    cudaStream_t s2 = st->s2;
+    if (gate && s2 != s) TC_CUDA(cudaStreamWaitEvent(s2, gate, 0));
+    TC_CUDA(cudaEventRecord(st->e0, s2));
+    const uint32_t z0 = vzone_start(g);
+    const uint32_t nh = (uint32_t)(g.n - z0);
+    const uint32_t hb = (uint32_t)(g.hz - z0);
+    const uint32_t *startp = st->capl ? g.vin_cap : st->start;
+    const HubPack hp = st->hp;
     constexpr int NT = 256;
     auto kern = k_count_vmajor<NT, 4>;
     const uint32_t cap = 0;  // heads below hz run in k_count_vlow_warp
@@ -1960,11 +2311,41 @@ int count_vmajor(const DeviceGraph &g, const RangeDev *rg, uint64_t span,
                                            hp, d_total);
         TC_LAUNCHED();
     }
-    TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    kern<<<kSMs * per_sm, NT, sm, s2>>>(g.src, g.dst, g.off32, g.hubstart, z0, g.hz, g.hwp, cap,
-                                        startp, st->cnt, st->in_e, st->tasks, st->tstart + hb, st->tstart + nh,
-                                        st->next, hp, d_total);
-    TC_LAUNCHED();
+    if (st->lo16t) {
+        // hub heads: lean sweep, 16-bit items for the top 2^16 heads
+        const uint32_t t16 = g.n - g.hz > kT16 ? (uint32_t)(g.n - kT16) : g.hz;
+        uint32_t w32 = 4;
+        while (w32 < g.hwp) w32 <<= 1;
+        const uint32_t amask = (w32 * 4 - 1) & ~3u;
+        const size_t hsm = 4 * (size_t)(w32 > kT16 / 32 ? w32 : kT16 / 32);
+        const int64_t vu = opts().vhub_unroll;
+        auto hk = vu == 4 ? k_count_vhub<NT, 4, false> : vu == 1 ? k_count_vhub<NT, 1, false> : k_count_vhub<NT, 2, false>;
+        auto hkb = vu == 4 ? k_count_vhub<NT, 4, true> : vu == 1 ? k_count_vhub<NT, 1, true> : k_count_vhub<NT, 2, true>;
+        TC_CUDA(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+        TC_CUDA(cudaFuncSetAttribute(hkb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+        int hper = 1;
+        TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hper, hk, NT, hsm));
+        hper = hper / share;
+        if (hper < 1) hper = 1;
+        // without source blocks one launch covers every hub head; with them the heads below
+        // the top band first, then the blocked top-band tasks
+        const uint32_t hend = st->nbands ? t16 - z0 : nh;
+        hk<<<kSMs * hper, NT, hsm, s2>>>(g.dst, st->lo16t, g.off32, z0, g.hz, t16, g.hwp, amask, startp, st->cnt,
+                                         st->in_e, st->tasks, st->tstart + hb, st->tstart + hend, st->next, d_total);
+        TC_LAUNCHED();
+        if (st->nbands) {
+            hkb<<<kSMs * hper, NT, hsm, s2>>>(g.dst, st->lo16t, g.off32, z0, g.hz, t16, g.hwp, amask, startp,
+                                              st->cnt, st->in_e, st->btasks, st->next + 4,
+                                              st->btst + (size_t)st->nb16 * st->nbands, st->next + 8, d_total);
+            TC_LAUNCHED();
+        }
+    } else {
+        TC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        kern<<<kSMs * per_sm, NT, sm, s2>>>(g.src, g.dst, g.off32, g.hubstart, z0, g.hz, g.hwp, cap,
+                                            startp, st->cnt, st->in_e, st->tasks, st->tstart + hb, st->tstart + nh,
+                                            st->next, hp, d_total);
+        TC_LAUNCHED();
+    }
     TC_CUDA(cudaEventRecord(st->e1, s2));
     TC_CUDA(cudaEventRecord(st->done, s2));
     return 0;
@@ -1996,6 +2377,11 @@ int vmajor_finish(VmajorState *st, cudaStream_t s, CountStats *stats, bool *over
     dfree(st->defer, s);
     dfree(st->next, s);
     dfree(st->lo16, s);
+    dfree(st->lo16t, s);
+    dfree(st->btasks, s);
+    dfree(st->bspl, s);
+    dfree(st->bcnt, s);
+    dfree(st->btst, s);
     dfree(st->hi2, s);
     *st = VmajorState{};
     return 0;
@@ -2106,17 +2492,21 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
     const int64_t conc_env = opts().concurrent;
     const bool conc = vmajor && conc_env;
     const int share = conc ? (int)(opts().share > 0 ? opts().share : 1) : 1;  // SM share of each concurrent kernel
+    // the in-edge index builds on the side stream while the u-major kernels run (vin_overlap);
+    // the v-major count kernels follow them (persistent grids do not share SMs well, §4.4)
+    const bool overlap = vmajor && !conc && opts().vin_overlap != 0;
     VmajorState vst;
     RangeDev *rg_all = nullptr;  // shard mode: the v-major index scans every edge for its heads
     if (vmajor && shard) {
         TC_CHECK(dalloc_t(&rg_all, 1, s));
         k_range_init<<<1, 1, 0, s>>>(g.src, 0, g.m, g.m, rg_all);
         TC_LAUNCHED();
-        TC_CHECK(count_vmajor(g, rg_all, g.m, d_total, s, conc ? side_stream() : s, share, &vst, shard->hlo,
+        TC_CHECK(vmajor_index(g, rg_all, g.m, s, (conc || overlap) ? side_stream() : s, &vst, shard->hlo,
                               shard->hhi));
     } else if (vmajor) {
-        TC_CHECK(count_vmajor(g, rg, span, d_total, s, conc ? side_stream() : s, share, &vst));
+        TC_CHECK(vmajor_index(g, rg, span, s, (conc || overlap) ? side_stream() : s, &vst));
     }
+    if (vmajor && !overlap) TC_CHECK(vmajor_count(g, d_total, s, share, &vst, nullptr));
     TC_CUDA(cudaEventRecord(ev[1], s));
     // Heavy classes first (largest tasks first), then the light sweep.
     for (int c = kClasses - 1; c >= 0; --c) {
@@ -2142,7 +2532,7 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
         if (sizeof(OffT) == 4 && g.rank_space && g.hubstart && hub_sm <= 200 * 1024) {
             const int ntc = c == 2 ? 512 : 256;
             // the packed copy is built on the v-major stream: usable once that phase is joined
-            const HubPack hp = conc ? HubPack{nullptr, nullptr} : HubPack{vst.lo16, vst.hi2};
+            const HubPack hp = (conc || overlap) ? HubPack{nullptr, nullptr} : HubPack{vst.lo16, vst.hi2};
             rc = ntc == 512 ? launch_hub<512>(g, rg, tasks[c], nt_c, next_c, hub_cap, vmajor, share, hp, d_total, s)
                             : launch_hub<256>(g, rg, tasks[c], nt_c, next_c, hub_cap, vmajor, share, hp, d_total, s);
             if (rc) return rc;
@@ -2190,6 +2580,8 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
             g.dense_off, g.dense_bits, g.dense_words, d_total);
     }
     TC_LAUNCHED();
+    TC_CUDA(cudaEventRecord(ev[3], s));
+    if (overlap) TC_CHECK(vmajor_count(g, d_total, s, 1, &vst, ev[3]));
     bool overflow = false;
     TC_CHECK(vmajor_finish(&vst, s, stats, &overflow));
     if (overflow) {
@@ -2204,7 +2596,6 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
         dfree(d_total, s);
         return count_impl<OffT>(g2, off, lo, hi, d_out, s, stats, shard);
     }
-    TC_CUDA(cudaEventRecord(ev[3], s));
     if (stats) {
         TC_CUDA(cudaEventSynchronize(ev[3]));
         cudaEventElapsedTime(&stats->classify_ms, ev[0], ev[1]);

@@ -63,6 +63,13 @@ struct Options {
     int64_t shard_ovh2 = 256;    // per-edge byte-equivalent overhead of shard model 2
     int64_t copy_threads = 0;    // host threads of the staged pageable H2D copy (0: auto)
     int64_t seg_fork = 1;        // rank-space preprocess: size-class sorts on concurrent streams
+    int64_t vin_overlap = 1;     // v-major in-edge index on a side stream beside the u-major kernels
+    int64_t vin_grid = 4;        // CTAs per SM of the in-edge fill when it overlaps
+    int64_t vhub_unroll = 2;     // k_count_vhub: 16-byte chunks per lane per pipelined round (1, 2, 4)
+    int64_t vhub_blocks = 1;     // k_count_vhub: source blocks of the top-band tasks (<= 1: unblocked)
+    int64_t vhub = 1;            // hub heads of the v-major schedule on k_count_vhub (lean sweep, 16-bit top band)
+    int64_t seg_w2k = 0;         // rank-space preprocess: 1025..2048-element lists on a warp register sort
+    int64_t seg_k16 = 1;         // rank-space preprocess: 257..512-element lists on a 512-wide sort
     int64_t dense_ranks = 1 << 17;  // dense-hub bitmaps for the top ranks
     int64_t bucket = 1;          // rank-space preprocess: bucket scatter + segmented sort
     int64_t count_stats = 0;     // tc_count_with_timings fills the per-kernel-class fields

@@ -828,17 +828,22 @@ __global__ void __launch_bounds__(256)
 }
 
 // Lists by size class (append order is irrelevant: lists are disjoint).
+// w512 == nullptr: 257..1024 all go to w1k (one 1024-wide network); w2k == nullptr:
+// 1025..2048 go to the CTA shared-memory sort with 2049..4096.
 __global__ void k_seg_classify(const uint32_t *__restrict__ off32, uint64_t n,
                                uint32_t *__restrict__ mid, uint32_t *__restrict__ big,
                                uint32_t *__restrict__ warpl, uint32_t *__restrict__ w256,
-                               uint32_t *__restrict__ w1k, unsigned *__restrict__ counts) {
+                               uint32_t *__restrict__ w512, uint32_t *__restrict__ w1k,
+                               uint32_t *__restrict__ w2k, unsigned *__restrict__ counts) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += stride) {
         const uint32_t d = off32[u + 1] - off32[u];
         if (d <= 16) continue;
         if (d <= 64) warpl[atomicAdd(counts + 0, 1u)] = (uint32_t)u;
         else if (d <= 256) w256[atomicAdd(counts + 3, 1u)] = (uint32_t)u;
+        else if (d <= 512 && w512) w512[atomicAdd(counts + 5, 1u)] = (uint32_t)u;
         else if (d <= 1024) w1k[atomicAdd(counts + 4, 1u)] = (uint32_t)u;
+        else if (d <= 2048 && w2k) w2k[atomicAdd(counts + 6, 1u)] = (uint32_t)u;
         else if (d <= 4096) mid[atomicAdd(counts + 1, 1u)] = (uint32_t)u;
         else big[atomicAdd(counts + 2, 1u)] = (uint32_t)u;
     }
@@ -1127,17 +1132,24 @@ static int bucket_csr_dev(const uint64_t *keys, uint64_t m, uint64_t n, int vb, 
         TC_LAUNCHED();
     }
     if (!n) return 0;
-    uint32_t *warpl = nullptr, *w256 = nullptr, *w1k = nullptr, *mid = nullptr, *big = nullptr;
+    uint32_t *warpl = nullptr, *w256 = nullptr, *w512 = nullptr, *w1k = nullptr, *mid = nullptr, *big = nullptr;
     unsigned *counts = nullptr;
+    // 257..512 on a 512-wide network (half the comparators of the 1024-wide one)
+    const bool k16 = opts().seg_k16 != 0;
     TC_CHECK(dalloc_t(&counts, 8, s));
     TC_CHECK(dalloc_t(&warpl, n, s));
     TC_CHECK(dalloc_t(&w256, n, s));
+    if (k16) TC_CHECK(dalloc_t(&w512, n, s));
+    // 1025..2048 as a warp network in registers (64 per lane) instead of shared memory
+    const bool w2 = opts().seg_w2k != 0;
+    uint32_t *w2k = nullptr;
+    if (w2) TC_CHECK(dalloc_t(&w2k, n, s));
     TC_CHECK(dalloc_t(&w1k, n, s));
     TC_CHECK(dalloc_t(&mid, n, s));
     TC_CHECK(dalloc_t(&big, n, s));
     TC_CUDA(cudaMemsetAsync(counts, 0, 8 * sizeof(unsigned), s));
     k_seg_classify<<<grid_for(n, 256, kSMs * 8), 256, 0, s>>>(out->off32, n, mid, big, warpl, w256,
-                                                              w1k, counts);
+                                                              w512, w1k, w2k, counts);
     TC_LAUNCHED();
     // hubstart (first element >= hz of every list) falls out of the sorts for free
     const uint32_t hz = n > kHubRanks ? (uint32_t)(n - kHubRanks) : 0u;
@@ -1161,6 +1173,14 @@ static int bucket_csr_dev(const uint64_t *keys, uint64_t m, uint64_t n, int vb, 
     TC_LAUNCHED();
     k_seg_sort_warp<32><<<kSMs * 8, 256, 0, ss[1]>>>(out->off32, w1k, counts + 4, out->dst, hz, hs);
     TC_LAUNCHED();
+    if (k16) {
+        k_seg_sort_warp<16><<<kSMs * 8, 256, 0, ss[2]>>>(out->off32, w512, counts + 5, out->dst, hz, hs);
+        TC_LAUNCHED();
+    }
+    if (w2) {
+        k_seg_sort_warp<64><<<kSMs * 4, 256, 0, ss[0]>>>(out->off32, w2k, counts + 6, out->dst, hz, hs);
+        TC_LAUNCHED();
+    }
     k_seg_sort_warp<8><<<kSMs * 8, 256, 0, ss[2]>>>(out->off32, w256, counts + 3, out->dst, hz, hs);
     TC_LAUNCHED();
     k_seg_sort64<<<kSMs * 8, 256, 0, ss[3]>>>(out->off32, warpl, counts + 0, out->dst, hz, hs);
@@ -1219,6 +1239,8 @@ static int bucket_csr_dev(const uint64_t *keys, uint64_t m, uint64_t n, int vb, 
     dfree(counts, s);
     dfree(warpl, s);
     dfree(w256, s);
+    dfree(w512, s);
+    dfree(w2k, s);
     dfree(w1k, s);
     dfree(mid, s);
     dfree(big, s);

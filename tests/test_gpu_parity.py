@@ -350,6 +350,10 @@ def test_rank_space_csr_matches_numpy(case):
     {"bucket": 0},                                   # rank-space preprocess by global key sort
     {"vmajor": 1, "hubpack": 1},                     # hub suffixes from the 18-bit packed copy
     {"vmajor": 1, "hubpack": 2},                     # packed reads, 4-byte cost model
+    {"vmajor": 1, "vhub": 0},                        # hub heads on the masked-sweep CTA kernel
+    {"vmajor": 1, "vin_overlap": 0, "seg_k16": 0},   # in-edge index serial; 1024-wide sorts
+    {"vmajor": 1, "vhub_blocks": 8, "seg_w2k": 1},   # source-blocked top-band tasks; warp 2K sorts
+    {"vmajor": 1, "vhub_unroll": 1},                 # unpipelined-width sweep
 ], ids=lambda o: ",".join(f"{k}={v}" for k, v in o.items()))
 def test_count_schedules_agree(opts, golden_big):
     """Every count schedule (v-major on/off and its zone, the per-edge bias, the light and
