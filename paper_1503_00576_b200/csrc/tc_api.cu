@@ -1167,6 +1167,9 @@ const OptionName kOptionNames[] = {
     {"vhub", &Options::vhub},
     {"vhub_unroll", &Options::vhub_unroll},
     {"vhub_blocks", &Options::vhub_blocks},
+    {"vhub_b16w", &Options::vhub_b16w},
+    {"hub_cap_div", &Options::hub_cap_div},
+    {"vix", &Options::vix},
     {"shard_w_dense", &Options::shard_w_dense}, {"shard_w_sparse", &Options::shard_w_sparse},
     {"shard_w_light", &Options::shard_w_light}, {"shard_w_stage", &Options::shard_w_stage},
     {"shard_w_edge", &Options::shard_w_edge},   {"shard_w_hub", &Options::shard_w_hub},

@@ -24,6 +24,7 @@
 
 #include "tc_common.cuh"
 #include "tc_internal.h"
+#include "tc_vsplit.cuh"
 
 namespace tc {
 
@@ -574,48 +575,6 @@ __global__ void __launch_bounds__(NT)
     block_add_total(acc, total);
 }
 
-// ------------------------------------------------------- v-major choice ---
-// Edge e = (u, v) with v in the hub zone runs v-major (k_count_vmajor: re-reads the
-// suffix of adj(u) after v, 4 B per item) when that is cheaper than the u-major read of
-// v's data (dense bitmap words, or adj(v) as 16-byte chunks).  Every kernel evaluates the
-// same predicate, so each edge is counted exactly once.  Edges with an empty suffix or
-// an empty adj(v) close no triangle and are skipped by everyone.
-#ifndef TC_VBIG
-#define TC_VBIG 256  // 256 / 512 / 1K / 2K / 4K / 8K: s26 count 210 / 210 / 213 / 216 / 222 / 236 ms
-#endif
-constexpr uint32_t kVBigNonHub = TC_VBIG;  // v-major heads below hz with long lists: non-hub cap
-
-struct VSplit {
-    uint32_t z0, hz, vt, hwp, factor, nhcap;  // v-major zone [z0, n); z0 = ~0: v-major off
-    uint32_t bias;                            // v-major iff bias/4 * vcost < ucost
-    uint32_t lowall;                          // below hz: 0 = short suffixes only, 1 = by bytes
-    const uint32_t *hubstart;
-    uint32_t packed = 0;                      // hub-head suffixes read from the 18-bit copy
-    uint32_t packed_cost = 0;                 // the per-edge choice charges packed bytes
-};
-
-__device__ __forceinline__ bool vmajor_edge(const VSplit &vp, uint32_t e, uint32_t eu, uint32_t v,
-                                            uint32_t vs, uint32_t ve) {
-    if (v < vp.z0) return false;
-    if (e + 1 >= eu || vs >= ve) return true;  // no work either way
-    uint32_t ucost;
-    if (v >= vp.hz) {
-        const uint32_t ws = ((v + 1 - vp.hz) >> 5) & ~3u;
-        const bool dense = v >= vp.vt && (vp.hwp - ws) < vp.factor * (ve - vs);
-        ucost = dense ? 4 * (vp.hwp - ws) : (vp.packed_cost ? 9 : 16) * ((ve - (vs & ~3u) + 3) >> 2);
-        // the suffix is read from the packed hub copy: 9 bytes per 4 items
-        if (vp.packed_cost) return (uint64_t)(9 * ((eu - e - 1 + 3) >> 2) + 8) * vp.bias < (uint64_t)ucost * 4;
-    } else {
-        // below the hub zone: adj(v) goes into a per-warp cuckoo table (k_count_vlow_warp) when
-        // |adj(v)| <= nhcap; longer lists run as CTA tasks (hub part as a bitmap, non-hub part
-        // in a cuckoo table of at most kVBigNonHub keys)
-        if (!vp.lowall && eu - e - 1 >= 32) return false;
-        if (ve - vs > vp.nhcap && __ldg(vp.hubstart + v) - vs > kVBigNonHub) return false;
-        ucost = 16 * ((ve - (vs & ~3u) + 3) >> 2) + 16;
-    }
-    return (uint64_t)(4 * (eu - e - 1) + 8) * vp.bias < (uint64_t)ucost * 4;
-}
-
 // ------------------------------------------------------------ light, TPE ---
 // Thread per oriented edge (u, v) with a light source (d+(u) <= 32).  In rank space
 // (RANKED) ranks increase along a list and every element of adj(v) exceeds v, so only the
@@ -1055,7 +1014,8 @@ __global__ void TC_HUB_BOUNDS(NT)
         bool tab_ok = true;
         if (nh) {
             tab_ok = false;
-            for (uint32_t seed = 0; seed < kCuckooSeeds && !tab_ok; ++seed) {
+            // a non-hub part beyond the table's 1/3 load goes straight to binary search
+            for (uint32_t seed = 0; seed < kCuckooSeeds && !tab_ok && 3 * nh <= cap; ++seed) {
                 ck.c1 = seed_mult(seed, 0);
                 ck.c2 = seed_mult(seed, 1);
                 for (uint32_t i = threadIdx.x; i < ck.T; i += NT) ctab[i] = kEmpty;
@@ -1225,17 +1185,32 @@ __global__ void __launch_bounds__(32 * WARPS)
             __syncwarp();
             tab_ok = !__any_sync(TC_FULL_MASK, fail);
         }
+        // window metadata software-pipelined: heads two windows ahead, their offsets one
+        // window ahead (the chain edge -> v -> off[v] is off the critical path)
+        auto load_v = [&](uint64_t w) -> uint32_t { return w + lane < ee ? __ldg(dst + w + lane) : 0xffffffffu; };
+        uint32_t v_n = load_v(es), v_nn = load_v(es + 32), m0 = 0, m1 = 0;
+        if (v_n != 0xffffffffu) {
+            m0 = __ldg(off + v_n);
+            m1 = __ldg(off + v_n + 1);
+        }
         for (uint64_t ws = es; ws < ee; ws += 32) {
-            uint32_t vs = 0, ve = 0, chunks = 0;
-            if (ws + lane < ee) {
+            const uint32_t v = v_n;
+            uint32_t vs = m0, ve = m1, chunks = 0;
+            v_n = v_nn;
+            m0 = m1 = 0;
+            if (v_n != 0xffffffffu) {
+                m0 = __ldg(off + v_n);
+                m1 = __ldg(off + v_n + 1);
+            }
+            v_nn = load_v(ws + 64);
+            if (v != 0xffffffffu) {
                 const uint32_t p = (uint32_t)(ws + lane);
-                const uint32_t v = __ldg(dst + p);
-                vs = __ldg(off + v);
-                ve = __ldg(off + v + 1);
                 if (p + 1 < e && vs < ve && !vmajor_edge(vp, p, e, v, vs, ve))
                     chunks = (ve - (vs & ~3u) + 3) >> 2;
                 else
                     vs = ve = 0;
+            } else {
+                vs = ve = 0;
             }
             const uint32_t incl = warp_inclusive_scan(chunks);
             const uint32_t tot = __shfl_sync(TC_FULL_MASK, incl, 31);
@@ -1326,7 +1301,11 @@ __global__ void __launch_bounds__(256)
                 atomicAdd(cnt + h, 1u);
             }
         }
+#if defined(TC_VIN_PROBE) && TC_VIN_PROBE == 1  // diagnostic build: atomics only, no index stores
+        if (false) {
+#else
         if (FILL) {
+#endif
 #pragma unroll
             for (int i = 0; i < kVinPP; ++i)
                 if (pos[i] != 0xffffffffu)
@@ -1566,7 +1545,6 @@ __global__ void TC_VM_BOUNDS(NT)
 //    [t16, n), so the suffixes are read from a 16-bit copy of edge_dst (lo16[p] = dst[p] -
 //    t16; 2 B per item, 8 items per 16-byte chunk) against a 2^16-bit bitmap (8 KB).  At
 //    R-MAT s26 these heads carry 52 % of the hub-head suffix items (scripts/hub16_stats.py).
-constexpr uint32_t kT16 = 1u << 16;
 
 __device__ __forceinline__ uint32_t bit16(const unsigned char *bm, uint32_t x) {
     // item x (16-bit): word x >> 5 at byte (x >> 3) & ~3 (x < 2^16), bit x & 31
@@ -1941,34 +1919,47 @@ size_t heavy_smem(int cls, uint32_t max_out) {
     return (size_t)4 * slots;
 }
 
-#ifndef TC_VLCAP
-#define TC_VLCAP 512
-#endif
-constexpr uint32_t kVNonHubCap = TC_VLCAP;  // v-major below hz: max |adj(v)| of the warp tasks
-
-static uint32_t vm_lowall_env() {
-    return (uint32_t)opts().vlow_all;
-}
-
 static uint32_t vzone_start(const DeviceGraph &g) { return vzone_start_of(g.n, g.hz); }
-
-static uint32_t vm_bias_env() {
-    return (uint32_t)opts().vm_bias;
-}
 
 static uint32_t dense_factor_env() {
     return (uint32_t)opts().dense_factor;
 }
 
+}  // namespace
+
 // The v-major split every kernel of one count evaluates (the same predicate everywhere, so
 // each edge is counted exactly once).
-static VSplit make_vsplit(const DeviceGraph &g, bool vmajor) {
+VSplit make_vsplit(const DeviceGraph &g, bool vmajor) {
     VSplit vp{vmajor ? vzone_start(g) : 0xffffffffu, g.hz, g.vt, g.hwp, dense_factor_env(), kVNonHubCap,
-              vm_bias_env(), vm_lowall_env(), g.hubstart};
+              (uint32_t)opts().vm_bias, (uint32_t)opts().vlow_all, g.hubstart};
     vp.packed = vmajor && opts().hubpack ? 1u : 0u;
     vp.packed_cost = vmajor && opts().hubpack == 1 ? 1u : 0u;  // 2: packed reads, 4-byte costs
+    if (vmajor && !vp.packed && opts().vhub) {
+        vp.t16 = g.n - g.hz > kT16 ? (uint32_t)(g.n - kT16) : g.hz;
+        vp.b16w = (uint32_t)(opts().vhub_b16w > 0 ? opts().vhub_b16w : 4);
+    }
     return vp;
 }
+
+bool vsplit_same(const VSplit &a, const VSplit &b) {
+    return a.z0 == b.z0 && a.hz == b.hz && a.vt == b.vt && a.hwp == b.hwp && a.factor == b.factor &&
+           a.nhcap == b.nhcap && a.bias == b.bias && a.lowall == b.lowall && a.hubstart == b.hubstart &&
+           a.packed == b.packed && a.packed_cost == b.packed_cost && a.t16 == b.t16 && a.b16w == b.b16w;
+}
+
+bool vmajor_schedule(const DeviceGraph &g) {
+    const int64_t vm_env = opts().vmajor;
+    bool vmajor = vm_env != 0 && g.off32 && g.rank_space && g.hubstart && g.n > g.hz &&
+                  (vm_env == 1 || (g.m >= (1ull << 27) && g.max_out > 256));
+    const uint32_t lower[kClasses] = {(uint32_t)kLightMax, kClassMax[0], kClassMax[1], kClassMax[2]};
+    for (int c = 0; c < kClasses && vmajor; ++c)
+        if (g.max_out > lower[c] &&
+            4 * ((size_t)g.hwp + 3 * (g.max_out < kClassMax[c] ? g.max_out : kClassMax[c])) > 200 * 1024)
+            vmajor = false;
+    return vmajor;
+}
+
+namespace {
 
 template <int NT>
 int launch_hub(const DeviceGraph &g, const RangeDev *rg, const uint2 *tasks, const unsigned *ntasks,
@@ -2151,6 +2142,7 @@ struct VmajorState {
     uint32_t *defer = nullptr;  // warp tasks whose cuckoo build failed (binary-search rerun)
     uint16_t *lo16 = nullptr;   // packed hub copy of edge_dst (HubPack)
     uint16_t *lo16t = nullptr;  // 16-bit copy of edge_dst relative to t16 (k_count_vhub)
+    bool borrowed = false;      // cnt / in_e are the graph's prebuilt index (not freed here)
     uint4 *btasks = nullptr;    // source-blocked top-band tasks (k_count_vhub<.., true>)
     uint32_t *bspl = nullptr, *bcnt = nullptr, *btst = nullptr;
     uint32_t nbands = 0, nb16 = 0;
@@ -2167,24 +2159,32 @@ struct VmajorState {
 // it overlaps the u-major kernels: the fill is bound by L2 atomics, the u-major kernels by
 // dependent-load latency, and neither depends on the other.
 int vmajor_index(const DeviceGraph &g, const RangeDev *rg, uint64_t span, cudaStream_t s, cudaStream_t s2,
-                 VmajorState *st, uint32_t hlo = 0, uint32_t hhi = 0xffffffffu) {
+                 VmajorState *st, bool full, uint32_t hlo = 0, uint32_t hhi = 0xffffffffu) {
     const uint32_t z0 = vzone_start(g);
     const uint32_t nh = (uint32_t)(g.n - z0);  // v-major zone size
-    TC_CHECK(dalloc_t(&st->cnt, nh, s));
+    const VSplit vp = make_vsplit(g, true);
+    // full counts reuse the index the rank-space sorts filled when its split is this one
+    st->borrowed = full && g.vix_ready && g.vin_cap && vsplit_same(g.vix_vp, vp);
     TC_CHECK(dalloc_t(&st->start, (size_t)nh + 1, s));
     TC_CHECK(dalloc_t(&st->tstart, (size_t)nh + 1, s));
     // capacity layout from preprocessing (in-degree prefix over the zone) when present: the
     // counting pass is skipped and in-edges land at vin_cap[v] + cursor
     const bool capl = g.vin_cap && g.vin_z0 == z0;
     const uint64_t ie = capl ? (g.vin_total > span ? g.vin_total : span) : span;
-    TC_CHECK(dalloc_t(&st->in_e, ie ? ie : 1, s));
+    if (st->borrowed) {
+        st->cnt = g.vix_cnt;
+        st->in_e = g.vix_in_e;
+    } else {
+        TC_CHECK(dalloc_t(&st->cnt, nh, s));
+        TC_CHECK(dalloc_t(&st->in_e, ie ? ie : 1, s));
+    }
     TC_CHECK(dalloc_t(&st->tasks, (size_t)nh + span / kVChunk + 1, s));
     // [0], [1] task cursors, [2] capacity overflow flag, [3] big-task count, [4] zero,
     // [5] big cursor, [6] deferred-task count, [7] deferred cursor
     TC_CHECK(dalloc_t(&st->next, 10, s));
     TC_CHECK(dalloc_t(&st->big, (size_t)nh + span / kVChunk + 1, s));
     TC_CHECK(dalloc_t(&st->defer, (size_t)nh + span / kVChunk + 1, s));
-    TC_CUDA(cudaMemsetAsync(st->cnt, 0, (size_t)nh * sizeof(uint32_t), s));
+    if (!st->borrowed) TC_CUDA(cudaMemsetAsync(st->cnt, 0, (size_t)nh * sizeof(uint32_t), s));
     TC_CUDA(cudaMemsetAsync(st->next, 0, 10 * sizeof(unsigned), s));
     st->capl = capl;
     // everything below runs on s2 (the index build too, so that with s2 != s it overlaps
@@ -2201,18 +2201,19 @@ int vmajor_index(const DeviceGraph &g, const RangeDev *rg, uint64_t span, cudaSt
     // not SM slots)
     const int64_t vg = opts().vin_grid;
     const unsigned grid = grid_for(span, 256 * kVinPP, kSMs * (unsigned)(s2 != s && vg > 0 ? vg : 8));
-    const VSplit vp = make_vsplit(g, true);
     const uint32_t *startp = g.vin_cap;
-    if (!capl) {
+    if (!capl && !st->borrowed) {
         k_vin_pass<false><<<grid, 256, 0, s2>>>(g.src, g.dst, g.off32, rg, vp, nullptr, st->cnt, nullptr,
                                                 nullptr, hlo, hhi);
         TC_LAUNCHED();
         TC_CHECK(vin_scan<false>(st->cnt, nh, st->start, s2));  // exact layout, cursors zeroed
         startp = st->start;
     }
-    k_vin_pass<true><<<grid, 256, 0, s2>>>(g.src, g.dst, g.off32, rg, vp, startp, st->cnt, st->in_e,
-                                           capl ? st->next + 2 : nullptr, hlo, hhi);
-    TC_LAUNCHED();
+    if (!st->borrowed) {
+        k_vin_pass<true><<<grid, 256, 0, s2>>>(g.src, g.dst, g.off32, rg, vp, startp, st->cnt, st->in_e,
+                                               capl ? st->next + 2 : nullptr, hlo, hhi);
+        TC_LAUNCHED();
+    }
     TC_CHECK(vin_scan<true>(st->cnt, nh, st->tstart, s2));  // tasks from the fill counts
     const uint32_t hb = (uint32_t)(g.hz - z0);  // first hub-zone head: tasks [tstart[hb], ...)
     k_vin_tasks<<<grid_for(nh, 256, kSMs * 4), 256, 0, s2>>>(startp, st->tstart, nh, st->tasks, g.off32, z0, hb,
@@ -2368,10 +2369,12 @@ int vmajor_finish(VmajorState *st, cudaStream_t s, CountStats *stats, bool *over
     cudaEventDestroy(st->e0);
     cudaEventDestroy(st->e1);
     cudaEventDestroy(st->done);
-    dfree(st->cnt, s);
+    if (!st->borrowed) {
+        dfree(st->cnt, s);
+        dfree(st->in_e, s);
+    }
     dfree(st->start, s);
     dfree(st->tstart, s);
-    dfree(st->in_e, s);
     dfree(st->tasks, s);
     dfree(st->big, s);
     dfree(st->defer, s);
@@ -2412,17 +2415,6 @@ int launch_mid(const DeviceGraph &g, const VSplit &vp, const RangeDev *rg, const
 }
 
 // The v-major decision of a count (rank-space graphs with u32 offsets).
-bool vmajor_schedule(const DeviceGraph &g) {
-    const int64_t vm_env = opts().vmajor;
-    bool vmajor = vm_env != 0 && g.off32 && g.rank_space && g.hubstart && g.n > g.hz &&
-                  (vm_env == 1 || (g.m >= (1ull << 27) && g.max_out > 256));
-    const uint32_t lower[kClasses] = {(uint32_t)kLightMax, kClassMax[0], kClassMax[1], kClassMax[2]};
-    for (int c = 0; c < kClasses && vmajor; ++c)
-        if (g.max_out > lower[c] &&
-            4 * ((size_t)g.hwp + 3 * (g.max_out < kClassMax[c] ? g.max_out : kClassMax[c])) > 200 * 1024)
-            vmajor = false;
-    return vmajor;
-}
 
 // Shard of a multi-GPU count: the non-v-major edges of [lo, hi) plus the v-major edges (of
 // the whole graph) whose head lies in [hlo, hhi).  Over a covering set of shards every edge
@@ -2501,10 +2493,10 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
         TC_CHECK(dalloc_t(&rg_all, 1, s));
         k_range_init<<<1, 1, 0, s>>>(g.src, 0, g.m, g.m, rg_all);
         TC_LAUNCHED();
-        TC_CHECK(vmajor_index(g, rg_all, g.m, s, (conc || overlap) ? side_stream() : s, &vst, shard->hlo,
+        TC_CHECK(vmajor_index(g, rg_all, g.m, s, (conc || overlap) ? side_stream() : s, &vst, false, shard->hlo,
                               shard->hhi));
     } else if (vmajor) {
-        TC_CHECK(vmajor_index(g, rg, span, s, (conc || overlap) ? side_stream() : s, &vst));
+        TC_CHECK(vmajor_index(g, rg, span, s, (conc || overlap) ? side_stream() : s, &vst, lo == 0 && hi >= g.m));
     }
     if (vmajor && !overlap) TC_CHECK(vmajor_count(g, d_total, s, share, &vst, nullptr));
     TC_CUDA(cudaEventRecord(ev[1], s));
@@ -2516,7 +2508,11 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
         unsigned *next_c = counters + kClasses + c;
         int rc = 0;
         // non-hub part of adj(u) in a cuckoo table at load <= 1/3 (smem: bitmap + table)
-        const uint32_t hub_cap = 3 * (g.max_out < kClassMax[c] ? g.max_out : kClassMax[c]);
+        // cuckoo slots for the non-hub part of adj(u) (load <= 1/3); heavy sources keep most
+        // items in the hub zone, so the table is sized for 1/hub_cap_div of the class maximum
+        // (a longer non-hub part is binary-searched) -- the smem it saves buys resident CTAs
+        const int64_t hcd = opts().hub_cap_div > 0 ? opts().hub_cap_div : 1;
+        const uint32_t hub_cap = (uint32_t)(3 * (g.max_out < kClassMax[c] ? g.max_out : kClassMax[c]) / hcd);
         const size_t hub_sm = 4 * ((size_t)g.hwp + hub_cap);
         const int64_t midwarp = opts().midwarp;
         // with v-major on, the hub heads' dense edges are gone and the class-0 tasks are
@@ -2588,6 +2584,7 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
         // not a symmetric edge array: redo the whole range without the capacity layout
         DeviceGraph g2 = g;
         g2.vin_cap = nullptr;
+        g2.vix_ready = false;
         for (auto &e : ev) cudaEventDestroy(e);
         for (int c = 0; c < kClasses; ++c) dfree(tasks[c], s);
         dfree(rg_all, s);

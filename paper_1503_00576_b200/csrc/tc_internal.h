@@ -67,6 +67,9 @@ struct Options {
     int64_t vin_grid = 4;        // CTAs per SM of the in-edge fill when it overlaps
     int64_t vhub_unroll = 2;     // k_count_vhub: 16-byte chunks per lane per pipelined round (1, 2, 4)
     int64_t vhub_blocks = 1;     // k_count_vhub: source blocks of the top-band tasks (<= 1: unblocked)
+    int64_t vhub_b16w = 4;       // per-edge choice: bytes charged per 16-bit suffix item (4 = as 32-bit)
+    int64_t hub_cap_div = 8;     // k_count_hub: cuckoo table of the non-hub part sized max / div
+    int64_t vix = 1;             // rank-space preprocess fills the v-major in-edge index in the sorts
     int64_t vhub = 1;            // hub heads of the v-major schedule on k_count_vhub (lean sweep, 16-bit top band)
     int64_t seg_w2k = 0;         // rank-space preprocess: 1025..2048-element lists on a warp register sort
     int64_t seg_k16 = 1;         // rank-space preprocess: 257..512-element lists on a 512-wide sort
@@ -139,6 +142,18 @@ inline int bits_for(uint64_t maxval) {
     return b;
 }
 
+// The per-edge v-major choice parameters (tc_vsplit.cuh: vmajor_edge).
+struct VSplit {
+    uint32_t z0, hz, vt, hwp, factor, nhcap;  // v-major zone [z0, n); z0 = ~0: v-major off
+    uint32_t bias;                            // v-major iff bias/4 * vcost < ucost
+    uint32_t lowall;                          // below hz: 0 = short suffixes only, 1 = by bytes
+    const uint32_t *hubstart;
+    uint32_t packed = 0;                      // hub-head suffixes read from the 18-bit copy
+    uint32_t packed_cost = 0;                 // the per-edge choice charges packed bytes
+    uint32_t t16 = 0xffffffffu;               // heads >= t16 read 16-bit suffixes (k_count_vhub)
+    uint32_t b16w = 4;                        // ... charged b16w bytes per suffix item
+};
+
 // ------------------------------------------------------------ device graph ---
 struct DeviceGraph {
     uint64_t m = 0, n = 0;
@@ -168,6 +183,12 @@ struct DeviceGraph {
     uint32_t *vin_cap = nullptr;
     uint32_t vin_z0 = 0;
     uint64_t vin_total = 0;  // vin_cap[n - vin_z0]
+    // v-major in-edge index filled by the rank-space segmented sorts (full-range counts whose
+    // split equals vix_vp use it instead of k_vin_pass): fill counts and (edge, end) entries
+    uint32_t *vix_cnt = nullptr;
+    uint2 *vix_in_e = nullptr;
+    VSplit vix_vp{};
+    bool vix_ready = false;
 };
 
 // First vertex of the v-major zone: the top 2^vzone_log2 ranks (default 2^22), never

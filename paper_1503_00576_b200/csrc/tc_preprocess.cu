@@ -10,6 +10,7 @@
 
 #include "tc_common.cuh"
 #include "tc_internal.h"
+#include "tc_vsplit.cuh"
 
 namespace tc {
 
@@ -481,6 +482,11 @@ void graph_release(DeviceGraph *g, cudaStream_t s) {
     dfree(g->dense_off, s);
     dfree(g->dense_bits, s);
     dfree(g->vin_cap, s);
+    dfree(g->vix_cnt, s);
+    dfree(g->vix_in_e, s);
+    g->vix_cnt = nullptr;
+    g->vix_in_e = nullptr;
+    g->vix_ready = false;
     g->vin_cap = nullptr;
     g->dense_off = g->dense_bits = nullptr;
     g->src = g->dst = nullptr;
@@ -739,6 +745,17 @@ int compute_ranks(const uint32_t *deg, uint64_t n, uint32_t *rank, cudaStream_t 
 
 }  // namespace
 
+// Hub zone [hz, n), dense-hub threshold vt, hub words hwp of a rank-space graph.
+static void set_hub_params(DeviceGraph *g) {
+    g->hz = g->n > kHubRanks ? (uint32_t)(g->n - kHubRanks) : 0u;
+    g->rank_space = true;
+    const uint32_t hub_n = (uint32_t)(g->n - g->hz);
+    g->hwp = ((hub_n + 31) / 32 + 3) & ~3u;
+    const uint32_t dense_ranks = (uint32_t)opts().dense_ranks;
+    const uint32_t T = hub_n < dense_ranks ? hub_n : dense_ranks;
+    g->vt = (uint32_t)g->n - T;
+}
+
 int build_hubstart_dev(DeviceGraph *g, cudaStream_t s) {
     if (!g->off32) {
         set_error("rank space needs m < 2^32");
@@ -755,17 +772,14 @@ int build_hubstart_dev(DeviceGraph *g, cudaStream_t s) {
                                                                       g->hz, g->hubstart);
         TC_LAUNCHED();
     }
-    g->rank_space = true;
-    // dense-hub bitmaps of the top kDenseRanks vertices
-    const uint32_t hub_n = (uint32_t)(g->n - g->hz);
-    g->hwp = ((hub_n + 31) / 32 + 3) & ~3u;
-    const uint32_t dense_ranks = (uint32_t)opts().dense_ranks;
-    const uint32_t T = hub_n < dense_ranks ? hub_n : dense_ranks;
-    g->vt = (uint32_t)g->n - T;
+    set_hub_params(g);
+    const uint32_t T = (uint32_t)g->n - g->vt;
     dfree(g->dense_off, s);
     dfree(g->dense_bits, s);
-    dfree(g->vin_cap, s);
-    g->vin_cap = nullptr;
+    if (!g->vix_ready) {  // the prebuilt v-major index was laid out on this capacity layout
+        dfree(g->vin_cap, s);
+        g->vin_cap = nullptr;
+    }
     g->dense_off = g->dense_bits = nullptr;
     TC_CHECK(dalloc_t(&g->dense_off, (size_t)T + 1, s, g->persistent));
     uint32_t words = 0;
@@ -858,7 +872,7 @@ __device__ __forceinline__ void cswap(uint32_t &a, uint32_t &b) {
 // d <= 16: thread per list, 16-wide bitonic network in registers (pad = ~0).
 __global__ void __launch_bounds__(256)
     k_seg_sort16(const uint32_t *__restrict__ off32, uint64_t n, uint32_t *__restrict__ dst, uint32_t hz,
-                 uint32_t *__restrict__ hs) {
+                 uint32_t *__restrict__ hs, const VFill vf) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += stride) {
         const uint32_t s = off32[u], d = off32[u + 1] - s;
@@ -885,7 +899,10 @@ __global__ void __launch_bounds__(256)
         uint32_t below = 0;  // non-hub prefix length (elements < hz; pads are ~0)
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-            if ((uint32_t)i < d) dst[s + i] = x[i];
+            if ((uint32_t)i < d) {
+                dst[s + i] = x[i];
+                vfill(vf, s + i, s + d, x[i]);
+            }
             below += x[i] < hz ? 1u : 0u;
         }
         if (hs) hs[u] = s + below;
@@ -896,7 +913,7 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     k_seg_sort64(const uint32_t *__restrict__ off32, const uint32_t *__restrict__ list,
                  const unsigned *__restrict__ count, uint32_t *__restrict__ dst, uint32_t hz,
-                 uint32_t *__restrict__ hs) {
+                 uint32_t *__restrict__ hs, const VFill vf) {
     const unsigned lane = lane_id();
     const unsigned nl = *count;
     const unsigned gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -931,7 +948,10 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const uint32_t i = 2 * lane + h;
-            if (i < d) dst[s + i] = x[h];
+            if (i < d) {
+                dst[s + i] = x[h];
+                vfill(vf, s + i, s + d, x[h]);
+            }
         }
         if (hs) {
             const uint32_t below = __popc(__ballot_sync(TC_FULL_MASK, x[0] < hz)) +
@@ -947,7 +967,7 @@ template <int K>
 __global__ void __launch_bounds__(256)
     k_seg_sort_warp(const uint32_t *__restrict__ off32, const uint32_t *__restrict__ list,
                     const unsigned *__restrict__ count, uint32_t *__restrict__ dst, uint32_t hz,
-                    uint32_t *__restrict__ hs) {
+                    uint32_t *__restrict__ hs, const VFill vf) {
     constexpr int N = 32 * K;
     const unsigned lane = lane_id();
     const unsigned nl = *count;
@@ -992,7 +1012,10 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int r = 0; r < K; ++r) {
             const uint32_t i = 32 * r + lane;
-            if (i < d) dst[s + i] = x[r];
+            if (i < d) {
+                dst[s + i] = x[r];
+                vfill(vf, s + i, s + d, x[r]);
+            }
             below += __popc(__ballot_sync(TC_FULL_MASK, x[r] < hz));
         }
         if (hs && lane == 0) hs[u] = s + below;
@@ -1006,7 +1029,7 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(TC_SORT4K_NT)
     k_seg_sort4k(const uint32_t *__restrict__ off32, const uint32_t *__restrict__ list,
                  const unsigned *__restrict__ count, uint32_t *__restrict__ dst, uint32_t hz,
-                 uint32_t *__restrict__ hs) {
+                 uint32_t *__restrict__ hs, const VFill vf) {
     __shared__ uint32_t sh[4096];
     const unsigned nl = *count;
     for (unsigned w = blockIdx.x; w < nl; w += gridDim.x) {
@@ -1029,7 +1052,10 @@ __global__ void __launch_bounds__(TC_SORT4K_NT)
                 __syncthreads();
             }
         }
-        for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) dst[s + i] = sh[i];
+        for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) {
+            dst[s + i] = sh[i];
+            vfill(vf, s + i, s + d, sh[i]);
+        }
         if (hs && threadIdx.x == 0) {  // lower bound of hz in the sorted list
             uint32_t a = 0, n2 = d;
             while (n2 > 0) {
@@ -1055,11 +1081,39 @@ __global__ void k_big_keys(const uint32_t *__restrict__ off32, const uint32_t *_
 
 __global__ void k_big_back(const uint32_t *__restrict__ off32, const uint32_t *__restrict__ big,
                            const uint32_t *__restrict__ cstart, uint32_t nbig, int vb,
-                           const uint64_t *__restrict__ keys, uint32_t *__restrict__ dst) {
+                           const uint64_t *__restrict__ keys, uint32_t *__restrict__ dst, const VFill vf) {
     const uint64_t mask = (1ull << vb) - 1;
     for (uint32_t b = blockIdx.x; b < nbig; b += gridDim.x) {
         const uint32_t u = big[b], s = off32[u], d = off32[u + 1] - s, c = cstart[b];
-        for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) dst[s + i] = (uint32_t)(keys[c + i] & mask);
+        for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) {
+            const uint32_t x = (uint32_t)(keys[c + i] & mask);
+            dst[s + i] = x;
+            vfill(vf, s + i, s + d, x);
+        }
+    }
+}
+
+// hubstart of the long lists below the hub zone before their sort (the v-major test reads
+// it for heads in [z0, hz) with |adj(v)| > nhcap): elements < hz of the unsorted list, one
+// warp per list.
+__global__ void __launch_bounds__(256)
+    k_hub_count_long(const uint32_t *__restrict__ off32, const uint32_t *__restrict__ dst, uint32_t z0,
+                     uint32_t hz, uint32_t nhcap, uint32_t *__restrict__ hs) {
+    const unsigned lane = lane_id();
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t b = z0 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; b < hz; b += nw * 32) {
+        const uint32_t v = b + lane;
+        const uint32_t d = v < hz ? off32[v + 1] - off32[v] : 0u;
+        unsigned lm = __ballot_sync(TC_FULL_MASK, d > nhcap);
+        while (lm) {
+            const int l = __ffs(lm) - 1;
+            lm &= lm - 1;
+            const uint32_t w = b + l, s = off32[w], e = off32[w + 1];
+            uint32_t c = 0;
+            for (uint32_t i = s + lane; i < e; i += 32) c += dst[i] < hz ? 1u : 0u;
+            c = warp_sum(c);
+            if (lane == 0) hs[w] = s + c;
+        }
     }
 }
 
@@ -1119,8 +1173,41 @@ static cudaStream_t fork_stream(int i) {
     return ss[i];
 }
 
+// Prepares the v-major in-edge index that the segmented sorts fill (VFill) when full counts
+// of this graph will run the v-major schedule: hub parameters, the capacity layout from the
+// degrees, hubstart of the long low-zone lists, zeroed fill counts.  Returns vf.vp.z0 = ~0
+// (fill off) otherwise.
+static int prepare_vfill(DeviceGraph *g, const uint32_t *deg_by_rank, const uint32_t *max_out_dev, VFill *vf,
+                         cudaStream_t s) {
+    vf->vp.z0 = 0xffffffffu;
+    if (!deg_by_rank || !opts().vix || !g->off32 || !g->hubstart || g->n == 0) return 0;
+    set_hub_params(g);
+    TC_CUDA(cudaMemcpyAsync(&g->max_out, max_out_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    if (!vmajor_schedule(*g)) return 0;
+    TC_CHECK(vin_capacity_dev(g, deg_by_rank, s));
+    const VSplit vp = make_vsplit(*g, true);
+    const uint32_t nz = (uint32_t)(g->n - vp.z0);
+    TC_CHECK(dalloc_t(&g->vix_cnt, (size_t)nz + 1, s, g->persistent));  // [nz]: overflow flag
+    TC_CHECK(dalloc_t(&g->vix_in_e, g->vin_total ? g->vin_total : 1, s, g->persistent));
+    TC_CUDA(cudaMemsetAsync(g->vix_cnt, 0, ((size_t)nz + 1) * sizeof(uint32_t), s));
+    if (vp.z0 < g->hz) {
+        k_hub_count_long<<<kSMs * 8, 256, 0, s>>>(g->off32, g->dst, vp.z0, g->hz, vp.nhcap, g->hubstart);
+        TC_LAUNCHED();
+    }
+    vf->vp = vp;
+    vf->off32 = g->off32;
+    vf->start = g->vin_cap;
+    vf->cnt = g->vix_cnt;
+    vf->flag = g->vix_cnt + nz;
+    vf->in_e = g->vix_in_e;
+    g->vix_vp = vp;
+    return 0;
+}
+
 static int bucket_csr_dev(const uint64_t *keys, uint64_t m, uint64_t n, int vb, uint32_t *outdeg,
-                          DeviceGraph *out, uint32_t *max_out_dev, cudaStream_t s) {
+                          DeviceGraph *out, uint32_t *max_out_dev, cudaStream_t s,
+                          const uint32_t *deg_by_rank) {
     unsigned long long *sums = nullptr;
     const uint64_t nt = (n + kScanTile - 1) / kScanTile;
     TC_CHECK(dalloc_t(&sums, nt ? nt : 1, s));
@@ -1155,6 +1242,9 @@ static int bucket_csr_dev(const uint64_t *keys, uint64_t m, uint64_t n, int vb, 
     const uint32_t hz = n > kHubRanks ? (uint32_t)(n - kHubRanks) : 0u;
     if (!out->hubstart) TC_CHECK(dalloc_t(&out->hubstart, n, s, out->persistent));
     uint32_t *hs = out->hubstart;
+    // the v-major in-edge index is filled as the sorts place every element
+    VFill vf;
+    TC_CHECK(prepare_vfill(out, deg_by_rank, max_out_dev, &vf, s));
     // The size classes sort disjoint lists: the five latency-bound sorts run concurrently
     // (forked off s, joined back before the long-list radix pass reads `counts`).
     const bool fork = opts().seg_fork != 0;
@@ -1169,23 +1259,23 @@ static int bucket_csr_dev(const uint64_t *keys, uint64_t m, uint64_t n, int vb, 
             TC_CUDA(cudaStreamWaitEvent(ss[i], ev_fork, 0));
         }
     }
-    k_seg_sort4k<<<kSMs * 8 * 256 / TC_SORT4K_NT, TC_SORT4K_NT, 0, ss[0]>>>(out->off32, mid, counts + 1, out->dst, hz, hs);
+    k_seg_sort4k<<<kSMs * 8 * 256 / TC_SORT4K_NT, TC_SORT4K_NT, 0, ss[0]>>>(out->off32, mid, counts + 1, out->dst, hz, hs, vf);
     TC_LAUNCHED();
-    k_seg_sort_warp<32><<<kSMs * 8, 256, 0, ss[1]>>>(out->off32, w1k, counts + 4, out->dst, hz, hs);
+    k_seg_sort_warp<32><<<kSMs * 8, 256, 0, ss[1]>>>(out->off32, w1k, counts + 4, out->dst, hz, hs, vf);
     TC_LAUNCHED();
     if (k16) {
-        k_seg_sort_warp<16><<<kSMs * 8, 256, 0, ss[2]>>>(out->off32, w512, counts + 5, out->dst, hz, hs);
+        k_seg_sort_warp<16><<<kSMs * 8, 256, 0, ss[2]>>>(out->off32, w512, counts + 5, out->dst, hz, hs, vf);
         TC_LAUNCHED();
     }
     if (w2) {
-        k_seg_sort_warp<64><<<kSMs * 4, 256, 0, ss[0]>>>(out->off32, w2k, counts + 6, out->dst, hz, hs);
+        k_seg_sort_warp<64><<<kSMs * 4, 256, 0, ss[0]>>>(out->off32, w2k, counts + 6, out->dst, hz, hs, vf);
         TC_LAUNCHED();
     }
-    k_seg_sort_warp<8><<<kSMs * 8, 256, 0, ss[2]>>>(out->off32, w256, counts + 3, out->dst, hz, hs);
+    k_seg_sort_warp<8><<<kSMs * 8, 256, 0, ss[2]>>>(out->off32, w256, counts + 3, out->dst, hz, hs, vf);
     TC_LAUNCHED();
-    k_seg_sort64<<<kSMs * 8, 256, 0, ss[3]>>>(out->off32, warpl, counts + 0, out->dst, hz, hs);
+    k_seg_sort64<<<kSMs * 8, 256, 0, ss[3]>>>(out->off32, warpl, counts + 0, out->dst, hz, hs, vf);
     TC_LAUNCHED();
-    k_seg_sort16<<<grid_for(n, 256, kSMs * 16), 256, 0, s>>>(out->off32, n, out->dst, hz, hs);
+    k_seg_sort16<<<grid_for(n, 256, kSMs * 16), 256, 0, s>>>(out->off32, n, out->dst, hz, hs, vf);
     TC_LAUNCHED();
     if (fork) {
         for (int i = 0; i < 4; ++i) {
@@ -1224,7 +1314,7 @@ static int bucket_csr_dev(const uint64_t *keys, uint64_t m, uint64_t n, int vb, 
         TC_CHECK(radix_sort(bk, balt, nullptr, nullptr, tot, plan, hist, kOutKeys, nullptr, nullptr, 0,
                             &sorted, nullptr, s));
         k_big_back<<<nbig < kSMs * 8 ? nbig : kSMs * 8, 256, 0, s>>>(out->off32, big, cstart, nbig, vb,
-                                                                    sorted, out->dst);
+                                                                    sorted, out->dst, vf);
         TC_LAUNCHED();
         k_big_hubstart<<<grid_for(nbig, 256, kSMs), 256, 0, s>>>(out->off32, big, nbig, out->dst, hz, hs);
         TC_LAUNCHED();
@@ -1236,6 +1326,20 @@ static int bucket_csr_dev(const uint64_t *keys, uint64_t m, uint64_t n, int vb, 
     k_fill_src<<<grid_for(n, 256, kSMs * 16), 256, 0, s>>>(out->off32, n, out->src);
     TC_LAUNCHED();
     out->hubstart_ready = true;
+    if (vf.vp.z0 != 0xffffffffu) {
+        // a non-symmetric input overflows the capacity layout: no prebuilt index then (the
+        // count builds an exact one)
+        uint32_t flag = 0;
+        TC_CUDA(cudaMemcpyAsync(&flag, vf.flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        TC_CUDA(cudaStreamSynchronize(s));
+        out->vix_ready = flag == 0;
+        if (!out->vix_ready) {
+            dfree(out->vix_cnt, s);
+            dfree(out->vix_in_e, s);
+            out->vix_cnt = nullptr;
+            out->vix_in_e = nullptr;
+        }
+    }
     dfree(counts, s);
     dfree(warpl, s);
     dfree(w256, s);
@@ -1312,7 +1416,7 @@ int preprocess_rank_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, 
     const uint64_t m = kept;
     TC_CHECK(graph_alloc(out, m, n, s));
     if (bucket) {
-        TC_CHECK(bucket_csr_dev(keys, m, n, vb, outdeg, out, scratch + 1, s));
+        TC_CHECK(bucket_csr_dev(keys, m, n, vb, outdeg, out, scratch + 1, s, deg_by_rank));
         TC_CUDA(cudaMemsetAsync(out->dst + m, 0, 8 * sizeof(uint32_t), s));
     } else {
         TC_CHECK(dalloc_t(&alt, m ? m : 1, s));
@@ -1323,7 +1427,7 @@ int preprocess_rank_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, 
     }
     TC_CHECK(build_hubstart_dev(out, s));
     if (deg_by_rank) {
-        TC_CHECK(vin_capacity_dev(out, deg_by_rank, s));
+        if (!out->vix_ready) TC_CHECK(vin_capacity_dev(out, deg_by_rank, s));
         dfree(deg_by_rank, s);
     }
     TC_CUDA(cudaMemcpyAsync(&out->max_out, scratch + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));

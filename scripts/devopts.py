@@ -8,7 +8,7 @@ NAMES = ("vmajor", "vzone_log2", "vlow_all", "vm_bias", "dense_factor", "hub_unr
          "shard_ovh", "shard_ucap", "dense_ranks", "bucket", "count_stats", "hubpack", "rank_primary",
          "shard_ovh2", "copy_threads", "seg_fork", "shard_w_dense", "shard_w_sparse", "shard_w_light",
          "shard_w_stage", "shard_w_edge", "shard_w_hub", "shard_w_vlow", "shard_w_vedge", "vin_overlap",
-         "vin_grid", "seg_k16", "vhub", "seg_w2k", "vhub_unroll", "vhub_blocks")
+         "vin_grid", "seg_k16", "vhub", "seg_w2k", "vhub_unroll", "vhub_blocks", "vhub_b16w", "hub_cap_div", "vix")
 
 
 def apply():

@@ -380,6 +380,29 @@ def test_count_schedules_agree(opts, golden_big):
         assert tcb.count_with_timings(EdgeArray(p))[0] == oracle.count(*oracle.preprocess(p))
 
 
+def test_prebuilt_vmajor_index():
+    """The rank-space preprocess fills the v-major in-edge index inside its segmented sorts
+    (option vix) when full counts will run v-major; a full count reuses it only when its
+    split equals the one the index was filled with.  Same count for: the reused index
+    (twice), a count under a different split (index rebuilt), the index turned off, and
+    ranged counts (always rebuilt over the range)."""
+    pairs = oracle.symmetrize(oracle.rmat_pairs(15, 16, seed=11))
+    want = oracle.count(*oracle.preprocess(pairs))
+    g = EdgeArray(np.ascontiguousarray(pairs, dtype=np.uint32))
+    got = []
+    with _lib.options(vmajor=1):
+        og = tcb.preprocess(g)
+        got += [tcb.count_triangles(og), tcb.count_triangles(og)]
+        with _lib.options(vmajor=1, vm_bias=2):
+            got.append(tcb.count_triangles(og))
+        half = og.m_dir // 2
+        got.append(tcb.count_partitioned(og, tcb.PartitionPlan(2, (0, half, og.m_dir)), 1))
+        got.append(tcb.count_with_timings(g)[0])
+    with _lib.options(vmajor=1, vix=0):
+        got.append(tcb.count_with_timings(g)[0])
+    assert got == [want] * len(got), got
+
+
 def test_forced_vmajor_without_hubs(golden_big):
     """v-major forced on graphs without hubs (BA 10^7, RGG 2*10^7: the zone lies below the
     hub zone, thousands of small warp tasks, cuckoo tables at load 1/3 -- RGG produced key
