@@ -1534,13 +1534,10 @@ __global__ void TC_VM_BOUNDS(NT)
 
 // ------------------------------------------------------- v-major, hub heads ---
 // Hub heads v >= hz: the same per-head schedule as k_count_vmajor, with a leaner item sweep.
-//  * No per-item bounds: every lane tests all items of its aligned 16-byte chunks.  The items
-//    of an in-edge's first and last chunk that lie outside its suffix [a, b) are tested a
-//    second time by the thread that owns the in-edge and subtracted (at most 3 + 3 items, or
-//    7 + 7 in 16-bit chunks), so the hot loop is load, shift, mask, LDS, shift, add.  Those
-//    outside items can be any vertex: the 32-bit probe masks the word address into the
-//    power-of-two bitmap allocation, which keeps every access in bounds and deterministic
-//    (the subtraction re-reads exactly what the sweep read).
+//  * No per-item bounds: the flattened sweep covers only the whole aligned chunks of each
+//    suffix [a, b) (16 bytes, or 32 bytes of 16-bit items); the < 1 chunk of items before
+//    the first and after the last whole chunk are probed one by one by the thread that owns
+//    the in-edge.  The hot loop is load, shift, mask, LDS, shift, add.
 //  * Heads in the top 2^16 ranks (t16 = n - 2^16): every suffix item after v lies in
 //    [t16, n), so the suffixes are read from a 16-bit copy of edge_dst (lo16[p] = dst[p] -
 //    t16; 2 B per item, 8 items per 16-byte chunk) against a 2^16-bit bitmap (8 KB).  At
@@ -1561,12 +1558,54 @@ __device__ __forceinline__ uint32_t bit32(const unsigned char *bm, uint32_t w, u
 // Software-pipelined: the U chunks of the next round are in flight while this round's items
 // are probed, and all shared-memory probes of a round are issued before their results are
 // used (the probe chain LDS -> shift -> add is latency-bound otherwise).
+// A chunk is CW consecutive 32-bit words: 16-bit items come in 32-byte chunks (16 items, one
+// 256-bit load), 32-bit items in 16-byte chunks (4 items).
+#ifndef TC_B16W
+#define TC_B16W 8  // words per 16-bit chunk: 4 (16 B, 8 items) or 8 (32 B, one 256-bit load)
+#endif
+template <bool B16>
+struct ChunkT {
+    static constexpr int CW = B16 ? TC_B16W : 4;               // words per chunk
+    static constexpr uint32_t E = B16 ? 2u * TC_B16W : 4u;      // items per chunk
+    uint32_t w[CW];
+};
+
+template <bool B16>
+__device__ __forceinline__ void ldg_chunk(const void *arr, uint32_t p, ChunkT<B16> &q) {
+    if (B16 && ChunkT<B16>::CW == 4) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(arr) + p));
+        q.w[0] = v.x;
+        q.w[1] = v.y;
+        q.w[2] = v.z;
+        q.w[3] = v.w;
+    } else if (B16) {
+        const uint16_t *a = static_cast<const uint16_t *>(arr) + p;  // 32-byte aligned
+        asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(q.w[0]), "=r"(q.w[1]), "=r"(q.w[2]), "=r"(q.w[3]), "=r"(q.w[4]), "=r"(q.w[5]),
+                       "=r"(q.w[6]), "=r"(q.w[7])
+                     : "l"(a));
+    } else {
+        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(arr) + p));
+        q.w[0] = v.x;
+        q.w[1] = v.y;
+        q.w[2] = v.z;
+        q.w[3] = v.w;
+    }
+}
+
+// Chunk c of the window belongs to the in-edge k with cst[k] <= c < cst[k+1]; its items are
+// at element cb[k] + E c.  Lanes past c1 count nothing.  Software-pipelined: the U chunks
+// of the next round are in flight while this round's items are probed, and all
+// shared-memory probes of a round are issued before their results are used (the probe
+// chain LDS -> shift -> add is latency-bound otherwise).
 template <int U, bool B16>
 __device__ __forceinline__ uint32_t sweep_nomask(const void *__restrict__ arr, const uint32_t *s_cb,
                                                  const uint32_t *s_cst, uint32_t nwin, uint32_t c0, uint32_t c1,
                                                  const unsigned char *bm, uint32_t hz, uint32_t amask) {
-    constexpr uint32_t E = B16 ? 8u : 4u;
-    constexpr int NI = B16 ? 8 * U : 4 * U;  // items per lane per round
+    using Q = ChunkT<B16>;
+    constexpr uint32_t E = Q::E;
+    constexpr int NIC = (int)E;   // items per chunk
+    constexpr int NI = NIC * U;   // items per lane per round
     const unsigned lane = lane_id();
     uint32_t k = 0;
     {
@@ -1579,7 +1618,7 @@ __device__ __forceinline__ uint32_t sweep_nomask(const void *__restrict__ arr, c
         k = a;
     }
     uint32_t nextb = s_cst[k + 1], cb = s_cb[k];
-    auto fetch = [&](uint32_t base, uint4 (&q)[U], uint32_t &live) {
+    auto fetch = [&](uint32_t base, Q (&q)[U], uint32_t &live) {
         live = 0;
 #pragma unroll
         for (int j = 0; j < U; ++j) {
@@ -1590,44 +1629,52 @@ __device__ __forceinline__ uint32_t sweep_nomask(const void *__restrict__ arr, c
                 do { nextb = s_cst[++k + 1]; } while (c >= nextb);
                 cb = s_cb[k];
             }
-            const uint32_t p = cb + E * c;
-            if (B16) q[j] = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(arr) + p));
-            else q[j] = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(arr) + p));
+#ifdef TC_VHUB_NOLOAD  // diagnostic build: no suffix loads (items synthesised)
+#pragma unroll
+            for (int i = 0; i < Q::CW; ++i) q[j].w[i] = (cb + E * c) * 2654435761u + i;
+#else
+            ldg_chunk<B16>(arr, cb + E * c, q[j]);
+#endif
         }
     };
-    auto probe = [&](const uint4 (&q)[U], uint32_t live) -> uint32_t {
+    auto probe = [&](const Q (&q)[U], uint32_t live) -> uint32_t {
         uint32_t ad[NI], sh[NI], wd[NI];
 #pragma unroll
         for (int j = 0; j < U; ++j) {
-            const uint32_t x4[4] = {q[j].x, q[j].y, q[j].z, q[j].w};
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
+            for (int i = 0; i < Q::CW; ++i) {
+                const uint32_t x = q[j].w[i];
                 if (B16) {
-                    ad[8 * j + 2 * i] = (x4[i] >> 3) & 0x1ffcu;
-                    sh[8 * j + 2 * i] = x4[i];
-                    ad[8 * j + 2 * i + 1] = (x4[i] >> 19) & 0x1ffcu;
-                    sh[8 * j + 2 * i + 1] = x4[i] >> 16;
+                    ad[NIC * j + 2 * i] = (x >> 3) & 0x1ffcu;
+                    sh[NIC * j + 2 * i] = x;
+                    ad[NIC * j + 2 * i + 1] = (x >> 19) & 0x1ffcu;
+                    sh[NIC * j + 2 * i + 1] = x >> 16;
                 } else {
-                    const uint32_t r = x4[i] - hz;
-                    ad[4 * j + i] = (r >> 3) & amask;
-                    sh[4 * j + i] = r;
+                    const uint32_t r = x - hz;
+                    ad[NIC * j + i] = (r >> 3) & amask;
+                    sh[NIC * j + i] = r;
                 }
             }
         }
 #pragma unroll
-        for (int t = 0; t < NI; ++t) wd[t] = *reinterpret_cast<const uint32_t *>(bm + ad[t]);
+        for (int t = 0; t < NI; ++t)
+#ifdef TC_VHUB_NOPROBE  // diagnostic build: no shared-memory probes
+            wd[t] = ad[t];
+#else
+            wd[t] = *reinterpret_cast<const uint32_t *>(bm + ad[t]);
+#endif
         uint32_t f = 0;
 #pragma unroll
         for (int j = 0; j < U; ++j) {
             uint32_t h = 0;
 #pragma unroll
-            for (int t = 0; t < NI / U; ++t) h += (wd[j * (NI / U) + t] >> (sh[j * (NI / U) + t] & 31u)) & 1u;
+            for (int t = 0; t < NIC; ++t) h += (wd[j * NIC + t] >> (sh[j * NIC + t] & 31u)) & 1u;
             f += ((live >> j) & 1u) ? h : 0u;
         }
         return f;
     };
     uint32_t found = 0;
-    uint4 qa[U], qb[U];
+    Q qa[U], qb[U];
     uint32_t la = 0, lb = 0;
     fetch(c0, qa, la);
     for (uint32_t base = c0;;) {
@@ -1641,37 +1688,6 @@ __device__ __forceinline__ uint32_t sweep_nomask(const void *__restrict__ arr, c
         if (base >= c1) break;
     }
     return found;
-}
-
-// The items of [F, F + E * chunks) outside [a, b): positions < a in the first chunk and
-// positions >= b in the last one (same chunk when chunks == 1).
-template <bool B16>
-__device__ __forceinline__ uint32_t edge_outside(const void *__restrict__ arr, uint32_t a, uint32_t b,
-                                                 uint32_t F, uint32_t chunks, const unsigned char *bm,
-                                                 uint32_t hz, uint32_t amask) {
-    constexpr uint32_t E = B16 ? 8u : 4u;
-    const uint32_t L = F + E * (chunks - 1);
-    uint32_t x = 0;
-    if (B16) {
-        const uint4 qf = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(arr) + F));
-        const uint4 ql = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(arr) + L));
-        const uint32_t f4[4] = {qf.x, qf.y, qf.z, qf.w}, l4[4] = {ql.x, ql.y, ql.z, ql.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            x += (F + 2 * i < a ? bit16(bm, f4[i] & 0xffffu) : 0u) + (F + 2 * i + 1 < a ? bit16(bm, f4[i] >> 16) : 0u);
-            x += (L + 2 * i >= b ? bit16(bm, l4[i] & 0xffffu) : 0u) + (L + 2 * i + 1 >= b ? bit16(bm, l4[i] >> 16) : 0u);
-        }
-    } else {
-        const uint4 qf = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(arr) + F));
-        const uint4 ql = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint32_t *>(arr) + L));
-        const uint32_t f4[4] = {qf.x, qf.y, qf.z, qf.w}, l4[4] = {ql.x, ql.y, ql.z, ql.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            x += F + i < a ? bit32(bm, f4[i], hz, amask) : 0u;
-            x += L + i >= b ? bit32(bm, l4[i], hz, amask) : 0u;
-        }
-    }
-    return x;
 }
 
 // BT: tasks are (head, first, end) index ranges (the source-blocked top-band tasks);
@@ -1735,27 +1751,40 @@ __global__ void __launch_bounds__(NT)
             const uint2 ie = ie_n;  // (edge, end of adj(u)); the next window's is loaded now
             ie_n = ps + NT + threadIdx.x < p1 ? __ldg(in_e + ps + NT + threadIdx.x) : make_uint2(0u, 0u);
             if (threadIdx.x < nwin) {
+                // whole aligned chunks [A, B) of the suffix [a, b) go to the sweep; the few
+                // items of [a, A) and [B, b) (< one chunk each) are probed here, one by one
                 const uint32_t a = ie.x + 1, b = ie.y;  // a < b by construction
-                if (b16) {
-                    F = a & ~7u;
-                    chunks = (b - F + 7) >> 3;
-                    acc -= edge_outside<true>(lo16, a, b, F, chunks, smem, hz, amask);
-                } else {
-                    F = a & ~3u;
-                    chunks = (b - F + 3) >> 2;
-                    acc -= edge_outside<false>(dst, a, b, F, chunks, smem, hz, amask);
+                const uint32_t E = b16 ? ChunkT<true>::E : ChunkT<false>::E;
+                const uint32_t A = (a + E - 1) & ~(E - 1), B = b & ~(E - 1);
+                uint32_t lead_end = b, tail_begin = b;  // no whole chunk: every item here
+                if (A < B) {
+                    F = A;
+                    chunks = (B - A) / E;
+                    lead_end = A;
+                    tail_begin = B;
                 }
+                uint32_t x = 0;
+                if (b16) {
+                    for (uint32_t p = a; p < lead_end; ++p) x += bit16(smem, __ldg(lo16 + p));
+                    for (uint32_t p = tail_begin; p < b; ++p) x += bit16(smem, __ldg(lo16 + p));
+                } else {
+                    for (uint32_t p = a; p < lead_end; ++p) x += bit32(smem, __ldg(dst + p), hz, amask);
+                    for (uint32_t p = tail_begin; p < b; ++p) x += bit32(smem, __ldg(dst + p), hz, amask);
+                }
+                acc += x;
             }
             uint32_t tot;
             const uint32_t cst = block_exclusive_scan<uint32_t>(chunks, s_scan, &tot);
-            s_cb[threadIdx.x] = F - (b16 ? 8u : 4u) * cst;
+            s_cb[threadIdx.x] = F - (b16 ? ChunkT<true>::E : ChunkT<false>::E) * cst;
             s_cst[threadIdx.x] = cst;
             if (threadIdx.x == 0) s_cst[NT] = tot;
             __syncthreads();
             const uint32_t c0 = (uint32_t)((uint64_t)tot * warp / NW);
             const uint32_t c1 = (uint32_t)((uint64_t)tot * (warp + 1) / NW);
             if (c0 < c1) {
-                if (b16) acc += sweep_nomask<U, true>(lo16, s_cb, s_cst, NT, c0, c1, smem, hz, amask);
+                if (b16)
+                    acc += sweep_nomask<TC_B16W == 4 ? U : (U + 1) / 2, true>(lo16, s_cb, s_cst, NT, c0, c1, smem, hz,
+                                                                              amask);
                 else acc += sweep_nomask<U, false>(dst, s_cb, s_cst, NT, c0, c1, smem, hz, amask);
             }
             __syncthreads();
@@ -2235,8 +2264,8 @@ int vmajor_index(const DeviceGraph &g, const RangeDev *rg, uint64_t span, cudaSt
         // 16-bit copy of edge_dst for the top-2^16 heads of k_count_vhub
         const uint64_t ng = (g.m + 3) / 4;
         const uint32_t t16 = g.n - g.hz > kT16 ? (uint32_t)(g.n - kT16) : g.hz;
-        TC_CHECK(dalloc_t(&st->lo16t, 4 * ng + 32, s2));
-        TC_CUDA(cudaMemsetAsync(st->lo16t + 4 * ng, 0, 64, s2));
+        TC_CHECK(dalloc_t(&st->lo16t, 4 * ng + 64, s2));  // 32-byte chunks read past m
+        TC_CUDA(cudaMemsetAsync(st->lo16t + 4 * ng, 0, 128, s2));
         k_pack16<<<grid_for(ng, 256, kSMs * 8), 256, 0, s2>>>(g.dst, g.m, t16, st->lo16t);
         TC_LAUNCHED();
         const int64_t nbo = opts().vhub_blocks;
@@ -2765,7 +2794,8 @@ __device__ __forceinline__ uint64_t edge_bytes(const uint32_t *__restrict__ src,
     const uint32_t sfx = eu - (uint32_t)e - 1;
     if (vmajor_edge(vp, (uint32_t)e, eu, v, vs, ve)) {
         *cls = 0;
-        return (vp.packed && v >= vp.hz ? 9ull * ((sfx + 3) / 4) : 4ull * sfx) + 8;
+        // 16-bit suffix copy for heads >= t16 (k_count_vhub): 2 B per item
+        return (vp.packed && v >= vp.hz ? 9ull * ((sfx + 3) / 4) : v >= vp.t16 ? 2ull * sfx : 4ull * sfx) + 8;
     }
     if (du > (uint32_t)kLightMax) {
         *cls = 1;
