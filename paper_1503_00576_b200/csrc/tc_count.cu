@@ -1143,7 +1143,11 @@ __global__ void TC_HUB_BOUNDS(NT)
 // keep their dependent load chains (task -> offsets -> lists) in flight together, which
 // the CTA-per-task hub kernel (one 32 KB bitmap per task) cannot.
 constexpr int kMidWarps = 8;
-constexpr uint32_t kMidSlots = 3 * 512;
+#ifndef TC_MID_LOADINV
+#define TC_MID_LOADINV 2  // 2: 4 KB per warp, 6 CTAs per SM (3: 6 KB, 4 CTAs; s26 mid 14.6 -> 13.6 ms)
+#endif
+constexpr uint32_t kMidLoadInv = TC_MID_LOADINV;  // per-warp cuckoo table load <= 1/kMidLoadInv
+constexpr uint32_t kMidSlots = kMidLoadInv * 512;
 
 template <int WARPS, uint32_t SLOTS, uint32_t LOADINV>
 __global__ void __launch_bounds__(32 * WARPS)
@@ -1560,6 +1564,9 @@ __device__ __forceinline__ uint32_t bit32(const unsigned char *bm, uint32_t w, u
 // used (the probe chain LDS -> shift -> add is latency-bound otherwise).
 // A chunk is CW consecutive 32-bit words: 16-bit items come in 32-byte chunks (16 items, one
 // 256-bit load), 32-bit items in 16-byte chunks (4 items).
+#ifndef TC_VHUB_DEPTH
+#define TC_VHUB_DEPTH 1  // rounds of suffix chunks in flight ahead of the probed one
+#endif
 #ifndef TC_B16W
 #define TC_B16W 8  // words per 16-bit chunk: 4 (16 B, 8 items) or 8 (32 B, one 256-bit load)
 #endif
@@ -1674,6 +1681,25 @@ __device__ __forceinline__ uint32_t sweep_nomask(const void *__restrict__ arr, c
         return f;
     };
     uint32_t found = 0;
+#if TC_VHUB_DEPTH >= 2
+    // two rounds in flight ahead of the one being probed
+    Q qa[U], qb[U], qc[U];
+    uint32_t la = 0, lb = 0, lc = 0;
+    constexpr uint32_t R = 32 * U;
+    fetch(c0, qa, la);
+    if (c0 + R < c1) fetch(c0 + R, qb, lb);
+    for (uint32_t base = c0;;) {
+        if (base + 2 * R < c1) fetch(base + 2 * R, qc, lc);  // warp-uniform
+        found += probe(qa, la);
+        if ((base += R) >= c1) break;
+        if (base + 2 * R < c1) fetch(base + 2 * R, qa, la);
+        found += probe(qb, lb);
+        if ((base += R) >= c1) break;
+        if (base + 2 * R < c1) fetch(base + 2 * R, qb, lb);
+        found += probe(qc, lc);
+        if ((base += R) >= c1) break;
+    }
+#else
     Q qa[U], qb[U];
     uint32_t la = 0, lb = 0;
     fetch(c0, qa, la);
@@ -1687,13 +1713,19 @@ __device__ __forceinline__ uint32_t sweep_nomask(const void *__restrict__ arr, c
         found += probe(qb, lb);
         if (base >= c1) break;
     }
+#endif
     return found;
 }
 
 // BT: tasks are (head, first, end) index ranges (the source-blocked top-band tasks);
 // otherwise (head, chunk) as in k_count_vmajor.
+#ifdef TC_VHUB_MINB
+#define TC_VHUB_BOUNDS(nt) __launch_bounds__(nt, TC_VHUB_MINB)
+#else
+#define TC_VHUB_BOUNDS(nt) __launch_bounds__(nt)
+#endif
 template <int NT, int U, bool BT>
-__global__ void __launch_bounds__(NT)
+__global__ void TC_VHUB_BOUNDS(NT)
     k_count_vhub(const uint32_t *__restrict__ dst, const uint16_t *__restrict__ lo16,
                  const uint32_t *__restrict__ off, uint32_t z0, uint32_t hz, uint32_t t16, uint32_t hwp,
                  uint32_t amask, const uint32_t *__restrict__ start, const uint32_t *__restrict__ fillc,
@@ -2075,7 +2107,11 @@ static void clear_l2_window(cudaStream_t s) {
 // over the lanes and probed.  These heads have small in-degrees, so many small independent
 // tasks are in flight per SM (no block barriers).
 constexpr int kVlWarps = 8;
-constexpr uint32_t kVlSlots = 3 * kVNonHubCap;  // cuckoo load <= 1/3: 4 CTAs per SM
+#ifndef TC_VL_LOADINV
+#define TC_VL_LOADINV 2  // 2: 4 KB per warp, 6 CTAs per SM (3: 6 KB, 4 CTAs; s26 vlow 27 -> 23 ms)
+#endif
+constexpr uint32_t kVlLoadInv = TC_VL_LOADINV;  // per-warp cuckoo table load <= 1/kVlLoadInv
+constexpr uint32_t kVlSlots = kVlLoadInv * kVNonHubCap;  // cuckoo load <= 1/3: 4 CTAs per SM
 
 // FB = false: the cuckoo path; a task whose table cannot be built is deferred (its index
 // appended to `defer`).  FB = true: the deferred tasks, probed by binary search of the sorted
@@ -2106,7 +2142,7 @@ __global__ void __launch_bounds__(32 * kVlWarps)
         const uint32_t h = task.x, v = z0 + h;
         const uint32_t vs = __ldg(off + v), ve = __ldg(off + v + 1), d = ve - vs;
         if (d > kVNonHubCap) continue;  // long list: a CTA task (warp-uniform)
-        Cuckoo32 ck{smem_addr(tab), 3 * d < kVlSlots ? 3 * d : kVlSlots, 0, 0};
+        Cuckoo32 ck{smem_addr(tab), kVlLoadInv * d < kVlSlots ? kVlLoadInv * d : kVlSlots, 0, 0};
         if (!FB) {
             bool deferred = false;
             for (uint32_t seed = 0;; ++seed) {
@@ -2550,7 +2586,7 @@ int count_impl(const DeviceGraph &g, const OffT *off, uint64_t lo, uint64_t hi,
             g.hubstart) {
             const VSplit vp = make_vsplit(g, vmajor);
             // cuckoo load <= 1/3: 6 KB per warp, 4 CTAs (32 warps) per SM (load 1/4: 3 CTAs, +12 %)
-            if (c == 0) TC_CHECK((launch_mid<kMidWarps, kMidSlots, 3>(g, vp, rg, tasks[c], nt_c, next_c, d_total, s)));
+            if (c == 0) TC_CHECK((launch_mid<kMidWarps, kMidSlots, kMidLoadInv>(g, vp, rg, tasks[c], nt_c, next_c, d_total, s)));
             else TC_CHECK((launch_mid<4, 3 * 2048, 3>(g, vp, rg, tasks[c], nt_c, next_c, d_total, s)));
             continue;
         }

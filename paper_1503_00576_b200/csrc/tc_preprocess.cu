@@ -38,9 +38,15 @@ constexpr int kPP = 8;  // pairs per thread per iteration (warp-striped)
 // deg[u] += 1 for every pair (u, .): reference degrees = np.diff(node array of the sorted
 // pairs) (preprocess.py:79-80), i.e. the first-column histogram (graph.py:279-281).
 // Runs of equal u inside a warp (the common, sorted-input case) become one atomic.
+#ifndef TC_DEG_PP
+#define TC_DEG_PP 8  // 4 / 8 / 16 pairs per lane: 4.9 / 4.7 / 4.9 ms at s26
+#endif
+constexpr int kDegPP = TC_DEG_PP;  // pairs per lane per iteration of the degree histogram
+
 __global__ void __launch_bounds__(256) k_degree_hist(const uint2 *__restrict__ pairs,
                                                      uint64_t npairs, uint32_t *__restrict__ deg,
                                                      uint64_t n, unsigned *__restrict__ bad) {
+    constexpr int kPP = kDegPP;
     const unsigned lane = lane_id();
     const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -144,7 +150,8 @@ __global__ void __launch_bounds__(256) k_orient(const uint2 *__restrict__ pairs,
 #pragma unroll
         for (int i = 0; i < kPP; ++i) {
             if (keepmask & (1u << i)) {
-                if (out < capacity) keys[out] = key[i];
+                // streaming store: the keys must not evict the rank table the gathers hit
+                if (out < capacity) __stcs(reinterpret_cast<unsigned long long *>(keys) + out, key[i]);
                 ++out;
 #pragma unroll
                 for (int p = 0; p < kMaxPasses; ++p)
@@ -602,7 +609,7 @@ int preprocess_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, Devic
     TC_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
 
     if (npairs) {
-        k_degree_hist<<<grid_for(npairs, 256 * kPP, kSMs * 8), 256, 0, s>>>(pairs, npairs, deg, n,
+        k_degree_hist<<<grid_for(npairs, 256 * kDegPP, kSMs * 8), 256, 0, s>>>(pairs, npairs, deg, n,
                                                                             scratch);
         TC_LAUNCHED();
     }
@@ -1372,7 +1379,7 @@ int preprocess_rank_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, 
     TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
     TC_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
     if (npairs) {
-        k_degree_hist<<<grid_for(npairs, 256 * kPP, kSMs * 8), 256, 0, s>>>(pairs, npairs, deg, n,
+        k_degree_hist<<<grid_for(npairs, 256 * kDegPP, kSMs * 8), 256, 0, s>>>(pairs, npairs, deg, n,
                                                                             scratch);
         TC_LAUNCHED();
     }
@@ -1617,7 +1624,7 @@ int dist_degrees_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, uin
     TC_CUDA(cudaMemsetAsync(bad_d, 0, sizeof(uint32_t), s));
     TC_CUDA(cudaMemsetAsync(deg, 0, (n ? n : 1) * sizeof(uint32_t), s));
     if (npairs) {
-        k_degree_hist<<<grid_for(npairs, 256 * kPP, kSMs * 8), 256, 0, s>>>(pairs, npairs, deg, n, bad_d);
+        k_degree_hist<<<grid_for(npairs, 256 * kDegPP, kSMs * 8), 256, 0, s>>>(pairs, npairs, deg, n, bad_d);
         TC_LAUNCHED();
     }
     uint32_t bad = 0;

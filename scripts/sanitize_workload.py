@@ -37,6 +37,9 @@ def main():
     check("k600", oracle.symmetrize(k600))
     with _lib.options(vmajor=1, vzone_log2=19):
         check("rmat_14_forced_vmajor", oracle.rmat_edges(14, 16, seed=0))
+    # the index built at count time (k_vin_pass, overlapped)
+    with _lib.options(vmajor=1, vzone_log2=19, vix=0):
+        check("rmat_14_forced_vmajor_vix0", oracle.rmat_edges(14, 16, seed=0))
     src = np.array([0, 0, 0, 0, 0, 1, 1], np.uint32)
     dst = np.array([1, 2, 3, 4, 5, 2, 6], np.uint32)
     off = np.array([0, 5, 7, 7, 7, 7, 7, 7], np.int64)

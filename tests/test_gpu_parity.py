@@ -354,6 +354,7 @@ def test_rank_space_csr_matches_numpy(case):
     {"vmajor": 1, "vin_overlap": 0, "seg_k16": 0},   # in-edge index serial; 1024-wide sorts
     {"vmajor": 1, "vhub_blocks": 8, "seg_w2k": 1},   # source-blocked top-band tasks; warp 2K sorts
     {"vmajor": 1, "vhub_unroll": 1},                 # unpipelined-width sweep
+    {"vmajor": 1, "vix": 0},                         # index built at count time (k_vin_pass)
 ], ids=lambda o: ",".join(f"{k}={v}" for k, v in o.items()))
 def test_count_schedules_agree(opts, golden_big):
     """Every count schedule (v-major on/off and its zone, the per-edge bias, the light and
