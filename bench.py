@@ -388,6 +388,7 @@ def main():
     og, _ = tcb.preprocess_device(dev_edges)
     W = tcb.merge_work(og)
     assert og.m_dir == m
+    del og  # ~30 GB of device graph (rank-space CSR, index, reference-id CSR) not needed below
     host_graph = None
     ops = B200Ops(local, comm="cpu" if args.share_gpu else "cuda") if world > 1 else None
     sb = shard_bounds(npairs, world)
@@ -497,7 +498,6 @@ def main():
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         if host_graph is None:
             host_graph = dev_edges.to_host(pinned=True)
-        del og
         dev_edges.free()
         cpu = cpu_baseline(host_graph.edges, host_graph.num_vertices, args.cpu_seconds, workload)
 

@@ -221,6 +221,68 @@ static void parallel_memcpy(void *dst, const void *src, size_t bytes, int thread
     g_copy_pool->copy(dst, src, bytes);
 }
 
+// Host pairs -> device with the first-column degree histogram of each chunk running on s
+// while the next chunk is still being copied (copies on a side stream, one event per
+// chunk): the histogram pass -- the only preprocessing step that needs no other chunk --
+// is hidden under the PCIe transfer.  *pre receives the degrees for preprocess_rank_dev.
+static cudaStream_t copy_stream() {
+    static cudaStream_t cs = nullptr;
+    if (!cs) cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    return cs;
+}
+
+static int h2d_degrees(uint32_t *dst, const uint32_t *src, uint64_t npairs, uint64_t n, PreDegrees *pre,
+                       cudaStream_t s) {
+    constexpr size_t kChunk = 256ull << 20;  // bytes per pinned chunk (a multiple of 8)
+    TC_CHECK(dalloc_t(&pre->deg, n ? n : 1, s));
+    TC_CHECK(dalloc_t(&pre->bad, 1, s));
+    TC_CUDA(cudaMemsetAsync(pre->deg, 0, (n ? n : 1) * sizeof(uint32_t), s));
+    TC_CUDA(cudaMemsetAsync(pre->bad, 0, sizeof(uint32_t), s));
+    if (!npairs) return 0;
+    cudaStream_t cs = copy_stream();
+    static cudaEvent_t ev = nullptr, ev0 = nullptr;
+    if (!ev) {
+        TC_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        TC_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
+    }
+    TC_CUDA(cudaEventRecord(ev0, s));  // dst allocated on s
+    TC_CUDA(cudaStreamWaitEvent(cs, ev0, 0));
+    const size_t bytes = npairs * 8;
+    auto chunk_done = [&](size_t off, size_t len) -> int {
+        TC_CUDA(cudaEventRecord(ev, cs));
+        TC_CUDA(cudaStreamWaitEvent(s, ev, 0));
+        return degree_hist_dev(dst + off / 4, len / 8, n, pre->deg, pre->bad, s);
+    };
+    if (bytes < (32u << 20) || !is_pageable(src)) {
+        for (size_t off = 0; off < bytes; off += kChunk) {
+            const size_t len = bytes - off < kChunk ? bytes - off : kChunk;
+            TC_CUDA(cudaMemcpyAsync((char *)dst + off, (const char *)src + off, len, cudaMemcpyHostToDevice, cs));
+            TC_CHECK(chunk_done(off, len));
+        }
+        return 0;
+    }
+    if (!g_stage[0])
+        for (int b = 0; b < kStageBufs; ++b) {
+            TC_CUDA(cudaHostAlloc(&g_stage[b], kStageBytes, cudaHostAllocDefault));
+            TC_CUDA(cudaEventCreateWithFlags(&g_stage_ev[b], cudaEventDisableTiming));
+        }
+    const unsigned hc = std::thread::hardware_concurrency();
+    const int threads = opts().copy_threads > 0 ? (int)opts().copy_threads
+                        : hc >= 16 ? 8 : hc >= 4 ? (int)hc / 2 : 1;
+    size_t off = 0;
+    for (int k = 0; off < bytes; ++k) {
+        const int b = k % kStageBufs;
+        const size_t len = bytes - off < kStageBytes ? bytes - off : kStageBytes;
+        TC_CUDA(cudaEventSynchronize(g_stage_ev[b]));  // the copy out of this buffer finished
+        parallel_memcpy(g_stage[b], (const char *)src + off, len, threads);
+        TC_CUDA(cudaMemcpyAsync((char *)dst + off, g_stage[b], len, cudaMemcpyHostToDevice, cs));
+        TC_CUDA(cudaEventRecord(g_stage_ev[b], cs));
+        TC_CHECK(chunk_done(off, len));
+        off += len;
+    }
+    return 0;
+}
+
 static int h2d(void *dst, const void *src, size_t bytes, cudaStream_t s) {
     if (!bytes) return 0;
     if (bytes < (32u << 20) || !is_pageable(src)) {
@@ -441,24 +503,31 @@ int tc_preprocess_ex(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, in
     TC_CUDA(cudaEventRecord(ev.e[0], s));
     const uint32_t *dpairs = pairs;
     uint32_t *owned = nullptr;  // staging copy: default pool, freed at the end of the call
+    const bool rank_path = (flags & TC_PREPROCESS_RANK_SPACE) ||
+                           (npairs / 2 < (1ull << 32) && nverts < (1ull << 32) && opts().rank_primary);
+    PreDegrees pre;
     if (!pairs_on_device && npairs) {
         TC_CHECK(dalloc_t(&owned, 2 * npairs, s, true));
-        TC_CHECK(h2d(owned, pairs, npairs * 8, s));
+        // rank path: the degree histogram runs chunk by chunk under the copy
+        if (rank_path && nverts < (1ull << 32) && npairs / 2 < (1ull << 32))
+            TC_CHECK(h2d_degrees(owned, pairs, npairs, nverts, &pre, s));
+        else TC_CHECK(h2d(owned, pairs, npairs * 8, s));
         dpairs = owned;
     }
+    const PreDegrees *prep = pre.deg ? &pre : nullptr;
     TC_CUDA(cudaEventRecord(ev.e[1], s));
     tc_graph *g = new tc_graph();
     g->g.persistent = true;
     int rc;
     if (flags & TC_PREPROCESS_RANK_SPACE) {
-        rc = preprocess_rank_dev(dpairs, npairs, nverts, &g->g, s);
+        rc = preprocess_rank_dev(dpairs, npairs, nverts, &g->g, s, nullptr, prep);
     } else if (npairs / 2 < (1ull << 32) && nverts < (1ull << 32) && opts().rank_primary) {
         // the count-ready rank-space CSR is built (as the fused path does) and the reference-id
         // CSR only on demand
         g->rank = new DeviceGraph();
         g->rank->persistent = true;
         rc = dalloc_t(&g->id_of_rank, nverts ? nverts : 1, s, true);
-        if (!rc) rc = preprocess_rank_dev(dpairs, npairs, nverts, g->rank, s, g->id_of_rank);
+        if (!rc) rc = preprocess_rank_dev(dpairs, npairs, nverts, g->rank, s, g->id_of_rank, prep);
         if (!rc) {
             g->g.m = g->rank->m;
             g->g.n = g->rank->n;
@@ -472,6 +541,7 @@ int tc_preprocess_ex(const uint32_t *pairs, uint64_t npairs, uint64_t nverts, in
     } else {
         rc = preprocess_dev(dpairs, npairs, nverts, &g->g, s);
     }
+    dfree(pre.bad, s);
     if (owned) dfree(owned, s);
     if (rc) {
         graph_release(&g->g, s);
@@ -717,16 +787,20 @@ int tc_count_with_timings(const uint32_t *pairs, uint64_t npairs, uint64_t nvert
     TC_CUDA(cudaEventRecord(ev.e[0], s));
     const uint32_t *dpairs = pairs;
     uint32_t *owned = nullptr;  // staging copy: default pool, freed at the end of the call
+    const bool rank = algo == TC_ALGO_AUTO && npairs / 2 < (1ull << 32) && nverts < (1ull << 32);
+    PreDegrees pre;
     if (!pairs_on_device && npairs) {
         TC_CHECK(dalloc_t(&owned, 2 * npairs, s, true));
-        TC_CHECK(h2d(owned, pairs, npairs * 8, s));
+        // rank path: the degree histogram runs chunk by chunk under the copy
+        if (rank) TC_CHECK(h2d_degrees(owned, pairs, npairs, nverts, &pre, s));
+        else TC_CHECK(h2d(owned, pairs, npairs * 8, s));
         dpairs = owned;
     }
     TC_CUDA(cudaEventRecord(ev.e[1], s));
     DeviceGraph g;
-    const bool rank = algo == TC_ALGO_AUTO && npairs / 2 < (1ull << 32) && nverts < (1ull << 32);
-    int rc = rank ? preprocess_rank_dev(dpairs, npairs, nverts, &g, s)
+    int rc = rank ? preprocess_rank_dev(dpairs, npairs, nverts, &g, s, nullptr, pre.deg ? &pre : nullptr)
                   : preprocess_dev(dpairs, npairs, nverts, &g, s);
+    dfree(pre.bad, s);
     if (rc) {
         if (owned) dfree(owned, s);
         graph_release(&g, s);

@@ -225,8 +225,17 @@ int preprocess_dev(const uint32_t *pairs, uint64_t npairs, uint64_t n, DeviceGra
                    cudaStream_t s);
 // The same pipeline producing the rank-space oriented CSR (+ hubstart) directly; with
 // id_of_rank (u32[n], caller-allocated) also the inverse relabelling.
+// pre: degrees (u32[n], zero-initialised then accumulated by degree_hist_dev over every
+// chunk of the pairs, e.g. while they were copied in) and its invalid-id flag; the
+// preprocess takes ownership of pre->deg (scratch pool, stream s).
+struct PreDegrees {
+    uint32_t *deg = nullptr, *bad = nullptr;
+};
 int preprocess_rank_dev(const uint32_t *pairs, uint64_t npairs, uint64_t n, DeviceGraph *out,
-                        cudaStream_t s, uint32_t *id_of_rank = nullptr);
+                        cudaStream_t s, uint32_t *id_of_rank = nullptr, const PreDegrees *pre = nullptr);
+// First-column histogram of pairs (u32 pairs) into deg; *bad |= 1 on an id >= n.
+int degree_hist_dev(const uint32_t *pairs, uint64_t npairs, uint64_t n, uint32_t *deg, uint32_t *bad,
+                    cudaStream_t s);
 // Reference-id CSR of a preprocess_rank_dev graph (exact inverse relabelling + sort).
 int derank_dev(const DeviceGraph &r, const uint32_t *id_of_rank, DeviceGraph *out, cudaStream_t s);
 // Distributed preprocessing steps (tc_preprocess.cu).

@@ -1358,8 +1358,17 @@ static int bucket_csr_dev(const uint64_t *keys, uint64_t m, uint64_t n, int vb, 
     return 0;
 }
 
+int degree_hist_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, uint32_t *deg, uint32_t *bad,
+                    cudaStream_t s) {
+    if (!npairs) return 0;
+    k_degree_hist<<<grid_for(npairs, 256 * kDegPP, kSMs * 8), 256, 0, s>>>(
+        reinterpret_cast<const uint2 *>(pairs_u32), npairs, deg, n, bad);
+    TC_LAUNCHED();
+    return 0;
+}
+
 int preprocess_rank_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, DeviceGraph *out,
-                        cudaStream_t s, uint32_t *id_of_rank) {
+                        cudaStream_t s, uint32_t *id_of_rank, const PreDegrees *pre) {
     const uint2 *pairs = reinterpret_cast<const uint2 *>(pairs_u32);
     if (n >= (1ull << 32) || npairs / 2 >= (1ull << 32)) {
         set_error("rank-space preprocessing needs num_vertices < 2^32 and m < 2^32");
@@ -1369,22 +1378,26 @@ int preprocess_rank_dev(const uint32_t *pairs_u32, uint64_t npairs, uint64_t n, 
     const RadixPlan plan = make_radix_plan(2 * vb);
     uint32_t *deg = nullptr, *rank = nullptr, *hist = nullptr, *scratch = nullptr;
     unsigned long long *cursor = nullptr;
-    TC_CHECK(dalloc_t(&deg, n ? n : 1, s));
+    if (pre) {
+        deg = pre->deg;  // histogram already taken chunk by chunk during the H2D copy (owned now)
+    } else {
+        TC_CHECK(dalloc_t(&deg, n ? n : 1, s));
+    }
     TC_CHECK(dalloc_t(&rank, n ? n : 1, s));
     TC_CHECK(dalloc_t(&scratch, 4, s));
     TC_CHECK(dalloc_t(&hist, kMaxPasses * kRadix, s));
     TC_CHECK(dalloc_t(&cursor, 1, s));
-    TC_CUDA(cudaMemsetAsync(deg, 0, (n ? n : 1) * sizeof(uint32_t), s));
+    if (!pre) TC_CUDA(cudaMemsetAsync(deg, 0, (n ? n : 1) * sizeof(uint32_t), s));
     TC_CUDA(cudaMemsetAsync(scratch, 0, 4 * sizeof(uint32_t), s));
     TC_CUDA(cudaMemsetAsync(hist, 0, kMaxPasses * kRadix * sizeof(uint32_t), s));
     TC_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
-    if (npairs) {
+    if (npairs && !pre) {
         k_degree_hist<<<grid_for(npairs, 256 * kDegPP, kSMs * 8), 256, 0, s>>>(pairs, npairs, deg, n,
                                                                             scratch);
         TC_LAUNCHED();
     }
     uint32_t bad = 0;
-    TC_CUDA(cudaMemcpyAsync(&bad, scratch, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaMemcpyAsync(&bad, pre ? pre->bad : scratch, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));
     if (bad) {
         set_error("edge array holds a vertex id >= num_vertices");
