@@ -210,7 +210,7 @@ def cpu_baseline(pairs, n, budget_s, workload):
     return out
 
 
-def e2e_variants(tcb, host_graph, m, tri_ref, timer, elapsed, barrier, steps=2):
+def e2e_variants(tcb, host_graph, m, tri_ref, timer, elapsed, barrier, steps=3):
     """The same metric through the other reference-facing call shapes:
     the two-call path count_triangles(preprocess(g)) of the reference's tests, and
     count_with_timings over an EdgeArray in ordinary pageable numpy memory."""
@@ -220,17 +220,24 @@ def e2e_variants(tcb, host_graph, m, tri_ref, timer, elapsed, barrier, steps=2):
     out = {}
 
     def run(name, fn):
-        fn()  # warm (twice: the first call of a shape grows the memory pools)
-        fn()
+        warm = []
+        for _ in range(3):  # warm: the first calls of a call shape grow the memory pools
+            t0 = time.perf_counter()
+            fn()
+            warm.append(round(1e3 * (time.perf_counter() - t0), 1))
         barrier()
         timer(4)
+        walls = []
         for _ in range(steps):
+            t0 = time.perf_counter()
             if fn() != tri_ref:
                 raise RuntimeError(f"{name}: count differs")
+            walls.append(round(1e3 * (time.perf_counter() - t0), 1))
         timer(5)
         barrier()
         ms = elapsed(4, 5) / steps
-        out[name] = {"value": m / (ms / 1e3), "unit": "edges/s", "ms_per_step": ms}
+        out[name] = {"value": m / (ms / 1e3), "unit": "edges/s", "ms_per_step": ms,
+                     "warm_wall_ms": warm, "step_wall_ms": walls}
 
     run("two_call_pinned", lambda: tcb.count_triangles(tcb.preprocess(host_graph)))
     nbytes = host_graph.edges.nbytes
