@@ -465,9 +465,11 @@ def main():
         tcb.count_with_timings(host_graph)  # warm
         barrier()
         timer(2)
-        phase = []
+        phase, walls = [], []
         for _ in range(e2e_steps):
+            t0 = time.perf_counter()
             tri, pt = tcb.count_with_timings(host_graph)
+            walls.append(round(1e3 * (time.perf_counter() - t0), 2))
             if tri != tri_ref:
                 raise RuntimeError("e2e count differs")
             phase.append(pt)
@@ -479,7 +481,7 @@ def main():
                "ms_per_step": e2e_ms / e2e_steps,
                "preprocess_ms_incl_h2d": statistics.mean(p.preprocess_ms for p in phase),
                "count_ms": statistics.mean(p.count_ms for p in phase),
-               "path": "count_with_timings(EdgeArray over pinned host memory)"}
+               "path": "count_with_timings(EdgeArray over pinned host memory)", "step_wall_ms": walls}
         e2e["variants"] = e2e_variants(tcb, host_graph, m, tri_ref, timer, elapsed, barrier)
     elif world > 1 and e2e_steps > 0:
         # every rank copies only its own shard of the pinned host edge array (sharded H2D)

@@ -407,6 +407,40 @@ __device__ __forceinline__ uint32_t sweep_and(const uint32_t *__restrict__ bits,
     return found;
 }
 
+// Block-wide exclusive scan of two values per thread with one set of barriers.
+// smem: 2 * 32 entries.  Returns the block totals in *ta, *tb.
+__device__ __forceinline__ void block_exclusive_scan2(unsigned long long a, uint32_t b, unsigned long long *s_a,
+                                                      uint32_t *s_b, unsigned long long *xa, uint32_t *xb,
+                                                      unsigned long long *ta, uint32_t *tb) {
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    unsigned long long ia = warp_inclusive_scan(a);
+    uint32_t ib = warp_inclusive_scan(b);
+    if (lane == 31) {
+        s_a[warp] = ia;
+        s_b[warp] = ib;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const unsigned long long wa = lane < nw ? s_a[lane] : 0ull;
+        const uint32_t wb = lane < nw ? s_b[lane] : 0u;
+        const unsigned long long wia = warp_inclusive_scan(wa);
+        const uint32_t wib = warp_inclusive_scan(wb);
+        if (lane < nw) {
+            s_a[lane] = wia - wa;
+            s_b[lane] = wib - wb;
+        }
+        if (lane == nw - 1) {
+            s_a[31] = wia;
+            s_b[31] = wib;
+        }
+    }
+    __syncthreads();
+    *xa = s_a[warp] + ia - a;
+    *xb = s_b[warp] + ib - b;
+    *ta = s_a[31];
+    *tb = s_b[31];
+}
+
 template <typename T>
 __device__ __forceinline__ void block_add_total(T acc, unsigned long long *total) {
     __shared__ unsigned long long s_red[32];
@@ -967,6 +1001,9 @@ __global__ void __launch_bounds__(NT)
 // see few bank conflicts); the few non-hub elements of adj(u) go into a small cuckoo
 // table.  hubstart[v] splits every adj(v) into a non-hub prefix and a hub suffix, which
 // are swept separately so each probe path is branch-free.
+#ifndef TC_HUB_FUSED
+#define TC_HUB_FUSED 1  // the three per-window passes scanned together (one barrier pair)
+#endif
 #ifdef TC_HUB_MINB
 #define TC_HUB_BOUNDS(nt) __launch_bounds__(nt, TC_HUB_MINB)
 #else
@@ -984,15 +1021,26 @@ __global__ void TC_HUB_BOUNDS(NT)
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t *bitmap = reinterpret_cast<uint32_t *>(smem);  // hwords
     uint32_t *ctab = bitmap + hwords;                        // cap slots
+#if TC_HUB_FUSED
+    // one table per pass (0: hub suffixes, 1: non-hub prefixes, 2: dense ANDs), all three
+    // scanned at once: one barrier pair per window instead of one per pass
+    __shared__ uint32_t s_cb3[3][NT], s_vs3[3][NT], s_ve3[2][NT];
+    __shared__ uint32_t s_cst3[3][NT + 4];
+    __shared__ unsigned long long s_sa[32];
+    __shared__ uint32_t s_sb[32];
+#else
     __shared__ uint32_t s_cb[NT], s_vs[NT], s_ve[NT];
     __shared__ uint32_t s_cst[NT + 4];
     __shared__ uint32_t s_scan[32];
+#endif
     __shared__ unsigned s_task, s_fail;
     constexpr int NW = NT / 32;
     const unsigned warp = threadIdx.x >> 5;
     const uint64_t lo = rg->lo, hi = rg->hi;
     const unsigned nt = *ntasks;
+#if !TC_HUB_FUSED
     const EdgeTable<uint32_t> et{s_cb, s_vs, s_ve, s_cst, nullptr};
+#endif
     const uint32_t bm = smem_addr(bitmap);
     for (uint32_t i = threadIdx.x; i < hwords; i += NT) bitmap[i] = 0;
     unsigned long long acc = 0;
@@ -1082,6 +1130,59 @@ __global__ void TC_HUB_BOUNDS(NT)
             // pass 1: non-hub prefixes [vs, hv) against the cuckoo table (only if adj(u)
             //         has non-hub elements -- otherwise they cannot match);
             // pass 2: dense edges, popcount(B_u & B_v) over v's hub words.
+#if TC_HUB_FUSED
+            {
+                const uint32_t h4 = hv & ~3u, v4 = vs & ~3u;
+                const uint32_t ch0 = ve > hv ? (ve - h4 + 3) >> 2 : 0u;
+                const uint32_t ch1 = nh && hv > vs ? (hv - v4 + 3) >> 2 : 0u;
+                const uint32_t ch2 = dense ? (hwords - dws) >> 2 : 0u;
+                unsigned long long x01, t01;
+                uint32_t x2, t2;
+                block_exclusive_scan2((unsigned long long)ch0 | ((unsigned long long)ch1 << 32), ch2, s_sa, s_sb,
+                                      &x01, &x2, &t01, &t2);
+                const uint32_t x0 = (uint32_t)x01, x1 = (uint32_t)(x01 >> 32);
+                const uint32_t tt[3] = {(uint32_t)t01, (uint32_t)(t01 >> 32), t2};
+                if (tt[0] | tt[1] | tt[2]) {  // block-uniform
+                    const uint32_t t = threadIdx.x;
+                    s_cb3[0][t] = h4 - 4 * x0;
+                    s_vs3[0][t] = hv;
+                    s_ve3[0][t] = ve;
+                    s_cst3[0][t] = x0;
+                    s_cb3[1][t] = v4 - 4 * x1;
+                    s_vs3[1][t] = vs;
+                    s_ve3[1][t] = hv;
+                    s_cst3[1][t] = x1;
+                    s_cb3[2][t] = dgo - 4 * x2;
+                    s_vs3[2][t] = dws - 4 * x2;
+                    s_cst3[2][t] = x2;
+                    if (t < 3) s_cst3[t][NT] = tt[t];
+                    __syncthreads();
+#pragma unroll
+                    for (int pass = 0; pass < 3; ++pass) {
+                        const uint32_t tot = tt[pass];
+                        const uint32_t c0 = (uint32_t)((uint64_t)tot * warp / NW);
+                        const uint32_t c1 = (uint32_t)((uint64_t)tot * (warp + 1) / NW);
+                        if (c0 >= c1) continue;
+                        const EdgeTable<uint32_t> et{s_cb3[pass], s_vs3[pass], pass < 2 ? s_ve3[pass] : nullptr,
+                                                     s_cst3[pass], nullptr};
+                        if (pass == 2) {
+                            acc += sweep_and<U>(dense_bits, et, NT, c0, c1, bm);
+                        } else if (pass == 0) {
+                            if (hp.lo16) acc += sweep_bits18<U>(hp, et, NT, c0, c1, bitmap);
+                            else acc += sweep_bits<U>(dst, et, NT, c0, c1, bitmap, hz);
+                        } else if (tab_ok) {
+                            acc += sweep<uint32_t, false>(dst, et, NT, c0, c1,
+                                                          [&](uint32_t w, uint32_t) { return ck.contains(w); });
+                        } else {
+                            acc += sweep<uint32_t, false>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t) {
+                                return sorted_contains(dst + s, nh, w);
+                            });
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+#else
             for (int pass = 0; pass < 3; ++pass) {
                 if (pass == 1 && !nh) continue;
                 uint32_t chunks, cb, vsb;
@@ -1125,6 +1226,7 @@ __global__ void TC_HUB_BOUNDS(NT)
                 }
                 __syncthreads();
             }
+#endif
         }
         // clear the bits this task set (O(d), not O(bitmap))
         for (uint32_t i = nh + threadIdx.x; i < e - s; i += NT)
