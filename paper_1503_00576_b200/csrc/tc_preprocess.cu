@@ -93,11 +93,12 @@ __global__ void __launch_bounds__(256) k_orient(const uint2 *__restrict__ pairs,
                                                 RadixPlan plan, uint32_t *__restrict__ ghist,
                                                 uint32_t *__restrict__ outdeg = nullptr) {
     __shared__ uint32_t sh[kMaxPasses * kRadix];
-    __shared__ uint32_t s_scan[32];
-    __shared__ unsigned long long s_base;
+    __shared__ uint32_t s_wcnt[2][32];
+    __shared__ unsigned long long s_base[2];
     for (int i = threadIdx.x; i < plan.npass * kRadix; i += blockDim.x) sh[i] = 0;
     __syncthreads();
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    unsigned iter = 0;
     const uint64_t per_block = (uint64_t)blockDim.x * kPP;
     for (uint64_t base = (uint64_t)blockIdx.x * per_block; base < npairs;
          base += (uint64_t)gridDim.x * per_block) {
@@ -142,11 +143,25 @@ __global__ void __launch_bounds__(256) k_orient(const uint2 *__restrict__ pairs,
                 if (k && lane == (unsigned)(__ffs(peers) - 1)) atomicAdd(outdeg + src, (unsigned)__popc(peers));
             }
         }
-        uint32_t mine = __popc(keepmask), tot;
-        uint32_t off = block_exclusive_scan<uint32_t>(mine, s_scan, &tot);
-        if (threadIdx.x == 0) s_base = atomicAdd(cursor, (unsigned long long)tot);
+        // block compaction: warp scan, then warp 0 scans the warp totals and reserves the
+        // block's output range with one cursor atomic -- two barriers per iteration (the
+        // warp-base array alternates between two buffers, so no trailing barrier)
+        const uint32_t mine = __popc(keepmask);
+        const uint32_t incl = warp_inclusive_scan(mine);
+        uint32_t *wc = s_wcnt[iter & 1];
+        if (lane == 31) wc[warp] = incl;
         __syncthreads();
-        uint64_t out = s_base + off;
+        if (warp == 0) {
+            const unsigned nw = blockDim.x >> 5;
+            const uint32_t w = lane < nw ? wc[lane] : 0u;
+            const uint32_t wi = warp_inclusive_scan(w);
+            const uint32_t tot = __shfl_sync(TC_FULL_MASK, wi, nw - 1);
+            if (lane < nw) wc[lane] = wi - w;
+            if (lane == 0) s_base[iter & 1] = tot ? atomicAdd(cursor, (unsigned long long)tot) : 0ull;
+        }
+        __syncthreads();
+        uint64_t out = s_base[iter & 1] + wc[warp] + incl - mine;
+        ++iter;
 #pragma unroll
         for (int i = 0; i < kPP; ++i) {
             if (keepmask & (1u << i)) {
@@ -159,7 +174,6 @@ __global__ void __launch_bounds__(256) k_orient(const uint2 *__restrict__ pairs,
                         atomicAdd(&sh[p * kRadix + ((key[i] >> plan.shift[p]) & ((1u << plan.bits[p]) - 1))], 1u);
             }
         }
-        __syncthreads();
     }
     __syncthreads();
     for (int i = threadIdx.x; i < plan.npass * kRadix; i += blockDim.x)
