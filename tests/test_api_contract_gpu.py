@@ -214,3 +214,25 @@ def test_foreign_oriented_graph_objects():
     assert tcb.count_triangles(og) == oracle.count(s, d, o)
     assert sum(tcb.intersect_count(og, int(u), int(v)) for u, v in zip(s[:200], d[:200])) == \
         sum(oracle.intersect_count(d, o, int(u), int(v)) for u, v in zip(s[:200], d[:200]))
+
+
+def test_chunked_copy_with_overlapped_degrees(golden_big):
+    """Host pairs are copied in 256 MB chunks (pinned) or 128 MB staged chunks (pageable)
+    while the degree histogram of each landed chunk runs on the compute stream.  R-MAT s21
+    (537 MB of pairs: several chunks of either kind) through count_with_timings and the
+    two-call path equals the reference golden; an out-of-range id placed in the last chunk
+    is still reported as ValueError by both entry points."""
+    d = generators.rmat_device(21, 16, seed=0)
+    pinned = d.to_host(pinned=True)
+    d.free()
+    want = golden_big["rmat_21_16_0"]["triangles"]
+    pageable = EdgeArray(np.array(pinned.edges), num_vertices=pinned.num_vertices)
+    for g in (pinned, pageable):
+        assert tcb.count_with_timings(g)[0] == want
+        assert tcb.count_triangles(tcb.preprocess(g)) == want
+    bad = np.array(pinned.edges)
+    bad[-1, 0] = pinned.num_vertices  # id == num_vertices: out of range
+    with pytest.raises(ValueError):
+        tcb.count_with_timings(EdgeArray(bad, num_vertices=pinned.num_vertices))
+    with pytest.raises(ValueError):
+        tcb.preprocess(EdgeArray(bad, num_vertices=pinned.num_vertices))
