@@ -213,7 +213,9 @@ int tc_reserve(uint64_t bytes);
  * them -- the library never reads the environment.  Names: vmajor, vzone_log2, vlow_all,
  * vm_bias, dense_factor, hub_unroll, l2_persist_mb, l2_target, concurrent, share, midwarp,
  * light, skew, light_vec, shard_model, shard_ovh, shard_ucap, dense_ranks, bucket,
- * count_stats, hubpack, rank_primary (see csrc/tc_internal.h Options).  Unknown names return -1. */
+ * count_stats, hubpack, rank_primary, seg_fork, vin_overlap, vin_grid, seg_k16, seg_w2k,
+ * vhub, vhub_unroll, vhub_blocks, vhub_b16w, hub_cap_div, vix, shard_w_* (see
+ * csrc/tc_internal.h Options).  Unknown names return -1. */
 /* Compulsory HBM bytes of the full-count schedule (rank-space copy of g): out[0] v-major
  * suffix streams + index entries, [1] u-major heavy-source reads of heads, [2] light-source
  * reads, [3] 16 B per edge (src, dst, two offsets), [4] heavy-source staging.  The roofline
