@@ -920,11 +920,15 @@ __global__ void __launch_bounds__(256)
         uint32_t below = 0;  // non-hub prefix length (elements < hz; pads are ~0)
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-            if ((uint32_t)i < d) {
-                dst[s + i] = x[i];
-                vfill(vf, s + i, s + d, x[i]);
-            }
+            if ((uint32_t)i < d) dst[s + i] = x[i];
             below += x[i] < hz ? 1u : 0u;
+        }
+#pragma unroll
+        for (int i0 = 0; i0 < 16; i0 += 4) {  // the index fill, 4 elements at a time
+            const uint32_t eg[4] = {s + i0, s + i0 + 1, s + i0 + 2, s + i0 + 3};
+            const uint32_t vg[4] = {x[i0], x[i0 + 1], x[i0 + 2], x[i0 + 3]};
+            const bool okg[4] = {(uint32_t)i0 < d, (uint32_t)i0 + 1 < d, (uint32_t)i0 + 2 < d, (uint32_t)i0 + 3 < d};
+            vfill_batch<4>(vf, eg, s + d, vg, okg);
         }
         if (hs) hs[u] = s + below;
     }
@@ -969,10 +973,12 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const uint32_t i = 2 * lane + h;
-            if (i < d) {
-                dst[s + i] = x[h];
-                vfill(vf, s + i, s + d, x[h]);
-            }
+            if (i < d) dst[s + i] = x[h];
+        }
+        {
+            const uint32_t e2[2] = {s + 2 * lane, s + 2 * lane + 1};
+            const bool ok2[2] = {2 * lane < d, 2 * lane + 1 < d};
+            vfill_batch<2>(vf, e2, s + d, x, ok2);
         }
         if (hs) {
             const uint32_t below = __popc(__ballot_sync(TC_FULL_MASK, x[0] < hz)) +
@@ -1033,11 +1039,22 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int r = 0; r < K; ++r) {
             const uint32_t i = 32 * r + lane;
-            if (i < d) {
-                dst[s + i] = x[r];
-                vfill(vf, s + i, s + d, x[r]);
-            }
+            if (i < d) dst[s + i] = x[r];
             below += __popc(__ballot_sync(TC_FULL_MASK, x[r] < hz));
+        }
+        // the index fill in groups of G registers (all loads / atomics of a group together)
+        constexpr int G = K < 8 ? K : 8;
+#pragma unroll
+        for (int r0 = 0; r0 < K; r0 += G) {
+            uint32_t eg[G], vg[G];
+            bool okg[G];
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+                eg[j] = s + 32 * (r0 + j) + lane;
+                vg[j] = x[r0 + j];
+                okg[j] = 32 * (r0 + j) + lane < d;
+            }
+            vfill_batch<G>(vf, eg, s + d, vg, okg);
         }
         if (hs && lane == 0) hs[u] = s + below;
     }

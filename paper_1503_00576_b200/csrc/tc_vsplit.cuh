@@ -76,4 +76,34 @@ __device__ __forceinline__ void vfill(const VFill &f, uint32_t e, uint32_t eu, u
 #endif
 }
 
+// vfill over N elements of one list at once: all offset loads first, then all predicates,
+// then all cursor atomics, then all stores -- the per-element chains overlap instead of
+// running back to back (the sorts are latency-bound).  ok[i]: element i exists.
+template <int N>
+__device__ __forceinline__ void vfill_batch(const VFill &f, const uint32_t (&e)[N], uint32_t eu,
+                                            const uint32_t (&v)[N], const bool (&ok)[N]) {
+    if (f.vp.z0 == 0xffffffffu) return;
+    uint32_t vs[N], ve[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const bool c = ok[i] && v[i] >= f.vp.z0 && e[i] + 1 < eu;
+        vs[i] = c ? __ldg(f.off32 + v[i]) : 1u;
+        ve[i] = c ? __ldg(f.off32 + v[i] + 1) : 0u;
+    }
+    bool take[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) take[i] = vs[i] < ve[i] && vmajor_edge(f.vp, e[i], eu, v[i], vs[i], ve[i]);
+    uint32_t k[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) k[i] = take[i] ? atomicAdd(f.cnt + (v[i] - f.vp.z0), 1u) : 0u;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        if (!take[i]) continue;
+        const uint32_t h = v[i] - f.vp.z0;
+        const uint32_t b = __ldg(f.start + h);
+        if (k[i] >= __ldg(f.start + h + 1) - b) *f.flag = 1u;  // not symmetric: capacity exceeded
+        else f.in_e[b + k[i]] = make_uint2(e[i], eu);
+    }
+}
+
 }  // namespace tc
