@@ -1666,6 +1666,9 @@ __device__ __forceinline__ uint32_t bit32(const unsigned char *bm, uint32_t w, u
 // used (the probe chain LDS -> shift -> add is latency-bound otherwise).
 // A chunk is CW consecutive 32-bit words: 16-bit items come in 32-byte chunks (16 items, one
 // 256-bit load), 32-bit items in 16-byte chunks (4 items).
+#ifndef TC_VHUB_WPT
+#define TC_VHUB_WPT 2  // in-edges per thread per window of k_count_vhub (window = WPT * NT)
+#endif
 #ifndef TC_VHUB_DEPTH
 #define TC_VHUB_DEPTH 1  // rounds of suffix chunks in flight ahead of the probed one
 #endif
@@ -1836,8 +1839,10 @@ __global__ void TC_VHUB_BOUNDS(NT)
                  unsigned *__restrict__ next, unsigned long long *__restrict__ total) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t *bitmap = reinterpret_cast<uint32_t *>(smem);  // (amask + 4) / 4 words
-    __shared__ uint32_t s_cb[NT];
-    __shared__ uint32_t s_cst[NT + 4];
+    constexpr int WPT = TC_VHUB_WPT;
+    constexpr uint32_t WIN = (uint32_t)NT * WPT;
+    __shared__ uint32_t s_cb[WIN];
+    __shared__ uint32_t s_cst[WIN + 4];
     __shared__ uint32_t s_scan[32];
     __shared__ unsigned s_task;
     constexpr int NW = NT / 32;
@@ -1878,48 +1883,72 @@ __global__ void TC_VHUB_BOUNDS(NT)
             atomicOr(bitmap + (r >> 5), 1u << (r & 31));
         }
         __syncthreads();
-        uint2 ie_n = p0 + threadIdx.x < p1 ? __ldg(in_e + p0 + threadIdx.x) : make_uint2(0u, 0u);
-        for (uint32_t ps = p0; ps < p1; ps += NT) {
-            const uint32_t nwin = min((uint32_t)NT, p1 - ps);
-            uint32_t chunks = 0, F = 0;
-            const uint2 ie = ie_n;  // (edge, end of adj(u)); the next window's is loaded now
-            ie_n = ps + NT + threadIdx.x < p1 ? __ldg(in_e + ps + NT + threadIdx.x) : make_uint2(0u, 0u);
-            if (threadIdx.x < nwin) {
-                // whole aligned chunks [A, B) of the suffix [a, b) go to the sweep; the few
-                // items of [a, A) and [B, b) (< one chunk each) are probed here, one by one
-                const uint32_t a = ie.x + 1, b = ie.y;  // a < b by construction
-                const uint32_t E = b16 ? ChunkT<true>::E : ChunkT<false>::E;
-                const uint32_t A = (a + E - 1) & ~(E - 1), B = b & ~(E - 1);
-                uint32_t lead_end = b, tail_begin = b;  // no whole chunk: every item here
-                if (A < B) {
-                    F = A;
-                    chunks = (B - A) / E;
-                    lead_end = A;
-                    tail_begin = B;
+        // windows of WPT * NT in-edges, WPT consecutive entries per thread (fewer barriers and
+        // scans per item); the next window's entries are loaded while this one is swept
+        uint2 ie_n[WPT];
+#pragma unroll
+        for (int i = 0; i < WPT; ++i) {
+            const uint32_t j = p0 + WPT * threadIdx.x + i;
+            ie_n[i] = j < p1 ? __ldg(in_e + j) : make_uint2(0u, 0u);
+        }
+        for (uint32_t ps = p0; ps < p1; ps += WIN) {
+            const uint32_t nwin = min(WIN, p1 - ps);
+            uint32_t ch[WPT], Fv[WPT];
+            uint2 ie[WPT];
+#pragma unroll
+            for (int i = 0; i < WPT; ++i) {
+                ie[i] = ie_n[i];
+                const uint32_t j = ps + WIN + WPT * threadIdx.x + i;
+                ie_n[i] = j < p1 ? __ldg(in_e + j) : make_uint2(0u, 0u);
+            }
+            uint32_t csum = 0;
+#pragma unroll
+            for (int i = 0; i < WPT; ++i) {
+                ch[i] = 0;
+                Fv[i] = 0;
+                if (WPT * threadIdx.x + i < nwin) {
+                    // whole aligned chunks [A, B) of the suffix [a, b) go to the sweep; the few
+                    // items of [a, A) and [B, b) (< one chunk each) are probed here, one by one
+                    const uint32_t a = ie[i].x + 1, b = ie[i].y;  // a < b by construction
+                    const uint32_t E = b16 ? ChunkT<true>::E : ChunkT<false>::E;
+                    const uint32_t A = (a + E - 1) & ~(E - 1), B = b & ~(E - 1);
+                    uint32_t lead_end = b, tail_begin = b;  // no whole chunk: every item here
+                    if (A < B) {
+                        Fv[i] = A;
+                        ch[i] = (B - A) / E;
+                        lead_end = A;
+                        tail_begin = B;
+                    }
+                    uint32_t x = 0;
+                    if (b16) {
+                        for (uint32_t p = a; p < lead_end; ++p) x += bit16(smem, __ldg(lo16 + p));
+                        for (uint32_t p = tail_begin; p < b; ++p) x += bit16(smem, __ldg(lo16 + p));
+                    } else {
+                        for (uint32_t p = a; p < lead_end; ++p) x += bit32(smem, __ldg(dst + p), hz, amask);
+                        for (uint32_t p = tail_begin; p < b; ++p) x += bit32(smem, __ldg(dst + p), hz, amask);
+                    }
+                    acc += x;
                 }
-                uint32_t x = 0;
-                if (b16) {
-                    for (uint32_t p = a; p < lead_end; ++p) x += bit16(smem, __ldg(lo16 + p));
-                    for (uint32_t p = tail_begin; p < b; ++p) x += bit16(smem, __ldg(lo16 + p));
-                } else {
-                    for (uint32_t p = a; p < lead_end; ++p) x += bit32(smem, __ldg(dst + p), hz, amask);
-                    for (uint32_t p = tail_begin; p < b; ++p) x += bit32(smem, __ldg(dst + p), hz, amask);
-                }
-                acc += x;
+                csum += ch[i];
             }
             uint32_t tot;
-            const uint32_t cst = block_exclusive_scan<uint32_t>(chunks, s_scan, &tot);
-            s_cb[threadIdx.x] = F - (b16 ? ChunkT<true>::E : ChunkT<false>::E) * cst;
-            s_cst[threadIdx.x] = cst;
-            if (threadIdx.x == 0) s_cst[NT] = tot;
+            uint32_t run = block_exclusive_scan<uint32_t>(csum, s_scan, &tot);
+#pragma unroll
+            for (int i = 0; i < WPT; ++i) {
+                const uint32_t j = WPT * threadIdx.x + i;
+                s_cb[j] = Fv[i] - (b16 ? ChunkT<true>::E : ChunkT<false>::E) * run;
+                s_cst[j] = run;
+                run += ch[i];
+            }
+            if (threadIdx.x == 0) s_cst[WIN] = tot;
             __syncthreads();
             const uint32_t c0 = (uint32_t)((uint64_t)tot * warp / NW);
             const uint32_t c1 = (uint32_t)((uint64_t)tot * (warp + 1) / NW);
             if (c0 < c1) {
                 if (b16)
-                    acc += sweep_nomask<TC_B16W == 4 ? U : (U + 1) / 2, true>(lo16, s_cb, s_cst, NT, c0, c1, smem, hz,
+                    acc += sweep_nomask<TC_B16W == 4 ? U : (U + 1) / 2, true>(lo16, s_cb, s_cst, WIN, c0, c1, smem, hz,
                                                                               amask);
-                else acc += sweep_nomask<U, false>(dst, s_cb, s_cst, NT, c0, c1, smem, hz, amask);
+                else acc += sweep_nomask<U, false>(dst, s_cb, s_cst, WIN, c0, c1, smem, hz, amask);
             }
             __syncthreads();
         }

@@ -44,9 +44,9 @@ void note_launch();
 // cannot change what the product runs.  Every schedule computes the same exact count.
 struct Options {
     int64_t vmajor = -1;         // v-major in-edge schedule: -1 auto, 0 off, 1 on
-    int64_t vzone_log2 = 22;     // v-major zone = top 2^vzone_log2 ranks (clamped to [18, 31])
+    int64_t vzone_log2 = 23;     // v-major zone = top 2^vzone_log2 ranks (clamped to [18, 31]; 22: +1 ms)
     int64_t vlow_all = 1;        // heads below the hub zone may run v-major
-    int64_t vm_bias = 4;         // per-edge choice bias (bytes) in favour of u-major
+    int64_t vm_bias = 3;         // per-edge choice bias: v-major iff bias/4 * vcost < ucost (4: +1.5 ms)
     int64_t dense_factor = 3;    // AND a dense head's bitmap when words < factor * items
     int64_t hub_unroll = 4;      // k_count_hub sweep unroll (2..4)
     int64_t l2_persist_mb = 32;  // u-major-only schedule: persisting-L2 window size

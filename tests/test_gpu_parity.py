@@ -344,6 +344,7 @@ def test_rank_space_csr_matches_numpy(case):
     {"vmajor": 1},                                   # hub-zone heads v-major
     {"vmajor": 1, "vzone_log2": 19, "vlow_all": 1},  # + heads below the hub zone
     {"vmajor": 1, "vm_bias": 1},                     # (almost) every hub-head edge v-major
+    {"vmajor": 1, "vm_bias": 4, "vzone_log2": 22},   # round-1 defaults: neutral bias, 2^22 zone
     {"vmajor": 1, "midwarp": 0, "light": 2},         # CTA mid class, warp light kernel
     {"vmajor": 0, "light": 0},                       # u-major only, CTA-window light kernel
     {"vmajor": 0, "light_vec": 1, "hub_unroll": 2},  # vector light loads, 2-way hub unroll
