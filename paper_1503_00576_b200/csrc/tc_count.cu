@@ -1519,6 +1519,9 @@ __global__ void k_vin_tasks(const uint32_t *__restrict__ start, const uint32_t *
     }
 }
 
+#ifndef TC_VHUB_WPT
+#define TC_VHUB_WPT 2  // in-edges per thread per window of k_count_vhub (window = WPT * NT)
+#endif
 #ifndef TC_VM_MINB
 #define TC_VM_BOUNDS(nt) __launch_bounds__(nt)
 #else
@@ -1537,8 +1540,10 @@ __global__ void TC_VM_BOUNDS(NT)
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t *bitmap = reinterpret_cast<uint32_t *>(smem);  // hwp words
     uint32_t *ctab = bitmap + hwp;                           // cap slots (v below hz)
-    __shared__ uint32_t s_cb[NT], s_vs[NT], s_ve[NT];
-    __shared__ uint32_t s_cst[NT + 4];
+    constexpr int VWPT = TC_VHUB_WPT;
+    constexpr uint32_t VWIN = (uint32_t)NT * VWPT;
+    __shared__ uint32_t s_cb[VWIN], s_vs[VWIN], s_ve[VWIN];
+    __shared__ uint32_t s_cst[VWIN + 4];
     __shared__ uint32_t s_scan[32];
     __shared__ unsigned s_task, s_fail;
     constexpr int NW = NT / 32;
@@ -1588,24 +1593,39 @@ __global__ void TC_VM_BOUNDS(NT)
         const uint32_t p0 = __ldg(start + h) + task.y * kVChunk;
         // fill count, clamped to the slot range (an overflowed capacity layout is recounted)
         const uint32_t p1 = min(p0 + kVChunk, min(__ldg(start + h) + __ldg(fillc + h), __ldg(start + h + 1)));
-        uint2 ie_n = p0 + threadIdx.x < p1 ? __ldg(in_e + p0 + threadIdx.x) : make_uint2(0u, 0u);
-        for (uint32_t ps = p0; ps < p1; ps += NT) {
-            const uint32_t nwin = min((uint32_t)NT, p1 - ps);
-            uint32_t chunks = 0, a = 0, b = 0;
-            const uint2 ie = ie_n;  // (edge, end of adj(u)); the next window's is loaded now
-            ie_n = ps + NT + threadIdx.x < p1 ? __ldg(in_e + ps + NT + threadIdx.x) : make_uint2(0u, 0u);
-            if (threadIdx.x < nwin) {
-                a = ie.x + 1;
-                b = ie.y;
-                chunks = (b - (a & ~3u) + 3) >> 2;  // a < b by construction
+        // windows of WPT * NT in-edges, WPT consecutive entries per thread (as k_count_vhub)
+        uint2 ie_n[VWPT];
+#pragma unroll
+        for (int i = 0; i < VWPT; ++i) {
+            const uint32_t j = p0 + VWPT * threadIdx.x + i;
+            ie_n[i] = j < p1 ? __ldg(in_e + j) : make_uint2(0u, 0u);
+        }
+        for (uint32_t ps = p0; ps < p1; ps += VWIN) {
+            const uint32_t nwin = min(VWIN, p1 - ps);
+            uint32_t ch[VWPT], av[VWPT], bv[VWPT], csum = 0;
+#pragma unroll
+            for (int i = 0; i < VWPT; ++i) {
+                const uint2 ie = ie_n[i];  // (edge, end of adj(u)); the next window's is loaded now
+                const uint32_t jn = ps + VWIN + VWPT * threadIdx.x + i;
+                ie_n[i] = jn < p1 ? __ldg(in_e + jn) : make_uint2(0u, 0u);
+                const bool ok = VWPT * threadIdx.x + i < nwin;
+                av[i] = ok ? ie.x + 1 : 0u;
+                bv[i] = ok ? ie.y : 0u;
+                ch[i] = ok ? (bv[i] - (av[i] & ~3u) + 3) >> 2 : 0u;  // a < b by construction
+                csum += ch[i];
             }
             uint32_t tot;
-            const uint32_t cst = block_exclusive_scan<uint32_t>(chunks, s_scan, &tot);
-            s_cb[threadIdx.x] = (a & ~3u) - 4 * cst;
-            s_vs[threadIdx.x] = a;
-            s_ve[threadIdx.x] = b;
-            s_cst[threadIdx.x] = cst;
-            if (threadIdx.x == 0) s_cst[NT] = tot;
+            uint32_t run = block_exclusive_scan<uint32_t>(csum, s_scan, &tot);
+#pragma unroll
+            for (int i = 0; i < VWPT; ++i) {
+                const uint32_t j = VWPT * threadIdx.x + i;
+                s_cb[j] = (av[i] & ~3u) - 4 * run;
+                s_vs[j] = av[i];
+                s_ve[j] = bv[i];
+                s_cst[j] = run;
+                run += ch[i];
+            }
+            if (threadIdx.x == 0) s_cst[VWIN] = tot;
             __syncthreads();
             const uint32_t c0 = (uint32_t)((uint64_t)tot * warp / NW);
             const uint32_t c1 = (uint32_t)((uint64_t)tot * (warp + 1) / NW);
@@ -1613,13 +1633,13 @@ __global__ void TC_VM_BOUNDS(NT)
                 // suffix items are > v: hub items hit words >= ws (staged); non-hub items
                 // (only when v < hz) are looked up in the cuckoo table
                 if (v < hz && tab_ok) {  // suffix items below hz exist: bitmap or cuckoo per item
-                    acc += sweep<uint32_t, false, U>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t) {
+                    acc += sweep<uint32_t, false, U>(dst, et, VWIN, c0, c1, [&](uint32_t w, uint32_t) {
                         const uint32_t r = w - hz;
                         const bool b = ((lds32(bm + 4 * min(r >> 5, hwp - 1)) >> (r & 31)) & 1u) != 0u;
                         return w >= hz ? b : (nh != 0 && ck.contains(w));
                     });
                 } else if (v < hz) {  // cuckoo build failed: binary search of the non-hub part
-                    acc += sweep<uint32_t, false, U>(dst, et, NT, c0, c1, [&](uint32_t w, uint32_t) {
+                    acc += sweep<uint32_t, false, U>(dst, et, VWIN, c0, c1, [&](uint32_t w, uint32_t) {
                         const uint32_t r = w - hz;
                         const bool b = ((lds32(bm + 4 * min(r >> 5, hwp - 1)) >> (r & 31)) & 1u) != 0u;
                         return w >= hz ? b : sorted_contains(dst + vs, nh, w);
@@ -1627,9 +1647,9 @@ __global__ void TC_VM_BOUNDS(NT)
                 } else if (hp.lo16) {
                     // suffix items exceed v >= hz: every valid item is a hub item, read from
                     // the 18-bit packed copy (2.25 B per item)
-                    acc += sweep_bits18<TC_PACK_U>(hp, et, NT, c0, c1, bitmap);
+                    acc += sweep_bits18<TC_PACK_U>(hp, et, VWIN, c0, c1, bitmap);
                 } else {
-                    acc += sweep_bits<U>(dst, et, NT, c0, c1, bitmap, hz);
+                    acc += sweep_bits<U>(dst, et, VWIN, c0, c1, bitmap, hz);
                 }
             }
             __syncthreads();
@@ -1666,12 +1686,6 @@ __device__ __forceinline__ uint32_t bit32(const unsigned char *bm, uint32_t w, u
 // used (the probe chain LDS -> shift -> add is latency-bound otherwise).
 // A chunk is CW consecutive 32-bit words: 16-bit items come in 32-byte chunks (16 items, one
 // 256-bit load), 32-bit items in 16-byte chunks (4 items).
-#ifndef TC_VHUB_WPT
-#define TC_VHUB_WPT 2  // in-edges per thread per window of k_count_vhub (window = WPT * NT)
-#endif
-#ifndef TC_VHUB_DEPTH
-#define TC_VHUB_DEPTH 1  // rounds of suffix chunks in flight ahead of the probed one
-#endif
 #ifndef TC_B16W
 #define TC_B16W 8  // words per 16-bit chunk: 4 (16 B, 8 items) or 8 (32 B, one 256-bit load)
 #endif
@@ -1786,25 +1800,6 @@ __device__ __forceinline__ uint32_t sweep_nomask(const void *__restrict__ arr, c
         return f;
     };
     uint32_t found = 0;
-#if TC_VHUB_DEPTH >= 2
-    // two rounds in flight ahead of the one being probed
-    Q qa[U], qb[U], qc[U];
-    uint32_t la = 0, lb = 0, lc = 0;
-    constexpr uint32_t R = 32 * U;
-    fetch(c0, qa, la);
-    if (c0 + R < c1) fetch(c0 + R, qb, lb);
-    for (uint32_t base = c0;;) {
-        if (base + 2 * R < c1) fetch(base + 2 * R, qc, lc);  // warp-uniform
-        found += probe(qa, la);
-        if ((base += R) >= c1) break;
-        if (base + 2 * R < c1) fetch(base + 2 * R, qa, la);
-        found += probe(qb, lb);
-        if ((base += R) >= c1) break;
-        if (base + 2 * R < c1) fetch(base + 2 * R, qb, lb);
-        found += probe(qc, lc);
-        if ((base += R) >= c1) break;
-    }
-#else
     Q qa[U], qb[U];
     uint32_t la = 0, lb = 0;
     fetch(c0, qa, la);
@@ -1818,7 +1813,6 @@ __device__ __forceinline__ uint32_t sweep_nomask(const void *__restrict__ arr, c
         found += probe(qb, lb);
         if (base >= c1) break;
     }
-#endif
     return found;
 }
 
