@@ -210,7 +210,7 @@ def cpu_baseline(pairs, n, budget_s, workload):
     return out
 
 
-def e2e_variants(tcb, host_graph, m, tri_ref, timer, elapsed, barrier, steps=3):
+def e2e_variants(tcb, host_graph, m, tri_ref, timer, elapsed, barrier, steps=5):
     """The same metric through the other reference-facing call shapes:
     the two-call path count_triangles(preprocess(g)) of the reference's tests, and
     count_with_timings over an EdgeArray in ordinary pageable numpy memory."""
@@ -236,8 +236,12 @@ def e2e_variants(tcb, host_graph, m, tri_ref, timer, elapsed, barrier, steps=3):
         timer(5)
         barrier()
         ms = elapsed(4, 5) / steps
+        # (these call shapes occasionally show one slow call -- a stretched H2D or preprocess
+        # inside the library's own event timing, not reproducible outside this process:
+        # scripts/two_call.py --bench-like; the median wall is reported beside the mean)
         out[name] = {"value": m / (ms / 1e3), "unit": "edges/s", "ms_per_step": ms,
-                     "warm_wall_ms": warm, "step_wall_ms": walls}
+                     "warm_wall_ms": warm, "step_wall_ms": walls,
+                     "median_wall_ms": statistics.median(walls)}
 
     run("two_call_pinned", lambda: tcb.count_triangles(tcb.preprocess(host_graph)))
     nbytes = host_graph.edges.nbytes

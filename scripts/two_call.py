@@ -1,6 +1,7 @@
 """Development aid: where the two-call path count_triangles(preprocess(g)) spends its time
 at R-MAT scale S (host pinned input): preprocess (H2D + reference-id CSR), then the first
 full count of that graph (rank-space relabel + count), then a second count (cached copy)."""
+import ctypes
 import sys
 import time
 
@@ -12,8 +13,25 @@ from paper_1503_00576_b200.preprocess import preprocess_with_timings  # noqa: E4
 S = int(sys.argv[1]) if len(sys.argv) > 1 else 26
 d = generators.rmat_device(S, 16, seed=0)
 g = d.to_host(pinned=True)
-d.free()
-for rep in range(3):
+if "--bench-like" in sys.argv:  # the bench's order: device-resident fused steps, fused pinned e2e
+    for _ in range(8):
+        tcb.count_with_timings_device(d)
+    for _ in range(6):
+        t0 = time.perf_counter()
+        tcb.count_with_timings(g)
+        print(f"fused pinned wall {1e3 * (time.perf_counter() - t0):.1f} ms", flush=True)
+else:
+    d.free()
+reps = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 3
+
+
+def mem_used_gb():
+    f, t = ctypes.c_size_t(), ctypes.c_size_t()
+    ctypes.CDLL("libcudart.so").cudaMemGetInfo(ctypes.byref(f), ctypes.byref(t))
+    return round((t.value - f.value) / 2**30, 1)
+
+
+for rep in range(reps):
     _lib.check(_lib.lib().tc_synchronize())
     t0 = time.perf_counter()
     og, tp = preprocess_with_timings(g)
@@ -26,3 +44,4 @@ for rep in range(3):
           f"first count wall {1e3 * (t2 - t1):.1f} ms (events {tc.count_ms:.1f}); "
           f"second count wall {1e3 * (t3 - t2):.1f} ms (events {tc2.count_ms:.1f}); tri {tri} {tri2}", flush=True)
     del og
+    print(f"  device memory used {mem_used_gb()} GB", flush=True)
