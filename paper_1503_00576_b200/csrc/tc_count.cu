@@ -407,6 +407,83 @@ __device__ __forceinline__ uint32_t sweep_and(const uint32_t *__restrict__ bits,
     return found;
 }
 
+// sweep_and with the edge table read through 32-bit shared addresses (a_cst / a_cb / a_vs:
+// cst, cb, vs) computed once per pass, whole rounds without liveness masks (only the last
+// round of a warp's range is masked), and a 32-bit word index into B_v: the per-chunk
+// address, owner-advance and mask work was most of k_count_hub's instructions (ncu).
+#ifndef TC_AND2
+#define TC_AND2 1
+#endif
+template <int U>
+__device__ __forceinline__ uint32_t sweep_and2(const uint32_t *__restrict__ bits, uint32_t a_cst, uint32_t a_cb,
+                                               uint32_t a_vs, uint32_t nwin, uint32_t c0, uint32_t c1,
+                                               uint32_t bm) {
+    const unsigned lane = lane_id();
+    uint32_t k = 0;
+    {
+        const uint32_t c = c0 + lane < c1 ? c0 + lane : c1 - 1;
+        uint32_t a = 0, b = nwin;
+        while (b - a > 1) {
+            const uint32_t mid = (a + b) >> 1;
+            if (lds32(a_cst + 4 * mid) <= c) a = mid; else b = mid;
+        }
+        k = a;
+    }
+    uint32_t nextb = lds32(a_cst + 4 * (k + 1)), gb = lds32(a_cb + 4 * k), sa = bm + 4 * lds32(a_vs + 4 * k);
+    uint32_t found = 0;
+    uint32_t base = c0;
+    for (; base + 32 * U <= c1; base += 32 * U) {
+        uint4 q[U];
+        uint32_t sw[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const uint32_t c = base + j * 32 + lane;
+            if (c >= nextb) {
+                do {
+                    ++k;
+                    nextb = lds32(a_cst + 4 * (k + 1));
+                } while (c >= nextb);
+                gb = lds32(a_cb + 4 * k);
+                sa = bm + 4 * lds32(a_vs + 4 * k);
+            }
+            q[j] = __ldg(reinterpret_cast<const uint4 *>(bits + (gb + 4 * c)));
+            sw[j] = sa + 16 * c;
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const uint4 b = lds128(sw[j]);
+            found += __popc(q[j].x & b.x) + __popc(q[j].y & b.y) + __popc(q[j].z & b.z) + __popc(q[j].w & b.w);
+        }
+    }
+    if (base < c1) {  // last, partial round: lanes past c1 reload the last chunk, masked
+        uint4 q[U];
+        uint32_t sw[U], live[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            uint32_t c = base + j * 32 + lane;
+            live[j] = c < c1 ? 0xffffffffu : 0u;
+            c = c < c1 ? c : c1 - 1;
+            if (c >= nextb) {
+                do {
+                    ++k;
+                    nextb = lds32(a_cst + 4 * (k + 1));
+                } while (c >= nextb);
+                gb = lds32(a_cb + 4 * k);
+                sa = bm + 4 * lds32(a_vs + 4 * k);
+            }
+            q[j] = __ldg(reinterpret_cast<const uint4 *>(bits + (gb + 4 * c)));
+            sw[j] = sa + 16 * c;
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const uint4 b = lds128(sw[j]);
+            found += __popc(q[j].x & b.x & live[j]) + __popc(q[j].y & b.y & live[j]) +
+                     __popc(q[j].z & b.z & live[j]) + __popc(q[j].w & b.w & live[j]);
+        }
+    }
+    return found;
+}
+
 // Block-wide exclusive scan of two values per thread with one set of barriers.
 // smem: 2 * 32 entries.  Returns the block totals in *ta, *tb.
 __device__ __forceinline__ void block_exclusive_scan2(unsigned long long a, uint32_t b, unsigned long long *s_a,
@@ -1166,7 +1243,12 @@ __global__ void TC_HUB_BOUNDS(NT)
                         const EdgeTable<uint32_t> et{s_cb3[pass], s_vs3[pass], pass < 2 ? s_ve3[pass] : nullptr,
                                                      s_cst3[pass], nullptr};
                         if (pass == 2) {
+#if TC_AND2
+                            acc += sweep_and2<U>(dense_bits, smem_addr(s_cst3[2]), smem_addr(s_cb3[2]),
+                                                 smem_addr(s_vs3[2]), NT, c0, c1, bm);
+#else
                             acc += sweep_and<U>(dense_bits, et, NT, c0, c1, bm);
+#endif
                         } else if (pass == 0) {
                             if (hp.lo16) acc += sweep_bits18<U>(hp, et, NT, c0, c1, bitmap);
                             else acc += sweep_bits<U>(dst, et, NT, c0, c1, bitmap, hz);
