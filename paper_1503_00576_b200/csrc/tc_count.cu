@@ -1806,10 +1806,31 @@ __device__ __forceinline__ void ldg_chunk(const void *arr, uint32_t p, ChunkT<B1
 // of the next round are in flight while this round's items are probed, and all
 // shared-memory probes of a round are issued before their results are used (the probe
 // chain LDS -> shift -> add is latency-bound otherwise).
+// TC_VHUB_SA: the bitmap and the window table are addressed through 32-bit shared
+// addresses computed once per kernel (bm32, a_cb, a_cst): without them the compiler
+// rebuilds the CTA's shared-window base (S2R SR_CgaCtaId) for every cursor advance and
+// adds it to every probe address.
+#ifndef TC_VHUB_SA
+#define TC_VHUB_SA 1
+#endif
+#ifndef TC_VHUB_ALIGN
+#define TC_VHUB_ALIGN 1
+#endif
 template <int U, bool B16>
 __device__ __forceinline__ uint32_t sweep_nomask(const void *__restrict__ arr, const uint32_t *s_cb,
                                                  const uint32_t *s_cst, uint32_t nwin, uint32_t c0, uint32_t c1,
-                                                 const unsigned char *bm, uint32_t hz, uint32_t amask) {
+                                                 const unsigned char *bm, uint32_t hz, uint32_t amask,
+                                                 uint32_t bm32, uint32_t a_cb, uint32_t a_cst) {
+#if TC_VHUB_SA
+    auto cst_at = [&](uint32_t i) { return lds32(a_cst + 4 * i); };
+    auto cb_at = [&](uint32_t i) { return lds32(a_cb + 4 * i); };
+#else
+    auto cst_at = [&](uint32_t i) { return s_cst[i]; };
+    auto cb_at = [&](uint32_t i) { return s_cb[i]; };
+    (void)bm32;
+    (void)a_cb;
+    (void)a_cst;
+#endif
     using Q = ChunkT<B16>;
     constexpr uint32_t E = Q::E;
     constexpr int NIC = (int)E;   // items per chunk
@@ -1821,11 +1842,11 @@ __device__ __forceinline__ uint32_t sweep_nomask(const void *__restrict__ arr, c
         uint32_t a = 0, b = nwin;
         while (b - a > 1) {
             const uint32_t mid = (a + b) >> 1;
-            if (s_cst[mid] <= c) a = mid; else b = mid;
+            if (cst_at(mid) <= c) a = mid; else b = mid;
         }
         k = a;
     }
-    uint32_t nextb = s_cst[k + 1], cb = s_cb[k];
+    uint32_t nextb = cst_at(k + 1), cb = cb_at(k);
     auto fetch = [&](uint32_t base, Q (&q)[U], uint32_t &live) {
         live = 0;
 #pragma unroll
@@ -1834,8 +1855,8 @@ __device__ __forceinline__ uint32_t sweep_nomask(const void *__restrict__ arr, c
             live |= (c < c1 ? 1u : 0u) << j;
             c = c < c1 ? c : c1 - 1;
             if (c >= nextb) {
-                do { nextb = s_cst[++k + 1]; } while (c >= nextb);
-                cb = s_cb[k];
+                do { nextb = cst_at(++k + 1); } while (c >= nextb);
+                cb = cb_at(k);
             }
 #ifdef TC_VHUB_NOLOAD  // diagnostic build: no suffix loads (items synthesised)
 #pragma unroll
@@ -1853,9 +1874,14 @@ __device__ __forceinline__ uint32_t sweep_nomask(const void *__restrict__ arr, c
             for (int i = 0; i < Q::CW; ++i) {
                 const uint32_t x = q[j].w[i];
                 if (B16) {
+#if TC_VHUB_SA && TC_VHUB_ALIGN
+                    ad[NIC * j + 2 * i] = ((x >> 3) & 0x1ffcu) | bm32;  // bm32: 8 KB aligned
+                    ad[NIC * j + 2 * i + 1] = ((x >> 19) & 0x1ffcu) | bm32;
+#else
                     ad[NIC * j + 2 * i] = (x >> 3) & 0x1ffcu;
-                    sh[NIC * j + 2 * i] = x;
                     ad[NIC * j + 2 * i + 1] = (x >> 19) & 0x1ffcu;
+#endif
+                    sh[NIC * j + 2 * i] = x;
                     sh[NIC * j + 2 * i + 1] = x >> 16;
                 } else {
                     const uint32_t r = x - hz;
@@ -1869,7 +1895,11 @@ __device__ __forceinline__ uint32_t sweep_nomask(const void *__restrict__ arr, c
 #ifdef TC_VHUB_NOPROBE  // diagnostic build: no shared-memory probes
             wd[t] = ad[t];
 #else
+#if TC_VHUB_SA
+            wd[t] = lds32(B16 && TC_VHUB_ALIGN ? ad[t] : bm32 + ad[t]);
+#else
             wd[t] = *reinterpret_cast<const uint32_t *>(bm + ad[t]);
+#endif
 #endif
         uint32_t f = 0;
 #pragma unroll
@@ -1913,7 +1943,14 @@ __global__ void TC_VHUB_BOUNDS(NT)
                  const uint2 *__restrict__ in_e, const void *__restrict__ tasks,
                  const uint32_t *__restrict__ tlo, const uint32_t *__restrict__ ntasks,
                  unsigned *__restrict__ next, unsigned long long *__restrict__ total) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+#if TC_VHUB_ALIGN
+    // the bitmap starts on an 8 KB boundary: a 16-bit item's probe address is one LOP3
+    // ((x >> 3) & 0x1ffc | base) instead of mask + add
+    unsigned char *smem = smem_raw + ((0u - smem_addr(smem_raw)) & 8191u);
+#else
+    unsigned char *smem = smem_raw;
+#endif
     uint32_t *bitmap = reinterpret_cast<uint32_t *>(smem);  // (amask + 4) / 4 words
     constexpr int WPT = TC_VHUB_WPT;
     constexpr uint32_t WIN = (uint32_t)NT * WPT;
@@ -1922,6 +1959,12 @@ __global__ void TC_VHUB_BOUNDS(NT)
     __shared__ uint32_t s_scan[32];
     __shared__ unsigned s_task;
     constexpr int NW = NT / 32;
+    // shared addresses held in registers (opaque moves: otherwise the compiler rebuilds the
+    // shared-window base from SR_CgaCtaId at every use)
+    uint32_t bm32, a_cb;
+    asm volatile("mov.b32 %0, %1;" : "=r"(bm32) : "r"(smem_addr(smem)));
+    asm volatile("mov.b32 %0, %1;" : "=r"(a_cb) : "r"(smem_addr(s_cb)));
+    const uint32_t a_cst = a_cb + (smem_addr(s_cst) - smem_addr(s_cb));
     const unsigned warp = threadIdx.x >> 5;
     const unsigned nt = *ntasks, t0 = *tlo;
     // the probes of outside items may read any word of the allocation: define them all
@@ -2023,8 +2066,8 @@ __global__ void TC_VHUB_BOUNDS(NT)
             if (c0 < c1) {
                 if (b16)
                     acc += sweep_nomask<TC_B16W == 4 ? U : (U + 1) / 2, true>(lo16, s_cb, s_cst, WIN, c0, c1, smem, hz,
-                                                                              amask);
-                else acc += sweep_nomask<U, false>(dst, s_cb, s_cst, WIN, c0, c1, smem, hz, amask);
+                                                                              amask, bm32, a_cb, a_cst);
+                else acc += sweep_nomask<U, false>(dst, s_cb, s_cst, WIN, c0, c1, smem, hz, amask, bm32, a_cb, a_cst);
             }
             __syncthreads();
         }
@@ -2590,7 +2633,7 @@ int vmajor_count(const DeviceGraph &g, unsigned long long *d_total, cudaStream_t
         uint32_t w32 = 4;
         while (w32 < g.hwp) w32 <<= 1;
         const uint32_t amask = (w32 * 4 - 1) & ~3u;
-        const size_t hsm = 4 * (size_t)(w32 > kT16 / 32 ? w32 : kT16 / 32);
+        const size_t hsm = 4 * (size_t)(w32 > kT16 / 32 ? w32 : kT16 / 32) + (TC_VHUB_ALIGN ? 8192 : 0);
         const int64_t vu = opts().vhub_unroll;
         auto hk = vu == 4 ? k_count_vhub<NT, 4, false> : vu == 1 ? k_count_vhub<NT, 1, false> : k_count_vhub<NT, 2, false>;
         auto hkb = vu == 4 ? k_count_vhub<NT, 4, true> : vu == 1 ? k_count_vhub<NT, 1, true> : k_count_vhub<NT, 2, true>;
