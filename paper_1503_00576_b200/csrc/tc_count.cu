@@ -484,6 +484,68 @@ __device__ __forceinline__ uint32_t sweep_and2(const uint32_t *__restrict__ bits
     return found;
 }
 
+// sweep_bits with the edge table (a_cst / a_cb / a_vs / a_ve) and the bitmap (bm) read
+// through 32-bit shared addresses held in registers (see sweep_and2).
+template <int U>
+__device__ __forceinline__ uint32_t sweep_bits_sa(const uint32_t *__restrict__ dst, uint32_t a_cst, uint32_t a_cb,
+                                                  uint32_t a_vs, uint32_t a_ve, uint32_t nwin, uint32_t c0,
+                                                  uint32_t c1, uint32_t bm, uint32_t hz) {
+    const unsigned lane = lane_id();
+    uint32_t k = 0;
+    {
+        const uint32_t c = c0 + lane < c1 ? c0 + lane : c1 - 1;
+        uint32_t a = 0, b = nwin;
+        while (b - a > 1) {
+            const uint32_t mid = (a + b) >> 1;
+            if (lds32(a_cst + 4 * mid) <= c) a = mid; else b = mid;
+        }
+        k = a;
+    }
+    uint32_t nextb = lds32(a_cst + 4 * (k + 1));
+    uint32_t cb = lds32(a_cb + 4 * k), lo = lds32(a_vs + 4 * k);
+    uint32_t span = lds32(a_ve + 4 * k) - lo;
+    uint32_t found = 0;
+    for (uint32_t base = c0; base < c1; base += 32 * U) {
+        uint4 q[U];
+        uint32_t rel[U], sp[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            uint32_t c = base + j * 32 + lane;
+            const bool live = c < c1;
+            c = live ? c : c1 - 1;
+            if (c >= nextb) {
+                do {
+                    ++k;
+                    nextb = lds32(a_cst + 4 * (k + 1));
+                } while (c >= nextb);
+                cb = lds32(a_cb + 4 * k);
+                lo = lds32(a_vs + 4 * k);
+                span = lds32(a_ve + 4 * k) - lo;
+            }
+            const uint32_t p = cb + 4 * c;
+            q[j] = __ldg(reinterpret_cast<const uint4 *>(dst + p));
+            rel[j] = p - lo;
+            sp[j] = live ? span : 0u;
+        }
+        uint32_t wd[4 * U], sh[4 * U], okm[4 * U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const uint32_t w4[4] = {q[j].x, q[j].y, q[j].z, q[j].w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t ok = (rel[j] + i < sp[j]) ? 1u : 0u;
+                const uint32_t r = (ok ? w4[i] : hz) - hz;
+                okm[4 * j + i] = ok;
+                sh[4 * j + i] = r;
+                wd[4 * j + i] = lds32(bm + 4 * (r >> 5));
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 4 * U; ++t) found += __funnelshift_r(wd[t], wd[t], sh[t]) & okm[t];
+    }
+    return found;
+}
+
 // Block-wide exclusive scan of two values per thread with one set of barriers.
 // smem: 2 * 32 entries.  Returns the block totals in *ta, *tb.
 __device__ __forceinline__ void block_exclusive_scan2(unsigned long long a, uint32_t b, unsigned long long *s_a,
@@ -1118,7 +1180,20 @@ __global__ void TC_HUB_BOUNDS(NT)
 #if !TC_HUB_FUSED
     const EdgeTable<uint32_t> et{s_cb, s_vs, s_ve, s_cst, nullptr};
 #endif
-    const uint32_t bm = smem_addr(bitmap);
+    // shared addresses in registers (opaque moves: no SR_CgaCtaId rebuild at every use)
+    uint32_t bm;
+    asm volatile("mov.b32 %0, %1;" : "=r"(bm) : "r"(smem_addr(bitmap)));
+#if TC_HUB_FUSED
+    uint32_t t3;
+    asm volatile("mov.b32 %0, %1;" : "=r"(t3) : "r"(smem_addr(&s_cb3[0][0])));
+    const uint32_t a_cst2 = t3 + (smem_addr(&s_cst3[2][0]) - smem_addr(&s_cb3[0][0]));
+    const uint32_t a_cb2 = t3 + (smem_addr(&s_cb3[2][0]) - smem_addr(&s_cb3[0][0]));
+    const uint32_t a_vs2 = t3 + (smem_addr(&s_vs3[2][0]) - smem_addr(&s_cb3[0][0]));
+    const uint32_t a_cst0 = t3 + (smem_addr(&s_cst3[0][0]) - smem_addr(&s_cb3[0][0]));
+    const uint32_t a_cb0 = t3;
+    const uint32_t a_vs0 = t3 + (smem_addr(&s_vs3[0][0]) - smem_addr(&s_cb3[0][0]));
+    const uint32_t a_ve0 = t3 + (smem_addr(&s_ve3[0][0]) - smem_addr(&s_cb3[0][0]));
+#endif
     for (uint32_t i = threadIdx.x; i < hwords; i += NT) bitmap[i] = 0;
     unsigned long long acc = 0;
     for (;;) {
@@ -1244,14 +1319,17 @@ __global__ void TC_HUB_BOUNDS(NT)
                                                      s_cst3[pass], nullptr};
                         if (pass == 2) {
 #if TC_AND2
-                            acc += sweep_and2<U>(dense_bits, smem_addr(s_cst3[2]), smem_addr(s_cb3[2]),
-                                                 smem_addr(s_vs3[2]), NT, c0, c1, bm);
+                            acc += sweep_and2<U>(dense_bits, a_cst2, a_cb2, a_vs2, NT, c0, c1, bm);
 #else
                             acc += sweep_and<U>(dense_bits, et, NT, c0, c1, bm);
 #endif
                         } else if (pass == 0) {
                             if (hp.lo16) acc += sweep_bits18<U>(hp, et, NT, c0, c1, bitmap);
+#if TC_AND2
+                            else acc += sweep_bits_sa<U>(dst, a_cst0, a_cb0, a_vs0, a_ve0, NT, c0, c1, bm, hz);
+#else
                             else acc += sweep_bits<U>(dst, et, NT, c0, c1, bitmap, hz);
+#endif
                         } else if (tab_ok) {
                             acc += sweep<uint32_t, false>(dst, et, NT, c0, c1,
                                                           [&](uint32_t w, uint32_t) { return ck.contains(w); });

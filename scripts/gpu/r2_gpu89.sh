@@ -1,0 +1,7 @@
+for i in 1 2; do
+timeout 300 python scripts/ab_opts.py rmat26 5 "" 2>&1 | tail -1 | cut -c1-140
+TC_LIB_PATH=variants/lib_prev.so timeout 300 python scripts/ab_opts.py rmat26 5 "" 2>&1 | tail -1 | cut -c1-140 | sed 's/^/prev /'
+done
+timeout 300 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum --clock-control none --csv --log-file gpurun_out/hubsa.csv -k regex:"k_count_hub" python scripts/fused_step.py 26 1 > /dev/null 2>&1; echo rc=$?
+TC_LIB_PATH=variants/lib_prev.so timeout 300 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum --clock-control none --csv --log-file gpurun_out/hubsa_prev.csv -k regex:"k_count_hub" python scripts/fused_step.py 26 1 > /dev/null 2>&1; echo rc=$?
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -p no:cacheprovider -k "schedules or headline or rmat or ba or rgg" 2>&1 | tail -2
