@@ -220,6 +220,62 @@ __device__ __forceinline__ uint32_t sweep(const uint32_t *__restrict__ dst, cons
     return found;
 }
 
+// sweep() over a window table addressed by 32-bit shared addresses held in registers
+// (uint32_t offsets, no aux): the generic version's table reads make the compiler rebuild
+// the shared-window base (S2R SR_CgaCtaId) at every cursor advance.
+struct EdgeTableSA {
+    uint32_t cb, vs, ve, cst;  // shared addresses of the per-edge arrays
+};
+template <int U, typename Probe>
+__device__ __forceinline__ uint32_t sweep_sa(const uint32_t *__restrict__ dst, const EdgeTableSA et, uint32_t nwin,
+                                             uint32_t c0, uint32_t c1, Probe probe) {
+    const unsigned lane = lane_id();
+    uint32_t k = 0;
+    {
+        const uint32_t c = c0 + lane < c1 ? c0 + lane : c1 - 1;
+        uint32_t a = 0, b = nwin;
+        while (b - a > 1) {
+            const uint32_t mid = (a + b) >> 1;
+            if (lds32(et.cst + 4 * mid) <= c) a = mid; else b = mid;
+        }
+        k = a;
+    }
+    uint32_t nextb = lds32(et.cst + 4 * (k + 1));
+    uint32_t cb = lds32(et.cb + 4 * k), lo = lds32(et.vs + 4 * k);
+    uint32_t span = lds32(et.ve + 4 * k) - lo;
+    uint32_t found = 0;
+    for (uint32_t base = c0; base < c1; base += 32 * U) {
+        uint4 q[U];
+        uint32_t rel[U], sp[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            uint32_t c = base + j * 32 + lane;
+            const bool live = c < c1;
+            c = live ? c : c1 - 1;
+            if (c >= nextb) {
+                do {
+                    ++k;
+                    nextb = lds32(et.cst + 4 * (k + 1));
+                } while (c >= nextb);
+                cb = lds32(et.cb + 4 * k);
+                lo = lds32(et.vs + 4 * k);
+                span = lds32(et.ve + 4 * k) - lo;
+            }
+            const uint32_t p = cb + 4 * c;
+            q[j] = __ldg(reinterpret_cast<const uint4 *>(dst + p));
+            rel[j] = p - lo;
+            sp[j] = live ? span : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const uint32_t w4[4] = {q[j].x, q[j].y, q[j].z, q[j].w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) found += ((rel[j] + i < sp[j]) & probe(w4[i])) ? 1u : 0u;
+        }
+    }
+    return found;
+}
+
 // sweep() specialised to a shared-memory bitmap probe over the hub zone: item w hits iff
 // bit (w - hz) of `bitmap` is set.  Branch-free and lean: an invalid item (outside its
 // list in a boundary chunk) is replaced by hz before the probe (bit 0 of word 0 -- always
@@ -1683,9 +1739,14 @@ __global__ void k_vin_tasks(const uint32_t *__restrict__ start, const uint32_t *
 #define TC_VHUB_WPT 2  // in-edges per thread per window of k_count_vhub (window = WPT * NT)
 #endif
 #ifndef TC_VM_MINB
-#define TC_VM_BOUNDS(nt) __launch_bounds__(nt)
-#else
+// 5 CTAs per SM (48 registers): with the hub heads in k_count_vhub this kernel only runs the
+// long low-zone lists, latency-bound (ncu 10.5 -> 9.8 ms at s26; 4 CTAs: 10.6 ms)
+#define TC_VM_MINB 5
+#endif
+#if TC_VM_MINB > 0
 #define TC_VM_BOUNDS(nt) __launch_bounds__(nt, TC_VM_MINB)
+#else
+#define TC_VM_BOUNDS(nt) __launch_bounds__(nt)
 #endif
 template <int NT, int U>
 __global__ void TC_VM_BOUNDS(NT)
@@ -1710,7 +1771,12 @@ __global__ void TC_VM_BOUNDS(NT)
     const unsigned warp = threadIdx.x >> 5;
     const unsigned nt = *ntasks, t0 = *tlo;
     const EdgeTable<uint32_t> et{s_cb, s_vs, s_ve, s_cst, nullptr};
-    const uint32_t bm = smem_addr(bitmap);
+    // shared addresses in registers (opaque moves: no SR_CgaCtaId rebuild at every use)
+    uint32_t bm, tb;
+    asm volatile("mov.b32 %0, %1;" : "=r"(bm) : "r"(smem_addr(bitmap)));
+    asm volatile("mov.b32 %0, %1;" : "=r"(tb) : "r"(smem_addr(s_cb)));
+    const EdgeTableSA eta{tb, tb + (smem_addr(s_vs) - smem_addr(s_cb)), tb + (smem_addr(s_ve) - smem_addr(s_cb)),
+                          tb + (smem_addr(s_cst) - smem_addr(s_cb))};
     unsigned long long acc = 0;
     for (;;) {
         if (threadIdx.x == 0) s_task = t0 + atomicAdd(next, 1u);
@@ -1727,7 +1793,7 @@ __global__ void TC_VM_BOUNDS(NT)
         const uint32_t ws = v >= hz ? ((v + 1 - hz) >> 5) & ~3u : 0u;
         for (uint32_t i = ws + 4 * threadIdx.x; i < hwp; i += 4 * NT)
             *reinterpret_cast<uint4 *>(bitmap + i) = make_uint4(0, 0, 0, 0);
-        Cuckoo32 ck{smem_addr(ctab), 4 * nh < cap ? 4 * nh : cap, 0, 0};
+        Cuckoo32 ck{bm + 4 * hwp, 4 * nh < cap ? 4 * nh : cap, 0, 0};  // ctab = bitmap + hwp
         bool tab_ok = true;
         if (nh) {
             tab_ok = false;
@@ -1793,7 +1859,7 @@ __global__ void TC_VM_BOUNDS(NT)
                 // suffix items are > v: hub items hit words >= ws (staged); non-hub items
                 // (only when v < hz) are looked up in the cuckoo table
                 if (v < hz && tab_ok) {  // suffix items below hz exist: bitmap or cuckoo per item
-                    acc += sweep<uint32_t, false, U>(dst, et, VWIN, c0, c1, [&](uint32_t w, uint32_t) {
+                    acc += sweep_sa<U>(dst, eta, VWIN, c0, c1, [&](uint32_t w) {
                         const uint32_t r = w - hz;
                         const bool b = ((lds32(bm + 4 * min(r >> 5, hwp - 1)) >> (r & 31)) & 1u) != 0u;
                         return w >= hz ? b : (nh != 0 && ck.contains(w));
