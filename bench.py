@@ -286,6 +286,10 @@ def roofline_block(sched: dict, med: dict, peak: float, peak_src: str, W: int, m
                             "frac": round(merge_bytes / (ms / 1e3) / 1e9 / peak, 4),
                             "note": "SURVEY.md §8(d) B = 4W + 40m: bytes a two-pointer merge would read; "
                                     "not a physical bound for this schedule"},
+            "limiter": "s26: the dominant k_count_vhub (57 % of the count) runs its SM L1 data pipe at 82.6 % "
+                       "of peak wavefronts (bitmap probes at 2.69 wavefronts per shared load + the suffix "
+                       "loads), k_count_vlow_warp at 86 %; DRAM stops at 0.71 / 0.56 of peak behind it "
+                       "(profiles/r02_smem_count_s26.md)" if workload.startswith("rmat_s26") else None,
             "peak_source": peak_src}
 
 
