@@ -538,11 +538,11 @@ def main():
                           "count_standalone": med["count_ms"],
                           "count_vmajor_phase": med["vmajor_ms"],
                           "count_umajor_heavy": med["heavy_ms"], "count_light": med["light_ms"],
-                          "generate_input_s": gen_s,
-                          "note": "when the count will run v-major (R-MAT s23+), preprocess includes the "
+                          "generate_input_s": gen_s},
+            "phases_note": "when the count will run v-major (R-MAT s23+), preprocess includes the "
                                   "v-major in-edge index filled by the segmented sorts (s26: +~20 ms of "
                                   "preprocess for -~26 ms of count vs building it at count time; DESIGN.md "
-                                  "§4.1 item 9)"},
+                                  "§4.1 item 9)",
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
             "gpu_launches": l1 - l0,
         }
